@@ -1,0 +1,943 @@
+/*
+ * oracle.c — plain, slow CPU oracle for the zkDL sumcheck hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.  It
+ * shares no code, header, table or constant generator with the CUDA path
+ * (paper_2307_16273_b200/csrc).  Every function follows a passage of
+ * /root/reference/PAPER.md ("P:Lnnn") or a DESIGN.md reading ("Dn").
+ *
+ * Representation (deliberately unlike the device's 8x32-bit CIOS code):
+ *   Fr = BLS12-381 scalar field (D1), 4 x 64-bit limbs,
+ *   Montgomery form with R = 2^256, textbook separated operand scanning:
+ *   full 512-bit schoolbook product, then word-by-word REDC (HAC 14.32).
+ *   R mod p and R^2 mod p are computed at start-up by repeated doubling.
+ *
+ * Pins (tests/test_oracle_*.py, -m "not gpu"): Python-int field arithmetic,
+ * p = x^4 - x^2 + 1 for the BLS parameter x, NIST SHA-256 vectors, SPEC
+ * worked examples, round identities + final checks against brute-force MLE,
+ * exhaustive m = 2 sumchecks, Lemma 1 exhaustive at Q=4 R=2, the matmul
+ * identity against integer products, tamper rejection.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <omp.h>
+
+typedef unsigned __int128 u128;
+typedef struct { uint64_t l[4]; } fr;
+
+/* p = 0x73eda753299d7d483339d80809a1d80553bda402fffe5bfeffffffff00000001 */
+static const uint64_t P[4] = {0xffffffff00000001ULL, 0x53bda402fffe5bfeULL,
+                              0x3339d80809a1d805ULL, 0x73eda753299d7d48ULL};
+static uint64_t PINV;          /* -p^{-1} mod 2^64, computed by Newton iteration at init */
+static fr R1;                  /* R mod p      (Montgomery form of 1) */
+static fr R2;                  /* R^2 mod p */
+static int g_init = 0;
+
+/* ---------------------------------------------------------------- integers */
+static int geq_p(const uint64_t a[4]) {
+    for (int i = 3; i >= 0; i--) {
+        if (a[i] > P[i]) return 1;
+        if (a[i] < P[i]) return 0;
+    }
+    return 1;
+}
+static void sub_p(uint64_t a[4]) {
+    u128 borrow = 0;
+    for (int i = 0; i < 4; i++) {
+        u128 d = (u128)a[i] - P[i] - borrow;
+        a[i] = (uint64_t)d;
+        borrow = (d >> 127) & 1;
+    }
+}
+
+/* ---------------------------------------------------------------- field ops */
+static fr fr_add(fr a, fr b) {
+    fr c; u128 carry = 0;
+    for (int i = 0; i < 4; i++) {
+        u128 s = (u128)a.l[i] + b.l[i] + carry;
+        c.l[i] = (uint64_t)s; carry = s >> 64;
+    }
+    if (carry || geq_p(c.l)) sub_p(c.l);
+    return c;
+}
+static fr fr_sub(fr a, fr b) {
+    fr c; u128 borrow = 0;
+    for (int i = 0; i < 4; i++) {
+        u128 d = (u128)a.l[i] - b.l[i] - borrow;
+        c.l[i] = (uint64_t)d; borrow = (d >> 127) & 1;
+    }
+    if (borrow) {           /* add p back */
+        u128 carry = 0;
+        for (int i = 0; i < 4; i++) {
+            u128 s = (u128)c.l[i] + P[i] + carry;
+            c.l[i] = (uint64_t)s; carry = s >> 64;
+        }
+    }
+    return c;
+}
+static fr fr_neg(fr a) { fr z = {{0, 0, 0, 0}}; return fr_sub(z, a); }
+
+/* Montgomery product a*b*R^{-1} mod p: schoolbook 512-bit product, then REDC. */
+static fr fr_mul(fr a, fr b) {
+    uint64_t t[9] = {0};
+    for (int i = 0; i < 4; i++) {
+        u128 carry = 0;
+        for (int j = 0; j < 4; j++) {
+            u128 s = (u128)a.l[i] * b.l[j] + t[i + j] + carry;
+            t[i + j] = (uint64_t)s; carry = s >> 64;
+        }
+        t[i + 4] = (uint64_t)carry;
+    }
+    for (int i = 0; i < 4; i++) {
+        uint64_t m = t[i] * PINV;
+        u128 carry = 0;
+        for (int j = 0; j < 4; j++) {
+            u128 s = (u128)m * P[j] + t[i + j] + carry;
+            t[i + j] = (uint64_t)s; carry = s >> 64;
+        }
+        for (int k = i + 4; k < 9 && carry; k++) {
+            u128 s = (u128)t[k] + carry;
+            t[k] = (uint64_t)s; carry = s >> 64;
+        }
+    }
+    fr c = {{t[4], t[5], t[6], t[7]}};
+    if (t[8] || geq_p(c.l)) sub_p(c.l);
+    return c;
+}
+static fr fr_zero(void) { fr z = {{0, 0, 0, 0}}; return z; }
+static fr fr_one(void) { return R1; }
+static int fr_eq(fr a, fr b) { return memcmp(a.l, b.l, 32) == 0; }
+static int fr_is_zero(fr a) { return (a.l[0] | a.l[1] | a.l[2] | a.l[3]) == 0; }
+
+/* canonical integer (< p) -> Montgomery */
+static fr fr_from_canon(const uint64_t v[4]) { fr a = {{v[0], v[1], v[2], v[3]}}; return fr_mul(a, R2); }
+static void fr_to_canon(fr a, uint64_t v[4]) {
+    fr one = {{1, 0, 0, 0}};
+    fr c = fr_mul(a, one);
+    memcpy(v, c.l, 32);
+}
+static fr fr_from_u64(uint64_t x) { uint64_t v[4] = {x, 0, 0, 0}; return fr_from_canon(v); }
+/* embed a signed integer: negatives map to p - |v| */
+static fr fr_from_i64(int64_t x) {
+    if (x >= 0) return fr_from_u64((uint64_t)x);
+    return fr_neg(fr_from_u64((uint64_t)(-(x + 1)) + 1));
+}
+static fr fr_pow(fr a, const uint64_t e[4]) {
+    fr r = fr_one();
+    for (int i = 3; i >= 0; i--)
+        for (int b = 63; b >= 0; b--) {
+            r = fr_mul(r, r);
+            if ((e[i] >> b) & 1) r = fr_mul(r, a);
+        }
+    return r;
+}
+static fr fr_inv(fr a) {          /* Fermat: a^(p-2) */
+    uint64_t e[4] = {P[0] - 2, P[1], P[2], P[3]};
+    return fr_pow(a, e);
+}
+
+static void init(void) {
+    if (g_init) return;
+    /* -p^{-1} mod 2^64 via Newton: x <- x(2 - p x) */
+    uint64_t x = 1;
+    for (int i = 0; i < 7; i++) x = x * (2 - P[0] * x);
+    PINV = (uint64_t)0 - x;
+    /* R mod p and R^2 mod p by doubling 1 (plain: 2^k mod p for k = 256, 512) */
+    uint64_t v[4] = {1, 0, 0, 0};
+    for (int k = 1; k <= 512; k++) {
+        uint64_t carry = 0;
+        for (int i = 0; i < 4; i++) {
+            uint64_t nv = (v[i] << 1) | carry;
+            carry = v[i] >> 63;
+            v[i] = nv;
+        }
+        if (carry || geq_p(v)) sub_p(v);
+        if (k == 256) memcpy(R1.l, v, 32);
+    }
+    memcpy(R2.l, v, 32);
+    g_init = 1;
+}
+
+/* ------------------------------------------------------------ byte I/O (LE) */
+static int load_canon(const uint8_t *b, fr *out) {
+    uint64_t v[4];
+    for (int i = 0; i < 4; i++) {
+        uint64_t w = 0;
+        for (int k = 7; k >= 0; k--) w = (w << 8) | b[8 * i + k];
+        v[i] = w;
+    }
+    if (geq_p(v)) return -3;   /* non-canonical */
+    *out = fr_from_canon(v);
+    return 0;
+}
+static void store_canon(fr a, uint8_t *b) {
+    uint64_t v[4];
+    fr_to_canon(a, v);
+    for (int i = 0; i < 4; i++)
+        for (int k = 0; k < 8; k++) b[8 * i + k] = (uint8_t)(v[i] >> (8 * k));
+}
+
+/* ------------------------------------------------------------ SHA-256 (FIPS 180-4) */
+typedef struct { uint32_t h[8]; uint8_t buf[64]; uint64_t len; uint32_t nbuf; } sha_ctx;
+static const uint32_t SHA_K[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+#define ROR(x, n) (((x) >> (n)) | ((x) << (32 - (n))))
+static void sha_block(sha_ctx *c, const uint8_t *p) {
+    uint32_t w[64];
+    for (int i = 0; i < 16; i++)
+        w[i] = ((uint32_t)p[4 * i] << 24) | ((uint32_t)p[4 * i + 1] << 16) | ((uint32_t)p[4 * i + 2] << 8) | p[4 * i + 3];
+    for (int i = 16; i < 64; i++) {
+        uint32_t s0 = ROR(w[i - 15], 7) ^ ROR(w[i - 15], 18) ^ (w[i - 15] >> 3);
+        uint32_t s1 = ROR(w[i - 2], 17) ^ ROR(w[i - 2], 19) ^ (w[i - 2] >> 10);
+        w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    uint32_t a = c->h[0], b = c->h[1], cc = c->h[2], d = c->h[3], e = c->h[4], f = c->h[5], g = c->h[6], h = c->h[7];
+    for (int i = 0; i < 64; i++) {
+        uint32_t S1 = ROR(e, 6) ^ ROR(e, 11) ^ ROR(e, 25);
+        uint32_t ch = (e & f) ^ (~e & g);
+        uint32_t t1 = h + S1 + ch + SHA_K[i] + w[i];
+        uint32_t S0 = ROR(a, 2) ^ ROR(a, 13) ^ ROR(a, 22);
+        uint32_t mj = (a & b) ^ (a & cc) ^ (b & cc);
+        uint32_t t2 = S0 + mj;
+        h = g; g = f; f = e; e = d + t1; d = cc; cc = b; b = a; a = t1 + t2;
+    }
+    c->h[0] += a; c->h[1] += b; c->h[2] += cc; c->h[3] += d;
+    c->h[4] += e; c->h[5] += f; c->h[6] += g; c->h[7] += h;
+}
+static void sha_init(sha_ctx *c) {
+    static const uint32_t H0[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                                   0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    memcpy(c->h, H0, 32); c->len = 0; c->nbuf = 0;
+}
+static void sha_update(sha_ctx *c, const void *data, uint64_t n) {
+    const uint8_t *p = (const uint8_t *)data;
+    c->len += n;
+    while (n) {
+        uint32_t take = 64 - c->nbuf;
+        if (take > n) take = (uint32_t)n;
+        memcpy(c->buf + c->nbuf, p, take);
+        c->nbuf += take; p += take; n -= take;
+        if (c->nbuf == 64) { sha_block(c, c->buf); c->nbuf = 0; }
+    }
+}
+static void sha_final(sha_ctx *c, uint8_t out[32]) {
+    uint64_t bits = c->len * 8;
+    uint8_t pad = 0x80;
+    sha_update(c, &pad, 1);
+    uint8_t z = 0;
+    while (c->nbuf != 56) sha_update(c, &z, 1);
+    uint8_t lb[8];
+    for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(bits >> (56 - 8 * i));
+    sha_update(c, lb, 8);
+    for (int i = 0; i < 8; i++) {
+        out[4 * i] = (uint8_t)(c->h[i] >> 24); out[4 * i + 1] = (uint8_t)(c->h[i] >> 16);
+        out[4 * i + 2] = (uint8_t)(c->h[i] >> 8); out[4 * i + 3] = (uint8_t)c->h[i];
+    }
+}
+void or_sha256(const uint8_t *msg, uint64_t n, uint8_t out[32]) {
+    sha_ctx c; sha_init(&c); sha_update(&c, msg, n); sha_final(&c, out);
+}
+
+/* ------------------------------------------------------------ transcript (D3) */
+typedef struct { uint8_t st[32]; } transcript;
+
+void or_transcript_init(transcript *t, const uint8_t seed[32]) {
+    sha_ctx c; sha_init(&c);
+    const char *lbl = "zkdl-b200/v1/init";
+    sha_update(&c, lbl, strlen(lbl));
+    sha_update(&c, seed, 32);
+    sha_final(&c, t->st);
+}
+void or_transcript_absorb(transcript *t, const char *tag, const uint8_t *msg, uint64_t len) {
+    sha_ctx c; sha_init(&c);
+    uint8_t dom = 0x01, tl = (uint8_t)strlen(tag), lb[8];
+    for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(len >> (56 - 8 * i));
+    sha_update(&c, t->st, 32); sha_update(&c, &dom, 1); sha_update(&c, &tl, 1);
+    sha_update(&c, tag, tl); sha_update(&c, lb, 8); sha_update(&c, msg, len);
+    sha_final(&c, t->st);
+}
+/* x = LE512(SHA256(st||0x00) || SHA256(st||0x01)) mod p, computed by plain
+ * shift-and-subtract long division (no Montgomery, no precomputed constants). */
+static fr reduce512(const uint8_t h[64]) {
+    uint64_t rem[4] = {0, 0, 0, 0};
+    for (int bit = 511; bit >= 0; bit--) {
+        uint64_t top = rem[3] >> 63;
+        for (int i = 3; i > 0; i--) rem[i] = (rem[i] << 1) | (rem[i - 1] >> 63);
+        rem[0] = (rem[0] << 1) | ((h[bit >> 3] >> (bit & 7)) & 1);
+        if (top || geq_p(rem)) sub_p(rem);
+    }
+    return fr_from_canon(rem);
+}
+static fr transcript_challenge(transcript *t, const char *tag) {
+    sha_ctx c; sha_init(&c);
+    uint8_t dom = 0x02, tl = (uint8_t)strlen(tag);
+    sha_update(&c, t->st, 32); sha_update(&c, &dom, 1); sha_update(&c, &tl, 1); sha_update(&c, tag, tl);
+    sha_final(&c, t->st);
+    uint8_t h[64], b;
+    for (int k = 0; k < 2; k++) {
+        sha_init(&c); sha_update(&c, t->st, 32); b = (uint8_t)k; sha_update(&c, &b, 1); sha_final(&c, h + 32 * k);
+    }
+    return reduce512(h);
+}
+void or_transcript_challenges(transcript *t, const char *tag, uint32_t n, uint8_t *out) {
+    init();
+    for (uint32_t i = 0; i < n; i++) store_canon(transcript_challenge(t, tag), out + 32 * i);
+}
+static void absorb_frs(transcript *t, const char *tag, const fr *v, int n) {
+    uint8_t *b = (uint8_t *)malloc(32 * (size_t)n);
+    for (int i = 0; i < n; i++) store_canon(v[i], b + 32 * i);
+    or_transcript_absorb(t, tag, b, 32 * (uint64_t)n);
+    free(b);
+}
+static void absorb_u32s(transcript *t, const char *tag, const uint32_t *w, int n) {
+    uint8_t b[64];
+    for (int i = 0; i < n; i++)
+        for (int k = 0; k < 4; k++) b[4 * i + k] = (uint8_t)(w[i] >> (8 * k));
+    or_transcript_absorb(t, tag, b, 4 * (uint64_t)n);
+}
+
+/* ------------------------------------------------------------ exported field ops (pins) */
+int or_fr_op(int op, const uint8_t *a, const uint8_t *b, uint8_t *out) {
+    init();
+    fr x, y = fr_zero();
+    int s = load_canon(a, &x); if (s) return s;
+    if (b) { s = load_canon(b, &y); if (s) return s; }
+    fr r;
+    switch (op) {
+        case 0: r = fr_add(x, y); break;
+        case 1: r = fr_sub(x, y); break;
+        case 2: r = fr_mul(x, y); break;
+        case 3: if (fr_is_zero(x)) return -1; r = fr_inv(x); break;
+        case 4: r = fr_neg(x); break;
+        default: return -1;
+    }
+    store_canon(r, out);
+    return 0;
+}
+void or_embed_i64(const int64_t *v, uint64_t n, uint8_t *out) {
+    init();
+    for (uint64_t i = 0; i < n; i++) store_canon(fr_from_i64(v[i]), out + 32 * i);
+}
+uint64_t or_pinv(void) { init(); return PINV; }
+
+/* ------------------------------------------------------------ eq / beta */
+/* beta(u, b) = prod_t (u_t b_t + (1 - u_t)(1 - b_t)), LSB-first: u_t <-> bit t of b (D2). */
+static fr eq_at(const fr *u, int k, uint64_t b) {
+    fr acc = fr_one();
+    for (int t = 0; t < k; t++) {
+        fr f = ((b >> t) & 1) ? u[t] : fr_sub(fr_one(), u[t]);
+        acc = fr_mul(acc, f);
+    }
+    return acc;
+}
+/* beta on two field points */
+int or_beta(const uint8_t *u, const uint8_t *v, uint32_t k, uint8_t *out) {
+    init();
+    fr acc = fr_one();
+    for (uint32_t t = 0; t < k; t++) {
+        fr a, b;
+        if (load_canon(u + 32 * t, &a) || load_canon(v + 32 * t, &b)) return -3;
+        fr term = fr_add(fr_mul(a, b), fr_mul(fr_sub(fr_one(), a), fr_sub(fr_one(), b)));
+        acc = fr_mul(acc, term);
+    }
+    store_canon(acc, out);
+    return 0;
+}
+static int load_point(const uint8_t *b, int k, fr *u) {
+    for (int i = 0; i < k; i++) if (load_canon(b + 32 * i, &u[i])) return -3;
+    return 0;
+}
+int or_eq_table(const uint8_t *point, uint32_t k, uint8_t *out) {
+    init();
+    fr u[64];
+    if (load_point(point, (int)k, u)) return -3;
+    uint64_t n = 1ULL << k;
+    #pragma omp parallel for schedule(static)
+    for (uint64_t b = 0; b < n; b++) store_canon(eq_at(u, (int)k, b), out + 32 * b);
+    return 0;
+}
+
+/* MLE (P:L146 Eq. multilinear-extension): S~(u) = sum_b S(b) beta(u, b), brute force. */
+static fr mle_fr(const fr *tab, int m, const fr *u) {
+    uint64_t n = 1ULL << m;
+    int nt = omp_get_max_threads();
+    fr *part = (fr *)calloc((size_t)nt, sizeof(fr));
+    #pragma omp parallel
+    {
+        int id = omp_get_thread_num();
+        fr acc = fr_zero();
+        #pragma omp for schedule(static)
+        for (uint64_t b = 0; b < n; b++)
+            if (!fr_is_zero(tab[b])) acc = fr_add(acc, fr_mul(tab[b], eq_at(u, m, b)));
+        part[id] = acc;
+    }
+    fr s = fr_zero();
+    for (int i = 0; i < nt; i++) s = fr_add(s, part[i]);
+    free(part);
+    return s;
+}
+static fr mle_i32(const int32_t *tab, int m, const fr *u) {
+    uint64_t n = 1ULL << m;
+    int nt = omp_get_max_threads();
+    fr *part = (fr *)calloc((size_t)nt, sizeof(fr));
+    #pragma omp parallel
+    {
+        int id = omp_get_thread_num();
+        fr acc = fr_zero();
+        #pragma omp for schedule(static)
+        for (uint64_t b = 0; b < n; b++)
+            if (tab[b]) acc = fr_add(acc, fr_mul(fr_from_i64(tab[b]), eq_at(u, m, b)));
+        part[id] = acc;
+    }
+    fr s = fr_zero();
+    for (int i = 0; i < nt; i++) s = fr_add(s, part[i]);
+    free(part);
+    return s;
+}
+int or_mle_fr(const uint8_t *tab, uint32_t m, const uint8_t *point, uint8_t *out) {
+    init();
+    fr u[64];
+    if (load_point(point, (int)m, u)) return -3;
+    uint64_t n = 1ULL << m;
+    fr *t = (fr *)malloc(n * sizeof(fr));
+    for (uint64_t i = 0; i < n; i++) if (load_canon(tab + 32 * i, &t[i])) { free(t); return -3; }
+    store_canon(mle_fr(t, (int)m, u), out);
+    free(t);
+    return 0;
+}
+int or_mle_i32(const int32_t *tab, uint32_t m, const uint8_t *point, uint8_t *out) {
+    init();
+    fr u[64];
+    if (load_point(point, (int)m, u)) return -3;
+    store_canon(mle_i32(tab, (int)m, u), out);
+    return 0;
+}
+
+/* ------------------------------------------------------------ univariate helpers */
+/* Lagrange interpolation through (0, e_0) ... (d, e_d), evaluated at x. */
+static fr interp(const fr *e, int d, fr x) {
+    fr acc = fr_zero();
+    for (int i = 0; i <= d; i++) {
+        fr num = fr_one(), den = fr_one();
+        for (int j = 0; j <= d; j++) {
+            if (j == i) continue;
+            num = fr_mul(num, fr_sub(x, fr_from_u64((uint64_t)j)));
+            den = fr_mul(den, fr_from_i64((int64_t)i - j));
+        }
+        acc = fr_add(acc, fr_mul(e[i], fr_mul(num, fr_inv(den))));
+    }
+    return acc;
+}
+
+/* ------------------------------------------------------------ product sumcheck (Prot. 3)
+ * Statement:
+ *     claim = sum_{x in {0,1}^m} beta(w, x_{<n_eq}) * prod_{k<K} T_k(x)
+ * Rounds bind bit t of the flat index (LSB first, D2).  Messages are the
+ * evaluations at X = 0..K (D4).  For t < n_eq the prover sends the paper's f_t
+ * (P:L511, L518 with D7's subscript fix): the beta over the first n_eq
+ * variables with the prefix beta(w_{<t}, r_{<t}) and beta(w_t, X) divided out;
+ * the verifier checks (1-w_t) f_t(0) + w_t f_t(1) = c_t.
+ * For t >= n_eq it sends g_t and checks g_t(0) + g_t(1) = c_t.
+ * Transcript (D3c): "sc/hdr" (m, n_eq, K) | "sc/claim" | per round "sc/msg"
+ * then challenge "sc/r" | "sc/final" (T_k~(r), k < K).
+ */
+static fr prod_term(fr *const *T, int K, uint64_t b, fr X) {
+    fr p = fr_one();
+    for (int k = 0; k < K; k++) {
+        fr lo = T[k][2 * b], hi = T[k][2 * b + 1];
+        p = fr_mul(p, fr_add(lo, fr_mul(X, fr_sub(hi, lo))));
+    }
+    return p;
+}
+
+int or_sumcheck_prove(transcript *tr, uint32_t m, uint32_t n_eq, uint32_t K, const uint8_t *w_b,
+                      const uint8_t *tables_b /* K x 2^m canonical */, const uint8_t *claim_b /* NULL: compute */,
+                      uint8_t *claim_out, uint8_t *msgs_out /* m x (K+1) */, uint8_t *r_out /* m */,
+                      uint8_t *finals_out /* K */) {
+    init();
+    if (K < 1 || K > 3 || n_eq > m || m > 40) return -1;
+    fr w[64];
+    if (load_point(w_b, (int)n_eq, w)) return -3;
+    uint64_t n = 1ULL << m;
+    fr *T[3];
+    for (uint32_t k = 0; k < K; k++) {
+        T[k] = (fr *)malloc(n * sizeof(fr));
+        for (uint64_t i = 0; i < n; i++)
+            if (load_canon(tables_b + 32 * (k * n + i), &T[k][i])) return -3;
+    }
+    fr claim;
+    if (claim_b) {
+        if (load_canon(claim_b, &claim)) return -3;
+    } else {   /* brute force: sum_x beta(w, x_{<n_eq}) prod_k T_k(x) */
+        claim = fr_zero();
+        for (uint64_t x = 0; x < n; x++) {
+            fr p = eq_at(w, (int)n_eq, x & ((1ULL << n_eq) - 1));
+            for (uint32_t k = 0; k < K; k++) p = fr_mul(p, T[k][x]);
+            claim = fr_add(claim, p);
+        }
+    }
+    store_canon(claim, claim_out);
+    uint32_t hdr[3] = {m, n_eq, K};
+    absorb_u32s(tr, "sc/hdr", hdr, 3);
+    absorb_frs(tr, "sc/claim", &claim, 1);
+    int nt = omp_get_max_threads();
+    for (uint32_t t = 0; t < m; t++) {
+        uint64_t half = n >> (t + 1);          /* number of pairs */
+        fr ev[4];
+        fr *part = (fr *)calloc((size_t)nt * 4, sizeof(fr));
+        #pragma omp parallel
+        {
+            int id = omp_get_thread_num();
+            fr acc[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+            #pragma omp for schedule(static)
+            for (uint64_t b = 0; b < half; b++) {
+                fr e = fr_one();
+                if (t < n_eq) {   /* beta(w_{t+1..n_eq-1}, low bits of b) */
+                    int rest = (int)(n_eq - t - 1);
+                    e = eq_at(w + t + 1, rest, b & ((1ULL << rest) - 1));
+                }
+                for (uint32_t X = 0; X <= K; X++)
+                    acc[X] = fr_add(acc[X], fr_mul(e, prod_term(T, (int)K, b, fr_from_u64(X))));
+            }
+            for (int X = 0; X < 4; X++) part[id * 4 + X] = acc[X];
+        }
+        for (uint32_t X = 0; X <= K; X++) {
+            ev[X] = fr_zero();
+            for (int i = 0; i < nt; i++) ev[X] = fr_add(ev[X], part[i * 4 + X]);
+        }
+        free(part);
+        absorb_frs(tr, "sc/msg", ev, (int)K + 1);
+        for (uint32_t X = 0; X <= K; X++) store_canon(ev[X], msgs_out + 32 * (t * (K + 1) + X));
+        fr r = transcript_challenge(tr, "sc/r");
+        store_canon(r, r_out + 32 * t);
+        for (uint32_t k = 0; k < K; k++)   /* fold: T'[b] = T[2b] + r (T[2b+1] - T[2b]) */
+            for (uint64_t b = 0; b < half; b++)
+                T[k][b] = fr_add(T[k][2 * b], fr_mul(r, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+    }
+    fr fin[3];
+    for (uint32_t k = 0; k < K; k++) { fin[k] = T[k][0]; store_canon(fin[k], finals_out + 32 * k); free(T[k]); }
+    absorb_frs(tr, "sc/final", fin, (int)K);
+    return 0;
+}
+
+/* Verifier: replays the transcript, checks every round identity, the final
+ * identity c_m = prod_k finals_k, and (if tables given) each final against a
+ * brute-force MLE of the ORIGINAL table at r.  Returns 0 = accept, >0 = the
+ * 1-based round that failed, -100 = final product, -200-k = final of table k. */
+int or_sumcheck_verify(transcript *tr, uint32_t m, uint32_t n_eq, uint32_t K, const uint8_t *w_b,
+                       const uint8_t *claim_b, const uint8_t *msgs_b, const uint8_t *finals_b,
+                       const uint8_t *tables_b /* may be NULL */, uint8_t *r_out) {
+    init();
+    fr w[64], c, ev[4], fin[3];
+    if (load_point(w_b, (int)n_eq, w) || load_canon(claim_b, &c)) return -3;
+    uint32_t hdr[3] = {m, n_eq, K};
+    absorb_u32s(tr, "sc/hdr", hdr, 3);
+    absorb_frs(tr, "sc/claim", &c, 1);
+    fr r[64];
+    for (uint32_t t = 0; t < m; t++) {
+        for (uint32_t X = 0; X <= K; X++) if (load_canon(msgs_b + 32 * (t * (K + 1) + X), &ev[X])) return -3;
+        fr lhs = (t < n_eq) ? fr_add(fr_mul(fr_sub(fr_one(), w[t]), ev[0]), fr_mul(w[t], ev[1]))
+                            : fr_add(ev[0], ev[1]);
+        if (!fr_eq(lhs, c)) return (int)t + 1;
+        absorb_frs(tr, "sc/msg", ev, (int)K + 1);
+        r[t] = transcript_challenge(tr, "sc/r");
+        if (r_out) store_canon(r[t], r_out + 32 * t);
+        c = interp(ev, (int)K, r[t]);
+    }
+    fr prod = fr_one();
+    for (uint32_t k = 0; k < K; k++) {
+        if (load_canon(finals_b + 32 * k, &fin[k])) return -3;
+        prod = fr_mul(prod, fin[k]);
+    }
+    if (!fr_eq(prod, c)) return -100;
+    absorb_frs(tr, "sc/final", fin, (int)K);
+    if (tables_b) {
+        uint64_t n = 1ULL << m;
+        fr *tb = (fr *)malloc(n * sizeof(fr));
+        for (uint32_t k = 0; k < K; k++) {
+            for (uint64_t i = 0; i < n; i++) load_canon(tables_b + 32 * (k * n + i), &tb[i]);
+            if (!fr_eq(mle_fr(tb, (int)m, r), fin[k])) { free(tb); return -200 - (int)k; }
+        }
+        free(tb);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------ matmul
+ * A stored [N][D1][D2] (or [N][D2][D1] if transA), B stored [N][D2][D3] (or
+ * [N][D3][D2] if transB), int32.  Transcript (D3a): "mm/hdr" (logN, logD1,
+ * logD2, logD3) | w = "mm/w" x logN | u1 = "mm/u1" x logD1 | u3 = "mm/u3" x logD3
+ * | product sumcheck over At[k][n] = sum_a beta(u1,a) A[n][a][k] and
+ * Bt[k][n] = sum_c B[n][k][c] beta(u3,c) (flat index k*N + n, so the stack
+ * variables are bound first as in Prot. 2-3), n_eq = logN, K = 2, claim
+ * = Y~(w, u1, u3) where Y = A B is formed in exact integers and its MLE
+ * evaluated by brute force — independent of the At/Bt route.
+ */
+static inline int64_t Aget(const int32_t *A, int transA, uint64_t D1, uint64_t D2, uint64_t n, uint64_t a, uint64_t k) {
+    return transA ? A[(n * D2 + k) * D1 + a] : A[(n * D1 + a) * D2 + k];
+}
+static inline int64_t Bget(const int32_t *B, int transB, uint64_t D2, uint64_t D3, uint64_t n, uint64_t k, uint64_t c) {
+    return transB ? B[(n * D3 + c) * D2 + k] : B[(n * D2 + k) * D3 + c];
+}
+
+int or_matmul_reduce(transcript *tr, const int32_t *A, const int32_t *B, uint32_t logN, uint32_t logD1,
+                     uint32_t logD2, uint32_t logD3, int transA, int transB,
+                     uint8_t *pts_out /* logN+logD1+logD3 */, uint8_t *claim_out,
+                     uint8_t *At_out /* D2*N */, uint8_t *Bt_out /* D2*N */) {
+    init();
+    uint64_t N = 1ULL << logN, D1 = 1ULL << logD1, D2 = 1ULL << logD2, D3 = 1ULL << logD3;
+    uint32_t hdr[4] = {logN, logD1, logD2, logD3};
+    absorb_u32s(tr, "mm/hdr", hdr, 4);
+    fr w[64], u1[64], u3[64];
+    for (uint32_t i = 0; i < logN; i++) w[i] = transcript_challenge(tr, "mm/w");
+    for (uint32_t i = 0; i < logD1; i++) u1[i] = transcript_challenge(tr, "mm/u1");
+    for (uint32_t i = 0; i < logD3; i++) u3[i] = transcript_challenge(tr, "mm/u3");
+    for (uint32_t i = 0; i < logN; i++) store_canon(w[i], pts_out + 32 * i);
+    for (uint32_t i = 0; i < logD1; i++) store_canon(u1[i], pts_out + 32 * (logN + i));
+    for (uint32_t i = 0; i < logD3; i++) store_canon(u3[i], pts_out + 32 * (logN + logD1 + i));
+    /* eq vectors, each entry by the direct product formula */
+    fr *Ew = (fr *)malloc(N * sizeof(fr)), *E1 = (fr *)malloc(D1 * sizeof(fr)), *E3 = (fr *)malloc(D3 * sizeof(fr));
+    for (uint64_t i = 0; i < N; i++) Ew[i] = eq_at(w, (int)logN, i);
+    for (uint64_t i = 0; i < D1; i++) E1[i] = eq_at(u1, (int)logD1, i);
+    for (uint64_t i = 0; i < D3; i++) E3[i] = eq_at(u3, (int)logD3, i);
+    /* claim = sum_{n,a,c} beta(w,n) beta(u1,a) beta(u3,c) (A B)[n][a][c], Y = A B in exact integers */
+    fr claim = fr_zero();
+    int nt = omp_get_max_threads();
+    fr *part = (fr *)calloc((size_t)nt, sizeof(fr));
+    #pragma omp parallel
+    {
+        int id = omp_get_thread_num();
+        fr acc = fr_zero();
+        __int128 *row = (__int128 *)malloc(D3 * sizeof(__int128));
+        #pragma omp for collapse(2) schedule(static)
+        for (uint64_t n = 0; n < N; n++)
+            for (uint64_t a = 0; a < D1; a++) {
+                for (uint64_t c = 0; c < D3; c++) row[c] = 0;
+                for (uint64_t k = 0; k < D2; k++) {
+                    int64_t av = Aget(A, transA, D1, D2, n, a, k);
+                    if (!av) continue;
+                    for (uint64_t c = 0; c < D3; c++) row[c] += (__int128)av * Bget(B, transB, D2, D3, n, k, c);
+                }
+                fr ew = fr_mul(Ew[n], E1[a]);
+                for (uint64_t c = 0; c < D3; c++) {
+                    __int128 y = row[c];
+                    if (y == 0) continue;
+                    int neg = y < 0;
+                    unsigned __int128 uy = neg ? (unsigned __int128)(-y) : (unsigned __int128)y;
+                    uint64_t v[4] = {(uint64_t)uy, (uint64_t)(uy >> 64), 0, 0};
+                    fr fy = fr_from_canon(v);
+                    if (neg) fy = fr_neg(fy);
+                    acc = fr_add(acc, fr_mul(fr_mul(ew, E3[c]), fy));
+                }
+            }
+        free(row);
+        part[id] = acc;
+    }
+    for (int i = 0; i < nt; i++) claim = fr_add(claim, part[i]);
+    free(part);
+    store_canon(claim, claim_out);
+    /* restrictions (brute force sums) */
+    #pragma omp parallel for collapse(2) schedule(static)
+    for (uint64_t k = 0; k < D2; k++)
+        for (uint64_t n = 0; n < N; n++) {
+            fr sa = fr_zero(), sb = fr_zero();
+            for (uint64_t a = 0; a < D1; a++) {
+                int64_t v = Aget(A, transA, D1, D2, n, a, k);
+                if (v) sa = fr_add(sa, fr_mul(E1[a], fr_from_i64(v)));
+            }
+            for (uint64_t c = 0; c < D3; c++) {
+                int64_t v = Bget(B, transB, D2, D3, n, k, c);
+                if (v) sb = fr_add(sb, fr_mul(E3[c], fr_from_i64(v)));
+            }
+            store_canon(sa, At_out + 32 * (k * N + n));
+            store_canon(sb, Bt_out + 32 * (k * N + n));
+        }
+    free(Ew); free(E1); free(E3);
+    return 0;
+}
+
+/* ------------------------------------------------------------ zkReLU (Sec. 3, App. A)
+ * Inputs Z, G_A int32 [D] (D = 2^logD); Q + R <= 32 bits, padded to
+ * B = 2^logB columns with zero bits and zero weights (D12).
+ * aux[0,i,j] = bit j of Z_i, aux[1,i,j] = bit j of G_A_i (two's complement,
+ * P:L188-191), sigma_i = aux[0,i,Q+R-1] (sign of Z, D10).
+ * A and G_Z are formed by Lemma 1, NOT from the bits:
+ *   A = round(1{Z>=0} Z / 2^R),  G_Z = 1{Z>=0} round(G_A / 2^R), half-up (D9).
+ */
+static int64_t rnd_half_up(int64_t x, int R) {     /* floor((x + 2^{R-1}) / 2^R) */
+    int64_t num = x + ((int64_t)1 << (R - 1)), den = (int64_t)1 << R;
+    int64_t q = num / den;
+    if ((num % den) != 0 && num < 0) q -= 1;
+    return q;
+}
+/* Lemma-1 tables + rescale remainders: Z' = round(Z/2^R),
+ * R_Z = Z - 2^R Z', likewise for G_A; sign = 1{Z < 0}. Returns -2 on range. */
+int or_relu_tables(const int32_t *Z, const int32_t *GA, uint64_t D, uint32_t Q, uint32_t R,
+                   uint8_t *sign, int32_t *A, int32_t *GZ, int32_t *Zp, int32_t *GAp, int32_t *RZ, int32_t *RGA) {
+    if (Q + R > 32 || R < 1 || Q < 1) return -1;
+    int64_t lo = -((int64_t)1 << (Q + R - 1)), hi = ((int64_t)1 << (Q + R - 1));
+    for (uint64_t i = 0; i < D; i++) {
+        int64_t z = Z[i], g = GA[i];
+        if (z < lo || z >= hi || g < lo || g >= hi) return -2;
+        int64_t zp = rnd_half_up(z, (int)R), gp = rnd_half_up(g, (int)R);
+        sign[i] = z < 0;
+        A[i] = (int32_t)rnd_half_up(z >= 0 ? z : 0, (int)R);
+        GZ[i] = (int32_t)(z >= 0 ? gp : 0);
+        if (Zp) Zp[i] = (int32_t)zp;
+        if (GAp) GAp[i] = (int32_t)gp;
+        if (RZ) RZ[i] = (int32_t)(z - (zp << R));
+        if (RGA) RGA[i] = (int32_t)(g - (gp << R));
+    }
+    return 0;
+}
+
+/* Generic dense sum-of-products sumcheck with g_t messages of degree `deg`
+ * (P:L140): H = sum_x sum_terms coef_s prod_{k in term s} T_k(x).  Used for the
+ * zkReLU statement with every table materialised at full size 2^m. */
+typedef struct { fr coef; int nf; int f[4]; } term_t;
+
+static void dense_round(fr *const *T, const term_t *terms, int nterms, uint64_t half, int deg, fr *ev) {
+    int nt = omp_get_max_threads();
+    fr *part = (fr *)calloc((size_t)nt * 8, sizeof(fr));
+    #pragma omp parallel
+    {
+        int id = omp_get_thread_num();
+        fr acc[8];
+        for (int X = 0; X <= deg; X++) acc[X] = fr_zero();
+        #pragma omp for schedule(static)
+        for (uint64_t b = 0; b < half; b++)
+            for (int X = 0; X <= deg; X++) {
+                fr x = fr_from_u64((uint64_t)X);
+                fr s = fr_zero();
+                for (int q = 0; q < nterms; q++) {
+                    fr p = terms[q].coef;
+                    for (int f = 0; f < terms[q].nf; f++) {
+                        const fr *tk = T[terms[q].f[f]];
+                        p = fr_mul(p, fr_add(tk[2 * b], fr_mul(x, fr_sub(tk[2 * b + 1], tk[2 * b]))));
+                    }
+                    s = fr_add(s, p);
+                }
+                acc[X] = fr_add(acc[X], s);
+            }
+        for (int X = 0; X <= deg; X++) part[id * 8 + X] = acc[X];
+    }
+    for (int X = 0; X <= deg; X++) {
+        ev[X] = fr_zero();
+        for (int i = 0; i < nt; i++) ev[X] = fr_add(ev[X], part[i * 8 + X]);
+    }
+    free(part);
+}
+
+/* s_B weights and s', padded with zeros to B columns. */
+static fr s_weight(int j, int Q, int R) {
+    int QR = Q + R;
+    if (j >= QR) return fr_zero();
+    if (j == QR - 1) return fr_neg(fr_from_u64(1ULL << (QR - 1)));
+    return fr_from_u64(1ULL << j);
+}
+static fr sp_weight(int j, int Q, int R) {
+    int QR = Q + R;
+    if (j >= QR || j < R - 1) return fr_zero();
+    if (j == R - 1) return fr_one();
+    if (j == QR - 1) return fr_neg(fr_from_u64(1ULL << (Q - 1)));
+    return fr_from_u64(1ULL << (j - R));
+}
+
+enum { T_A0, T_A1, T_OMS, T_EZ, T_EA, T_EGA, T_EGZ, T_EB, T_S, T_SP, T_NT };
+
+/* zkReLU prover (App. A), dense, following the paper's six
+ * statements combined with weights r^2, r, 1, r'r^2, r'r, r' (D13).
+ * Transcript (D3b): "relu/hdr" (logD, Q, R) | u_Z, u_A, u_GA, u_GZ ("relu/uZ",
+ * "relu/uA", "relu/uGA", "relu/uGZ", logD each) | "relu/claims" (Z~(u_Z),
+ * A~(u_A), G_A~(u_GA), G_Z~(u_GZ)) | r = "relu/r", r' = "relu/rp", u_bin =
+ * "relu/ubin" x (logB + logD) (D5, D6) | per round "relu/msg" (4 evals) then
+ * "relu/x" | "relu/final" (aux~(0,v,w), aux~(1,v,w), aux~(0,v,Q+R-1)).
+ * Variables x = (j, i): flat index i*B + j, j bound first (D2).
+ */
+int or_relu_prove(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
+                  uint8_t *claims_out /* 4 */, uint8_t *chal_out /* 2 + logB + logD: r, r', u_bin */,
+                  uint8_t *msgs_out /* (logB+logD) x 4 */, uint8_t *rpt_out /* logB+logD */,
+                  uint8_t *finals_out /* 3 */) {
+    init();
+    uint64_t D = 1ULL << logD;
+    uint32_t QR = Q + R;
+    if (QR > 32 || Q < 1 || R < 1) return -1;
+    uint32_t logB = 0;
+    while ((1u << logB) < QR) logB++;
+    uint64_t B = 1ULL << logB;
+    int32_t *A = (int32_t *)malloc(D * 4), *GZ = (int32_t *)malloc(D * 4);
+    uint8_t *sg = (uint8_t *)malloc(D);
+    int st = or_relu_tables(Z, GA, D, Q, R, sg, A, GZ, NULL, NULL, NULL, NULL);
+    if (st) { free(A); free(GZ); free(sg); return st; }
+    uint32_t hdr[3] = {logD, Q, R};
+    absorb_u32s(tr, "relu/hdr", hdr, 3);
+    fr uZ[64], uA[64], uGA[64], uGZ[64], ub[64];
+    for (uint32_t i = 0; i < logD; i++) uZ[i] = transcript_challenge(tr, "relu/uZ");
+    for (uint32_t i = 0; i < logD; i++) uA[i] = transcript_challenge(tr, "relu/uA");
+    for (uint32_t i = 0; i < logD; i++) uGA[i] = transcript_challenge(tr, "relu/uGA");
+    for (uint32_t i = 0; i < logD; i++) uGZ[i] = transcript_challenge(tr, "relu/uGZ");
+    fr cl[4] = {mle_i32(Z, (int)logD, uZ), mle_i32(A, (int)logD, uA), mle_i32(GA, (int)logD, uGA),
+                mle_i32(GZ, (int)logD, uGZ)};
+    for (int i = 0; i < 4; i++) store_canon(cl[i], claims_out + 32 * i);
+    absorb_frs(tr, "relu/claims", cl, 4);
+    fr r = transcript_challenge(tr, "relu/r"), rp = transcript_challenge(tr, "relu/rp");
+    for (uint32_t i = 0; i < logB + logD; i++) ub[i] = transcript_challenge(tr, "relu/ubin");
+    store_canon(r, chal_out); store_canon(rp, chal_out + 32);
+    for (uint32_t i = 0; i < logB + logD; i++) store_canon(ub[i], chal_out + 64 + 32 * i);
+
+    uint32_t m = logB + logD;
+    uint64_t n = 1ULL << m;
+    fr *T[T_NT];
+    for (int k = 0; k < T_NT; k++) T[k] = (fr *)malloc(n * sizeof(fr));
+    #pragma omp parallel for schedule(static)
+    for (uint64_t i = 0; i < D; i++) {
+        fr ez = eq_at(uZ, (int)logD, i), ea = eq_at(uA, (int)logD, i);
+        fr ega = eq_at(uGA, (int)logD, i), egz = eq_at(uGZ, (int)logD, i);
+        uint32_t z = (uint32_t)Z[i], g = (uint32_t)GA[i];
+        fr oms = ((z >> (QR - 1)) & 1) ? fr_zero() : fr_one();
+        for (uint64_t j = 0; j < B; j++) {
+            uint64_t x = i * B + j;
+            T[T_A0][x] = (j < QR && ((z >> j) & 1)) ? fr_one() : fr_zero();
+            T[T_A1][x] = (j < QR && ((g >> j) & 1)) ? fr_one() : fr_zero();
+            T[T_OMS][x] = oms;
+            T[T_EZ][x] = ez; T[T_EA][x] = ea; T[T_EGA][x] = ega; T[T_EGZ][x] = egz;
+            T[T_EB][x] = eq_at(ub, (int)m, x);       /* beta(u_bin, i (+) j) with (+) = concatenation (D5) */
+            T[T_S][x] = s_weight((int)j, (int)Q, (int)R);
+            T[T_SP][x] = sp_weight((int)j, (int)Q, (int)R);
+        }
+    }
+    fr r2 = fr_mul(r, r);
+    term_t terms[8] = {
+        {r2, 3, {T_EZ, T_A0, T_S}},                               /* Eq. zkrelu-forward-in-sc   (r^2)  */
+        {r, 4, {T_EA, T_OMS, T_A0, T_SP}},                        /* Eq. zkrelu-forward-out-sc  (r)    */
+        {fr_one(), 3, {T_EB, T_A0, T_A0}},                        /* Eq. zkrelu-forward-bin-sc  (1)    */
+        {fr_neg(fr_one()), 2, {T_EB, T_A0}},
+        {fr_mul(rp, r2), 3, {T_EGA, T_A1, T_S}},                  /* Eq. zkrelu-backward-in-sc  (r'r^2)*/
+        {fr_mul(rp, r), 4, {T_EGZ, T_OMS, T_A1, T_SP}},           /* Eq. zkrelu-backward-out-sc (r'r)  */
+        {rp, 3, {T_EB, T_A1, T_A1}},                              /* Eq. zkrelu-backward-bin-sc (r')   */
+        {fr_neg(rp), 2, {T_EB, T_A1}},
+    };
+    for (uint32_t t = 0; t < m; t++) {
+        uint64_t half = n >> (t + 1);
+        fr ev[4];
+        dense_round(T, terms, 8, half, 3, ev);
+        absorb_frs(tr, "relu/msg", ev, 4);
+        for (int X = 0; X < 4; X++) store_canon(ev[X], msgs_out + 32 * (t * 4 + X));
+        fr x = transcript_challenge(tr, "relu/x");
+        store_canon(x, rpt_out + 32 * t);
+        #pragma omp parallel for schedule(static)
+        for (int k = 0; k < T_NT; k++)
+            for (uint64_t b = 0; b < half; b++)
+                T[k][b] = fr_add(T[k][2 * b], fr_mul(x, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+    }
+    fr fin[3] = {T[T_A0][0], T[T_A1][0], fr_sub(fr_one(), T[T_OMS][0])};
+    for (int i = 0; i < 3; i++) store_canon(fin[i], finals_out + 32 * i);
+    absorb_frs(tr, "relu/final", fin, 3);
+    for (int k = 0; k < T_NT; k++) free(T[k]);
+    free(A); free(GZ); free(sg);
+    return 0;
+}
+
+/* zkReLU verifier: replays the transcript from the proof, checks the claims
+ * against Z, G_A (brute-force MLE of the Lemma-1 tensors) when given, every
+ * round identity g(0)+g(1) = c, and the final identity using the verifier's
+ * own beta / s / s' evaluations, then the three aux finals against the
+ * brute-force MLE of the bits of Z and G_A.  Returns 0 on accept. */
+int or_relu_verify(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
+                   const uint8_t *claims_b, const uint8_t *msgs_b, const uint8_t *finals_b) {
+    init();
+    uint32_t QR = Q + R, logB = 0;
+    while ((1u << logB) < QR) logB++;
+    uint64_t D = 1ULL << logD;
+    uint32_t hdr[3] = {logD, Q, R};
+    absorb_u32s(tr, "relu/hdr", hdr, 3);
+    fr uZ[64], uA[64], uGA[64], uGZ[64], ub[64], cl[4], fin[3], ev[4], pt[64];
+    for (uint32_t i = 0; i < logD; i++) uZ[i] = transcript_challenge(tr, "relu/uZ");
+    for (uint32_t i = 0; i < logD; i++) uA[i] = transcript_challenge(tr, "relu/uA");
+    for (uint32_t i = 0; i < logD; i++) uGA[i] = transcript_challenge(tr, "relu/uGA");
+    for (uint32_t i = 0; i < logD; i++) uGZ[i] = transcript_challenge(tr, "relu/uGZ");
+    for (int i = 0; i < 4; i++) if (load_canon(claims_b + 32 * i, &cl[i])) return -3;
+    if (Z && GA) {
+        int32_t *A = (int32_t *)malloc(D * 4), *GZ = (int32_t *)malloc(D * 4);
+        uint8_t *sg = (uint8_t *)malloc(D);
+        if (or_relu_tables(Z, GA, D, Q, R, sg, A, GZ, NULL, NULL, NULL, NULL)) return -2;
+        int bad = !fr_eq(cl[0], mle_i32(Z, (int)logD, uZ)) || !fr_eq(cl[1], mle_i32(A, (int)logD, uA)) ||
+                  !fr_eq(cl[2], mle_i32(GA, (int)logD, uGA)) || !fr_eq(cl[3], mle_i32(GZ, (int)logD, uGZ));
+        free(A); free(GZ); free(sg);
+        if (bad) return -300;
+    }
+    absorb_frs(tr, "relu/claims", cl, 4);
+    fr r = transcript_challenge(tr, "relu/r"), rp = transcript_challenge(tr, "relu/rp");
+    uint32_t m = logB + logD;
+    for (uint32_t i = 0; i < m; i++) ub[i] = transcript_challenge(tr, "relu/ubin");
+    fr r2 = fr_mul(r, r);
+    fr c = fr_add(fr_add(fr_mul(r2, cl[0]), fr_mul(r, cl[1])),
+                  fr_mul(rp, fr_add(fr_mul(r2, cl[2]), fr_mul(r, cl[3]))));
+    for (uint32_t t = 0; t < m; t++) {
+        for (int X = 0; X < 4; X++) if (load_canon(msgs_b + 32 * (t * 4 + X), &ev[X])) return -3;
+        if (!fr_eq(fr_add(ev[0], ev[1]), c)) return (int)t + 1;
+        absorb_frs(tr, "relu/msg", ev, 4);
+        pt[t] = transcript_challenge(tr, "relu/x");
+        c = interp(ev, 3, pt[t]);
+    }
+    for (int i = 0; i < 3; i++) if (load_canon(finals_b + 32 * i, &fin[i])) return -3;
+    /* final identity: P(pt) with pt = (v_j, v_i) */
+    const fr *vj = pt, *vi = pt + logB;
+    fr s = fr_zero(), sp = fr_zero();
+    for (uint64_t j = 0; j < (1ULL << logB); j++) {
+        fr e = eq_at(vj, (int)logB, j);
+        s = fr_add(s, fr_mul(e, s_weight((int)j, (int)Q, (int)R)));
+        sp = fr_add(sp, fr_mul(e, sp_weight((int)j, (int)Q, (int)R)));
+    }
+    fr bez = fr_one(), bea = fr_one(), bega = fr_one(), begz = fr_one(), beb = fr_one();
+    for (uint32_t k = 0; k < logD; k++) {
+        #define BETA1(u, v) fr_add(fr_mul(u, v), fr_mul(fr_sub(fr_one(), u), fr_sub(fr_one(), v)))
+        bez = fr_mul(bez, BETA1(uZ[k], vi[k])); bea = fr_mul(bea, BETA1(uA[k], vi[k]));
+        bega = fr_mul(bega, BETA1(uGA[k], vi[k])); begz = fr_mul(begz, BETA1(uGZ[k], vi[k]));
+    }
+    for (uint32_t k = 0; k < m; k++) beb = fr_mul(beb, BETA1(ub[k], pt[k]));
+    #undef BETA1
+    fr a0 = fin[0], a1 = fin[1], oms = fr_sub(fr_one(), fin[2]);
+    fr P = fr_mul(r2, fr_mul(bez, fr_mul(a0, s)));
+    P = fr_add(P, fr_mul(r, fr_mul(bea, fr_mul(oms, fr_mul(a0, sp)))));
+    P = fr_add(P, fr_mul(beb, fr_sub(fr_mul(a0, a0), a0)));
+    P = fr_add(P, fr_mul(fr_mul(rp, r2), fr_mul(bega, fr_mul(a1, s))));
+    P = fr_add(P, fr_mul(fr_mul(rp, r), fr_mul(begz, fr_mul(oms, fr_mul(a1, sp)))));
+    P = fr_add(P, fr_mul(rp, fr_mul(beb, fr_sub(fr_mul(a1, a1), a1))));
+    if (!fr_eq(P, c)) return -100;
+    absorb_frs(tr, "relu/final", fin, 3);
+    if (Z && GA) {   /* the three aux claims against the bits of Z and G_A (brute force) */
+        fr s0 = fr_zero(), s1 = fr_zero(), sg = fr_zero();
+        for (uint64_t i = 0; i < D; i++) {
+            fr ei = eq_at(vi, (int)logD, i);
+            uint32_t z = (uint32_t)Z[i], g = (uint32_t)GA[i];
+            fr bz = fr_zero(), bg = fr_zero();
+            for (uint32_t j = 0; j < QR; j++) {
+                fr ej = eq_at(vj, (int)logB, j);
+                if ((z >> j) & 1) bz = fr_add(bz, ej);
+                if ((g >> j) & 1) bg = fr_add(bg, ej);
+            }
+            s0 = fr_add(s0, fr_mul(ei, bz));
+            s1 = fr_add(s1, fr_mul(ei, bg));
+            if ((z >> (QR - 1)) & 1) sg = fr_add(sg, ei);
+        }
+        if (!fr_eq(s0, fin[0])) return -201;
+        if (!fr_eq(s1, fin[1])) return -202;
+        if (!fr_eq(sg, fin[2])) return -203;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------ misc exports */
+void or_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
+int or_get_threads(void) { return omp_get_max_threads(); }
+uint64_t or_transcript_size(void) { return sizeof(transcript); }

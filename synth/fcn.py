@@ -1,0 +1,241 @@
+"""Quantized FCN training trace and FAC4DNN family assembly (input generation only).
+
+The prover's input is the training trace of PAPER.md Example 2 (L292-312):
+    Z^(l)   = A^(l-1) W^(l)                              (Eq. fcnn-Z)
+    A^(l)   = ReLU(round(Z^(l) / 2^R)),  1 <= l <= L-1    (L170)
+    G_Z^(L) = round(Z^(L) / 2^R) - Y                      (Eq. fcnn-GZ-last, rescaled once: DESIGN.md D16)
+    G_A^(l) = G_Z^(l+1) W^(l+1)^T,       1 <= l <= L-1    (Eq. fcnn-GA)
+    G_Z^(l) = 1{Z^(l) >= 0} * round(G_A^(l) / 2^R)        (L177, Lemma 1)
+    G_W^(l) = G_Z^(l)^T A^(l-1),         1 <= l <= L      (Eq. fcnn-GW)
+    W^(l)  -= round(G_W^(l)^T / 2^20)                     (optimizer unspecified, L309; trace only)
+round() is half-up (D9).  This module runs the *training* (the
+prover's input, Protocol 1 line 2), never any part of the proof.  Matmuls run
+in float64 BLAS, exact because every partial sum is an integer below 2^53
+(|entries| < 2^13, inner dimension <= 4096).
+
+Families: every forward / input-gradient /
+weight-gradient matmul and every ReLU is grouped by (equation type, shape);
+instances are ordered by (step, layer) and the stack axis is zero-padded to a
+power of two.  The family order is fixed: all F, then GA, then
+GW families (each in increasing first-layer order), then ReLU families.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .prng import DATA_SEED, uniform_range
+
+R_BITS = 16
+Q_BITS = 16
+LR_SHIFT = 20
+
+
+def _round_half_up(x: np.ndarray, r: int) -> np.ndarray:
+    return (x + (1 << (r - 1))) >> r
+
+
+def _matmul_exact(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    out = (a.astype(np.float64) @ b.astype(np.float64))
+    res = np.rint(out).astype(np.int64)
+    return res
+
+
+def _to_i32(x: np.ndarray, what: str) -> np.ndarray:
+    lim = 1 << 31
+    if x.size and (x.max() >= lim or x.min() < -lim):
+        raise OverflowError(f"{what} leaves int32: [{x.min()}, {x.max()}]")
+    return x.astype(np.int32)
+
+
+@dataclass
+class FcnShape:
+    name: str
+    dims: list            # padded widths d_0 .. d_L (powers of two)
+    real_dims: list       # unpadded widths
+    batch: int
+    steps: int            # T'
+
+
+C3_SHAPE = FcnShape("C3", [1024] * 9, [1024] * 9, 64, 1)
+C4_SHAPE = FcnShape("C4", [4096] + [1024] * 8 + [16], [3072] + [1024] * 8 + [10], 64, 16)
+
+
+def tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4):
+    dims = [din] + [width] * (layers - 1) + [dout]
+    return FcnShape(f"tiny{layers}x{width}", dims, list(dims), batch, steps)
+
+
+@dataclass
+class StepTrace:
+    A: list = field(default_factory=list)    # A[0] = X, A[l] for l=1..L-1 (int32 [B, d_l])
+    Z: list = field(default_factory=list)    # Z[l] for l=1..L (index 0 unused)
+    W: list = field(default_factory=list)    # W[l] [d_{l-1}, d_l] for l=1..L
+    GZ: list = field(default_factory=list)   # G_Z[l] for l=1..L
+    GA: list = field(default_factory=list)   # G_A[l] for l=1..L-1
+    GW: list = field(default_factory=list)   # G_W[l] [d_l, d_{l-1}] for l=1..L
+
+
+def _pad_mask(shape: FcnShape, l: int):
+    """Boolean mask of the real (unpadded) entries of W^(l)."""
+    r_in, r_out = shape.real_dims[l - 1], shape.real_dims[l]
+    m = np.zeros((shape.dims[l - 1], shape.dims[l]), dtype=bool)
+    m[:r_in, :r_out] = True
+    return m
+
+
+def generate_trace(shape: FcnShape, seed: int = DATA_SEED, x_bits=11, w_bits=12, y_bits=10):
+    """Run T' quantized SGD steps; returns a list of StepTrace (one per step)."""
+    L = len(shape.dims) - 1
+    B = shape.batch
+    W = [None]
+    for l in range(1, L + 1):
+        w = uniform_range(seed, 1000 + l, (shape.dims[l - 1], shape.dims[l]), -(1 << w_bits), 1 << w_bits).astype(np.int64)
+        w[~_pad_mask(shape, l)] = 0
+        W.append(w)
+    steps = []
+    for s in range(shape.steps):
+        tr = StepTrace()
+        x = uniform_range(seed, 100000 + s, (B, shape.dims[0]), -(1 << x_bits), 1 << x_bits).astype(np.int64)
+        x[:, shape.real_dims[0]:] = 0
+        A = [x]
+        Z = [None]
+        for l in range(1, L + 1):
+            z = _matmul_exact(A[l - 1], W[l])
+            _to_i32(z, f"Z^{l}")
+            Z.append(z)
+            if l < L:
+                A.append(np.where(z >= 0, _round_half_up(z, R_BITS), 0))
+        noise = uniform_range(seed, 200000 + s, (B, shape.dims[L]), -(1 << y_bits), 1 << y_bits).astype(np.int64)
+        noise[:, shape.real_dims[L]:] = 0
+        GZ = [None] * (L + 1)
+        GA = [None] * (L + 1)
+        GZ[L] = noise                     # = round(Z^(L)/2^R) - Y with Y := round(Z^(L)/2^R) - noise
+        for l in range(L - 1, 0, -1):
+            ga = _matmul_exact(GZ[l + 1], W[l + 1].T)
+            _to_i32(ga, f"G_A^{l}")
+            GA[l] = ga
+            GZ[l] = np.where(Z[l] >= 0, _round_half_up(ga, R_BITS), 0)
+        GW = [None]
+        for l in range(1, L + 1):
+            gw = _matmul_exact(GZ[l].T, A[l - 1])
+            _to_i32(gw, f"G_W^{l}")
+            GW.append(gw)
+        tr.A = [_to_i32(a, "A") for a in A]
+        tr.Z = [None] + [_to_i32(z, "Z") for z in Z[1:]]
+        tr.W = [None] + [_to_i32(w, "W") for w in W[1:]]
+        tr.GZ = [None] + [_to_i32(g, "G_Z") for g in GZ[1:]]
+        tr.GA = [None] + [_to_i32(GA[l], "G_A") for l in range(1, L)]
+        tr.GW = [None] + [_to_i32(g, "G_W") for g in GW[1:]]
+        steps.append(tr)
+        for l in range(1, L + 1):
+            W[l] = W[l] - _round_half_up(GW[l].T.astype(np.int64), LR_SHIFT)
+            W[l][~_pad_mask(shape, l)] = 0
+    return steps
+
+
+def _next_pow2(n: int) -> int:
+    return 1 << max(0, (n - 1).bit_length())
+
+
+def _stack(mats, n_pad):
+    shp = mats[0].shape
+    out = np.zeros((n_pad,) + shp, dtype=np.int32)
+    for i, m in enumerate(mats):
+        out[i] = m
+    return out
+
+
+@dataclass
+class MatmulFamily:
+    """Y[n] = op(A[n]) @ op(B[n]) for n < N (zero instances beyond the real count).
+
+    A is stored [N][D1][D2] (transA=False) or [N][D2][D1] (transA=True);
+    B is stored [N][D2][D3] (transB=False) or [N][D3][D2] (transB=True).
+    Y ([N][D1][D3]) is the trace's product tensor, kept for the oracle's checks.
+    """
+    name: str
+    A: np.ndarray
+    B: np.ndarray
+    Y: np.ndarray
+    transA: bool
+    transB: bool
+    n_real: int
+
+    @property
+    def logs(self):
+        N = self.A.shape[0]
+        D1 = self.A.shape[2] if self.transA else self.A.shape[1]
+        D2 = self.A.shape[1] if self.transA else self.A.shape[2]
+        D3 = self.B.shape[1] if self.transB else self.B.shape[2]
+        return tuple(int(v).bit_length() - 1 for v in (N, D1, D2, D3))
+
+
+@dataclass
+class ReluFamily:
+    """Stacked zkReLU instances: Z, G_A flattened to [D] int32 (D = N * per-instance size)."""
+    name: str
+    Z: np.ndarray
+    GA: np.ndarray
+    Q: int
+    R: int
+    n_real: int
+
+
+def assemble_families(shape: FcnShape, trace):
+    """Group the trace's operations into FAC4DNN families (fixed order, see module doc)."""
+    L = len(shape.dims) - 1
+    fam = []
+
+    def group(kind, layers, key_fn):
+        groups = {}
+        for l in layers:
+            groups.setdefault(key_fn(l), []).append(l)
+        return sorted(groups.items(), key=lambda kv: kv[1][0])
+
+    # forward: Z^(l) = A^(l-1) W^(l)
+    for key, ls in group("F", range(1, L + 1), lambda l: (shape.dims[l - 1], shape.dims[l])):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        fam.append(MatmulFamily(
+            f"F[{','.join(map(str, ls))}]",
+            _stack([trace[s].A[l - 1] for s, l in insts], N),
+            _stack([trace[s].W[l] for s, l in insts], N),
+            _stack([trace[s].Z[l] for s, l in insts], N), False, False, len(insts)))
+    # input gradients: G_A^(l) = G_Z^(l+1) W^(l+1)^T
+    for key, ls in group("GA", range(1, L), lambda l: (shape.dims[l + 1], shape.dims[l])):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        fam.append(MatmulFamily(
+            f"GA[{','.join(map(str, ls))}]",
+            _stack([trace[s].GZ[l + 1] for s, l in insts], N),
+            _stack([trace[s].W[l + 1] for s, l in insts], N),
+            _stack([trace[s].GA[l] for s, l in insts], N), False, True, len(insts)))
+    # weight gradients: G_W^(l) = G_Z^(l)^T A^(l-1)
+    for key, ls in group("GW", range(1, L + 1), lambda l: (shape.dims[l], shape.dims[l - 1])):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        fam.append(MatmulFamily(
+            f"GW[{','.join(map(str, ls))}]",
+            _stack([trace[s].GZ[l] for s, l in insts], N),
+            _stack([trace[s].A[l - 1] for s, l in insts], N),
+            _stack([trace[s].GW[l] for s, l in insts], N), True, False, len(insts)))
+    # zkReLU after every hidden layer
+    for key, ls in group("ReLU", range(1, L), lambda l: shape.dims[l]):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        per = shape.batch * shape.dims[ls[0]]
+        Z = np.zeros(N * per, dtype=np.int32)
+        G = np.zeros(N * per, dtype=np.int32)
+        for i, (s, l) in enumerate(insts):
+            Z[i * per:(i + 1) * per] = trace[s].Z[l].reshape(-1)
+            G[i * per:(i + 1) * per] = trace[s].GA[l].reshape(-1)
+        fam.append(ReluFamily(f"ReLU[{','.join(map(str, ls))}]", Z, G, Q_BITS, R_BITS, len(insts)))
+    return fam
+
+
+def fcn_header(shape: FcnShape) -> bytes:
+    """Bytes absorbed under tag "fcn/hdr" before the first family (D3d)."""
+    words = [len(shape.dims) - 1, shape.batch, shape.steps] + list(shape.dims)
+    return b"".join(int(w).to_bytes(4, "little") for w in words)

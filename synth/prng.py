@@ -1,0 +1,62 @@
+"""Counter-based PRNG (splitmix64) used for every synthetic tensor.
+
+Recipe (frozen in DESIGN.md "Input recipe"):
+    key   = (seed XOR (tensor_id * 0x9E3779B97F4A7C15)) + index      (mod 2^64)
+    x     = splitmix64(key)
+    value = lo + (x >> (64 - b))        for a range [lo, lo + 2^b)
+
+The data seed is 230716273 (the arXiv id).  The Fiat-Shamir seed of a named
+configuration is SHA256("zkdl-b200/fs-seed/" || name).
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+DATA_SEED = 230716273
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def fs_seed(config_name: str) -> bytes:
+    """32-byte Fiat-Shamir seed of a named configuration."""
+    return hashlib.sha256(b"zkdl-b200/fs-seed/" + config_name.encode()).digest()
+
+
+def splitmix64(z: np.ndarray) -> np.ndarray:
+    z = z.astype(np.uint64, copy=True)
+    with np.errstate(over="ignore"):
+        z += _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+        z = z ^ (z >> np.uint64(31))
+    return z
+
+
+def _keys(seed: int, tensor_id: int, n: int, offset: int = 0) -> np.ndarray:
+    base = (seed ^ ((tensor_id * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+    idx = np.arange(offset, offset + n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return idx + np.uint64(base)
+
+
+def uniform_bits(seed: int, tensor_id: int, n: int, lo: int, bits: int, offset: int = 0) -> np.ndarray:
+    """n int64 values uniform in [lo, lo + 2^bits), 1 <= bits <= 63."""
+    if not 1 <= bits <= 63:
+        raise ValueError("bits must be in [1, 63]")
+    x = splitmix64(_keys(seed, tensor_id, n, offset))
+    return (x >> np.uint64(64 - bits)).astype(np.int64) + np.int64(lo)
+
+
+def uniform_range(seed: int, tensor_id: int, shape, lo: int, hi: int, dtype=np.int32) -> np.ndarray:
+    """Tensor of the given shape, uniform in [lo, hi) where hi - lo is a power of two."""
+    span = hi - lo
+    bits = span.bit_length() - 1
+    if span <= 0 or (1 << bits) != span:
+        raise ValueError("hi - lo must be a positive power of two")
+    n = int(np.prod(shape)) if len(shape) else 1
+    if bits == 0:
+        return np.full(shape, lo, dtype=dtype)
+    return uniform_bits(seed, tensor_id, n, lo, bits).astype(dtype).reshape(shape)
