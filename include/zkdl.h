@@ -1,0 +1,150 @@
+/*
+ * zkdl.h — C ABI of libzkdl: the B200 (sm_100a) prover hot path of zkDL
+ * (arXiv 2307.16273).  Citations: P:Lnnn = PAPER.md line; Dn = DESIGN.md §3.
+ *
+ * Conventions for every entry point
+ *  - Field elements crossing the ABI are zk_fr: 32-byte little-endian canonical
+ *    integers < p (D1).  A non-canonical input returns ZK_ERR_NONCANONICAL.
+ *  - "d_" pointers are DEVICE pointers, borrowed: the library never frees them,
+ *    they must stay valid until the context stream has executed the call.
+ *    Int32 tensors are contiguous row-major; Fr tables are contiguous arrays of
+ *    32-byte elements in the library's internal Montgomery form (produced by
+ *    zk_embed_i32 / zk_eq_table; convert with zk_fr_table_to_canonical).
+ *    Device buffers must be 16-byte aligned (torch allocations are 256-B aligned).
+ *  - Host pointers ("out", "proof", "point_out", ...) are caller-allocated.
+ *    Calls that return host values enqueue their work on the context stream and
+ *    synchronise that stream once before returning.  Calls without host
+ *    outputs are asynchronous (stream-ordered).
+ *  - Sizes are powers of two given as log2 ("zero-padding may be
+ *    applied"); the Python layer pads.  Variables are bound LSB-first (D2).
+ *  - Every call returns a zk_status; zk_last_error(ctx) describes the last
+ *    failure.  There is no CPU fallback: without a CUDA device, calls return
+ *    ZK_ERR_CUDA.
+ *  - One context per host thread.  Scratch memory comes from the stream-ordered
+ *    CUDA memory pool of the context's device.
+ */
+#ifndef ZKDL_H
+#define ZKDL_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct zk_ctx zk_ctx;
+typedef struct zk_transcript zk_transcript;
+typedef struct { uint8_t b[32]; } zk_fr;
+
+typedef enum {
+    ZK_OK = 0,
+    ZK_ERR_ARG = -1,            /* bad size / null pointer / non power of two */
+    ZK_ERR_RANGE = -2,          /* input outside the (Q+R)-bit range */
+    ZK_ERR_NONCANONICAL = -3,   /* field element >= p */
+    ZK_ERR_OOM = -4,
+    ZK_ERR_CUDA = -5,
+    ZK_ERR_NCCL = -6,
+    ZK_ERR_UNIMPLEMENTED = -7,
+    ZK_ERR_INTERNAL = -8
+} zk_status;
+
+/* ------------------------------------------------------------------ context */
+/* device: CUDA ordinal; cuda_stream: a cudaStream_t (NULL = the legacy default stream). */
+zk_status zk_ctx_create(int device, void* cuda_stream, zk_ctx** out);
+void zk_ctx_destroy(zk_ctx* ctx);
+const char* zk_last_error(const zk_ctx* ctx);
+/* Library version string and the number of kernel launches issued by this context so far. */
+const char* zk_version(void);
+uint64_t zk_ctx_launch_count(const zk_ctx* ctx);
+zk_status zk_ctx_synchronize(zk_ctx* ctx);
+
+/* --------------------------------------------------- Fiat-Shamir transcript (D3)
+ * The 32-byte state lives in device memory; absorb/challenge run on the device.
+ * zk_transcript_absorb: tag is a NUL-terminated ASCII string of <= 255 bytes,
+ *   msg a HOST buffer of len bytes (asynchronous; msg may be reused on return).
+ * zk_transcript_challenges: n challenges with the same tag, returned to the host
+ *   (synchronises).  zk_transcript_state copies the 32-byte state to the host. */
+zk_status zk_transcript_new(zk_ctx* ctx, const uint8_t seed[32], zk_transcript** out);
+zk_status zk_transcript_absorb(zk_transcript* tr, const char* tag, const void* msg, uint64_t len);
+zk_status zk_transcript_challenges(zk_transcript* tr, const char* tag, uint32_t n, zk_fr* out);
+zk_status zk_transcript_state(zk_transcript* tr, uint8_t out[32]);
+void zk_transcript_free(zk_transcript* tr);
+
+/* ------------------------------------------------------------ tables (rows a1, a2)
+ * zk_embed_i32 (row a1): d_out[i] = v mod p (negatives -> p - |v|), Montgomery form.
+ * zk_eq_table  (row a2):   d_out[b] = scale * prod_t (u_t b_t + (1-u_t)(1-b_t)),
+ *   b in [0, 2^k), u_t <-> bit t of b (D2); scale NULL means 1.  k <= 32.
+ * zk_mle_eval_* (P:L146 Eq. multilinear-extension): out = sum_b T[b] beta(u, b), m = log2 |T|.
+ * zk_fr_table_to_canonical: d_out[i] = canonical 32-byte encoding of d_in[i] (may alias).
+ * zk_fr_table_from_canonical: the inverse; returns ZK_ERR_NONCANONICAL if any input >= p. */
+zk_status zk_embed_i32(zk_ctx* ctx, const int32_t* d_in, uint64_t n, void* d_out);
+zk_status zk_eq_table(zk_ctx* ctx, const zk_fr* point, uint32_t k, const zk_fr* scale, void* d_out);
+zk_status zk_mle_eval_i32(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const zk_fr* point, zk_fr* out);
+zk_status zk_mle_eval_fr(zk_ctx* ctx, const void* d_tab, uint32_t m, const zk_fr* point, zk_fr* out);
+zk_status zk_fr_table_to_canonical(zk_ctx* ctx, const void* d_in, uint64_t n, void* d_out);
+zk_status zk_fr_table_from_canonical(zk_ctx* ctx, const void* d_in, uint64_t n, void* d_out);
+
+/* ------------------------------------------- matmul -> sumcheck (row a3)
+ * Stacked product Y[n] = A[n] B[n], n < N.  A is stored [N][D1][D2] (trans_a = 0) or
+ * [N][D2][D1] (trans_a = 1); B is stored [N][D2][D3] (trans_b = 0) or [N][D3][D2].
+ * Transcript (D3a): absorb "mm/hdr" (logN, logD1, logD2, logD3 as u32le), draw
+ * w ("mm/w" x logN), u1 ("mm/u1" x logD1), u3 ("mm/u3" x logD3).
+ * Writes the restricted tables (Fr, Montgomery, flat index k*N + n, n minor):
+ *     d_At[k][n] = sum_a beta(u1, a) A[n][a][k]     d_Bt[k][n] = sum_c B[n][k][c] beta(u3, c)
+ * and returns (host) the point w||u1||u3 (logN + logD1 + logD3 elements) and the claim
+ *     claim = Y~(w, u1, u3) = sum_{k,n} beta(w, n) At[k][n] Bt[k][n].
+ * Follow with zk_sumcheck_prove(m = logN + logD2, n_eq = logN, K = 2, w, claim). */
+typedef struct { uint32_t logN, logD1, logD2, logD3; uint32_t trans_a, trans_b; } zk_mm_shape;
+zk_status zk_matmul_reduce(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, const int32_t* d_B, zk_mm_shape shape,
+                           void* d_At, void* d_Bt, zk_fr* point_out, zk_fr* claim_out);
+
+/* ------------------------------------- aggregated product sumcheck (rows a4-a6; Prot. 3 P:L504-527)
+ * Proves  claim = sum_{x in {0,1}^m} beta(w, x_{<n_eq}) * prod_{k<K} T_k(x),  1 <= K <= 3.
+ * d_tables[k]: Fr tables of 2^m elements (Montgomery), or int32 tables if bit k of i32_mask
+ * is set (embedded on the fly).  The tables are NOT modified.  w: host, n_eq elements.
+ * claim: host pointer, or NULL to let the prover compute it (it is then absorbed and
+ * returned in claim_out).  Transcript (D3c): "sc/hdr" (m, n_eq, K) | "sc/claim" | per round
+ * "sc/msg" (K+1 evaluations at X = 0..K: f_t for t < n_eq, g_t otherwise, D4) then
+ * challenge "sc/r" | "sc/final" (T_k~(r)).
+ * proof (host): u32le m, n_eq, K | claim | m*(K+1) evaluations | K finals; *proof_len is in/out.
+ * proof == NULL with proof_len != NULL is a size query (nothing is proved, transcript untouched);
+ * a too-small buffer returns ZK_ERR_ARG with the required size; proof == proof_len == NULL proves
+ * without returning the proof bytes.
+ * point_out (host, m elements) and finals_out (host, K elements) may be NULL. */
+typedef struct { uint32_t m, n_eq, n_tables, i32_mask; const zk_fr* w; } zk_prod_stmt;
+zk_status zk_sumcheck_prove(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt* st, void* const* d_tables,
+                            const zk_fr* claim, zk_fr* claim_out, uint8_t* proof, uint64_t* proof_len,
+                            zk_fr* point_out, zk_fr* finals_out);
+
+/* ----------------------------------------------------- zkReLU (rows a7, a8; Sec. 3, App. A)
+ * zk_relu_tables (row a7): from Z, G_A (int32, D entries, Q+R <= 32 bits) writes
+ *   sign = 1{Z < 0} (u8, D10), A = (1 - sign) Z', G_Z = (1 - sign) G_A' with Z' = round(Z / 2^R),
+ *   G_A' = round(G_A / 2^R) half-up (D9), and optionally Z', G_A', R_Z = Z - 2^R Z',
+ *   R_GA = G_A - 2^R G_A' (NULL to skip).  Returns ZK_ERR_RANGE (synchronising) if any
+ *   input leaves [-2^{Q+R-1}, 2^{Q+R-1}).
+ * zk_relu_prove (row a8): transcript (D3b): "relu/hdr" (logD, Q, R) | u_Z, u_A,
+ *   u_GA, u_GZ | "relu/claims" (Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ)) | r, r', u_bin |
+ *   logB + logD rounds of 4 evaluations (j bits first) | "relu/final" (aux~(0,v,w),
+ *   aux~(1,v,w), aux~(0,v,Q+R-1)), with logB = ceil(log2(Q+R)).
+ *   proof (host): u32le logD, Q, R | 4 claims | rounds x 4 evaluations | 3 finals; proof / proof_len
+ *   follow zk_sumcheck_prove's size-query convention.
+ *   claims_out (4), point_out (logB + logD) and finals_out (3) may be NULL. */
+zk_status zk_relu_tables(zk_ctx* ctx, const int32_t* d_Z, const int32_t* d_GA, uint64_t D, uint32_t Q, uint32_t R,
+                         uint8_t* d_sign, int32_t* d_A, int32_t* d_GZ, int32_t* d_Zp, int32_t* d_GAp, int32_t* d_RZ,
+                         int32_t* d_RGA);
+zk_status zk_relu_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                        uint32_t Q, uint32_t R, uint8_t* proof, uint64_t* proof_len, zk_fr* claims_out,
+                        zk_fr* point_out, zk_fr* finals_out);
+
+/* ----------------------------------------------------------------- diagnostics
+ * zk_diag_fr_op: element-wise d_out[i] = op(d_a[i], d_b[i]) on Montgomery tables, op 0 add, 1 sub,
+ *   2 mul, 3 inverse, 4 negate, 5 square (d_b may be NULL for 3-5).  Used by the parity tests.
+ * zk_diag_mul_bench: blocks x 256 threads each run 4 independent chains of `iters` Montgomery
+ *   products on register-resident values (d_seed: 1024 elements; d_out: blocks*256 elements);
+ *   bench.py times it to measure this implementation's sustained Fr-mul rate. */
+zk_status zk_diag_fr_op(zk_ctx* ctx, int op, const void* d_a, const void* d_b, uint64_t n, void* d_out);
+zk_status zk_diag_mul_bench(zk_ctx* ctx, const void* d_seed, uint32_t iters, uint32_t blocks, void* d_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZKDL_H */

@@ -1,0 +1,279 @@
+"""Thin Python binding of libzkdl (include/zkdl.h) — argument marshalling only.
+
+Every step of the proving path runs in the library's CUDA kernels; torch is
+used for device memory and streams.  Field elements are Python ints in
+[0, p); device Fr tables are torch.uint8 tensors of shape [n, 32] holding the
+library's internal (Montgomery) representation.  Function names follow the
+ABI with the ``zk_`` prefix dropped.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import MmShape, ProdStmt, ZkError, lib
+
+P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+
+
+def _fr_buf(vals) -> ctypes.Array:
+    b = b"".join((int(v) % P).to_bytes(32, "little") for v in vals)
+    return ctypes.create_string_buffer(b, max(1, len(b)))
+
+
+def _ints(buf, n: int) -> list:
+    raw = bytes(buf)[:32 * n]
+    return [int.from_bytes(raw[32 * i:32 * i + 32], "little") for i in range(n)]
+
+
+def _dev_ptr(t: torch.Tensor, dtype=None) -> int:
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"expected {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+class Context:
+    """zk_ctx: a device, a CUDA stream (torch's current stream by default), the last error."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = ctypes.c_void_p()
+        st = lib().zk_ctx_create(device, ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if st != 0:
+            raise ZkError(st, "zk_ctx_create failed (no sm_100 CUDA device?)")
+        self.h = h
+
+    def check(self, st: int):
+        if st != 0:
+            raise ZkError(st, lib().zk_last_error(self.h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(lib().zk_ctx_launch_count(self.h))
+
+    def synchronize(self):
+        self.check(lib().zk_ctx_synchronize(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().zk_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Transcript:
+    """zk_transcript: device-resident Fiat-Shamir state (D3)."""
+
+    def __init__(self, ctx: Context, seed: bytes):
+        assert len(seed) == 32
+        self.ctx = ctx
+        h = ctypes.c_void_p()
+        ctx.check(lib().zk_transcript_new(ctx.h, seed, ctypes.byref(h)))
+        self.h = h
+
+    def absorb(self, tag: str, msg: bytes):
+        self.ctx.check(lib().zk_transcript_absorb(self.h, tag.encode(), msg, len(msg)))
+
+    def challenges(self, tag: str, n: int) -> list:
+        out = ctypes.create_string_buffer(max(1, 32 * n))
+        self.ctx.check(lib().zk_transcript_challenges(self.h, tag.encode(), n, out))
+        return _ints(out, n)
+
+    def state(self) -> bytes:
+        out = ctypes.create_string_buffer(32)
+        self.ctx.check(lib().zk_transcript_state(self.h, out))
+        return out.raw[:32]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().zk_transcript_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- tables (rows a1, a2)
+def fr_empty(n: int, device) -> torch.Tensor:
+    return torch.empty((n, 32), dtype=torch.uint8, device=device)
+
+
+def embed_i32(ctx: Context, t: torch.Tensor) -> torch.Tensor:
+    out = fr_empty(t.numel(), t.device)
+    ctx.check(lib().zk_embed_i32(ctx.h, _dev_ptr(t, torch.int32), t.numel(), out.data_ptr()))
+    return out
+
+
+def eq_table(ctx: Context, point: list, scale: int | None = None, device="cuda") -> torch.Tensor:
+    k = len(point)
+    out = fr_empty(1 << k, device)
+    sc = _fr_buf([scale]) if scale is not None else None
+    ctx.check(lib().zk_eq_table(ctx.h, _fr_buf(point), k, sc, out.data_ptr()))
+    return out
+
+
+def mle_eval_i32(ctx: Context, tab: torch.Tensor, point: list) -> int:
+    out = ctypes.create_string_buffer(32)
+    ctx.check(lib().zk_mle_eval_i32(ctx.h, _dev_ptr(tab, torch.int32), len(point), _fr_buf(point), out))
+    return _ints(out, 1)[0]
+
+
+def mle_eval_fr(ctx: Context, tab: torch.Tensor, point: list) -> int:
+    out = ctypes.create_string_buffer(32)
+    ctx.check(lib().zk_mle_eval_fr(ctx.h, _dev_ptr(tab, torch.uint8), len(point), _fr_buf(point), out))
+    return _ints(out, 1)[0]
+
+
+def fr_table_to_canonical(ctx: Context, tab: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(tab)
+    ctx.check(lib().zk_fr_table_to_canonical(ctx.h, _dev_ptr(tab, torch.uint8), tab.shape[0], out.data_ptr()))
+    return out
+
+
+def fr_table_from_canonical(ctx: Context, tab: torch.Tensor) -> torch.Tensor:
+    out = torch.empty_like(tab)
+    ctx.check(lib().zk_fr_table_from_canonical(ctx.h, _dev_ptr(tab, torch.uint8), tab.shape[0], out.data_ptr()))
+    return out
+
+
+def fr_table_to_ints(ctx: Context, tab: torch.Tensor) -> list:
+    raw = fr_table_to_canonical(ctx, tab).cpu().numpy().tobytes()
+    return [int.from_bytes(raw[32 * i:32 * i + 32], "little") for i in range(tab.shape[0])]
+
+
+def fr_table_from_ints(ctx: Context, vals, device="cuda") -> torch.Tensor:
+    raw = b"".join((int(v) % P).to_bytes(32, "little") for v in vals)
+    t = torch.frombuffer(bytearray(raw), dtype=torch.uint8).reshape(-1, 32).to(device)
+    return fr_table_from_canonical(ctx, t)
+
+
+# ---------------------------------------------------------------- matmul (row a3)
+def _log2(n: int) -> int:
+    l = n.bit_length() - 1
+    if n != 1 << l:
+        raise ValueError(f"{n} is not a power of two")
+    return l
+
+
+def matmul_reduce(ctx: Context, tr: Transcript, A: torch.Tensor, B: torch.Tensor, trans_a=False, trans_b=False):
+    """A: [N][D1][D2] (or [N][D2][D1]), B: [N][D2][D3] (or [N][D3][D2]) int32 on the device."""
+    N = A.shape[0]
+    D1, D2 = (A.shape[2], A.shape[1]) if trans_a else (A.shape[1], A.shape[2])
+    D3 = B.shape[1] if trans_b else B.shape[2]
+    lN, l1, l2, l3 = (_log2(int(v)) for v in (N, D1, D2, D3))
+    At = fr_empty(D2 * N, A.device)
+    Bt = fr_empty(D2 * N, A.device)
+    np_ = lN + l1 + l3
+    pts = ctypes.create_string_buffer(max(32, 32 * np_))
+    claim = ctypes.create_string_buffer(32)
+    sh = MmShape(lN, l1, l2, l3, int(trans_a), int(trans_b))
+    ctx.check(lib().zk_matmul_reduce(ctx.h, tr.h, _dev_ptr(A, torch.int32), _dev_ptr(B, torch.int32), sh,
+                                     At.data_ptr(), Bt.data_ptr(), pts, claim))
+    P_ = _ints(pts, np_)
+    return dict(logs=(lN, l1, l2, l3), At=At, Bt=Bt, w=P_[:lN], u1=P_[lN:lN + l1], u3=P_[lN + l1:],
+                claim=_ints(claim, 1)[0])
+
+
+# ---------------------------------------------------------------- product sumcheck (rows a4-a6)
+def parse_sumcheck_proof(raw: bytes) -> dict:
+    m, n_eq, K = (int.from_bytes(raw[4 * i:4 * i + 4], "little") for i in range(3))
+    vals = [int.from_bytes(raw[12 + 32 * i:44 + 32 * i], "little") for i in range((len(raw) - 12) // 32)]
+    claim = vals[0]
+    msgs = [vals[1 + t * (K + 1):1 + (t + 1) * (K + 1)] for t in range(m)]
+    finals = vals[1 + m * (K + 1):1 + m * (K + 1) + K]
+    return dict(m=m, n_eq=n_eq, K=K, claim=claim, msgs=msgs, finals=finals)
+
+
+def sumcheck_prove(ctx: Context, tr: Transcript, m: int, n_eq: int, tables: list, w: list, claim: int | None = None):
+    """tables: Fr tables ([2^m, 32] uint8, Montgomery) or int32 tables of 2^m entries."""
+    K = len(tables)
+    mask = 0
+    ptrs = (ctypes.c_void_p * K)()
+    for k, t in enumerate(tables):
+        if t.dtype == torch.int32:
+            mask |= 1 << k
+            assert t.numel() == 1 << m
+        else:
+            assert t.dtype == torch.uint8 and t.shape == (1 << m, 32)
+        ptrs[k] = _dev_ptr(t)
+    wbuf = _fr_buf(w)
+    stmt = ProdStmt(m, n_eq, K, mask, ctypes.cast(wbuf, ctypes.c_void_p))
+    plen = ctypes.c_uint64(12 + 32 + 32 * m * (K + 1) + 32 * K)
+    proof = ctypes.create_string_buffer(plen.value)
+    point = ctypes.create_string_buffer(32 * m)
+    cbuf = _fr_buf([claim]) if claim is not None else None
+    ctx.check(lib().zk_sumcheck_prove(ctx.h, tr.h, ctypes.byref(stmt), ptrs, cbuf, None, proof, ctypes.byref(plen),
+                                      point, None))
+    res = parse_sumcheck_proof(proof.raw[:plen.value])
+    res["r"] = _ints(point, m)
+    res["proof"] = proof.raw[:plen.value]
+    return res
+
+
+# ---------------------------------------------------------------- zkReLU (rows a7, a8)
+def relu_tables(ctx: Context, Z: torch.Tensor, GA: torch.Tensor, Q: int = 16, R: int = 16, extras: bool = True):
+    D = Z.numel()
+    dev = Z.device
+    sign = torch.empty(D, dtype=torch.uint8, device=dev)
+    outs = {k: torch.empty(D, dtype=torch.int32, device=dev) for k in ("A", "GZ", "Zp", "GAp", "RZ", "RGA")}
+    ex = [outs[k].data_ptr() if extras else None for k in ("Zp", "GAp", "RZ", "RGA")]
+    ctx.check(lib().zk_relu_tables(ctx.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), D, Q, R,
+                                   sign.data_ptr(), outs["A"].data_ptr(), outs["GZ"].data_ptr(), *ex))
+    outs["sign"] = sign
+    return outs
+
+
+def relu_logB(Q: int, R: int) -> int:
+    return max(0, (Q + R - 1).bit_length())
+
+
+def parse_relu_proof(raw: bytes, logB: int) -> dict:
+    logD, Q, R = (int.from_bytes(raw[4 * i:4 * i + 4], "little") for i in range(3))
+    vals = [int.from_bytes(raw[12 + 32 * i:44 + 32 * i], "little") for i in range((len(raw) - 12) // 32)]
+    m = logB + logD
+    return dict(logD=logD, Q=Q, R=R, claims=vals[:4], msgs=[vals[4 + 4 * t:8 + 4 * t] for t in range(m)],
+                finals=vals[4 + 4 * m:7 + 4 * m])
+
+
+def relu_prove(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, Q: int = 16, R: int = 16):
+    D = Z.numel()
+    logD = _log2(D)
+    logB = relu_logB(Q, R)
+    plen = ctypes.c_uint64(12 + 128 + 128 * (logB + logD) + 96)
+    proof = ctypes.create_string_buffer(plen.value)
+    point = ctypes.create_string_buffer(32 * (logB + logD))
+    ctx.check(lib().zk_relu_prove(ctx.h, tr.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), logD, Q, R, proof,
+                                  ctypes.byref(plen), None, point, None))
+    res = parse_relu_proof(proof.raw[:plen.value], logB)
+    res["point"] = _ints(point, logB + logD)
+    res["proof"] = proof.raw[:plen.value]
+    return res
+
+
+# ---------------------------------------------------------------- diagnostics
+def diag_fr_op(ctx: Context, op: str, a: torch.Tensor, b: torch.Tensor | None = None) -> torch.Tensor:
+    code = {"add": 0, "sub": 1, "mul": 2, "inv": 3, "neg": 4, "sqr": 5}[op]
+    out = torch.empty_like(a)
+    ctx.check(lib().zk_diag_fr_op(ctx.h, code, _dev_ptr(a), None if b is None else _dev_ptr(b), a.shape[0],
+                                  out.data_ptr()))
+    return out
+
+
+def diag_mul_bench(ctx: Context, seed: torch.Tensor, iters: int, blocks: int) -> torch.Tensor:
+    out = fr_empty(blocks * 256, seed.device)
+    ctx.check(lib().zk_diag_mul_bench(ctx.h, _dev_ptr(seed), iters, blocks, out.data_ptr()))
+    return out

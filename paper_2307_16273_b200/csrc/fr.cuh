@@ -1,0 +1,302 @@
+// fr.cuh — BLS12-381 scalar field Fr on sm_100a (D1).
+//
+// Representation: 8 x 32-bit little-endian limbs, Montgomery form with R = 2^256,
+// array-of-structs in HBM (32 B per element, two 16-B vector accesses).
+// Multiplication: CIOS (coarsely integrated operand scanning) with PTX carry
+// chains: per limb b_i one mad.lo chain and one mad.hi chain for a*b_i, then
+// m = t_0 * n0 (n0 = -p^{-1} mod 2^32 = 0xffffffff) and the same two chains for
+// m*p.  Because p < 2^255 the running value stays < 2p and every pre-shift sum
+// < 2p * 2^32 < 2^288, so 9 limbs suffice (no carry word).  Constants below were
+// derived with Python integers (tests/test_build.py re-derives them).
+#pragma once
+#include <stdint.h>
+
+namespace zk {
+
+struct __align__(16) fr_t { uint32_t v[8]; };
+
+// p = 0x73eda753299d7d483339d80809a1d80553bda402fffe5bfeffffffff00000001
+#define ZK_P0 0x00000001u
+#define ZK_P1 0xffffffffu
+#define ZK_P2 0xfffe5bfeu
+#define ZK_P3 0x53bda402u
+#define ZK_P4 0x09a1d805u
+#define ZK_P5 0x3339d808u
+#define ZK_P6 0x299d7d48u
+#define ZK_P7 0x73eda753u
+
+__host__ __device__ constexpr fr_t fr_const(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                            uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+    return fr_t{{a0, a1, a2, a3, a4, a5, a6, a7}};
+}
+// R mod p (Montgomery 1), R^2 mod p, R^3 mod p, Montgomery form of 2^31
+#define ZK_ONE  fr_const(0xfffffffeu, 0x00000001u, 0x00034802u, 0x5884b7fau, 0xecbc4ff5u, 0x998c4fefu, 0xacc5056fu, 0x1824b159u)
+#define ZK_R2   fr_const(0xf3f29c6du, 0xc999e990u, 0x87925c23u, 0x2b6cedcbu, 0x7254398fu, 0x05d31496u, 0x9f59ff11u, 0x0748d9d9u)
+#define ZK_R3   fr_const(0x439b73afu, 0xc62c1807u, 0x8cf06990u, 0x1b3e0d18u, 0xc7b5f418u, 0x73d13c71u, 0xc8db33e9u, 0x6e2a5bb9u)
+#define ZK_TWO31_MONT fr_const(0xe557b58au, 0x1aa84a74u, 0x34d1e277u, 0xa537585bu, 0x25370837u, 0x0b017f57u, 0x8b620bfbu, 0x73ac0a47u)
+
+__device__ __forceinline__ fr_t fr_zero() { return fr_t{{0, 0, 0, 0, 0, 0, 0, 0}}; }
+__device__ __forceinline__ fr_t fr_one() { return ZK_ONE; }
+
+__device__ __forceinline__ bool fr_is_zero(const fr_t& a) {
+    return (a.v[0] | a.v[1] | a.v[2] | a.v[3] | a.v[4] | a.v[5] | a.v[6] | a.v[7]) == 0;
+}
+__device__ __forceinline__ bool fr_equal(const fr_t& a, const fr_t& b) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) d |= a.v[i] ^ b.v[i];
+    return d == 0;
+}
+
+// x - p if x >= p (x < 2p < 2^256), branch-free
+__device__ __forceinline__ fr_t fr_reduce_once(const fr_t& x) {
+    fr_t r;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %9,  %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]), "=r"(r.v[6]),
+          "=r"(r.v[7]), "=r"(borrow)
+        : "r"(x.v[0]), "r"(x.v[1]), "r"(x.v[2]), "r"(x.v[3]), "r"(x.v[4]), "r"(x.v[5]), "r"(x.v[6]), "r"(x.v[7]),
+          "n"(ZK_P0), "n"(ZK_P1), "n"(ZK_P2), "n"(ZK_P3), "n"(ZK_P4), "n"(ZK_P5), "n"(ZK_P6), "n"(ZK_P7));
+    // borrow = 0xffffffff when x < p: keep x
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = borrow ? x.v[i] : r.v[i];
+    return r;
+}
+
+__device__ __forceinline__ fr_t fr_add(const fr_t& a, const fr_t& b) {
+    fr_t s;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(s.v[0]), "=r"(s.v[1]), "=r"(s.v[2]), "=r"(s.v[3]), "=r"(s.v[4]), "=r"(s.v[5]), "=r"(s.v[6]), "=r"(s.v[7])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    return fr_reduce_once(s);   // a + b < 2p < 2^256: no carry out
+}
+
+__device__ __forceinline__ fr_t fr_sub(const fr_t& a, const fr_t& b) {
+    fr_t d;
+    uint32_t borrow;
+    asm("sub.cc.u32  %0, %9,  %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(d.v[0]), "=r"(d.v[1]), "=r"(d.v[2]), "=r"(d.v[3]), "=r"(d.v[4]), "=r"(d.v[5]), "=r"(d.v[6]),
+          "=r"(d.v[7]), "=r"(borrow)
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]), "r"(a.v[6]), "r"(a.v[7]),
+          "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]), "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    // add (p & borrow)
+    const uint32_t m = borrow;
+    asm("add.cc.u32  %0, %0, %8;\n\t"
+        "addc.cc.u32 %1, %1, %9;\n\t"
+        "addc.cc.u32 %2, %2, %10;\n\t"
+        "addc.cc.u32 %3, %3, %11;\n\t"
+        "addc.cc.u32 %4, %4, %12;\n\t"
+        "addc.cc.u32 %5, %5, %13;\n\t"
+        "addc.cc.u32 %6, %6, %14;\n\t"
+        "addc.u32    %7, %7, %15;"
+        : "+r"(d.v[0]), "+r"(d.v[1]), "+r"(d.v[2]), "+r"(d.v[3]), "+r"(d.v[4]), "+r"(d.v[5]), "+r"(d.v[6]), "+r"(d.v[7])
+        : "r"(ZK_P0 & m), "r"(ZK_P1 & m), "r"(ZK_P2 & m), "r"(ZK_P3 & m), "r"(ZK_P4 & m), "r"(ZK_P5 & m),
+          "r"(ZK_P6 & m), "r"(ZK_P7 & m));
+    return d;
+}
+
+__device__ __forceinline__ fr_t fr_neg(const fr_t& a) { return fr_sub(fr_zero(), a); }
+__device__ __forceinline__ fr_t fr_dbl(const fr_t& a) { return fr_add(a, a); }
+
+// t[0..8] += a[0..7] * bi   (two carry chains; total stays < 2^288 by the CIOS bound)
+#define ZK_MAC_ROW(t, a, bi)                                                                           \
+    asm("mad.lo.cc.u32  %0, %9,  %17, %0;\n\t"                                                         \
+        "madc.lo.cc.u32 %1, %10, %17, %1;\n\t"                                                         \
+        "madc.lo.cc.u32 %2, %11, %17, %2;\n\t"                                                         \
+        "madc.lo.cc.u32 %3, %12, %17, %3;\n\t"                                                         \
+        "madc.lo.cc.u32 %4, %13, %17, %4;\n\t"                                                         \
+        "madc.lo.cc.u32 %5, %14, %17, %5;\n\t"                                                         \
+        "madc.lo.cc.u32 %6, %15, %17, %6;\n\t"                                                         \
+        "madc.lo.cc.u32 %7, %16, %17, %7;\n\t"                                                         \
+        "addc.u32       %8, %8, 0;\n\t"                                                                \
+        "mad.hi.cc.u32  %1, %9,  %17, %1;\n\t"                                                         \
+        "madc.hi.cc.u32 %2, %10, %17, %2;\n\t"                                                         \
+        "madc.hi.cc.u32 %3, %11, %17, %3;\n\t"                                                         \
+        "madc.hi.cc.u32 %4, %12, %17, %4;\n\t"                                                         \
+        "madc.hi.cc.u32 %5, %13, %17, %5;\n\t"                                                         \
+        "madc.hi.cc.u32 %6, %14, %17, %6;\n\t"                                                         \
+        "madc.hi.cc.u32 %7, %15, %17, %7;\n\t"                                                         \
+        "madc.hi.u32    %8, %16, %17, %8;"                                                             \
+        : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), \
+          "+r"(t[8])                                                                                   \
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(bi))
+
+// t[0..8] += p * m, then t >>= 32 (t[0] becomes 0 by construction of m)
+#define ZK_REDC_ROW(t)                                                                                 \
+    do {                                                                                               \
+        uint32_t m_ = t[0] * 0xffffffffu;                                                              \
+        asm("mad.lo.cc.u32  %0, %9, %10, %0;\n\t"                                                      \
+            "madc.lo.cc.u32 %1, %9, %11, %1;\n\t"                                                      \
+            "madc.lo.cc.u32 %2, %9, %12, %2;\n\t"                                                      \
+            "madc.lo.cc.u32 %3, %9, %13, %3;\n\t"                                                      \
+            "madc.lo.cc.u32 %4, %9, %14, %4;\n\t"                                                      \
+            "madc.lo.cc.u32 %5, %9, %15, %5;\n\t"                                                      \
+            "madc.lo.cc.u32 %6, %9, %16, %6;\n\t"                                                      \
+            "madc.lo.cc.u32 %7, %9, %17, %7;\n\t"                                                      \
+            "addc.u32       %8, %8, 0;\n\t"                                                            \
+            "mad.hi.cc.u32  %1, %9, %10, %1;\n\t"                                                      \
+            "madc.hi.cc.u32 %2, %9, %11, %2;\n\t"                                                      \
+            "madc.hi.cc.u32 %3, %9, %12, %3;\n\t"                                                      \
+            "madc.hi.cc.u32 %4, %9, %13, %4;\n\t"                                                      \
+            "madc.hi.cc.u32 %5, %9, %14, %5;\n\t"                                                      \
+            "madc.hi.cc.u32 %6, %9, %15, %6;\n\t"                                                      \
+            "madc.hi.cc.u32 %7, %9, %16, %7;\n\t"                                                      \
+            "madc.hi.u32    %8, %9, %17, %8;"                                                          \
+            : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]),    \
+              "+r"(t[7]), "+r"(t[8])                                                                   \
+            : "r"(m_), "n"(ZK_P0), "n"(ZK_P1), "n"(ZK_P2), "n"(ZK_P3), "n"(ZK_P4), "n"(ZK_P5),        \
+              "n"(ZK_P6), "n"(ZK_P7));                                                                 \
+        t[0] = t[1]; t[1] = t[2]; t[2] = t[3]; t[3] = t[4]; t[4] = t[5]; t[5] = t[6]; t[6] = t[7];     \
+        t[7] = t[8]; t[8] = 0;                                                                         \
+    } while (0)
+
+// Montgomery product a * b * R^{-1} mod p.  Requires a < p; b may be any value < 2^256.
+__device__ __forceinline__ fr_t fr_mul(const fr_t& a, const fr_t& b) {
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        ZK_MAC_ROW(t, a.v, b.v[i]);
+        ZK_REDC_ROW(t);
+    }
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = t[i];
+    return fr_reduce_once(r);
+}
+__device__ __forceinline__ fr_t fr_sqr(const fr_t& a) { return fr_mul(a, a); }
+
+// Montgomery reduction of a wide unsigned integer T (10 limbs, T < p * 2^256):
+// returns T * R^{-1} mod p.  Used by the int32 x Fr lazy accumulators.
+__device__ __forceinline__ fr_t fr_redc_wide(const uint32_t w[10]) {
+    uint32_t t[9] = {w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8]};
+    uint32_t hi = w[9];
+    // 8 reduction steps; after each shift the next input limb enters at t[8]
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint32_t m_ = t[0] * 0xffffffffu;
+        uint32_t carry;
+        asm("mad.lo.cc.u32  %0, %10, %11, %0;\n\t"
+            "madc.lo.cc.u32 %1, %10, %12, %1;\n\t"
+            "madc.lo.cc.u32 %2, %10, %13, %2;\n\t"
+            "madc.lo.cc.u32 %3, %10, %14, %3;\n\t"
+            "madc.lo.cc.u32 %4, %10, %15, %4;\n\t"
+            "madc.lo.cc.u32 %5, %10, %16, %5;\n\t"
+            "madc.lo.cc.u32 %6, %10, %17, %6;\n\t"
+            "madc.lo.cc.u32 %7, %10, %18, %7;\n\t"
+            "addc.cc.u32    %8, %8, 0;\n\t"
+            "addc.u32       %9, 0, 0;\n\t"
+            "mad.hi.cc.u32  %1, %10, %11, %1;\n\t"
+            "madc.hi.cc.u32 %2, %10, %12, %2;\n\t"
+            "madc.hi.cc.u32 %3, %10, %13, %3;\n\t"
+            "madc.hi.cc.u32 %4, %10, %14, %4;\n\t"
+            "madc.hi.cc.u32 %5, %10, %15, %5;\n\t"
+            "madc.hi.cc.u32 %6, %10, %16, %6;\n\t"
+            "madc.hi.cc.u32 %7, %10, %17, %7;\n\t"
+            "madc.hi.cc.u32 %8, %10, %18, %8;\n\t"
+            "addc.u32       %9, %9, 0;"
+            : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]),
+              "+r"(t[8]), "=r"(carry)
+            : "r"(m_), "n"(ZK_P0), "n"(ZK_P1), "n"(ZK_P2), "n"(ZK_P3), "n"(ZK_P4), "n"(ZK_P5), "n"(ZK_P6),
+              "n"(ZK_P7));
+        // shift down one limb; the carry and the next input limb (hi) form the new t[8]
+        t[0] = t[1]; t[1] = t[2]; t[2] = t[3]; t[3] = t[4]; t[4] = t[5]; t[5] = t[6]; t[6] = t[7]; t[7] = t[8];
+        t[8] = carry + (i == 0 ? hi : 0u);
+    }
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = t[i];
+    // T < 2^300 ⇒ result < 2^44 + p < 2p; t[8] == 0
+    return fr_reduce_once(r);
+}
+
+// ---------------------------------------------------------------- conversions
+__device__ __forceinline__ fr_t fr_from_u32(uint32_t x) {      // Montgomery form of a small integer
+    fr_t b = fr_zero();
+    b.v[0] = x;
+    return fr_mul(ZK_R2, b);
+}
+__device__ __forceinline__ fr_t fr_from_i32(int32_t x) {
+    fr_t a = fr_from_u32(x < 0 ? (uint32_t)(-(int64_t)x) : (uint32_t)x);
+    return x < 0 ? fr_neg(a) : a;
+}
+__device__ __forceinline__ fr_t fr_to_canonical(const fr_t& a) {   // Montgomery -> integer in [0, p)
+    fr_t one = fr_zero();
+    one.v[0] = 1;
+    return fr_mul(a, one);
+}
+__device__ __forceinline__ fr_t fr_from_canonical(const fr_t& x) {  // integer < 2^256 -> Montgomery
+    return fr_mul(ZK_R2, x);
+}
+// a * small unsigned integer k (k < 2^32)
+__device__ __forceinline__ fr_t fr_mul_u32(const fr_t& a, uint32_t k) {
+    fr_t b = fr_zero();
+    b.v[0] = k;
+    return fr_mul(fr_mul(a, ZK_R2), b);
+}
+
+// ---------------------------------------------------------------- memory access
+__device__ __forceinline__ fr_t fr_load(const fr_t* p) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 x = __ldg(q), y = __ldg(q + 1);
+    return fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
+}
+__device__ __forceinline__ fr_t fr_load_cg(const fr_t* p) {   // streaming (not kept in L1)
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 x = __ldcs(q), y = __ldcs(q + 1);
+    return fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
+}
+__device__ __forceinline__ void fr_store(fr_t* p, const fr_t& a) {
+    uint4* q = reinterpret_cast<uint4*>(p);
+    q[0] = make_uint4(a.v[0], a.v[1], a.v[2], a.v[3]);
+    q[1] = make_uint4(a.v[4], a.v[5], a.v[6], a.v[7]);
+}
+__device__ __forceinline__ fr_t fr_shfl_down(const fr_t& a, int delta) {
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = __shfl_down_sync(0xffffffffu, a.v[i], delta);
+    return r;
+}
+__device__ __forceinline__ fr_t fr_shfl_xor(const fr_t& a, int mask) {
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = __shfl_xor_sync(0xffffffffu, a.v[i], mask);
+    return r;
+}
+
+// Fermat inverse a^(p-2) (single thread; used only for a handful of scalars)
+__device__ inline fr_t fr_inv(const fr_t& a) {
+    const uint32_t e[8] = {ZK_P0 - 2, ZK_P1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7};
+    fr_t r = fr_one();
+    for (int i = 7; i >= 0; i--)
+        for (int b = 31; b >= 0; b--) {
+            r = fr_sqr(r);
+            if ((e[i] >> b) & 1) r = fr_mul(r, a);
+        }
+    return r;
+}
+
+}  // namespace zk

@@ -1,0 +1,758 @@
+// relu.cu — zkReLU on the B200 (PAPER §3, App. A).
+//
+// Statement (D3b, D5, D10, D13): variables x = (j, i), j = bit position (logB bits, bound first),
+// i = entry (logD bits):
+//   sum_{i,j} [ r^2 E_Z(i) a0 s(j) + r E_A(i) (1-sig(i)) a0 s'(j) + E_b(i,j)(a0^2 - a0)
+//             + r'r^2 E_GA(i) a1 s(j) + r'r E_GZ(i) (1-sig(i)) a1 s'(j) + r' E_b(i,j)(a1^2 - a1) ]
+//   = r^2 Z~(u_Z) + r A~(u_A) + r'r^2 G_A~(u_GA) + r'r G_Z~(u_GZ)
+// with a0(i,j) = bit j of Z_i, a1(i,j) = bit j of G_A_i (two's complement, Q+R bits), sig = bit Q+R-1
+// of Z, E_x(i) = beta(u_x, i), E_b(i,j) = beta(u_bin, (j, i)).
+//
+// Prover algorithm ("bits first"; the transcript is the statement's unique one, D18):
+//  * j-rounds: every j-round polynomial is a function of four linear sums M_x[j] = sum_i c_x(i) bit_j
+//    and two 32x32 co-occurrence matrices C_s[j1][j2] = sum_i e_b(i) bit_j1 bit_j2 (L_s = diag C_s),
+//    because a0~(i, rho)^2 = sum_{j1,j2} beta(rho,j1) beta(rho,j2) bit_j1 bit_j2 and
+//    E_b(i, j) = beta(u_bin_j, j) beta(u_bin_i, i).  One pass over the int32 words computes them with
+//    masked lazy additions (no Fr multiplication per entry); the 5 rounds then run on 32-entry
+//    vectors and a 32x32 matrix in one CTA (bilinear fold for C).
+//  * i-rounds: after the j-rounds, a0(i) = sum_j beta(r_j, j) bit_j(Z_i) = sum of 4 byte-table lookups;
+//    the remaining logD rounds are a degree-3 sumcheck over a0, a1, 1-sig and five eq tables held as
+//    LO (low variables, pair-summed in the round kernel) x HI (<= 5 variables, rescaled by
+//    beta(u_t, r_t) in the finalizer), so no 2^logD eq table is ever written.
+#include "relu.cuh"
+#include "tables.cuh"
+
+namespace zk {
+
+// ---------------------------------------------------------------- row a7: tables
+__global__ void k_relu_tables(const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t Q, uint32_t R, uint8_t* sign,
+                              int32_t* A, int32_t* GZ, int32_t* Zp, int32_t* GAp, int32_t* RZ, int32_t* RGA,
+                              unsigned int* bad) {
+    const int64_t lim = 1ll << (Q + R - 1);
+    const int64_t half = 1ll << (R - 1);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t z = Z[i], g = GA[i];
+        if (z < -lim || z >= lim || g < -lim || g >= lim) atomicOr(bad, 1u);
+        int64_t zp = (z + half) >> R, gp = (g + half) >> R;   // half-up rounding (D9)
+        bool neg = z < 0;                                      // sign of Z gates both (D10)
+        sign[i] = neg;
+        A[i] = neg ? 0 : (int32_t)zp;
+        GZ[i] = neg ? 0 : (int32_t)gp;
+        if (Zp) Zp[i] = (int32_t)zp;
+        if (GAp) GAp[i] = (int32_t)gp;
+        if (RZ) RZ[i] = (int32_t)(z - (zp << R));
+        if (RGA) RGA[i] = (int32_t)(g - (gp << R));
+    }
+}
+
+bool relu_tables_dev(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t Q, uint32_t R, uint8_t* sign,
+                     int32_t* A, int32_t* GZ, int32_t* Zp, int32_t* GAp, int32_t* RZ, int32_t* RGA, Scratch& s) {
+    unsigned int* bad = s.alloc_zero<unsigned int>(1);
+    if (D) ZK_LAUNCH(ctx, k_relu_tables, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, Q, R, sign, A, GZ, Zp, GAp, RZ, RGA, bad);
+    unsigned int h = 0;
+    ZK_CUDA(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return h == 0;
+}
+
+__global__ void k_relu_range(const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t QR, unsigned int* bad) {
+    const int64_t lim = 1ll << (QR - 1);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t z = Z[i], g = GA[i];
+        if (z < -lim || z >= lim || g < -lim || g >= lim) atomicOr(bad, 1u);
+    }
+}
+
+// ---------------------------------------------------------------- bit sums for the j-rounds
+// A cell accumulates sum_i c_lot(i) [ (word_i & m1) == m1 ] [ !(gate && sig_i) ].
+struct BitCell {
+    uint32_t m1;
+    uint8_t word;   // 0: Z, 1: G_A
+    uint8_t gate;   // multiply by (1 - sig)
+    uint8_t lot;    // eq table: 0 Z, 1 A, 2 GA, 3 GZ, 4 b
+    uint8_t pad;
+};
+
+struct BitsumArgs {
+    const int32_t* Z;
+    const int32_t* GA;
+    uint32_t logD, lo_bits, qr_mask, sig_bit;
+    const fr_t* LO[5];   // eq over the low lo_bits variables, scaled by R (lazy accumulation)
+    const fr_t* HI[5];   // eq over the remaining variables
+    const BitCell* cells;
+    uint32_t ncell;
+    fr_t* partials;      // gridDim.x * ncell
+};
+
+constexpr int BS_CH = 128;   // entries staged per chunk
+
+__device__ __forceinline__ void masked_add10(uint32_t (&a)[10], const fr_t& v, uint32_t mm) {
+    asm("add.cc.u32  %0, %0, %10;\n\t"
+        "addc.cc.u32 %1, %1, %11;\n\t"
+        "addc.cc.u32 %2, %2, %12;\n\t"
+        "addc.cc.u32 %3, %3, %13;\n\t"
+        "addc.cc.u32 %4, %4, %14;\n\t"
+        "addc.cc.u32 %5, %5, %15;\n\t"
+        "addc.cc.u32 %6, %6, %16;\n\t"
+        "addc.cc.u32 %7, %7, %17;\n\t"
+        "addc.cc.u32 %8, %8, 0;\n\t"
+        "addc.u32    %9, %9, 0;"
+        : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+          "+r"(a[8]), "+r"(a[9])
+        : "r"(v.v[0] & mm), "r"(v.v[1] & mm), "r"(v.v[2] & mm), "r"(v.v[3] & mm), "r"(v.v[4] & mm),
+          "r"(v.v[5] & mm), "r"(v.v[6] & mm), "r"(v.v[7] & mm));
+}
+
+// Each thread owns cells tid and tid + blockDim.x.  Each block walks a contiguous range of chunks;
+// the lazy accumulators are closed (REDC, times HI[row]) whenever the row i >> lo_bits changes.
+__global__ void __launch_bounds__(640) k_relu_bitsums(BitsumArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    fr_t* sLO = reinterpret_cast<fr_t*>(smem_raw);                       // [5][BS_CH]
+    uint32_t* sW = reinterpret_cast<uint32_t*>(sLO + 5 * BS_CH);          // [2][BS_CH]
+    uint8_t* sSig = reinterpret_cast<uint8_t*>(sW + 2 * BS_CH);           // [BS_CH]
+    const uint64_t D = 1ull << a.logD;
+    const uint64_t CH = D < BS_CH ? D : BS_CH;
+    const uint64_t nchunks = D / CH;
+    const uint64_t c_begin = blockIdx.x * nchunks / gridDim.x, c_end = (blockIdx.x + 1) * nchunks / gridDim.x;
+    BitCell cell[2];
+    bool have[2];
+    for (int q = 0; q < 2; q++) {
+        uint32_t c = threadIdx.x + q * blockDim.x;
+        have[q] = c < a.ncell;
+        cell[q] = have[q] ? a.cells[c] : BitCell{0, 0, 0, 0, 0};
+    }
+    uint32_t acc[2][10];
+    fr_t tot[2] = {fr_zero(), fr_zero()};
+    for (int q = 0; q < 2; q++)
+        for (int k = 0; k < 10; k++) acc[q][k] = 0;
+    const uint64_t lo_mask = (1ull << a.lo_bits) - 1;
+    uint64_t row = c_begin * CH >> a.lo_bits;
+    for (uint64_t ch = c_begin; ch < c_end; ch++) {
+        const uint64_t i0 = ch * CH;
+        const uint64_t r_here = i0 >> a.lo_bits;
+        if (r_here != row) {
+            for (int q = 0; q < 2; q++)
+                if (have[q]) {
+                    tot[q] = fr_add(tot[q], fr_mul(fr_redc_wide(acc[q]), fr_load(&a.HI[cell[q].lot][row])));
+                    for (int k = 0; k < 10; k++) acc[q][k] = 0;
+                }
+            row = r_here;
+        }
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < 5 * CH; e += blockDim.x) {
+            uint32_t lot = e / CH, k = e % CH;
+            fr_store(&sLO[lot * BS_CH + k], fr_load(&a.LO[lot][(i0 + k) & lo_mask]));
+        }
+        for (uint32_t k = threadIdx.x; k < CH; k += blockDim.x) {
+            uint32_t z = (uint32_t)__ldg(a.Z + i0 + k), g = (uint32_t)__ldg(a.GA + i0 + k);
+            sW[k] = z & a.qr_mask;
+            sW[BS_CH + k] = g & a.qr_mask;
+            sSig[k] = (z >> a.sig_bit) & 1;
+        }
+        __syncthreads();
+        for (uint32_t k = 0; k < CH; k++) {
+            const uint32_t sg = sSig[k];
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                const uint32_t w = sW[cell[q].word * BS_CH + k];
+                const bool on = have[q] && ((w & cell[q].m1) == cell[q].m1) && !(cell[q].gate && sg);
+                const fr_t v = sLO[cell[q].lot * BS_CH + k];
+                masked_add10(acc[q], v, on ? 0xffffffffu : 0u);
+            }
+        }
+    }
+    if (c_begin < c_end)
+        for (int q = 0; q < 2; q++)
+            if (have[q]) tot[q] = fr_add(tot[q], fr_mul(fr_redc_wide(acc[q]), fr_load(&a.HI[cell[q].lot][row])));
+    for (int q = 0; q < 2; q++)
+        if (have[q]) fr_store(&a.partials[(uint64_t)blockIdx.x * a.ncell + threadIdx.x + q * blockDim.x], tot[q]);
+}
+
+__global__ void k_relu_bitsums_reduce(const fr_t* partials, uint32_t nblocks, uint32_t ncell, fr_t* out) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        fr_t s = fr_zero();
+        for (uint32_t b = 0; b < nblocks; b++) s = fr_add(s, fr_load(&partials[(uint64_t)b * ncell + c]));
+        fr_store(&out[c], s);
+    }
+}
+
+// ---------------------------------------------------------------- j-rounds (one CTA)
+struct JRoundArgs {
+    const fr_t* cells;     // cell totals: [0,B) MZ, [B,2B) MA, [2B,3B) MGA, [3B,4B) MGZ, then C0, C1 upper triangles
+    uint32_t B, logB, Q, R;
+    const fr_t* r;         // r, r'
+    const fr_t* ubin;      // u_bin (first logB entries: j variables)
+    uint8_t* st;
+    uint8_t* msg_out;      // logB rounds x 4 x 32 bytes
+    uint8_t* point_out;    // logB x 32 canonical
+    fr_t* rj_out;          // logB challenges (Montgomery)
+    fr_t* byte_tab;        // ceil(B/8) x 256 entries
+    fr_t* kappa;           // [0] kZ [1] kA [2] kGA [3] kGZ [4] kb [5] r' [6] claim after the j-phase
+};
+
+__device__ __forceinline__ int tri_index(int j1, int j2, int B) {   // j1 <= j2, row-major upper triangle
+    return j1 * B - j1 * (j1 - 1) / 2 + (j2 - j1);
+}
+
+__device__ fr_t small_pow2(int e) {   // Montgomery form of 2^e, 0 <= e < 64
+    fr_t b = fr_zero();
+    if (e < 32) b.v[0] = 1u << e; else b.v[1] = 1u << (e - 32);
+    return fr_mul(ZK_R2, b);
+}
+
+__global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
+    __shared__ fr_t S[32], SP[32], EB[32], LS[32], LSP[32], LQ[32];
+    __shared__ fr_t CQ[32][32];
+    __shared__ fr_t vals[64];
+    __shared__ fr_t msg[4];
+    __shared__ fr_t rt_sm;
+    __shared__ fr_t ej[32];
+    const int B = a.B, tid = threadIdx.x;
+    const int QR = a.Q + a.R;
+    const fr_t r = fr_load(&a.r[0]), rp = fr_load(&a.r[1]);
+    const fr_t r2 = fr_mul(r, r);
+    const fr_t* MZ = a.cells;
+    const fr_t* MA = a.cells + B;
+    const fr_t* MGA = a.cells + 2 * B;
+    const fr_t* MGZ = a.cells + 3 * B;
+    const fr_t* C0 = a.cells + 4 * B;
+    const fr_t* C1 = C0 + B * (B + 1) / 2;
+    // initial vectors
+    for (int j = tid; j < B; j += blockDim.x) {
+        // s_{Q+R} and s', zero-padded to B columns (D12)
+        fr_t s = fr_zero(), sp = fr_zero();
+        if (j < QR - 1) s = small_pow2(j);
+        else if (j == QR - 1) s = fr_neg(small_pow2(QR - 1));
+        if (j == (int)a.R - 1) sp = fr_one();
+        else if (j >= (int)a.R && j < QR - 1) sp = small_pow2(j - a.R);
+        else if (j == QR - 1) sp = fr_neg(small_pow2(a.Q - 1));
+        S[j] = s;
+        SP[j] = sp;
+        fr_t e = fr_one();
+        for (uint32_t t = 0; t < a.logB; t++) {
+            fr_t u = fr_load(&a.ubin[t]);
+            e = fr_mul(e, ((j >> t) & 1) ? u : fr_sub(fr_one(), u));
+        }
+        EB[j] = e;
+        LS[j] = fr_add(fr_mul(r2, fr_load(&MZ[j])), fr_mul(fr_mul(rp, r2), fr_load(&MGA[j])));
+        LSP[j] = fr_add(fr_mul(r, fr_load(&MA[j])), fr_mul(fr_mul(rp, r), fr_load(&MGZ[j])));
+    }
+    for (int e = tid; e < B * B; e += blockDim.x) {
+        int j1 = e / B, j2 = e % B;
+        int lo = j1 < j2 ? j1 : j2, hi = j1 < j2 ? j2 : j1;
+        int ti = tri_index(lo, hi, B);
+        fr_t c = fr_add(fr_load(&C0[ti]), fr_mul(rp, fr_load(&C1[ti])));
+        CQ[j1][j2] = c;
+        if (j1 == j2) LQ[j1] = c;   // L_s = diag(C_s) since bit^2 = bit
+    }
+    __syncthreads();
+    fr_t claim = fr_zero();
+    for (uint32_t t = 0; t < a.logB; t++) {
+        const int n = B >> t, np = n >> 1;
+        // evaluations: item (b, X)
+        if (tid < 4 * np) {
+            const int b = tid >> 2, X = tid & 3;
+            const fr_t x = fr_from_u32((uint32_t)X), omx = fr_sub(fr_one(), x);
+#define LIN(v) fr_add(v[2 * b], fr_mul(x, fr_sub(v[2 * b + 1], v[2 * b])))
+            fr_t sv = LIN(S), spv = LIN(SP), ebv = LIN(EB), lsv = LIN(LS), lspv = LIN(LSP), lqv = LIN(LQ);
+#undef LIN
+            // bilinear: sum_{x1,x2} l(x1) l(x2) CQ[2b+x1][2b+x2]
+            fr_t c00 = CQ[2 * b][2 * b], c01 = CQ[2 * b][2 * b + 1], c10 = CQ[2 * b + 1][2 * b], c11 = CQ[2 * b + 1][2 * b + 1];
+            fr_t cq = fr_add(fr_mul(fr_mul(omx, omx), c00),
+                             fr_add(fr_mul(fr_mul(omx, x), fr_add(c01, c10)), fr_mul(fr_mul(x, x), c11)));
+            fr_t v = fr_add(fr_add(fr_mul(sv, lsv), fr_mul(spv, lspv)), fr_mul(ebv, fr_sub(cq, lqv)));
+            vals[tid] = v;
+        }
+        __syncthreads();
+        if (tid < 4) {
+            fr_t sum = fr_zero();
+            for (int b = 0; b < np; b++) sum = fr_add(sum, vals[4 * b + tid]);
+            msg[tid] = sum;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            fr_t ev[4] = {msg[0], msg[1], msg[2], msg[3]};
+            tr_absorb_frs(a.st, "relu/msg", ev, 4, a.msg_out + 128ull * t);
+            fr_t rt = tr_challenge(a.st, "relu/x");
+            fr_to_bytes(rt, a.point_out + 32ull * t);
+            fr_store(&a.rj_out[t], rt);
+            rt_sm = rt;
+            if (t + 1 == a.logB) claim = interp_small(ev, 3, rt);
+        }
+        __syncthreads();
+        const fr_t rt = rt_sm;
+        // fold vectors
+        fr_t nv[6];
+        if (tid < np) {
+            const int b = tid;
+#define FOLD(v) fr_add(v[2 * b], fr_mul(rt, fr_sub(v[2 * b + 1], v[2 * b])))
+            nv[0] = FOLD(S); nv[1] = FOLD(SP); nv[2] = FOLD(EB); nv[3] = FOLD(LS); nv[4] = FOLD(LSP); nv[5] = FOLD(LQ);
+#undef FOLD
+        }
+        // fold CQ: columns then rows, staged through registers (n * np <= 512 = 2 per thread)
+        fr_t cv[2];
+        int cc = 0;
+        for (int e = tid; e < n * np; e += blockDim.x) {
+            int i = e / np, c = e % np;
+            cv[cc++] = fr_add(CQ[i][2 * c], fr_mul(rt, fr_sub(CQ[i][2 * c + 1], CQ[i][2 * c])));
+        }
+        __syncthreads();
+        cc = 0;
+        for (int e = tid; e < n * np; e += blockDim.x) CQ[e / np][e % np] = cv[cc++];
+        if (tid < np) {
+            S[tid] = nv[0]; SP[tid] = nv[1]; EB[tid] = nv[2]; LS[tid] = nv[3]; LSP[tid] = nv[4]; LQ[tid] = nv[5];
+        }
+        __syncthreads();
+        fr_t rv = fr_zero();
+        if (tid < np * np) {
+            int b = tid / np, c = tid % np;
+            rv = fr_add(CQ[2 * b][c], fr_mul(rt, fr_sub(CQ[2 * b + 1][c], CQ[2 * b][c])));
+        }
+        __syncthreads();
+        if (tid < np * np) CQ[tid / np][tid % np] = rv;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const fr_t s = S[0], sp = SP[0];
+        fr_store(&a.kappa[0], fr_mul(r2, s));
+        fr_store(&a.kappa[1], fr_mul(r, sp));
+        fr_store(&a.kappa[2], fr_mul(fr_mul(rp, r2), s));
+        fr_store(&a.kappa[3], fr_mul(fr_mul(rp, r), sp));
+        fr_store(&a.kappa[4], EB[0]);
+        fr_store(&a.kappa[5], rp);
+        fr_store(&a.kappa[6], claim);
+    }
+    // byte tables: T[b][v] = sum_{k<8} [bit k of v] beta(r_j, 8b + k)
+    for (int j = tid; j < B; j += blockDim.x) {
+        fr_t e = fr_one();
+        for (uint32_t t = 0; t < a.logB; t++) {
+            fr_t u = fr_load(&a.rj_out[t]);
+            e = fr_mul(e, ((j >> t) & 1) ? u : fr_sub(fr_one(), u));
+        }
+        ej[j] = e;
+    }
+    __syncthreads();
+    const int nb = (B + 7) / 8;
+    for (int e = tid; e < nb * 256; e += blockDim.x) {
+        int bb = e >> 8, v = e & 255;
+        fr_t acc = fr_zero();
+        for (int k = 0; k < 8; k++)
+            if (((v >> k) & 1) && 8 * bb + k < B) acc = fr_add(acc, ej[8 * bb + k]);
+        fr_store(&a.byte_tab[e], acc);
+    }
+}
+
+// ---------------------------------------------------------------- i-phase tables
+// a0(i) = sum_b T[b][byte_b(Z_i & mask)], a1 likewise from G_A, oms(i) = 1 - sig_i
+__global__ void k_relu_materialize(const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t qr_mask, uint32_t sig_bit,
+                                   uint32_t nbytes, const fr_t* T, fr_t* a0, fr_t* a1, fr_t* oms) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t z = (uint32_t)__ldg(Z + i), g = (uint32_t)__ldg(GA + i);
+        uint32_t zm = z & qr_mask, gm = g & qr_mask;
+        fr_t x = fr_zero(), y = fr_zero();
+        for (uint32_t b = 0; b < nbytes; b++) {
+            x = fr_add(x, fr_load(&T[b * 256 + ((zm >> (8 * b)) & 255)]));
+            y = fr_add(y, fr_load(&T[b * 256 + ((gm >> (8 * b)) & 255)]));
+        }
+        fr_store(&a0[i], x);
+        fr_store(&a1[i], y);
+        fr_store(&oms[i], ((z >> sig_bit) & 1) ? fr_zero() : fr_one());
+    }
+}
+
+struct IRoundArgs {
+    const fr_t* src[3];   // a0, a1, oms
+    fr_t* dst[3];
+    uint64_t n_pairs;
+    const fr_t* r_prev;
+    const fr_t* lo_cur[5];
+    fr_t* lo_next[5];
+    fr_t* hi[5];           // scaled HI' (rescaled in place by the finalizer)
+    uint32_t lo_cnt;       // LO variables of this round (>= 1), including the current one
+    uint32_t hb;
+    const fr_t* u[5];      // eq points over i (Montgomery)
+    uint32_t t;            // i-round index
+    const fr_t* kappa;     // [4] kb, [5] r'
+    fr_t* partials;
+    unsigned int* ticket;
+    uint8_t* st;
+    uint8_t* msg_out;
+    fr_t* r_out;
+    uint8_t* point_out;
+};
+
+template <bool FOLD>
+__global__ void __launch_bounds__(256) k_relu_iround(IRoundArgs a) {
+    fr_t acc[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
+    fr_t r;
+    if (FOLD) r = fr_load(a.r_prev);
+    const fr_t rp = fr_load(&a.kappa[5]);
+    const uint64_t lo_mask = (1ull << a.lo_cnt) - 1;
+    const uint64_t next_count = 1ull << (a.lo_cnt - 1);
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < a.n_pairs;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        fr_t v0[3], dv[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            fr_t x0, x1;
+            if (FOLD) {
+                const fr_t* s = a.src[k] + 4 * b;
+                fr_t y0 = fr_load_cg(s), y1 = fr_load_cg(s + 1), y2 = fr_load_cg(s + 2), y3 = fr_load_cg(s + 3);
+                x0 = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+                x1 = fr_add(y2, fr_mul(r, fr_sub(y3, y2)));
+                fr_store(a.dst[k] + 2 * b, x0);
+                fr_store(a.dst[k] + 2 * b + 1, x1);
+            } else {
+                x0 = fr_load_cg(a.src[k] + 2 * b);
+                x1 = fr_load_cg(a.src[k] + 2 * b + 1);
+            }
+            v0[k] = x0;
+            dv[k] = fr_sub(x1, x0);
+        }
+        const uint64_t l0 = (2 * b) & lo_mask;
+        const uint64_t h = b >> (a.lo_cnt - 1);
+        if (b < next_count)
+#pragma unroll
+            for (int x = 0; x < 5; x++)
+                fr_store(&a.lo_next[x][b], fr_add(fr_load(&a.lo_cur[x][2 * b]), fr_load(&a.lo_cur[x][2 * b + 1])));
+        // eq values at X = 0, 1 of the b-term (index 4) and per-side pairs
+        fr_t eb0, ebd;
+        {
+            fr_t hh = fr_load(&a.hi[4][h]);
+            fr_t e0 = fr_mul(fr_load(&a.lo_cur[4][l0]), hh), e1 = fr_mul(fr_load(&a.lo_cur[4][l0 + 1]), hh);
+            eb0 = e0;
+            ebd = fr_sub(e1, e0);
+        }
+        // side s = 0 (a0 with E_Z, E_A) and s = 1 (a1 with E_GA, E_GZ); AIVP weight 1 and r'
+        const fr_t a00 = v0[0], a0d = dv[0], a10 = v0[1], a1d = dv[1], om0 = v0[2], omd = dv[2];
+#pragma unroll 1
+        for (int sd = 0; sd < 2; sd++) {
+            const fr_t* hia = sd ? a.hi[2] : a.hi[0];
+            const fr_t* hic = sd ? a.hi[3] : a.hi[1];
+            const fr_t* loa = sd ? a.lo_cur[2] : a.lo_cur[0];
+            const fr_t* loc = sd ? a.lo_cur[3] : a.lo_cur[1];
+            fr_t ha = fr_load(&hia[h]), hb_ = fr_load(&hic[h]);
+            fr_t ea = fr_mul(fr_load(&loa[l0]), ha);
+            fr_t ead = fr_sub(fr_mul(fr_load(&loa[l0 + 1]), ha), ea);
+            fr_t ec = fr_mul(fr_load(&loc[l0]), hb_);
+            fr_t ecd = fr_sub(fr_mul(fr_load(&loc[l0 + 1]), hb_), ec);
+            fr_t av = sd ? a10 : a00, ad = sd ? a1d : a0d;
+            fr_t om = om0, eb = eb0;
+            const fr_t wq = sd ? rp : fr_one();
+#pragma unroll
+            for (int X = 0; X < 4; X++) {
+                // a * (E_a + E_c * oms) + E_b * (a^2 - a) * (sd ? r' : 1)
+                fr_t tq = fr_add(ea, fr_mul(ec, om));
+                fr_t q = fr_mul(av, fr_sub(av, fr_one()));
+                if (sd) q = fr_mul(q, wq);
+                fr_t p = fr_add(fr_mul(av, tq), fr_mul(eb, q));
+                acc[X] = fr_add(acc[X], p);
+                if (X < 3) {
+                    av = fr_add(av, ad);
+                    om = fr_add(om, omd);
+                    ea = fr_add(ea, ead);
+                    ec = fr_add(ec, ecd);
+                    eb = fr_add(eb, ebd);
+                }
+            }
+        }
+    }
+    __shared__ fr_t tot[4];
+    __shared__ fr_t eqr[5];
+    if (grid_reduce_fr_block<4>(acc, a.partials, a.ticket, tot)) {
+        if (threadIdx.x == 0) {
+            fr_t ev[4] = {tot[0], tot[1], tot[2], tot[3]};
+            tr_absorb_frs(a.st, "relu/msg", ev, 4, a.msg_out);
+            fr_t rt = tr_challenge(a.st, "relu/x");
+            fr_store(a.r_out, rt);
+            fr_to_bytes(rt, a.point_out);
+            for (int x = 0; x < 5; x++) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur
+                fr_t u = fr_load(&a.u[x][a.t]);
+                fr_t ur = fr_mul(u, rt);
+                eqr[x] = fr_add(fr_sub(fr_sub(fr_one(), u), rt), fr_add(ur, ur));
+            }
+        }
+        __syncthreads();
+        const uint32_t nh = 1u << a.hb;
+        for (uint32_t e = threadIdx.x; e < 5 * nh; e += blockDim.x) {
+            uint32_t x = e / nh, hh = e % nh;
+            fr_store(&a.hi[x][hh], fr_mul(fr_load(&a.hi[x][hh]), eqr[x]));
+        }
+    }
+}
+
+// Last hb i-rounds in one CTA with every table (a0, a1, oms, 5 eq) materialised in shared memory.
+struct ITailArgs {
+    const fr_t* src[3];
+    int fold;               // fold src (2 * n0 entries) by r_prev first
+    const fr_t* r_prev;
+    const fr_t* hi[5];      // E_x tables (n0 entries, already scaled)
+    uint32_t hb;            // rounds in the tail; n0 = 2^hb
+    const fr_t* kappa;
+    uint8_t* st;
+    uint8_t* msg_out;       // hb x 128 bytes
+    uint8_t* point_out;     // hb x 32
+    fr_t* r_out;
+    uint8_t* finals_out;    // 96 bytes
+};
+
+__global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
+    __shared__ fr_t T[8][32];
+    __shared__ fr_t vals[16][4];
+    __shared__ fr_t rt_sm;
+    const int tid = threadIdx.x;
+    const int n0 = 1 << a.hb;
+    const fr_t rp = fr_load(&a.kappa[5]);
+    for (int e = tid; e < 3 * n0; e += blockDim.x) {
+        int k = e / n0, i = e % n0;
+        fr_t v;
+        if (a.fold) {
+            fr_t r = fr_load(a.r_prev);
+            fr_t y0 = fr_load(&a.src[k][2 * i]), y1 = fr_load(&a.src[k][2 * i + 1]);
+            v = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+        } else {
+            v = fr_load(&a.src[k][i]);
+        }
+        T[k][i] = v;
+    }
+    for (int e = tid; e < 5 * n0; e += blockDim.x) T[3 + e / n0][e % n0] = fr_load(&a.hi[e / n0][e % n0]);
+    __syncthreads();
+    for (uint32_t t = 0; t < a.hb; t++) {
+        const int n = n0 >> t, np = n >> 1;
+        if (tid < 4 * np) {
+            const int b = tid >> 2, X = tid & 3;
+            const fr_t x = fr_from_u32((uint32_t)X);
+            fr_t v[8];
+            for (int k = 0; k < 8; k++) v[k] = fr_add(T[k][2 * b], fr_mul(x, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+            // tables: 0 a0, 1 a1, 2 oms, 3 EZ, 4 EA, 5 EGA, 6 EGZ, 7 Eb
+            fr_t t0 = fr_mul(v[0], fr_add(v[3], fr_mul(v[4], v[2])));
+            fr_t t1 = fr_mul(v[1], fr_add(v[5], fr_mul(v[6], v[2])));
+            fr_t q = fr_add(fr_mul(v[0], fr_sub(v[0], fr_one())), fr_mul(rp, fr_mul(v[1], fr_sub(v[1], fr_one()))));
+            vals[b][X] = fr_add(fr_add(t0, t1), fr_mul(v[7], q));
+        }
+        __syncthreads();
+        if (tid == 0) {
+            fr_t ev[4];
+            for (int X = 0; X < 4; X++) {
+                fr_t s = fr_zero();
+                for (int b = 0; b < np; b++) s = fr_add(s, vals[b][X]);
+                ev[X] = s;
+            }
+            tr_absorb_frs(a.st, "relu/msg", ev, 4, a.msg_out + 128ull * t);
+            fr_t rt = tr_challenge(a.st, "relu/x");
+            fr_store(&a.r_out[t], rt);
+            fr_to_bytes(rt, a.point_out + 32ull * t);
+            rt_sm = rt;
+        }
+        __syncthreads();
+        const fr_t rt = rt_sm;
+        fr_t nv[2];
+        int cnt = 0;
+        for (int e = tid; e < 8 * np; e += blockDim.x) {
+            int k = e / np, b = e % np;
+            nv[cnt++] = fr_add(T[k][2 * b], fr_mul(rt, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+        }
+        __syncthreads();
+        cnt = 0;
+        for (int e = tid; e < 8 * np; e += blockDim.x) T[e / np][e % np] = nv[cnt++];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        fr_t fin[3] = {T[0][0], T[1][0], fr_sub(fr_one(), T[2][0])};
+        tr_absorb_frs(a.st, "relu/final", fin, 3, a.finals_out);
+    }
+}
+
+// ---------------------------------------------------------------- driver
+void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,
+                    uint32_t R, ReluOutputs& out, unsigned int** range_bad, Scratch& s) {
+    const uint32_t QR = Q + R;
+    const uint32_t logB = relu_logB(Q, R), B = 1u << logB;
+    const uint64_t D = 1ull << logD;
+    const uint32_t qr_mask = QR >= 32 ? 0xffffffffu : ((1u << QR) - 1);
+    const uint32_t m = logB + logD;
+    uint8_t* proof = out.d_proof;
+    *range_bad = nullptr;
+    if (QR < 32) {
+        *range_bad = s.alloc_zero<unsigned int>(1);
+        ZK_LAUNCH(ctx, k_relu_range, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, QR, *range_bad);
+    }
+    // header
+    uint8_t hdr[12];
+    const uint32_t hv[3] = {logD, Q, R};
+    for (int i = 0; i < 3; i++)
+        for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
+    ZK_CUDA(cudaMemcpyAsync(proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
+    tr_absorb_host(tr, "relu/hdr", hdr, 12);
+    // points u_Z, u_A, u_GA, u_GZ
+    fr_t* U = s.alloc<fr_t>(4ull * logD);
+    tr_challenges_dev(tr, "relu/uZ", logD, U, nullptr);
+    tr_challenges_dev(tr, "relu/uA", logD, U + logD, nullptr);
+    tr_challenges_dev(tr, "relu/uGA", logD, U + 2 * logD, nullptr);
+    tr_challenges_dev(tr, "relu/uGZ", logD, U + 3 * logD, nullptr);
+    // claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) with A, G_Z formed on the fly (Lemma 1)
+    fr_t* claims = s.alloc<fr_t>(4);
+    mle_i32_plain(ctx, Z, logD, U, claims, s);
+    mle_i32_relu(ctx, 0, Z, GA, R, logD, U + logD, claims + 1, s);
+    mle_i32_plain(ctx, GA, logD, U + 2 * logD, claims + 2, s);
+    mle_i32_relu(ctx, 1, Z, GA, R, logD, U + 3 * logD, claims + 3, s);
+    ZK_LAUNCH(ctx, k_tr_absorb_frs, 1, 1, 0, tr->d_st, make_tag("relu/claims"), (const fr_t*)claims, 4u, proof + 12);
+    // r, r', u_bin
+    fr_t* rr = s.alloc<fr_t>(2);
+    fr_t* ubin = s.alloc<fr_t>(m);
+    tr_challenges_dev(tr, "relu/r", 1, rr, nullptr);
+    tr_challenges_dev(tr, "relu/rp", 1, rr + 1, nullptr);
+    tr_challenges_dev(tr, "relu/ubin", m, ubin, nullptr);
+    const fr_t* u_i[5] = {U, U + logD, U + 2 * logD, U + 3 * logD, ubin + logB};
+
+    // ---- bit sums
+    std::vector<BitCell> cells;
+    for (int x = 0; x < 4; x++)
+        for (uint32_t j = 0; j < B; j++) {
+            BitCell c{(j < QR) ? (1u << j) : 0u, (uint8_t)(x >= 2), (uint8_t)(x == 1 || x == 3), (uint8_t)x, 0};
+            if (j >= QR) c.m1 = 0xffffffffu;   // never matches a masked word: padding columns are zero
+            cells.push_back(c);
+        }
+    for (int sd = 0; sd < 2; sd++)
+        for (uint32_t j1 = 0; j1 < B; j1++)
+            for (uint32_t j2 = j1; j2 < B; j2++) {
+                BitCell c{(j1 < QR && j2 < QR) ? ((1u << j1) | (1u << j2)) : 0xffffffffu, (uint8_t)sd, 0, 4, 0};
+                cells.push_back(c);
+            }
+    // (with Q+R = 32 there are no padding columns, so the never-matching mask 0xffffffff is not used)
+    const uint32_t ncell = (uint32_t)cells.size();
+    BitCell* d_cells = s.alloc<BitCell>(ncell);
+    ZK_CUDA(cudaMemcpyAsync(d_cells, cells.data(), sizeof(BitCell) * ncell, cudaMemcpyHostToDevice, ctx->stream));
+    const uint32_t lo_bits = logD < 12 ? logD : 12, hi_bits = logD - lo_bits;
+    BitsumArgs ba;
+    memset(&ba, 0, sizeof ba);
+    ba.Z = Z;
+    ba.GA = GA;
+    ba.logD = logD;
+    ba.lo_bits = lo_bits;
+    ba.qr_mask = qr_mask;
+    ba.sig_bit = QR - 1;
+    for (int x = 0; x < 5; x++) {
+        fr_t* lo = s.alloc<fr_t>(1ull << lo_bits);
+        fr_t* hi = s.alloc<fr_t>(1ull << hi_bits);
+        eq_table_r2_dev(ctx, u_i[x], lo_bits, lo, s);
+        eq_table_dev(ctx, u_i[x] + lo_bits, hi_bits, nullptr, hi, s);
+        ba.LO[x] = lo;
+        ba.HI[x] = hi;
+    }
+    ba.cells = d_cells;
+    ba.ncell = ncell;
+    uint32_t bs_threads = ((ncell + 1) / 2 + 31) / 32 * 32;
+    if (bs_threads > 640) bs_threads = 640;
+    uint64_t nchunks = D / (D < BS_CH ? D : BS_CH);
+    uint32_t bs_grid = (uint32_t)(nchunks < (uint64_t)ctx->num_sms * 2 ? nchunks : (uint64_t)ctx->num_sms * 2);
+    ba.partials = s.alloc<fr_t>((size_t)bs_grid * ncell);
+    size_t bs_smem = 5 * BS_CH * sizeof(fr_t) + 2 * BS_CH * 4 + BS_CH;
+    ZK_CUDA(cudaFuncSetAttribute(k_relu_bitsums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
+    ZK_REQUIRE(ncell <= 2 * bs_threads, ZK_ERR_INTERNAL, "bitsum cells exceed the block");
+    ZK_LAUNCH(ctx, k_relu_bitsums, bs_grid, bs_threads, bs_smem, ba);
+    fr_t* cell_tot = s.alloc<fr_t>(ncell);
+    ZK_LAUNCH(ctx, k_relu_bitsums_reduce, (ncell + 127) / 128, 128, 0, (const fr_t*)ba.partials, bs_grid, ncell, cell_tot);
+
+    // ---- j-rounds
+    const uint32_t nbytes = (B + 7) / 8;
+    fr_t* byte_tab = s.alloc<fr_t>(256ull * nbytes);
+    fr_t* kappa = s.alloc<fr_t>(8);
+    fr_t* r_all = s.alloc<fr_t>(m);
+    JRoundArgs ja;
+    ja.cells = cell_tot;
+    ja.B = B;
+    ja.logB = logB;
+    ja.Q = Q;
+    ja.R = R;
+    ja.r = rr;
+    ja.ubin = ubin;
+    ja.st = tr->d_st;
+    ja.msg_out = proof + 140;
+    ja.point_out = out.d_point;
+    ja.rj_out = r_all;
+    ja.byte_tab = byte_tab;
+    ja.kappa = kappa;
+    ZK_LAUNCH(ctx, k_relu_jrounds, 1, 256, 0, ja);
+
+    // ---- i-phase tables
+    fr_t* full[3];
+    for (int k = 0; k < 3; k++) full[k] = s.alloc<fr_t>(D);
+    ZK_LAUNCH(ctx, k_relu_materialize, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, qr_mask, QR - 1, nbytes,
+              (const fr_t*)byte_tab, full[0], full[1], full[2]);
+    const uint32_t hb = logD < 5 ? logD : 5;
+    const uint32_t H = logD - hb;
+    fr_t* HIs[5];
+    fr_t* LOs[5][2];
+    for (int x = 0; x < 5; x++) {
+        HIs[x] = s.alloc<fr_t>(1ull << hb);
+        eq_table_dev(ctx, u_i[x] + H, hb, kappa + (x < 4 ? x : 4), HIs[x], s);
+        LOs[x][0] = LOs[x][1] = nullptr;
+        if (H) {
+            LOs[x][0] = s.alloc<fr_t>(1ull << H);
+            LOs[x][1] = s.alloc<fr_t>(1ull << (H - 1));
+            eq_table_dev(ctx, u_i[x], H, nullptr, LOs[x][0], s);
+        }
+    }
+    fr_t* buf[2][3];
+    for (int k = 0; k < 3; k++) {
+        buf[1][k] = s.alloc<fr_t>(D >> 1);
+        buf[0][k] = s.alloc<fr_t>(D >= 4 ? D >> 2 : 1);
+    }
+    unsigned int max_grid = (unsigned int)ctx->num_sms * 4;
+    fr_t* partials = s.alloc<fr_t>((size_t)max_grid * 4);
+    unsigned int* ticket = s.alloc_zero<unsigned int>(1);
+    const fr_t* cur[3] = {full[0], full[1], full[2]};
+    int lo_level = 0;
+    for (uint32_t t = 0; t < H; t++) {
+        IRoundArgs a;
+        memset(&a, 0, sizeof a);
+        const bool fold = t > 0;
+        for (int k = 0; k < 3; k++) {
+            a.src[k] = cur[k];
+            a.dst[k] = fold ? buf[t & 1][k] : nullptr;
+        }
+        a.n_pairs = D >> (t + 1);
+        a.r_prev = fold ? r_all + logB + t - 1 : nullptr;
+        for (int x = 0; x < 5; x++) {
+            a.lo_cur[x] = LOs[x][lo_level];
+            a.lo_next[x] = LOs[x][lo_level ^ 1];
+            a.hi[x] = HIs[x];
+            a.u[x] = u_i[x];
+        }
+        a.lo_cnt = H - t;
+        a.hb = hb;
+        a.t = t;
+        a.kappa = kappa;
+        a.partials = partials;
+        a.ticket = ticket;
+        a.st = tr->d_st;
+        a.msg_out = proof + 140 + 128ull * (logB + t);
+        a.r_out = r_all + logB + t;
+        a.point_out = out.d_point + 32ull * (logB + t);
+        unsigned int grid = grid_for(ctx, a.n_pairs, 256, 4);
+        if (fold)
+            ZK_LAUNCH(ctx, k_relu_iround<true>, grid, 256, 0, a);
+        else
+            ZK_LAUNCH(ctx, k_relu_iround<false>, grid, 256, 0, a);
+        lo_level ^= 1;
+        if (fold)
+            for (int k = 0; k < 3; k++) cur[k] = buf[t & 1][k];
+    }
+    ITailArgs ta;
+    memset(&ta, 0, sizeof ta);
+    for (int k = 0; k < 3; k++) ta.src[k] = cur[k];
+    ta.fold = H > 0;
+    ta.r_prev = H > 0 ? r_all + logB + H - 1 : nullptr;
+    for (int x = 0; x < 5; x++) ta.hi[x] = HIs[x];
+    ta.hb = hb;
+    ta.kappa = kappa;
+    ta.st = tr->d_st;
+    ta.msg_out = proof + 140 + 128ull * (logB + H);
+    ta.point_out = out.d_point + 32ull * (logB + H);
+    ta.r_out = r_all + logB + H;
+    ta.finals_out = proof + 140 + 128ull * m;
+    ZK_LAUNCH(ctx, k_relu_itail, 1, 256, 0, ta);
+}
+
+}  // namespace zk

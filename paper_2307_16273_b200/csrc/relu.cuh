@@ -1,0 +1,26 @@
+// relu.cuh — zkReLU tables and aggregated six-statement sumcheck (rows a7, a8).
+#pragma once
+#include "common.cuh"
+
+namespace zk {
+
+struct ReluOutputs {
+    uint8_t* d_proof;   // relu_proof_len bytes
+    uint8_t* d_point;   // (logB + logD) canonical challenges
+};
+
+inline uint32_t relu_logB(uint32_t Q, uint32_t R) {
+    uint32_t qr = Q + R, l = 0;
+    while ((1u << l) < qr) l++;
+    return l;
+}
+inline uint64_t relu_proof_len(uint32_t logD, uint32_t logB) { return 12 + 128 + 128ull * (logB + logD) + 96; }
+
+bool relu_tables_dev(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t Q, uint32_t R, uint8_t* sign,
+                     int32_t* A, int32_t* GZ, int32_t* Zp, int32_t* GAp, int32_t* RZ, int32_t* RGA, Scratch& s);
+
+// Enqueues the whole proof; *range_bad (device flag, may be null when Q+R = 32) is set if an input is out of range.
+void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,
+                    uint32_t R, ReluOutputs& out, unsigned int** range_bad, Scratch& s);
+
+}  // namespace zk

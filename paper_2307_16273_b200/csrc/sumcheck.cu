@@ -1,0 +1,256 @@
+// sumcheck.cu — aggregated product sumcheck (Protocol 3 P:L504-527).
+//
+// Statement: claim = sum_{x in {0,1}^m} beta(w, x_{<n_eq}) prod_{k<K} T_k(x), variables bound LSB first (D2).
+// Round t, pair b = (T[2b], T[2b+1]) of the current tables; message = evaluations at X = 0..K of
+//   f_t(X) = sum_b beta(w_{t+1..n_eq-1}, b) prod_k (T_k[2b] + X (T_k[2b+1] - T_k[2b]))     (t < n_eq, D4)
+//   g_t(X) = sum_b prod_k (...)                                                            (t >= n_eq)
+// One kernel per round fuses: the fold of every table by r_{t-1} (row a5: reads 4 elements per pair,
+// writes the 2 folded ones to a ping-pong buffer), the suffix-eq weight of the pair, the K+1
+// evaluations, a warp-shuffle + block-tree + last-block grid reduction, and the Fiat-Shamir step on
+// the device (absorb the message, squeeze r_t) — no host synchronisation inside a sumcheck.
+//
+// Suffix eq weights without materialising 2^n_eq entries: E_t(b) = LO_t[b mod 2^l] * HI[(b >> l) mod 2^h]
+// with HI = beta(w_{n_eq-h..n_eq-1}, .) (h <= 10) fixed and LO_t = beta(w_{t+1..n_eq-h-1}, .).  Because
+// beta(w_s, 0) + beta(w_s, 1) = 1, LO_{t+1}[c] = LO_t[2c] + LO_t[2c+1]: the round kernel writes the next
+// LO level with additions only.  Once LO is exhausted the HI table is pair-summed the same way.
+#include "sumcheck.cuh"
+#include "tables.cuh"
+
+namespace zk {
+
+struct ScRoundArgs {
+    const fr_t* src[3];
+    fr_t* dst[3];
+    uint64_t n_pairs;
+    const fr_t* r_prev;      // r_{t-1} (Montgomery) when folding
+    // eq weights: mode 0 none, 1 split (cur = LO level, hi = HI), 2 single table (cur)
+    int eq_mode;
+    const fr_t* eq_cur;
+    const fr_t* eq_hi;
+    fr_t* eq_next;
+    uint32_t lo_cnt;         // number of variables in the current LO (mode 1) or current table (mode 2)
+    uint32_t hb;             // variables in HI (mode 1)
+    // reduction + finalize
+    fr_t* partials;
+    unsigned int* ticket;
+    uint8_t* st;
+    uint32_t t, n_eq;
+    const fr_t* w;           // device w (Montgomery), for the claim of round 0
+    fr_t* claim;             // device claim (Montgomery)
+    int compute_claim;       // round 0 only: derive the claim from the message and absorb it
+    uint8_t* claim_bytes;    // canonical claim in the proof
+    uint8_t* msg_out;        // canonical message bytes in the proof
+    fr_t* r_out;             // r_t (Montgomery)
+    uint8_t* point_out;      // r_t canonical
+};
+
+template <int K, bool FOLD>
+__global__ void __launch_bounds__(256) k_sc_round(ScRoundArgs a) {
+    fr_t acc[K + 1];
+#pragma unroll
+    for (int x = 0; x <= K; x++) acc[x] = fr_zero();
+    fr_t r;
+    if (FOLD) r = fr_load(a.r_prev);
+    const uint64_t lo_mask = (1ull << a.lo_cnt) - 1, hi_mask = (1ull << a.hb) - 1;
+    const uint64_t next_count = a.lo_cnt ? (1ull << (a.lo_cnt - 1)) : 0;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < a.n_pairs;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        fr_t lo[K], d[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            fr_t v0, v1;
+            if (FOLD) {
+                const fr_t* s = a.src[k] + 4 * b;
+                fr_t x0 = fr_load_cg(s), x1 = fr_load_cg(s + 1), x2 = fr_load_cg(s + 2), x3 = fr_load_cg(s + 3);
+                v0 = fr_add(x0, fr_mul(r, fr_sub(x1, x0)));
+                v1 = fr_add(x2, fr_mul(r, fr_sub(x3, x2)));
+                fr_store(a.dst[k] + 2 * b, v0);
+                fr_store(a.dst[k] + 2 * b + 1, v1);
+            } else {
+                v0 = fr_load_cg(a.src[k] + 2 * b);
+                v1 = fr_load_cg(a.src[k] + 2 * b + 1);
+            }
+            lo[k] = v0;
+            d[k] = fr_sub(v1, v0);
+        }
+        // suffix eq weight of this pair
+        fr_t e;
+        bool has_e = a.eq_mode != 0;
+        if (a.eq_mode == 1) {
+            e = fr_mul(fr_load(&a.eq_cur[b & lo_mask]), fr_load(&a.eq_hi[(b >> a.lo_cnt) & hi_mask]));
+        } else if (a.eq_mode == 2) {
+            e = fr_load(&a.eq_cur[b & lo_mask]);
+        }
+        if (a.eq_mode && b < next_count)
+            fr_store(&a.eq_next[b], fr_add(fr_load(&a.eq_cur[2 * b]), fr_load(&a.eq_cur[2 * b + 1])));
+        // evaluations at X = 0..K: v_k(X) = lo_k + X d_k
+        fr_t v[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) v[k] = lo[k];
+#pragma unroll
+        for (int x = 0; x <= K; x++) {
+            fr_t p = v[0];
+#pragma unroll
+            for (int k = 1; k < K; k++) p = fr_mul(p, v[k]);
+            if (has_e) p = fr_mul(p, e);
+            acc[x] = fr_add(acc[x], p);
+            if (x < K)
+#pragma unroll
+                for (int k = 0; k < K; k++) v[k] = fr_add(v[k], d[k]);
+        }
+    }
+    fr_t tot[K + 1];
+    if (grid_reduce_fr<K + 1>(acc, a.partials, a.ticket, tot)) {
+        if (a.compute_claim) {
+            fr_t c;
+            if (a.t < a.n_eq) {
+                fr_t w0 = fr_load(&a.w[a.t]);
+                c = fr_add(fr_mul(fr_sub(fr_one(), w0), tot[0]), fr_mul(w0, tot[1]));
+            } else {
+                c = fr_add(tot[0], tot[1]);
+            }
+            fr_store(a.claim, c);
+            tr_absorb_frs(a.st, "sc/claim", &c, 1, a.claim_bytes);
+        }
+        tr_absorb_frs(a.st, "sc/msg", tot, K + 1, a.msg_out);
+        fr_t rt = tr_challenge(a.st, "sc/r");
+        fr_store(a.r_out, rt);
+        fr_to_bytes(rt, a.point_out);
+    }
+}
+
+// header (+ provided claim) before round 0
+__global__ void k_sc_header(uint8_t* st, Bytes256 hdr, const fr_t* claim, int absorb_claim, uint8_t* claim_bytes) {
+    tr_absorb(st, "sc/hdr", hdr.b, hdr.len);
+    if (absorb_claim) {
+        fr_t c = fr_load(claim);
+        tr_absorb_frs(st, "sc/claim", &c, 1, claim_bytes);
+    }
+}
+
+// finals T_k~(r) = T_k[0] + r_{m-1} (T_k[1] - T_k[0]) on the last 2-element tables
+__global__ void k_sc_finals(const fr_t* t0, const fr_t* t1, const fr_t* t2, int K, const fr_t* r_last, uint8_t* st,
+                            uint8_t* finals_bytes, fr_t* finals_mont) {
+    const fr_t* T[3] = {t0, t1, t2};
+    fr_t r = fr_load(r_last), f[3];
+    for (int k = 0; k < K; k++) {
+        fr_t a = fr_load(T[k]), b = fr_load(T[k] + 1);
+        f[k] = fr_add(a, fr_mul(r, fr_sub(b, a)));
+        if (finals_mont) fr_store(&finals_mont[k], f[k]);
+    }
+    tr_absorb_frs(st, "sc/final", f, K, finals_bytes);
+}
+
+template <int K>
+static void launch_round(zk_ctx* ctx, bool fold, unsigned int grid, const ScRoundArgs& a) {
+    if (fold)
+        ZK_LAUNCH(ctx, (k_sc_round<K, true>), grid, 256, 0, a);
+    else
+        ZK_LAUNCH(ctx, (k_sc_round<K, false>), grid, 256, 0, a);
+}
+
+void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
+    const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
+    ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
+    const uint64_t N = 1ull << m;
+    uint8_t* proof = S.d_proof;
+    // header bytes
+    uint8_t hdr[12];
+    const uint32_t hv[3] = {m, n_eq, K};
+    for (int i = 0; i < 3; i++)
+        for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
+    ZK_CUDA(cudaMemcpyAsync(proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
+    ZK_LAUNCH(ctx, k_sc_header, 1, 1, 0, tr->d_st, make_bytes(hdr, 12), S.d_claim, S.claim_given ? 1 : 0, proof + 12);
+
+    // eq split (only the suffix variables w_{t+1..n_eq-1} are ever needed)
+    const uint32_t hb = n_eq >= 1 ? (n_eq - 1 < 10 ? n_eq - 1 : 10) : 0;
+    const uint32_t lo0 = n_eq >= 1 ? n_eq - 1 - hb : 0;    // variables w_1 .. w_{lo0}
+    fr_t *HI = nullptr, *LO[2] = {nullptr, nullptr}, *HP[2] = {nullptr, nullptr};
+    if (n_eq >= 2) {
+        HI = s.alloc<fr_t>(1ull << hb);
+        eq_table_dev(ctx, S.d_w + 1 + lo0, hb, nullptr, HI, s);
+        if (lo0) {
+            LO[0] = s.alloc<fr_t>(1ull << lo0);
+            LO[1] = s.alloc<fr_t>(lo0 >= 1 ? (1ull << (lo0 - 1)) : 1);
+            eq_table_dev(ctx, S.d_w + 1, lo0, nullptr, LO[0], s);
+        }
+        HP[0] = s.alloc<fr_t>(1ull << hb);
+        HP[1] = s.alloc<fr_t>(1ull << hb);
+    }
+    // ping-pong fold buffers: round t (t >= 1) writes 2^{m-t} elements into buf[t & 1]
+    fr_t* buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    for (uint32_t k = 0; k < K; k++) {
+        if (m >= 1) buf[1][k] = s.alloc<fr_t>(N >> 1);
+        if (m >= 2) buf[0][k] = s.alloc<fr_t>(N >> 2);
+    }
+    unsigned int max_grid = (unsigned int)ctx->num_sms * 4;
+    fr_t* partials = s.alloc<fr_t>((size_t)max_grid * (K + 1));
+    unsigned int* ticket = s.alloc_zero<unsigned int>(1);
+
+    const fr_t* cur[3] = {S.tables[0], K > 1 ? S.tables[1] : nullptr, K > 2 ? S.tables[2] : nullptr};
+    int lo_level = 0;            // which LO buffer holds the current level
+    const fr_t* hi_cur = HI;     // current HI level once LO is exhausted
+    int hp_next = 0;
+    for (uint32_t t = 0; t < m; t++) {
+        ScRoundArgs a;
+        memset(&a, 0, sizeof a);
+        const bool fold = t > 0;
+        const uint64_t n_pairs = N >> (t + 1);
+        for (uint32_t k = 0; k < K; k++) {
+            a.src[k] = cur[k];
+            a.dst[k] = fold ? buf[t & 1][k] : nullptr;
+        }
+        a.n_pairs = n_pairs;
+        a.r_prev = fold ? S.d_r + (t - 1) : nullptr;
+        // eq mode for this round
+        if (t < n_eq && n_eq - t - 1 >= 1) {
+            uint32_t nv = n_eq - t - 1;              // suffix variables
+            uint32_t lo_cnt = nv > hb ? nv - hb : 0;
+            if (lo_cnt >= 1) {
+                a.eq_mode = 1;
+                a.eq_cur = LO[lo_level];
+                a.eq_hi = HI;
+                a.eq_next = LO[lo_level ^ 1];
+                a.lo_cnt = lo_cnt;
+                a.hb = hb;
+            } else {
+                a.eq_mode = 2;
+                a.eq_cur = hi_cur;
+                a.eq_next = HP[hp_next];
+                a.lo_cnt = nv;
+            }
+        }
+        a.partials = partials;
+        a.ticket = ticket;
+        a.st = tr->d_st;
+        a.t = t;
+        a.n_eq = n_eq;
+        a.w = S.d_w;
+        a.claim = S.d_claim;
+        a.compute_claim = (t == 0 && !S.claim_given) ? 1 : 0;
+        a.claim_bytes = proof + 12;
+        a.msg_out = proof + 44 + 32ull * t * (K + 1);
+        a.r_out = S.d_r + t;
+        a.point_out = S.d_point + 32ull * t;
+        unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
+        if (K == 1) launch_round<1>(ctx, fold, grid, a);
+        else if (K == 2) launch_round<2>(ctx, fold, grid, a);
+        else launch_round<3>(ctx, fold, grid, a);
+        // advance eq levels
+        if (a.eq_mode == 1) {
+            lo_level ^= 1;
+            // LO exhausted after this round?  then the next round uses HI directly (pair-summed later)
+        } else if (a.eq_mode == 2) {
+            hi_cur = HP[hp_next];
+            hp_next ^= 1;
+        }
+        if (fold)
+            for (uint32_t k = 0; k < K; k++) cur[k] = buf[t & 1][k];
+    }
+    ZK_LAUNCH(ctx, k_sc_finals, 1, 1, 0, cur[0], K > 1 ? cur[1] : cur[0], K > 2 ? cur[2] : cur[0], (int)K,
+              S.d_r + (m - 1), tr->d_st, proof + 44 + 32ull * m * (K + 1), S.d_finals);
+}
+
+uint64_t sumcheck_proof_len(uint32_t m, uint32_t K) { return 12 + 32 + 32ull * m * (K + 1) + 32ull * K; }
+
+}  // namespace zk

@@ -1,0 +1,276 @@
+"""GPU parity: every CUDA entry point against the CPU oracle on the same seeded inputs.
+
+Bit-exact (D18): transcripts, messages, claims, points and finals must be
+identical integers.  Sizes span several tiles/blocks and ragged grid tails;
+full-size configurations are checked by the oracle verifier (round identities,
+final identities, finals against brute-force MLE of the inputs).
+"""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from synth.prng import fs_seed, uniform_range
+
+pytestmark = pytest.mark.gpu
+P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2307_16273_b200 import build
+    build.build(verbose=False)
+    from paper_2307_16273_b200 import api
+    return api.Context(0)
+
+
+@pytest.fixture(scope="module")
+def O():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ---------------------------------------------------------------- Fr arithmetic
+def test_fr_ops_vs_python_ints(ctx):
+    from paper_2307_16273_b200 import api
+    rng = random.Random(1)
+    edges = [0, 1, 2, P - 1, P - 2, (1 << 256) % P, (1 << 255) % P, (1 << 32) - 1, 1 << 32, (1 << 64) - 1,
+             P >> 1, (P >> 1) + 1]
+    a = edges + [rng.randrange(P) for _ in range(4000)]
+    b = [rng.choice(edges) for _ in edges] + [rng.randrange(P) for _ in range(4000)]
+    b = b[:len(a)]
+    ta, tb = api.fr_table_from_ints(ctx, a), api.fr_table_from_ints(ctx, b)
+    assert api.fr_table_to_ints(ctx, ta) == a
+    for op, f in [("add", lambda x, y: (x + y) % P), ("sub", lambda x, y: (x - y) % P),
+                  ("mul", lambda x, y: x * y % P)]:
+        got = api.fr_table_to_ints(ctx, api.diag_fr_op(ctx, op, ta, tb))
+        assert got == [f(x, y) for x, y in zip(a, b)], op
+    got = api.fr_table_to_ints(ctx, api.diag_fr_op(ctx, "sqr", ta))
+    assert got == [x * x % P for x in a]
+    got = api.fr_table_to_ints(ctx, api.diag_fr_op(ctx, "neg", ta))
+    assert got == [(-x) % P for x in a]
+    small = api.fr_table_from_ints(ctx, a[1:200])
+    got = api.fr_table_to_ints(ctx, api.diag_fr_op(ctx, "inv", small))
+    assert got == [pow(x, P - 2, P) for x in a[1:200]]
+
+
+def test_noncanonical_rejected(ctx):
+    from paper_2307_16273_b200 import api
+    from paper_2307_16273_b200._lib import ZkError
+    raw = torch.frombuffer(bytearray(P.to_bytes(32, "little")), dtype=torch.uint8).reshape(1, 32).cuda()
+    with pytest.raises(ZkError):
+        api.fr_table_from_canonical(ctx, raw)
+    with pytest.raises(ZkError):
+        api.eq_table(ctx, [P])
+
+
+# ---------------------------------------------------------------- transcript (D3)
+def test_transcript_vs_oracle(ctx, O):
+    from paper_2307_16273_b200 import api
+    seed = fs_seed("gpu-transcript")
+    g, o = api.Transcript(ctx, seed), O.Transcript(seed)
+    rng = random.Random(2)
+    for step in range(40):
+        if step % 3 == 0:
+            msg = bytes(rng.randrange(256) for _ in range(rng.choice([0, 1, 12, 55, 56, 64, 119, 300, 1000])))
+            g.absorb("t/abs", msg)
+            o.absorb("t/abs", msg)
+        else:
+            n = rng.choice([1, 2, 5, 33, 300])
+            assert g.challenges("t/ch", n) == o.challenges("t/ch", n)
+    assert g.state() == o.state()
+
+
+# ---------------------------------------------------------------- tables (rows a1, a2)
+def test_embed(ctx):
+    from paper_2307_16273_b200 import api
+    v = uniform_range(3, 3, (5000,), -(1 << 31), 1 << 31)
+    v[:4] = [0, -1, (1 << 31) - 1, -(1 << 31)]
+    got = api.fr_table_to_ints(ctx, api.embed_i32(ctx, dev(v)))
+    assert got == [int(x) % P for x in v]
+
+
+@pytest.mark.parametrize("k", [0, 1, 3, 10, 11, 14])
+def test_eq_table(ctx, O, k):
+    from paper_2307_16273_b200 import api
+    rng = random.Random(k)
+    u = [rng.randrange(P) for _ in range(k)]
+    assert api.fr_table_to_ints(ctx, api.eq_table(ctx, u)) == O.eq_table(u)
+    s = rng.randrange(P)
+    assert api.fr_table_to_ints(ctx, api.eq_table(ctx, u, scale=s)) == [x * s % P for x in O.eq_table(u)]
+
+
+@pytest.mark.parametrize("m", [1, 5, 12, 13, 17])
+def test_mle(ctx, O, m):
+    from paper_2307_16273_b200 import api
+    rng = random.Random(m)
+    u = [rng.randrange(P) for _ in range(m)]
+    t = uniform_range(4, m, (1 << m,), -(1 << 31), 1 << 31)
+    assert api.mle_eval_i32(ctx, dev(t), u) == O.mle_i32(t, u)
+    tf = api.embed_i32(ctx, dev(t))
+    assert api.mle_eval_fr(ctx, tf, u) == O.mle_i32(t, u)
+
+
+# ---------------------------------------------------------------- product sumcheck (rows a4-a6)
+SC_CASES = [(1, 0, 1), (1, 1, 2), (2, 2, 3), (3, 0, 2), (6, 6, 2), (8, 3, 3), (10, 10, 1), (11, 11, 2),
+            (12, 12, 2), (13, 12, 2), (14, 14, 3), (16, 5, 2), (17, 17, 2)]
+
+
+@pytest.mark.parametrize("m,n_eq,K", SC_CASES)
+def test_sumcheck_vs_oracle(ctx, O, m, n_eq, K):
+    from paper_2307_16273_b200 import api
+    rng = random.Random(m * 1000 + n_eq * 10 + K)
+    tabs = [uniform_range(7, 100 * m + k, (1 << m,), -(1 << 15), 1 << 15) for k in range(K)]
+    w = [rng.randrange(P) for _ in range(n_eq)]
+    seed = fs_seed(f"sc-{m}-{n_eq}-{K}")
+    give_claim = (m % 2 == 0)
+    ot = [[int(v) % P for v in t] for t in tabs]
+    o = O.sumcheck_prove(O.Transcript(seed), m, n_eq, ot, w, None)
+    claim = o["claim"] if give_claim else None
+    # mix int32 and Fr inputs
+    gt = [dev(t) if k % 2 == 0 else api.embed_i32(ctx, dev(t)) for k, t in enumerate(tabs)]
+    tr = api.Transcript(ctx, seed)
+    g = api.sumcheck_prove(ctx, tr, m, n_eq, gt, w, claim)
+    assert g["claim"] == o["claim"]
+    assert g["msgs"] == o["msgs"]
+    assert g["r"] == o["r"]
+    assert g["finals"] == o["finals"]
+    ot2 = O.Transcript(seed)
+    O.sumcheck_prove(ot2, m, n_eq, ot, w, claim)
+    assert tr.state() == ot2.state()
+
+
+# ---------------------------------------------------------------- matmul (row a3)
+MM_CASES = [(0, 5, 6, 6, False, False), (2, 3, 4, 2, False, False), (3, 4, 5, 3, True, False),
+            (2, 6, 7, 5, False, True), (1, 6, 6, 10, True, True), (4, 2, 9, 12, False, True), (3, 10, 6, 4, True, False)]
+
+
+@pytest.mark.parametrize("lN,l1,l2,l3,ta,tb", MM_CASES)
+def test_matmul_vs_oracle(ctx, O, lN, l1, l2, l3, ta, tb):
+    from paper_2307_16273_b200 import api
+    N, D1, D2, D3 = 1 << lN, 1 << l1, 1 << l2, 1 << l3
+    A = uniform_range(8, 1 + lN, (N, D2, D1) if ta else (N, D1, D2), -(1 << 15), 1 << 15)
+    B = uniform_range(8, 2 + l3, (N, D3, D2) if tb else (N, D2, D3), -(1 << 15), 1 << 15)
+    seed = fs_seed(f"mm-{lN}-{l1}-{l2}-{l3}")
+    o = O.matmul_prove(O.Transcript(seed), A, B, ta, tb)
+    tr = api.Transcript(ctx, seed)
+    red = api.matmul_reduce(ctx, tr, dev(A), dev(B), ta, tb)
+    assert (red["w"], red["u1"], red["u3"]) == (o["w"], o["u1"], o["u3"])
+    assert api.fr_table_to_ints(ctx, red["At"]) == o["At"]
+    assert api.fr_table_to_ints(ctx, red["Bt"]) == o["Bt"]
+    assert red["claim"] == o["claim"]
+    g = api.sumcheck_prove(ctx, tr, lN + l2, lN, [red["At"], red["Bt"]], red["w"], red["claim"])
+    assert g["msgs"] == o["msgs"] and g["finals"] == o["finals"] and g["r"] == o["r"]
+
+
+def test_c1_golden(ctx):
+    """C1 (BASELINE configs[0]) against the frozen oracle transcript (tests/golden, written from oracle/ only)."""
+    import json
+    import os
+    from oracle import drivers
+    from paper_2307_16273_b200 import api
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_transcript.json")))
+    A, B = drivers.c1_inputs()
+    tr = api.Transcript(ctx, fs_seed("C1"))
+    red = api.matmul_reduce(ctx, tr, dev(A), dev(B))
+    g = api.sumcheck_prove(ctx, tr, 6, 0, [red["At"], red["Bt"]], red["w"], red["claim"])
+    assert hex(red["claim"]) == gold["claim"]
+    assert [[hex(v) for v in row] for row in g["msgs"]] == gold["msgs"]
+    assert [hex(v) for v in g["finals"]] == gold["finals"]
+    assert tr.state().hex() == gold["final_state"]
+
+
+# ---------------------------------------------------------------- zkReLU (rows a7, a8)
+def test_relu_tables_vs_oracle(ctx, O):
+    from paper_2307_16273_b200 import api
+    for (Q, R) in [(4, 2), (16, 16), (8, 8)]:
+        half = 1 << (Q + R - 1)
+        Z = uniform_range(9, Q, (4096,), -half, half)
+        GA = uniform_range(9, Q + 1, (4096,), -half, half)
+        o = O.relu_tables(Z, GA, Q, R)
+        g = api.relu_tables(ctx, dev(Z), dev(GA), Q, R)
+        for k in ("A", "GZ", "Zp", "GAp", "RZ", "RGA", "sign"):
+            assert np.array_equal(g[k].cpu().numpy(), o[k]), (Q, R, k)
+    from paper_2307_16273_b200._lib import ZkError
+    with pytest.raises(ZkError):
+        api.relu_tables(ctx, dev(np.array([32, 0], np.int32)), dev(np.array([0, 0], np.int32)), 4, 2)
+
+
+RELU_CASES = [(4, 2, 1), (4, 2, 3), (4, 2, 6), (4, 4, 5), (16, 16, 2), (16, 16, 6), (8, 8, 9), (16, 16, 11),
+              (12, 4, 8), (16, 16, 13)]
+
+
+@pytest.mark.parametrize("Q,R,logD", RELU_CASES)
+def test_relu_vs_oracle(ctx, O, Q, R, logD):
+    from paper_2307_16273_b200 import api
+    half = 1 << (Q + R - 1)
+    Z = uniform_range(10, 7 * logD + Q, (1 << logD,), -half, half)
+    GA = uniform_range(10, 7 * logD + R + 100, (1 << logD,), -half, half)
+    Z[:2] = [-1, half - 1]          # D10/D11 edges
+    seed = fs_seed(f"relu-{Q}-{R}-{logD}")
+    o = O.relu_prove(O.Transcript(seed), Z, GA, Q, R)
+    tr = api.Transcript(ctx, seed)
+    g = api.relu_prove(ctx, tr, dev(Z), dev(GA), Q, R)
+    assert g["claims"] == o["claims"]
+    for t, (gm, om) in enumerate(zip(g["msgs"], o["msgs"])):
+        assert gm == om, f"round {t}"
+    assert g["point"] == o["point"]
+    assert g["finals"] == o["finals"]
+
+
+def test_relu_range_error(ctx):
+    from paper_2307_16273_b200 import api
+    from paper_2307_16273_b200._lib import ZkError
+    Z = np.zeros(16, np.int32)
+    Z[3] = 40
+    with pytest.raises(ZkError):
+        api.relu_prove(ctx, api.Transcript(ctx, bytes(32)), dev(Z), dev(np.zeros(16, np.int32)), 4, 2)
+
+
+def test_c2_full_vs_oracle(ctx, O):
+    """C2 (BASELINE configs[1]) at full size: 64 x 1024 entries, Q = R = 16, bit-exact against the dense oracle."""
+    from oracle import drivers
+    from paper_2307_16273_b200 import api
+    Z, GA = drivers.c2_inputs()
+    o = drivers.c2_prove()
+    tr = api.Transcript(ctx, fs_seed("C2"))
+    g = api.relu_prove(ctx, tr, dev(Z), dev(GA), 16, 16)
+    assert g["claims"] == o["claims"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
+    assert tr.state() == o["state"]
+
+
+# ---------------------------------------------------------------- C5 single sumcheck
+@pytest.mark.parametrize("m", [12, 19])
+def test_c5_vs_oracle(ctx, O, m):
+    from oracle import drivers
+    from paper_2307_16273_b200 import api
+    A, B = drivers.c5_inputs(m)
+    o = drivers.c5_prove(m)
+    tr = api.Transcript(ctx, fs_seed(f"C5-m{m}"))
+    tr.absorb("c5/hdr", m.to_bytes(4, "little"))
+    w = tr.challenges("c5/w", m)
+    g = api.sumcheck_prove(ctx, tr, m, m, [dev(A), dev(B)], w, None)
+    assert g["claim"] == o["claim"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
+    assert tr.state() == o["state"]
+
+
+# ---------------------------------------------------------------- FCN family driver (row a9)
+def test_fcn_tiny_vs_oracle(ctx, O):
+    from oracle import drivers
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4)
+    trace = fcn.generate_trace(shape, x_bits=4, w_bits=4, y_bits=3)
+    fams = fcn.assemble_families(shape, trace)
+    o = drivers.fcn_prove(shape, fams, "tiny")
+    g = dfcn.prove_window(ctx, fs_seed("tiny"), fcn.fcn_header(shape), dfcn.upload_families(fams))
+    for gr, orr in zip(g, o):
+        assert gr["msgs"] == orr["msgs"], gr["name"]
+        assert gr["finals"] == orr["finals"], gr["name"]
+        assert gr["state"] == orr["state"], gr["name"]
