@@ -1,0 +1,355 @@
+"""Benchmark of the zkDL prover hot path on B200 (contract: see DESIGN.md §7 "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
+
+One step = one FAC4DNN proving window of the C4 workload (BASELINE.json metric: "prover s per
+batch update (8-layer 10M FCN, bs 64)"): all 9 families (forward, input-gradient and
+weight-gradient matmul families restricted and proved by the product sumcheck, and the stacked
+zkReLU of 8 layers x 16 steps) under one Fiat-Shamir transcript, T' = 16 training steps per window.
+value = seconds per batch update = window time / 16 (whole job: total time / total updates).
+Under torchrun each rank proves its own window (weak scaling, no data-path collective).
+The reference arm (--impl reference) times the CPU oracle on a bounded sample of the same window.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prover s per batch update (8-layer 10M FCN, bs 64); sumcheck Fr-mul/s vs peak"
+UNIT = "s/update"
+IMAD_LANES_PER_SM_CLK = 64          # fma pipe: rt_SMSP = 2 -> 16 lanes/clk/SMSP (B300_MICROARCH.md "Pipe rates")
+IMAD_PER_FRMUL = 256                # CIOS 8x32-bit lower bound: 128 product + 128 reduction half-products
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.rows.append([c.strip() for c in line.split(",")])
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) > 8:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- distributed helpers
+def dist_setup(n_gpus: int):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- workload
+def c4_workload(rank: int):
+    from synth import fcn
+    from synth.prng import DATA_SEED
+    t0 = time.time()
+    trace = fcn.generate_trace(fcn.C4_SHAPE, seed=DATA_SEED + rank)
+    fams = fcn.assemble_families(fcn.C4_SHAPE, trace)
+    log(f"[bench] rank {rank}: C4 trace + families generated in {time.time() - t0:.1f}s")
+    return fcn.C4_SHAPE, fams
+
+
+def family_bytes(fams) -> int:
+    tot = 0
+    for f in fams:
+        tot += (f.A.nbytes + f.B.nbytes) if hasattr(f, "A") else (f.Z.nbytes + f.GA.nbytes)
+    return tot
+
+
+def frmul_model(fams) -> dict:
+    """Algorithmic Fr-mul counts per window by kernel family (DESIGN.md §6 counting model)."""
+    relu = [f for f in fams if not hasattr(f, "A")]
+    out = {"k_relu_iround": 0, "k_sc_round": 0}
+    for f in relu:
+        D = f.Z.size
+        # i-rounds: 40 Fr-mul per pair (fold 6 + eq 10 + 4 evaluations x 6), pairs summed over rounds ~ D
+        out["k_relu_iround"] += 40 * D
+    for f in fams:
+        if hasattr(f, "A"):
+            N = f.A.shape[0]
+            D2 = f.A.shape[1] if f.transA else f.A.shape[2]
+            # K = 2 product rounds: fold 4 + eq 1 + 3 evaluations x 2 = 11 per pair, pairs summed ~ N * D2
+            out["k_sc_round"] += 11 * N * D2
+    return out
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_2307_16273_b200 import api, build
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    from synth.prng import fs_seed
+
+    build.build(verbose=False)
+    shape, fams = c4_workload(rank)
+    in_bytes = family_bytes(fams)
+    dev_fams = dfcn.upload_families(fams, device=f"cuda:{local}")
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=local)
+    ctx = api.Context(local, stream)
+    header = fcn.fcn_header(shape)
+    seed = fs_seed(f"C4-rank{rank}")
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            dfcn.prove_window(ctx, seed, header, dev_fams)
+        ctx.synchronize()
+        # ---- timed region: K windows, inputs resident in HBM (1.45 GB per window > 126 MB L2)
+        clocks = Clocks(local)
+        clocks.start()
+        launches0 = ctx.launches
+        ctx.profile(True)
+        ctx.profile_read()
+        barrier(world)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = dfcn.prove_window(ctx, seed, header, dev_fams)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        launches = ctx.launches - launches0
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        clk = clocks.stop()
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, world)
+    updates = world * args.steps * shape.steps
+    value = (ms / 1000.0) / updates
+    # ---- e2e: host (pinned) -> device copies of the window's inputs inside the timed region
+    host_fams = [(f, {k: torch.from_numpy(getattr(f, k)).pin_memory() for k in (("A", "B") if hasattr(f, "A") else ("Z", "GA"))})
+                 for f in fams]
+    e2e_steps = max(1, min(args.steps, 3))
+    with torch.cuda.stream(stream):
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(e2e_steps):
+            up = []
+            for f, hb in host_fams:
+                if hasattr(f, "A"):
+                    up.append(dfcn.DeviceFamily(f.name, "matmul", A=hb["A"].to(f"cuda:{local}", non_blocking=True),
+                                                B=hb["B"].to(f"cuda:{local}", non_blocking=True),
+                                                trans_a=f.transA, trans_b=f.transB))
+                else:
+                    up.append(dfcn.DeviceFamily(f.name, "relu", Z=hb["Z"].to(f"cuda:{local}", non_blocking=True),
+                                                GA=hb["GA"].to(f"cuda:{local}", non_blocking=True), Q=f.Q, R=f.R))
+            out = dfcn.prove_window(ctx, seed, header, up)      # proof bytes come back to the host
+            d2h = sum(len(r["proof"]) for r in out)
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    e2e_value = e2e_s / (world * e2e_steps * shape.steps)
+    # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
+    per_step = {k: (n / args.steps, t / args.steps) for k, (n, t) in prof.items()}
+    total_kernel_ms = sum(t for _, t in per_step.values())
+    dom = max(per_step.items(), key=lambda kv: kv[1][1]) if per_step else ("none", (0, 0.0))
+    dom_name, (dom_launches, dom_ms) = dom
+    model = frmul_model(fams)
+    clock_mhz = clk.get("sm_max_mhz") or 1965.0
+    imad_peak = 148 * IMAD_LANES_PER_SM_CLK * clock_mhz * 1e6             # lane-IMAD/s
+    frmul_peak = imad_peak / IMAD_PER_FRMUL
+    rf = None
+    key = next((k for k in model if dom_name.startswith(k) or k in dom_name), None)
+    if key and dom_ms > 0:
+        achieved = model[key] / (dom_ms / 1000.0) / 1e9
+        rf = {"bound": "alu", "kernel": dom_name, "achieved": round(achieved, 3), "peak": round(frmul_peak / 1e9, 3),
+              "unit": "GFr-mul/s", "frac": round(achieved / (frmul_peak / 1e9), 4), "traffic": None,
+              "peak_basis": f"148 SM x {IMAD_LANES_PER_SM_CLK} IMAD lanes/clk x {clock_mhz:.0f} MHz / {IMAD_PER_FRMUL} IMAD per Fr-mul",
+              "ms_per_step": round(dom_ms, 4), "share_of_step": round(dom_ms / ms_local * args.steps, 4)}
+    else:
+        rf = {"bound": "alu", "kernel": dom_name, "achieved": None, "peak": round(frmul_peak / 1e9, 3),
+              "unit": "GFr-mul/s", "frac": None, "traffic": None, "ms_per_step": round(dom_ms, 4),
+              "share_of_step": round(dom_ms / ms_local * args.steps, 4) if ms_local else None}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fr_bls12_381 (8x32-bit Montgomery)", "data": "synthetic (seeded quantized FCN training trace)",
+        "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps, "
+                               "9 families (F x3, GA x2, GW x3, ReLU D=2^23), one transcript",
+                   "updates_per_step": shape.steps, "input_bytes_per_step": in_bytes,
+                   "l2": "inputs larger than L2 (1.45 GB per window vs 126 MB)", "parallelism": f"replica x{world}"},
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": d2h},
+        "roofline": rf,
+        "kernels_ms_per_step": {k: round(t, 4) for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:12]},
+        "kernel_ms_total_per_step": round(total_kernel_ms, 4),
+        "clocks": clk,
+        "paper_context": {"value": 0.84, "unit": "s/update", "hardware": "A100", "note": "PT/step at T'=16, BS 64 (PAPER.md L405); includes commitments, not this metric"},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(fams, shape, sample_scale=args.cpu_sample)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- oracle (CPU) arm
+def oracle_window_sample(fams, shape, frac_inst: int, relu_instances: int):
+    """Time the oracle on a sub-stack of every family; return (seconds for the full window, sample note)."""
+    import numpy as np
+    import oracle as O
+    from synth.fcn import fcn_header
+    from synth.prng import fs_seed
+    tr = O.Transcript(fs_seed("C4-oracle-sample"))
+    tr.absorb("fcn/hdr", fcn_header(shape))
+    est = 0.0
+    parts = []
+    for f in fams:
+        tr.absorb("fcn/fam", f.name.encode())
+        if hasattr(f, "A"):
+            N = f.A.shape[0]
+            n = max(1, N // frac_inst)
+            t0 = time.perf_counter()
+            O.matmul_prove(tr, np.ascontiguousarray(f.A[:n]), np.ascontiguousarray(f.B[:n]), f.transA, f.transB)
+            dt = time.perf_counter() - t0
+            est += dt * N / n
+            parts.append(f"{f.name}:{n}/{N}")
+        else:
+            per = shape.batch * 1024
+            n = relu_instances
+            D = f.Z.size
+            t0 = time.perf_counter()
+            O.relu_prove(tr, np.ascontiguousarray(f.Z[:n * per]), np.ascontiguousarray(f.GA[:n * per]), f.Q, f.R)
+            dt = time.perf_counter() - t0
+            est += dt * D / (n * per)
+            parts.append(f"{f.name}:{n}/{D // per}")
+    return est, "oracle on sub-stacks " + ", ".join(parts) + " (time scaled linearly in the instance count)"
+
+
+def cpu_baseline(fams, shape, sample_scale: int = 16):
+    import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    O.set_threads(cores)
+    t0 = time.perf_counter()
+    est, note = oracle_window_sample(fams, shape, frac_inst=sample_scale, relu_instances=1)
+    wall = time.perf_counter() - t0
+    return {"value": est / shape.steps, "unit": UNIT, "cores": O.threads(), "kind": "oracle",
+            "sample": note + f"; sample wall {wall:.1f}s"}
+
+
+def run_reference(args, rank, world, local):
+    if rank != 0:
+        return
+    import oracle as O
+    shape, fams = c4_workload(0)
+    cores = len(os.sched_getaffinity(0))
+    O.set_threads(cores)
+    for _ in range(args.warmup):
+        oracle_window_sample(fams, shape, frac_inst=64, relu_instances=1)
+    ests = []
+    t0 = time.perf_counter()
+    note = ""
+    for _ in range(args.steps):
+        est, note = oracle_window_sample(fams, shape, frac_inst=64, relu_instances=1)
+        ests.append(est)
+    wall = time.perf_counter() - t0
+    value = statistics.mean(ests) / shape.steps
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(ests), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "fr_bls12_381 (4x64-bit Montgomery, CPU)",
+           "data": "synthetic (seeded quantized FCN training trace)",
+           "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps",
+                      "updates_per_step": shape.steps, "parallelism": f"cpu x{O.threads()}"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.threads(), "kind": "oracle",
+                            "sample": note + f"; {args.steps} samples in {wall:.1f}s"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="sub-stack divisor for the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, rank, 1, 0)
+        return
+    rank, world, local = dist_setup(args.gpus)
+    run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

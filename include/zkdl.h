@@ -56,6 +56,11 @@ const char* zk_last_error(const zk_ctx* ctx);
 const char* zk_version(void);
 uint64_t zk_ctx_launch_count(const zk_ctx* ctx);
 zk_status zk_ctx_synchronize(zk_ctx* ctx);
+/* Per-launch profiling: while enabled, every kernel launch of the context is bracketed by two
+ * CUDA events on the context stream.  zk_ctx_profile_read synchronises, writes one line per kernel
+ * "name<TAB>launches<TAB>total_ms\n" (NUL-terminated, cap bytes max) and clears the records. */
+zk_status zk_ctx_profile(zk_ctx* ctx, int enable);
+zk_status zk_ctx_profile_read(zk_ctx* ctx, char* out, uint64_t cap);
 
 /* --------------------------------------------------- Fiat-Shamir transcript (D3)
  * The 32-byte state lives in device memory; absorb/challenge run on the device.

@@ -52,6 +52,8 @@ def lib():
         "zk_version": ([], c.c_char_p),
         "zk_ctx_launch_count": ([vp], u64),
         "zk_ctx_synchronize": ([vp], i32),
+        "zk_ctx_profile": ([vp, i32], i32),
+        "zk_ctx_profile_read": ([vp, c.c_char_p, u64], i32),
         "zk_transcript_new": ([vp, vp, c.POINTER(vp)], i32),
         "zk_transcript_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_transcript_challenges": ([vp, c.c_char_p, u32, vp], i32),

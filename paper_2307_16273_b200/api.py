@@ -60,6 +60,19 @@ class Context:
     def synchronize(self):
         self.check(lib().zk_ctx_synchronize(self.h))
 
+    def profile(self, enable: bool):
+        self.check(lib().zk_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (launches, total_ms)} since the last read (synchronises)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        self.check(lib().zk_ctx_profile_read(self.h, buf, len(buf)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, n, ms = line.split("\t")
+            out[name] = (int(n), float(ms))
+        return out
+
     def close(self):
         if getattr(self, "h", None):
             lib().zk_ctx_destroy(self.h)

@@ -75,6 +75,49 @@ zk_status zk_ctx_synchronize(zk_ctx* ctx) {
     ZK_API_END(ctx)
 }
 
+zk_status zk_ctx_profile(zk_ctx* ctx, int enable) {
+    ZK_API_BEGIN(ctx)
+    ctx->prof = enable != 0;
+    ZK_API_END(ctx)
+}
+
+zk_status zk_ctx_profile_read(zk_ctx* ctx, char* out, uint64_t cap) {
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(out && cap, ZK_ERR_ARG, "null buffer");
+    ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    struct Agg {
+        std::string name;
+        uint64_t n;
+        double ms;
+    };
+    std::vector<Agg> agg;
+    for (auto& r : ctx->recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        bool found = false;
+        for (auto& g : agg)
+            if (g.name == r.name) {
+                g.n++;
+                g.ms += ms;
+                found = true;
+                break;
+            }
+        if (!found) agg.push_back({r.name, 1, (double)ms});
+        ctx->ev_pool.push_back(r.a);
+        ctx->ev_pool.push_back(r.b);
+    }
+    ctx->recs.clear();
+    std::string s;
+    char line[512];
+    for (auto& g : agg) {
+        snprintf(line, sizeof line, "%s\t%llu\t%.6f\n", g.name.c_str(), (unsigned long long)g.n, g.ms);
+        s += line;
+    }
+    ZK_REQUIRE(s.size() + 1 <= cap, ZK_ERR_ARG, "profile buffer too small");
+    memcpy(out, s.c_str(), s.size() + 1);
+    ZK_API_END(ctx)
+}
+
 // ------------------------------------------------------------------ transcript
 zk_status zk_transcript_new(zk_ctx* ctx, const uint8_t seed[32], zk_transcript** out) {
     ZK_API_BEGIN(ctx)

@@ -18,6 +18,24 @@ struct zk_ctx {
     int num_sms = 148;
     uint64_t launches = 0;
     std::string err;
+    // per-launch CUDA-event profiling (zk_ctx_profile): events bracket each launch on the ctx stream
+    bool prof = false;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t take_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
 };
 
 struct zk_transcript {
@@ -53,8 +71,18 @@ inline void after_launch(zk_ctx* ctx, const char* what) {
 }
 #define ZK_LAUNCH(ctx, kernel, grid, block, smem, ...)                                                 \
     do {                                                                                               \
+        cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;                                                  \
+        if ((ctx)->prof) {                                                                             \
+            ev_a_ = (ctx)->take_event();                                                               \
+            ev_b_ = (ctx)->take_event();                                                               \
+            cudaEventRecord(ev_a_, (ctx)->stream);                                                     \
+        }                                                                                              \
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                               \
         ::zk::after_launch((ctx), #kernel);                                                            \
+        if ((ctx)->prof) {                                                                             \
+            cudaEventRecord(ev_b_, (ctx)->stream);                                                     \
+            (ctx)->recs.push_back({#kernel, ev_a_, ev_b_});                                            \
+        }                                                                                              \
     } while (0)
 
 // Stream-ordered scratch buffer (CUDA memory pool of the device), freed on scope exit.

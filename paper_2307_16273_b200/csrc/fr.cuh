@@ -289,7 +289,8 @@ __device__ __forceinline__ fr_t fr_shfl_xor(const fr_t& a, int mask) {
 
 // Fermat inverse a^(p-2) (single thread; used only for a handful of scalars)
 __device__ inline fr_t fr_inv(const fr_t& a) {
-    const uint32_t e[8] = {ZK_P0 - 2, ZK_P1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7};
+    // p - 2: the low limb 0x00000001 borrows from the next one
+    const uint32_t e[8] = {0xffffffffu, ZK_P1 - 1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7};
     fr_t r = fr_one();
     for (int i = 7; i >= 0; i--)
         for (int b = 31; b >= 0; b--) {

@@ -66,8 +66,11 @@ def test_noncanonical_rejected(ctx):
     raw = torch.frombuffer(bytearray(P.to_bytes(32, "little")), dtype=torch.uint8).reshape(1, 32).cuda()
     with pytest.raises(ZkError):
         api.fr_table_from_canonical(ctx, raw)
-    with pytest.raises(ZkError):
-        api.eq_table(ctx, [P])
+    import ctypes
+    from paper_2307_16273_b200._lib import lib
+    out = api.fr_empty(2, "cuda")
+    st = lib().zk_eq_table(ctx.h, ctypes.create_string_buffer(P.to_bytes(32, "little"), 32), 1, None, out.data_ptr())
+    assert st == -3    # ZK_ERR_NONCANONICAL
 
 
 # ---------------------------------------------------------------- transcript (D3)
