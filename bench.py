@@ -193,7 +193,7 @@ def run_ours(args, rank, world, local):
     # ---- e2e: host (pinned) -> device copies of the window's inputs inside the timed region
     host_fams = [(f, {k: torch.from_numpy(getattr(f, k)).pin_memory() for k in (("A", "B") if hasattr(f, "A") else ("Z", "GA"))})
                  for f in fams]
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = 0 if args.profile_mode else max(1, min(args.steps, 3))
     with torch.cuda.stream(stream):
         barrier(world)
         torch.cuda.synchronize()
@@ -213,7 +213,7 @@ def run_ours(args, rank, world, local):
             d2h = sum(len(r["proof"]) for r in out)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e_value = e2e_s / (world * e2e_steps * shape.steps)
+    e2e_value = e2e_s / (world * e2e_steps * shape.steps) if e2e_steps else None
     # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
     per_step = {k: (n / args.steps, t / args.steps) for k, (n, t) in prof.items()}
     total_kernel_ms = sum(t for _, t in per_step.values())
@@ -251,7 +251,7 @@ def run_ours(args, rank, world, local):
         "clocks": clk,
         "paper_context": {"value": 0.84, "unit": "s/update", "hardware": "A100", "note": "PT/step at T'=16, BS 64 (PAPER.md L405); includes commitments, not this metric"},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_mode:
         out["cpu_baseline"] = cpu_baseline(fams, shape, sample_scale=args.cpu_sample)
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -338,6 +338,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=["C4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-mode", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")
     ap.add_argument("--cpu-sample", type=int, default=16, help="sub-stack divisor for the cpu_baseline sample")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -189,6 +189,11 @@ __device__ __forceinline__ fr_t fr_mul(const fr_t& a, const fr_t& b) {
 }
 __device__ __forceinline__ fr_t fr_sqr(const fr_t& a) { return fr_mul(a, a); }
 
+// One out-of-line copy for cold code (finalizers, single-CTA round kernels): the inlined product is
+// ~560 SASS instructions, and cold code that inlines dozens of them runs out of the instruction
+// cache (ncu: stall_no_inst dominated the round kernels' finalize).
+static __device__ __noinline__ fr_t fr_mul_cold(fr_t a, fr_t b) { return fr_mul(a, b); }
+
 // Montgomery reduction of a wide unsigned integer T (10 limbs, T < p * 2^256):
 // returns T * R^{-1} mod p.  Used by the int32 x Fr lazy accumulators.
 __device__ __forceinline__ fr_t fr_redc_wide(const uint32_t w[10]) {
@@ -247,6 +252,11 @@ __device__ __forceinline__ fr_t fr_to_canonical(const fr_t& a) {   // Montgomery
     fr_t one = fr_zero();
     one.v[0] = 1;
     return fr_mul(a, one);
+}
+__device__ __forceinline__ fr_t fr_to_canonical_cold(const fr_t& a) {
+    fr_t one = fr_zero();
+    one.v[0] = 1;
+    return fr_mul_cold(a, one);
 }
 __device__ __forceinline__ fr_t fr_from_canonical(const fr_t& x) {  // integer < 2^256 -> Montgomery
     return fr_mul(ZK_R2, x);

@@ -103,6 +103,189 @@ __device__ __forceinline__ void masked_add10(uint32_t (&a)[10], const fr_t& v, u
           "r"(v.v[5] & mm), "r"(v.v[6] & mm), "r"(v.v[7] & mm));
 }
 
+// ---------------------------------------------------------------- bit sums, subset-sum tables (v2)
+// Per chunk of 64 entries (within one LO row): byte planes P[s][g][j] (bit j of the 8 words of
+// byte-group g), byte subset-sum tables Tb[g][v] = sum_{k in v} e_b(8g + k) for the co-occurrence
+// cells, nibble tables Tm[x][h][v] = sum_{k in v} c_x(4h + k) for the linear cells.  A C cell
+// (j1, j2) then costs one lookup Tb[g][P[g][j1] & P[g][j2]] and one lazy 320-bit add per 8 entries,
+// an M cell one lookup per 4 entries; the tables cost ~2.5 Fr additions per entry for all cells.
+// Table entries are sums of LO' values (eq * R, "double Montgomery"), reduced mod p; the lazy
+// accumulators are closed with REDC (-> Montgomery) and multiplied by HI[row] when the row changes.
+constexpr int BS2_CH = 64;
+constexpr int BS2_T = 256;
+constexpr int BS2_MAXC = 6;   // cell slots per thread: 1 linear (M) + up to 5 co-occurrence (C)
+
+struct BitCell2 {
+    uint8_t j1, j2, s, x;   // bit positions, word (0 Z, 1 G_A), weight table (M cells: 0..3; C cells: 4)
+};
+
+struct Bitsum2Args {
+    const int32_t* Z;
+    const int32_t* GA;
+    uint32_t logD, lo_bits, qr_mask, sig_bit;
+    const fr_t* LO[5];
+    const fr_t* HI[5];
+    const BitCell2* cells;   // [0, nM) linear cells, [nM, nM + nC) co-occurrence cells
+    uint32_t nM, nC;
+    fr_t* partials;          // gridDim.x * (nM + nC)
+};
+
+struct Bitsum2Smem {
+    fr_t Tb[8][256];
+    fr_t Tm[4][16][16];
+    fr_t E[5][BS2_CH];
+    fr_t U[8][8];
+    uint32_t W[2][BS2_CH];
+    uint8_t P[2][8][32];
+    uint8_t sig[BS2_CH];
+};
+
+__device__ __forceinline__ void wide_add_fr(uint32_t (&a)[10], const fr_t& v) {
+    asm("add.cc.u32  %0, %0, %10;\n\t"
+        "addc.cc.u32 %1, %1, %11;\n\t"
+        "addc.cc.u32 %2, %2, %12;\n\t"
+        "addc.cc.u32 %3, %3, %13;\n\t"
+        "addc.cc.u32 %4, %4, %14;\n\t"
+        "addc.cc.u32 %5, %5, %15;\n\t"
+        "addc.cc.u32 %6, %6, %16;\n\t"
+        "addc.cc.u32 %7, %7, %17;\n\t"
+        "addc.cc.u32 %8, %8, 0;\n\t"
+        "addc.u32    %9, %9, 0;"
+        : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
+          "+r"(a[8]), "+r"(a[9])
+        : "r"(v.v[0]), "r"(v.v[1]), "r"(v.v[2]), "r"(v.v[3]), "r"(v.v[4]), "r"(v.v[5]), "r"(v.v[6]), "r"(v.v[7]));
+}
+
+__global__ void __launch_bounds__(BS2_T, 1) k_relu_bitsums2(Bitsum2Args a) {
+    extern __shared__ __align__(16) uint8_t smem2_raw[];
+    Bitsum2Smem& S = *reinterpret_cast<Bitsum2Smem*>(smem2_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t D = 1ull << a.logD;
+    const uint64_t nchunks = D / BS2_CH;
+    const uint64_t c_begin = blockIdx.x * nchunks / gridDim.x, c_end = (blockIdx.x + 1) * nchunks / gridDim.x;
+    const uint32_t ncell = a.nM + a.nC;
+    // this thread's cells: slot 0 = linear cell tid (if tid < nM), slots 1.. = co-occurrence cells
+    BitCell2 cl[BS2_MAXC];
+    int cid[BS2_MAXC];
+#pragma unroll
+    for (int q = 0; q < BS2_MAXC; q++) {
+        int c = q == 0 ? (tid < (int)a.nM ? tid : -1) : ((int)a.nM + tid + (q - 1) * BS2_T);
+        if (q > 0 && c >= (int)ncell) c = -1;
+        cid[q] = c;
+        cl[q] = c >= 0 ? a.cells[c] : BitCell2{0, 0, 0, 0};
+    }
+    uint32_t acc[BS2_MAXC][10];
+    fr_t tot[BS2_MAXC];
+#pragma unroll
+    for (int q = 0; q < BS2_MAXC; q++) {
+        tot[q] = fr_zero();
+#pragma unroll
+        for (int k = 0; k < 10; k++) acc[q][k] = 0;
+    }
+    const uint64_t lo_mask = (1ull << a.lo_bits) - 1;
+    uint64_t row = (c_begin * BS2_CH) >> a.lo_bits;
+    for (uint64_t ch = c_begin; ch < c_end; ch++) {
+        const uint64_t i0 = ch * BS2_CH;
+        const uint64_t r_here = i0 >> a.lo_bits;
+        if (r_here != row) {
+#pragma unroll
+            for (int q = 0; q < BS2_MAXC; q++)
+                if (cid[q] >= 0) {
+                    tot[q] = fr_add(tot[q], fr_mul(fr_redc_wide(acc[q]), fr_load(&a.HI[cl[q].x][row])));
+#pragma unroll
+                    for (int k = 0; k < 10; k++) acc[q][k] = 0;
+                }
+            row = r_here;
+        }
+        __syncthreads();
+        // stage words, sign bits and LO' weights of the chunk
+        for (int e = tid; e < 5 * BS2_CH; e += BS2_T) {
+            const int x = e / BS2_CH, k = e % BS2_CH;
+            S.E[x][k] = fr_load(&a.LO[x][(i0 + k) & lo_mask]);
+        }
+        if (tid < BS2_CH) {
+            uint32_t z = (uint32_t)__ldg(a.Z + i0 + tid), g = (uint32_t)__ldg(a.GA + i0 + tid);
+            S.W[0][tid] = z & a.qr_mask;
+            S.W[1][tid] = g & a.qr_mask;
+            S.sig[tid] = (z >> a.sig_bit) & 1;
+        }
+        __syncthreads();
+        // gate c_A, c_GZ by (1 - sig); byte planes
+        if (tid < 2 * BS2_CH) {
+            const int k = tid % BS2_CH, x = tid < BS2_CH ? 1 : 3;
+            if (S.sig[k]) S.E[x][k] = fr_zero();
+        }
+        for (int e = tid; e < 2 * 8 * 32; e += BS2_T) {
+            const int s = e >> 8, g = (e >> 5) & 7, j = e & 31;
+            uint32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) m |= ((S.W[s][8 * g + k] >> j) & 1u) << k;
+            S.P[s][g][j] = (uint8_t)m;
+        }
+        // U[g][q] = sum_{k<3, bit k of q} e_b(8g + 5 + k)
+        if (lane < 8) {
+            const fr_t* eb = &S.E[4][8 * warp + 5];
+            fr_t u = fr_zero();
+            if (lane & 1) u = eb[0];
+            if (lane & 2) u = fr_add(u, eb[1]);
+            if (lane & 4) u = fr_add(u, eb[2]);
+            S.U[warp][lane] = u;
+        }
+        __syncthreads();
+        // byte tables: warp g builds Tb[g][l + 32 q] = base(l) + U[g][q]
+        {
+            const int g = warp;
+            const fr_t* eb = &S.E[4][8 * g];
+            fr_t base = fr_zero();
+#pragma unroll
+            for (int k = 0; k < 5; k++)
+                if ((lane >> k) & 1) base = fr_add(base, eb[k]);
+            S.Tb[g][lane] = base;
+#pragma unroll
+            for (int q = 1; q < 8; q++) S.Tb[g][lane + 32 * q] = fr_add(base, S.U[g][q]);
+        }
+        // nibble tables Tm[x][h][v]
+        for (int e = tid; e < 4 * 16 * 16; e += BS2_T) {
+            const int x = e >> 8, h = (e >> 4) & 15, v = e & 15;
+            const fr_t* cx = &S.E[x][4 * h];
+            fr_t t = fr_zero();
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if ((v >> k) & 1) t = fr_add(t, cx[k]);
+            S.Tm[x][h][v] = t;
+        }
+        __syncthreads();
+        // accumulate
+        if (cid[0] >= 0) {
+            const int s = cl[0].s, j = cl[0].j1, x = cl[0].x;
+#pragma unroll 4
+            for (int h = 0; h < 16; h++) {
+                const int nib = (S.P[s][h >> 1][j] >> (4 * (h & 1))) & 15;
+                wide_add_fr(acc[0], S.Tm[x][h][nib]);
+            }
+        }
+#pragma unroll
+        for (int q = 1; q < BS2_MAXC; q++) {
+            if (cid[q] >= 0) {
+                const int s = cl[q].s, j1 = cl[q].j1, j2 = cl[q].j2;
+#pragma unroll
+                for (int g = 0; g < 8; g++) {
+                    const int m = S.P[s][g][j1] & S.P[s][g][j2];
+                    wide_add_fr(acc[q], S.Tb[g][m]);
+                }
+            }
+        }
+    }
+    if (c_begin < c_end) {
+#pragma unroll
+        for (int q = 0; q < BS2_MAXC; q++)
+            if (cid[q] >= 0) tot[q] = fr_add(tot[q], fr_mul(fr_redc_wide(acc[q]), fr_load(&a.HI[cl[q].x][row])));
+    }
+#pragma unroll
+    for (int q = 0; q < BS2_MAXC; q++)
+        if (cid[q] >= 0) fr_store(&a.partials[(uint64_t)blockIdx.x * ncell + cid[q]], tot[q]);
+}
+
 // Each thread owns cells tid and tid + blockDim.x.  Each block walks a contiguous range of chunks;
 // the lazy accumulators are closed (REDC, times HI[row]) whenever the row i >> lo_bits changes.
 __global__ void __launch_bounds__(640) k_relu_bitsums(BitsumArgs a) {
@@ -197,7 +380,7 @@ __device__ __forceinline__ int tri_index(int j1, int j2, int B) {   // j1 <= j2,
 __device__ fr_t small_pow2(int e) {   // Montgomery form of 2^e, 0 <= e < 64
     fr_t b = fr_zero();
     if (e < 32) b.v[0] = 1u << e; else b.v[1] = 1u << (e - 32);
-    return fr_mul(ZK_R2, b);
+    return fr_mul_cold(ZK_R2, b);
 }
 
 __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
@@ -210,7 +393,7 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
     const int B = a.B, tid = threadIdx.x;
     const int QR = a.Q + a.R;
     const fr_t r = fr_load(&a.r[0]), rp = fr_load(&a.r[1]);
-    const fr_t r2 = fr_mul(r, r);
+    const fr_t r2 = fr_mul_cold(r, r);
     const fr_t* MZ = a.cells;
     const fr_t* MA = a.cells + B;
     const fr_t* MGA = a.cells + 2 * B;
@@ -231,36 +414,38 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_t e = fr_one();
         for (uint32_t t = 0; t < a.logB; t++) {
             fr_t u = fr_load(&a.ubin[t]);
-            e = fr_mul(e, ((j >> t) & 1) ? u : fr_sub(fr_one(), u));
+            e = fr_mul_cold(e, ((j >> t) & 1) ? u : fr_sub(fr_one(), u));
         }
         EB[j] = e;
-        LS[j] = fr_add(fr_mul(r2, fr_load(&MZ[j])), fr_mul(fr_mul(rp, r2), fr_load(&MGA[j])));
-        LSP[j] = fr_add(fr_mul(r, fr_load(&MA[j])), fr_mul(fr_mul(rp, r), fr_load(&MGZ[j])));
+        LS[j] = fr_add(fr_mul_cold(r2, fr_load(&MZ[j])), fr_mul_cold(fr_mul_cold(rp, r2), fr_load(&MGA[j])));
+        LSP[j] = fr_add(fr_mul_cold(r, fr_load(&MA[j])), fr_mul_cold(fr_mul_cold(rp, r), fr_load(&MGZ[j])));
     }
     for (int e = tid; e < B * B; e += blockDim.x) {
         int j1 = e / B, j2 = e % B;
         int lo = j1 < j2 ? j1 : j2, hi = j1 < j2 ? j2 : j1;
         int ti = tri_index(lo, hi, B);
-        fr_t c = fr_add(fr_load(&C0[ti]), fr_mul(rp, fr_load(&C1[ti])));
+        fr_t c = fr_add(fr_load(&C0[ti]), fr_mul_cold(rp, fr_load(&C1[ti])));
         CQ[j1][j2] = c;
         if (j1 == j2) LQ[j1] = c;   // L_s = diag(C_s) since bit^2 = bit
     }
+    __shared__ FsScratch fs;
+    if (tid < 32) fs_begin(fs, a.st);
     __syncthreads();
-    fr_t claim = fr_zero();
+    const fr_t claim = fr_zero();   // (the i-phase computes every evaluation; the running claim is not needed)
     for (uint32_t t = 0; t < a.logB; t++) {
         const int n = B >> t, np = n >> 1;
         // evaluations: item (b, X)
         if (tid < 4 * np) {
             const int b = tid >> 2, X = tid & 3;
             const fr_t x = fr_from_u32((uint32_t)X), omx = fr_sub(fr_one(), x);
-#define LIN(v) fr_add(v[2 * b], fr_mul(x, fr_sub(v[2 * b + 1], v[2 * b])))
+#define LIN(v) fr_add(v[2 * b], fr_mul_cold(x, fr_sub(v[2 * b + 1], v[2 * b])))
             fr_t sv = LIN(S), spv = LIN(SP), ebv = LIN(EB), lsv = LIN(LS), lspv = LIN(LSP), lqv = LIN(LQ);
 #undef LIN
             // bilinear: sum_{x1,x2} l(x1) l(x2) CQ[2b+x1][2b+x2]
             fr_t c00 = CQ[2 * b][2 * b], c01 = CQ[2 * b][2 * b + 1], c10 = CQ[2 * b + 1][2 * b], c11 = CQ[2 * b + 1][2 * b + 1];
-            fr_t cq = fr_add(fr_mul(fr_mul(omx, omx), c00),
-                             fr_add(fr_mul(fr_mul(omx, x), fr_add(c01, c10)), fr_mul(fr_mul(x, x), c11)));
-            fr_t v = fr_add(fr_add(fr_mul(sv, lsv), fr_mul(spv, lspv)), fr_mul(ebv, fr_sub(cq, lqv)));
+            fr_t cq = fr_add(fr_mul_cold(fr_mul_cold(omx, omx), c00),
+                             fr_add(fr_mul_cold(fr_mul_cold(omx, x), fr_add(c01, c10)), fr_mul_cold(fr_mul_cold(x, x), c11)));
+            fr_t v = fr_add(fr_add(fr_mul_cold(sv, lsv), fr_mul_cold(spv, lspv)), fr_mul_cold(ebv, fr_sub(cq, lqv)));
             vals[tid] = v;
         }
         __syncthreads();
@@ -270,14 +455,14 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
             msg[tid] = sum;
         }
         __syncthreads();
-        if (tid == 0) {
-            fr_t ev[4] = {msg[0], msg[1], msg[2], msg[3]};
-            tr_absorb_frs(a.st, "relu/msg", ev, 4, a.msg_out + 128ull * t);
-            fr_t rt = tr_challenge(a.st, "relu/x");
-            fr_to_bytes(rt, a.point_out + 32ull * t);
-            fr_store(&a.rj_out[t], rt);
-            rt_sm = rt;
-            if (t + 1 == a.logB) claim = interp_small(ev, 3, rt);
+        if (tid < 32) {
+            fs_absorb_frs(fs, "relu/msg", tid < 4 ? msg[tid & 3] : fr_zero(), 4, a.msg_out + 128ull * t);
+            fr_t rt = fs_challenge(fs, "relu/x");
+            if (tid == 0) {
+                fr_canon_to_bytes(fs.rc, a.point_out + 32ull * t);
+                fr_store(&a.rj_out[t], rt);
+                rt_sm = rt;
+            }
         }
         __syncthreads();
         const fr_t rt = rt_sm;
@@ -285,7 +470,7 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_t nv[6];
         if (tid < np) {
             const int b = tid;
-#define FOLD(v) fr_add(v[2 * b], fr_mul(rt, fr_sub(v[2 * b + 1], v[2 * b])))
+#define FOLD(v) fr_add(v[2 * b], fr_mul_cold(rt, fr_sub(v[2 * b + 1], v[2 * b])))
             nv[0] = FOLD(S); nv[1] = FOLD(SP); nv[2] = FOLD(EB); nv[3] = FOLD(LS); nv[4] = FOLD(LSP); nv[5] = FOLD(LQ);
 #undef FOLD
         }
@@ -294,7 +479,7 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         int cc = 0;
         for (int e = tid; e < n * np; e += blockDim.x) {
             int i = e / np, c = e % np;
-            cv[cc++] = fr_add(CQ[i][2 * c], fr_mul(rt, fr_sub(CQ[i][2 * c + 1], CQ[i][2 * c])));
+            cv[cc++] = fr_add(CQ[i][2 * c], fr_mul_cold(rt, fr_sub(CQ[i][2 * c + 1], CQ[i][2 * c])));
         }
         __syncthreads();
         cc = 0;
@@ -306,18 +491,19 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_t rv = fr_zero();
         if (tid < np * np) {
             int b = tid / np, c = tid % np;
-            rv = fr_add(CQ[2 * b][c], fr_mul(rt, fr_sub(CQ[2 * b + 1][c], CQ[2 * b][c])));
+            rv = fr_add(CQ[2 * b][c], fr_mul_cold(rt, fr_sub(CQ[2 * b + 1][c], CQ[2 * b][c])));
         }
         __syncthreads();
         if (tid < np * np) CQ[tid / np][tid % np] = rv;
         __syncthreads();
     }
+    if (tid < 32) fs_end(fs, a.st);
     if (tid == 0) {
         const fr_t s = S[0], sp = SP[0];
-        fr_store(&a.kappa[0], fr_mul(r2, s));
-        fr_store(&a.kappa[1], fr_mul(r, sp));
-        fr_store(&a.kappa[2], fr_mul(fr_mul(rp, r2), s));
-        fr_store(&a.kappa[3], fr_mul(fr_mul(rp, r), sp));
+        fr_store(&a.kappa[0], fr_mul_cold(r2, s));
+        fr_store(&a.kappa[1], fr_mul_cold(r, sp));
+        fr_store(&a.kappa[2], fr_mul_cold(fr_mul_cold(rp, r2), s));
+        fr_store(&a.kappa[3], fr_mul_cold(fr_mul_cold(rp, r), sp));
         fr_store(&a.kappa[4], EB[0]);
         fr_store(&a.kappa[5], rp);
         fr_store(&a.kappa[6], claim);
@@ -327,7 +513,7 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_t e = fr_one();
         for (uint32_t t = 0; t < a.logB; t++) {
             fr_t u = fr_load(&a.rj_out[t]);
-            e = fr_mul(e, ((j >> t) & 1) ? u : fr_sub(fr_one(), u));
+            e = fr_mul_cold(e, ((j >> t) & 1) ? u : fr_sub(fr_one(), u));
         }
         ej[j] = e;
     }
@@ -459,18 +645,24 @@ __global__ void __launch_bounds__(256) k_relu_iround(IRoundArgs a) {
     }
     __shared__ fr_t tot[4];
     __shared__ fr_t eqr[5];
+    __shared__ FsScratch fs;
     if (grid_reduce_fr_block<4>(acc, a.partials, a.ticket, tot)) {
-        if (threadIdx.x == 0) {
-            fr_t ev[4] = {tot[0], tot[1], tot[2], tot[3]};
-            tr_absorb_frs(a.st, "relu/msg", ev, 4, a.msg_out);
-            fr_t rt = tr_challenge(a.st, "relu/x");
-            fr_store(a.r_out, rt);
-            fr_to_bytes(rt, a.point_out);
-            for (int x = 0; x < 5; x++) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur
-                fr_t u = fr_load(&a.u[x][a.t]);
-                fr_t ur = fr_mul(u, rt);
-                eqr[x] = fr_add(fr_sub(fr_sub(fr_one(), u), rt), fr_add(ur, ur));
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            fs_begin(fs, a.st);
+            fs_absorb_frs(fs, "relu/msg", lane < 4 ? tot[lane & 3] : fr_zero(), 4, a.msg_out);
+            fr_t rt = fs_challenge(fs, "relu/x");
+            if (lane == 0) {
+                fr_store(a.r_out, rt);
+                fr_canon_to_bytes(fs.rc, a.point_out);
             }
+            if (lane < 5) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur, one lane per eq point
+                const fr_t* up = lane == 0 ? a.u[0] : lane == 1 ? a.u[1] : lane == 2 ? a.u[2] : lane == 3 ? a.u[3] : a.u[4];
+                fr_t u = fr_load(&up[a.t]);
+                fr_t ur = fr_mul(u, rt);
+                eqr[lane] = fr_add(fr_sub(fr_sub(fr_one(), u), rt), fr_add(ur, ur));
+            }
+            fs_end(fs, a.st);
         }
         __syncthreads();
         const uint32_t nh = 1u << a.hb;
@@ -509,13 +701,15 @@ __global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
         if (a.fold) {
             fr_t r = fr_load(a.r_prev);
             fr_t y0 = fr_load(&a.src[k][2 * i]), y1 = fr_load(&a.src[k][2 * i + 1]);
-            v = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+            v = fr_add(y0, fr_mul_cold(r, fr_sub(y1, y0)));
         } else {
             v = fr_load(&a.src[k][i]);
         }
         T[k][i] = v;
     }
     for (int e = tid; e < 5 * n0; e += blockDim.x) T[3 + e / n0][e % n0] = fr_load(&a.hi[e / n0][e % n0]);
+    __shared__ FsScratch fs;
+    if (tid < 32) fs_begin(fs, a.st);
     __syncthreads();
     for (uint32_t t = 0; t < a.hb; t++) {
         const int n = n0 >> t, np = n >> 1;
@@ -523,26 +717,25 @@ __global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
             const int b = tid >> 2, X = tid & 3;
             const fr_t x = fr_from_u32((uint32_t)X);
             fr_t v[8];
-            for (int k = 0; k < 8; k++) v[k] = fr_add(T[k][2 * b], fr_mul(x, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+            for (int k = 0; k < 8; k++) v[k] = fr_add(T[k][2 * b], fr_mul_cold(x, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
             // tables: 0 a0, 1 a1, 2 oms, 3 EZ, 4 EA, 5 EGA, 6 EGZ, 7 Eb
-            fr_t t0 = fr_mul(v[0], fr_add(v[3], fr_mul(v[4], v[2])));
-            fr_t t1 = fr_mul(v[1], fr_add(v[5], fr_mul(v[6], v[2])));
-            fr_t q = fr_add(fr_mul(v[0], fr_sub(v[0], fr_one())), fr_mul(rp, fr_mul(v[1], fr_sub(v[1], fr_one()))));
-            vals[b][X] = fr_add(fr_add(t0, t1), fr_mul(v[7], q));
+            fr_t t0 = fr_mul_cold(v[0], fr_add(v[3], fr_mul_cold(v[4], v[2])));
+            fr_t t1 = fr_mul_cold(v[1], fr_add(v[5], fr_mul_cold(v[6], v[2])));
+            fr_t q = fr_add(fr_mul_cold(v[0], fr_sub(v[0], fr_one())), fr_mul_cold(rp, fr_mul_cold(v[1], fr_sub(v[1], fr_one()))));
+            vals[b][X] = fr_add(fr_add(t0, t1), fr_mul_cold(v[7], q));
         }
         __syncthreads();
-        if (tid == 0) {
-            fr_t ev[4];
-            for (int X = 0; X < 4; X++) {
-                fr_t s = fr_zero();
-                for (int b = 0; b < np; b++) s = fr_add(s, vals[b][X]);
-                ev[X] = s;
+        if (tid < 32) {
+            fr_t ev = fr_zero();
+            if (tid < 4)
+                for (int b = 0; b < np; b++) ev = fr_add(ev, vals[b][tid]);
+            fs_absorb_frs(fs, "relu/msg", ev, 4, a.msg_out + 128ull * t);
+            fr_t rt = fs_challenge(fs, "relu/x");
+            if (tid == 0) {
+                fr_store(&a.r_out[t], rt);
+                fr_canon_to_bytes(fs.rc, a.point_out + 32ull * t);
+                rt_sm = rt;
             }
-            tr_absorb_frs(a.st, "relu/msg", ev, 4, a.msg_out + 128ull * t);
-            fr_t rt = tr_challenge(a.st, "relu/x");
-            fr_store(&a.r_out[t], rt);
-            fr_to_bytes(rt, a.point_out + 32ull * t);
-            rt_sm = rt;
         }
         __syncthreads();
         const fr_t rt = rt_sm;
@@ -550,16 +743,17 @@ __global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
         int cnt = 0;
         for (int e = tid; e < 8 * np; e += blockDim.x) {
             int k = e / np, b = e % np;
-            nv[cnt++] = fr_add(T[k][2 * b], fr_mul(rt, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+            nv[cnt++] = fr_add(T[k][2 * b], fr_mul_cold(rt, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
         }
         __syncthreads();
         cnt = 0;
         for (int e = tid; e < 8 * np; e += blockDim.x) T[e / np][e % np] = nv[cnt++];
         __syncthreads();
     }
-    if (tid == 0) {
-        fr_t fin[3] = {T[0][0], T[1][0], fr_sub(fr_one(), T[2][0])};
-        tr_absorb_frs(a.st, "relu/final", fin, 3, a.finals_out);
+    if (tid < 32) {
+        fr_t fin = tid == 0 ? T[0][0] : tid == 1 ? T[1][0] : fr_sub(fr_one(), T[2][0]);
+        fs_absorb_frs(fs, "relu/final", fin, 3, a.finals_out);
+        fs_end(fs, a.st);
     }
 }
 
@@ -596,7 +790,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     mle_i32_relu(ctx, 0, Z, GA, R, logD, U + logD, claims + 1, s);
     mle_i32_plain(ctx, GA, logD, U + 2 * logD, claims + 2, s);
     mle_i32_relu(ctx, 1, Z, GA, R, logD, U + 3 * logD, claims + 3, s);
-    ZK_LAUNCH(ctx, k_tr_absorb_frs, 1, 1, 0, tr->d_st, make_tag("relu/claims"), (const fr_t*)claims, 4u, proof + 12);
+    ZK_LAUNCH(ctx, k_tr_absorb_frs, 1, 32, 0, tr->d_st, make_tag("relu/claims"), (const fr_t*)claims, 4u, proof + 12);
     // r, r', u_bin
     fr_t* rr = s.alloc<fr_t>(2);
     fr_t* ubin = s.alloc<fr_t>(m);
@@ -642,17 +836,52 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     }
     ba.cells = d_cells;
     ba.ncell = ncell;
-    uint32_t bs_threads = ((ncell + 1) / 2 + 31) / 32 * 32;
-    if (bs_threads > 640) bs_threads = 640;
-    uint64_t nchunks = D / (D < BS_CH ? D : BS_CH);
-    uint32_t bs_grid = (uint32_t)(nchunks < (uint64_t)ctx->num_sms * 2 ? nchunks : (uint64_t)ctx->num_sms * 2);
-    ba.partials = s.alloc<fr_t>((size_t)bs_grid * ncell);
-    size_t bs_smem = 5 * BS_CH * sizeof(fr_t) + 2 * BS_CH * 4 + BS_CH;
-    ZK_CUDA(cudaFuncSetAttribute(k_relu_bitsums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
-    ZK_REQUIRE(ncell <= 2 * bs_threads, ZK_ERR_INTERNAL, "bitsum cells exceed the block");
-    ZK_LAUNCH(ctx, k_relu_bitsums, bs_grid, bs_threads, bs_smem, ba);
     fr_t* cell_tot = s.alloc<fr_t>(ncell);
-    ZK_LAUNCH(ctx, k_relu_bitsums_reduce, (ncell + 127) / 128, 128, 0, (const fr_t*)ba.partials, bs_grid, ncell, cell_tot);
+    if (logD >= 6) {   // subset-sum tables over chunks of 64 entries
+        std::vector<BitCell2> c2;
+        for (int x = 0; x < 4; x++)
+            for (uint32_t j = 0; j < B; j++) c2.push_back(BitCell2{(uint8_t)j, (uint8_t)j, (uint8_t)(x >= 2), (uint8_t)x});
+        for (int sd = 0; sd < 2; sd++)
+            for (uint32_t j1 = 0; j1 < B; j1++)
+                for (uint32_t j2 = j1; j2 < B; j2++) c2.push_back(BitCell2{(uint8_t)j1, (uint8_t)j2, (uint8_t)sd, 4});
+        ZK_REQUIRE(c2.size() == ncell && ncell - 4 * B <= (BS2_MAXC - 1) * BS2_T, ZK_ERR_INTERNAL, "bitsum cells");
+        BitCell2* d_c2 = s.alloc<BitCell2>(ncell);
+        ZK_CUDA(cudaMemcpyAsync(d_c2, c2.data(), sizeof(BitCell2) * ncell, cudaMemcpyHostToDevice, ctx->stream));
+        Bitsum2Args b2;
+        memset(&b2, 0, sizeof b2);
+        b2.Z = Z;
+        b2.GA = GA;
+        b2.logD = logD;
+        b2.lo_bits = lo_bits;
+        b2.qr_mask = qr_mask;
+        b2.sig_bit = QR - 1;
+        for (int x = 0; x < 5; x++) {
+            b2.LO[x] = ba.LO[x];
+            b2.HI[x] = ba.HI[x];
+        }
+        b2.cells = d_c2;
+        b2.nM = 4 * B;
+        b2.nC = ncell - 4 * B;
+        const uint64_t nchunks = D / BS2_CH;
+        const uint32_t grid = (uint32_t)(nchunks < (uint64_t)ctx->num_sms * 2 ? nchunks : (uint64_t)ctx->num_sms * 2);
+        b2.partials = s.alloc<fr_t>((size_t)grid * ncell);
+        const size_t smem = sizeof(Bitsum2Smem);
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_bitsums2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ZK_LAUNCH(ctx, k_relu_bitsums2, grid, BS2_T, smem, b2);
+        ZK_LAUNCH(ctx, k_relu_bitsums_reduce, (ncell + 127) / 128, 128, 0, (const fr_t*)b2.partials, grid, ncell, cell_tot);
+    } else {           // tiny D: one masked lazy addition per (entry, cell)
+        uint32_t bs_threads = ((ncell + 1) / 2 + 31) / 32 * 32;
+        if (bs_threads > 640) bs_threads = 640;
+        uint64_t nchunks = D / (D < BS_CH ? D : BS_CH);
+        uint32_t bs_grid = (uint32_t)(nchunks < (uint64_t)ctx->num_sms * 2 ? nchunks : (uint64_t)ctx->num_sms * 2);
+        ba.partials = s.alloc<fr_t>((size_t)bs_grid * ncell);
+        size_t bs_smem = 5 * BS_CH * sizeof(fr_t) + 2 * BS_CH * 4 + BS_CH;
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_bitsums, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
+        ZK_REQUIRE(ncell <= 2 * bs_threads, ZK_ERR_INTERNAL, "bitsum cells exceed the block");
+        ZK_LAUNCH(ctx, k_relu_bitsums, bs_grid, bs_threads, bs_smem, ba);
+        ZK_LAUNCH(ctx, k_relu_bitsums_reduce, (ncell + 127) / 128, 128, 0, (const fr_t*)ba.partials, bs_grid, ncell,
+                  cell_tot);
+    }
 
     // ---- j-rounds
     const uint32_t nbytes = (B + 7) / 8;

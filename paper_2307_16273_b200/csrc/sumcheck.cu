@@ -99,46 +99,62 @@ __global__ void __launch_bounds__(256) k_sc_round(ScRoundArgs a) {
                 for (int k = 0; k < K; k++) v[k] = fr_add(v[k], d[k]);
         }
     }
-    fr_t tot[K + 1];
-    if (grid_reduce_fr<K + 1>(acc, a.partials, a.ticket, tot)) {
+    __shared__ fr_t tot[K + 1];
+    __shared__ FsScratch fs;
+    if (grid_reduce_fr_block<K + 1>(acc, a.partials, a.ticket, tot) && threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        fs_begin(fs, a.st);
         if (a.compute_claim) {
-            fr_t c;
-            if (a.t < a.n_eq) {
-                fr_t w0 = fr_load(&a.w[a.t]);
-                c = fr_add(fr_mul(fr_sub(fr_one(), w0), tot[0]), fr_mul(w0, tot[1]));
-            } else {
-                c = fr_add(tot[0], tot[1]);
+            __shared__ fr_t claim_sm;
+            if (lane == 0) {
+                fr_t c;
+                if (a.t < a.n_eq) {
+                    fr_t w0 = fr_load(&a.w[a.t]);
+                    c = fr_add(fr_mul(fr_sub(fr_one(), w0), tot[0]), fr_mul(w0, tot[1]));
+                } else {
+                    c = fr_add(tot[0], tot[1]);
+                }
+                fr_store(a.claim, c);
+                claim_sm = c;
             }
-            fr_store(a.claim, c);
-            tr_absorb_frs(a.st, "sc/claim", &c, 1, a.claim_bytes);
+            __syncwarp();
+            fs_absorb_frs(fs, "sc/claim", claim_sm, 1, a.claim_bytes);
         }
-        tr_absorb_frs(a.st, "sc/msg", tot, K + 1, a.msg_out);
-        fr_t rt = tr_challenge(a.st, "sc/r");
-        fr_store(a.r_out, rt);
-        fr_to_bytes(rt, a.point_out);
+        fs_absorb_frs(fs, "sc/msg", lane <= K ? tot[lane < K + 1 ? lane : 0] : fr_zero(), K + 1, a.msg_out);
+        fr_t rt = fs_challenge(fs, "sc/r");
+        if (lane == 0) {
+            fr_store(a.r_out, rt);
+            fr_canon_to_bytes(fs.rc, a.point_out);
+        }
+        fs_end(fs, a.st);
     }
 }
 
-// header (+ provided claim) before round 0
+// header (+ provided claim) before round 0; one warp
 __global__ void k_sc_header(uint8_t* st, Bytes256 hdr, const fr_t* claim, int absorb_claim, uint8_t* claim_bytes) {
-    tr_absorb(st, "sc/hdr", hdr.b, hdr.len);
-    if (absorb_claim) {
-        fr_t c = fr_load(claim);
-        tr_absorb_frs(st, "sc/claim", &c, 1, claim_bytes);
-    }
+    __shared__ FsScratch fs;
+    fs_begin(fs, st);
+    fs_absorb_bytes(fs, "sc/hdr", hdr.b, hdr.len);
+    if (absorb_claim) fs_absorb_frs(fs, "sc/claim", fr_load(claim), 1, claim_bytes);
+    fs_end(fs, st);
 }
 
-// finals T_k~(r) = T_k[0] + r_{m-1} (T_k[1] - T_k[0]) on the last 2-element tables
+// finals T_k~(r) = T_k[0] + r_{m-1} (T_k[1] - T_k[0]) on the last 2-element tables; one warp
 __global__ void k_sc_finals(const fr_t* t0, const fr_t* t1, const fr_t* t2, int K, const fr_t* r_last, uint8_t* st,
                             uint8_t* finals_bytes, fr_t* finals_mont) {
-    const fr_t* T[3] = {t0, t1, t2};
-    fr_t r = fr_load(r_last), f[3];
-    for (int k = 0; k < K; k++) {
-        fr_t a = fr_load(T[k]), b = fr_load(T[k] + 1);
-        f[k] = fr_add(a, fr_mul(r, fr_sub(b, a)));
-        if (finals_mont) fr_store(&finals_mont[k], f[k]);
+    __shared__ FsScratch fs;
+    const int lane = threadIdx.x & 31;
+    const fr_t* T = lane == 0 ? t0 : (lane == 1 ? t1 : t2);
+    fr_t f = fr_zero();
+    if (lane < K) {
+        fr_t r = fr_load(r_last);
+        fr_t a = fr_load(T), b = fr_load(T + 1);
+        f = fr_add(a, fr_mul(r, fr_sub(b, a)));
+        if (finals_mont) fr_store(&finals_mont[lane], f);
     }
-    tr_absorb_frs(st, "sc/final", f, K, finals_bytes);
+    fs_begin(fs, st);
+    fs_absorb_frs(fs, "sc/final", f, K, finals_bytes);
+    fs_end(fs, st);
 }
 
 template <int K>
@@ -160,7 +176,7 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
     for (int i = 0; i < 3; i++)
         for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
     ZK_CUDA(cudaMemcpyAsync(proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
-    ZK_LAUNCH(ctx, k_sc_header, 1, 1, 0, tr->d_st, make_bytes(hdr, 12), S.d_claim, S.claim_given ? 1 : 0, proof + 12);
+    ZK_LAUNCH(ctx, k_sc_header, 1, 32, 0, tr->d_st, make_bytes(hdr, 12), S.d_claim, S.claim_given ? 1 : 0, proof + 12);
 
     // eq split (only the suffix variables w_{t+1..n_eq-1} are ever needed)
     const uint32_t hb = n_eq >= 1 ? (n_eq - 1 < 10 ? n_eq - 1 : 10) : 0;
@@ -247,7 +263,7 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
         if (fold)
             for (uint32_t k = 0; k < K; k++) cur[k] = buf[t & 1][k];
     }
-    ZK_LAUNCH(ctx, k_sc_finals, 1, 1, 0, cur[0], K > 1 ? cur[1] : cur[0], K > 2 ? cur[2] : cur[0], (int)K,
+    ZK_LAUNCH(ctx, k_sc_finals, 1, 32, 0, cur[0], K > 1 ? cur[1] : cur[0], K > 2 ? cur[2] : cur[0], (int)K,
               S.d_r + (m - 1), tr->d_st, proof + 44 + 32ull * m * (K + 1), S.d_finals);
 }
 

@@ -1,74 +1,115 @@
 // transcript.cu — Fiat-Shamir transcript kernels and host wrappers (D3; row a6).
+// Every kernel here is launched with one warp (or a block whose warp 0 runs the transcript).
 #include "common.cuh"
 
 namespace zk {
 
-__global__ void k_tr_init(uint8_t* st, Bytes256 seed) { tr_init(st, seed.b); }
+__global__ void k_tr_init(uint8_t* st, Bytes256 seed) {
+    __shared__ uint32_t buf[32];
+    if (threadIdx.x == 0) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(buf);
+        const char* lbl = "zkdl-b200/v1/init";
+        uint32_t n = zk_strlen(lbl);
+        for (uint32_t i = 0; i < n; i++) b[i] = (uint8_t)lbl[i];
+        for (int i = 0; i < 32; i++) b[n + i] = seed.b[i];
+        uint32_t d[8];
+        sha256_buf(b, n + 32, d);
+        st_words_to_bytes(d, st);
+    }
+}
 
 __global__ void k_tr_absorb(uint8_t* st, Tag32 tag, Bytes256 msg) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) tr_absorb(st, tag.s, msg.b, msg.len);
+    __shared__ FsScratch s;
+    fs_begin(s, st);
+    fs_absorb_bytes(s, tag.s, msg.b, msg.len);
+    fs_end(s, st);
 }
 
+// long messages from device memory (lane 0 streams the blocks)
 __global__ void k_tr_absorb_dev(uint8_t* st, Tag32 tag, const uint8_t* msg, uint64_t len) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) tr_absorb(st, tag.s, msg, len);
-}
-
-__global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t n, uint8_t* copy_out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        Sha256 s;
-        tr_absorb_begin(s, st, tag.s, 32ull * n);
-        for (uint32_t i = 0; i < n; i++) {
-            uint8_t b[32];
-            fr_to_bytes(fr_load(&v[i]), b);
-            s.update(b, 32);
-            if (copy_out)
-                for (int k = 0; k < 32; k++) copy_out[32 * i + k] = b[k];
+    if (threadIdx.x != 0) return;
+    __shared__ uint32_t buf[32];
+    uint8_t* b = reinterpret_cast<uint8_t*>(buf);
+    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    // header
+    uint8_t hdr[80];
+    for (int i = 0; i < 32; i++) hdr[i] = st[i];
+    uint32_t tl = zk_strlen(tag.s);
+    hdr[32] = 0x01;
+    hdr[33] = (uint8_t)tl;
+    for (uint32_t i = 0; i < tl; i++) hdr[34 + i] = (uint8_t)tag.s[i];
+    for (int i = 0; i < 8; i++) hdr[34 + tl + i] = (uint8_t)(len >> (56 - 8 * i));
+    const uint64_t hl = 42 + tl, total = hl + len;
+    const uint64_t padded = (total + 9 + 63) & ~63ull;
+    for (uint64_t off = 0; off < padded; off += 64) {
+        for (int i = 0; i < 64; i++) {
+            uint64_t p = off + i;
+            uint8_t v;
+            if (p < hl) v = hdr[p];
+            else if (p < total) v = msg[p - hl];
+            else if (p == total) v = 0x80;
+            else if (p >= padded - 8) v = (uint8_t)((total * 8) >> (56 - 8 * (p - (padded - 8))));
+            else v = 0;
+            b[i] = v;
         }
-        s.final(st);
+        sha256_compress(h, buf);
     }
+    st_words_to_bytes(h, st);
 }
 
-// Squeeze x = LE512(SHA256(st||0) || SHA256(st||1)) mod p for one challenge state.
-__device__ fr_t squeeze_from_state(const uint8_t* st) {
-    Sha256 s;
-    uint8_t h[64];
+// n <= 8 field elements from device memory (Montgomery)
+__global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t n, uint8_t* copy_out) {
+    __shared__ FsScratch s;
+    const int lane = threadIdx.x & 31;
+    fs_begin(s, st);
+    fr_t mine = lane < (int)n ? fr_load(&v[lane]) : fr_zero();
+    fs_absorb_frs(s, tag.s, mine, (int)n, copy_out);
+    fs_end(s, st);
+}
+
+// Squeeze x = LE512(SHA256(st||0) || SHA256(st||1)) mod p for one challenge state (one thread).
+__device__ void squeeze_from_state(const uint8_t* st, uint32_t* scratch /* 32 words */, fr_t& mont, fr_t& canon) {
+    uint8_t* b = reinterpret_cast<uint8_t*>(scratch);
+    fr_t half[2];
     for (int k = 0; k < 2; k++) {
-        s.init();
-        s.update(st, 32);
-        s.update_byte((uint8_t)k);
-        s.final(h + 32 * k);
+        for (int i = 0; i < 32; i++) b[i] = st[i];
+        b[32] = (uint8_t)k;
+        uint32_t d[8];
+        sha256_buf(b, 33, d);
+        for (int i = 0; i < 8; i++) half[k].v[i] = bswap32(d[i]);
     }
-    fr_t lo, hi;
-    for (int i = 0; i < 8; i++) {
-        lo.v[i] = (uint32_t)h[4 * i] | ((uint32_t)h[4 * i + 1] << 8) | ((uint32_t)h[4 * i + 2] << 16) |
-                  ((uint32_t)h[4 * i + 3] << 24);
-        hi.v[i] = (uint32_t)h[32 + 4 * i] | ((uint32_t)h[33 + 4 * i] << 8) | ((uint32_t)h[34 + 4 * i] << 16) |
-                  ((uint32_t)h[35 + 4 * i] << 24);
-    }
-    return fr_add(fr_mul(ZK_R2, lo), fr_mul(ZK_R3, hi));
+    mont = fr_add(fr_mul(ZK_R2, half[0]), fr_mul(ZK_R3, half[1]));
+    canon = fr_add(fr_reduce_once(fr_reduce_once(half[0])), fr_mul(ZK_R2, half[1]));
 }
 
-// blockDim.x >= 1; n <= 256 per launch (the host splits larger requests)
+// n challenges with one tag: lane 0 advances the state chain, all threads squeeze in parallel.
+// blockDim.x >= 32; n <= 256 per launch (the host splits larger requests)
 __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mont, uint8_t* out_canon) {
     __shared__ uint8_t states[256][32];
+    __shared__ uint32_t scratch[256][32];
     if (threadIdx.x == 0) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(scratch[0]);
         uint32_t tl = zk_strlen(tag.s);
+        uint8_t cur[32];
+        for (int i = 0; i < 32; i++) cur[i] = st[i];
         for (uint32_t i = 0; i < n; i++) {
-            Sha256 s;
-            s.init();
-            s.update(st, 32);
-            s.update_byte(0x02);
-            s.update_byte((uint8_t)tl);
-            s.update((const uint8_t*)tag.s, tl);
-            s.final(st);
-            for (int k = 0; k < 32; k++) states[i][k] = st[k];
+            for (int k = 0; k < 32; k++) b[k] = cur[k];
+            b[32] = 0x02;
+            b[33] = (uint8_t)tl;
+            for (uint32_t k = 0; k < tl; k++) b[34 + k] = (uint8_t)tag.s[k];
+            uint32_t d[8];
+            sha256_buf(b, 34 + tl, d);
+            st_words_to_bytes(d, cur);
+            for (int k = 0; k < 32; k++) states[i][k] = cur[k];
         }
+        for (int i = 0; i < 32; i++) st[i] = cur[i];
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        fr_t x = squeeze_from_state(states[i]);
+        fr_t x, c;
+        squeeze_from_state(states[i], scratch[threadIdx.x], x, c);
         if (out_mont) fr_store(&out_mont[i], x);
-        if (out_canon) fr_to_bytes(x, out_canon + 32 * i);
+        if (out_canon) fr_canon_to_bytes(c, out_canon + 32 * i);
     }
 }
 
@@ -90,13 +131,14 @@ void tr_challenges_dev(zk_transcript* tr, const char* tag, uint32_t n, fr_t* d_o
     Tag32 t = make_tag(tag);
     for (uint32_t off = 0; off < n; off += 256) {
         uint32_t c = n - off < 256 ? n - off : 256;
-        ZK_LAUNCH(ctx, k_tr_challenges, 1, 256, 0, tr->d_st, t, c, d_out_mont ? d_out_mont + off : nullptr,
+        uint32_t threads = (c + 31) / 32 * 32;
+        ZK_LAUNCH(ctx, k_tr_challenges, 1, threads, 0, tr->d_st, t, c, d_out_mont ? d_out_mont + off : nullptr,
                   d_out_canon ? d_out_canon + 32 * (size_t)off : nullptr);
     }
 }
 
 void tr_init_dev(zk_transcript* tr, const uint8_t seed[32]) {
-    ZK_LAUNCH(tr->ctx, k_tr_init, 1, 1, 0, tr->d_st, make_bytes(seed, 32));
+    ZK_LAUNCH(tr->ctx, k_tr_init, 1, 32, 0, tr->d_st, make_bytes(seed, 32));
 }
 
 }  // namespace zk

@@ -7,7 +7,13 @@
 //   absorb(tag, m) : st = SHA256(st || 0x01 || u8(|tag|) || tag || u64be(|m|) || m)
 //   challenge(tag) : st = SHA256(st || 0x02 || u8(|tag|) || tag)
 //                    x  = LE512(SHA256(st || 0x00) || SHA256(st || 0x01)) mod p
-// All functions here run on ONE thread (the finalizing thread of a kernel).
+//
+// Latency matters (one transcript step per sumcheck round), so the step runs on one WARP of the
+// finalizing block: messages are assembled in shared memory and hashed word-wise with the round
+// function fully unrolled in registers; the field elements of a message are canonicalised by
+// parallel lanes; the two squeeze hashes and the four half-reductions of the 512-bit challenge
+// run on separate lanes.  x = lo + hi 2^256:  mont(x) = mont_mul(R^2, lo) + mont_mul(R^3, hi),
+// canonical(x) = (lo mod p) + mont_mul(R^2, hi).
 #pragma once
 #include "fr.cuh"
 
@@ -23,79 +29,68 @@ __device__ __constant__ static const uint32_t SHA_K[64] = {
     0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
     0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
 
-struct Sha256 {
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+__device__ __forceinline__ uint32_t ror32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+struct Sha8 {
     uint32_t h[8];
-    uint8_t buf[64];
-    uint32_t nbuf;
-    uint64_t len;
+};
 
-    __device__ __forceinline__ static uint32_t ror(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
-
-    __device__ void init() {
-        h[0] = 0x6a09e667; h[1] = 0xbb67ae85; h[2] = 0x3c6ef372; h[3] = 0xa54ff53a;
-        h[4] = 0x510e527f; h[5] = 0x9b05688c; h[6] = 0x1f83d9ab; h[7] = 0x5be0cd19;
-        nbuf = 0;
-        len = 0;
-    }
-    __device__ void block(const uint8_t* p) {
-        uint32_t w[16];
+// One compression of a 64-byte block given as 16 little-endian-loaded words (byte-swapped here).
+// Out of line and rolled 4 x 16 rounds: the transcript runs on cold code paths (see fr_mul_cold).
+static __device__ __noinline__ Sha8 sha256_compress_s(Sha8 s, const uint32_t* blk) {
+    uint32_t w[16];
 #pragma unroll
-        for (int i = 0; i < 16; i++)
-            w[i] = ((uint32_t)p[4 * i] << 24) | ((uint32_t)p[4 * i + 1] << 16) | ((uint32_t)p[4 * i + 2] << 8) | p[4 * i + 3];
-        uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    for (int i = 0; i < 16; i++) w[i] = bswap32(blk[i]);
+    uint32_t a = s.h[0], b = s.h[1], c = s.h[2], d = s.h[3], e = s.h[4], f = s.h[5], g = s.h[6], hh = s.h[7];
+#pragma unroll 1
+    for (int j = 0; j < 64; j += 16) {
 #pragma unroll
-        for (int i = 0; i < 64; i++) {
+        for (int i = 0; i < 16; i++) {
             uint32_t wi;
-            if (i < 16) {
+            if (j == 0) {
                 wi = w[i];
             } else {
-                uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
-                uint32_t s0 = ror(w15, 7) ^ ror(w15, 18) ^ (w15 >> 3);
-                uint32_t s1 = ror(w2, 17) ^ ror(w2, 19) ^ (w2 >> 10);
-                wi = w[i & 15] + s0 + w[(i - 7) & 15] + s1;
-                w[i & 15] = wi;
+                const uint32_t w15 = w[(i + 1) & 15], w2 = w[(i + 14) & 15];
+                const uint32_t s0 = ror32(w15, 7) ^ ror32(w15, 18) ^ (w15 >> 3);
+                const uint32_t s1 = ror32(w2, 17) ^ ror32(w2, 19) ^ (w2 >> 10);
+                wi = w[i] + s0 + w[(i + 9) & 15] + s1;
+                w[i] = wi;
             }
-            uint32_t S1 = ror(e, 6) ^ ror(e, 11) ^ ror(e, 25);
-            uint32_t ch = (e & f) ^ (~e & g);
-            uint32_t t1 = hh + S1 + ch + SHA_K[i] + wi;
-            uint32_t S0 = ror(a, 2) ^ ror(a, 13) ^ ror(a, 22);
-            uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
-            uint32_t t2 = S0 + mj;
-            hh = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
-        }
-        h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
-    }
-    __device__ void update(const uint8_t* p, uint64_t n) {
-        len += n;
-        while (n) {
-            uint32_t take = 64 - nbuf;
-            if (take > n) take = (uint32_t)n;
-            for (uint32_t i = 0; i < take; i++) buf[nbuf + i] = p[i];
-            nbuf += take;
-            p += take;
-            n -= take;
-            if (nbuf == 64) {
-                block(buf);
-                nbuf = 0;
-            }
+            const uint32_t S1 = ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25);
+            const uint32_t ch = (e & f) ^ (~e & g);
+            const uint32_t t1 = hh + S1 + ch + SHA_K[j + i] + wi;
+            const uint32_t S0 = ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22);
+            const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+            hh = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
         }
     }
-    __device__ void update_byte(uint8_t b) { update(&b, 1); }
-    __device__ void final(uint8_t out[32]) {
-        uint64_t bits = len * 8;
-        update_byte(0x80);
-        while (nbuf != 56) update_byte(0);
-        uint8_t lb[8];
-        for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(bits >> (56 - 8 * i));
-        update(lb, 8);
-        for (int i = 0; i < 8; i++) {
-            out[4 * i] = (uint8_t)(h[i] >> 24);
-            out[4 * i + 1] = (uint8_t)(h[i] >> 16);
-            out[4 * i + 2] = (uint8_t)(h[i] >> 8);
-            out[4 * i + 3] = (uint8_t)h[i];
-        }
-    }
-};
+    s.h[0] += a; s.h[1] += b; s.h[2] += c; s.h[3] += d; s.h[4] += e; s.h[5] += f; s.h[6] += g; s.h[7] += hh;
+    return s;
+}
+__device__ __forceinline__ void sha256_compress(uint32_t h[8], const uint32_t* blk) {
+    Sha8 s;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s.h[i] = h[i];
+    s = sha256_compress_s(s, blk);
+#pragma unroll
+    for (int i = 0; i < 8; i++) h[i] = s.h[i];
+}
+
+// SHA-256 of n bytes held in a 4-byte-aligned buffer with room for the padding
+// (capacity >= round_up(n + 9, 64)); the buffer is padded in place.  out: digest words (BE values).
+__device__ inline void sha256_buf(uint8_t* buf, uint32_t n, uint32_t out[8]) {
+    uint32_t total = (n + 9 + 63) & ~63u;
+    buf[n] = 0x80;
+    for (uint32_t i = n + 1; i < total - 8; i++) buf[i] = 0;
+    const uint64_t bits = (uint64_t)n * 8;
+    for (int i = 0; i < 8; i++) buf[total - 8 + i] = (uint8_t)(bits >> (56 - 8 * i));
+    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf);
+    for (uint32_t blk = 0; blk < total / 64; blk++) sha256_compress(h, wp + 16 * blk);
+#pragma unroll
+    for (int i = 0; i < 8; i++) out[i] = h[i];
+}
 
 __device__ __forceinline__ uint32_t zk_strlen(const char* s) {
     uint32_t n = 0;
@@ -103,9 +98,27 @@ __device__ __forceinline__ uint32_t zk_strlen(const char* s) {
     return n;
 }
 
+// digest words <-> the 32 state bytes
+__device__ __forceinline__ void st_words_to_bytes(const uint32_t w[8], uint8_t* out) {
+    for (int i = 0; i < 8; i++) {
+        out[4 * i] = (uint8_t)(w[i] >> 24);
+        out[4 * i + 1] = (uint8_t)(w[i] >> 16);
+        out[4 * i + 2] = (uint8_t)(w[i] >> 8);
+        out[4 * i + 3] = (uint8_t)w[i];
+    }
+}
+
 // Canonical 32-byte little-endian encoding of a Montgomery element.
-__device__ inline void fr_to_bytes(const fr_t& a, uint8_t out[32]) {
-    fr_t c = fr_to_canonical(a);
+__device__ inline void fr_to_bytes(const fr_t& a, uint8_t* out) {
+    fr_t c = fr_to_canonical_cold(a);
+    for (int i = 0; i < 8; i++) {
+        out[4 * i] = (uint8_t)c.v[i];
+        out[4 * i + 1] = (uint8_t)(c.v[i] >> 8);
+        out[4 * i + 2] = (uint8_t)(c.v[i] >> 16);
+        out[4 * i + 3] = (uint8_t)(c.v[i] >> 24);
+    }
+}
+__device__ inline void fr_canon_to_bytes(const fr_t& c, uint8_t* out) {
     for (int i = 0; i < 8; i++) {
         out[4 * i] = (uint8_t)c.v[i];
         out[4 * i + 1] = (uint8_t)(c.v[i] >> 8);
@@ -114,74 +127,124 @@ __device__ inline void fr_to_bytes(const fr_t& a, uint8_t out[32]) {
     }
 }
 
-__device__ inline void tr_init(uint8_t* st, const uint8_t seed[32]) {
-    Sha256 s;
-    s.init();
-    const char* lbl = "zkdl-b200/v1/init";
-    s.update((const uint8_t*)lbl, zk_strlen(lbl));
-    s.update(seed, 32);
-    s.final(st);
+// ---------------------------------------------------------------- warp-cooperative transcript steps
+// Shared scratch of one finalizing warp.
+struct FsScratch {
+    uint32_t buf[2][80];   // two 320-byte message buffers
+    uint8_t st[32];        // current state bytes
+    fr_t part[4];
+    fr_t r;
+    fr_t rc;               // canonical r
+};
+
+// lane 0 copies the global state in / out
+__device__ __forceinline__ void fs_begin(FsScratch& s, const uint8_t* st_g) {
+    if ((threadIdx.x & 31) == 0)
+        for (int i = 0; i < 32; i++) s.st[i] = st_g[i];
+    __syncwarp();
+}
+__device__ __forceinline__ void fs_end(FsScratch& s, uint8_t* st_g) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0)
+        for (int i = 0; i < 32; i++) st_g[i] = s.st[i];
+    __syncwarp();
 }
 
-__device__ inline void tr_absorb_begin(Sha256& s, const uint8_t* st, const char* tag, uint64_t len) {
-    s.init();
-    s.update(st, 32);
-    s.update_byte(0x01);
+// header of an absorb: st || 0x01 || u8(|tag|) || tag || u64be(len); returns its length
+__device__ inline uint32_t fs_absorb_header(FsScratch& s, uint8_t* b, const char* tag, uint64_t len) {
+    for (int i = 0; i < 32; i++) b[i] = s.st[i];
     uint32_t tl = zk_strlen(tag);
-    s.update_byte((uint8_t)tl);
-    s.update((const uint8_t*)tag, tl);
-    uint8_t lb[8];
-    for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(len >> (56 - 8 * i));
-    s.update(lb, 8);
+    b[32] = 0x01;
+    b[33] = (uint8_t)tl;
+    for (uint32_t i = 0; i < tl; i++) b[34 + i] = (uint8_t)tag[i];
+    for (int i = 0; i < 8; i++) b[34 + tl + i] = (uint8_t)(len >> (56 - 8 * i));
+    return 42 + tl;
 }
 
-__device__ inline void tr_absorb(uint8_t* st, const char* tag, const uint8_t* msg, uint64_t len) {
-    Sha256 s;
-    tr_absorb_begin(s, st, tag, len);
-    s.update(msg, len);
-    s.final(st);
-}
-
-// absorb n field elements (Montgomery in registers/memory) as canonical LE bytes
-__device__ inline void tr_absorb_frs(uint8_t* st, const char* tag, const fr_t* v, int n, uint8_t* copy_out = nullptr) {
-    Sha256 s;
-    tr_absorb_begin(s, st, tag, 32ull * n);
-    for (int i = 0; i < n; i++) {
-        uint8_t b[32];
-        fr_to_bytes(v[i], b);
-        s.update(b, 32);
+// Absorb n <= 8 field elements; lane l < n contributes `mine` (Montgomery).  The canonical bytes are
+// also written to copy_out (global, may be null).  All 32 lanes of the warp must call.
+__device__ inline void fs_absorb_frs(FsScratch& s, const char* tag, const fr_t& mine, int n, uint8_t* copy_out) {
+    const int lane = threadIdx.x & 31;
+    uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[0]);
+    __shared__ uint32_t hlen_sm;
+    if (lane == 0) hlen_sm = fs_absorb_header(s, b, tag, 32ull * n);
+    __syncwarp();
+    const uint32_t hl = hlen_sm;
+    if (lane < n) {
+        uint8_t tmp[32];
+        fr_to_bytes(mine, tmp);
+        for (int k = 0; k < 32; k++) b[hl + 32 * lane + k] = tmp[k];
         if (copy_out)
-            for (int k = 0; k < 32; k++) copy_out[32 * i + k] = b[k];
+            for (int k = 0; k < 32; k++) copy_out[32 * lane + k] = tmp[k];
     }
-    s.final(st);
+    __syncwarp();
+    if (lane == 0) {
+        uint32_t d[8];
+        sha256_buf(b, hl + 32 * n, d);
+        st_words_to_bytes(d, s.st);
+    }
+    __syncwarp();
 }
 
-// challenge: returns the Montgomery form of the squeezed element
-__device__ inline fr_t tr_challenge(uint8_t* st, const char* tag) {
-    Sha256 s;
-    s.init();
-    s.update(st, 32);
-    s.update_byte(0x02);
-    uint32_t tl = zk_strlen(tag);
-    s.update_byte((uint8_t)tl);
-    s.update((const uint8_t*)tag, tl);
-    s.final(st);
-    uint8_t h[64];
-    for (int k = 0; k < 2; k++) {
-        s.init();
-        s.update(st, 32);
-        s.update_byte((uint8_t)k);
-        s.final(h + 32 * k);
+// Absorb raw bytes (lane 0 only does the work; all lanes call).  len <= 256.
+__device__ inline void fs_absorb_bytes(FsScratch& s, const char* tag, const uint8_t* msg, uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[0]);
+        uint32_t hl = fs_absorb_header(s, b, tag, len);
+        for (uint32_t i = 0; i < len; i++) b[hl + i] = msg[i];
+        uint32_t d[8];
+        sha256_buf(b, hl + len, d);
+        st_words_to_bytes(d, s.st);
     }
-    // x = lo + hi * 2^256 with lo, hi < 2^256;  mont(x) = lo*R + hi*R^2 = mont_mul(R2, lo) + mont_mul(R3, hi)
-    fr_t lo, hi;
-    for (int i = 0; i < 8; i++) {
-        lo.v[i] = (uint32_t)h[4 * i] | ((uint32_t)h[4 * i + 1] << 8) | ((uint32_t)h[4 * i + 2] << 16) |
-                  ((uint32_t)h[4 * i + 3] << 24);
-        hi.v[i] = (uint32_t)h[32 + 4 * i] | ((uint32_t)h[32 + 4 * i + 1] << 8) | ((uint32_t)h[32 + 4 * i + 2] << 16) |
-                  ((uint32_t)h[32 + 4 * i + 3] << 24);
+    __syncwarp();
+}
+
+// lane 0: the challenge state update; lanes 0/1: the two squeeze hashes; lanes 0-3: the four
+// half-reductions.  Returns the Montgomery challenge on every lane (and s.rc = canonical).
+__device__ inline fr_t fs_challenge(FsScratch& s, const char* tag) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[0]);
+        for (int i = 0; i < 32; i++) b[i] = s.st[i];
+        uint32_t tl = zk_strlen(tag);
+        b[32] = 0x02;
+        b[33] = (uint8_t)tl;
+        for (uint32_t i = 0; i < tl; i++) b[34 + i] = (uint8_t)tag[i];
+        uint32_t d[8];
+        sha256_buf(b, 34 + tl, d);
+        st_words_to_bytes(d, s.st);
     }
-    return fr_add(fr_mul(ZK_R2, lo), fr_mul(ZK_R3, hi));
+    __syncwarp();
+    __shared__ fr_t half[2];
+    if (lane < 2) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[lane]);
+        for (int i = 0; i < 32; i++) b[i] = s.st[i];
+        b[32] = (uint8_t)lane;
+        uint32_t d[8];
+        sha256_buf(b, 33, d);
+        // digest bytes are d[i] big-endian; as a little-endian 256-bit integer limb i = bytes 4i..4i+3
+        fr_t x;
+        for (int i = 0; i < 8; i++) x.v[i] = bswap32(d[i]);
+        half[lane] = x;   // lane 0: lo, lane 1: hi
+    }
+    __syncwarp();
+    if (lane < 4) {
+        const fr_t lo = half[0], hi = half[1];
+        fr_t v;
+        if (lane == 0) v = fr_mul_cold(ZK_R2, lo);          // mont part of lo
+        else if (lane == 1) v = fr_mul_cold(ZK_R3, hi);     // mont part of hi * 2^256
+        else if (lane == 2) v = fr_mul_cold(ZK_R2, hi);     // canonical hi * 2^256 mod p
+        else v = fr_reduce_once(fr_reduce_once(lo));   // canonical lo mod p (lo < 2^256 < 3p)
+        s.part[lane] = v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        s.r = fr_add(s.part[0], s.part[1]);
+        s.rc = fr_add(s.part[2], s.part[3]);
+    }
+    __syncwarp();
+    return s.r;
 }
 
 // Lagrange interpolation of the degree-d polynomial with values e[0..d] at 0..d, evaluated at x (d <= 3).
@@ -197,13 +260,13 @@ __device__ inline fr_t interp_small(const fr_t* e, int d, const fr_t& x) {
         int den = 1;
         for (int j = 0; j <= d; j++) {
             if (j == i) continue;
-            num = fr_mul(num, xm[j]);
+            num = fr_mul_cold(num, xm[j]);
             den *= (i - j);
         }
         int ad = den < 0 ? -den : den;
-        fr_t term = fr_mul(e[i], num);
-        if (ad == 2) term = fr_mul(term, ZK_INV2);
-        else if (ad == 6) term = fr_mul(term, ZK_INV6);
+        fr_t term = fr_mul_cold(e[i], num);
+        if (ad == 2) term = fr_mul_cold(term, ZK_INV2);
+        else if (ad == 6) term = fr_mul_cold(term, ZK_INV6);
         acc = den < 0 ? fr_sub(acc, term) : fr_add(acc, term);
     }
     return acc;
