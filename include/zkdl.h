@@ -120,6 +120,34 @@ zk_status zk_sumcheck_prove(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt* 
                             const zk_fr* claim, zk_fr* claim_out, uint8_t* proof, uint64_t* proof_len,
                             zk_fr* point_out, zk_fr* finals_out);
 
+/* ------------------------------------------- sharded product sumcheck (SURVEY §8(e), G = 2^s devices)
+ * Rank g (of world = G, a power of two) holds entries [g 2^L, (g+1) 2^L) of every table, L = m - s:
+ * the top s index bits (the last-bound variables, D2) are the rank id, so every round pair is local.
+ * Protocol per round, driven by the caller:
+ *   zk_sc_shard_partial(sh, d_part)  — this rank's K+1 partial evaluations (32-byte internal-form
+ *                                      elements, already scaled by the rank's eq factor) into d_part;
+ *   caller all-gathers the G partials in rank order into d_all (NCCL all_gather, G*(K+1)*32 bytes);
+ *   zk_sc_shard_finish(sh, d_all)    — adds them mod p and runs the transcript step (identical on
+ *                                      every rank, so no broadcast of challenges is needed).
+ * When zk_sc_shard_local_log(sh) reaches the caller's threshold (or right away), zk_sc_shard_export
+ * writes the K folded local tables ([K][2^local_log] elements), the caller all-gathers them
+ * ([G][K][2^local_log]) and zk_sc_shard_adopt finishes every remaining round and the finals on each rank.
+ * The transcript, proof bytes and point equal zk_sumcheck_prove's on the full tables for every G
+ * (D3c).  zk_sc_shard_result copies them out (synchronises); all other calls are asynchronous.
+ * d_local_tables follow zk_prod_stmt's i32_mask convention; claim as in zk_sumcheck_prove. */
+typedef struct zk_sc_shard zk_sc_shard;
+zk_status zk_sc_shard_create(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt* st, void* const* d_local_tables,
+                             const zk_fr* claim, uint32_t rank, uint32_t world, zk_sc_shard** out);
+zk_status zk_sc_shard_partial(zk_sc_shard* sh, void* d_part);
+zk_status zk_sc_shard_finish(zk_sc_shard* sh, const void* d_all);
+uint32_t zk_sc_shard_rounds_done(const zk_sc_shard* sh);
+uint32_t zk_sc_shard_local_log(const zk_sc_shard* sh);
+zk_status zk_sc_shard_export(zk_sc_shard* sh, void* d_out);
+zk_status zk_sc_shard_adopt(zk_sc_shard* sh, const void* d_full);
+zk_status zk_sc_shard_result(zk_sc_shard* sh, uint8_t* proof, uint64_t* proof_len, zk_fr* point_out, zk_fr* finals_out,
+                             zk_fr* claim_out);
+void zk_sc_shard_free(zk_sc_shard* sh);
+
 /* ----------------------------------------------------- zkReLU (rows a7, a8; Sec. 3, App. A)
  * zk_relu_tables (row a7): from Z, G_A (int32, D entries, Q+R <= 32 bits) writes
  *   sign = 1{Z < 0} (u8, D10), A = (1 - sign) Z', G_Z = (1 - sign) G_A' with Z' = round(Z / 2^R),

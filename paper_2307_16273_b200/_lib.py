@@ -69,6 +69,15 @@ def lib():
         "zk_sumcheck_prove": ([vp, vp, c.POINTER(ProdStmt), vp, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_relu_tables": ([vp, vp, vp, u64, u32, u32, vp, vp, vp, vp, vp, vp, vp], i32),
         "zk_relu_prove": ([vp, vp, vp, vp, u32, u32, u32, vp, c.POINTER(u64), vp, vp, vp], i32),
+        "zk_sc_shard_create": ([vp, vp, c.POINTER(ProdStmt), vp, vp, u32, u32, c.POINTER(vp)], i32),
+        "zk_sc_shard_partial": ([vp, vp], i32),
+        "zk_sc_shard_finish": ([vp, vp], i32),
+        "zk_sc_shard_rounds_done": ([vp], u32),
+        "zk_sc_shard_local_log": ([vp], u32),
+        "zk_sc_shard_export": ([vp, vp], i32),
+        "zk_sc_shard_adopt": ([vp, vp], i32),
+        "zk_sc_shard_result": ([vp, vp, c.POINTER(u64), vp, vp, vp], i32),
+        "zk_sc_shard_free": ([vp], None),
         "zk_diag_fr_op": ([vp, i32, vp, vp, u64, vp], i32),
         "zk_diag_mul_bench": ([vp, vp, u32, u32, vp], i32),
     }
@@ -85,4 +94,4 @@ def declared_symbols(header: str | None = None) -> list:
     import re
     header = header or os.path.join(os.path.dirname(HERE), "include", "zkdl.h")
     txt = open(header).read()
-    return sorted(set(re.findall(r"^\s*(?:zk_status|void|const char\*|uint64_t)\s+(zk_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:zk_status|void|const char\*|uint64_t|uint32_t)\s+(zk_\w+)\s*\(", txt, re.M)))

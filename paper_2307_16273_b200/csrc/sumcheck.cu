@@ -42,6 +42,8 @@ struct ScRoundArgs {
     uint8_t* msg_out;        // canonical message bytes in the proof
     fr_t* r_out;             // r_t (Montgomery)
     uint8_t* point_out;      // r_t canonical
+    fr_t* part_out;          // sharded mode: write the (scaled) K+1 totals here instead of the transcript step
+    const fr_t* scale;       // sharded mode: the rank's eq factor over its high bits (nullptr = 1)
 };
 
 template <int K, bool FOLD>
@@ -103,6 +105,14 @@ __global__ void __launch_bounds__(256) k_sc_round(ScRoundArgs a) {
     __shared__ FsScratch fs;
     if (grid_reduce_fr_block<K + 1>(acc, a.partials, a.ticket, tot) && threadIdx.x < 32) {
         const int lane = threadIdx.x;
+        if (a.part_out) {
+            if (lane <= K) {
+                fr_t v = tot[lane & 3];
+                if (a.scale) v = fr_mul_cold(v, fr_load(a.scale));
+                fr_store(&a.part_out[lane], v);
+            }
+            return;
+        }
         fs_begin(fs, a.st);
         if (a.compute_claim) {
             __shared__ fr_t claim_sm;
@@ -157,6 +167,47 @@ __global__ void k_sc_finals(const fr_t* t0, const fr_t* t1, const fr_t* t2, int 
     fs_end(fs, st);
 }
 
+
+// Sum the G rank partials (rank order) and run the transcript step of round t (sharded mode, §8(e));
+// one warp.  all: G x (K+1) Montgomery elements.
+__global__ void k_sc_combine(const fr_t* all, uint32_t G, int K, uint32_t t, uint32_t n_eq, const fr_t* w, fr_t* claim,
+                             int compute_claim, uint8_t* st, uint8_t* claim_bytes, uint8_t* msg_out, fr_t* r_out,
+                             uint8_t* point_out) {
+    __shared__ FsScratch fs;
+    __shared__ fr_t tot[4];
+    const int lane = threadIdx.x & 31;
+    if (lane <= K) {
+        fr_t v = fr_zero();
+        for (uint32_t g = 0; g < G; g++) v = fr_add(v, fr_load(&all[(size_t)g * (K + 1) + lane]));
+        tot[lane] = v;
+    }
+    __syncwarp();
+    fs_begin(fs, st);
+    if (compute_claim) {
+        __shared__ fr_t claim_sm;
+        if (lane == 0) {
+            fr_t c;
+            if (t < n_eq) {
+                fr_t w0 = fr_load(&w[t]);
+                c = fr_add(fr_mul_cold(fr_sub(fr_one(), w0), tot[0]), fr_mul_cold(w0, tot[1]));
+            } else {
+                c = fr_add(tot[0], tot[1]);
+            }
+            fr_store(claim, c);
+            claim_sm = c;
+        }
+        __syncwarp();
+        fs_absorb_frs(fs, "sc/claim", claim_sm, 1, claim_bytes);
+    }
+    fs_absorb_frs(fs, "sc/msg", lane <= K ? tot[lane & 3] : fr_zero(), K + 1, msg_out);
+    fr_t rt = fs_challenge(fs, "sc/r");
+    if (lane == 0) {
+        fr_store(r_out, rt);
+        fr_canon_to_bytes(fs.rc, point_out);
+    }
+    fs_end(fs, st);
+}
+
 template <int K>
 static void launch_round(zk_ctx* ctx, bool fold, unsigned int grid, const ScRoundArgs& a) {
     if (fold)
@@ -165,106 +216,143 @@ static void launch_round(zk_ctx* ctx, bool fold, unsigned int grid, const ScRoun
         ZK_LAUNCH(ctx, (k_sc_round<K, false>), grid, 256, 0, a);
 }
 
-void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
-    const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
-    ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
-    const uint64_t N = 1ull << m;
-    uint8_t* proof = S.d_proof;
-    // header bytes
+// ---------------------------------------------------------------- engine
+void ScEngine::setup(const fr_t* const tables[3], uint32_t L_, uint32_t t0_, uint32_t n_eq_loc_) {
+    L = L_;
+    t0 = t0_;
+    t = t0_;
+    n_eq_loc = n_eq_loc_;
+    const uint64_t N = 1ull << L;
+    for (uint32_t k = 0; k < 3; k++) cur[k] = k < K ? tables[k] : nullptr;
+    for (uint32_t k = 0; k < K; k++) {
+        buf[1][k] = L >= 1 ? s->alloc<fr_t>(N >> 1) : nullptr;
+        buf[0][k] = L >= 2 ? s->alloc<fr_t>(N >> 2) : nullptr;
+    }
+    // suffix eq tables over w[t0+1 .. t0+n_eq_loc-1]: LO (pair-summed in the round kernel) x HI (<= 10 vars)
+    HI = LO[0] = LO[1] = HP[0] = HP[1] = nullptr;
+    hb = n_eq_loc >= 1 ? (n_eq_loc - 1 < 10 ? n_eq_loc - 1 : 10) : 0;
+    lo0 = n_eq_loc >= 1 ? n_eq_loc - 1 - hb : 0;
+    if (n_eq_loc >= 2) {
+        HI = s->alloc<fr_t>(1ull << hb);
+        eq_table_dev(ctx, d_w + t0 + 1 + lo0, hb, nullptr, HI, *s);
+        if (lo0) {
+            LO[0] = s->alloc<fr_t>(1ull << lo0);
+            LO[1] = s->alloc<fr_t>(1ull << (lo0 - 1));
+            eq_table_dev(ctx, d_w + t0 + 1, lo0, nullptr, LO[0], *s);
+        }
+        HP[0] = s->alloc<fr_t>(1ull << hb);
+        HP[1] = s->alloc<fr_t>(1ull << hb);
+    }
+    lo_level = 0;
+    hp_next = 0;
+    hi_cur = HI;
+    if (!partials) {
+        partials = s->alloc<fr_t>((size_t)ctx->num_sms * 4 * 4);
+        ticket = s->alloc_zero<unsigned int>(1);
+    }
+}
+
+void ScEngine::round(fr_t* part_out) {
+    const uint32_t tl = t - t0;
+    ZK_REQUIRE(tl < L, ZK_ERR_INTERNAL, "sumcheck engine: no rounds left");
+    ScRoundArgs a;
+    memset(&a, 0, sizeof a);
+    const bool fold = tl > 0;
+    const uint64_t n_pairs = 1ull << (L - tl - 1);
+    for (uint32_t k = 0; k < K; k++) {
+        a.src[k] = cur[k];
+        a.dst[k] = fold ? buf[tl & 1][k] : nullptr;
+    }
+    a.n_pairs = n_pairs;
+    a.r_prev = fold ? d_r + (t - 1) : nullptr;
+    const uint32_t n_eq_end = t0 + n_eq_loc;
+    if (t < n_eq_end && n_eq_end - t - 1 >= 1) {
+        const uint32_t nv = n_eq_end - t - 1;
+        const uint32_t lo_cnt = nv > hb ? nv - hb : 0;
+        if (lo_cnt >= 1) {
+            a.eq_mode = 1;
+            a.eq_cur = LO[lo_level];
+            a.eq_hi = HI;
+            a.eq_next = LO[lo_level ^ 1];
+            a.lo_cnt = lo_cnt;
+            a.hb = hb;
+        } else {
+            a.eq_mode = 2;
+            a.eq_cur = hi_cur;
+            a.eq_next = HP[hp_next];
+            a.lo_cnt = nv;
+        }
+    }
+    a.partials = partials;
+    a.ticket = ticket;
+    a.st = tr->d_st;
+    a.t = t;
+    a.n_eq = n_eq;
+    a.w = d_w;
+    a.claim = d_claim;
+    a.compute_claim = (t == 0 && !claim_given) ? 1 : 0;
+    a.claim_bytes = d_proof + 12;
+    a.msg_out = d_proof + 44 + 32ull * t * (K + 1);
+    a.r_out = d_r + t;
+    a.point_out = d_point + 32ull * t;
+    a.part_out = part_out;
+    a.scale = d_scale;
+    unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
+    if (K == 1) launch_round<1>(ctx, fold, grid, a);
+    else if (K == 2) launch_round<2>(ctx, fold, grid, a);
+    else launch_round<3>(ctx, fold, grid, a);
+    if (a.eq_mode == 1) {
+        lo_level ^= 1;
+    } else if (a.eq_mode == 2) {
+        hi_cur = HP[hp_next];
+        hp_next ^= 1;
+    }
+    if (fold)
+        for (uint32_t k = 0; k < K; k++) cur[k] = buf[tl & 1][k];
+    t++;
+}
+
+void ScEngine::combine(const fr_t* all, uint32_t G) {
+    ZK_LAUNCH(ctx, k_sc_combine, 1, 32, 0, all, G, (int)K, t - 1, n_eq, d_w, d_claim, (t - 1 == 0 && !claim_given) ? 1 : 0,
+              tr->d_st, d_proof + 12, d_proof + 44 + 32ull * (t - 1) * (K + 1), d_r + (t - 1), d_point + 32ull * (t - 1));
+}
+
+void ScEngine::header() {
     uint8_t hdr[12];
     const uint32_t hv[3] = {m, n_eq, K};
     for (int i = 0; i < 3; i++)
         for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
-    ZK_CUDA(cudaMemcpyAsync(proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
-    ZK_LAUNCH(ctx, k_sc_header, 1, 32, 0, tr->d_st, make_bytes(hdr, 12), S.d_claim, S.claim_given ? 1 : 0, proof + 12);
+    ZK_CUDA(cudaMemcpyAsync(d_proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
+    ZK_LAUNCH(ctx, k_sc_header, 1, 32, 0, tr->d_st, make_bytes(hdr, 12), d_claim, claim_given ? 1 : 0, d_proof + 12);
+}
 
-    // eq split (only the suffix variables w_{t+1..n_eq-1} are ever needed)
-    const uint32_t hb = n_eq >= 1 ? (n_eq - 1 < 10 ? n_eq - 1 : 10) : 0;
-    const uint32_t lo0 = n_eq >= 1 ? n_eq - 1 - hb : 0;    // variables w_1 .. w_{lo0}
-    fr_t *HI = nullptr, *LO[2] = {nullptr, nullptr}, *HP[2] = {nullptr, nullptr};
-    if (n_eq >= 2) {
-        HI = s.alloc<fr_t>(1ull << hb);
-        eq_table_dev(ctx, S.d_w + 1 + lo0, hb, nullptr, HI, s);
-        if (lo0) {
-            LO[0] = s.alloc<fr_t>(1ull << lo0);
-            LO[1] = s.alloc<fr_t>(lo0 >= 1 ? (1ull << (lo0 - 1)) : 1);
-            eq_table_dev(ctx, S.d_w + 1, lo0, nullptr, LO[0], s);
-        }
-        HP[0] = s.alloc<fr_t>(1ull << hb);
-        HP[1] = s.alloc<fr_t>(1ull << hb);
-    }
-    // ping-pong fold buffers: round t (t >= 1) writes 2^{m-t} elements into buf[t & 1]
-    fr_t* buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-    for (uint32_t k = 0; k < K; k++) {
-        if (m >= 1) buf[1][k] = s.alloc<fr_t>(N >> 1);
-        if (m >= 2) buf[0][k] = s.alloc<fr_t>(N >> 2);
-    }
-    unsigned int max_grid = (unsigned int)ctx->num_sms * 4;
-    fr_t* partials = s.alloc<fr_t>((size_t)max_grid * (K + 1));
-    unsigned int* ticket = s.alloc_zero<unsigned int>(1);
+void ScEngine::finals() {
+    ZK_LAUNCH(ctx, k_sc_finals, 1, 32, 0, cur[0], K > 1 ? cur[1] : cur[0], K > 2 ? cur[2] : cur[0], (int)K, d_r + (m - 1),
+              tr->d_st, d_proof + 44 + 32ull * m * (K + 1), d_finals);
+}
 
-    const fr_t* cur[3] = {S.tables[0], K > 1 ? S.tables[1] : nullptr, K > 2 ? S.tables[2] : nullptr};
-    int lo_level = 0;            // which LO buffer holds the current level
-    const fr_t* hi_cur = HI;     // current HI level once LO is exhausted
-    int hp_next = 0;
-    for (uint32_t t = 0; t < m; t++) {
-        ScRoundArgs a;
-        memset(&a, 0, sizeof a);
-        const bool fold = t > 0;
-        const uint64_t n_pairs = N >> (t + 1);
-        for (uint32_t k = 0; k < K; k++) {
-            a.src[k] = cur[k];
-            a.dst[k] = fold ? buf[t & 1][k] : nullptr;
-        }
-        a.n_pairs = n_pairs;
-        a.r_prev = fold ? S.d_r + (t - 1) : nullptr;
-        // eq mode for this round
-        if (t < n_eq && n_eq - t - 1 >= 1) {
-            uint32_t nv = n_eq - t - 1;              // suffix variables
-            uint32_t lo_cnt = nv > hb ? nv - hb : 0;
-            if (lo_cnt >= 1) {
-                a.eq_mode = 1;
-                a.eq_cur = LO[lo_level];
-                a.eq_hi = HI;
-                a.eq_next = LO[lo_level ^ 1];
-                a.lo_cnt = lo_cnt;
-                a.hb = hb;
-            } else {
-                a.eq_mode = 2;
-                a.eq_cur = hi_cur;
-                a.eq_next = HP[hp_next];
-                a.lo_cnt = nv;
-            }
-        }
-        a.partials = partials;
-        a.ticket = ticket;
-        a.st = tr->d_st;
-        a.t = t;
-        a.n_eq = n_eq;
-        a.w = S.d_w;
-        a.claim = S.d_claim;
-        a.compute_claim = (t == 0 && !S.claim_given) ? 1 : 0;
-        a.claim_bytes = proof + 12;
-        a.msg_out = proof + 44 + 32ull * t * (K + 1);
-        a.r_out = S.d_r + t;
-        a.point_out = S.d_point + 32ull * t;
-        unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
-        if (K == 1) launch_round<1>(ctx, fold, grid, a);
-        else if (K == 2) launch_round<2>(ctx, fold, grid, a);
-        else launch_round<3>(ctx, fold, grid, a);
-        // advance eq levels
-        if (a.eq_mode == 1) {
-            lo_level ^= 1;
-            // LO exhausted after this round?  then the next round uses HI directly (pair-summed later)
-        } else if (a.eq_mode == 2) {
-            hi_cur = HP[hp_next];
-            hp_next ^= 1;
-        }
-        if (fold)
-            for (uint32_t k = 0; k < K; k++) cur[k] = buf[t & 1][k];
-    }
-    ZK_LAUNCH(ctx, k_sc_finals, 1, 32, 0, cur[0], K > 1 ? cur[1] : cur[0], K > 2 ? cur[2] : cur[0], (int)K,
-              S.d_r + (m - 1), tr->d_st, proof + 44 + 32ull * m * (K + 1), S.d_finals);
+void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
+    const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
+    ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
+    ScEngine e;
+    e.ctx = ctx;
+    e.tr = tr;
+    e.s = &s;
+    e.m = m;
+    e.n_eq = n_eq;
+    e.K = K;
+    e.d_w = S.d_w;
+    e.d_scale = nullptr;
+    e.d_proof = S.d_proof;
+    e.d_r = S.d_r;
+    e.d_point = S.d_point;
+    e.d_claim = S.d_claim;
+    e.claim_given = S.claim_given;
+    e.d_finals = S.d_finals;
+    e.header();
+    e.setup(S.tables, m, 0, n_eq);
+    for (uint32_t t = 0; t < m; t++) e.round(nullptr);
+    e.finals();
 }
 
 uint64_t sumcheck_proof_len(uint32_t m, uint32_t K) { return 12 + 32 + 32ull * m * (K + 1) + 32ull * K; }

@@ -1,4 +1,4 @@
-// sumcheck.cuh — device-side product sumcheck driver interface (rows a4-a6).
+// sumcheck.cuh — device-side product sumcheck driver interface (rows a4-a6, §8(e) sharding).
 #pragma once
 #include "common.cuh"
 
@@ -14,6 +14,39 @@ struct ScStatement {
     fr_t* d_r;               // m challenges (Montgomery)
     uint8_t* d_point;        // m challenges (canonical)
     fr_t* d_finals;          // K finals (Montgomery), may be null
+};
+
+// Round engine shared by the single-device prover, the sharded prover (partial + combine per round)
+// and the continuation after the sharded tables are gathered onto every rank.
+struct ScEngine {
+    zk_ctx* ctx = nullptr;
+    zk_transcript* tr = nullptr;
+    Scratch* s = nullptr;
+    uint32_t m = 0, n_eq = 0, K = 0;   // global statement
+    uint32_t L = 0, t0 = 0, n_eq_loc = 0, t = 0;
+    const fr_t* cur[3] = {nullptr, nullptr, nullptr};
+    fr_t* buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    fr_t *HI = nullptr, *LO[2] = {nullptr, nullptr}, *HP[2] = {nullptr, nullptr};
+    uint32_t hb = 0, lo0 = 0;
+    int lo_level = 0, hp_next = 0;
+    const fr_t* hi_cur = nullptr;
+    const fr_t* d_w = nullptr;
+    const fr_t* d_scale = nullptr;
+    fr_t* partials = nullptr;
+    unsigned int* ticket = nullptr;
+    uint8_t* d_proof = nullptr;
+    fr_t* d_r = nullptr;
+    uint8_t* d_point = nullptr;
+    fr_t* d_claim = nullptr;
+    bool claim_given = false;
+    fr_t* d_finals = nullptr;
+
+    // local tables of 2^L entries entering at global round t0; eq over w[t0 .. t0 + n_eq_loc - 1]
+    void setup(const fr_t* const tables[3], uint32_t L, uint32_t t0, uint32_t n_eq_loc);
+    void header();                    // absorb "sc/hdr" (+ the given claim)
+    void round(fr_t* part_out);       // round t: fused (part_out == nullptr) or partial-only
+    void combine(const fr_t* all, uint32_t G);   // sharded: sum G partials + transcript step of round t-1
+    void finals();
 };
 
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s);

@@ -277,3 +277,59 @@ def test_fcn_tiny_vs_oracle(ctx, O):
         assert gr["msgs"] == orr["msgs"], gr["name"]
         assert gr["finals"] == orr["finals"], gr["name"]
         assert gr["state"] == orr["state"], gr["name"]
+
+
+# ---------------------------------------------------------------- §8(e) sharded sumcheck
+SHARD_CASES = [(10, 10, 2), (12, 7, 2), (13, 13, 3), (9, 0, 1), (16, 16, 2)]
+
+
+@pytest.mark.parametrize("m,n_eq,K", SHARD_CASES)
+def test_shard_virtual_vs_oracle(ctx, O, m, n_eq, K):
+    """G virtual shards on one device (same kernels as the multi-GPU path): transcript = single-device."""
+    from paper_2307_16273_b200 import api, shard
+    rng = random.Random(m + 100 * n_eq)
+    tabs = [uniform_range(12, 31 * m + k, (1 << m,), -(1 << 15), 1 << 15) for k in range(K)]
+    w = [rng.randrange(P) for _ in range(n_eq)]
+    seed = fs_seed(f"shard-{m}-{n_eq}-{K}")
+    o = O.sumcheck_prove(O.Transcript(seed), m, n_eq, [[int(v) % P for v in t] for t in tabs], w, None)
+    for G in (1, 2, 4, 8):
+        L = m - (G.bit_length() - 1)
+        for switch in (0, 3, 40):
+            trs = [api.Transcript(ctx, seed) for _ in range(G)]
+            sess = [shard.ShardSession(ctx, trs[g], m, n_eq, [dev(t[g << L:(g + 1) << L]) for t in tabs], w, g, G)
+                    for g in range(G)]
+            res = shard.prove_virtual(sess, switch_log=switch)
+            for g, r in enumerate(res):
+                assert r["claim"] == o["claim"] and r["msgs"] == o["msgs"], (G, switch, g)
+                assert r["finals"] == o["finals"] and r["r"] == o["r"], (G, switch, g)
+            assert trs[0].state() == trs[-1].state()
+            for s_ in sess:
+                s_.close()
+
+
+def test_shard_nccl_single_rank(ctx, O):
+    """The torch.distributed/NCCL exchange path with one rank (the only GPU count gpurun grants)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2307_16273_b200 import api, shard
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        m, n_eq = 14, 14
+        A = uniform_range(13, 1, (1 << m,), -(1 << 15), 1 << 15)
+        B = uniform_range(13, 2, (1 << m,), -(1 << 15), 1 << 15)
+        rng = random.Random(3)
+        w = [rng.randrange(P) for _ in range(n_eq)]
+        seed = fs_seed("shard-nccl")
+        o = O.sumcheck_prove(O.Transcript(seed), m, n_eq, [[int(v) % P for v in A], [int(v) % P for v in B]], w, None)
+        tr = api.Transcript(ctx, seed)
+        sess = shard.ShardSession(ctx, tr, m, n_eq, [dev(A), dev(B)], w, 0, 1)
+        res = shard.prove(sess, shard.TorchComm(), switch_log=6)
+        assert res["msgs"] == o["msgs"] and res["finals"] == o["finals"] and res["claim"] == o["claim"]
+    finally:
+        dist.destroy_process_group()
