@@ -192,7 +192,22 @@ __device__ __forceinline__ fr_t fr_sqr(const fr_t& a) { return fr_mul(a, a); }
 // One out-of-line copy for cold code (finalizers, single-CTA round kernels): the inlined product is
 // ~560 SASS instructions, and cold code that inlines dozens of them runs out of the instruction
 // cache (ncu: stall_no_inst dominated the round kernels' finalize).
-static __device__ __noinline__ fr_t fr_mul_cold(fr_t a, fr_t b) { return fr_mul(a, b); }
+static __device__ __noinline__ fr_t fr_mul_cold(fr_t a, fr_t b) {
+    // rolled over the 8 limbs of b (one MAC row + one REDC row of code, ~10x smaller than fr_mul)
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t bb[8] = {b.v[0], b.v[1], b.v[2], b.v[3], b.v[4], b.v[5], b.v[6], b.v[7]};
+#pragma unroll 1
+    for (int i = 0; i < 8; i++) {
+        const uint32_t bi = bb[0];
+        bb[0] = bb[1]; bb[1] = bb[2]; bb[2] = bb[3]; bb[3] = bb[4]; bb[4] = bb[5]; bb[5] = bb[6]; bb[6] = bb[7];
+        ZK_MAC_ROW(t, a.v, bi);
+        ZK_REDC_ROW(t);
+    }
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = t[i];
+    return fr_reduce_once(r);
+}
 
 // Montgomery reduction of a wide unsigned integer T (10 limbs, T < p * 2^256):
 // returns T * R^{-1} mod p.  Used by the int32 x Fr lazy accumulators.
@@ -277,6 +292,11 @@ __device__ __forceinline__ fr_t fr_load(const fr_t* p) {
 __device__ __forceinline__ fr_t fr_load_cg(const fr_t* p) {   // streaming (not kept in L1)
     const uint4* q = reinterpret_cast<const uint4*>(p);
     uint4 x = __ldcs(q), y = __ldcs(q + 1);
+    return fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
+}
+__device__ __forceinline__ fr_t fr_load_l2(const fr_t* p) {   // bypass L1: data written earlier in the same kernel
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    uint4 x = __ldcg(q), y = __ldcg(q + 1);
     return fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
 }
 __device__ __forceinline__ void fr_store(fr_t* p, const fr_t& a) {

@@ -112,8 +112,8 @@ __device__ __forceinline__ void masked_add10(uint32_t (&a)[10], const fr_t& v, u
 // Table entries are sums of LO' values (eq * R, "double Montgomery"), reduced mod p; the lazy
 // accumulators are closed with REDC (-> Montgomery) and multiplied by HI[row] when the row changes.
 constexpr int BS2_CH = 64;
-constexpr int BS2_T = 256;
-constexpr int BS2_MAXC = 6;   // cell slots per thread: 1 linear (M) + up to 5 co-occurrence (C)
+constexpr int BS2_T = 512;
+constexpr int BS2_MAXC = 3;   // cell slots per thread: cells tid, tid + 512, tid + 1024
 
 struct BitCell2 {
     uint8_t j1, j2, s, x;   // bit positions, word (0 Z, 1 G_A), weight table (M cells: 0..3; C cells: 4)
@@ -127,7 +127,7 @@ struct Bitsum2Args {
     const fr_t* HI[5];
     const BitCell2* cells;   // [0, nM) linear cells, [nM, nM + nC) co-occurrence cells
     uint32_t nM, nC;
-    fr_t* partials;          // gridDim.x * (nM + nC)
+    fr_t* partials;          // gridDim.x * (nM + nC), zero-initialised; per-block running totals
 };
 
 struct Bitsum2Smem {
@@ -135,8 +135,8 @@ struct Bitsum2Smem {
     fr_t Tm[4][16][16];
     fr_t E[5][BS2_CH];
     fr_t U[8][8];
+    uint64_t P64[2][32];     // [s][j]: byte g = bit j of the 8 words of group g
     uint32_t W[2][BS2_CH];
-    uint8_t P[2][8][32];
     uint8_t sig[BS2_CH];
 };
 
@@ -156,6 +156,13 @@ __device__ __forceinline__ void wide_add_fr(uint32_t (&a)[10], const fr_t& v) {
         : "r"(v.v[0]), "r"(v.v[1]), "r"(v.v[2]), "r"(v.v[3]), "r"(v.v[4]), "r"(v.v[5]), "r"(v.v[6]), "r"(v.v[7]));
 }
 
+__device__ __forceinline__ void bs2_flush(uint32_t (&acc)[10], const fr_t* hi, uint64_t row, fr_t* tot) {
+    fr_t v = fr_mul(fr_redc_wide(acc), fr_load(&hi[row]));
+    fr_store(tot, fr_add(fr_load(tot), v));
+#pragma unroll
+    for (int k = 0; k < 10; k++) acc[k] = 0;
+}
+
 __global__ void __launch_bounds__(BS2_T, 1) k_relu_bitsums2(Bitsum2Args a) {
     extern __shared__ __align__(16) uint8_t smem2_raw[];
     Bitsum2Smem& S = *reinterpret_cast<Bitsum2Smem*>(smem2_raw);
@@ -164,24 +171,20 @@ __global__ void __launch_bounds__(BS2_T, 1) k_relu_bitsums2(Bitsum2Args a) {
     const uint64_t nchunks = D / BS2_CH;
     const uint64_t c_begin = blockIdx.x * nchunks / gridDim.x, c_end = (blockIdx.x + 1) * nchunks / gridDim.x;
     const uint32_t ncell = a.nM + a.nC;
-    // this thread's cells: slot 0 = linear cell tid (if tid < nM), slots 1.. = co-occurrence cells
     BitCell2 cl[BS2_MAXC];
     int cid[BS2_MAXC];
 #pragma unroll
     for (int q = 0; q < BS2_MAXC; q++) {
-        int c = q == 0 ? (tid < (int)a.nM ? tid : -1) : ((int)a.nM + tid + (q - 1) * BS2_T);
-        if (q > 0 && c >= (int)ncell) c = -1;
-        cid[q] = c;
-        cl[q] = c >= 0 ? a.cells[c] : BitCell2{0, 0, 0, 0};
+        const int c = tid + q * BS2_T;
+        cid[q] = c < (int)ncell ? c : -1;
+        cl[q] = c < (int)ncell ? a.cells[c] : BitCell2{0, 0, 0, 0};
     }
+    fr_t* tot = a.partials + (uint64_t)blockIdx.x * ncell;
     uint32_t acc[BS2_MAXC][10];
-    fr_t tot[BS2_MAXC];
 #pragma unroll
-    for (int q = 0; q < BS2_MAXC; q++) {
-        tot[q] = fr_zero();
+    for (int q = 0; q < BS2_MAXC; q++)
 #pragma unroll
         for (int k = 0; k < 10; k++) acc[q][k] = 0;
-    }
     const uint64_t lo_mask = (1ull << a.lo_bits) - 1;
     uint64_t row = (c_begin * BS2_CH) >> a.lo_bits;
     for (uint64_t ch = c_begin; ch < c_end; ch++) {
@@ -190,50 +193,43 @@ __global__ void __launch_bounds__(BS2_T, 1) k_relu_bitsums2(Bitsum2Args a) {
         if (r_here != row) {
 #pragma unroll
             for (int q = 0; q < BS2_MAXC; q++)
-                if (cid[q] >= 0) {
-                    tot[q] = fr_add(tot[q], fr_mul(fr_redc_wide(acc[q]), fr_load(&a.HI[cl[q].x][row])));
-#pragma unroll
-                    for (int k = 0; k < 10; k++) acc[q][k] = 0;
-                }
+                if (cid[q] >= 0) bs2_flush(acc[q], a.HI[cl[q].x], row, &tot[cid[q]]);
             row = r_here;
         }
         __syncthreads();
-        // stage words, sign bits and LO' weights of the chunk
-        for (int e = tid; e < 5 * BS2_CH; e += BS2_T) {
-            const int x = e / BS2_CH, k = e % BS2_CH;
+        // stage the chunk: LO' weights, words, sign bits
+        if (tid < 5 * BS2_CH) {
+            const int x = tid / BS2_CH, k = tid % BS2_CH;
             S.E[x][k] = fr_load(&a.LO[x][(i0 + k) & lo_mask]);
-        }
-        if (tid < BS2_CH) {
-            uint32_t z = (uint32_t)__ldg(a.Z + i0 + tid), g = (uint32_t)__ldg(a.GA + i0 + tid);
-            S.W[0][tid] = z & a.qr_mask;
-            S.W[1][tid] = g & a.qr_mask;
-            S.sig[tid] = (z >> a.sig_bit) & 1;
+        } else if (tid >= 384 && tid < 384 + BS2_CH) {
+            const int k = tid - 384;
+            uint32_t z = (uint32_t)__ldg(a.Z + i0 + k), g = (uint32_t)__ldg(a.GA + i0 + k);
+            S.W[0][k] = z & a.qr_mask;
+            S.W[1][k] = g & a.qr_mask;
+            S.sig[k] = (z >> a.sig_bit) & 1;
         }
         __syncthreads();
-        // gate c_A, c_GZ by (1 - sig); byte planes
+        // gate c_A, c_GZ by (1 - sig); bit planes; U
         if (tid < 2 * BS2_CH) {
             const int k = tid % BS2_CH, x = tid < BS2_CH ? 1 : 3;
             if (S.sig[k]) S.E[x][k] = fr_zero();
-        }
-        for (int e = tid; e < 2 * 8 * 32; e += BS2_T) {
-            const int s = e >> 8, g = (e >> 5) & 7, j = e & 31;
-            uint32_t m = 0;
+        } else if (tid >= 128 && tid < 192) {
+            const int e = tid - 128, sd = e >> 5, j = e & 31;
+            uint64_t m = 0;
 #pragma unroll
-            for (int k = 0; k < 8; k++) m |= ((S.W[s][8 * g + k] >> j) & 1u) << k;
-            S.P[s][g][j] = (uint8_t)m;
-        }
-        // U[g][q] = sum_{k<3, bit k of q} e_b(8g + 5 + k)
-        if (lane < 8) {
-            const fr_t* eb = &S.E[4][8 * warp + 5];
+            for (int k = 0; k < BS2_CH; k++) m |= (uint64_t)((S.W[sd][k] >> j) & 1u) << k;
+            S.P64[sd][j] = m;   // bit k of the chunk = byte k/8, bit k%8: byte g holds group g
+        } else if (tid >= 256 && tid < 256 + 64) {
+            const int g = (tid - 256) >> 3, q = (tid - 256) & 7;
+            const fr_t* eb = &S.E[4][8 * g + 5];
             fr_t u = fr_zero();
-            if (lane & 1) u = eb[0];
-            if (lane & 2) u = fr_add(u, eb[1]);
-            if (lane & 4) u = fr_add(u, eb[2]);
-            S.U[warp][lane] = u;
+            if (q & 1) u = eb[0];
+            if (q & 2) u = fr_add(u, eb[1]);
+            if (q & 4) u = fr_add(u, eb[2]);
+            S.U[g][q] = u;
         }
         __syncthreads();
-        // byte tables: warp g builds Tb[g][l + 32 q] = base(l) + U[g][q]
-        {
+        if (warp < 8) {   // byte tables: warp g builds Tb[g][l + 32 q] = base(l) + U[g][q]
             const int g = warp;
             const fr_t* eb = &S.E[4][8 * g];
             fr_t base = fr_zero();
@@ -243,47 +239,38 @@ __global__ void __launch_bounds__(BS2_T, 1) k_relu_bitsums2(Bitsum2Args a) {
             S.Tb[g][lane] = base;
 #pragma unroll
             for (int q = 1; q < 8; q++) S.Tb[g][lane + 32 * q] = fr_add(base, S.U[g][q]);
-        }
-        // nibble tables Tm[x][h][v]
-        for (int e = tid; e < 4 * 16 * 16; e += BS2_T) {
-            const int x = e >> 8, h = (e >> 4) & 15, v = e & 15;
-            const fr_t* cx = &S.E[x][4 * h];
-            fr_t t = fr_zero();
+        } else {          // nibble tables Tm[x][h][v]
+            for (int e = tid - 256; e < 4 * 16 * 16; e += 256) {
+                const int x = e >> 8, h = (e >> 4) & 15, v = e & 15;
+                const fr_t* cx = &S.E[x][4 * h];
+                fr_t t = fr_zero();
 #pragma unroll
-            for (int k = 0; k < 4; k++)
-                if ((v >> k) & 1) t = fr_add(t, cx[k]);
-            S.Tm[x][h][v] = t;
-        }
-        __syncthreads();
-        // accumulate
-        if (cid[0] >= 0) {
-            const int s = cl[0].s, j = cl[0].j1, x = cl[0].x;
-#pragma unroll 4
-            for (int h = 0; h < 16; h++) {
-                const int nib = (S.P[s][h >> 1][j] >> (4 * (h & 1))) & 15;
-                wide_add_fr(acc[0], S.Tm[x][h][nib]);
+                for (int k = 0; k < 4; k++)
+                    if ((v >> k) & 1) t = fr_add(t, cx[k]);
+                S.Tm[x][h][v] = t;
             }
         }
+        __syncthreads();
 #pragma unroll
-        for (int q = 1; q < BS2_MAXC; q++) {
-            if (cid[q] >= 0) {
-                const int s = cl[q].s, j1 = cl[q].j1, j2 = cl[q].j2;
+        for (int q = 0; q < BS2_MAXC; q++) {
+            if (cid[q] < 0) continue;
+            if (cid[q] < (int)a.nM) {   // linear cell: 16 nibble lookups
+                const uint64_t pm = S.P64[cl[q].s][cl[q].j1];
+                const int x = cl[q].x;
+#pragma unroll 4
+                for (int h = 0; h < 16; h++) wide_add_fr(acc[q], S.Tm[x][h][(pm >> (4 * h)) & 15]);
+            } else {                     // co-occurrence cell: 8 byte lookups
+                const uint64_t pm = S.P64[cl[q].s][cl[q].j1] & S.P64[cl[q].s][cl[q].j2];
 #pragma unroll
-                for (int g = 0; g < 8; g++) {
-                    const int m = S.P[s][g][j1] & S.P[s][g][j2];
-                    wide_add_fr(acc[q], S.Tb[g][m]);
-                }
+                for (int g = 0; g < 8; g++) wide_add_fr(acc[q], S.Tb[g][(pm >> (8 * g)) & 255]);
             }
         }
     }
     if (c_begin < c_end) {
 #pragma unroll
         for (int q = 0; q < BS2_MAXC; q++)
-            if (cid[q] >= 0) tot[q] = fr_add(tot[q], fr_mul(fr_redc_wide(acc[q]), fr_load(&a.HI[cl[q].x][row])));
+            if (cid[q] >= 0) bs2_flush(acc[q], a.HI[cl[q].x], row, &tot[cid[q]]);
     }
-#pragma unroll
-    for (int q = 0; q < BS2_MAXC; q++)
-        if (cid[q] >= 0) fr_store(&a.partials[(uint64_t)blockIdx.x * ncell + cid[q]], tot[q]);
 }
 
 // Each thread owns cells tid and tid + blockDim.x.  Each block walks a contiguous range of chunks;
@@ -431,7 +418,7 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
     __shared__ FsScratch fs;
     if (tid < 32) fs_begin(fs, a.st);
     __syncthreads();
-    const fr_t claim = fr_zero();   // (the i-phase computes every evaluation; the running claim is not needed)
+    __shared__ fr_t claim_sm;   // g_{logB-1}(r_{logB-1}): the claim entering the i-phase
     for (uint32_t t = 0; t < a.logB; t++) {
         const int n = B >> t, np = n >> 1;
         // evaluations: item (b, X)
@@ -462,6 +449,10 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
                 fr_canon_to_bytes(fs.rc, a.point_out + 32ull * t);
                 fr_store(&a.rj_out[t], rt);
                 rt_sm = rt;
+                if (t + 1 == a.logB) {
+                    fr_t ev[4] = {msg[0], msg[1], msg[2], msg[3]};
+                    claim_sm = interp_small(ev, 3, rt);
+                }
             }
         }
         __syncthreads();
@@ -506,7 +497,8 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_store(&a.kappa[3], fr_mul_cold(fr_mul_cold(rp, r), sp));
         fr_store(&a.kappa[4], EB[0]);
         fr_store(&a.kappa[5], rp);
-        fr_store(&a.kappa[6], claim);
+        fr_store(&a.kappa[6], claim_sm);
+        fr_store(&a.kappa[7], fr_mul_cold(rp, EB[0]));
     }
     // byte tables: T[b][v] = sum_{k<8} [bit k of v] beta(r_j, 8b + k)
     for (int j = tid; j < B; j += blockDim.x) {
@@ -553,12 +545,12 @@ struct IRoundArgs {
     const fr_t* r_prev;
     const fr_t* lo_cur[5];
     fr_t* lo_next[5];
-    fr_t* hi[5];           // scaled HI' (rescaled in place by the finalizer)
+    fr_t* hi[6];           // scaled HI' tables: Z, A, GA, GZ, b, b' = r' b (rescaled in place by the finalizer)
     uint32_t lo_cnt;       // LO variables of this round (>= 1), including the current one
     uint32_t hb;
     const fr_t* u[5];      // eq points over i (Montgomery)
     uint32_t t;            // i-round index
-    const fr_t* kappa;     // [4] kb, [5] r'
+    fr_t* claim;           // running claim c_t (device); g_t(1) = c_t - g_t(0), then c_{t+1} = g_t(r_t)
     fr_t* partials;
     unsigned int* ticket;
     uint8_t* st;
@@ -567,106 +559,126 @@ struct IRoundArgs {
     uint8_t* point_out;
 };
 
+// Two threads per pair b: side s = 0 carries a0 with E_Z, E_A and the AIVP weight E_b; side s = 1
+// carries a1 with E_GA, E_GZ and E_b' = r' E_b (its own HI table, so no per-pair r' product).  Per side
+// and X in {0, 2, 3}: P_s(X) = a (E_a + E_c oms) + E_b a (a - 1); X = 1 follows from g(0) + g(1) = c_t.
 template <bool FOLD>
-__global__ void __launch_bounds__(256) k_relu_iround(IRoundArgs a) {
-    fr_t acc[4] = {fr_zero(), fr_zero(), fr_zero(), fr_zero()};
-    fr_t r;
-    if (FOLD) r = fr_load(a.r_prev);
-    const fr_t rp = fr_load(&a.kappa[5]);
+__global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
+    fr_t acc[3] = {fr_zero(), fr_zero(), fr_zero()};   // X = 0, 2, 3
+    const int side = threadIdx.x & 1;
     const uint64_t lo_mask = (1ull << a.lo_cnt) - 1;
     const uint64_t next_count = 1ull << (a.lo_cnt - 1);
-    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < a.n_pairs;
-         b += (uint64_t)gridDim.x * blockDim.x) {
-        fr_t v0[3], dv[3];
-#pragma unroll
-        for (int k = 0; k < 3; k++) {
-            fr_t x0, x1;
-            if (FOLD) {
-                const fr_t* s = a.src[k] + 4 * b;
-                fr_t y0 = fr_load_cg(s), y1 = fr_load_cg(s + 1), y2 = fr_load_cg(s + 2), y3 = fr_load_cg(s + 3);
-                x0 = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
-                x1 = fr_add(y2, fr_mul(r, fr_sub(y3, y2)));
-                fr_store(a.dst[k] + 2 * b, x0);
-                fr_store(a.dst[k] + 2 * b + 1, x1);
-            } else {
-                x0 = fr_load_cg(a.src[k] + 2 * b);
-                x1 = fr_load_cg(a.src[k] + 2 * b + 1);
+    const fr_t* srcA = side ? a.src[1] : a.src[0];
+    fr_t* dstA = side ? a.dst[1] : a.dst[0];
+    const fr_t* loA = side ? a.lo_cur[2] : a.lo_cur[0];
+    const fr_t* loC = side ? a.lo_cur[3] : a.lo_cur[1];
+    const fr_t* loB = a.lo_cur[4];
+    const fr_t* hiA = side ? a.hi[2] : a.hi[0];
+    const fr_t* hiC = side ? a.hi[3] : a.hi[1];
+    const fr_t* hiB = side ? a.hi[5] : a.hi[4];
+    fr_t r;
+    if (FOLD) r = fr_load(a.r_prev);
+    const uint64_t first = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 1;
+    const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 1;
+    for (uint64_t b = first; b < a.n_pairs; b += stride) {
+        fr_t av, ad, om, omd;
+        if (FOLD) {
+            const fr_t* s = srcA + 4 * b;
+            fr_t y0 = fr_load_cg(s), y1 = fr_load_cg(s + 1), y2 = fr_load_cg(s + 2), y3 = fr_load_cg(s + 3);
+            fr_t x0 = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+            fr_t x1 = fr_add(y2, fr_mul(r, fr_sub(y3, y2)));
+            fr_store(dstA + 2 * b, x0);
+            fr_store(dstA + 2 * b + 1, x1);
+            av = x0;
+            ad = fr_sub(x1, x0);
+            const fr_t* so = a.src[2] + 4 * b;
+            y0 = fr_load_cg(so); y1 = fr_load_cg(so + 1); y2 = fr_load_cg(so + 2); y3 = fr_load_cg(so + 3);
+            x0 = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+            x1 = fr_add(y2, fr_mul(r, fr_sub(y3, y2)));
+            if (side == 0) {
+                fr_store(a.dst[2] + 2 * b, x0);
+                fr_store(a.dst[2] + 2 * b + 1, x1);
             }
-            v0[k] = x0;
-            dv[k] = fr_sub(x1, x0);
+            om = x0;
+            omd = fr_sub(x1, x0);
+        } else {
+            av = fr_load_cg(srcA + 2 * b);
+            ad = fr_sub(fr_load_cg(srcA + 2 * b + 1), av);
+            om = fr_load_cg(a.src[2] + 2 * b);
+            omd = fr_sub(fr_load_cg(a.src[2] + 2 * b + 1), om);
+        }
+        if (b < next_count) {   // next LO level: side 0 handles Z, A, b; side 1 handles GA, GZ
+            fr_store(&a.lo_next[side ? 2 : 0][b], fr_add(fr_load(&loA[2 * b]), fr_load(&loA[2 * b + 1])));
+            fr_store(&a.lo_next[side ? 3 : 1][b], fr_add(fr_load(&loC[2 * b]), fr_load(&loC[2 * b + 1])));
+            if (side == 0) fr_store(&a.lo_next[4][b], fr_add(fr_load(&loB[2 * b]), fr_load(&loB[2 * b + 1])));
         }
         const uint64_t l0 = (2 * b) & lo_mask;
         const uint64_t h = b >> (a.lo_cnt - 1);
-        if (b < next_count)
+        const fr_t ha = fr_load(&hiA[h]), hc = fr_load(&hiC[h]), hb = fr_load(&hiB[h]);
+        fr_t ea = fr_mul(fr_load(&loA[l0]), ha);
+        fr_t ead = fr_sub(fr_mul(fr_load(&loA[l0 + 1]), ha), ea);
+        fr_t ec = fr_mul(fr_load(&loC[l0]), hc);
+        fr_t ecd = fr_sub(fr_mul(fr_load(&loC[l0 + 1]), hc), ec);
+        fr_t eb = fr_mul(fr_load(&loB[l0]), hb);
+        fr_t ebd = fr_sub(fr_mul(fr_load(&loB[l0 + 1]), hb), eb);
 #pragma unroll
-            for (int x = 0; x < 5; x++)
-                fr_store(&a.lo_next[x][b], fr_add(fr_load(&a.lo_cur[x][2 * b]), fr_load(&a.lo_cur[x][2 * b + 1])));
-        // eq values at X = 0, 1 of the b-term (index 4) and per-side pairs
-        fr_t eb0, ebd;
-        {
-            fr_t hh = fr_load(&a.hi[4][h]);
-            fr_t e0 = fr_mul(fr_load(&a.lo_cur[4][l0]), hh), e1 = fr_mul(fr_load(&a.lo_cur[4][l0 + 1]), hh);
-            eb0 = e0;
-            ebd = fr_sub(e1, e0);
-        }
-        // side s = 0 (a0 with E_Z, E_A) and s = 1 (a1 with E_GA, E_GZ); AIVP weight 1 and r'
-        const fr_t a00 = v0[0], a0d = dv[0], a10 = v0[1], a1d = dv[1], om0 = v0[2], omd = dv[2];
-#pragma unroll 1
-        for (int sd = 0; sd < 2; sd++) {
-            const fr_t* hia = sd ? a.hi[2] : a.hi[0];
-            const fr_t* hic = sd ? a.hi[3] : a.hi[1];
-            const fr_t* loa = sd ? a.lo_cur[2] : a.lo_cur[0];
-            const fr_t* loc = sd ? a.lo_cur[3] : a.lo_cur[1];
-            fr_t ha = fr_load(&hia[h]), hb_ = fr_load(&hic[h]);
-            fr_t ea = fr_mul(fr_load(&loa[l0]), ha);
-            fr_t ead = fr_sub(fr_mul(fr_load(&loa[l0 + 1]), ha), ea);
-            fr_t ec = fr_mul(fr_load(&loc[l0]), hb_);
-            fr_t ecd = fr_sub(fr_mul(fr_load(&loc[l0 + 1]), hb_), ec);
-            fr_t av = sd ? a10 : a00, ad = sd ? a1d : a0d;
-            fr_t om = om0, eb = eb0;
-            const fr_t wq = sd ? rp : fr_one();
-#pragma unroll
-            for (int X = 0; X < 4; X++) {
-                // a * (E_a + E_c * oms) + E_b * (a^2 - a) * (sd ? r' : 1)
-                fr_t tq = fr_add(ea, fr_mul(ec, om));
-                fr_t q = fr_mul(av, fr_sub(av, fr_one()));
-                if (sd) q = fr_mul(q, wq);
-                fr_t p = fr_add(fr_mul(av, tq), fr_mul(eb, q));
-                acc[X] = fr_add(acc[X], p);
-                if (X < 3) {
-                    av = fr_add(av, ad);
-                    om = fr_add(om, omd);
-                    ea = fr_add(ea, ead);
-                    ec = fr_add(ec, ecd);
-                    eb = fr_add(eb, ebd);
-                }
+        for (int X = 0; X < 4; X++) {
+            if (X != 1) {
+                const fr_t q = fr_mul(av, fr_sub(av, fr_one()));
+                const fr_t p = fr_add(fr_mul(av, fr_add(ea, fr_mul(ec, om))), fr_mul(eb, q));
+                acc[X == 0 ? 0 : X - 1] = fr_add(acc[X == 0 ? 0 : X - 1], p);
+            }
+            if (X < 3) {
+                av = fr_add(av, ad);
+                om = fr_add(om, omd);
+                ea = fr_add(ea, ead);
+                ec = fr_add(ec, ecd);
+                eb = fr_add(eb, ebd);
             }
         }
     }
-    __shared__ fr_t tot[4];
-    __shared__ fr_t eqr[5];
+    __shared__ fr_t tot[3];
+    __shared__ fr_t eqr[6];
+    __shared__ fr_t msg[4];
+    __shared__ fr_t terms[4];
     __shared__ FsScratch fs;
-    if (grid_reduce_fr_block<4>(acc, a.partials, a.ticket, tot)) {
+    if (grid_reduce_fr_block<3>(acc, a.partials, a.ticket, tot)) {
         if (threadIdx.x < 32) {
             const int lane = threadIdx.x;
+            if (lane == 0) {
+                msg[0] = tot[0];
+                msg[1] = fr_sub(fr_load(a.claim), tot[0]);
+                msg[2] = tot[1];
+                msg[3] = tot[2];
+            }
+            __syncwarp();
             fs_begin(fs, a.st);
-            fs_absorb_frs(fs, "relu/msg", lane < 4 ? tot[lane & 3] : fr_zero(), 4, a.msg_out);
+            fs_absorb_frs(fs, "relu/msg", lane < 4 ? msg[lane & 3] : fr_zero(), 4, a.msg_out);
             fr_t rt = fs_challenge(fs, "relu/x");
             if (lane == 0) {
                 fr_store(a.r_out, rt);
                 fr_canon_to_bytes(fs.rc, a.point_out);
             }
-            if (lane < 5) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur, one lane per eq point
+            if (lane < 6) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur, one lane per HI table
                 const fr_t* up = lane == 0 ? a.u[0] : lane == 1 ? a.u[1] : lane == 2 ? a.u[2] : lane == 3 ? a.u[3] : a.u[4];
                 fr_t u = fr_load(&up[a.t]);
-                fr_t ur = fr_mul(u, rt);
+                fr_t ur = fr_mul_cold(u, rt);
                 eqr[lane] = fr_add(fr_sub(fr_sub(fr_one(), u), rt), fr_add(ur, ur));
+            } else if (lane < 10) {   // Lagrange term i of g_t(r_t) through 0..3: e_i prod_{j != i}(r - j) / (i - j)
+                const int i = lane - 6;
+                fr_t num = msg[i];
+                for (int j = 0; j < 4; j++)
+                    if (j != i) num = fr_mul_cold(num, fr_sub(rt, fr_from_u32((uint32_t)j)));
+                num = fr_mul_cold(num, (i == 0 || i == 3) ? ZK_INV6 : ZK_INV2);
+                terms[i] = (i == 0 || i == 2) ? fr_neg(num) : num;   // denominators -6, 2, -2, 6
             }
+            __syncwarp();
+            if (lane == 0) fr_store(a.claim, fr_add(fr_add(terms[0], terms[1]), fr_add(terms[2], terms[3])));
             fs_end(fs, a.st);
         }
         __syncthreads();
         const uint32_t nh = 1u << a.hb;
-        for (uint32_t e = threadIdx.x; e < 5 * nh; e += blockDim.x) {
+        for (uint32_t e = threadIdx.x; e < 6 * nh; e += blockDim.x) {
             uint32_t x = e / nh, hh = e % nh;
             fr_store(&a.hi[x][hh], fr_mul(fr_load(&a.hi[x][hh]), eqr[x]));
         }
@@ -844,7 +856,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         for (int sd = 0; sd < 2; sd++)
             for (uint32_t j1 = 0; j1 < B; j1++)
                 for (uint32_t j2 = j1; j2 < B; j2++) c2.push_back(BitCell2{(uint8_t)j1, (uint8_t)j2, (uint8_t)sd, 4});
-        ZK_REQUIRE(c2.size() == ncell && ncell - 4 * B <= (BS2_MAXC - 1) * BS2_T, ZK_ERR_INTERNAL, "bitsum cells");
+        ZK_REQUIRE(c2.size() == ncell && ncell <= BS2_MAXC * BS2_T, ZK_ERR_INTERNAL, "bitsum cells");
         BitCell2* d_c2 = s.alloc<BitCell2>(ncell);
         ZK_CUDA(cudaMemcpyAsync(d_c2, c2.data(), sizeof(BitCell2) * ncell, cudaMemcpyHostToDevice, ctx->stream));
         Bitsum2Args b2;
@@ -863,8 +875,8 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         b2.nM = 4 * B;
         b2.nC = ncell - 4 * B;
         const uint64_t nchunks = D / BS2_CH;
-        const uint32_t grid = (uint32_t)(nchunks < (uint64_t)ctx->num_sms * 2 ? nchunks : (uint64_t)ctx->num_sms * 2);
-        b2.partials = s.alloc<fr_t>((size_t)grid * ncell);
+        const uint32_t grid = (uint32_t)(nchunks < (uint64_t)ctx->num_sms ? nchunks : (uint64_t)ctx->num_sms);
+        b2.partials = s.alloc_zero<fr_t>((size_t)grid * ncell);
         const size_t smem = sizeof(Bitsum2Smem);
         ZK_CUDA(cudaFuncSetAttribute(k_relu_bitsums2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         ZK_LAUNCH(ctx, k_relu_bitsums2, grid, BS2_T, smem, b2);
@@ -911,11 +923,15 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
               (const fr_t*)byte_tab, full[0], full[1], full[2]);
     const uint32_t hb = logD < 5 ? logD : 5;
     const uint32_t H = logD - hb;
-    fr_t* HIs[5];
+    fr_t* HIs[6];
     fr_t* LOs[5][2];
     for (int x = 0; x < 5; x++) {
         HIs[x] = s.alloc<fr_t>(1ull << hb);
         eq_table_dev(ctx, u_i[x] + H, hb, kappa + (x < 4 ? x : 4), HIs[x], s);
+        if (x == 4) {   // E_b' = r' E_b for the a1 side of the AIVP
+            HIs[5] = s.alloc<fr_t>(1ull << hb);
+            eq_table_dev(ctx, u_i[4] + H, hb, kappa + 7, HIs[5], s);
+        }
         LOs[x][0] = LOs[x][1] = nullptr;
         if (H) {
             LOs[x][0] = s.alloc<fr_t>(1ull << H);
@@ -949,17 +965,18 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
             a.hi[x] = HIs[x];
             a.u[x] = u_i[x];
         }
+        a.hi[5] = HIs[5];
         a.lo_cnt = H - t;
         a.hb = hb;
         a.t = t;
-        a.kappa = kappa;
+        a.claim = kappa + 6;
         a.partials = partials;
         a.ticket = ticket;
         a.st = tr->d_st;
         a.msg_out = proof + 140 + 128ull * (logB + t);
         a.r_out = r_all + logB + t;
         a.point_out = out.d_point + 32ull * (logB + t);
-        unsigned int grid = grid_for(ctx, a.n_pairs, 256, 4);
+        unsigned int grid = grid_for(ctx, 2 * a.n_pairs, 256, 2);   // two threads per pair
         if (fold)
             ZK_LAUNCH(ctx, k_relu_iround<true>, grid, 256, 0, a);
         else

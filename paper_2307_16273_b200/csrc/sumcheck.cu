@@ -13,6 +13,8 @@
 // with HI = beta(w_{n_eq-h..n_eq-1}, .) (h <= 10) fixed and LO_t = beta(w_{t+1..n_eq-h-1}, .).  Because
 // beta(w_s, 0) + beta(w_s, 1) = 1, LO_{t+1}[c] = LO_t[2c] + LO_t[2c+1]: the round kernel writes the next
 // LO level with additions only.  Once LO is exhausted the HI table is pair-summed the same way.
+#include <cstdlib>
+
 #include "sumcheck.cuh"
 #include "tables.cuh"
 
@@ -331,9 +333,277 @@ void ScEngine::finals() {
               tr->d_st, d_proof + 44 + 32ull * m * (K + 1), d_finals);
 }
 
+// ---------------------------------------------------------------- persistent small-statement prover
+// Every round of a small statement (2^m <= 2^SC_ALL_MAX_LOG entries) in ONE cooperative launch: the
+// per-round kernel launch, the cold re-fetch of the round code and the separate finalizer launch are
+// replaced by two device-side waits per round (blocks publish partials and bump a monotonic arrival
+// counter; block 0 reduces them, runs the transcript step on its warp 0 and publishes r_t through a
+// round flag).  Eq suffix levels E_t = beta(w_{t+1..n_eq-1}, .) are pair-summed one level ahead.
+constexpr uint32_t SC_ALL_MAX_LOG = 18;
+
+struct ScAllArgs {
+    const fr_t* src[3];
+    fr_t* buf[2][3];
+    fr_t* E[2];                 // E[0] = level 0 = beta(w_1..w_{n_eq-1}); levels alternate
+    uint32_t m, n_eq;
+    const fr_t* w;
+    fr_t* claim;
+    int compute_claim;
+    uint8_t* st;
+    uint8_t* proof;
+    fr_t* d_r;
+    uint8_t* d_point;
+    fr_t* d_finals;
+    fr_t* partials;             // gridDim.x * 4
+    unsigned int* arrive;       // monotonic: blocks that finished round t = (t+1) * gridDim.x
+    unsigned int* flag;         // rounds whose challenge is published
+};
+
+__device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
+    __shared__ fr_t sm_red[32 * (K + 1)];
+    __shared__ fr_t tot[K + 1];
+    __shared__ FsScratch fs;
+    __shared__ fr_t claim_sm;
+    const uint32_t m = a.m, n_eq = a.n_eq;
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0 && tid < 32) fs_begin(fs, a.st);
+    for (uint32_t t = 0; t < m; t++) {
+        const uint64_t n_pairs = 1ull << (m - t - 1);
+        const fr_t* src[K];
+        fr_t* dst[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            src[k] = t == 0 ? a.src[k] : (t == 1 ? a.src[k] : a.buf[(t - 1) & 1][k]);
+            dst[k] = a.buf[t & 1][k];
+        }
+        fr_t r;
+        if (t > 0) {
+            const uint4* q = reinterpret_cast<const uint4*>(&a.d_r[t - 1]);
+            uint4 x = __ldcg(q), y = __ldcg(q + 1);
+            r = fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
+        }
+        const bool has_e = n_eq >= 2 && t + 1 < n_eq;
+        const uint32_t nv = has_e ? n_eq - t - 1 : 0;
+        const fr_t* Ecur = a.E[t & 1];
+        fr_t* Enext = a.E[(t + 1) & 1];
+        const uint64_t emask = (1ull << nv) - 1, enext = nv >= 1 ? (1ull << (nv - 1)) : 0;
+        fr_t acc[K + 1];
+#pragma unroll
+        for (int x = 0; x <= K; x++) acc[x] = fr_zero();
+        const uint64_t nworkers = gridDim.x - 1;
+        for (uint64_t b = blockIdx.x == 0 ? n_pairs : (blockIdx.x - 1) * (uint64_t)blockDim.x + tid; b < n_pairs;
+             b += nworkers * blockDim.x) {
+            fr_t lo[K], d[K];
+#pragma unroll
+            for (int k = 0; k < K; k++) {
+                fr_t v0, v1;
+                if (t > 0) {
+                    const fr_t* s = src[k] + 4 * b;
+                    fr_t x0 = fr_load_l2(s), x1 = fr_load_l2(s + 1), x2 = fr_load_l2(s + 2), x3 = fr_load_l2(s + 3);
+                    v0 = fr_add(x0, fr_mul(r, fr_sub(x1, x0)));
+                    v1 = fr_add(x2, fr_mul(r, fr_sub(x3, x2)));
+                    fr_store(dst[k] + 2 * b, v0);
+                    fr_store(dst[k] + 2 * b + 1, v1);
+                } else {
+                    v0 = fr_load_l2(src[k] + 2 * b);
+                    v1 = fr_load_l2(src[k] + 2 * b + 1);
+                }
+                lo[k] = v0;
+                d[k] = fr_sub(v1, v0);
+            }
+            fr_t e;
+            if (has_e) {
+                const uint4* q = reinterpret_cast<const uint4*>(&Ecur[b & emask]);
+                uint4 x = __ldcg(q), y = __ldcg(q + 1);
+                e = fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
+                if (b < enext) {
+                    const uint4* q0 = reinterpret_cast<const uint4*>(&Ecur[2 * b]);
+                    uint4 a0 = __ldcg(q0), a1 = __ldcg(q0 + 1), b0 = __ldcg(q0 + 2), b1 = __ldcg(q0 + 3);
+                    fr_store(&Enext[b], fr_add(fr_t{{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w}},
+                                               fr_t{{b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w}}));
+                }
+            }
+            fr_t v[K];
+#pragma unroll
+            for (int k = 0; k < K; k++) v[k] = lo[k];
+#pragma unroll
+            for (int x = 0; x <= K; x++) {
+                fr_t p = v[0];
+#pragma unroll
+                for (int k = 1; k < K; k++) p = fr_mul(p, v[k]);
+                if (has_e) p = fr_mul(p, e);
+                acc[x] = fr_add(acc[x], p);
+                if (x < K)
+#pragma unroll
+                    for (int k = 0; k < K; k++) v[k] = fr_add(v[k], d[k]);
+            }
+        }
+        if (blockIdx.x != 0) {   // worker: publish the block partial
+            block_reduce_fr<K + 1>(acc, sm_red);
+            if (tid == 0) {
+#pragma unroll
+                for (int x = 0; x <= K; x++) fr_store(&a.partials[(blockIdx.x - 1) * (K + 1) + x], acc[x]);
+                __threadfence();
+                atomicAdd(a.arrive, 1u);
+            }
+        }
+        if (blockIdx.x == 0) {   // dedicated reducer + transcript block (its I-cache keeps only this code)
+            if (tid == 0) {
+                while (ld_volatile(a.arrive) < (t + 1) * (gridDim.x - 1)) {
+                }
+                __threadfence();
+            }
+            __syncthreads();
+            fr_t s_[K + 1];
+#pragma unroll
+            for (int x = 0; x <= K; x++) s_[x] = fr_zero();
+            for (unsigned int bb = tid; bb < gridDim.x - 1; bb += blockDim.x)
+#pragma unroll
+                for (int x = 0; x <= K; x++) {
+                    const uint4* q = reinterpret_cast<const uint4*>(&a.partials[bb * (K + 1) + x]);
+                    uint4 xx = __ldcg(q), yy = __ldcg(q + 1);
+                    s_[x] = fr_add(s_[x], fr_t{{xx.x, xx.y, xx.z, xx.w, yy.x, yy.y, yy.z, yy.w}});
+                }
+            block_reduce_fr<K + 1>(s_, sm_red);
+            if (tid == 0)
+#pragma unroll
+                for (int x = 0; x <= K; x++) tot[x] = s_[x];
+            __syncthreads();
+            if (tid < 32) {
+                const int lane = tid;
+                if (t == 0 && a.compute_claim) {
+                    if (lane == 0) {
+                        fr_t c;
+                        if (n_eq >= 1) {
+                            fr_t w0 = fr_load(&a.w[0]);
+                            c = fr_add(fr_mul_cold(fr_sub(fr_one(), w0), tot[0]), fr_mul_cold(w0, tot[1]));
+                        } else {
+                            c = fr_add(tot[0], tot[1]);
+                        }
+                        fr_store(a.claim, c);
+                        claim_sm = c;
+                    }
+                    __syncwarp();
+                    fs_absorb_frs(fs, "sc/claim", claim_sm, 1, a.proof + 12);
+                }
+                fs_absorb_frs(fs, "sc/msg", lane <= K ? tot[lane & 3] : fr_zero(), K + 1, a.proof + 44 + 32ull * t * (K + 1));
+                fr_t rt = fs_challenge(fs, "sc/r");
+                if (lane == 0) {
+                    fr_store(&a.d_r[t], rt);
+                    fr_canon_to_bytes(fs.rc, a.d_point + 32ull * t);
+                    __threadfence();
+                    atomicExch(a.flag, t + 1);
+                }
+            }
+        } else {
+            if (tid == 0) {
+                while (ld_volatile(a.flag) < t + 1) {
+                }
+                __threadfence();
+            }
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid < 32) {   // finals on the last 2-element tables
+        const int lane = tid;
+        const fr_t* T = lane == 0 ? a.buf[(m - 1) & 1][0] : (lane == 1 ? a.buf[(m - 1) & 1][K > 1 ? 1 : 0]
+                                                                        : a.buf[(m - 1) & 1][K > 2 ? 2 : 0]);
+        if (m == 1) T = lane == 0 ? a.src[0] : (lane == 1 ? a.src[K > 1 ? 1 : 0] : a.src[K > 2 ? 2 : 0]);
+        fr_t f = fr_zero();
+        if (lane < K) {
+            fr_t rr = fr_load(&a.d_r[m - 1]);
+            fr_t x0 = fr_load_l2(T), x1 = fr_load_l2(T + 1);
+            f = fr_add(x0, fr_mul_cold(rr, fr_sub(x1, x0)));
+            if (a.d_finals) fr_store(&a.d_finals[lane], f);
+        }
+        fs_absorb_frs(fs, "sc/final", f, K, a.proof + 44 + 32ull * m * (K + 1));
+        fs_end(fs, a.st);
+    }
+}
+
+template <int K>
+static void launch_all(zk_ctx* ctx, const ScAllArgs& a, unsigned int grid) {
+    void* args[] = {(void*)&a};
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    if (ctx->prof) {
+        ev_a = ctx->take_event();
+        ev_b = ctx->take_event();
+        cudaEventRecord(ev_a, ctx->stream);
+    }
+    ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_sc_all<K>, dim3(grid), dim3(256), args, 0, ctx->stream));
+    after_launch(ctx, "k_sc_all");
+    if (ctx->prof) {
+        cudaEventRecord(ev_b, ctx->stream);
+        ctx->recs.push_back({"k_sc_all", ev_a, ev_b});
+    }
+}
+
+template <int K>
+static unsigned int all_grid(zk_ctx* ctx, uint32_t m) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sc_all<K>, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t cap = (uint64_t)per_sm * ctx->num_sms;
+    uint64_t need = ((1ull << (m - 1)) + 255) / 256 + 1;   // + the reducer block
+    if (need < 2) need = 2;
+    return (unsigned int)(need < cap ? need : cap);
+}
+
+static void sumcheck_prove_small(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
+    const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
+    uint8_t hdr[12];
+    const uint32_t hv[3] = {m, n_eq, K};
+    for (int i = 0; i < 3; i++)
+        for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
+    ZK_CUDA(cudaMemcpyAsync(S.d_proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
+    ZK_LAUNCH(ctx, k_sc_header, 1, 32, 0, tr->d_st, make_bytes(hdr, 12), S.d_claim, S.claim_given ? 1 : 0, S.d_proof + 12);
+    ScAllArgs a;
+    memset(&a, 0, sizeof a);
+    const uint64_t N = 1ull << m;
+    for (uint32_t k = 0; k < K; k++) {
+        a.src[k] = S.tables[k];
+        a.buf[1][k] = s.alloc<fr_t>(N >> 1);
+        a.buf[0][k] = s.alloc<fr_t>(m >= 2 ? N >> 2 : 1);
+    }
+    if (n_eq >= 2) {
+        a.E[0] = s.alloc<fr_t>(1ull << (n_eq - 1));
+        a.E[1] = s.alloc<fr_t>(n_eq >= 3 ? 1ull << (n_eq - 2) : 1);
+        eq_table_dev(ctx, S.d_w + 1, n_eq - 1, nullptr, a.E[0], s);
+    }
+    a.m = m;
+    a.n_eq = n_eq;
+    a.w = S.d_w;
+    a.claim = S.d_claim;
+    a.compute_claim = S.claim_given ? 0 : 1;
+    a.st = tr->d_st;
+    a.proof = S.d_proof;
+    a.d_r = S.d_r;
+    a.d_point = S.d_point;
+    a.d_finals = S.d_finals;
+    unsigned int grid = K == 1 ? all_grid<1>(ctx, m) : K == 2 ? all_grid<2>(ctx, m) : all_grid<3>(ctx, m);
+    a.partials = s.alloc<fr_t>((size_t)grid * 4);
+    unsigned int* ctr = s.alloc_zero<unsigned int>(2);
+    a.arrive = ctr;
+    a.flag = ctr + 1;
+    if (K == 1) launch_all<1>(ctx, a, grid);
+    else if (K == 2) launch_all<2>(ctx, a, grid);
+    else launch_all<3>(ctx, a, grid);
+}
+
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
     const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
     ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
+    if (m <= SC_ALL_MAX_LOG && !getenv("ZKDL_NO_PERSISTENT")) {
+        sumcheck_prove_small(ctx, tr, S, s);
+        return;
+    }
     ScEngine e;
     e.ctx = ctx;
     e.tr = tr;

@@ -142,3 +142,44 @@ void tr_init_dev(zk_transcript* tr, const uint8_t seed[32]) {
 }
 
 }  // namespace zk
+
+namespace zk {
+// Diagnostics: latency of the per-round transcript step (absorb K+1 = 3 elements, squeeze one challenge),
+// and of the out-of-line field multiply, on one warp.  mode 0: full step, 1: SHA-256 compressions only,
+// 2: fr_mul_cold chain.
+__global__ void k_diag_fs(uint8_t* st, uint32_t n, int mode, fr_t* out) {
+    __shared__ FsScratch fs;
+    fs_begin(fs, st);
+    const int lane = threadIdx.x & 31;
+    fr_t v = fr_one();
+    if (mode == 0) {
+        for (uint32_t i = 0; i < n; i++) {
+            fs_absorb_frs(fs, "sc/msg", v, 3, nullptr);
+            v = fs_challenge(fs, "sc/r");
+        }
+    } else if (mode == 1) {
+        if (lane == 0) {
+            uint32_t h[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+            for (uint32_t i = 0; i < n; i++) sha256_compress(h, fs.buf[0]);
+            v.v[0] = h[0];
+        }
+    } else {
+        if (lane == 0)
+            for (uint32_t i = 0; i < n; i++) v = fr_mul_cold(v, ZK_R2);
+    }
+    if (lane == 0) fr_store(out, v);
+    fs_end(fs, st);
+}
+}  // namespace zk
+
+extern "C" zk_status zk_diag_fs_bench(zk_transcript* tr, uint32_t n, int mode, void* d_out) {
+    if (!tr) return ZK_ERR_ARG;
+    zk_ctx* ctx = tr->ctx;
+    try {
+        ZK_LAUNCH(ctx, zk::k_diag_fs, 1, 32, 0, tr->d_st, n, mode, static_cast<zk::fr_t*>(d_out));
+    } catch (const zk::ZkError& e) {
+        ctx->err = e.msg;
+        return e.st;
+    }
+    return ZK_OK;
+}

@@ -37,35 +37,49 @@ struct Sha8 {
 };
 
 // One compression of a 64-byte block given as 16 little-endian-loaded words (byte-swapped here).
-// Out of line and rolled 4 x 16 rounds: the transcript runs on cold code paths (see fr_mul_cold).
+// Fully unrolled so the round constants are immediates (a rolled loop with constant-bank loads ran
+// at ~66 cycles/round on the B200); one out-of-line copy (~1K instructions) for the cold paths.
+#define ZK_SHA_R(a, b, c, d, e, f, g, h, k, wv)                                                        \
+    do {                                                                                               \
+        const uint32_t t1_ = h + (ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25)) + ((e & f) ^ (~e & g)) + (k) + (wv); \
+        const uint32_t t2_ = (ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22)) + ((a & b) ^ (a & c) ^ (b & c)); \
+        d += t1_;                                                                                      \
+        h = t1_ + t2_;                                                                                 \
+    } while (0)
+#define ZK_SHA_W(w, i)                                                                                 \
+    (w[(i) & 15] += (ror32(w[((i) + 14) & 15], 17) ^ ror32(w[((i) + 14) & 15], 19) ^ (w[((i) + 14) & 15] >> 10)) + \
+                    w[((i) + 9) & 15] +                                                                \
+                    (ror32(w[((i) + 1) & 15], 7) ^ ror32(w[((i) + 1) & 15], 18) ^ (w[((i) + 1) & 15] >> 3)))
 static __device__ __noinline__ Sha8 sha256_compress_s(Sha8 s, const uint32_t* blk) {
+    static constexpr uint32_t K[64] = {
+        0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+        0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+        0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+        0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+        0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+        0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+        0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+        0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
     uint32_t w[16];
 #pragma unroll
     for (int i = 0; i < 16; i++) w[i] = bswap32(blk[i]);
-    uint32_t a = s.h[0], b = s.h[1], c = s.h[2], d = s.h[3], e = s.h[4], f = s.h[5], g = s.h[6], hh = s.h[7];
-#pragma unroll 1
-    for (int j = 0; j < 64; j += 16) {
+    uint32_t a = s.h[0], b = s.h[1], c = s.h[2], d = s.h[3], e = s.h[4], f = s.h[5], g = s.h[6], h = s.h[7];
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            uint32_t wi;
-            if (j == 0) {
-                wi = w[i];
-            } else {
-                const uint32_t w15 = w[(i + 1) & 15], w2 = w[(i + 14) & 15];
-                const uint32_t s0 = ror32(w15, 7) ^ ror32(w15, 18) ^ (w15 >> 3);
-                const uint32_t s1 = ror32(w2, 17) ^ ror32(w2, 19) ^ (w2 >> 10);
-                wi = w[i] + s0 + w[(i + 9) & 15] + s1;
-                w[i] = wi;
-            }
-            const uint32_t S1 = ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25);
-            const uint32_t ch = (e & f) ^ (~e & g);
-            const uint32_t t1 = hh + S1 + ch + SHA_K[j + i] + wi;
-            const uint32_t S0 = ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22);
-            const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
-            hh = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
+    for (int i = 0; i < 64; i += 8) {
+        if (i >= 16) {
+#pragma unroll
+            for (int q = 0; q < 8; q++) ZK_SHA_W(w, i + q);
         }
+        ZK_SHA_R(a, b, c, d, e, f, g, h, K[i + 0], w[(i + 0) & 15]);
+        ZK_SHA_R(h, a, b, c, d, e, f, g, K[i + 1], w[(i + 1) & 15]);
+        ZK_SHA_R(g, h, a, b, c, d, e, f, K[i + 2], w[(i + 2) & 15]);
+        ZK_SHA_R(f, g, h, a, b, c, d, e, K[i + 3], w[(i + 3) & 15]);
+        ZK_SHA_R(e, f, g, h, a, b, c, d, K[i + 4], w[(i + 4) & 15]);
+        ZK_SHA_R(d, e, f, g, h, a, b, c, K[i + 5], w[(i + 5) & 15]);
+        ZK_SHA_R(c, d, e, f, g, h, a, b, K[i + 6], w[(i + 6) & 15]);
+        ZK_SHA_R(b, c, d, e, f, g, h, a, K[i + 7], w[(i + 7) & 15]);
     }
-    s.h[0] += a; s.h[1] += b; s.h[2] += c; s.h[3] += d; s.h[4] += e; s.h[5] += f; s.h[6] += g; s.h[7] += hh;
+    s.h[0] += a; s.h[1] += b; s.h[2] += c; s.h[3] += d; s.h[4] += e; s.h[5] += f; s.h[6] += g; s.h[7] += h;
     return s;
 }
 __device__ __forceinline__ void sha256_compress(uint32_t h[8], const uint32_t* blk) {
@@ -132,105 +146,113 @@ __device__ inline void fr_canon_to_bytes(const fr_t& c, uint8_t* out) {
 struct FsScratch {
     uint32_t buf[2][80];   // two 320-byte message buffers
     uint8_t st[32];        // current state bytes
+    uint8_t pay[256];      // payload (canonical field elements) of an absorb
     fr_t part[4];
+    fr_t half[2];
     fr_t r;
     fr_t rc;               // canonical r
 };
 
-// lane 0 copies the global state in / out
+// lanes copy the global state in / out
 __device__ __forceinline__ void fs_begin(FsScratch& s, const uint8_t* st_g) {
-    if ((threadIdx.x & 31) == 0)
-        for (int i = 0; i < 32; i++) s.st[i] = st_g[i];
+    const int lane = threadIdx.x & 31;
+    s.st[lane] = st_g[lane];
     __syncwarp();
 }
 __device__ __forceinline__ void fs_end(FsScratch& s, uint8_t* st_g) {
     __syncwarp();
-    if ((threadIdx.x & 31) == 0)
-        for (int i = 0; i < 32; i++) st_g[i] = s.st[i];
+    const int lane = threadIdx.x & 31;
+    st_g[lane] = s.st[lane];
     __syncwarp();
 }
 
-// header of an absorb: st || 0x01 || u8(|tag|) || tag || u64be(len); returns its length
-__device__ inline uint32_t fs_absorb_header(FsScratch& s, uint8_t* b, const char* tag, uint64_t len) {
-    for (int i = 0; i < 32; i++) b[i] = s.st[i];
-    uint32_t tl = zk_strlen(tag);
-    b[32] = 0x01;
-    b[33] = (uint8_t)tl;
-    for (uint32_t i = 0; i < tl; i++) b[34 + i] = (uint8_t)tag[i];
-    for (int i = 0; i < 8; i++) b[34 + tl + i] = (uint8_t)(len >> (56 - 8 * i));
-    return 42 + tl;
+// The 32 lanes assemble the padded message  st || dom || u8(|tag|) || tag || [u64be(plen)] || payload
+// into s.buf[which] (each lane a strided subset of the bytes), then lane `hasher` compresses it and
+// writes the digest to `out` (state bytes).  Every lane of the warp must call.
+__device__ inline void fs_hash_msg(FsScratch& s, int which, uint8_t dom, const char* tag, uint32_t tl, bool with_len,
+                                   const uint8_t* pay, uint32_t plen, int hasher, uint8_t* out) {
+    const int lane = threadIdx.x & 31;
+    uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[which]);
+    const uint32_t hl = 34 + tl + (with_len ? 8 : 0);
+    const uint32_t total = hl + plen;
+    const uint32_t padded = (total + 9 + 63) & ~63u;
+    const uint64_t bits = (uint64_t)total * 8;
+    for (uint32_t p = lane; p < padded; p += 32) {
+        uint8_t v;
+        if (p < 32) v = s.st[p];
+        else if (p == 32) v = dom;
+        else if (p == 33) v = (uint8_t)tl;
+        else if (p < 34 + tl) v = (uint8_t)tag[p - 34];
+        else if (p < hl) v = (uint8_t)((uint64_t)plen >> (56 - 8 * (p - 34 - tl)));
+        else if (p < total) v = pay[p - hl];
+        else if (p == total) v = 0x80;
+        else if (p >= padded - 8) v = (uint8_t)(bits >> (56 - 8 * (p - (padded - 8))));
+        else v = 0;
+        b[p] = v;
+    }
+    __syncwarp();
+    if (lane == hasher) {
+        uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+        for (uint32_t blk = 0; blk < padded / 64; blk++) sha256_compress(h, s.buf[which] + 16 * blk);
+        if (out) st_words_to_bytes(h, out);
+    }
+    __syncwarp();
 }
 
 // Absorb n <= 8 field elements; lane l < n contributes `mine` (Montgomery).  The canonical bytes are
 // also written to copy_out (global, may be null).  All 32 lanes of the warp must call.
 __device__ inline void fs_absorb_frs(FsScratch& s, const char* tag, const fr_t& mine, int n, uint8_t* copy_out) {
     const int lane = threadIdx.x & 31;
-    uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[0]);
-    __shared__ uint32_t hlen_sm;
-    if (lane == 0) hlen_sm = fs_absorb_header(s, b, tag, 32ull * n);
-    __syncwarp();
-    const uint32_t hl = hlen_sm;
     if (lane < n) {
         uint8_t tmp[32];
         fr_to_bytes(mine, tmp);
-        for (int k = 0; k < 32; k++) b[hl + 32 * lane + k] = tmp[k];
+        for (int k = 0; k < 32; k++) s.pay[32 * lane + k] = tmp[k];
         if (copy_out)
             for (int k = 0; k < 32; k++) copy_out[32 * lane + k] = tmp[k];
     }
     __syncwarp();
-    if (lane == 0) {
-        uint32_t d[8];
-        sha256_buf(b, hl + 32 * n, d);
-        st_words_to_bytes(d, s.st);
-    }
-    __syncwarp();
+    fs_hash_msg(s, 0, 0x01, tag, zk_strlen(tag), true, s.pay, 32u * n, 0, s.st);
 }
 
-// Absorb raw bytes (lane 0 only does the work; all lanes call).  len <= 256.
+// Absorb raw bytes (len <= 256) from any memory space; all lanes call.
 __device__ inline void fs_absorb_bytes(FsScratch& s, const char* tag, const uint8_t* msg, uint32_t len) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) {
-        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[0]);
-        uint32_t hl = fs_absorb_header(s, b, tag, len);
-        for (uint32_t i = 0; i < len; i++) b[hl + i] = msg[i];
-        uint32_t d[8];
-        sha256_buf(b, hl + len, d);
-        st_words_to_bytes(d, s.st);
-    }
+    for (uint32_t i = lane; i < len; i += 32) s.pay[i] = msg[i];
     __syncwarp();
+    fs_hash_msg(s, 0, 0x01, tag, zk_strlen(tag), true, s.pay, len, 0, s.st);
 }
 
-// lane 0: the challenge state update; lanes 0/1: the two squeeze hashes; lanes 0-3: the four
-// half-reductions.  Returns the Montgomery challenge on every lane (and s.rc = canonical).
+// challenge state update (lane 0), the two squeeze hashes (lanes 0 / 1, in parallel), the four
+// half-reductions (lanes 0-3).  Returns the Montgomery challenge on every lane (and s.rc = canonical).
 __device__ inline fr_t fs_challenge(FsScratch& s, const char* tag) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) {
-        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[0]);
-        for (int i = 0; i < 32; i++) b[i] = s.st[i];
-        uint32_t tl = zk_strlen(tag);
-        b[32] = 0x02;
-        b[33] = (uint8_t)tl;
-        for (uint32_t i = 0; i < tl; i++) b[34 + i] = (uint8_t)tag[i];
-        uint32_t d[8];
-        sha256_buf(b, 34 + tl, d);
-        st_words_to_bytes(d, s.st);
+    fs_hash_msg(s, 0, 0x02, tag, zk_strlen(tag), false, nullptr, 0, 0, s.st);
+    // squeeze messages st || k (33 bytes, one block each) built by all lanes, hashed by lanes 0 and 1
+    for (int k = 0; k < 2; k++) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[k]);
+        for (uint32_t p = lane; p < 64; p += 32) {
+            uint8_t v;
+            if (p < 32) v = s.st[p];
+            else if (p == 32) v = (uint8_t)k;
+            else if (p == 33) v = 0x80;
+            else if (p == 62) v = (uint8_t)((33 * 8) >> 8);
+            else if (p == 63) v = (uint8_t)(33 * 8);
+            else v = 0;
+            b[p] = v;
+        }
     }
     __syncwarp();
-    __shared__ fr_t half[2];
     if (lane < 2) {
-        uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[lane]);
-        for (int i = 0; i < 32; i++) b[i] = s.st[i];
-        b[32] = (uint8_t)lane;
-        uint32_t d[8];
-        sha256_buf(b, 33, d);
-        // digest bytes are d[i] big-endian; as a little-endian 256-bit integer limb i = bytes 4i..4i+3
+        uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+        sha256_compress(h, s.buf[lane]);
+        // digest bytes are h[i] big-endian; as a little-endian 256-bit integer limb i = bytes 4i..4i+3
         fr_t x;
-        for (int i = 0; i < 8; i++) x.v[i] = bswap32(d[i]);
-        half[lane] = x;   // lane 0: lo, lane 1: hi
+        for (int i = 0; i < 8; i++) x.v[i] = bswap32(h[i]);
+        s.half[lane] = x;   // lane 0: lo, lane 1: hi
     }
     __syncwarp();
     if (lane < 4) {
-        const fr_t lo = half[0], hi = half[1];
+        const fr_t lo = s.half[0], hi = s.half[1];
         fr_t v;
         if (lane == 0) v = fr_mul_cold(ZK_R2, lo);          // mont part of lo
         else if (lane == 1) v = fr_mul_cold(ZK_R3, hi);     // mont part of hi * 2^256
