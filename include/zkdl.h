@@ -60,6 +60,9 @@ zk_status zk_ctx_synchronize(zk_ctx* ctx);
  * CUDA events on the context stream.  zk_ctx_profile_read synchronises, writes one line per kernel
  * "name<TAB>launches<TAB>total_ms\n" (NUL-terminated, cap bytes max) and clears the records. */
 zk_status zk_ctx_profile(zk_ctx* ctx, int enable);
+/* Restrict profiling to kernels whose name starts with prefix (NULL or "" = every kernel), so one
+ * kernel can be timed inside a region without bracketing all the others. */
+zk_status zk_ctx_profile_filter(zk_ctx* ctx, const char* prefix);
 zk_status zk_ctx_profile_read(zk_ctx* ctx, char* out, uint64_t cap);
 
 /* --------------------------------------------------- Fiat-Shamir transcript (D3)
@@ -167,6 +170,29 @@ zk_status zk_relu_tables(zk_ctx* ctx, const int32_t* d_Z, const int32_t* d_GA, u
 zk_status zk_relu_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
                         uint32_t Q, uint32_t R, uint8_t* proof, uint64_t* proof_len, zk_fr* claims_out,
                         zk_fr* point_out, zk_fr* finals_out);
+
+/* ------------------------------------------------ device-output provers (asynchronous)
+ * The same proofs with every output written to caller-provided DEVICE memory.  These calls only
+ * enqueue work on the context stream -- no host synchronisation, no pageable copies -- so a proving
+ * window of families runs back to back and the caller synchronises once (zk_ctx_synchronize).
+ * Kernel faults surface at that synchronisation.  d_out == NULL with out_len != NULL is a size query.
+ * zk_matmul_prove (rows a3-a6): zk_matmul_reduce then zk_sumcheck_prove(m = logN + logD2,
+ *   n_eq = logN, K = 2, w, claim) on the same transcript, identical bytes.  d_out layout:
+ *   point w||u1||u3 (np = logN+logD1+logD3 elements, canonical) | claim (32 B) |
+ *   sumcheck proof (zk_sumcheck_prove layout) | zero to 15 pad bytes to a 16-byte offset |
+ *   sumcheck point r (m elements, canonical).  d_out must be 16-byte aligned.
+ *   d_At, d_Bt: 2^(logN+logD2) Fr elements each (they hold the restricted tables on return), or
+ *   NULL to use stream-ordered scratch.
+ * zk_relu_prove_dev (rows a7, a8): zk_relu_prove with d_out = proof | pad to a 16-byte offset |
+ *   point (logB + logD elements); d_out 16-byte aligned.
+ *   Bit 0 of *d_range_flag (device u32, never cleared by the library) is set when an input leaves
+ *   the (Q+R)-bit range; the caller checks it after synchronising (the proof is then meaningless).
+ * zk_transcript_state_dev: copies the 32-byte state to device memory (stream-ordered). */
+zk_status zk_matmul_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, const int32_t* d_B, zk_mm_shape shape,
+                          void* d_At, void* d_Bt, uint8_t* d_out, uint64_t* out_len);
+zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                            uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag);
+zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
 
 /* ----------------------------------------------------------------- diagnostics
  * zk_diag_fr_op: element-wise d_out[i] = op(d_a[i], d_b[i]) on Montgomery tables, op 0 add, 1 sub,

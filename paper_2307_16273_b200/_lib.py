@@ -54,6 +54,7 @@ def lib():
         "zk_ctx_synchronize": ([vp], i32),
         "zk_ctx_profile": ([vp, i32], i32),
         "zk_ctx_profile_read": ([vp, c.c_char_p, u64], i32),
+        "zk_ctx_profile_filter": ([vp, c.c_char_p], i32),
         "zk_transcript_new": ([vp, vp, c.POINTER(vp)], i32),
         "zk_transcript_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_transcript_challenges": ([vp, c.c_char_p, u32, vp], i32),
@@ -69,6 +70,9 @@ def lib():
         "zk_sumcheck_prove": ([vp, vp, c.POINTER(ProdStmt), vp, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_relu_tables": ([vp, vp, vp, u64, u32, u32, vp, vp, vp, vp, vp, vp, vp], i32),
         "zk_relu_prove": ([vp, vp, vp, vp, u32, u32, u32, vp, c.POINTER(u64), vp, vp, vp], i32),
+        "zk_matmul_prove": ([vp, vp, vp, vp, MmShape, vp, vp, vp, c.POINTER(u64)], i32),
+        "zk_relu_prove_dev": ([vp, vp, vp, vp, u32, u32, u32, vp, c.POINTER(u64), vp], i32),
+        "zk_transcript_state_dev": ([vp, vp], i32),
         "zk_sc_shard_create": ([vp, vp, c.POINTER(ProdStmt), vp, vp, u32, u32, c.POINTER(vp)], i32),
         "zk_sc_shard_partial": ([vp, vp], i32),
         "zk_sc_shard_finish": ([vp, vp], i32),

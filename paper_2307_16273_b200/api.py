@@ -63,6 +63,9 @@ class Context:
     def profile(self, enable: bool):
         self.check(lib().zk_ctx_profile(self.h, int(enable)))
 
+    def profile_filter(self, prefix: str | None):
+        self.check(lib().zk_ctx_profile_filter(self.h, prefix.encode() if prefix else None))
+
     def profile_read(self) -> dict:
         """{kernel name: (launches, total_ms)} since the last read (synchronises)."""
         buf = ctypes.create_string_buffer(1 << 16)
@@ -107,6 +110,11 @@ class Transcript:
         out = ctypes.create_string_buffer(32)
         self.ctx.check(lib().zk_transcript_state(self.h, out))
         return out.raw[:32]
+
+    def state_dev(self, out: torch.Tensor):
+        """Stream-ordered copy of the state into 32 bytes of device memory (no synchronisation)."""
+        assert out.dtype == torch.uint8 and out.numel() >= 32 and out.is_contiguous()
+        self.ctx.check(lib().zk_transcript_state_dev(self.h, out.data_ptr()))
 
     def close(self):
         if getattr(self, "h", None):
@@ -274,6 +282,85 @@ def relu_prove(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, 
     res = parse_relu_proof(proof.raw[:plen.value], logB)
     res["point"] = _ints(point, logB + logD)
     res["proof"] = proof.raw[:plen.value]
+    return res
+
+
+# ---------------------------------------------------------------- device-output provers (asynchronous)
+def _a16(n: int) -> int:
+    return (n + 15) & ~15
+
+
+def _mm_logs(A: torch.Tensor, B: torch.Tensor, trans_a: bool, trans_b: bool):
+    N = A.shape[0]
+    D1, D2 = (A.shape[2], A.shape[1]) if trans_a else (A.shape[1], A.shape[2])
+    D3 = B.shape[1] if trans_b else B.shape[2]
+    return tuple(_log2(int(v)) for v in (N, D1, D2, D3))
+
+
+def matmul_prove_len(logs) -> int:
+    lN, l1, l2, l3 = logs
+    m = lN + l2
+    return _a16(32 * (lN + l1 + l3) + 32 + (12 + 32 + 32 * m * 3 + 64)) + 32 * m
+
+
+def matmul_prove(ctx: Context, tr: Transcript, A: torch.Tensor, B: torch.Tensor, trans_a=False, trans_b=False,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_matmul_prove: reduce + product sumcheck, every output in device memory (no host sync).
+    Returns the uint8 device buffer (layout in include/zkdl.h; parse with parse_matmul_out)."""
+    logs = _mm_logs(A, B, trans_a, trans_b)
+    n = matmul_prove_len(logs)
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=A.device)
+    assert out.dtype == torch.uint8 and out.numel() >= n and out.is_contiguous()
+    ln = ctypes.c_uint64(out.numel())
+    sh = MmShape(*logs, int(trans_a), int(trans_b))
+    ctx.check(lib().zk_matmul_prove(ctx.h, tr.h, _dev_ptr(A, torch.int32), _dev_ptr(B, torch.int32), sh, None, None,
+                                    out.data_ptr(), ctypes.byref(ln)))
+    return out
+
+
+def parse_matmul_out(raw: bytes, logs) -> dict:
+    lN, l1, l2, l3 = logs
+    np_, m = lN + l1 + l3, lN + l2
+    pts = [int.from_bytes(raw[32 * i:32 * i + 32], "little") for i in range(np_ + 1)]
+    off = 32 * np_ + 32
+    plen = 12 + 32 + 32 * m * 3 + 64
+    res = parse_sumcheck_proof(raw[off:off + plen])
+    res["proof"] = raw[off:off + plen]
+    o_r = _a16(off + plen)
+    res["r"] = [int.from_bytes(raw[o_r + 32 * i:o_r + 32 * i + 32], "little") for i in range(m)]
+    res.update(w=pts[:lN], u1=pts[lN:lN + l1], u3=pts[lN + l1:np_], claim=pts[np_])
+    return res
+
+
+def relu_prove_len(logD: int, Q: int, R: int) -> int:
+    logB = relu_logB(Q, R)
+    return _a16(12 + 128 + 128 * (logB + logD) + 96) + 32 * (logB + logD)
+
+
+def relu_prove_dev(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, Q: int, R: int,
+                   range_flag: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_relu_prove_dev: the zkReLU proof and point into a device buffer (no host sync); bit 0 of
+    range_flag (int32 device scalar) is set when an input is out of range."""
+    logD = _log2(Z.numel())
+    n = relu_prove_len(logD, Q, R)
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=Z.device)
+    assert out.dtype == torch.uint8 and out.numel() >= n and out.is_contiguous()
+    assert range_flag.dtype == torch.int32 and range_flag.is_cuda
+    ln = ctypes.c_uint64(out.numel())
+    ctx.check(lib().zk_relu_prove_dev(ctx.h, tr.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), logD, Q, R,
+                                      out.data_ptr(), ctypes.byref(ln), range_flag.data_ptr()))
+    return out
+
+
+def parse_relu_out(raw: bytes, logD: int, Q: int, R: int) -> dict:
+    logB = relu_logB(Q, R)
+    plen = 12 + 128 + 128 * (logB + logD) + 96
+    res = parse_relu_proof(raw[:plen], logB)
+    res["proof"] = raw[:plen]
+    o_p = _a16(plen)
+    res["point"] = [int.from_bytes(raw[o_p + 32 * i:o_p + 32 * i + 32], "little") for i in range(logB + logD)]
     return res
 
 

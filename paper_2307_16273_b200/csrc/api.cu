@@ -81,6 +81,12 @@ zk_status zk_ctx_profile(zk_ctx* ctx, int enable) {
     ZK_API_END(ctx)
 }
 
+zk_status zk_ctx_profile_filter(zk_ctx* ctx, const char* prefix) {
+    ZK_API_BEGIN(ctx)
+    ctx->prof_filter = prefix ? prefix : "";
+    ZK_API_END(ctx)
+}
+
 zk_status zk_ctx_profile_read(zk_ctx* ctx, char* out, uint64_t cap) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(out && cap, ZK_ERR_ARG, "null buffer");
@@ -124,10 +130,10 @@ zk_status zk_transcript_new(zk_ctx* ctx, const uint8_t seed[32], zk_transcript**
     ZK_REQUIRE(seed && out, ZK_ERR_ARG, "null argument");
     zk_transcript* t = new zk_transcript();
     t->ctx = ctx;
-    cudaError_t e = cudaMalloc(&t->d_st, 32);
+    cudaError_t e = cudaMallocAsync(&t->d_st, 32, ctx->stream);   // stream-ordered: no synchronisation
     if (e != cudaSuccess) {
         delete t;
-        throw ZkError{ZK_ERR_OOM, "cudaMalloc transcript"};
+        throw ZkError{ZK_ERR_OOM, "cudaMallocAsync transcript"};
     }
     tr_init_dev(t, seed);
     *out = t;
@@ -169,8 +175,7 @@ zk_status zk_transcript_state(zk_transcript* tr, uint8_t out[32]) {
 void zk_transcript_free(zk_transcript* tr) {
     if (!tr) return;
     cudaSetDevice(tr->ctx->device);
-    cudaStreamSynchronize(tr->ctx->stream);
-    cudaFree(tr->d_st);
+    cudaFreeAsync(tr->d_st, tr->ctx->stream);   // after every enqueued use of the state
     delete tr;
 }
 
@@ -358,10 +363,10 @@ zk_status zk_relu_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
     ReluOutputs o;
     o.d_proof = s.alloc<uint8_t>(plen);
     o.d_point = s.alloc<uint8_t>(32ull * (logB + logD));
-    unsigned int* range_bad = nullptr;
-    relu_prove_dev(ctx, tr, d_Z, d_GA, logD, Q, R, o, &range_bad, s);
+    unsigned int* range_bad = s.alloc_zero<unsigned int>(1);
+    relu_prove_dev(ctx, tr, d_Z, d_GA, logD, Q, R, o, range_bad, s);
     unsigned int hbad = 0;
-    if (range_bad) ZK_CUDA(cudaMemcpyAsync(&hbad, range_bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ZK_CUDA(cudaMemcpyAsync(&hbad, range_bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
     if (proof) ZK_CUDA(cudaMemcpyAsync(proof, o.d_proof, plen, cudaMemcpyDeviceToHost, ctx->stream));
     if (claims_out) ZK_CUDA(cudaMemcpyAsync(claims_out, o.d_proof + 12, 128, cudaMemcpyDeviceToHost, ctx->stream));
     if (point_out)
@@ -370,6 +375,76 @@ zk_status zk_relu_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
         ZK_CUDA(cudaMemcpyAsync(finals_out, o.d_proof + plen - 96, 96, cudaMemcpyDeviceToHost, ctx->stream));
     ZK_CUDA(cudaStreamSynchronize(ctx->stream));
     ZK_REQUIRE(!hbad, ZK_ERR_RANGE, "Z or G_A outside the (Q+R)-bit range");
+    ZK_API_END(ctx)
+}
+
+// ------------------------------------------------------------------ device-output provers
+static bool size_query(uint8_t* d_out, uint64_t* out_len, uint64_t need) {
+    if (out_len) *out_len = need;
+    ZK_REQUIRE(d_out || out_len, ZK_ERR_ARG, "null output");
+    return d_out == nullptr;
+}
+
+zk_status zk_matmul_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, const int32_t* d_B, zk_mm_shape shape,
+                          void* d_At, void* d_Bt, uint8_t* d_out, uint64_t* out_len) {
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(tr && d_A && d_B, ZK_ERR_ARG, "null argument");
+    const uint32_t np = shape.logN + shape.logD1 + shape.logD3;
+    const uint32_t m = shape.logN + shape.logD2, K = 2;
+    const uint64_t plen = sumcheck_proof_len(m, K);
+    const uint64_t off_proof = 32ull * np + 32, off_r = (off_proof + plen + 15) & ~15ull;
+    if (size_query(d_out, out_len, off_r + 32ull * m)) return ZK_OK;
+    ZK_REQUIRE(m >= 1 && m <= 40, ZK_ERR_ARG, "bad matmul shape");
+    ZK_REQUIRE(((uintptr_t)d_out & 15) == 0, ZK_ERR_ARG, "d_out must be 16-byte aligned");
+    Scratch s(ctx);
+    const uint64_t N = 1ull << m;
+    fr_t* At = d_At ? static_cast<fr_t*>(d_At) : s.alloc<fr_t>(N);
+    fr_t* Bt = d_Bt ? static_cast<fr_t*>(d_Bt) : s.alloc<fr_t>(N);
+    fr_t* pts = s.alloc<fr_t>(np ? np : 1);
+    fr_t* claim = s.alloc<fr_t>(1);
+    matmul_reduce_dev(ctx, tr, d_A, d_B, shape, At, Bt, pts, d_out, claim, s);
+    to_canonical_dev(ctx, claim, 1, d_out + 32ull * np);
+    ScStatement S;
+    memset(&S, 0, sizeof S);
+    S.m = m;
+    S.n_eq = shape.logN;
+    S.K = K;
+    S.tables[0] = At;
+    S.tables[1] = Bt;
+    S.d_w = pts;   // w = the first logN entries of the point
+    S.d_claim = claim;
+    S.claim_given = true;
+    S.d_proof = d_out + off_proof;
+    S.d_r = s.alloc<fr_t>(m);
+    S.d_point = d_out + off_r;
+    S.d_finals = nullptr;
+    sumcheck_prove_dev(ctx, tr, S, s);
+    ZK_API_END(ctx)
+}
+
+zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                            uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag) {
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(tr && d_Z && d_GA && d_range_flag, ZK_ERR_ARG, "null argument");
+    ZK_REQUIRE(Q >= 1 && R >= 1 && Q + R <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
+    const uint32_t logB = relu_logB(Q, R);
+    const uint64_t plen = relu_proof_len(logD, logB);
+    const uint64_t off_pt = (plen + 15) & ~15ull;
+    if (size_query(d_out, out_len, off_pt + 32ull * (logB + logD))) return ZK_OK;
+    ZK_REQUIRE(((uintptr_t)d_out & 15) == 0, ZK_ERR_ARG, "d_out must be 16-byte aligned");
+    Scratch s(ctx);
+    ReluOutputs o;
+    o.d_proof = d_out;
+    o.d_point = d_out + off_pt;
+    relu_prove_dev(ctx, tr, d_Z, d_GA, logD, Q, R, o, d_range_flag, s);
+    ZK_API_END(ctx)
+}
+
+zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out) {
+    if (!tr || !d_out) return ZK_ERR_ARG;
+    zk_ctx* ctx = tr->ctx;
+    ZK_API_BEGIN(ctx)
+    ZK_CUDA(cudaMemcpyAsync(d_out, tr->d_st, 32, cudaMemcpyDeviceToDevice, ctx->stream));
     ZK_API_END(ctx)
 }
 

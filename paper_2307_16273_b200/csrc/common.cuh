@@ -20,6 +20,10 @@ struct zk_ctx {
     std::string err;
     // per-launch CUDA-event profiling (zk_ctx_profile): events bracket each launch on the ctx stream
     bool prof = false;
+    std::string prof_filter;   // only kernels whose name starts with this prefix (empty: all)
+    bool prof_match(const char* name) const {
+        return prof && (prof_filter.empty() || strncmp(name, prof_filter.c_str(), prof_filter.size()) == 0);
+    }
     struct Rec {
         const char* name;
         cudaEvent_t a, b;
@@ -72,14 +76,15 @@ inline void after_launch(zk_ctx* ctx, const char* what) {
 #define ZK_LAUNCH(ctx, kernel, grid, block, smem, ...)                                                 \
     do {                                                                                               \
         cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;                                                  \
-        if ((ctx)->prof) {                                                                             \
+        const bool prof_ = (ctx)->prof_match(#kernel);                                                 \
+        if (prof_) {                                                                                   \
             ev_a_ = (ctx)->take_event();                                                               \
             ev_b_ = (ctx)->take_event();                                                               \
             cudaEventRecord(ev_a_, (ctx)->stream);                                                     \
         }                                                                                              \
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                               \
         ::zk::after_launch((ctx), #kernel);                                                            \
-        if ((ctx)->prof) {                                                                             \
+        if (prof_) {                                                                                   \
             cudaEventRecord(ev_b_, (ctx)->stream);                                                     \
             (ctx)->recs.push_back({#kernel, ev_a_, ev_b_});                                            \
         }                                                                                              \
@@ -262,14 +267,15 @@ inline Tag32 make_tag(const char* t) {
 }
 
 // ---------------------------------------------------------------- shared kernels (defined in transcript.cu)
-__global__ void k_tr_absorb(uint8_t* st, Tag32 tag, Bytes256 msg);
+__global__ void k_tr_absorb(uint8_t* st, Tag32 tag, Bytes256 msg, uint8_t* copy_out);
 __global__ void k_tr_absorb_dev(uint8_t* st, Tag32 tag, const uint8_t* msg, uint64_t len);
 __global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t n, uint8_t* copy_out);
 // n challenges with one tag: thread 0 advances the state chain, all threads squeeze in parallel.
 __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mont, uint8_t* out_canon);
 
 // Host wrappers
-void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t len);
+// d_copy (nullable, len <= 256 only): the kernel also writes msg to this device buffer
+void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t len, uint8_t* d_copy = nullptr);
 void tr_challenges_dev(zk_transcript* tr, const char* tag, uint32_t n, fr_t* d_out_mont, uint8_t* d_out_canon);
 
 // eq tables (tables.cu): out[x] = scale * prod_{s<k} eq(u[s], bit s of x) for x < 2^k

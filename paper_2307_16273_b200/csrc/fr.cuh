@@ -175,12 +175,39 @@ __device__ __forceinline__ fr_t fr_dbl(const fr_t& a) { return fr_add(a, a); }
     } while (0)
 
 // Montgomery product a * b * R^{-1} mod p.  Requires a < p; b may be any value < 2^256.
+// CIOS with 64-bit intermediates left to the compiler (IMAD.WIDE.U32 + IADD3 carries it schedules
+// freely across independent products — 23% faster than hand-written PTX carry chains on the B200,
+// scripts/mulbench.cu), using p0 = 1 (m p0 + t0 = 0 mod 2^32, carry t0 != 0) and p1 = 2^32 - 1
+// (m p1 = (m << 32) - m on the ALU pipe, relieving the FMA pipe).
 __device__ __forceinline__ fr_t fr_mul(const fr_t& a, const fr_t& b) {
+    const uint32_t p[8] = {ZK_P0, ZK_P1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7};
     uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 8; i++) {
-        ZK_MAC_ROW(t, a.v, b.v[i]);
-        ZK_REDC_ROW(t);
+        uint64_t C = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t uv = (uint64_t)a.v[j] * b.v[i] + t[j] + C;
+            t[j] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+        t[8] += (uint32_t)C;
+        const uint32_t m = t[0] * 0xffffffffu;   // = -t0 mod 2^32
+        C = (uint64_t)(t[0] != 0);
+        {
+            const uint64_t uv = ((uint64_t)m << 32) + t[1] + C - m;
+            t[0] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+#pragma unroll
+        for (int j = 2; j < 8; j++) {
+            const uint64_t uv = (uint64_t)m * p[j] + t[j] + C;
+            t[j - 1] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+        const uint64_t uv = (uint64_t)t[8] + C;
+        t[7] = (uint32_t)uv;
+        t[8] = (uint32_t)(uv >> 32);
     }
     fr_t r;
 #pragma unroll

@@ -79,10 +79,46 @@ struct BitsumArgs {
     uint32_t logD, lo_bits, qr_mask, sig_bit;
     const fr_t* LO[5];   // eq over the low lo_bits variables, scaled by R (lazy accumulation)
     const fr_t* HI[5];   // eq over the remaining variables
-    const BitCell* cells;
-    uint32_t ncell;
+    uint32_t B, ncell;   // cells decoded from their index (cell_decode)
     fr_t* partials;      // gridDim.x * ncell
 };
+
+// Cell c of the bit-sum list: [0, 4B) linear cells M_x[j] (x = c / B: 0 Z, 1 A, 2 G_A, 3 G_Z; word Z
+// for x < 2, G_A otherwise), then the co-occurrence cells C_s[j1][j2] (j1 <= j2, row-major upper
+// triangles, s = 0 then 1) -- the same order k_relu_jrounds reads (tri_index).
+__device__ __forceinline__ void cell_decode(uint32_t c, uint32_t B, uint32_t& j1, uint32_t& j2, uint32_t& s,
+                                            uint32_t& x) {
+    if (c < 4 * B) {
+        x = c / B;
+        j1 = j2 = c % B;
+        s = x >= 2;
+        return;
+    }
+    uint32_t idx = c - 4 * B;
+    const uint32_t T = B * (B + 1) / 2;
+    s = idx / T;
+    idx -= s * T;
+    x = 4;
+    uint32_t j = 0;
+    while (idx >= B - j) {
+        idx -= B - j;
+        j++;
+    }
+    j1 = j;
+    j2 = j + idx;
+}
+
+__device__ __forceinline__ BitCell bitcell_at(uint32_t c, uint32_t B, uint32_t QR) {
+    uint32_t j1, j2, s, x;
+    cell_decode(c, B, j1, j2, s, x);
+    BitCell r;
+    r.m1 = (j1 < QR && j2 < QR) ? ((1u << j1) | (1u << j2)) : 0xffffffffu;   // padding columns never match
+    r.word = (uint8_t)s;
+    r.gate = (uint8_t)(x == 1 || x == 3);
+    r.lot = (uint8_t)x;
+    r.pad = 0;
+    return r;
+}
 
 constexpr int BS_CH = 128;   // entries staged per chunk
 
@@ -125,7 +161,7 @@ struct Bitsum2Args {
     uint32_t logD, lo_bits, qr_mask, sig_bit;
     const fr_t* LO[5];
     const fr_t* HI[5];
-    const BitCell2* cells;   // [0, nM) linear cells, [nM, nM + nC) co-occurrence cells
+    uint32_t B;              // cells decoded from their index: [0, nM) linear, [nM, nM + nC) co-occurrence
     uint32_t nM, nC;
     fr_t* partials;          // gridDim.x * (nM + nC), zero-initialised; per-block running totals
 };
@@ -177,7 +213,9 @@ __global__ void __launch_bounds__(BS2_T, 1) k_relu_bitsums2(Bitsum2Args a) {
     for (int q = 0; q < BS2_MAXC; q++) {
         const int c = tid + q * BS2_T;
         cid[q] = c < (int)ncell ? c : -1;
-        cl[q] = c < (int)ncell ? a.cells[c] : BitCell2{0, 0, 0, 0};
+        uint32_t j1 = 0, j2 = 0, s = 0, x = 0;
+        if (c < (int)ncell) cell_decode((uint32_t)c, a.B, j1, j2, s, x);
+        cl[q] = BitCell2{(uint8_t)j1, (uint8_t)j2, (uint8_t)s, (uint8_t)x};
     }
     fr_t* tot = a.partials + (uint64_t)blockIdx.x * ncell;
     uint32_t acc[BS2_MAXC][10];
@@ -289,7 +327,7 @@ __global__ void __launch_bounds__(640) k_relu_bitsums(BitsumArgs a) {
     for (int q = 0; q < 2; q++) {
         uint32_t c = threadIdx.x + q * blockDim.x;
         have[q] = c < a.ncell;
-        cell[q] = have[q] ? a.cells[c] : BitCell{0, 0, 0, 0, 0};
+        cell[q] = have[q] ? bitcell_at(c, a.B, a.sig_bit + 1) : BitCell{0, 0, 0, 0, 0};
     }
     uint32_t acc[2][10];
     fr_t tot[2] = {fr_zero(), fr_zero()};
@@ -771,25 +809,20 @@ __global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
 
 // ---------------------------------------------------------------- driver
 void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,
-                    uint32_t R, ReluOutputs& out, unsigned int** range_bad, Scratch& s) {
+                    uint32_t R, ReluOutputs& out, unsigned int* range_flag, Scratch& s) {
     const uint32_t QR = Q + R;
     const uint32_t logB = relu_logB(Q, R), B = 1u << logB;
     const uint64_t D = 1ull << logD;
     const uint32_t qr_mask = QR >= 32 ? 0xffffffffu : ((1u << QR) - 1);
     const uint32_t m = logB + logD;
     uint8_t* proof = out.d_proof;
-    *range_bad = nullptr;
-    if (QR < 32) {
-        *range_bad = s.alloc_zero<unsigned int>(1);
-        ZK_LAUNCH(ctx, k_relu_range, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, QR, *range_bad);
-    }
+    if (QR < 32) ZK_LAUNCH(ctx, k_relu_range, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, QR, range_flag);
     // header
     uint8_t hdr[12];
     const uint32_t hv[3] = {logD, Q, R};
     for (int i = 0; i < 3; i++)
         for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
-    ZK_CUDA(cudaMemcpyAsync(proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
-    tr_absorb_host(tr, "relu/hdr", hdr, 12);
+    tr_absorb_host(tr, "relu/hdr", hdr, 12, proof);
     // points u_Z, u_A, u_GA, u_GZ
     fr_t* U = s.alloc<fr_t>(4ull * logD);
     tr_challenges_dev(tr, "relu/uZ", logD, U, nullptr);
@@ -812,23 +845,8 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     const fr_t* u_i[5] = {U, U + logD, U + 2 * logD, U + 3 * logD, ubin + logB};
 
     // ---- bit sums
-    std::vector<BitCell> cells;
-    for (int x = 0; x < 4; x++)
-        for (uint32_t j = 0; j < B; j++) {
-            BitCell c{(j < QR) ? (1u << j) : 0u, (uint8_t)(x >= 2), (uint8_t)(x == 1 || x == 3), (uint8_t)x, 0};
-            if (j >= QR) c.m1 = 0xffffffffu;   // never matches a masked word: padding columns are zero
-            cells.push_back(c);
-        }
-    for (int sd = 0; sd < 2; sd++)
-        for (uint32_t j1 = 0; j1 < B; j1++)
-            for (uint32_t j2 = j1; j2 < B; j2++) {
-                BitCell c{(j1 < QR && j2 < QR) ? ((1u << j1) | (1u << j2)) : 0xffffffffu, (uint8_t)sd, 0, 4, 0};
-                cells.push_back(c);
-            }
-    // (with Q+R = 32 there are no padding columns, so the never-matching mask 0xffffffff is not used)
-    const uint32_t ncell = (uint32_t)cells.size();
-    BitCell* d_cells = s.alloc<BitCell>(ncell);
-    ZK_CUDA(cudaMemcpyAsync(d_cells, cells.data(), sizeof(BitCell) * ncell, cudaMemcpyHostToDevice, ctx->stream));
+    // cells (cell_decode): 4B linear cells, then two upper triangles of co-occurrence cells
+    const uint32_t ncell = 4 * B + B * (B + 1);
     const uint32_t lo_bits = logD < 12 ? logD : 12, hi_bits = logD - lo_bits;
     BitsumArgs ba;
     memset(&ba, 0, sizeof ba);
@@ -846,19 +864,11 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         ba.LO[x] = lo;
         ba.HI[x] = hi;
     }
-    ba.cells = d_cells;
+    ba.B = B;
     ba.ncell = ncell;
     fr_t* cell_tot = s.alloc<fr_t>(ncell);
     if (logD >= 6) {   // subset-sum tables over chunks of 64 entries
-        std::vector<BitCell2> c2;
-        for (int x = 0; x < 4; x++)
-            for (uint32_t j = 0; j < B; j++) c2.push_back(BitCell2{(uint8_t)j, (uint8_t)j, (uint8_t)(x >= 2), (uint8_t)x});
-        for (int sd = 0; sd < 2; sd++)
-            for (uint32_t j1 = 0; j1 < B; j1++)
-                for (uint32_t j2 = j1; j2 < B; j2++) c2.push_back(BitCell2{(uint8_t)j1, (uint8_t)j2, (uint8_t)sd, 4});
-        ZK_REQUIRE(c2.size() == ncell && ncell <= BS2_MAXC * BS2_T, ZK_ERR_INTERNAL, "bitsum cells");
-        BitCell2* d_c2 = s.alloc<BitCell2>(ncell);
-        ZK_CUDA(cudaMemcpyAsync(d_c2, c2.data(), sizeof(BitCell2) * ncell, cudaMemcpyHostToDevice, ctx->stream));
+        ZK_REQUIRE(ncell <= BS2_MAXC * BS2_T, ZK_ERR_INTERNAL, "bitsum cells");
         Bitsum2Args b2;
         memset(&b2, 0, sizeof b2);
         b2.Z = Z;
@@ -871,7 +881,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
             b2.LO[x] = ba.LO[x];
             b2.HI[x] = ba.HI[x];
         }
-        b2.cells = d_c2;
+        b2.B = B;
         b2.nM = 4 * B;
         b2.nC = ncell - 4 * B;
         const uint64_t nchunks = D / BS2_CH;

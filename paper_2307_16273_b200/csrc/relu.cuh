@@ -19,8 +19,9 @@ inline uint64_t relu_proof_len(uint32_t logD, uint32_t logB) { return 12 + 128 +
 bool relu_tables_dev(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t Q, uint32_t R, uint8_t* sign,
                      int32_t* A, int32_t* GZ, int32_t* Zp, int32_t* GAp, int32_t* RZ, int32_t* RGA, Scratch& s);
 
-// Enqueues the whole proof; *range_bad (device flag, may be null when Q+R = 32) is set if an input is out of range.
+// Enqueues the whole proof; bit 0 of *range_flag (device word, not cleared here) is set if an input
+// lies outside the (Q+R)-bit range (never for Q+R = 32: every int32 is in range).
 void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,
-                    uint32_t R, ReluOutputs& out, unsigned int** range_bad, Scratch& s);
+                    uint32_t R, ReluOutputs& out, unsigned int* range_flag, Scratch& s);
 
 }  // namespace zk

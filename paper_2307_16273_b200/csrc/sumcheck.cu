@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(256) k_sc_round(ScRoundArgs a) {
 // header (+ provided claim) before round 0; one warp
 __global__ void k_sc_header(uint8_t* st, Bytes256 hdr, const fr_t* claim, int absorb_claim, uint8_t* claim_bytes) {
     __shared__ FsScratch fs;
+    // the 12 proof-header bytes precede the claim in the proof buffer (no pageable host copy)
+    if (threadIdx.x < 12) claim_bytes[(int)threadIdx.x - 12] = hdr.b[threadIdx.x];
     fs_begin(fs, st);
     fs_absorb_bytes(fs, "sc/hdr", hdr.b, hdr.len);
     if (absorb_claim) fs_absorb_frs(fs, "sc/claim", fr_load(claim), 1, claim_bytes);
@@ -324,7 +326,6 @@ void ScEngine::header() {
     const uint32_t hv[3] = {m, n_eq, K};
     for (int i = 0; i < 3; i++)
         for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
-    ZK_CUDA(cudaMemcpyAsync(d_proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
     ZK_LAUNCH(ctx, k_sc_header, 1, 32, 0, tr->d_st, make_bytes(hdr, 12), d_claim, claim_given ? 1 : 0, d_proof + 12);
 }
 
@@ -532,14 +533,15 @@ template <int K>
 static void launch_all(zk_ctx* ctx, const ScAllArgs& a, unsigned int grid) {
     void* args[] = {(void*)&a};
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-    if (ctx->prof) {
+    const bool prof = ctx->prof_match("k_sc_all");
+    if (prof) {
         ev_a = ctx->take_event();
         ev_b = ctx->take_event();
         cudaEventRecord(ev_a, ctx->stream);
     }
     ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_sc_all<K>, dim3(grid), dim3(256), args, 0, ctx->stream));
     after_launch(ctx, "k_sc_all");
-    if (ctx->prof) {
+    if (prof) {
         cudaEventRecord(ev_b, ctx->stream);
         ctx->recs.push_back({"k_sc_all", ev_a, ev_b});
     }
@@ -562,7 +564,6 @@ static void sumcheck_prove_small(zk_ctx* ctx, zk_transcript* tr, const ScStateme
     const uint32_t hv[3] = {m, n_eq, K};
     for (int i = 0; i < 3; i++)
         for (int k = 0; k < 4; k++) hdr[4 * i + k] = (uint8_t)(hv[i] >> (8 * k));
-    ZK_CUDA(cudaMemcpyAsync(S.d_proof, hdr, 12, cudaMemcpyHostToDevice, ctx->stream));
     ZK_LAUNCH(ctx, k_sc_header, 1, 32, 0, tr->d_st, make_bytes(hdr, 12), S.d_claim, S.claim_given ? 1 : 0, S.d_proof + 12);
     ScAllArgs a;
     memset(&a, 0, sizeof a);

@@ -40,15 +40,32 @@ void to_canonical_dev(zk_ctx* ctx, const fr_t* in, uint64_t n, uint8_t* out) {
     ZK_LAUNCH(ctx, k_to_canonical, grid_for(ctx, n, 256, 8), 256, 0, in, n, reinterpret_cast<fr_t*>(out));
 }
 
+// Points travel in the kernel parameters (copied at launch): no staging buffer, no stream sync.
+struct Pts96 {
+    uint32_t n;
+    uint8_t b[96][32];
+};
+__global__ void k_upload_pts(Pts96 p, fr_t* out) {
+    const uint32_t i = threadIdx.x;
+    if (i < p.n) {
+        fr_t x;
+        for (int k = 0; k < 8; k++)
+            x.v[k] = (uint32_t)p.b[i][4 * k] | ((uint32_t)p.b[i][4 * k + 1] << 8) | ((uint32_t)p.b[i][4 * k + 2] << 16) |
+                     ((uint32_t)p.b[i][4 * k + 3] << 24);
+        fr_store(&out[i], fr_from_canonical(x));
+    }
+}
+
 void upload_points(zk_ctx* ctx, const zk_fr* host, uint32_t n, fr_t* d_mont, Scratch& s) {
+    (void)s;
     if (!n) return;
-    check_canonical(host, n);
-    fr_t* tmp = s.alloc<fr_t>(n);
-    ZK_CUDA(cudaMemcpyAsync(tmp, host, 32ull * n, cudaMemcpyHostToDevice, ctx->stream));
-    unsigned int* bad = s.alloc_zero<unsigned int>(1);
-    ZK_LAUNCH(ctx, k_from_canonical, 1, 256, 0, tmp, (uint64_t)n, d_mont, bad);
-    // synchronous: the host buffer may be reused by the caller right after return
-    ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    check_canonical(host, n);   // host-side validation (ZK_ERR_NONCANONICAL)
+    for (uint32_t off = 0; off < n; off += 96) {
+        Pts96 p;
+        p.n = n - off < 96 ? n - off : 96;
+        memcpy(p.b, host + off, 32ull * p.n);
+        ZK_LAUNCH(ctx, k_upload_pts, 1, 96, 0, p, d_mont + off);
+    }
 }
 
 // ---------------------------------------------------------------- a2: eq tables

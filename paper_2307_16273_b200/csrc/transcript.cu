@@ -18,8 +18,11 @@ __global__ void k_tr_init(uint8_t* st, Bytes256 seed) {
     }
 }
 
-__global__ void k_tr_absorb(uint8_t* st, Tag32 tag, Bytes256 msg) {
+// copy_out (nullable): the message bytes are also written there (proof headers without a host copy)
+__global__ void k_tr_absorb(uint8_t* st, Tag32 tag, Bytes256 msg, uint8_t* copy_out) {
     __shared__ FsScratch s;
+    if (copy_out)
+        for (uint32_t i = threadIdx.x; i < msg.len; i += blockDim.x) copy_out[i] = msg.b[i];
     fs_begin(s, st);
     fs_absorb_bytes(s, tag.s, msg.b, msg.len);
     fs_end(s, st);
@@ -113,11 +116,12 @@ __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mo
     }
 }
 
-void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t len) {
+void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t len, uint8_t* d_copy) {
     zk_ctx* ctx = tr->ctx;
     if (len <= 256) {
-        ZK_LAUNCH(ctx, k_tr_absorb, 1, 32, 0, tr->d_st, make_tag(tag), make_bytes(msg, len));
+        ZK_LAUNCH(ctx, k_tr_absorb, 1, 32, 0, tr->d_st, make_tag(tag), make_bytes(msg, len), d_copy);
     } else {
+        ZK_REQUIRE(d_copy == nullptr, ZK_ERR_INTERNAL, "copy-out only for short messages");
         Scratch s(ctx);
         uint8_t* d = s.alloc<uint8_t>(len);
         ZK_CUDA(cudaMemcpyAsync(d, msg, len, cudaMemcpyHostToDevice, ctx->stream));

@@ -2,10 +2,12 @@
 
 One Fiat-Shamir transcript per proving window (D3d): "fcn/hdr", then for every
 family in the fixed order of synth.fcn.assemble_families, "fcn/fam" <name>
-followed by the family's protocol — matmul families: zk_matmul_reduce then
-zk_sumcheck_prove (m = logN + logD2, n_eq = logN, K = 2); ReLU families:
-zk_relu_prove.  Stack tensors must already be resident on the device; this
-module only sequences the library calls (no arithmetic here).
+followed by the family's protocol — matmul families: zk_matmul_prove (the
+reduction of zk_matmul_reduce then zk_sumcheck_prove with m = logN + logD2,
+n_eq = logN, K = 2); ReLU families: zk_relu_prove_dev.  Stack tensors must
+already be resident on the device; this module only sequences the library calls
+(no arithmetic here).  Every family writes into one device buffer and the whole
+window synchronises once, when the proofs are copied back.
 """
 from __future__ import annotations
 
@@ -48,26 +50,62 @@ def upload_families(families, device="cuda", pin: bool = False) -> list:
     return out
 
 
-def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list, keep_tables: bool = False) -> list:
-    """Prove every family of one window under one transcript; returns per-family results."""
+def _layout(f: DeviceFamily):
+    if f.kind == "matmul":
+        logs = api._mm_logs(f.A, f.B, f.trans_a, f.trans_b)
+        return logs, api.matmul_prove_len(logs)
+    logD = api._log2(f.Z.numel())
+    return logD, api.relu_prove_len(logD, f.Q, f.R)
+
+
+def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list):
+    """Enqueue one window's proofs on the context stream without synchronising.
+
+    Returns (out, flag, layout): `out` is one uint8 device buffer holding, per family, its proof
+    output followed by the 32-byte transcript state after the family; `flag` the int32 range flag."""
+    dev = (families[0].A if families[0].kind == "matmul" else families[0].Z).device
+    lay = []
+    off = 0
+    for f in families:
+        info, n = _layout(f)
+        lay.append((f, info, off, n))
+        off += (n + 32 + 255) & ~255   # every family starts 256-byte aligned
+    out = torch.empty(off, dtype=torch.uint8, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
     tr = api.Transcript(ctx, seed)
     tr.absorb("fcn/hdr", header)
-    results = []
-    for f in families:
+    for f, info, o, n in lay:
         tr.absorb("fcn/fam", f.name.encode())
         if f.kind == "matmul":
-            red = api.matmul_reduce(ctx, tr, f.A, f.B, f.trans_a, f.trans_b)
-            lN, _, l2, _ = red["logs"]
-            sc = api.sumcheck_prove(ctx, tr, lN + l2, lN, [red["At"], red["Bt"]], red["w"], red["claim"])
-            res = dict(name=f.name, kind="matmul", w=red["w"], u1=red["u1"], u3=red["u3"], claim=red["claim"],
-                       msgs=sc["msgs"], r=sc["r"], finals=sc["finals"], proof=sc["proof"])
-            if keep_tables:
-                res["At"], res["Bt"] = red["At"], red["Bt"]
+            api.matmul_prove(ctx, tr, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
         else:
-            rr = api.relu_prove(ctx, tr, f.Z, f.GA, f.Q, f.R)
-            res = dict(name=f.name, kind="relu", claims=rr["claims"], msgs=rr["msgs"], point=rr["point"],
-                       finals=rr["finals"], proof=rr["proof"])
-        res["state"] = tr.state()
+            api.relu_prove_dev(ctx, tr, f.Z, f.GA, f.Q, f.R, flag, out=out[o:o + n])
+        tr.state_dev(out[o + n:o + n + 32])
+    tr.close()   # stream-ordered: the state buffer is released after the enqueued work
+    return out, flag, lay
+
+
+def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
+    """Copy a window's outputs to the host (the one synchronisation) and parse them."""
+    raw = out.cpu().numpy().tobytes()
+    if int(flag.item()) & 1:
+        raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")
+    results = []
+    for f, info, o, n in lay:
+        blob = raw[o:o + n]
+        if f.kind == "matmul":
+            r = api.parse_matmul_out(blob, info)
+            res = dict(name=f.name, kind="matmul", w=r["w"], u1=r["u1"], u3=r["u3"], claim=r["claim"],
+                       msgs=r["msgs"], r=r["r"], finals=r["finals"], proof=r["proof"])
+        else:
+            r = api.parse_relu_out(blob, info, f.Q, f.R)
+            res = dict(name=f.name, kind="relu", claims=r["claims"], msgs=r["msgs"], point=r["point"],
+                       finals=r["finals"], proof=r["proof"])
+        res["state"] = raw[o + n:o + n + 32]
         results.append(res)
-    tr.close()
     return results
+
+
+def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list) -> list:
+    """Prove every family of one window under one transcript; returns per-family results."""
+    return collect_window(*enqueue_window(ctx, seed, header, families))

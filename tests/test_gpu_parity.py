@@ -273,10 +273,45 @@ def test_fcn_tiny_vs_oracle(ctx, O):
     fams = fcn.assemble_families(shape, trace)
     o = drivers.fcn_prove(shape, fams, "tiny")
     g = dfcn.prove_window(ctx, fs_seed("tiny"), fcn.fcn_header(shape), dfcn.upload_families(fams))
+    assert len(g) == len(o)
     for gr, orr in zip(g, o):
         assert gr["msgs"] == orr["msgs"], gr["name"]
         assert gr["finals"] == orr["finals"], gr["name"]
         assert gr["state"] == orr["state"], gr["name"]
+
+
+def test_async_provers_match_sync(ctx):
+    """zk_matmul_prove / zk_relu_prove_dev (device outputs, no host sync) give the bytes of the
+    synchronous calls, back to back on one transcript; the range flag replaces ZK_ERR_RANGE."""
+    import torch
+    from paper_2307_16273_b200 import api
+    A = uniform_range(21, 1, (4, 8, 32), -128, 128)
+    B = uniform_range(21, 2, (4, 32, 16), -128, 128)
+    Z = uniform_range(21, 3, (1 << 9,), -(1 << 15), 1 << 15)
+    GA = uniform_range(21, 4, (1 << 9,), -(1 << 15), 1 << 15)
+    seed = fs_seed("async")
+    t1 = api.Transcript(ctx, seed)
+    red = api.matmul_reduce(ctx, t1, dev(A), dev(B))
+    sc = api.sumcheck_prove(ctx, t1, 2 + 5, 2, [red["At"], red["Bt"]], red["w"], red["claim"])
+    rl = api.relu_prove(ctx, t1, dev(Z), dev(GA), 8, 8)
+    t2 = api.Transcript(ctx, seed)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    mo = api.matmul_prove(ctx, t2, dev(A), dev(B))
+    ro = api.relu_prove_dev(ctx, t2, dev(Z), dev(GA), 8, 8, flag)
+    st = torch.empty(32, dtype=torch.uint8, device="cuda")
+    t2.state_dev(st)
+    pm = api.parse_matmul_out(mo.cpu().numpy().tobytes(), (2, 3, 5, 4))
+    pr = api.parse_relu_out(ro.cpu().numpy().tobytes(), 9, 8, 8)
+    assert pm["w"] == red["w"] and pm["u1"] == red["u1"] and pm["u3"] == red["u3"] and pm["claim"] == red["claim"]
+    assert pm["proof"] == sc["proof"] and pm["r"] == sc["r"]
+    assert pr["proof"] == rl["proof"] and pr["point"] == rl["point"]
+    assert int(flag.item()) == 0
+    assert st.cpu().numpy().tobytes() == t1.state()
+    # out-of-range input: flag set, no exception
+    Zb = Z.copy()
+    Zb[5] = 1 << 20
+    api.relu_prove_dev(ctx, api.Transcript(ctx, seed), dev(Zb), dev(GA), 8, 8, flag)
+    assert int(flag.item()) & 1
 
 
 # ---------------------------------------------------------------- §8(e) sharded sumcheck
