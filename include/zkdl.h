@@ -60,9 +60,10 @@ zk_status zk_ctx_synchronize(zk_ctx* ctx);
  * CUDA events on the context stream.  zk_ctx_profile_read synchronises, writes one line per kernel
  * "name<TAB>launches<TAB>total_ms\n" (NUL-terminated, cap bytes max) and clears the records. */
 zk_status zk_ctx_profile(zk_ctx* ctx, int enable);
-/* Restrict profiling to kernels whose name starts with prefix (NULL or "" = every kernel), so one
- * kernel can be timed inside a region without bracketing all the others. */
-zk_status zk_ctx_profile_filter(zk_ctx* ctx, const char* prefix);
+/* Restrict profiling to one kernel: name is a kernel's base name (every template instantiation
+ * "name<...>" matches); NULL or "" = every kernel.  Lets one kernel be timed inside a region
+ * without bracketing all the others. */
+zk_status zk_ctx_profile_filter(zk_ctx* ctx, const char* name);
 zk_status zk_ctx_profile_read(zk_ctx* ctx, char* out, uint64_t cap);
 
 /* --------------------------------------------------- Fiat-Shamir transcript (D3)

@@ -20,9 +20,12 @@ struct zk_ctx {
     std::string err;
     // per-launch CUDA-event profiling (zk_ctx_profile): events bracket each launch on the ctx stream
     bool prof = false;
-    std::string prof_filter;   // only kernels whose name starts with this prefix (empty: all)
+    std::string prof_filter;   // only this kernel, every template instantiation (empty: all kernels)
     bool prof_match(const char* name) const {
-        return prof && (prof_filter.empty() || strncmp(name, prof_filter.c_str(), prof_filter.size()) == 0);
+        if (!prof) return false;
+        if (prof_filter.empty()) return true;
+        const size_t n = prof_filter.size();
+        return strncmp(name, prof_filter.c_str(), n) == 0 && (name[n] == '\0' || name[n] == '<');
     }
     struct Rec {
         const char* name;

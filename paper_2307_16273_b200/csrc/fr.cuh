@@ -337,10 +337,26 @@ __device__ __forceinline__ fr_t fr_shfl_down(const fr_t& a, int delta) {
     for (int i = 0; i < 8; i++) r.v[i] = __shfl_down_sync(0xffffffffu, a.v[i], delta);
     return r;
 }
-__device__ __forceinline__ fr_t fr_shfl_xor(const fr_t& a, int mask) {
+__device__ __forceinline__ fr_t fr_shfl_xor(const fr_t& a, int mask, unsigned lanes = 0xffffffffu) {
     fr_t r;
 #pragma unroll
-    for (int i = 0; i < 8; i++) r.v[i] = __shfl_xor_sync(0xffffffffu, a.v[i], mask);
+    for (int i = 0; i < 8; i++) r.v[i] = __shfl_xor_sync(lanes, a.v[i], mask);
+    return r;
+}
+// m * e for a small integer m in [-3, 3] (selects and additions, no multiplication, no branches)
+__device__ __forceinline__ fr_t fr_mul_small(const fr_t& e, int m) {
+    const int am = m < 0 ? -m : m;
+    const fr_t e2 = fr_add(e, e);
+    fr_t r = fr_zero(), t = fr_zero();
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        r.v[i] = (am & 1) ? e.v[i] : 0u;
+        t.v[i] = (am & 2) ? e2.v[i] : 0u;
+    }
+    r = fr_add(r, t);
+    const fr_t n = fr_neg(r);
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = m < 0 ? n.v[i] : r.v[i];
     return r;
 }
 

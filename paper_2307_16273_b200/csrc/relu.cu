@@ -620,6 +620,7 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
     const uint64_t stride = ((uint64_t)gridDim.x * blockDim.x) >> 1;
     for (uint64_t b = first; b < a.n_pairs; b += stride) {
         fr_t av, ad, om, omd;
+        int o0 = 0, od = 0;   // first round: oms(0), oms(1) - oms(0) as small integers (oms is boolean)
         if (FOLD) {
             const fr_t* s = srcA + 4 * b;
             fr_t y0 = fr_load_cg(s), y1 = fr_load_cg(s + 1), y2 = fr_load_cg(s + 2), y3 = fr_load_cg(s + 3);
@@ -629,21 +630,20 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
             fr_store(dstA + 2 * b + 1, x1);
             av = x0;
             ad = fr_sub(x1, x0);
-            const fr_t* so = a.src[2] + 4 * b;
-            y0 = fr_load_cg(so); y1 = fr_load_cg(so + 1); y2 = fr_load_cg(so + 2); y3 = fr_load_cg(so + 3);
-            x0 = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
-            x1 = fr_add(y2, fr_mul(r, fr_sub(y3, y2)));
-            if (side == 0) {
-                fr_store(a.dst[2] + 2 * b, x0);
-                fr_store(a.dst[2] + 2 * b + 1, x1);
-            }
-            om = x0;
-            omd = fr_sub(x1, x0);
+            // oms fold shared by the pair's two lanes: side s folds entry s and stores it
+            const fr_t* so = a.src[2] + 4 * b + 2 * side;
+            y0 = fr_load_cg(so);
+            y1 = fr_load_cg(so + 1);
+            const fr_t mine = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+            fr_store(a.dst[2] + 2 * b + side, mine);
+            const fr_t other = fr_shfl_xor(mine, 1, __activemask());
+            om = side ? other : mine;
+            omd = fr_sub(side ? mine : other, om);
         } else {
             av = fr_load_cg(srcA + 2 * b);
             ad = fr_sub(fr_load_cg(srcA + 2 * b + 1), av);
-            om = fr_load_cg(a.src[2] + 2 * b);
-            omd = fr_sub(fr_load_cg(a.src[2] + 2 * b + 1), om);
+            o0 = !fr_is_zero(fr_load_cg(a.src[2] + 2 * b));
+            od = (int)!fr_is_zero(fr_load_cg(a.src[2] + 2 * b + 1)) - o0;
         }
         if (b < next_count) {   // next LO level: side 0 handles Z, A, b; side 1 handles GA, GZ
             fr_store(&a.lo_next[side ? 2 : 0][b], fr_add(fr_load(&loA[2 * b]), fr_load(&loA[2 * b + 1])));
@@ -659,16 +659,18 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
         fr_t ecd = fr_sub(fr_mul(fr_load(&loC[l0 + 1]), hc), ec);
         fr_t eb = fr_mul(fr_load(&loB[l0]), hb);
         fr_t ebd = fr_sub(fr_mul(fr_load(&loB[l0 + 1]), hb), eb);
+        // P(X) = a (E_a + oms E_c + (a - 1) E_b): three products per evaluation point (two when oms is
+        // a small integer in the first round)
 #pragma unroll
         for (int X = 0; X < 4; X++) {
             if (X != 1) {
-                const fr_t q = fr_mul(av, fr_sub(av, fr_one()));
-                const fr_t p = fr_add(fr_mul(av, fr_add(ea, fr_mul(ec, om))), fr_mul(eb, q));
-                acc[X == 0 ? 0 : X - 1] = fr_add(acc[X == 0 ? 0 : X - 1], p);
+                const fr_t t_c = FOLD ? fr_mul(ec, om) : fr_mul_small(ec, o0 + X * od);
+                const fr_t q = fr_add(fr_add(ea, t_c), fr_mul(eb, fr_sub(av, fr_one())));
+                acc[X == 0 ? 0 : X - 1] = fr_add(acc[X == 0 ? 0 : X - 1], fr_mul(av, q));
             }
             if (X < 3) {
                 av = fr_add(av, ad);
-                om = fr_add(om, omd);
+                if (FOLD) om = fr_add(om, omd);
                 ea = fr_add(ea, ead);
                 ec = fr_add(ec, ecd);
                 eb = fr_add(eb, ebd);

@@ -33,14 +33,18 @@ class DeviceFamily:
 
 
 def upload_families(families, device="cuda", pin: bool = False) -> list:
-    """Copy synth.fcn families (numpy int32 stacks) to the device."""
+    """Copy synth.fcn families (numpy int32 stacks) to the device; a stack shared by several
+    families (same array) is copied once and shared."""
     out = []
+    seen = {}
 
     def dev(a):
-        t = torch.from_numpy(a)
-        if pin:
-            t = t.pin_memory()
-        return t.to(device, non_blocking=pin)
+        if id(a) not in seen:
+            t = torch.from_numpy(a)
+            if pin:
+                t = t.pin_memory()
+            seen[id(a)] = t.to(device, non_blocking=pin)
+        return seen[id(a)]
 
     for f in families:
         if hasattr(f, "A"):
@@ -58,9 +62,21 @@ def _layout(f: DeviceFamily):
     return logD, api.relu_prove_len(logD, f.Q, f.R)
 
 
-def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list):
+def _slot(n: int) -> int:
+    return (n + 32 + 255) & ~255   # family output + 32-byte state, every family 256-byte aligned
+
+
+def window_out_bytes(families: list) -> int:
+    """Size of a window's device output buffer (what collect_window copies back)."""
+    return sum(_slot(_layout(f)[1]) for f in families)
+
+
+def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list, ready: list | None = None):
     """Enqueue one window's proofs on the context stream without synchronising.
 
+    ready (optional): one torch.cuda.Event per family that the context stream waits on before that
+    family's proof -- e.g. the end of its host->device upload on a copy stream, so uploads of later
+    families overlap the proofs of earlier ones.
     Returns (out, flag, layout): `out` is one uint8 device buffer holding, per family, its proof
     output followed by the 32-byte transcript state after the family; `flag` the int32 range flag."""
     dev = (families[0].A if families[0].kind == "matmul" else families[0].Z).device
@@ -69,12 +85,14 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list)
     for f in families:
         info, n = _layout(f)
         lay.append((f, info, off, n))
-        off += (n + 32 + 255) & ~255   # every family starts 256-byte aligned
+        off += _slot(n)
     out = torch.empty(off, dtype=torch.uint8, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     tr = api.Transcript(ctx, seed)
     tr.absorb("fcn/hdr", header)
-    for f, info, o, n in lay:
+    for i, (f, info, o, n) in enumerate(lay):
+        if ready is not None:
+            ctx.stream.wait_event(ready[i])
         tr.absorb("fcn/fam", f.name.encode())
         if f.kind == "matmul":
             api.matmul_prove(ctx, tr, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
@@ -109,3 +127,35 @@ def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
 def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list) -> list:
     """Prove every family of one window under one transcript; returns per-family results."""
     return collect_window(*enqueue_window(ctx, seed, header, families))
+
+
+def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None) -> list:
+    """The user-facing end-to-end call: families given as host (ideally pinned) int32 tensors.
+
+    Each family's stacks are copied host->device on `copy_stream` (one is created if None) and its
+    proof waits only for its own upload, so the transfers of later families overlap the proofs of
+    earlier ones.  A host buffer shared by several families (the weight stack W[2..8] is the B operand
+    of F[2..8] and of GA[1..7]) is copied once.  The proof bytes come back to the host (one
+    synchronisation).  host_families: DeviceFamily records whose tensors live on the host."""
+    dev = torch.device("cuda", ctx.device)
+    cs = copy_stream if copy_stream is not None else torch.cuda.Stream(device=dev)
+    fams, ready = [], []
+    uploaded = {}   # host buffer -> device tensor: a stack shared by several families is copied once
+
+    def upload(t):
+        key = (t.data_ptr(), t.numel(), t.dtype)
+        if key not in uploaded:
+            uploaded[key] = t.to(dev, non_blocking=True)
+        return uploaded[key]
+
+    with torch.cuda.stream(cs):
+        for f in host_families:
+            up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
+            g = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
+            for t in up.values():
+                t.record_stream(ctx.stream)   # the proof reads it on the context stream
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            fams.append(g)
+            ready.append(ev)
+    return collect_window(*enqueue_window(ctx, seed, header, fams, ready))

@@ -16,8 +16,8 @@ in float64 BLAS, exact because every partial sum is an integer below 2^53
 Families: every forward / input-gradient /
 weight-gradient matmul and every ReLU is grouped by (equation type, shape);
 instances are ordered by (step, layer) and the stack axis is zero-padded to a
-power of two.  The family order is fixed: all F, then GA, then
-GW families (each in increasing first-layer order), then ReLU families.
+power of two.  The family order is fixed: ReLU families, then all
+F, then GA, then GW families (each in increasing first-layer order).
 """
 from __future__ import annotations
 
@@ -187,6 +187,15 @@ def assemble_families(shape: FcnShape, trace):
     """Group the trace's operations into FAC4DNN families (fixed order, see module doc)."""
     L = len(shape.dims) - 1
     fam = []
+    cache = {}
+
+    def stk(field, idx, N):
+        # one array per distinct stack: e.g. W[2..8] is the B operand of F[2..8] and of GA[1..7],
+        # A[1..7] of F[2..8] and GW[2..8], G_Z[2..8] of GA[1..7] and GW[2..8]
+        key = (field, tuple(idx), N)
+        if key not in cache:
+            cache[key] = _stack([getattr(trace[s], field)[l] for s, l in idx], N)
+        return cache[key]
 
     def group(kind, layers, key_fn):
         groups = {}
@@ -194,34 +203,8 @@ def assemble_families(shape: FcnShape, trace):
             groups.setdefault(key_fn(l), []).append(l)
         return sorted(groups.items(), key=lambda kv: kv[1][0])
 
-    # forward: Z^(l) = A^(l-1) W^(l)
-    for key, ls in group("F", range(1, L + 1), lambda l: (shape.dims[l - 1], shape.dims[l])):
-        insts = [(s, l) for s in range(shape.steps) for l in ls]
-        N = _next_pow2(len(insts))
-        fam.append(MatmulFamily(
-            f"F[{','.join(map(str, ls))}]",
-            _stack([trace[s].A[l - 1] for s, l in insts], N),
-            _stack([trace[s].W[l] for s, l in insts], N),
-            _stack([trace[s].Z[l] for s, l in insts], N), False, False, len(insts)))
-    # input gradients: G_A^(l) = G_Z^(l+1) W^(l+1)^T
-    for key, ls in group("GA", range(1, L), lambda l: (shape.dims[l + 1], shape.dims[l])):
-        insts = [(s, l) for s in range(shape.steps) for l in ls]
-        N = _next_pow2(len(insts))
-        fam.append(MatmulFamily(
-            f"GA[{','.join(map(str, ls))}]",
-            _stack([trace[s].GZ[l + 1] for s, l in insts], N),
-            _stack([trace[s].W[l + 1] for s, l in insts], N),
-            _stack([trace[s].GA[l] for s, l in insts], N), False, True, len(insts)))
-    # weight gradients: G_W^(l) = G_Z^(l)^T A^(l-1)
-    for key, ls in group("GW", range(1, L + 1), lambda l: (shape.dims[l], shape.dims[l - 1])):
-        insts = [(s, l) for s in range(shape.steps) for l in ls]
-        N = _next_pow2(len(insts))
-        fam.append(MatmulFamily(
-            f"GW[{','.join(map(str, ls))}]",
-            _stack([trace[s].GZ[l] for s, l in insts], N),
-            _stack([trace[s].A[l - 1] for s, l in insts], N),
-            _stack([trace[s].GW[l] for s, l in insts], N), True, False, len(insts)))
-    # zkReLU after every hidden layer
+    # zkReLU after every hidden layer (first: the most proving work on the least data, so an
+    # end-to-end prover's uploads of the large matmul stacks overlap it)
     for key, ls in group("ReLU", range(1, L), lambda l: shape.dims[l]):
         insts = [(s, l) for s in range(shape.steps) for l in ls]
         N = _next_pow2(len(insts))
@@ -232,6 +215,33 @@ def assemble_families(shape: FcnShape, trace):
             Z[i * per:(i + 1) * per] = trace[s].Z[l].reshape(-1)
             G[i * per:(i + 1) * per] = trace[s].GA[l].reshape(-1)
         fam.append(ReluFamily(f"ReLU[{','.join(map(str, ls))}]", Z, G, Q_BITS, R_BITS, len(insts)))
+    # forward: Z^(l) = A^(l-1) W^(l)
+    for key, ls in group("F", range(1, L + 1), lambda l: (shape.dims[l - 1], shape.dims[l])):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        fam.append(MatmulFamily(
+            f"F[{','.join(map(str, ls))}]",
+            stk("A", [(s, l - 1) for s, l in insts], N),
+            stk("W", [(s, l) for s, l in insts], N),
+            stk("Z", [(s, l) for s, l in insts], N), False, False, len(insts)))
+    # input gradients: G_A^(l) = G_Z^(l+1) W^(l+1)^T
+    for key, ls in group("GA", range(1, L), lambda l: (shape.dims[l + 1], shape.dims[l])):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        fam.append(MatmulFamily(
+            f"GA[{','.join(map(str, ls))}]",
+            stk("GZ", [(s, l + 1) for s, l in insts], N),
+            stk("W", [(s, l + 1) for s, l in insts], N),
+            stk("GA", [(s, l) for s, l in insts], N), False, True, len(insts)))
+    # weight gradients: G_W^(l) = G_Z^(l)^T A^(l-1)
+    for key, ls in group("GW", range(1, L + 1), lambda l: (shape.dims[l], shape.dims[l - 1])):
+        insts = [(s, l) for s in range(shape.steps) for l in ls]
+        N = _next_pow2(len(insts))
+        fam.append(MatmulFamily(
+            f"GW[{','.join(map(str, ls))}]",
+            stk("GZ", [(s, l) for s, l in insts], N),
+            stk("A", [(s, l - 1) for s, l in insts], N),
+            stk("GW", [(s, l) for s, l in insts], N), True, False, len(insts)))
     return fam
 
 

@@ -278,6 +278,11 @@ def test_fcn_tiny_vs_oracle(ctx, O):
         assert gr["msgs"] == orr["msgs"], gr["name"]
         assert gr["finals"] == orr["finals"], gr["name"]
         assert gr["state"] == orr["state"], gr["name"]
+    # end-to-end entry (host tensors, per-family uploads overlapped with proofs): same bytes
+    host = dfcn.upload_families(fams, device="cpu")
+    h = dfcn.prove_window_from_host(ctx, fs_seed("tiny"), fcn.fcn_header(shape), host)
+    assert [r["proof"] for r in h] == [r["proof"] for r in g]
+    assert [r["state"] for r in h] == [r["state"] for r in g]
 
 
 def test_async_provers_match_sync(ctx):

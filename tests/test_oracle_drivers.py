@@ -52,7 +52,7 @@ def test_fcn_family_driver_tiny(oracle_lib):
     trace = fcn.generate_trace(shape, x_bits=4, w_bits=4, y_bits=3)
     fams = fcn.assemble_families(shape, trace)
     names = [f.name for f in fams]
-    assert names[0].startswith("F[") and names[-1].startswith("ReLU[")
+    assert names[0].startswith("ReLU[") and names[1].startswith("F[") and names[-1].startswith("GW[")
     out = drivers.fcn_prove(shape, fams, "tiny")
     assert len(out) == len(fams)
     # the trace's product tensors satisfy the matmul identity at the drawn points
