@@ -1,0 +1,415 @@
+// gram.cu — zkReLU bit sums on the 5th-generation tensor cores (row a8, j-phase inputs).
+//
+// The j-rounds of the zkReLU sumcheck (relu.cu) need, for the bit words w_s(i) (s = 0: Z, s = 1: G_A,
+// masked to Q+R bits) and eq weights c_x(i) = eq(u_x, i):
+//     M_x[j]       = sum_i c_x(i) [1 - sig_i]^{x in {A, G_Z}} bit_j(w_{s(x)}(i))        (linear cells)
+//     C_s[j1][j2]  = sum_i e_b(i) bit_j1(w_s(i)) bit_j2(w_s(i)),   j1 <= j2              (Gram cells)
+// (P:L449-470 AIVP with the bits-first order of DESIGN.md D5/D12).  Both are dense contractions over i:
+// with the eq table split eq(u, i) = LO(i mod 2^16) HI(i >> 16) and the LO values (R^2-scaled residues)
+// written as 32 bytes L_k, a row segment of entries gives exact int32 sums
+//     G_k[j1][j2] = sum_i L_k(i) b_j1(i) b_j2(i)          (A = L_k & b_j1 : u8,  B = b_j2 : u8)
+// which tcgen05.mma.kind::i8 computes with A in TMEM (rows (j1, k): 4 j1 x 32 limbs per M = 128 tile),
+// B in shared memory (32 bit planes x 32 entries per K step) and the s32 accumulators in TMEM.  At the
+// end of a row segment the 32 limb sums of a cell are recombined, sum_k 2^{8k} G_k (< p 2^24),
+// Montgomery-reduced and multiplied by HI[row].
+//
+// CTA roles: blockIdx.x = 2 g + s: word s, K-step range g of G.  Warps 0-7 produce the operands
+// (warp w: bit planes 4w..4w+3; C tiles t = 4 (w / 4) .. +3 with j1 = 4t + (w % 4); warps 0, 1 also the
+// linear-cell tile), warp 8 issues the MMAs.  TMEM columns: [0, 256) Gram accumulators (tile t at 32t),
+// [256, 288) linear-cell accumulator, [288, 504) three A stages of 9 tiles x 8 columns.
+#include "relu.cuh"
+#include "tables.cuh"
+
+namespace zk {
+
+constexpr int GR_STAGES = 3;
+constexpr uint32_t GR_ACC_LIN = 256;
+constexpr uint32_t GR_ASTAGE = 288;
+constexpr uint32_t GR_STAGE_COLS = 72;
+// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A and B u8, both K-major, N = 32 (N >> 3 at
+// bit 17), M = 128 (M >> 4 at bit 24)
+constexpr uint32_t GR_IDESC = (2u << 4) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+
+// Operand chunks (256 entries = 8 K steps) are streamed into shared memory by a loader warp with bulk
+// async copies: the bit words and, per eq table used, 32 limb rows of 256 bytes padded to 272 (so the
+// 32 lanes' 32-byte reads of one K step fall in distinct bank groups).
+constexpr int GR_CH_KS = 8;
+constexpr int GR_CH = 32 * GR_CH_KS;
+constexpr int GR_LROW = GR_CH + 16;
+constexpr int GR_LBLK = 32 * GR_LROW;   // one chunk of one limb-transposed table
+constexpr int GR_CSTAGES = 3;
+
+struct GramArgs {
+    const int32_t* Z;
+    const int32_t* GA;
+    uint64_t nch;          // chunks (D / 256)
+    uint32_t ch_per_row;   // 2^lo_bits / 256
+    uint32_t qr_mask, sig_bit, B;
+    const uint8_t* LOT[5]; // limb-transposed LO tables, chunk c of a row at LOT[x] + c * GR_LBLK: [limb k][GR_LROW]
+    const fr_t* HI[5];
+    uint32_t G;            // CTAs per word
+    fr_t* partials;        // [2][G][ncs]: ncs = 2B linear cells of the word, then its B(B+1)/2 Gram cells
+};
+
+struct GramChunk {
+    uint32_t z[GR_CH];             // Z words (sign bits; the bit word when s = 0)
+    uint32_t w[GR_CH];             // G_A words (s = 1)
+    uint8_t lot[3][GR_LBLK];       // limb rows: e_b, then the word's two linear-cell tables
+};
+
+struct GramSmem {
+    GramChunk ch[GR_CSTAGES];
+    uint8_t sB[GR_STAGES][1024];   // B tiles: plane j, entry byte kb at (j/8)*256 + (kb/16)*128 + (j%8)*16 + kb%16
+    uint32_t mask[2][32][8];       // plane masks (0xFF bytes) for the K step of parity it & 1
+    uint32_t gate[2][8];           // (1 - sig) masks
+    uint32_t stage[8][32][33];     // epilogue: warp, column, limb
+    fr_t tot[64 + 528];            // running cell totals of this CTA
+    uint64_t full[GR_STAGES], empty[GR_STAGES], accfull, cfull[GR_CSTAGES], cempty[GR_CSTAGES];
+    uint32_t tmem;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(su32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&w)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(w[0]),
+                 "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a), "l"(bdesc), "r"(GR_IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b)) : "memory");
+}
+// shared-memory matrix descriptor: K-major, no swizzle, core matrices of 8 rows x 16 B;
+// LBO = 128 B (second 16-byte K chunk), SBO = 256 B (next 8 rows), descriptor version 1 (sm_100)
+__device__ __forceinline__ uint64_t bdesc(const void* p) {
+    return (uint64_t)((su32(p) >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+}
+// 4 bits -> 4 bytes of 0x00 / 0xFF
+__device__ __forceinline__ uint32_t expand4(uint32_t n) { return ((n * 0x00204081u) & 0x01010101u) * 0xFFu; }
+
+// sum_k 2^{8k} x_k (x_k < 2^25) as a 10-limb integer, Montgomery-reduced
+__device__ __forceinline__ fr_t compose_limbs(const uint32_t* x /* 32 limbs, stride 1 */) {
+    uint64_t a[9];
+#pragma unroll
+    for (int i = 0; i < 9; i++) a[i] = 0;
+#pragma unroll
+    for (int k = 0; k < 32; k++) a[k >> 2] += (uint64_t)x[k] << (8 * (k & 3));
+    uint32_t w[10];
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const uint64_t t = a[i] + c;
+        w[i] = (uint32_t)t;
+        c = t >> 32;
+    }
+    w[9] = (uint32_t)c;
+    return fr_redc_wide(w);
+}
+
+__device__ __forceinline__ int gr_tri(int j1, int j2, int B) { return j1 * B - j1 * (j1 - 1) / 2 + (j2 - j1); }
+
+__global__ void __launch_bounds__(320, 1) k_relu_gram(GramArgs a) {
+    extern __shared__ __align__(1024) uint8_t gsm_raw[];
+    GramSmem& S = *reinterpret_cast<GramSmem*>(gsm_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x & 1;
+    const uint32_t g = blockIdx.x >> 1;
+    const uint64_t c0 = g * a.nch / a.G, c1 = (g + 1) * a.nch / a.G;   // this CTA's chunks
+    const uint32_t B = a.B, T = B * (B + 1) / 2, ncs = 2 * B + T;
+    for (uint32_t i = threadIdx.x; i < ncs; i += blockDim.x) S.tot[i] = fr_zero();
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&S.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (lane == 0) {
+            for (int i = 0; i < GR_STAGES; i++) {
+                mbar_init(&S.full[i], 8);
+                mbar_init(&S.empty[i], 1);
+            }
+            for (int i = 0; i < GR_CSTAGES; i++) {
+                mbar_init(&S.cfull[i], 1);
+                mbar_init(&S.cempty[i], 8);
+            }
+            mbar_init(&S.accfull, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+
+    if (warp == 9) {
+        // ---------------- loader: bulk async copies of the operand chunks
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)(GR_CH * 4 * (1 + s) + 3 * GR_LBLK);
+            uint32_t i = 0;
+            for (uint64_t c = c0; c < c1; c++, i++) {
+                const uint32_t slot = i % GR_CSTAGES;
+                if (i >= GR_CSTAGES) mbar_wait(&S.cempty[slot], ((i / GR_CSTAGES) - 1) & 1);
+                GramChunk& C = S.ch[slot];
+                uint64_t* bar = &S.cfull[slot];
+                mbar_expect_tx(bar, bytes);
+                const uint64_t l0 = c * GR_CH;
+                const size_t lofs = (size_t)(c % a.ch_per_row) * GR_LBLK;
+                bulk_g2s(C.z, a.Z + l0, GR_CH * 4, bar);
+                if (s) bulk_g2s(C.w, a.GA + l0, GR_CH * 4, bar);
+                bulk_g2s(C.lot[0], a.LOT[4] + lofs, GR_LBLK, bar);
+                bulk_g2s(C.lot[1], a.LOT[2 * s] + lofs, GR_LBLK, bar);
+                bulk_g2s(C.lot[2], a.LOT[2 * s + 1] + lofs, GR_LBLK, bar);
+            }
+        }
+    } else if (warp == 8) {
+        // ---------------- MMA issuer
+        uint32_t it = 0;
+        for (uint64_t c = c0; c < c1; c++) {
+            const bool seg_first = c == c0 || c % a.ch_per_row == 0;
+            const bool seg_last = c + 1 == c1 || (c + 1) % a.ch_per_row == 0;
+            for (int kk = 0; kk < GR_CH_KS; kk++, it++) {
+                const uint32_t st = it % GR_STAGES;
+                mbar_wait(&S.full[st], (it / GR_STAGES) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint64_t bd = bdesc(S.sB[st]);
+                    const uint32_t abase = tmem + GR_ASTAGE + st * GR_STAGE_COLS;
+                    const uint32_t acc = !(seg_first && kk == 0);
+#pragma unroll
+                    for (int t = 0; t < 8; t++) mma_i8(tmem + 32 * t, abase + 8 * t, bd, acc);
+                    mma_i8(tmem + GR_ACC_LIN, abase + 64, bd, acc);
+                    mma_commit(&S.empty[st]);
+                    if (seg_last && kk == GR_CH_KS - 1) mma_commit(&S.accfull);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- operand producers + epilogue
+        const int q = warp & 3, grp = warp >> 2;
+        const bool lin = grp == 0 && q < 2;   // this warp also builds the linear-cell tile rows (x_local = q)
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        uint32_t it = 0, seg = 0, ci = 0;
+        for (uint64_t c = c0; c < c1; c++, ci++) {
+            const uint32_t slot = ci % GR_CSTAGES;
+            const uint64_t row = c / a.ch_per_row;
+            const bool seg_last = c + 1 == c1 || (c + 1) % a.ch_per_row == 0;
+            mbar_wait(&S.cfull[slot], (ci / GR_CSTAGES) & 1);
+            const GramChunk& C = S.ch[slot];
+            const uint32_t* Wsm = s ? C.w : C.z;
+            for (int kk = 0; kk < GR_CH_KS; kk++, it++) {
+                const uint32_t st = it % GR_STAGES, par = it & 1;
+                const uint32_t wv = Wsm[32 * kk + lane] & a.qr_mask;
+                const uint32_t zv = C.z[32 * kk + lane];
+                const uint4* lb = reinterpret_cast<const uint4*>(&C.lot[0][lane * GR_LROW + 32 * kk]);
+                const uint4 b0 = lb[0], b1 = lb[1];
+                uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
+                if (lin) {
+                    const uint4* lx = reinterpret_cast<const uint4*>(&C.lot[1 + q][lane * GR_LROW + 32 * kk]);
+                    x0 = lx[0];
+                    x1 = lx[1];
+                }
+                if (kk == GR_CH_KS - 1) {   // last reads of this chunk are in registers: release the slot
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&S.cempty[slot]);
+                }
+                // phase 1: bit planes 4w..4w+3 -> masks and the B tile
+                uint32_t pl[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++) pl[jj] = __ballot_sync(0xffffffffu, (wv >> (4 * warp + jj)) & 1u);
+                const uint32_t sigp = __ballot_sync(0xffffffffu, (zv >> a.sig_bit) & 1u);
+                if (it >= GR_STAGES) mbar_wait(&S.empty[st], ((it / GR_STAGES) - 1) & 1);
+                {
+                    const int jj = lane >> 3, c = lane & 7, j = 4 * warp + jj;
+                    const uint32_t P = jj == 0 ? pl[0] : jj == 1 ? pl[1] : jj == 2 ? pl[2] : pl[3];
+                    const uint32_t m = expand4((P >> (4 * c)) & 15u);
+                    S.mask[par][j][c] = m;
+                    *reinterpret_cast<uint32_t*>(&S.sB[st][(j >> 3) * 256 + ((4 * c) >> 4) * 128 + (j & 7) * 16 + ((4 * c) & 15)]) =
+                        m & 0x01010101u;
+                    if (warp == 0 && lane < 8) S.gate[par][lane] = expand4(((~sigp) >> (4 * lane)) & 15u);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                // phase 2: A tiles into TMEM
+                const uint32_t lo[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const uint32_t abase = tmem + lane_base + GR_ASTAGE + st * GR_STAGE_COLS;
+#pragma unroll
+                for (int tt = 0; tt < 4; tt++) {
+                    const int t = 4 * grp + tt, j1 = 4 * t + q;
+                    const uint4 m0 = *reinterpret_cast<const uint4*>(&S.mask[par][j1][0]);
+                    const uint4 m1 = *reinterpret_cast<const uint4*>(&S.mask[par][j1][4]);
+                    const uint32_t w8[8] = {lo[0] & m0.x, lo[1] & m0.y, lo[2] & m0.z, lo[3] & m0.w,
+                                            lo[4] & m1.x, lo[5] & m1.y, lo[6] & m1.z, lo[7] & m1.w};
+                    tmem_st8(abase + 8 * t, w8);
+                }
+                if (grp == 0) {   // linear-cell tile: rows (x_local = q, limb k); q >= 2 rows are zero
+                    uint32_t w8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    if (q == 1) {
+                        const uint4 g0 = *reinterpret_cast<const uint4*>(&S.gate[par][0]);
+                        const uint4 g1 = *reinterpret_cast<const uint4*>(&S.gate[par][4]);
+                        w8[0] &= g0.x; w8[1] &= g0.y; w8[2] &= g0.z; w8[3] &= g0.w;
+                        w8[4] &= g1.x; w8[5] &= g1.y; w8[6] &= g1.z; w8[7] &= g1.w;
+                    }
+                    tmem_st8(abase + 64, w8);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.full[st]);
+            }
+            if (!seg_last) continue;
+            // ---- segment epilogue: 32 limb sums per cell -> Fr, times HI[row]
+            mbar_wait(&S.accfull, seg & 1);
+            seg++;
+            tc_fence_after();
+            uint32_t (*stg)[33] = S.stage[warp];
+            for (int tt = 0; tt < 4; tt++) {
+                const int t = 4 * grp + tt, j1 = 4 * t + q;
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + 32 * t, v);
+#pragma unroll
+                for (int c = 0; c < 32; c++) stg[c][lane] = v[c];
+                __syncwarp();
+                const int j2 = lane;
+                if (j1 < (int)B && j2 >= j1 && j2 < (int)B) {
+                    fr_t val = fr_mul(compose_limbs(stg[j2]), fr_load(&a.HI[4][row]));
+                    fr_t& dst = S.tot[2 * B + gr_tri(j1, j2, B)];
+                    dst = fr_add(dst, val);
+                }
+                __syncwarp();
+            }
+            if (grp == 0 && q < 2) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + GR_ACC_LIN, v);
+#pragma unroll
+                for (int c = 0; c < 32; c++) stg[c][lane] = v[c];
+                __syncwarp();
+                const int j = lane;
+                if (j < (int)B) {
+                    fr_t val = fr_mul(compose_limbs(stg[j]), fr_load(&a.HI[2 * s + q][row]));
+                    fr_t& dst = S.tot[q * B + j];
+                    dst = fr_add(dst, val);
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    fr_t* out = a.partials + ((size_t)s * a.G + g) * ncs;
+    for (uint32_t i = threadIdx.x; i < ncs; i += blockDim.x) fr_store(&out[i], S.tot[i]);
+    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// global cell c (relu.cu cell_decode order) <- sum over the G CTAs of its word
+__global__ void k_relu_gram_reduce(const fr_t* partials, uint32_t G, uint32_t B, fr_t* out) {
+    const uint32_t T = B * (B + 1) / 2, ncs = 2 * B + T, ncell = 4 * B + 2 * T;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+        uint32_t s, local;
+        if (c < 4 * B) {
+            const uint32_t x = c / B, j = c % B;
+            s = x >> 1;
+            local = (x & 1) * B + j;
+        } else {
+            s = (c - 4 * B) / T;
+            local = 2 * B + (c - 4 * B) % T;
+        }
+        fr_t acc = fr_zero();
+        for (uint32_t gg = 0; gg < G; gg++) acc = fr_add(acc, fr_load(&partials[((size_t)s * G + gg) * ncs + local]));
+        fr_store(&out[c], acc);
+    }
+}
+
+// LOT[(l / 256) * GR_LBLK + k * GR_LROW + l % 256] = byte k of LO[l]
+__global__ void k_lo_limbs(const fr_t* LO, uint32_t n, uint8_t* LOT) {
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l < n; l += gridDim.x * blockDim.x) {
+        const fr_t v = fr_load(&LO[l]);
+        uint8_t* dst = LOT + (size_t)(l / GR_CH) * GR_LBLK + (l % GR_CH);
+#pragma unroll
+        for (int k = 0; k < 32; k++) dst[k * GR_LROW] = (uint8_t)(v.v[k >> 2] >> (8 * (k & 3)));
+    }
+}
+
+bool relu_gram_supported(uint32_t logD, uint32_t B) { return logD >= 12 && B >= 8 && B <= 32; }
+
+void relu_bitsums_gram(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t qr_mask,
+                       uint32_t sig_bit, uint32_t B, const fr_t* const u_i[5], fr_t* cell_tot, Scratch& s) {
+    const uint32_t lo_bits = logD < 16 ? logD : 16, hi_bits = logD - lo_bits;
+    const uint32_t lo_n = 1u << lo_bits;
+    GramArgs ga;
+    memset(&ga, 0, sizeof ga);
+    for (int x = 0; x < 5; x++) {
+        fr_t* lo = s.alloc<fr_t>(lo_n);
+        fr_t* hi = s.alloc<fr_t>(1ull << hi_bits);
+        eq_table_r2_dev(ctx, u_i[x], lo_bits, lo, s);
+        eq_table_dev(ctx, u_i[x] + lo_bits, hi_bits, nullptr, hi, s);
+        uint8_t* lot = s.alloc<uint8_t>((size_t)(lo_n / GR_CH) * GR_LBLK);
+        ZK_LAUNCH(ctx, k_lo_limbs, grid_for(ctx, lo_n, 256, 4), 256, 0, (const fr_t*)lo, lo_n, lot);
+        ga.LOT[x] = lot;
+        ga.HI[x] = hi;
+    }
+    ga.Z = Z;
+    ga.GA = GA;
+    ga.nch = (1ull << logD) / GR_CH;
+    ga.ch_per_row = lo_n / GR_CH;
+    ga.qr_mask = qr_mask;
+    ga.sig_bit = sig_bit;
+    ga.B = B;
+    uint32_t G = (uint32_t)ctx->num_sms / 2;
+    if ((uint64_t)G > ga.nch) G = (uint32_t)ga.nch;
+    ga.G = G;
+    const uint32_t T = B * (B + 1) / 2, ncs = 2 * B + T;
+    ga.partials = s.alloc<fr_t>(2ull * G * ncs);
+    // > half the SM's shared memory: one CTA per SM, so the 512-column TMEM allocation never waits
+    const size_t smem = sizeof(GramSmem) + 1024 > 120 * 1024 ? sizeof(GramSmem) + 1024 : 120 * 1024;
+    ZK_CUDA(cudaFuncSetAttribute(k_relu_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ZK_LAUNCH(ctx, k_relu_gram, 2 * G, 320, smem, ga);
+    ZK_LAUNCH(ctx, k_relu_gram_reduce, (4 * B + 2 * T + 127) / 128, 128, 0, (const fr_t*)ga.partials, G, B, cell_tot);
+}
+
+}  // namespace zk

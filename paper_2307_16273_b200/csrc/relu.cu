@@ -849,6 +849,11 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     // ---- bit sums
     // cells (cell_decode): 4B linear cells, then two upper triangles of co-occurrence cells
     const uint32_t ncell = 4 * B + B * (B + 1);
+    fr_t* cell_tot = s.alloc<fr_t>(ncell);
+    static const bool no_gram = getenv("ZKDL_NO_GRAM") != nullptr;   // A/B switch for the CUDA-core path
+    if (relu_gram_supported(logD, B) && !no_gram) {
+        relu_bitsums_gram(ctx, Z, GA, logD, qr_mask, QR - 1, B, u_i, cell_tot, s);
+    } else {
     const uint32_t lo_bits = logD < 12 ? logD : 12, hi_bits = logD - lo_bits;
     BitsumArgs ba;
     memset(&ba, 0, sizeof ba);
@@ -868,7 +873,6 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     }
     ba.B = B;
     ba.ncell = ncell;
-    fr_t* cell_tot = s.alloc<fr_t>(ncell);
     if (logD >= 6) {   // subset-sum tables over chunks of 64 entries
         ZK_REQUIRE(ncell <= BS2_MAXC * BS2_T, ZK_ERR_INTERNAL, "bitsum cells");
         Bitsum2Args b2;
@@ -905,6 +909,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         ZK_LAUNCH(ctx, k_relu_bitsums, bs_grid, bs_threads, bs_smem, ba);
         ZK_LAUNCH(ctx, k_relu_bitsums_reduce, (ncell + 127) / 128, 128, 0, (const fr_t*)ba.partials, bs_grid, ncell,
                   cell_tot);
+    }
     }
 
     // ---- j-rounds

@@ -19,6 +19,11 @@ inline uint64_t relu_proof_len(uint32_t logD, uint32_t logB) { return 12 + 128 +
 bool relu_tables_dev(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint64_t D, uint32_t Q, uint32_t R, uint8_t* sign,
                      int32_t* A, int32_t* GZ, int32_t* Zp, int32_t* GAp, int32_t* RZ, int32_t* RGA, Scratch& s);
 
+// Bit-sum cells on the tensor cores (gram.cu): writes the 4B + B(B+1) cell totals in cell_decode order.
+bool relu_gram_supported(uint32_t logD, uint32_t B);
+void relu_bitsums_gram(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t qr_mask,
+                       uint32_t sig_bit, uint32_t B, const fr_t* const u_i[5], fr_t* cell_tot, Scratch& s);
+
 // Enqueues the whole proof; bit 0 of *range_flag (device word, not cleared here) is set if an input
 // lies outside the (Q+R)-bit range (never for Q+R = 32: every int32 is in range).
 void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,

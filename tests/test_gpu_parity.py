@@ -205,8 +205,10 @@ def test_relu_tables_vs_oracle(ctx, O):
         api.relu_tables(ctx, dev(np.array([32, 0], np.int32)), dev(np.array([0, 0], np.int32)), 4, 2)
 
 
+# logD >= 12 with B >= 8 runs the tensor-core bit sums (gram.cu): (16,16,12) gives most CTAs one or two
+# K steps, (16,16,17) crosses a 2^16-entry row inside CTAs, (4,4,12) and (8,8,14) have B = 8 and 16.
 RELU_CASES = [(4, 2, 1), (4, 2, 3), (4, 2, 6), (4, 4, 5), (16, 16, 2), (16, 16, 6), (8, 8, 9), (16, 16, 11),
-              (12, 4, 8), (16, 16, 13)]
+              (12, 4, 8), (16, 16, 13), (16, 16, 12), (4, 4, 12), (8, 8, 14), (12, 4, 15), (16, 16, 17)]
 
 
 @pytest.mark.parametrize("Q,R,logD", RELU_CASES)
