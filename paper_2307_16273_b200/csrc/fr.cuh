@@ -216,6 +216,11 @@ __device__ __forceinline__ fr_t fr_mul(const fr_t& a, const fr_t& b) {
 }
 __device__ __forceinline__ fr_t fr_sqr(const fr_t& a) { return fr_mul(a, a); }
 
+// Out-of-line but fully unrolled product for hot loops with many multiplications: one ~560-instruction
+// body shared by every call site keeps the loop inside the instruction cache (the inlined k_relu_iround
+// body was > 100 KB of SASS; ncu stall_no_inst 36%).
+static __device__ __noinline__ fr_t fr_mul_ni(fr_t a, fr_t b) { return fr_mul(a, b); }
+
 // One out-of-line copy for cold code (finalizers, single-CTA round kernels): the inlined product is
 // ~560 SASS instructions, and cold code that inlines dozens of them runs out of the instruction
 // cache (ncu: stall_no_inst dominated the round kernels' finalize).

@@ -600,6 +600,7 @@ struct IRoundArgs {
 // Two threads per pair b: side s = 0 carries a0 with E_Z, E_A and the AIVP weight E_b; side s = 1
 // carries a1 with E_GA, E_GZ and E_b' = r' E_b (its own HI table, so no per-pair r' product).  Per side
 // and X in {0, 2, 3}: P_s(X) = a (E_a + E_c oms) + E_b a (a - 1); X = 1 follows from g(0) + g(1) = c_t.
+#define IR_MUL fr_mul_ni   // one out-of-line product body: the loop fits the instruction cache
 template <bool FOLD>
 __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
     fr_t acc[3] = {fr_zero(), fr_zero(), fr_zero()};   // X = 0, 2, 3
@@ -624,8 +625,8 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
         if (FOLD) {
             const fr_t* s = srcA + 4 * b;
             fr_t y0 = fr_load_cg(s), y1 = fr_load_cg(s + 1), y2 = fr_load_cg(s + 2), y3 = fr_load_cg(s + 3);
-            fr_t x0 = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
-            fr_t x1 = fr_add(y2, fr_mul(r, fr_sub(y3, y2)));
+            fr_t x0 = fr_add(y0, IR_MUL(r, fr_sub(y1, y0)));
+            fr_t x1 = fr_add(y2, IR_MUL(r, fr_sub(y3, y2)));
             fr_store(dstA + 2 * b, x0);
             fr_store(dstA + 2 * b + 1, x1);
             av = x0;
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
             const fr_t* so = a.src[2] + 4 * b + 2 * side;
             y0 = fr_load_cg(so);
             y1 = fr_load_cg(so + 1);
-            const fr_t mine = fr_add(y0, fr_mul(r, fr_sub(y1, y0)));
+            const fr_t mine = fr_add(y0, IR_MUL(r, fr_sub(y1, y0)));
             fr_store(a.dst[2] + 2 * b + side, mine);
             const fr_t other = fr_shfl_xor(mine, 1, __activemask());
             om = side ? other : mine;
@@ -653,20 +654,20 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
         const uint64_t l0 = (2 * b) & lo_mask;
         const uint64_t h = b >> (a.lo_cnt - 1);
         const fr_t ha = fr_load(&hiA[h]), hc = fr_load(&hiC[h]), hb = fr_load(&hiB[h]);
-        fr_t ea = fr_mul(fr_load(&loA[l0]), ha);
-        fr_t ead = fr_sub(fr_mul(fr_load(&loA[l0 + 1]), ha), ea);
-        fr_t ec = fr_mul(fr_load(&loC[l0]), hc);
-        fr_t ecd = fr_sub(fr_mul(fr_load(&loC[l0 + 1]), hc), ec);
-        fr_t eb = fr_mul(fr_load(&loB[l0]), hb);
-        fr_t ebd = fr_sub(fr_mul(fr_load(&loB[l0 + 1]), hb), eb);
+        fr_t ea = IR_MUL(fr_load(&loA[l0]), ha);
+        fr_t ead = fr_sub(IR_MUL(fr_load(&loA[l0 + 1]), ha), ea);
+        fr_t ec = IR_MUL(fr_load(&loC[l0]), hc);
+        fr_t ecd = fr_sub(IR_MUL(fr_load(&loC[l0 + 1]), hc), ec);
+        fr_t eb = IR_MUL(fr_load(&loB[l0]), hb);
+        fr_t ebd = fr_sub(IR_MUL(fr_load(&loB[l0 + 1]), hb), eb);
         // P(X) = a (E_a + oms E_c + (a - 1) E_b): three products per evaluation point (two when oms is
         // a small integer in the first round)
 #pragma unroll
         for (int X = 0; X < 4; X++) {
             if (X != 1) {
-                const fr_t t_c = FOLD ? fr_mul(ec, om) : fr_mul_small(ec, o0 + X * od);
-                const fr_t q = fr_add(fr_add(ea, t_c), fr_mul(eb, fr_sub(av, fr_one())));
-                acc[X == 0 ? 0 : X - 1] = fr_add(acc[X == 0 ? 0 : X - 1], fr_mul(av, q));
+                const fr_t t_c = FOLD ? IR_MUL(ec, om) : fr_mul_small(ec, o0 + X * od);
+                const fr_t q = fr_add(fr_add(ea, t_c), IR_MUL(eb, fr_sub(av, fr_one())));
+                acc[X == 0 ? 0 : X - 1] = fr_add(acc[X == 0 ? 0 : X - 1], IR_MUL(av, q));
             }
             if (X < 3) {
                 av = fr_add(av, ad);
