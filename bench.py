@@ -355,7 +355,8 @@ def run_ours(args, rank, world, local):
                 "path": "fcn.prove_window_from_host: pinned host stacks -> HBM per family on a copy stream "
                         "(shared stacks once), overlapped with the proofs; proofs back to the host"},
         "roofline": rf,
-        "kernels_ms_per_step": {k: round(t, 4) for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:12]},
+        "kernels_ms_per_step": {k: round(t, 4) for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:16]},
+        "kernel_launches_per_step": {k: n for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:16]},
         "kernel_ms_total_per_step": round(total_kernel_ms, 4),
         "clocks": clk,
         "paper_context": {"value": 0.84, "unit": "s/update", "hardware": "A100", "note": "PT/step at T'=16, BS 64 (PAPER.md L405); includes commitments, not this metric"},

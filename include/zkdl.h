@@ -204,7 +204,7 @@ zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
 zk_status zk_diag_fr_op(zk_ctx* ctx, int op, const void* d_a, const void* d_b, uint64_t n, void* d_out);
 zk_status zk_diag_mul_bench(zk_ctx* ctx, const void* d_seed, uint32_t iters, uint32_t blocks, void* d_out);
 /* zk_diag_fs_bench: n sequential transcript steps on one warp (mode 0: absorb 3 elements + squeeze,
- * 1: SHA-256 compressions only, 2: out-of-line Montgomery products); d_out receives one element. */
+ * 1: transcript-hash (BLAKE2s) compressions only, 2: out-of-line Montgomery products); d_out receives one element. */
 zk_status zk_diag_fs_bench(zk_transcript* tr, uint32_t n, int mode, void* d_out);
 
 #ifdef __cplusplus

@@ -42,7 +42,7 @@ def lib():
         L.or_fr_op.argtypes = [c.c_int, vp, vp, vp]
         L.or_embed_i64.argtypes = [vp, c.c_uint64, vp]
         L.or_pinv.restype = c.c_uint64
-        L.or_sha256.argtypes = [vp, c.c_uint64, vp]
+        L.or_blake2s.argtypes = [vp, c.c_uint64, vp]
         L.or_transcript_init.argtypes = [vp, vp]
         L.or_transcript_absorb.argtypes = [vp, u8p, vp, c.c_uint64]
         L.or_transcript_challenges.argtypes = [vp, u8p, c.c_uint32, vp]
@@ -110,9 +110,10 @@ def embed(v) -> list:
     return from_bytes(out.raw[:32 * v.size])
 
 
-def sha256(msg: bytes) -> bytes:
+def blake2s(msg: bytes) -> bytes:
+    """BLAKE2s-256 (RFC 7693), the transcript hash H of DESIGN.md D3."""
     out = _buf(32)
-    lib().or_sha256(msg, len(msg), out)
+    lib().or_blake2s(msg, len(msg), out)
     return out.raw[:32]
 
 

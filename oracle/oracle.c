@@ -14,7 +14,7 @@
  *   R mod p and R^2 mod p are computed at start-up by repeated doubling.
  *
  * Pins (tests/test_oracle_*.py, -m "not gpu"): Python-int field arithmetic,
- * p = x^4 - x^2 + 1 for the BLS parameter x, NIST SHA-256 vectors, SPEC
+ * p = x^4 - x^2 + 1 for the BLS parameter x, RFC 7693 BLAKE2s vectors, SPEC
  * worked examples, round identities + final checks against brute-force MLE,
  * exhaustive m = 2 sumchecks, Lemma 1 exhaustive at Q=4 R=2, the matmul
  * identity against integer products, tamper rejection.
@@ -179,93 +179,96 @@ static void store_canon(fr a, uint8_t *b) {
         for (int k = 0; k < 8; k++) b[8 * i + k] = (uint8_t)(v[i] >> (8 * k));
 }
 
-/* ------------------------------------------------------------ SHA-256 (FIPS 180-4) */
-typedef struct { uint32_t h[8]; uint8_t buf[64]; uint64_t len; uint32_t nbuf; } sha_ctx;
-static const uint32_t SHA_K[64] = {
-    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
-    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
-    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
-    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
-    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
-    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
-    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
-    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
-#define ROR(x, n) (((x) >> (n)) | ((x) << (32 - (n))))
-static void sha_block(sha_ctx *c, const uint8_t *p) {
-    uint32_t w[64];
+/* ------------------------------------------------------------ BLAKE2s-256 (RFC 7693) */
+/* Written from RFC 7693 sections 2-3: 10 rounds of G over a 16-word state, 64-byte blocks,
+ * byte counter t and final-block flag; unkeyed, 32-byte digest (parameter word 0x01010020). */
+typedef struct { uint32_t h[8]; uint8_t buf[64]; uint64_t t; uint32_t nbuf; } hash_ctx;
+static const uint32_t B2S_IV[8] = {0x6A09E667, 0xBB67AE85, 0x3C6EF372, 0xA54FF53A,
+                                   0x510E527F, 0x9B05688C, 0x1F83D9AB, 0x5BE0CD19};
+static const uint8_t B2S_SIGMA[10][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0}};
+#define ROTR32(x, n) (((x) >> (n)) | ((x) << (32 - (n))))
+static void b2s_g(uint32_t v[16], int a, int b, int c, int d, uint32_t x, uint32_t y) {
+    v[a] = v[a] + v[b] + x; v[d] = ROTR32(v[d] ^ v[a], 16);
+    v[c] = v[c] + v[d];     v[b] = ROTR32(v[b] ^ v[c], 12);
+    v[a] = v[a] + v[b] + y; v[d] = ROTR32(v[d] ^ v[a], 8);
+    v[c] = v[c] + v[d];     v[b] = ROTR32(v[b] ^ v[c], 7);
+}
+static void b2s_compress(hash_ctx *c, int last) {
+    uint32_t m[16], v[16];
     for (int i = 0; i < 16; i++)
-        w[i] = ((uint32_t)p[4 * i] << 24) | ((uint32_t)p[4 * i + 1] << 16) | ((uint32_t)p[4 * i + 2] << 8) | p[4 * i + 3];
-    for (int i = 16; i < 64; i++) {
-        uint32_t s0 = ROR(w[i - 15], 7) ^ ROR(w[i - 15], 18) ^ (w[i - 15] >> 3);
-        uint32_t s1 = ROR(w[i - 2], 17) ^ ROR(w[i - 2], 19) ^ (w[i - 2] >> 10);
-        w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+        m[i] = (uint32_t)c->buf[4 * i] | ((uint32_t)c->buf[4 * i + 1] << 8) | ((uint32_t)c->buf[4 * i + 2] << 16) |
+               ((uint32_t)c->buf[4 * i + 3] << 24);
+    for (int i = 0; i < 8; i++) { v[i] = c->h[i]; v[i + 8] = B2S_IV[i]; }
+    v[12] ^= (uint32_t)c->t;
+    v[13] ^= (uint32_t)(c->t >> 32);
+    if (last) v[14] = ~v[14];
+    for (int r = 0; r < 10; r++) {
+        const uint8_t *s = B2S_SIGMA[r];
+        b2s_g(v, 0, 4, 8, 12, m[s[0]], m[s[1]]);
+        b2s_g(v, 1, 5, 9, 13, m[s[2]], m[s[3]]);
+        b2s_g(v, 2, 6, 10, 14, m[s[4]], m[s[5]]);
+        b2s_g(v, 3, 7, 11, 15, m[s[6]], m[s[7]]);
+        b2s_g(v, 0, 5, 10, 15, m[s[8]], m[s[9]]);
+        b2s_g(v, 1, 6, 11, 12, m[s[10]], m[s[11]]);
+        b2s_g(v, 2, 7, 8, 13, m[s[12]], m[s[13]]);
+        b2s_g(v, 3, 4, 9, 14, m[s[14]], m[s[15]]);
     }
-    uint32_t a = c->h[0], b = c->h[1], cc = c->h[2], d = c->h[3], e = c->h[4], f = c->h[5], g = c->h[6], h = c->h[7];
-    for (int i = 0; i < 64; i++) {
-        uint32_t S1 = ROR(e, 6) ^ ROR(e, 11) ^ ROR(e, 25);
-        uint32_t ch = (e & f) ^ (~e & g);
-        uint32_t t1 = h + S1 + ch + SHA_K[i] + w[i];
-        uint32_t S0 = ROR(a, 2) ^ ROR(a, 13) ^ ROR(a, 22);
-        uint32_t mj = (a & b) ^ (a & cc) ^ (b & cc);
-        uint32_t t2 = S0 + mj;
-        h = g; g = f; f = e; e = d + t1; d = cc; cc = b; b = a; a = t1 + t2;
-    }
-    c->h[0] += a; c->h[1] += b; c->h[2] += cc; c->h[3] += d;
-    c->h[4] += e; c->h[5] += f; c->h[6] += g; c->h[7] += h;
+    for (int i = 0; i < 8; i++) c->h[i] ^= v[i] ^ v[i + 8];
 }
-static void sha_init(sha_ctx *c) {
-    static const uint32_t H0[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
-                                   0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
-    memcpy(c->h, H0, 32); c->len = 0; c->nbuf = 0;
+static void h_init(hash_ctx *c) {
+    memcpy(c->h, B2S_IV, 32);
+    c->h[0] ^= 0x01010020u;   /* digest length 32, no key, fanout 1, depth 1 */
+    c->t = 0; c->nbuf = 0;
 }
-static void sha_update(sha_ctx *c, const void *data, uint64_t n) {
+static void h_update(hash_ctx *c, const void *data, uint64_t n) {
     const uint8_t *p = (const uint8_t *)data;
-    c->len += n;
     while (n) {
+        if (c->nbuf == 64) {   /* a full block is compressed only once more input follows */
+            c->t += 64;
+            b2s_compress(c, 0);
+            c->nbuf = 0;
+        }
         uint32_t take = 64 - c->nbuf;
         if (take > n) take = (uint32_t)n;
         memcpy(c->buf + c->nbuf, p, take);
         c->nbuf += take; p += take; n -= take;
-        if (c->nbuf == 64) { sha_block(c, c->buf); c->nbuf = 0; }
     }
 }
-static void sha_final(sha_ctx *c, uint8_t out[32]) {
-    uint64_t bits = c->len * 8;
-    uint8_t pad = 0x80;
-    sha_update(c, &pad, 1);
-    uint8_t z = 0;
-    while (c->nbuf != 56) sha_update(c, &z, 1);
-    uint8_t lb[8];
-    for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(bits >> (56 - 8 * i));
-    sha_update(c, lb, 8);
-    for (int i = 0; i < 8; i++) {
-        out[4 * i] = (uint8_t)(c->h[i] >> 24); out[4 * i + 1] = (uint8_t)(c->h[i] >> 16);
-        out[4 * i + 2] = (uint8_t)(c->h[i] >> 8); out[4 * i + 3] = (uint8_t)c->h[i];
-    }
+static void h_final(hash_ctx *c, uint8_t out[32]) {
+    c->t += c->nbuf;
+    memset(c->buf + c->nbuf, 0, 64 - c->nbuf);
+    b2s_compress(c, 1);
+    for (int i = 0; i < 8; i++)
+        for (int k = 0; k < 4; k++) out[4 * i + k] = (uint8_t)(c->h[i] >> (8 * k));
 }
-void or_sha256(const uint8_t *msg, uint64_t n, uint8_t out[32]) {
-    sha_ctx c; sha_init(&c); sha_update(&c, msg, n); sha_final(&c, out);
+void or_blake2s(const uint8_t *msg, uint64_t n, uint8_t out[32]) {
+    hash_ctx c; h_init(&c); h_update(&c, msg, n); h_final(&c, out);
 }
 
 /* ------------------------------------------------------------ transcript (D3) */
 typedef struct { uint8_t st[32]; } transcript;
 
 void or_transcript_init(transcript *t, const uint8_t seed[32]) {
-    sha_ctx c; sha_init(&c);
+    hash_ctx c; h_init(&c);
     const char *lbl = "zkdl-b200/v1/init";
-    sha_update(&c, lbl, strlen(lbl));
-    sha_update(&c, seed, 32);
-    sha_final(&c, t->st);
+    h_update(&c, lbl, strlen(lbl));
+    h_update(&c, seed, 32);
+    h_final(&c, t->st);
 }
 void or_transcript_absorb(transcript *t, const char *tag, const uint8_t *msg, uint64_t len) {
-    sha_ctx c; sha_init(&c);
+    hash_ctx c; h_init(&c);
     uint8_t dom = 0x01, tl = (uint8_t)strlen(tag), lb[8];
     for (int i = 0; i < 8; i++) lb[i] = (uint8_t)(len >> (56 - 8 * i));
-    sha_update(&c, t->st, 32); sha_update(&c, &dom, 1); sha_update(&c, &tl, 1);
-    sha_update(&c, tag, tl); sha_update(&c, lb, 8); sha_update(&c, msg, len);
-    sha_final(&c, t->st);
+    h_update(&c, t->st, 32); h_update(&c, &dom, 1); h_update(&c, &tl, 1);
+    h_update(&c, tag, tl); h_update(&c, lb, 8); h_update(&c, msg, len);
+    h_final(&c, t->st);
 }
-/* x = LE512(SHA256(st||0x00) || SHA256(st||0x01)) mod p, computed by plain
+/* x = LE512(H(st||0x00) || H(st||0x01)) mod p, computed by plain
  * shift-and-subtract long division (no Montgomery, no precomputed constants). */
 static fr reduce512(const uint8_t h[64]) {
     uint64_t rem[4] = {0, 0, 0, 0};
@@ -278,13 +281,13 @@ static fr reduce512(const uint8_t h[64]) {
     return fr_from_canon(rem);
 }
 static fr transcript_challenge(transcript *t, const char *tag) {
-    sha_ctx c; sha_init(&c);
+    hash_ctx c; h_init(&c);
     uint8_t dom = 0x02, tl = (uint8_t)strlen(tag);
-    sha_update(&c, t->st, 32); sha_update(&c, &dom, 1); sha_update(&c, &tl, 1); sha_update(&c, tag, tl);
-    sha_final(&c, t->st);
+    h_update(&c, t->st, 32); h_update(&c, &dom, 1); h_update(&c, &tl, 1); h_update(&c, tag, tl);
+    h_final(&c, t->st);
     uint8_t h[64], b;
     for (int k = 0; k < 2; k++) {
-        sha_init(&c); sha_update(&c, t->st, 32); b = (uint8_t)k; sha_update(&c, &b, 1); sha_final(&c, h + 32 * k);
+        h_init(&c); h_update(&c, t->st, 32); b = (uint8_t)k; h_update(&c, &b, 1); h_final(&c, h + 32 * k);
     }
     return reduce512(h);
 }

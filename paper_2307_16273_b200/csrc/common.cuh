@@ -47,7 +47,7 @@ struct zk_ctx {
 
 struct zk_transcript {
     zk_ctx* ctx = nullptr;
-    uint8_t* d_st = nullptr;   // 32-byte SHA-256 state on the device
+    uint8_t* d_st = nullptr;   // 32-byte transcript state (BLAKE2s digest, D3) on the device
 };
 
 namespace zk {

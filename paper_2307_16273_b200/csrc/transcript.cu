@@ -13,7 +13,7 @@ __global__ void k_tr_init(uint8_t* st, Bytes256 seed) {
         for (uint32_t i = 0; i < n; i++) b[i] = (uint8_t)lbl[i];
         for (int i = 0; i < 32; i++) b[n + i] = seed.b[i];
         uint32_t d[8];
-        sha256_buf(b, n + 32, d);
+        hash_buf(b, n + 32, d);
         st_words_to_bytes(d, st);
     }
 }
@@ -33,7 +33,8 @@ __global__ void k_tr_absorb_dev(uint8_t* st, Tag32 tag, const uint8_t* msg, uint
     if (threadIdx.x != 0) return;
     __shared__ uint32_t buf[32];
     uint8_t* b = reinterpret_cast<uint8_t*>(buf);
-    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    uint32_t h[8];
+    hash_init(h);
     // header
     uint8_t hdr[80];
     for (int i = 0; i < 32; i++) hdr[i] = st[i];
@@ -43,19 +44,14 @@ __global__ void k_tr_absorb_dev(uint8_t* st, Tag32 tag, const uint8_t* msg, uint
     for (uint32_t i = 0; i < tl; i++) hdr[34 + i] = (uint8_t)tag.s[i];
     for (int i = 0; i < 8; i++) hdr[34 + tl + i] = (uint8_t)(len >> (56 - 8 * i));
     const uint64_t hl = 42 + tl, total = hl + len;
-    const uint64_t padded = (total + 9 + 63) & ~63ull;
-    for (uint64_t off = 0; off < padded; off += 64) {
+    const uint64_t nb = total == 0 ? 1 : (total + 63) / 64;
+    for (uint64_t blk = 0; blk < nb; blk++) {
+        const uint64_t off = 64 * blk;
         for (int i = 0; i < 64; i++) {
-            uint64_t p = off + i;
-            uint8_t v;
-            if (p < hl) v = hdr[p];
-            else if (p < total) v = msg[p - hl];
-            else if (p == total) v = 0x80;
-            else if (p >= padded - 8) v = (uint8_t)((total * 8) >> (56 - 8 * (p - (padded - 8))));
-            else v = 0;
-            b[i] = v;
+            const uint64_t p = off + i;
+            b[i] = p < hl ? hdr[p] : p < total ? msg[p - hl] : 0;
         }
-        sha256_compress(h, buf);
+        hash_compress(h, buf, (uint32_t)(total < off + 64 ? total : off + 64), blk + 1 == nb);
     }
     st_words_to_bytes(h, st);
 }
@@ -70,7 +66,7 @@ __global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t 
     fs_end(s, st);
 }
 
-// Squeeze x = LE512(SHA256(st||0) || SHA256(st||1)) mod p for one challenge state (one thread).
+// Squeeze x = LE512(H(st||0) || H(st||1)) mod p for one challenge state (one thread).
 __device__ void squeeze_from_state(const uint8_t* st, uint32_t* scratch /* 32 words */, fr_t& mont, fr_t& canon) {
     uint8_t* b = reinterpret_cast<uint8_t*>(scratch);
     fr_t half[2];
@@ -78,8 +74,8 @@ __device__ void squeeze_from_state(const uint8_t* st, uint32_t* scratch /* 32 wo
         for (int i = 0; i < 32; i++) b[i] = st[i];
         b[32] = (uint8_t)k;
         uint32_t d[8];
-        sha256_buf(b, 33, d);
-        for (int i = 0; i < 8; i++) half[k].v[i] = bswap32(d[i]);
+        hash_buf(b, 33, d);
+        for (int i = 0; i < 8; i++) half[k].v[i] = d[i];   // little-endian digest words = limbs
     }
     mont = fr_add(fr_mul(ZK_R2, half[0]), fr_mul(ZK_R3, half[1]));
     canon = fr_add(fr_reduce_once(fr_reduce_once(half[0])), fr_mul(ZK_R2, half[1]));
@@ -101,7 +97,7 @@ __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mo
             b[33] = (uint8_t)tl;
             for (uint32_t k = 0; k < tl; k++) b[34 + k] = (uint8_t)tag.s[k];
             uint32_t d[8];
-            sha256_buf(b, 34 + tl, d);
+            hash_buf(b, 34 + tl, d);
             st_words_to_bytes(d, cur);
             for (int k = 0; k < 32; k++) states[i][k] = cur[k];
         }
@@ -149,7 +145,7 @@ void tr_init_dev(zk_transcript* tr, const uint8_t seed[32]) {
 
 namespace zk {
 // Diagnostics: latency of the per-round transcript step (absorb K+1 = 3 elements, squeeze one challenge),
-// and of the out-of-line field multiply, on one warp.  mode 0: full step, 1: SHA-256 compressions only,
+// and of the out-of-line field multiply, on one warp.  mode 0: full step, 1: hash (BLAKE2s) compressions only,
 // 2: fr_mul_cold chain.
 __global__ void k_diag_fs(uint8_t* st, uint32_t n, int mode, fr_t* out) {
     __shared__ FsScratch fs;
@@ -164,7 +160,7 @@ __global__ void k_diag_fs(uint8_t* st, uint32_t n, int mode, fr_t* out) {
     } else if (mode == 1) {
         if (lane == 0) {
             uint32_t h[8] = {1, 2, 3, 4, 5, 6, 7, 8};
-            for (uint32_t i = 0; i < n; i++) sha256_compress(h, fs.buf[0]);
+            for (uint32_t i = 0; i < n; i++) hash_compress(h, fs.buf[0], 64, false);
             v.v[0] = h[0];
         }
     } else {

@@ -1,12 +1,12 @@
 // transcript.cuh — device-resident Fiat-Shamir transcript (D3).
 //
 // The paper's protocols are interactive ("chosen by the verifier"); the
-// challenges here come from a SHA-256 transcript whose 32-byte state lives in
-// device memory so a whole sumcheck runs without a host round trip:
-//   st0            = SHA256("zkdl-b200/v1/init" || seed32)
-//   absorb(tag, m) : st = SHA256(st || 0x01 || u8(|tag|) || tag || u64be(|m|) || m)
-//   challenge(tag) : st = SHA256(st || 0x02 || u8(|tag|) || tag)
-//                    x  = LE512(SHA256(st || 0x00) || SHA256(st || 0x01)) mod p
+// challenges here come from a hash transcript (H = BLAKE2s-256, RFC 7693) whose 32-byte state lives
+// in device memory so a whole sumcheck runs without a host round trip:
+//   st0            = H("zkdl-b200/v1/init" || seed32)
+//   absorb(tag, m) : st = H(st || 0x01 || u8(|tag|) || tag || u64be(|m|) || m)
+//   challenge(tag) : st = H(st || 0x02 || u8(|tag|) || tag)
+//                    x  = LE512(H(st || 0x00) || H(st || 0x01)) mod p
 //
 // Latency matters (one transcript step per sumcheck round), so the step runs on one WARP of the
 // finalizing block: messages are assembled in shared memory and hashed word-wise with the round
@@ -14,94 +14,90 @@
 // parallel lanes; the two squeeze hashes and the four half-reductions of the 512-bit challenge
 // run on separate lanes.  x = lo + hi 2^256:  mont(x) = mont_mul(R^2, lo) + mont_mul(R^3, hi),
 // canonical(x) = (lo mod p) + mont_mul(R^2, hi).
+// BLAKE2s rather than SHA-256: a single-warp hash is bound by the ALU pipe (2 cycles per operation
+// per SMSP); BLAKE2s needs ~960 add/xor/rotate operations per 64-byte block against ~1900 for SHA-256
+// (no message schedule), which halves the serial transcript latency of every round.
 #pragma once
 #include "fr.cuh"
 
 namespace zk {
 
-__device__ __constant__ static const uint32_t SHA_K[64] = {
-    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
-    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
-    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
-    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
-    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
-    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
-    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
-    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
-
-__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 __device__ __forceinline__ uint32_t ror32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
 
-struct Sha8 {
+struct Hs8 {
     uint32_t h[8];
 };
 
-// One compression of a 64-byte block given as 16 little-endian-loaded words (byte-swapped here).
-// Fully unrolled so the round constants are immediates (a rolled loop with constant-bank loads ran
-// at ~66 cycles/round on the B200); one out-of-line copy (~1K instructions) for the cold paths.
-#define ZK_SHA_R(a, b, c, d, e, f, g, h, k, wv)                                                        \
+// BLAKE2s G; the message-word schedule (sigma) is resolved at compile time by the full unroll.
+#define ZK_B2_G(a, b, c, d, x, y)                                                                      \
     do {                                                                                               \
-        const uint32_t t1_ = h + (ror32(e, 6) ^ ror32(e, 11) ^ ror32(e, 25)) + ((e & f) ^ (~e & g)) + (k) + (wv); \
-        const uint32_t t2_ = (ror32(a, 2) ^ ror32(a, 13) ^ ror32(a, 22)) + ((a & b) ^ (a & c) ^ (b & c)); \
-        d += t1_;                                                                                      \
-        h = t1_ + t2_;                                                                                 \
+        a += b + (x);                                                                                  \
+        d = ror32(d ^ a, 16);                                                                          \
+        c += d;                                                                                        \
+        b = ror32(b ^ c, 12);                                                                          \
+        a += b + (y);                                                                                  \
+        d = ror32(d ^ a, 8);                                                                           \
+        c += d;                                                                                        \
+        b = ror32(b ^ c, 7);                                                                           \
     } while (0)
-#define ZK_SHA_W(w, i)                                                                                 \
-    (w[(i) & 15] += (ror32(w[((i) + 14) & 15], 17) ^ ror32(w[((i) + 14) & 15], 19) ^ (w[((i) + 14) & 15] >> 10)) + \
-                    w[((i) + 9) & 15] +                                                                \
-                    (ror32(w[((i) + 1) & 15], 7) ^ ror32(w[((i) + 1) & 15], 18) ^ (w[((i) + 1) & 15] >> 3)))
-static __device__ __noinline__ Sha8 sha256_compress_s(Sha8 s, const uint32_t* blk) {
-    static constexpr uint32_t K[64] = {
-        0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
-        0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
-        0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
-        0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
-        0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
-        0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
-        0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
-        0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
-    uint32_t w[16];
+
+// One compression F(h, m, t, f) of a 64-byte block (16 little-endian words): t = bytes hashed so far
+// including this block (messages here are < 2^32 bytes), last = final-block flag.  One out-of-line
+// copy (~1K instructions) shared by every call site.
+static __device__ __noinline__ Hs8 blake2s_compress_s(Hs8 s, const uint32_t* blk, uint32_t t, uint32_t last) {
+    static constexpr uint8_t SIG[10][16] = {
+        {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15}, {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+        {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4}, {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+        {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13}, {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+        {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11}, {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+        {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5}, {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0}};
+    uint32_t m[16];
 #pragma unroll
-    for (int i = 0; i < 16; i++) w[i] = bswap32(blk[i]);
-    uint32_t a = s.h[0], b = s.h[1], c = s.h[2], d = s.h[3], e = s.h[4], f = s.h[5], g = s.h[6], h = s.h[7];
+    for (int i = 0; i < 16; i++) m[i] = blk[i];
+    uint32_t v[16] = {s.h[0], s.h[1], s.h[2], s.h[3], s.h[4], s.h[5], s.h[6], s.h[7],
+                      0x6A09E667u, 0xBB67AE85u, 0x3C6EF372u, 0xA54FF53Au, 0x510E527Fu ^ t, 0x9B05688Cu,
+                      last ? ~0x1F83D9ABu : 0x1F83D9ABu, 0x5BE0CD19u};
 #pragma unroll
-    for (int i = 0; i < 64; i += 8) {
-        if (i >= 16) {
-#pragma unroll
-            for (int q = 0; q < 8; q++) ZK_SHA_W(w, i + q);
-        }
-        ZK_SHA_R(a, b, c, d, e, f, g, h, K[i + 0], w[(i + 0) & 15]);
-        ZK_SHA_R(h, a, b, c, d, e, f, g, K[i + 1], w[(i + 1) & 15]);
-        ZK_SHA_R(g, h, a, b, c, d, e, f, K[i + 2], w[(i + 2) & 15]);
-        ZK_SHA_R(f, g, h, a, b, c, d, e, K[i + 3], w[(i + 3) & 15]);
-        ZK_SHA_R(e, f, g, h, a, b, c, d, K[i + 4], w[(i + 4) & 15]);
-        ZK_SHA_R(d, e, f, g, h, a, b, c, K[i + 5], w[(i + 5) & 15]);
-        ZK_SHA_R(c, d, e, f, g, h, a, b, K[i + 6], w[(i + 6) & 15]);
-        ZK_SHA_R(b, c, d, e, f, g, h, a, K[i + 7], w[(i + 7) & 15]);
+    for (int r = 0; r < 10; r++) {
+        ZK_B2_G(v[0], v[4], v[8], v[12], m[SIG[r][0]], m[SIG[r][1]]);
+        ZK_B2_G(v[1], v[5], v[9], v[13], m[SIG[r][2]], m[SIG[r][3]]);
+        ZK_B2_G(v[2], v[6], v[10], v[14], m[SIG[r][4]], m[SIG[r][5]]);
+        ZK_B2_G(v[3], v[7], v[11], v[15], m[SIG[r][6]], m[SIG[r][7]]);
+        ZK_B2_G(v[0], v[5], v[10], v[15], m[SIG[r][8]], m[SIG[r][9]]);
+        ZK_B2_G(v[1], v[6], v[11], v[12], m[SIG[r][10]], m[SIG[r][11]]);
+        ZK_B2_G(v[2], v[7], v[8], v[13], m[SIG[r][12]], m[SIG[r][13]]);
+        ZK_B2_G(v[3], v[4], v[9], v[14], m[SIG[r][14]], m[SIG[r][15]]);
     }
-    s.h[0] += a; s.h[1] += b; s.h[2] += c; s.h[3] += d; s.h[4] += e; s.h[5] += f; s.h[6] += g; s.h[7] += h;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s.h[i] ^= v[i] ^ v[i + 8];
     return s;
 }
-__device__ __forceinline__ void sha256_compress(uint32_t h[8], const uint32_t* blk) {
-    Sha8 s;
+__device__ __forceinline__ void hash_init(uint32_t h[8]) {
+    h[0] = 0x6A09E667u ^ 0x01010020u;   // parameter block: 32-byte digest, unkeyed, fanout 1, depth 1
+    h[1] = 0xBB67AE85u; h[2] = 0x3C6EF372u; h[3] = 0xA54FF53Au;
+    h[4] = 0x510E527Fu; h[5] = 0x9B05688Cu; h[6] = 0x1F83D9ABu; h[7] = 0x5BE0CD19u;
+}
+__device__ __forceinline__ void hash_compress(uint32_t h[8], const uint32_t* blk, uint32_t t, bool last) {
+    Hs8 s;
 #pragma unroll
     for (int i = 0; i < 8; i++) s.h[i] = h[i];
-    s = sha256_compress_s(s, blk);
+    s = blake2s_compress_s(s, blk, t, last ? 1u : 0u);
 #pragma unroll
     for (int i = 0; i < 8; i++) h[i] = s.h[i];
 }
+// blocks of an n-byte message: the final (possibly partial, zero-padded) block carries the flag; the
+// empty message is one zero block
+__device__ __forceinline__ uint32_t hash_nblocks(uint32_t n) { return n == 0 ? 1u : (n + 63) / 64; }
 
-// SHA-256 of n bytes held in a 4-byte-aligned buffer with room for the padding
-// (capacity >= round_up(n + 9, 64)); the buffer is padded in place.  out: digest words (BE values).
-__device__ inline void sha256_buf(uint8_t* buf, uint32_t n, uint32_t out[8]) {
-    uint32_t total = (n + 9 + 63) & ~63u;
-    buf[n] = 0x80;
-    for (uint32_t i = n + 1; i < total - 8; i++) buf[i] = 0;
-    const uint64_t bits = (uint64_t)n * 8;
-    for (int i = 0; i < 8; i++) buf[total - 8 + i] = (uint8_t)(bits >> (56 - 8 * i));
-    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+// H of n bytes held in a 4-byte-aligned buffer with capacity >= 64 * hash_nblocks(n); the tail of the
+// last block is zeroed in place.  out: digest words (little-endian: state byte 4i + k = byte k of out[i]).
+__device__ inline void hash_buf(uint8_t* buf, uint32_t n, uint32_t out[8]) {
+    const uint32_t nb = hash_nblocks(n);
+    for (uint32_t i = n; i < 64 * nb; i++) buf[i] = 0;
+    uint32_t h[8];
+    hash_init(h);
     const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf);
-    for (uint32_t blk = 0; blk < total / 64; blk++) sha256_compress(h, wp + 16 * blk);
+    for (uint32_t blk = 0; blk < nb; blk++) hash_compress(h, wp + 16 * blk, min(64 * (blk + 1), n), blk + 1 == nb);
 #pragma unroll
     for (int i = 0; i < 8; i++) out[i] = h[i];
 }
@@ -112,13 +108,13 @@ __device__ __forceinline__ uint32_t zk_strlen(const char* s) {
     return n;
 }
 
-// digest words <-> the 32 state bytes
+// digest words -> the 32 state bytes (little-endian words)
 __device__ __forceinline__ void st_words_to_bytes(const uint32_t w[8], uint8_t* out) {
     for (int i = 0; i < 8; i++) {
-        out[4 * i] = (uint8_t)(w[i] >> 24);
-        out[4 * i + 1] = (uint8_t)(w[i] >> 16);
-        out[4 * i + 2] = (uint8_t)(w[i] >> 8);
-        out[4 * i + 3] = (uint8_t)w[i];
+        out[4 * i] = (uint8_t)w[i];
+        out[4 * i + 1] = (uint8_t)(w[i] >> 8);
+        out[4 * i + 2] = (uint8_t)(w[i] >> 16);
+        out[4 * i + 3] = (uint8_t)(w[i] >> 24);
     }
 }
 
@@ -144,7 +140,7 @@ __device__ inline void fr_canon_to_bytes(const fr_t& c, uint8_t* out) {
 // ---------------------------------------------------------------- warp-cooperative transcript steps
 // Shared scratch of one finalizing warp.
 struct FsScratch {
-    uint32_t buf[2][80];   // two 320-byte message buffers
+    uint32_t buf[2][96];   // two 384-byte message buffers (header <= 73 B + payload <= 256 B, whole blocks)
     uint8_t st[32];        // current state bytes
     uint8_t pay[256];      // payload (canonical field elements) of an absorb
     fr_t part[4];
@@ -166,18 +162,17 @@ __device__ __forceinline__ void fs_end(FsScratch& s, uint8_t* st_g) {
     __syncwarp();
 }
 
-// The 32 lanes assemble the padded message  st || dom || u8(|tag|) || tag || [u64be(plen)] || payload
-// into s.buf[which] (each lane a strided subset of the bytes), then lane `hasher` compresses it and
-// writes the digest to `out` (state bytes).  Every lane of the warp must call.
+// The 32 lanes assemble the message  st || dom || u8(|tag|) || tag || [u64be(plen)] || payload  (zero
+// tail to a whole block) into s.buf[which] (each lane a strided subset of the bytes), then lane `hasher`
+// compresses it and writes the digest to `out` (state bytes).  Every lane of the warp must call.
 __device__ inline void fs_hash_msg(FsScratch& s, int which, uint8_t dom, const char* tag, uint32_t tl, bool with_len,
                                    const uint8_t* pay, uint32_t plen, int hasher, uint8_t* out) {
     const int lane = threadIdx.x & 31;
     uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[which]);
     const uint32_t hl = 34 + tl + (with_len ? 8 : 0);
     const uint32_t total = hl + plen;
-    const uint32_t padded = (total + 9 + 63) & ~63u;
-    const uint64_t bits = (uint64_t)total * 8;
-    for (uint32_t p = lane; p < padded; p += 32) {
+    const uint32_t nb = hash_nblocks(total);
+    for (uint32_t p = lane; p < 64 * nb; p += 32) {
         uint8_t v;
         if (p < 32) v = s.st[p];
         else if (p == 32) v = dom;
@@ -185,15 +180,14 @@ __device__ inline void fs_hash_msg(FsScratch& s, int which, uint8_t dom, const c
         else if (p < 34 + tl) v = (uint8_t)tag[p - 34];
         else if (p < hl) v = (uint8_t)((uint64_t)plen >> (56 - 8 * (p - 34 - tl)));
         else if (p < total) v = pay[p - hl];
-        else if (p == total) v = 0x80;
-        else if (p >= padded - 8) v = (uint8_t)(bits >> (56 - 8 * (p - (padded - 8))));
         else v = 0;
         b[p] = v;
     }
     __syncwarp();
     if (lane == hasher) {
-        uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
-        for (uint32_t blk = 0; blk < padded / 64; blk++) sha256_compress(h, s.buf[which] + 16 * blk);
+        uint32_t h[8];
+        hash_init(h);
+        for (uint32_t blk = 0; blk < nb; blk++) hash_compress(h, s.buf[which] + 16 * blk, min(64 * (blk + 1), total), blk + 1 == nb);
         if (out) st_words_to_bytes(h, out);
     }
     __syncwarp();
@@ -230,24 +224,16 @@ __device__ inline fr_t fs_challenge(FsScratch& s, const char* tag) {
     // squeeze messages st || k (33 bytes, one block each) built by all lanes, hashed by lanes 0 and 1
     for (int k = 0; k < 2; k++) {
         uint8_t* b = reinterpret_cast<uint8_t*>(s.buf[k]);
-        for (uint32_t p = lane; p < 64; p += 32) {
-            uint8_t v;
-            if (p < 32) v = s.st[p];
-            else if (p == 32) v = (uint8_t)k;
-            else if (p == 33) v = 0x80;
-            else if (p == 62) v = (uint8_t)((33 * 8) >> 8);
-            else if (p == 63) v = (uint8_t)(33 * 8);
-            else v = 0;
-            b[p] = v;
-        }
+        for (uint32_t p = lane; p < 64; p += 32) b[p] = p < 32 ? s.st[p] : p == 32 ? (uint8_t)k : 0;
     }
     __syncwarp();
     if (lane < 2) {
-        uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
-        sha256_compress(h, s.buf[lane]);
-        // digest bytes are h[i] big-endian; as a little-endian 256-bit integer limb i = bytes 4i..4i+3
+        uint32_t h[8];
+        hash_init(h);
+        hash_compress(h, s.buf[lane], 33, true);
+        // the digest bytes as a little-endian 256-bit integer: limb i = word i
         fr_t x;
-        for (int i = 0; i < 8; i++) x.v[i] = bswap32(h[i]);
+        for (int i = 0; i < 8; i++) x.v[i] = h[i];
         s.half[lane] = x;   // lane 0: lo, lane 1: hi
     }
     __syncwarp();
