@@ -228,51 +228,63 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     stream = torch.cuda.Stream(device=local)
     ctx = api.Context(local, stream)
+    # zkReLU families on a second stream, concurrent with the matmul families (D3d transcripts)
+    relu_ctx = api.Context(local, torch.cuda.Stream(device=local)) if args.streams == 2 else None
+    ctxs = [ctx] + ([relu_ctx] if relu_ctx else [])
     header = fcn.fcn_header(shape)
     seed = fs_seed(f"C4-rank{rank}")
+
+    def prof_on(name):
+        for c in ctxs:
+            c.profile_filter(name)
+            c.profile(True)
+            c.profile_read()
+
+    def prof_off() -> dict:
+        merged = {}
+        for c in ctxs:
+            for k, (n, t) in c.profile_read().items():
+                n0, t0 = merged.get(k, (0, 0.0))
+                merged[k] = (n0 + n, t0 + t)
+            c.profile(False)
+            c.profile_filter(None)
+        return merged
+
     def profiled_pass():
-        """K windows with CUDA events around every launch: the per-kernel table."""
-        ctx.profile_filter(None)
-        ctx.profile(True)
-        ctx.profile_read()
+        """K windows, one stream, CUDA events around every launch: the per-kernel table."""
+        prof_on(None)
         for _ in range(args.steps):
             dfcn.enqueue_window(ctx, seed, header, dev_fams)
         torch.cuda.synchronize()
-        p = ctx.profile_read()
-        ctx.profile(False)
-        return p
+        return prof_off()
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            dfcn.prove_window(ctx, seed, header, dev_fams)
-        ctx.synchronize()
+            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx)
+        torch.cuda.synchronize()
         # kernel table first (outside the timed region) -> the dominant kernel
         prof_table = profiled_pass() if args.prof == "dominant" else None
         dom_name = dominant_kernel(prof_table) if prof_table else None
-        # ---- timed region: K windows, inputs resident in HBM (1.45 GB per window > 126 MB L2)
+        # ---- timed region: K windows, inputs resident in HBM (0.97 GB of stacks per window > 126 MB L2)
         clocks = Clocks(local)
         clocks.start()
-        launches0 = ctx.launches
+        launches0 = sum(c.launches for c in ctxs)
         if args.prof in ("inline", "dominant"):
             # events around every launch ("inline") or only around the dominant kernel's launches
-            ctx.profile_filter(dom_name)
-            ctx.profile(True)
-            ctx.profile_read()
+            prof_on(dom_name)
         barrier(world)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams) for _ in range(args.steps)]
-        ev1.record(stream)
+        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx) for _ in range(args.steps)]
+        ev1.record(stream)   # each window joins the zkReLU stream back into this one before its end
         torch.cuda.synchronize()
         res = dfcn.collect_window(*pending[-1])   # outputs stay in HBM until here (outside the timed region)
         del pending
         barrier(world)
-        launches = ctx.launches - launches0
+        launches = sum(c.launches for c in ctxs) - launches0
         clk = clocks.stop()
-        prof_live = ctx.profile_read() if args.prof in ("inline", "dominant") else {}
-        ctx.profile(False)
-        ctx.profile_filter(None)
+        prof_live = prof_off() if args.prof in ("inline", "dominant") else {}
         if args.prof == "inline":
             prof_table = prof_live
         elif args.prof == "separate":
@@ -298,7 +310,7 @@ def run_ours(args, rank, world, local):
     copy_stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         if e2e_steps:   # one untimed end-to-end window: allocator warm-up for the upload buffers
-            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream)
+            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx)
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -306,7 +318,7 @@ def run_ours(args, rank, world, local):
         for _ in range(e2e_steps):
             # pinned host -> HBM per family on a copy stream, overlapped with the earlier families'
             # proofs; proof bytes come back to the host
-            out = dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream)
+            out = dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     h2d = sum(t.numel() * t.element_size() for t in pinned.values())   # distinct stacks, copied once each
@@ -349,7 +361,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps, "
                                "9 families (F x3, GA x2, GW x3, ReLU D=2^23), one transcript",
                    "updates_per_step": shape.steps, "input_bytes_per_step": in_bytes,
-                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}"},
+                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams},
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "fcn.prove_window_from_host: pinned host stacks -> HBM per family on a copy stream "
@@ -448,6 +460,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4", choices=["C4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
+                    help="2: zkReLU families on a second stream, concurrent with the matmul families")
     ap.add_argument("--prof", default="dominant", choices=["dominant", "inline", "separate"],
                     help="where per-kernel CUDA-event durations come from (see roofline.durations)")
     ap.add_argument("--profile-mode", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")

@@ -76,6 +76,16 @@ zk_status zk_transcript_new(zk_ctx* ctx, const uint8_t seed[32], zk_transcript**
 zk_status zk_transcript_absorb(zk_transcript* tr, const char* tag, const void* msg, uint64_t len);
 zk_status zk_transcript_challenges(zk_transcript* tr, const char* tag, uint32_t n, zk_fr* out);
 zk_status zk_transcript_state(zk_transcript* tr, uint8_t out[32]);
+/* Fork / join (D3d: independent statements get independent transcripts, so they can be proved
+ * concurrently).  zk_transcript_fork: the parent draws challenge `tag` (one field element x) and *out
+ * is a new transcript seeded with the canonical 32 bytes of x (as zk_transcript_new(x) would be);
+ * it runs on child_ctx's stream (NULL: the parent's).  The fork kernel runs on the parent's stream:
+ * order the child's first use after it (cudaEvent) when the streams differ.
+ * zk_transcript_absorb_state: absorb(tag, <32-byte state of other>) on tr's stream; other's work must
+ * be ordered before it.  Free a transcript only after every use on every stream is ordered before
+ * its own stream's free (zk_transcript_free is stream-ordered on its ctx's stream). */
+zk_status zk_transcript_fork(zk_transcript* parent, const char* tag, zk_ctx* child_ctx, zk_transcript** out);
+zk_status zk_transcript_absorb_state(zk_transcript* tr, const char* tag, const zk_transcript* other);
 void zk_transcript_free(zk_transcript* tr);
 
 /* ------------------------------------------------------------ tables (rows a1, a2)

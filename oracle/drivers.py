@@ -85,19 +85,30 @@ def c5_prove(m: int):
 
 
 def fcn_prove(shape, families, seed_name: str, only=None):
-    """D3d: one transcript, "fcn/hdr" then per family "fcn/fam" <name> and its protocol."""
-    tr = O.Transcript(fs_seed(seed_name))
-    tr.absorb("fcn/hdr", fcn_header(shape))
+    """D3d: window transcript W: "fcn/hdr"; per family (in order) "fcn/fam" <name> and a fork: the family
+    transcript T_f is seeded with the canonical bytes of W's challenge "fcn/fork"; each family's protocol
+    runs on its own T_f; finally W absorbs "fcn/join" <T_f state> for every family (in order).
+    Returns the per-family results (res["state"] = T_f's final state) and, as the last entry's
+    "window_state", W's final state."""
+    W = O.Transcript(fs_seed(seed_name))
+    W.absorb("fcn/hdr", fcn_header(shape))
+    fams = list(families if only is None else families[:only])
+    forks = []
+    for f in fams:
+        W.absorb("fcn/fam", f.name.encode())
+        c = W.challenges("fcn/fork", 1)[0]
+        forks.append(O.Transcript(c.to_bytes(32, "little")))
     out = []
-    for f in families:
-        tr.absorb("fcn/fam", f.name.encode())
+    for f, T in zip(fams, forks):
         if isinstance(f, MatmulFamily):
-            res = O.matmul_prove(tr, f.A, f.B, f.transA, f.transB)
+            res = O.matmul_prove(T, f.A, f.B, f.transA, f.transB)
         else:
-            res = O.relu_prove(tr, f.Z, f.GA, f.Q, f.R)
+            res = O.relu_prove(T, f.Z, f.GA, f.Q, f.R)
         res["name"] = f.name
-        res["state"] = tr.state()
+        res["state"] = T.state()
         out.append(res)
-        if only is not None and len(out) >= only:
-            break
+    for T in forks:
+        W.absorb("fcn/join", T.state())
+    if out:
+        out[-1]["window_state"] = W.state()
     return out

@@ -59,6 +59,8 @@ def lib():
         "zk_transcript_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_transcript_challenges": ([vp, c.c_char_p, u32, vp], i32),
         "zk_transcript_state": ([vp, vp], i32),
+        "zk_transcript_fork": ([vp, c.c_char_p, vp, c.POINTER(vp)], i32),
+        "zk_transcript_absorb_state": ([vp, c.c_char_p, vp], i32),
         "zk_transcript_free": ([vp], None),
         "zk_embed_i32": ([vp, vp, u64, vp], i32),
         "zk_eq_table": ([vp, vp, u32, vp, vp], i32),

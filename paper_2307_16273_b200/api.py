@@ -91,12 +91,27 @@ class Context:
 class Transcript:
     """zk_transcript: device-resident Fiat-Shamir state (D3)."""
 
-    def __init__(self, ctx: Context, seed: bytes):
-        assert len(seed) == 32
+    def __init__(self, ctx: Context, seed: bytes | None, _handle=None):
         self.ctx = ctx
+        if _handle is not None:
+            self.h = _handle
+            return
+        assert len(seed) == 32
         h = ctypes.c_void_p()
         ctx.check(lib().zk_transcript_new(ctx.h, seed, ctypes.byref(h)))
         self.h = h
+
+    def fork(self, tag: str, ctx: Context | None = None) -> "Transcript":
+        """D3d fork: a child transcript seeded with this transcript's challenge `tag`, bound to `ctx`
+        (its stream; default this transcript's).  Enqueued on this transcript's stream."""
+        h = ctypes.c_void_p()
+        child_ctx = ctx if ctx is not None else self.ctx
+        self.ctx.check(lib().zk_transcript_fork(self.h, tag.encode(), child_ctx.h, ctypes.byref(h)))
+        return Transcript(child_ctx, None, _handle=h)
+
+    def absorb_state(self, tag: str, other: "Transcript"):
+        """absorb(tag, other's 32-byte state), device to device (D3d join)."""
+        self.ctx.check(lib().zk_transcript_absorb_state(self.h, tag.encode(), other.h))
 
     def absorb(self, tag: str, msg: bytes):
         self.ctx.check(lib().zk_transcript_absorb(self.h, tag.encode(), msg, len(msg)))

@@ -11,6 +11,8 @@ using namespace zk;
 namespace zk {
 __global__ void k_from_canonical(const fr_t* in, uint64_t n, fr_t* out, unsigned int* bad);
 void tr_init_dev(zk_transcript* tr, const uint8_t seed[32]);
+void tr_fork_dev(zk_transcript* parent, const char* tag, uint8_t* d_child_st);
+void tr_absorb_state_dev(zk_transcript* tr, const char* tag, const uint8_t* d_other_st);
 void selftest_op_dev(zk_ctx* ctx, int op, const fr_t* a, const fr_t* b, uint64_t n, fr_t* out);
 void mul_bench_dev(zk_ctx* ctx, const fr_t* seed, uint32_t iters, uint32_t blocks, fr_t* out);
 }
@@ -169,6 +171,38 @@ zk_status zk_transcript_state(zk_transcript* tr, uint8_t out[32]) {
     ZK_API_BEGIN(ctx)
     ZK_CUDA(cudaMemcpyAsync(out, tr->d_st, 32, cudaMemcpyDeviceToHost, ctx->stream));
     ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    ZK_API_END(ctx)
+}
+
+zk_status zk_transcript_fork(zk_transcript* parent, const char* tag, zk_ctx* child_ctx, zk_transcript** out) {
+    if (!parent) return ZK_ERR_ARG;
+    zk_ctx* ctx = parent->ctx;
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(tag && out, ZK_ERR_ARG, "null argument");
+    zk_transcript* t = new zk_transcript();
+    t->ctx = child_ctx ? child_ctx : ctx;
+    cudaError_t e = cudaMallocAsync(&t->d_st, 32, ctx->stream);   // written on the parent's stream
+    if (e != cudaSuccess) {
+        delete t;
+        throw ZkError{ZK_ERR_OOM, "cudaMallocAsync transcript"};
+    }
+    try {
+        tr_fork_dev(parent, tag, t->d_st);
+    } catch (...) {
+        cudaFreeAsync(t->d_st, ctx->stream);
+        delete t;
+        throw;
+    }
+    *out = t;
+    ZK_API_END(ctx)
+}
+
+zk_status zk_transcript_absorb_state(zk_transcript* tr, const char* tag, const zk_transcript* other) {
+    if (!tr || !other) return ZK_ERR_ARG;
+    zk_ctx* ctx = tr->ctx;
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(tag, ZK_ERR_ARG, "null tag");
+    tr_absorb_state_dev(tr, tag, other->d_st);
     ZK_API_END(ctx)
 }
 

@@ -56,6 +56,26 @@ __global__ void k_tr_absorb_dev(uint8_t* st, Tag32 tag, const uint8_t* msg, uint
     st_words_to_bytes(h, st);
 }
 
+// Fork (D3d): the parent draws challenge `tag`; the child's initial state is
+// H("zkdl-b200/v1/init" || canonical bytes of that challenge), i.e. a transcript seeded with it.
+__global__ void k_tr_fork(uint8_t* st, Tag32 tag, uint8_t* child_st) {
+    __shared__ FsScratch s;
+    __shared__ uint32_t buf[32];
+    fs_begin(s, st);
+    fs_challenge(s, tag.s);
+    if (threadIdx.x == 0) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(buf);
+        const char* lbl = "zkdl-b200/v1/init";
+        const uint32_t n = zk_strlen(lbl);
+        for (uint32_t i = 0; i < n; i++) b[i] = (uint8_t)lbl[i];
+        fr_canon_to_bytes(s.rc, b + n);
+        uint32_t d[8];
+        hash_buf(b, n + 32, d);
+        st_words_to_bytes(d, child_st);
+    }
+    fs_end(s, st);
+}
+
 // n <= 8 field elements from device memory (Montgomery)
 __global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t n, uint8_t* copy_out) {
     __shared__ FsScratch s;
@@ -139,6 +159,14 @@ void tr_challenges_dev(zk_transcript* tr, const char* tag, uint32_t n, fr_t* d_o
 
 void tr_init_dev(zk_transcript* tr, const uint8_t seed[32]) {
     ZK_LAUNCH(tr->ctx, k_tr_init, 1, 32, 0, tr->d_st, make_bytes(seed, 32));
+}
+
+void tr_fork_dev(zk_transcript* parent, const char* tag, uint8_t* d_child_st) {
+    ZK_LAUNCH(parent->ctx, k_tr_fork, 1, 32, 0, parent->d_st, make_tag(tag), d_child_st);
+}
+
+void tr_absorb_state_dev(zk_transcript* tr, const char* tag, const uint8_t* d_other_st) {
+    ZK_LAUNCH(tr->ctx, k_tr_absorb_dev, 1, 32, 0, tr->d_st, make_tag(tag), d_other_st, (uint64_t)32);
 }
 
 }  // namespace zk

@@ -1,13 +1,16 @@
 """FAC4DNN family driver (PAPER Example 2 P:L292-312, Protocol 1 line 7 P:L326).
 
-One Fiat-Shamir transcript per proving window (D3d): "fcn/hdr", then for every
-family in the fixed order of synth.fcn.assemble_families, "fcn/fam" <name>
-followed by the family's protocol — matmul families: zk_matmul_prove (the
+Fiat-Shamir per proving window (D3d): the window transcript absorbs "fcn/hdr",
+then for every family in the fixed order of synth.fcn.assemble_families
+"fcn/fam" <name> and forks the family's own transcript, on which the family's
+protocol runs — matmul families: zk_matmul_prove (the
 reduction of zk_matmul_reduce then zk_sumcheck_prove with m = logN + logD2,
 n_eq = logN, K = 2); ReLU families: zk_relu_prove_dev.  Stack tensors must
 already be resident on the device; this module only sequences the library calls
-(no arithmetic here).  Every family writes into one device buffer and the whole
-window synchronises once, when the proofs are copied back.
+(no arithmetic here).  The window absorbs every family's final state at the end
+("fcn/join").  Independent transcripts let the zkReLU family run on a second
+stream concurrently with the matmul families.  Every family writes into one
+device buffer and the window synchronises once, when the proofs are copied back.
 """
 from __future__ import annotations
 
@@ -68,17 +71,23 @@ def _slot(n: int) -> int:
 
 def window_out_bytes(families: list) -> int:
     """Size of a window's device output buffer (what collect_window copies back)."""
-    return sum(_slot(_layout(f)[1]) for f in families)
+    return sum(_slot(_layout(f)[1]) for f in families) + 256   # + the window transcript's final state
 
 
-def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list, ready: list | None = None):
-    """Enqueue one window's proofs on the context stream without synchronising.
+def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list, ready: list | None = None,
+                   relu_ctx: api.Context | None = None, proof_order: list | None = None):
+    """Enqueue one window's proofs without synchronising.
 
-    ready (optional): one torch.cuda.Event per family that the context stream waits on before that
-    family's proof -- e.g. the end of its host->device upload on a copy stream, so uploads of later
-    families overlap the proofs of earlier ones.
-    Returns (out, flag, layout): `out` is one uint8 device buffer holding, per family, its proof
-    output followed by the 32-byte transcript state after the family; `flag` the int32 range flag."""
+    Transcripts (D3d): the window transcript W absorbs "fcn/hdr", then per family "fcn/fam"
+    <name> and forks that family's transcript ("fcn/fork"); every family is proved on its own
+    transcript; W finally absorbs "fcn/join" <family state> for every family.  With relu_ctx (a context
+    on a second stream) the zkReLU families run there, concurrently with the matmul families on ctx.
+    ready (optional): one torch.cuda.Event per family that its stream waits on before its proof (the
+    end of its host->device upload on a copy stream).  proof_order (optional): the order in which the
+    families' proofs are enqueued (indices into `families`); forks and joins always follow the list
+    order, so the transcripts and proof bytes do not depend on it.
+    Returns (out, flag, layout): `out` holds, per family, its proof output followed by the family
+    transcript's final state, then W's final state; `flag` is the int32 range flag."""
     dev = (families[0].A if families[0].kind == "matmul" else families[0].Z).device
     lay = []
     off = 0
@@ -86,25 +95,50 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
         info, n = _layout(f)
         lay.append((f, info, off, n))
         off += _slot(n)
-    out = torch.empty(off, dtype=torch.uint8, device=dev)
+    out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
-    tr = api.Transcript(ctx, seed)
-    tr.absorb("fcn/hdr", header)
-    for i, (f, info, o, n) in enumerate(lay):
+    two = relu_ctx is not None and relu_ctx.stream != ctx.stream
+    ctx_of = lambda f: relu_ctx if (two and f.kind == "relu") else ctx
+    W = api.Transcript(ctx, seed)
+    W.absorb("fcn/hdr", header)
+    kids = []
+    for f in families:
+        W.absorb("fcn/fam", f.name.encode())
+        kids.append(W.fork("fcn/fork", ctx_of(f)))
+    if two:
+        ev = torch.cuda.Event()
+        ev.record(ctx.stream)
+        relu_ctx.stream.wait_event(ev)
+    for i in (proof_order if proof_order is not None else range(len(lay))):
+        f, info, o, n = lay[i]
+        c, T = ctx_of(f), kids[i]
         if ready is not None:
-            ctx.stream.wait_event(ready[i])
-        tr.absorb("fcn/fam", f.name.encode())
+            c.stream.wait_event(ready[i])
         if f.kind == "matmul":
-            api.matmul_prove(ctx, tr, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
+            api.matmul_prove(c, T, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
         else:
-            api.relu_prove_dev(ctx, tr, f.Z, f.GA, f.Q, f.R, flag, out=out[o:o + n])
-        tr.state_dev(out[o + n:o + n + 32])
-    tr.close()   # stream-ordered: the state buffer is released after the enqueued work
+            api.relu_prove_dev(c, T, f.Z, f.GA, f.Q, f.R, flag, out=out[o:o + n])
+        T.state_dev(out[o + n:o + n + 32])
+    if two:
+        ev = torch.cuda.Event()
+        ev.record(relu_ctx.stream)
+        ctx.stream.wait_event(ev)
+    for T in kids:
+        W.absorb_state("fcn/join", T)
+    W.state_dev(out[off:off + 32])
+    if two:   # the children are freed on their own streams: after the joins
+        ev = torch.cuda.Event()
+        ev.record(ctx.stream)
+        relu_ctx.stream.wait_event(ev)
+    for T in kids:
+        T.close()
+    W.close()   # stream-ordered: the state buffers are released after the enqueued work
     return out, flag, lay
 
 
 def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
-    """Copy a window's outputs to the host (the one synchronisation) and parse them."""
+    """Copy a window's outputs to the host (the one synchronisation) and parse them.  The last result
+    also carries "window_state" (the window transcript after the joins)."""
     raw = out.cpu().numpy().tobytes()
     if int(flag.item()) & 1:
         raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")
@@ -121,15 +155,19 @@ def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
                        finals=r["finals"], proof=r["proof"])
         res["state"] = raw[o + n:o + n + 32]
         results.append(res)
+    end = len(raw) - 256
+    results[-1]["window_state"] = raw[end:end + 32]
     return results
 
 
-def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list) -> list:
-    """Prove every family of one window under one transcript; returns per-family results."""
-    return collect_window(*enqueue_window(ctx, seed, header, families))
+def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
+                 relu_ctx: api.Context | None = None) -> list:
+    """Prove every family of one window (D3d transcripts); returns per-family results."""
+    return collect_window(*enqueue_window(ctx, seed, header, families, relu_ctx=relu_ctx))
 
 
-def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None) -> list:
+def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None,
+                           relu_ctx: api.Context | None = None) -> list:
     """The user-facing end-to-end call: families given as host (ideally pinned) int32 tensors.
 
     Each family's stacks are copied host->device on `copy_stream` (one is created if None) and its
@@ -148,14 +186,23 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
             uploaded[key] = t.to(dev, non_blocking=True)
         return uploaded[key]
 
+    # upload (and proof) order: zkReLU families first (least data, most work), then the matmul
+    # families by decreasing operand bytes, so the families proved last have the least left to do
+    def nbytes(f):
+        ts = (f.A, f.B) if f.kind == "matmul" else (f.Z, f.GA)
+        return sum(t.numel() * t.element_size() for t in ts)
+    order = sorted(range(len(host_families)),
+                   key=lambda i: (host_families[i].kind != "relu", -nbytes(host_families[i]), i))
+    fams, ready = [None] * len(host_families), [None] * len(host_families)
     with torch.cuda.stream(cs):
-        for f in host_families:
+        for i in order:
+            f = host_families[i]
             up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
             g = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
-            for t in up.values():
-                t.record_stream(ctx.stream)   # the proof reads it on the context stream
+            for t in up.values():   # the proof reads it on its family's stream
+                t.record_stream(relu_ctx.stream if (relu_ctx is not None and f.kind == "relu") else ctx.stream)
             ev = torch.cuda.Event()
             ev.record(cs)
-            fams.append(g)
-            ready.append(ev)
-    return collect_window(*enqueue_window(ctx, seed, header, fams, ready))
+            fams[i] = g
+            ready[i] = ev
+    return collect_window(*enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order))

@@ -280,11 +280,19 @@ def test_fcn_tiny_vs_oracle(ctx, O):
         assert gr["msgs"] == orr["msgs"], gr["name"]
         assert gr["finals"] == orr["finals"], gr["name"]
         assert gr["state"] == orr["state"], gr["name"]
-    # end-to-end entry (host tensors, per-family uploads overlapped with proofs): same bytes
+    assert g[-1]["window_state"] == o[-1]["window_state"]          # D3d joins
+    # end-to-end entry (host tensors, per-family uploads overlapped with proofs) with the zkReLU
+    # family on a second stream: same bytes
+    import torch
+    from paper_2307_16273_b200 import api
+    relu_ctx = api.Context(0, torch.cuda.Stream())
     host = dfcn.upload_families(fams, device="cpu")
-    h = dfcn.prove_window_from_host(ctx, fs_seed("tiny"), fcn.fcn_header(shape), host)
+    h = dfcn.prove_window_from_host(ctx, fs_seed("tiny"), fcn.fcn_header(shape), host, relu_ctx=relu_ctx)
     assert [r["proof"] for r in h] == [r["proof"] for r in g]
     assert [r["state"] for r in h] == [r["state"] for r in g]
+    assert h[-1]["window_state"] == g[-1]["window_state"]
+    g2 = dfcn.prove_window(ctx, fs_seed("tiny"), fcn.fcn_header(shape), dfcn.upload_families(fams), relu_ctx=relu_ctx)
+    assert [r["proof"] for r in g2] == [r["proof"] for r in g] and g2[-1]["window_state"] == g[-1]["window_state"]
 
 
 def test_async_provers_match_sync(ctx):

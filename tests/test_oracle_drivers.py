@@ -63,3 +63,16 @@ def test_fcn_family_driver_tiny(oracle_lib):
             assert res["claim"] == O.mle_i32(Y, res["u3"] + res["u1"] + res["w"])
     again = drivers.fcn_prove(shape, fams, "tiny")
     assert [r["state"] for r in again] == [r["state"] for r in out]       # determinism
+    # D3d forks: family f's transcript depends only on the window header and the names up to f
+    first = drivers.fcn_prove(shape, fams, "tiny", only=2)
+    assert [r["state"] for r in first] == [r["state"] for r in out[:2]]
+    # the window state is the join of the family states, written out with the transcript primitives
+    from synth.prng import fs_seed
+    W = O.Transcript(fs_seed("tiny"))
+    W.absorb("fcn/hdr", fcn.fcn_header(shape))
+    for f in fams:
+        W.absorb("fcn/fam", f.name.encode())
+        W.challenges("fcn/fork", 1)
+    for r in out:
+        W.absorb("fcn/join", r["state"])
+    assert W.state() == out[-1]["window_state"]
