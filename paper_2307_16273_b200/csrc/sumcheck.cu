@@ -505,8 +505,9 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
             }
         } else {
             if (tid == 0) {
-                while (ld_volatile(a.flag) < t + 1) {
-                }
+                // back off while the reducer hashes: the waiting warps leave the issue slots to
+                // kernels of the other stream sharing the SM
+                while (ld_volatile(a.flag) < t + 1) __nanosleep(256);
                 __threadfence();
             }
         }
@@ -552,7 +553,10 @@ static unsigned int all_grid(zk_ctx* ctx, uint32_t m) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sc_all<K>, 256, 0);
     if (per_sm < 1) per_sm = 1;
+    // at most one block per SM: the rounds are latency-bound after the first few, and a persistent
+    // grid that fills the GPU would crowd out the zkReLU kernels running on the other stream
     uint64_t cap = (uint64_t)per_sm * ctx->num_sms;
+    if (cap > (uint64_t)ctx->num_sms) cap = (uint64_t)ctx->num_sms;
     uint64_t need = ((1ull << (m - 1)) + 255) / 256 + 1;   // + the reducer block
     if (need < 2) need = 2;
     return (unsigned int)(need < cap ? need : cap);
