@@ -177,23 +177,29 @@ def family_bytes(fams) -> int:
     return tot
 
 
-def frmul_model(fams) -> dict:
-    """Algorithmic Fr-mul counts per window by kernel family (DESIGN.md §6 counting model)."""
+def frmul_model(fams, persist_log: int = 16, hb: int = 5) -> dict:
+    """Algorithmic Fr-mul counts per window by kernel (DESIGN.md §6 counting model).  The split of the
+    zkReLU i-rounds between the per-round kernel and the persistent one mirrors relu.cu (rounds with at
+    most 2^persist_log pairs run in k_relu_ipersist; the last hb rounds in k_relu_itail)."""
     relu = [f for f in fams if not hasattr(f, "A")]
-    out = {"k_relu_iround": 0, "k_sc_round": 0}
+    out = {"k_relu_iround_f": 0, "k_relu_ipersist": 0, "k_sc_all": 0}
     for f in relu:
         D = f.Z.size
-        # i-rounds, per pair and side (two sides per pair): eq scaling 6 + per evaluation point X in
-        # {0, 2, 3} P = a (E_a + oms E_c + (a-1) E_b): 3 products (2 in the first round, where oms is a
-        # small integer); folds (rounds >= 2): a 2 + shared oms 1.  First round D/2 pairs x 2 x 12, later
-        # rounds D/4 + D/8 + ... ~ D/2 pairs x 2 x 18  ->  ~30 D
-        out["k_relu_iround"] += 30 * D
+        logD = D.bit_length() - 1
+        H = logD - min(hb, logD)
+        t0 = next((t for t in range(1, H) if (D >> (t + 1)) <= (1 << persist_log)), H)
+        # factored i-round, per pair (two sides): first round 2 x (6 E'a + 3 T_b) = 18; folding rounds
+        # 2 x (3 fold + 6 E'a + 3 T_c + 3 T_b) = 30; plus 8 HI' products per thread and launch (not counted)
+        for t in range(H):
+            pairs = D >> (t + 1)
+            per = 18 if t == 0 else 30
+            out["k_relu_iround_f" if t < t0 else "k_relu_ipersist"] += per * pairs
     for f in fams:
         if hasattr(f, "A"):
             N = f.A.shape[0]
             D2 = f.A.shape[1] if f.transA else f.A.shape[2]
             # K = 2 product rounds: fold 4 + eq 1 + 3 evaluations x 2 = 11 per pair, pairs summed ~ N * D2
-            out["k_sc_round"] += 11 * N * D2
+            out["k_sc_all"] += 11 * N * D2
     return out
 
 
@@ -230,7 +236,12 @@ def run_ours(args, rank, world, local):
     ctx = api.Context(local, stream)
     # zkReLU families on a second stream, concurrent with the matmul families (D3d transcripts)
     relu_ctx = api.Context(local, torch.cuda.Stream(device=local)) if args.streams == 2 else None
-    ctxs = [ctx] + ([relu_ctx] if relu_ctx else [])
+    # matmul families spread over --mm-streams contexts (one stream each), persistent grids budgeted
+    mm_ctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.mm_streams - 1)]
+    if args.mm_streams > 1:
+        for c in [ctx] + mm_ctxs:
+            c.set_sm_budget(max(8, 148 // args.mm_streams))
+    ctxs = [ctx] + ([relu_ctx] if relu_ctx else []) + mm_ctxs
     header = fcn.fcn_header(shape)
     seed = fs_seed(f"C4-rank{rank}")
 
@@ -260,7 +271,7 @@ def run_ours(args, rank, world, local):
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx)
+            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
         torch.cuda.synchronize()
         # kernel table first (outside the timed region) -> the dominant kernel
         prof_table = profiled_pass() if args.prof == "dominant" else None
@@ -276,7 +287,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx) for _ in range(args.steps)]
+        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs) for _ in range(args.steps)]
         ev1.record(stream)   # each window joins the zkReLU stream back into this one before its end
         torch.cuda.synchronize()
         res = dfcn.collect_window(*pending[-1])   # outputs stay in HBM until here (outside the timed region)
@@ -310,7 +321,7 @@ def run_ours(args, rank, world, local):
     copy_stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         if e2e_steps:   # one untimed end-to-end window: allocator warm-up for the upload buffers
-            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx)
+            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -318,7 +329,7 @@ def run_ours(args, rank, world, local):
         for _ in range(e2e_steps):
             # pinned host -> HBM per family on a copy stream, overlapped with the earlier families'
             # proofs; proof bytes come back to the host
-            out = dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx)
+            out = dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     h2d = sum(t.numel() * t.element_size() for t in pinned.values())   # distinct stacks, copied once each
@@ -361,7 +372,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps, "
                                "9 families (F x3, GA x2, GW x3, ReLU D=2^23), one transcript",
                    "updates_per_step": shape.steps, "input_bytes_per_step": in_bytes,
-                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams},
+                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams},
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "fcn.prove_window_from_host: pinned host stacks -> HBM per family on a copy stream "
@@ -462,6 +473,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")
+    ap.add_argument("--mm-streams", type=int, default=1,
+                    help="streams (contexts) the matmul families are spread over, side by side")
     ap.add_argument("--prof", default="dominant", choices=["dominant", "inline", "separate"],
                     help="where per-kernel CUDA-event durations come from (see roofline.durations)")
     ap.add_argument("--profile-mode", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")

@@ -56,6 +56,11 @@ const char* zk_last_error(const zk_ctx* ctx);
 const char* zk_version(void);
 uint64_t zk_ctx_launch_count(const zk_ctx* ctx);
 zk_status zk_ctx_synchronize(zk_ctx* ctx);
+/* Cap the grid of the context's persistent kernels (the one-launch small-statement sumcheck) at
+ * `sms` CTAs, at most one per SM (0 = every SM, the default).  Several contexts on several streams
+ * with budgets that add up to the SM count prove independent statements side by side instead of
+ * each latency-bound statement spreading thinly over the whole GPU.  Never changes any output. */
+zk_status zk_ctx_set_sm_budget(zk_ctx* ctx, uint32_t sms);
 /* Per-launch profiling: while enabled, every kernel launch of the context is bracketed by two
  * CUDA events on the context stream.  zk_ctx_profile_read synchronises, writes one line per kernel
  * "name<TAB>launches<TAB>total_ms\n" (NUL-terminated, cap bytes max) and clears the records. */

@@ -55,6 +55,7 @@ def lib():
         "zk_ctx_profile": ([vp, i32], i32),
         "zk_ctx_profile_read": ([vp, c.c_char_p, u64], i32),
         "zk_ctx_profile_filter": ([vp, c.c_char_p], i32),
+        "zk_ctx_set_sm_budget": ([vp, u32], i32),
         "zk_transcript_new": ([vp, vp, c.POINTER(vp)], i32),
         "zk_transcript_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_transcript_challenges": ([vp, c.c_char_p, u32, vp], i32),

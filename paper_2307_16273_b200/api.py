@@ -60,6 +60,10 @@ class Context:
     def synchronize(self):
         self.check(lib().zk_ctx_synchronize(self.h))
 
+    def set_sm_budget(self, sms: int):
+        """zk_ctx_set_sm_budget: cap the grid of this context's persistent kernels (0 = every SM)."""
+        self.check(lib().zk_ctx_set_sm_budget(self.h, int(sms)))
+
     def profile(self, enable: bool):
         self.check(lib().zk_ctx_profile(self.h, int(enable)))
 

@@ -77,6 +77,12 @@ zk_status zk_ctx_synchronize(zk_ctx* ctx) {
     ZK_API_END(ctx)
 }
 
+zk_status zk_ctx_set_sm_budget(zk_ctx* ctx, uint32_t sms) {
+    ZK_API_BEGIN(ctx)
+    ctx->sm_budget = (int)sms;
+    ZK_API_END(ctx)
+}
+
 zk_status zk_ctx_profile(zk_ctx* ctx, int enable) {
     ZK_API_BEGIN(ctx)
     ctx->prof = enable != 0;

@@ -16,6 +16,7 @@ struct zk_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
+    int sm_budget = 0;         // cap on the grid of persistent kernels (0 = every SM), zk_ctx_set_sm_budget
     uint64_t launches = 0;
     std::string err;
     // per-launch CUDA-event profiling (zk_ctx_profile): events bracket each launch on the ctx stream

@@ -221,6 +221,14 @@ __device__ __forceinline__ fr_t fr_sqr(const fr_t& a) { return fr_mul(a, a); }
 // body was > 100 KB of SASS; ncu stall_no_inst 36%).
 static __device__ __noinline__ fr_t fr_mul_ni(fr_t a, fr_t b) { return fr_mul(a, b); }
 
+// Three independent products in one out-of-line body: the scheduler interleaves the three CIOS
+// chains, so a warp has three-way instruction-level parallelism inside the product (the single
+// product is a dependent chain that leaves the pipes idle at low occupancy).
+struct fr3_t { fr_t x, y, z; };
+static __device__ __noinline__ fr3_t fr_mul3_ni(fr_t a0, fr_t b0, fr_t a1, fr_t b1, fr_t a2, fr_t b2) {
+    return fr3_t{fr_mul(a0, b0), fr_mul(a1, b1), fr_mul(a2, b2)};
+}
+
 // One out-of-line copy for cold code (finalizers, single-CTA round kernels): the inlined product is
 // ~560 SASS instructions, and cold code that inlines dozens of them runs out of the instruction
 // cache (ncu: stall_no_inst dominated the round kernels' finalize).

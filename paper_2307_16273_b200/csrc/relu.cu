@@ -577,6 +577,7 @@ __global__ void k_relu_materialize(const int32_t* Z, const int32_t* GA, uint64_t
 }
 
 struct IRoundArgs {
+    uint32_t cpb;          // k_relu_iround_f: CTAs per HI block (grid = 2^hb * cpb)
     const fr_t* src[3];   // a0, a1, oms
     fr_t* dst[3];
     uint64_t n_pairs;
@@ -597,9 +598,102 @@ struct IRoundArgs {
     uint8_t* point_out;
 };
 
+// Finalizer of an i-round (last block, after the grid reduction), in two parts so that the persistent
+// kernel can release the next round as soon as r_t exists:
+//  iround_transcript: message (g(0), c - g(0), g(2), g(3)) (D4: g(1) follows from g(0) + g(1) = c_t),
+//    absorb, squeeze r_t (stored Montgomery at r_out, canonical at point_out); warp 0 only.
+//  iround_rescale: HI'_dst = HI'_src * beta(u_x[t], r_t); iround_claim: next claim g_t(r_t) by
+//    Lagrange interpolation through 0..3 (every thread calls both).
+struct IFinish {
+    uint8_t* st;
+    fr_t* claim;
+    uint8_t* msg_out;
+    fr_t* r_out;
+    uint8_t* point_out;
+    const fr_t* u[5];
+    fr_t* hi[6];       // source HI' tables of the round
+    fr_t* hi_dst[6];   // rescaled tables (== hi outside the persistent kernel)
+    uint32_t t, hb;
+};
+__device__ __noinline__ void iround_transcript(const IFinish a, const fr_t* g, fr_t* msg /* smem [4] */) {
+    __shared__ FsScratch fs;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (lane == 0) {
+            msg[0] = g[0];
+            msg[1] = fr_sub(fr_load_l2(a.claim), g[0]);
+            msg[2] = g[1];
+            msg[3] = g[2];
+        }
+        __syncwarp();
+        fs_begin(fs, a.st);
+        fs_absorb_frs(fs, "relu/msg", lane < 4 ? msg[lane & 3] : fr_zero(), 4, a.msg_out);
+        fr_t rt = fs_challenge(fs, "relu/x");
+        if (lane == 0) {
+            fr_store(a.r_out, rt);
+            fr_canon_to_bytes(fs.rc, a.point_out);
+        }
+        fs_end(fs, a.st);
+    }
+    __syncthreads();
+}
+__device__ __noinline__ void iround_rescale(const IFinish a) {
+    __shared__ fr_t eqr[6];
+    const int lane = threadIdx.x;
+    if (lane < 6) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur, one lane per HI table
+        const fr_t rt = fr_load_l2(a.r_out);
+        const fr_t* up = lane == 0 ? a.u[0] : lane == 1 ? a.u[1] : lane == 2 ? a.u[2] : lane == 3 ? a.u[3] : a.u[4];
+        fr_t u = fr_load(&up[a.t]);
+        fr_t ur = fr_mul_cold(u, rt);
+        eqr[lane] = fr_add(fr_sub(fr_sub(fr_one(), u), rt), fr_add(ur, ur));
+    }
+    __syncthreads();
+    const uint32_t nh = 1u << a.hb;
+    for (uint32_t e = threadIdx.x; e < 6 * nh; e += blockDim.x) {
+        uint32_t x = e / nh, hh = e % nh;
+        fr_store(&a.hi_dst[x][hh], fr_mul_cold(fr_load_l2(&a.hi[x][hh]), eqr[x]));
+    }
+}
+__device__ __noinline__ void iround_claim(const IFinish a, const fr_t* msg /* smem [4] */) {
+    __shared__ fr_t terms[4];
+    const int lane = threadIdx.x;
+    if (lane < 4) {   // Lagrange term i of g_t(r_t) through 0..3: e_i prod_{j != i}(r - j) / (i - j)
+        const fr_t rt = fr_load_l2(a.r_out);
+        const int i = lane;
+        fr_t num = msg[i];
+        for (int j = 0; j < 4; j++)
+            if (j != i) num = fr_mul_cold(num, fr_sub(rt, fr_from_u32((uint32_t)j)));
+        num = fr_mul_cold(num, (i == 0 || i == 3) ? ZK_INV6 : ZK_INV2);
+        terms[i] = (i == 0 || i == 2) ? fr_neg(num) : num;   // denominators -6, 2, -2, 6
+    }
+    __syncthreads();
+    if (lane == 0) fr_store(a.claim, fr_add(fr_add(terms[0], terms[1]), fr_add(terms[2], terms[3])));
+}
+__device__ __forceinline__ void iround_finish(const IFinish a, const fr_t* g) {
+    __shared__ fr_t msg[4];
+    iround_transcript(a, g, msg);
+    iround_rescale(a);
+    iround_claim(a, msg);
+}
+
+__device__ __forceinline__ IFinish ifinish_of(const IRoundArgs& a) {
+    IFinish f;
+    f.st = a.st;
+    f.claim = a.claim;
+    f.msg_out = a.msg_out;
+    f.r_out = a.r_out;
+    f.point_out = a.point_out;
+    for (int x = 0; x < 5; x++) f.u[x] = a.u[x];
+    for (int x = 0; x < 6; x++) f.hi[x] = f.hi_dst[x] = a.hi[x];
+    f.t = a.t;
+    f.hb = a.hb;
+    return f;
+}
+
 // Two threads per pair b: side s = 0 carries a0 with E_Z, E_A and the AIVP weight E_b; side s = 1
 // carries a1 with E_GA, E_GZ and E_b' = r' E_b (its own HI table, so no per-pair r' product).  Per side
 // and X in {0, 2, 3}: P_s(X) = a (E_a + E_c oms) + E_b a (a - 1); X = 1 follows from g(0) + g(1) = c_t.
+// (The pre-factoring round kernel, kept as the A/B reference: ZKDL_IROUND_V=0.)
 #define IR_MUL fr_mul_ni   // one out-of-line product body: the loop fits the instruction cache
 template <bool FOLD>
 __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
@@ -679,49 +773,383 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround(IRoundArgs a) {
         }
     }
     __shared__ fr_t tot[3];
-    __shared__ fr_t eqr[6];
-    __shared__ fr_t msg[4];
-    __shared__ fr_t terms[4];
-    __shared__ FsScratch fs;
-    if (grid_reduce_fr_block<3>(acc, a.partials, a.ticket, tot)) {
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            if (lane == 0) {
-                msg[0] = tot[0];
-                msg[1] = fr_sub(fr_load(a.claim), tot[0]);
-                msg[2] = tot[1];
-                msg[3] = tot[2];
-            }
-            __syncwarp();
-            fs_begin(fs, a.st);
-            fs_absorb_frs(fs, "relu/msg", lane < 4 ? msg[lane & 3] : fr_zero(), 4, a.msg_out);
-            fr_t rt = fs_challenge(fs, "relu/x");
-            if (lane == 0) {
-                fr_store(a.r_out, rt);
-                fr_canon_to_bytes(fs.rc, a.point_out);
-            }
-            if (lane < 6) {   // beta(u_x[t], r_t) = 1 - u - r + 2ur, one lane per HI table
-                const fr_t* up = lane == 0 ? a.u[0] : lane == 1 ? a.u[1] : lane == 2 ? a.u[2] : lane == 3 ? a.u[3] : a.u[4];
-                fr_t u = fr_load(&up[a.t]);
-                fr_t ur = fr_mul_cold(u, rt);
-                eqr[lane] = fr_add(fr_sub(fr_sub(fr_one(), u), rt), fr_add(ur, ur));
-            } else if (lane < 10) {   // Lagrange term i of g_t(r_t) through 0..3: e_i prod_{j != i}(r - j) / (i - j)
-                const int i = lane - 6;
-                fr_t num = msg[i];
-                for (int j = 0; j < 4; j++)
-                    if (j != i) num = fr_mul_cold(num, fr_sub(rt, fr_from_u32((uint32_t)j)));
-                num = fr_mul_cold(num, (i == 0 || i == 3) ? ZK_INV6 : ZK_INV2);
-                terms[i] = (i == 0 || i == 2) ? fr_neg(num) : num;   // denominators -6, 2, -2, 6
-            }
-            __syncwarp();
-            if (lane == 0) fr_store(a.claim, fr_add(fr_add(terms[0], terms[1]), fr_add(terms[2], terms[3])));
-            fs_end(fs, a.st);
+    if (grid_reduce_fr_block<3>(acc, a.partials, a.ticket, tot)) iround_finish(ifinish_of(a), tot);
+}
+
+// Factored i-round (default).  The current variable's eq factor is pulled out of every eq table:
+// E_x(2b + c) = beta(u_x[t], c) E'_x(b) with E'_x(b) = LO_x[2b] + LO_x[2b+1] (the next LO level, additions
+// only: beta(u, 0) + beta(u, 1) = 1) times HI'_x[h] (one value per CTA: every CTA works inside one HI
+// block).  Per side the round polynomial is then a sum of three terms, each a fixed linear factor
+// beta(u_x[t], X) times a per-pair polynomial that is accumulated on its own:
+//   T_a(X) = sum E'_a a(X)                      (linear: accumulated at X = 0, 1)
+//   T_c(X) = sum E'_c a(X) oms(X)               (quadratic: X = 0, 1, infinity)
+//   T_b(X) = sum E'_b a(X) (a(X) - 1)           (quadratic; both sides' T_b share beta(u_b[t], X))
+// with y = E' a formed at X = 0, 1 once (two products) and the quadratic's values at 0, 1, infinity as
+// three more (oms is a 0/1 integer in the first round: selects).  That is 15 Fr products per side and
+// pair in folding rounds (3 fold + 6 + 3 + 3) and 9 in the first (6 + 3), against 18 and 12 for the
+// unfactored form; HI', beta(u_x[t], X) and the cross-side sums are applied once per CTA / per round.
+// Values (13 Fr per CTA): Z: T_a side 0 [0..1]; A: T_c side 0 [2..4]; GA: T_a side 1 [5..6];
+// GZ: T_c side 1 [7..9]; b: T_b both sides [10..12].
+constexpr int IR_NV = 13;
+
+struct IPtrs {   // one side's view of a round (L2 loads: the persistent kernel re-reads buffers it wrote)
+    const fr_t* srcA;
+    const fr_t* srcO;
+    fr_t* dstA;
+    fr_t* dstO;
+    const fr_t* loA;
+    const fr_t* loC;
+    const fr_t* loB;
+    fr_t* nxA;
+    fr_t* nxC;
+    fr_t* nxB;   // null on side 1
+};
+
+// Accumulate this thread's pairs j = j0, j0 + js, ... < P_blk of HI block h into T[0..7] =
+// (T_a(0), T_a(1), T_c(0), T_c(1), T_c(inf), T_b(0), T_b(1), T_b(inf)) of its side.
+template <bool FOLD>
+__device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint32_t h, uint32_t pb, uint64_t j0,
+                                             uint64_t js, const int side, fr_t (&T)[8]) {
+    const fr_t one = fr_one();
+    const uint64_t P_blk = 1ull << pb;
+    for (uint64_t j = j0; j < P_blk; j += js) {
+        const uint64_t b = ((uint64_t)h << pb) + j;
+        fr_t a0, a1, om0, om1;
+        int o0 = 0, o1 = 0;
+        if (FOLD) {
+            const fr_t* s = q.srcA + 4 * b;
+            const fr_t y0 = fr_load_l2(s), y1 = fr_load_l2(s + 1), y2 = fr_load_l2(s + 2), y3 = fr_load_l2(s + 3);
+            // oms fold shared by the pair's two lanes: side s folds entry s and stores it
+            const fr_t* so = q.srcO + 4 * b + 2 * side;
+            const fr_t z0 = fr_load_l2(so), z1 = fr_load_l2(so + 1);
+            const fr3_t f = fr_mul3_ni(r, fr_sub(y1, y0), r, fr_sub(y3, y2), r, fr_sub(z1, z0));
+            a0 = fr_add(y0, f.x);
+            a1 = fr_add(y2, f.y);
+            const fr_t mine = fr_add(z0, f.z);
+            fr_store(q.dstA + 2 * b, a0);
+            fr_store(q.dstA + 2 * b + 1, a1);
+            fr_store(q.dstO + 2 * b + side, mine);
+            const fr_t other = fr_shfl_xor(mine, 1, __activemask());
+            om0 = side ? other : mine;
+            om1 = side ? mine : other;
+        } else {
+            a0 = fr_load_cg(q.srcA + 2 * b);
+            a1 = fr_load_cg(q.srcA + 2 * b + 1);
+            o0 = !fr_is_zero(fr_load_cg(q.srcO + 2 * b));
+            o1 = !fr_is_zero(fr_load_cg(q.srcO + 2 * b + 1));
         }
-        __syncthreads();
-        const uint32_t nh = 1u << a.hb;
-        for (uint32_t e = threadIdx.x; e < 6 * nh; e += blockDim.x) {
-            uint32_t x = e / nh, hh = e % nh;
-            fr_store(&a.hi[x][hh], fr_mul(fr_load(&a.hi[x][hh]), eqr[x]));
+        const fr_t eA = fr_add(fr_load_l2(&q.loA[2 * j]), fr_load_l2(&q.loA[2 * j + 1]));
+        const fr_t eC = fr_add(fr_load_l2(&q.loC[2 * j]), fr_load_l2(&q.loC[2 * j + 1]));
+        const fr_t eB = fr_add(fr_load_l2(&q.loB[2 * j]), fr_load_l2(&q.loB[2 * j + 1]));
+        if (h == 0) {   // the next LO level: side 0 writes Z, A, b; side 1 writes GA, GZ
+            fr_store(&q.nxA[j], eA);
+            fr_store(&q.nxC[j], eC);
+            if (q.nxB) fr_store(&q.nxB[j], eB);
+        }
+        const fr3_t p = fr_mul3_ni(eA, a0, eA, a1, eC, a0);
+        const fr3_t pq = fr_mul3_ni(eC, a1, eB, a0, eB, a1);
+        T[0] = fr_add(T[0], p.x);
+        T[1] = fr_add(T[1], p.y);
+        const fr_t yC0 = p.z, yC1 = pq.x, zB0 = pq.y, zB1 = pq.z;
+        if (FOLD) {
+            const fr3_t c = fr_mul3_ni(yC0, om0, yC1, om1, fr_sub(yC1, yC0), fr_sub(om1, om0));
+            T[2] = fr_add(T[2], c.x);
+            T[3] = fr_add(T[3], c.y);
+            T[4] = fr_add(T[4], c.z);
+        } else {   // oms(0), oms(1) in {0, 1}: T_c at infinity is (o1 - o0)(y1 - y0)
+            const fr_t yd = fr_sub(yC1, yC0);
+            const fr_t zero = fr_zero();
+            T[2] = fr_add(T[2], o0 ? yC0 : zero);
+            T[3] = fr_add(T[3], o1 ? yC1 : zero);
+            T[4] = fr_add(T[4], o1 == o0 ? zero : (o1 ? yd : fr_neg(yd)));
+        }
+        const fr3_t d = fr_mul3_ni(zB0, fr_sub(a0, one), zB1, fr_sub(a1, one), fr_sub(zB1, zB0), fr_sub(a1, a0));
+        T[5] = fr_add(T[5], d.x);
+        T[6] = fr_add(T[6], d.y);
+        T[7] = fr_add(T[7], d.z);
+    }
+}
+
+// T[] times this CTA's HI' values (kappa_x * prior betas; side 1's b table carries r'), then scattered
+// into the 13 reduction slots (zeros in the other side's slots).  Threads without pairs skip the products.
+__device__ __forceinline__ void iround_scale_scatter(fr_t (&T)[8], fr_t* const* hi, uint32_t h, int side, bool any,
+                                                     fr_t (&acc)[16]) {
+    if (any) {
+        const fr_t hA = fr_load_l2(&(side ? hi[2] : hi[0])[h]);
+        const fr_t hC = fr_load_l2(&(side ? hi[3] : hi[1])[h]);
+        const fr_t hB = fr_load_l2(&(side ? hi[5] : hi[4])[h]);
+        const fr3_t u = fr_mul3_ni(T[0], hA, T[1], hA, T[2], hC);
+        const fr3_t v = fr_mul3_ni(T[3], hC, T[4], hC, T[5], hB);
+        const fr3_t w = fr_mul3_ni(T[6], hB, T[7], hB, fr_zero(), fr_zero());
+        T[0] = u.x; T[1] = u.y; T[2] = u.z; T[3] = v.x; T[4] = v.y; T[5] = v.z; T[6] = w.x; T[7] = w.y;
+    }
+    const fr_t zero = fr_zero();
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        acc[k] = side ? zero : T[k];
+        acc[5 + k] = side ? T[k] : zero;
+    }
+    acc[10] = T[5];
+    acc[11] = T[6];
+    acc[12] = T[7];
+    acc[13] = acc[14] = acc[15] = zero;
+}
+
+// Transposed block reduction of 16 values per thread: each butterfly step of the warp halves the
+// values a lane keeps (16 Fr shuffles and 16 additions per lane instead of 16 x 5 of a per-value
+// tree), then warp 0 adds the 8 warps' rows.  On return lane k < 16 of warp 0 holds the total of
+// value k in v[0] (the other lanes hold partial sums).  Small code, short dependency chains: this
+// runs once per round on the critical path.
+__device__ __forceinline__ void warp_transpose_sum16(fr_t (&v)[16]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16, c = 8; o >= 2; o >>= 1, c >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < c; i++) {
+            fr_t send, keep;
+#pragma unroll
+            for (int l = 0; l < 8; l++) {
+                send.v[l] = up ? v[i].v[l] : v[i + c].v[l];
+                keep.v[l] = up ? v[i + c].v[l] : v[i].v[l];
+            }
+            v[i] = fr_add(keep, fr_shfl_xor(send, o));
+        }
+    }
+    v[0] = fr_add(v[0], fr_shfl_xor(v[0], 1));   // lane holds the warp total of value (lane >> 1) & 15
+}
+__device__ __forceinline__ void block_transpose_sum16(fr_t (&v)[16], fr_t* sm /* >= 8 * 16 */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    warp_transpose_sum16(v);
+    if (!(lane & 1)) sm[wid * 16 + (lane >> 1)] = v[0];
+    __syncthreads();
+    if (wid == 0 && lane < 16) {
+        fr_t x = sm[lane];
+        for (int w = 1; w < nw; w++) x = fr_add(x, sm[w * 16 + lane]);
+        v[0] = x;
+    }
+    __syncthreads();
+}
+
+// g(X) = sum_x beta(u_x[t], X) T_x(X) at X = 0, 2, 3 from the 13 round totals (lane 3x + k, X = {0,2,3}[k]);
+// called by every thread of the block, writes g[0..2].
+__device__ __noinline__ void iround_g(const fr_t* tot, const fr_t* const* u, uint32_t t, fr_t* prod, fr_t* g) {
+    const int lane = threadIdx.x;
+    const fr_t one = fr_one(), zero = fr_zero();
+    if (lane < 15) {
+        const int x = lane / 3, k = lane % 3;
+        const uint32_t X = k == 0 ? 0u : k + 1u;
+        const int base = x == 0 ? 0 : x == 1 ? 2 : x == 2 ? 5 : x == 3 ? 7 : 10;
+        const bool quad = x != 0 && x != 2;
+        const fr_t V0 = tot[base], V1 = tot[base + 1], Vi = quad ? tot[base + 2] : zero;
+        // T(X) = V0 + X (V1 - V0 - Vi) + X^2 Vi
+        const fr_t lin = fr_sub(fr_sub(V1, V0), Vi);
+        fr_t T = V0;
+        for (uint32_t i = 0; i < X; i++) T = fr_add(T, lin);
+        for (uint32_t i = 0; i < X * X; i++) T = fr_add(T, Vi);
+        // beta(u, X) = (1 - u) + X (2u - 1)
+        const fr_t uu = fr_load(&u[x][t]);
+        const fr_t slope = fr_sub(fr_add(uu, uu), one);
+        fr_t be = fr_sub(one, uu);
+        for (uint32_t i = 0; i < X; i++) be = fr_add(be, slope);
+        prod[lane] = fr_mul_cold(be, T);
+    }
+    __syncthreads();
+    if (lane < 3) {
+        fr_t sum = zero;
+        for (int x = 0; x < 5; x++) sum = fr_add(sum, prod[3 * x + lane]);
+        g[lane] = sum;
+    }
+    __syncthreads();
+}
+
+template <bool FOLD>
+__global__ void __launch_bounds__(256, 2) k_relu_iround_f(IRoundArgs a) {
+    const int side = threadIdx.x & 1;
+    const uint32_t pb = a.lo_cnt - 1;   // log2 of the pairs per HI block
+    const uint32_t h = blockIdx.x / a.cpb, cib = blockIdx.x % a.cpb;
+    IPtrs q;
+    q.srcA = side ? a.src[1] : a.src[0];
+    q.srcO = a.src[2];
+    q.dstA = side ? a.dst[1] : a.dst[0];
+    q.dstO = a.dst[2];
+    q.loA = side ? a.lo_cur[2] : a.lo_cur[0];
+    q.loC = side ? a.lo_cur[3] : a.lo_cur[1];
+    q.loB = a.lo_cur[4];
+    q.nxA = a.lo_next[side ? 2 : 0];
+    q.nxC = a.lo_next[side ? 3 : 1];
+    q.nxB = side ? nullptr : a.lo_next[4];
+    fr_t r;
+    if (FOLD) r = fr_load(a.r_prev);
+    fr_t T[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) T[k] = fr_zero();
+    const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
+    iround_pairs<FOLD>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+    fr_t v[16];
+    iround_scale_scatter(T, a.hi, h, side, j0 < (1ull << pb), v);
+    __shared__ fr_t sm[8 * 16];
+    __shared__ fr_t tot[16];
+    __shared__ fr_t prod[15];
+    __shared__ fr_t g[3];
+    __shared__ bool is_last;
+    block_transpose_sum16(v, sm);
+    if (threadIdx.x < IR_NV) fr_store(&a.partials[blockIdx.x * IR_NV + threadIdx.x], v[0]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    {   // thread i sums the partials of CTAs i, i + 256, ...
+        fr_t w[16];
+#pragma unroll
+        for (int k = 0; k < 16; k++) w[k] = fr_zero();
+        for (unsigned int bb = threadIdx.x; bb < gridDim.x; bb += blockDim.x)
+#pragma unroll
+            for (int k = 0; k < IR_NV; k++) w[k] = fr_add(w[k], fr_load_l2(&a.partials[bb * IR_NV + k]));
+        block_transpose_sum16(w, sm);
+        if (threadIdx.x < IR_NV) tot[threadIdx.x] = w[0];
+    }
+    if (threadIdx.x == 0) *a.ticket = 0;
+    __syncthreads();
+    iround_g(tot, a.u, a.t, prod, g);
+    iround_finish(ifinish_of(a), g);
+}
+
+// The small i-rounds t0 .. t1-1 in ONE cooperative launch (1 + 2^hb * cpb CTAs, at most one per SM):
+// per round the workers fold, accumulate, reduce and publish their 13 partials and bump a monotonic
+// arrival counter; block 0 (dedicated) sums them, forms g, runs the transcript step and releases the
+// next round through `flag` as soon as r_t exists; the claim update and the HI' rescale (into the other
+// HI' buffer) follow off the critical path and are released through `hiflag`, which the workers
+// only need after their pair loop.  Every buffer written inside the launch is read back through L2
+// (ld.cg): L1 is not coherent across SMs.  The code stays in the instruction cache across rounds.
+struct IPersistArgs {
+    const fr_t* full[3];    // sources of round 1 (round 0 does not fold)
+    fr_t* buf[2][3];        // round t folds into buf[t & 1]
+    fr_t* LO[5][2];         // round t reads LO[x][t & 1] and writes LO[x][(t & 1) ^ 1]
+    fr_t* hi[2][6];         // round t reads hi[(t - t0) & 1] and writes the rescaled tables to the other
+    const fr_t* u[5];
+    uint32_t t0, t1, H, hb, cpb;
+    fr_t* claim;
+    fr_t* r_i;              // r of i-round t at r_i[t]
+    uint8_t* msg_base;      // i-round t message at msg_base + 128 t
+    uint8_t* point_base;    // r_t canonical at point_base + 32 t
+    uint8_t* st;
+    fr_t* partials;         // (gridDim.x - 1) * 13
+    unsigned int* arrive;
+    unsigned int* flag;     // rounds whose r_t is published
+    unsigned int* hiflag;   // rounds whose HI' rescale is published
+    unsigned long long* trace;   // diagnostics (ZKDL_IPERSIST_TRACE): 4 timestamps per round, or null
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void wait_counter(const unsigned int* p, unsigned int target) {
+    if (threadIdx.x == 0) {
+        while (ld_volatile_u32(p) < target) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
+    __shared__ fr_t sm[8 * 16];
+    __shared__ fr_t tot[16];
+    __shared__ fr_t prod[15];
+    __shared__ fr_t g[3];
+    __shared__ fr_t msg[4];
+    const int side = threadIdx.x & 1;
+    const uint32_t nworkers = gridDim.x - 1;
+    for (uint32_t t = a.t0; t < a.t1; t++) {
+        const uint32_t pb = a.H - t - 1;
+        const int lv = t & 1, hv = (t - a.t0) & 1;
+        if (blockIdx.x != 0) {
+            if (t > a.t0) wait_counter(a.flag, t);   // r_{t-1}, the LO level and the folded tables
+            const uint32_t w = blockIdx.x - 1, h = w / a.cpb, cib = w % a.cpb;
+            IPtrs q;
+            const fr_t* const* src = t == 1 ? a.full : (const fr_t* const*)a.buf[(t - 1) & 1];
+            q.srcA = side ? src[1] : src[0];
+            q.srcO = src[2];
+            q.dstA = side ? a.buf[t & 1][1] : a.buf[t & 1][0];
+            q.dstO = a.buf[t & 1][2];
+            q.loA = side ? a.LO[2][lv] : a.LO[0][lv];
+            q.loC = side ? a.LO[3][lv] : a.LO[1][lv];
+            q.loB = a.LO[4][lv];
+            q.nxA = a.LO[side ? 2 : 0][lv ^ 1];
+            q.nxC = a.LO[side ? 3 : 1][lv ^ 1];
+            q.nxB = side ? nullptr : a.LO[4][lv ^ 1];
+            const fr_t r = fr_load_l2(&a.r_i[t - 1]);
+            fr_t T[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) T[k] = fr_zero();
+            const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
+            iround_pairs<true>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+            if (t > a.t0) wait_counter(a.hiflag, t);   // HI' rescaled by round t-1
+            fr_t v[16];
+            iround_scale_scatter(T, a.hi[hv], h, side, j0 < (1ull << pb), v);
+            block_transpose_sum16(v, sm);
+            if (threadIdx.x < IR_NV) fr_store(&a.partials[w * IR_NV + threadIdx.x], v[0]);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(a.arrive, 1u);
+            }
+        } else {
+            wait_counter(a.arrive, (t - a.t0 + 1) * nworkers);
+            if (a.trace && threadIdx.x == 0) a.trace[(t - a.t0) * 4 + 0] = globaltimer_ns();
+            {
+                fr_t v[16];
+#pragma unroll
+                for (int k = 0; k < 16; k++) v[k] = fr_zero();
+                for (unsigned int bb = threadIdx.x; bb < nworkers; bb += blockDim.x)
+#pragma unroll
+                    for (int k = 0; k < IR_NV; k++) v[k] = fr_add(v[k], fr_load_l2(&a.partials[bb * IR_NV + k]));
+                block_transpose_sum16(v, sm);
+                if (threadIdx.x < IR_NV) tot[threadIdx.x] = v[0];
+            }
+            __syncthreads();
+            if (a.trace && threadIdx.x == 0) a.trace[(t - a.t0) * 4 + 1] = globaltimer_ns();
+            iround_g(tot, a.u, t, prod, g);
+            IFinish f;
+            f.st = a.st;
+            f.claim = a.claim;
+            f.msg_out = a.msg_base + 128ull * t;
+            f.r_out = a.r_i + t;
+            f.point_out = a.point_base + 32ull * t;
+            for (int x = 0; x < 5; x++) f.u[x] = a.u[x];
+            for (int x = 0; x < 6; x++) {
+                f.hi[x] = a.hi[hv][x];
+                f.hi_dst[x] = a.hi[hv ^ 1][x];
+            }
+            f.t = t;
+            f.hb = a.hb;
+            iround_transcript(f, g, msg);
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicExch(a.flag, t + 1);
+                if (a.trace) a.trace[(t - a.t0) * 4 + 2] = globaltimer_ns();
+            }
+            iround_rescale(f);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicExch(a.hiflag, t + 1);
+                if (a.trace) a.trace[(t - a.t0) * 4 + 3] = globaltimer_ns();
+            }
+            iround_claim(f, msg);   // needed only by the next round's message
         }
     }
 }
@@ -963,11 +1391,22 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         buf[0][k] = s.alloc<fr_t>(D >= 4 ? D >> 2 : 1);
     }
     unsigned int max_grid = (unsigned int)ctx->num_sms * 4;
-    fr_t* partials = s.alloc<fr_t>((size_t)max_grid * 4);
+    fr_t* partials = s.alloc<fr_t>((size_t)max_grid * 13);
     unsigned int* ticket = s.alloc_zero<unsigned int>(1);
     const fr_t* cur[3] = {full[0], full[1], full[2]};
     int lo_level = 0;
-    for (uint32_t t = 0; t < H; t++) {
+    static const bool unfactored = getenv("ZKDL_IROUND_V") && atoi(getenv("ZKDL_IROUND_V")) == 0;   // A/B switch
+    // rounds with at most 2^plog pairs run in one persistent launch (k_relu_ipersist)
+    static const int plog = getenv("ZKDL_IPERSIST_LOG") ? atoi(getenv("ZKDL_IPERSIST_LOG")) : 16;
+    const uint32_t pcpb = (uint32_t)((ctx->num_sms - 1) >> hb);
+    uint32_t t0 = H;
+    if (!unfactored && pcpb >= 1 && plog >= 0)
+        for (uint32_t t = 1; t < H; t++)
+            if ((D >> (t + 1)) <= (1ull << plog)) {
+                t0 = t;
+                break;
+            }
+    for (uint32_t t = 0; t < t0; t++) {
         IRoundArgs a;
         memset(&a, 0, sizeof a);
         const bool fold = t > 0;
@@ -994,14 +1433,93 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         a.msg_out = proof + 140 + 128ull * (logB + t);
         a.r_out = r_all + logB + t;
         a.point_out = out.d_point + 32ull * (logB + t);
-        unsigned int grid = grid_for(ctx, 2 * a.n_pairs, 256, 2);   // two threads per pair
-        if (fold)
-            ZK_LAUNCH(ctx, k_relu_iround<true>, grid, 256, 0, a);
-        else
-            ZK_LAUNCH(ctx, k_relu_iround<false>, grid, 256, 0, a);
+        if (unfactored) {
+            const unsigned int grid = grid_for(ctx, 2 * a.n_pairs, 256, 2);   // two threads per pair
+            if (fold)
+                ZK_LAUNCH(ctx, k_relu_iround<true>, grid, 256, 0, a);
+            else
+                ZK_LAUNCH(ctx, k_relu_iround<false>, grid, 256, 0, a);
+        } else {
+            // grid = 2^hb HI blocks x cpb CTAs each, at most two CTAs per SM
+            const uint64_t per_blk = a.n_pairs >> hb;
+            uint64_t cpb = (per_blk + 127) / 128;
+            const uint64_t cap = ((uint64_t)ctx->num_sms * 2) >> hb;
+            if (cpb > cap) cpb = cap;
+            if (cpb < 1) cpb = 1;
+            a.cpb = (uint32_t)cpb;
+            const unsigned int grid = (unsigned int)(cpb << hb);
+            if (fold)
+                ZK_LAUNCH(ctx, k_relu_iround_f<true>, grid, 256, 0, a);
+            else
+                ZK_LAUNCH(ctx, k_relu_iround_f<false>, grid, 256, 0, a);
+        }
         lo_level ^= 1;
         if (fold)
             for (int k = 0; k < 3; k++) cur[k] = buf[t & 1][k];
+    }
+    if (t0 < H) {
+        IPersistArgs pa;
+        memset(&pa, 0, sizeof pa);
+        for (int k = 0; k < 3; k++) {
+            pa.full[k] = full[k];
+            pa.buf[0][k] = buf[0][k];
+            pa.buf[1][k] = buf[1][k];
+        }
+        for (int x = 0; x < 5; x++) {
+            pa.LO[x][0] = LOs[x][0];
+            pa.LO[x][1] = LOs[x][1];
+            pa.u[x] = u_i[x];
+        }
+        for (int x = 0; x < 6; x++) {
+            pa.hi[0][x] = HIs[x];
+            pa.hi[1][x] = s.alloc<fr_t>(1ull << hb);
+        }
+        pa.t0 = t0;
+        pa.t1 = H;
+        pa.H = H;
+        pa.hb = hb;
+        pa.cpb = pcpb;
+        pa.claim = kappa + 6;
+        pa.r_i = r_all + logB;
+        pa.msg_base = proof + 140 + 128ull * logB;
+        pa.point_base = out.d_point + 32ull * logB;
+        pa.st = tr->d_st;
+        const unsigned int grid = 1 + (pcpb << hb);
+        pa.partials = s.alloc<fr_t>((size_t)grid * IR_NV);
+        unsigned int* ctr = s.alloc_zero<unsigned int>(3);
+        pa.arrive = ctr;
+        pa.flag = ctr + 1;
+        pa.hiflag = ctr + 2;
+        static const bool trace = getenv("ZKDL_IPERSIST_TRACE") != nullptr;
+        if (trace) pa.trace = s.alloc_zero<unsigned long long>(4ull * (H - t0) + 1);
+        void* args[] = {(void*)&pa};
+        cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+        const bool prof = ctx->prof_match("k_relu_ipersist");
+        if (prof) {
+            ev_a = ctx->take_event();
+            ev_b = ctx->take_event();
+            cudaEventRecord(ev_a, ctx->stream);
+        }
+        ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_relu_ipersist, dim3(grid), dim3(256), args, 0, ctx->stream));
+        after_launch(ctx, "k_relu_ipersist");
+        if (prof) {
+            cudaEventRecord(ev_b, ctx->stream);
+            ctx->recs.push_back({"k_relu_ipersist", ev_a, ev_b});
+        }
+        for (int k = 0; k < 3; k++) cur[k] = buf[(H - 1) & 1][k];
+        if ((H - t0) & 1)   // the last persistent round rescaled HI' into the second buffer
+            for (int x = 0; x < 6; x++) HIs[x] = pa.hi[1][x];
+        if (trace) {
+            std::vector<unsigned long long> h(4ull * (H - t0));
+            ZK_CUDA(cudaMemcpyAsync(h.data(), pa.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+            for (uint32_t t = t0; t < H; t++) {
+                const unsigned long long* q = &h[4ull * (t - t0)];
+                const unsigned long long prev = t > t0 ? h[4ull * (t - t0) - 2] : q[0];
+                fprintf(stderr, "ipersist t=%u workers %.1f us, reduce %.1f, g+transcript %.1f, update %.1f\n", t,
+                        (q[0] - prev) / 1e3, (q[1] - q[0]) / 1e3, (q[2] - q[1]) / 1e3, (q[3] - q[2]) / 1e3);
+            }
+        }
     }
     ITailArgs ta;
     memset(&ta, 0, sizeof ta);

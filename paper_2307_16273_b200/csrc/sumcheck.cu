@@ -557,6 +557,8 @@ static unsigned int all_grid(zk_ctx* ctx, uint32_t m) {
     // grid that fills the GPU would crowd out the zkReLU kernels running on the other stream
     uint64_t cap = (uint64_t)per_sm * ctx->num_sms;
     if (cap > (uint64_t)ctx->num_sms) cap = (uint64_t)ctx->num_sms;
+    if (ctx->sm_budget > 0 && cap > (uint64_t)ctx->sm_budget) cap = (uint64_t)ctx->sm_budget;
+    if (cap < 2) cap = 2;   // one worker + the reducer block
     uint64_t need = ((1ull << (m - 1)) + 255) / 256 + 1;   // + the reducer block
     if (need < 2) need = 2;
     return (unsigned int)(need < cap ? need : cap);

@@ -74,8 +74,15 @@ def window_out_bytes(families: list) -> int:
     return sum(_slot(_layout(f)[1]) for f in families) + 256   # + the window transcript's final state
 
 
+def _family_work(f: DeviceFamily) -> int:
+    if f.kind == "matmul":
+        return f.A.numel() + f.B.numel()
+    return 64 * f.Z.numel()
+
+
 def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list, ready: list | None = None,
-                   relu_ctx: api.Context | None = None, proof_order: list | None = None):
+                   relu_ctx: api.Context | None = None, proof_order: list | None = None,
+                   mm_ctxs: list | None = None):
     """Enqueue one window's proofs without synchronising.
 
     Transcripts (D3d): the window transcript W absorbs "fcn/hdr", then per family "fcn/fam"
@@ -86,6 +93,9 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
     end of its host->device upload on a copy stream).  proof_order (optional): the order in which the
     families' proofs are enqueued (indices into `families`); forks and joins always follow the list
     order, so the transcripts and proof bytes do not depend on it.
+    mm_ctxs (optional): extra contexts (own streams, typically with an SM budget) over which the matmul
+    families are spread, largest first onto the least-loaded one, so their latency-bound sumchecks run
+    side by side; ctx keeps its share.
     Returns (out, flag, layout): `out` holds, per family, its proof output followed by the family
     transcript's final state, then W's final state; `flag` is the int32 range flag."""
     dev = (families[0].A if families[0].kind == "matmul" else families[0].Z).device
@@ -98,20 +108,30 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
     out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     two = relu_ctx is not None and relu_ctx.stream != ctx.stream
-    ctx_of = lambda f: relu_ctx if (two and f.kind == "relu") else ctx
+    lanes = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
+    home = {}
+    load = [0] * len(lanes)
+    for i in sorted(range(len(families)), key=lambda i: -_family_work(families[i])):
+        if families[i].kind == "matmul":
+            j = min(range(len(lanes)), key=lambda j: load[j])
+            home[i] = lanes[j]
+            load[j] += _family_work(families[i])
+    ctx_of_i = lambda i: relu_ctx if (two and families[i].kind == "relu") else home.get(i, ctx)
+    side = ([relu_ctx] if two else []) + lanes[1:]   # streams that fork from and join back into ctx
     W = api.Transcript(ctx, seed)
     W.absorb("fcn/hdr", header)
     kids = []
-    for f in families:
+    for i, f in enumerate(families):
         W.absorb("fcn/fam", f.name.encode())
-        kids.append(W.fork("fcn/fork", ctx_of(f)))
-    if two:
+        kids.append(W.fork("fcn/fork", ctx_of_i(i)))
+    if side:
         ev = torch.cuda.Event()
         ev.record(ctx.stream)
-        relu_ctx.stream.wait_event(ev)
+        for c in side:
+            c.stream.wait_event(ev)
     for i in (proof_order if proof_order is not None else range(len(lay))):
         f, info, o, n = lay[i]
-        c, T = ctx_of(f), kids[i]
+        c, T = ctx_of_i(i), kids[i]
         if ready is not None:
             c.stream.wait_event(ready[i])
         if f.kind == "matmul":
@@ -119,17 +139,18 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
         else:
             api.relu_prove_dev(c, T, f.Z, f.GA, f.Q, f.R, flag, out=out[o:o + n])
         T.state_dev(out[o + n:o + n + 32])
-    if two:
+    for c in side:
         ev = torch.cuda.Event()
-        ev.record(relu_ctx.stream)
+        ev.record(c.stream)
         ctx.stream.wait_event(ev)
     for T in kids:
         W.absorb_state("fcn/join", T)
     W.state_dev(out[off:off + 32])
-    if two:   # the children are freed on their own streams: after the joins
+    if side:   # the children are freed on their own streams: after the joins
         ev = torch.cuda.Event()
         ev.record(ctx.stream)
-        relu_ctx.stream.wait_event(ev)
+        for c in side:
+            c.stream.wait_event(ev)
     for T in kids:
         T.close()
     W.close()   # stream-ordered: the state buffers are released after the enqueued work
@@ -161,13 +182,13 @@ def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
 
 
 def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
-                 relu_ctx: api.Context | None = None) -> list:
+                 relu_ctx: api.Context | None = None, mm_ctxs: list | None = None) -> list:
     """Prove every family of one window (D3d transcripts); returns per-family results."""
-    return collect_window(*enqueue_window(ctx, seed, header, families, relu_ctx=relu_ctx))
+    return collect_window(*enqueue_window(ctx, seed, header, families, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs))
 
 
 def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None,
-                           relu_ctx: api.Context | None = None) -> list:
+                           relu_ctx: api.Context | None = None, mm_ctxs: list | None = None) -> list:
     """The user-facing end-to-end call: families given as host (ideally pinned) int32 tensors.
 
     Each family's stacks are copied host->device on `copy_stream` (one is created if None) and its
@@ -199,10 +220,14 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
             f = host_families[i]
             up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
             g = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
+            readers = [relu_ctx.stream] if (relu_ctx is not None and f.kind == "relu") else \
+                [ctx.stream] + [c.stream for c in (mm_ctxs or [])]
             for t in up.values():   # the proof reads it on its family's stream
-                t.record_stream(relu_ctx.stream if (relu_ctx is not None and f.kind == "relu") else ctx.stream)
+                for st in readers:
+                    t.record_stream(st)
             ev = torch.cuda.Event()
             ev.record(cs)
             fams[i] = g
             ready[i] = ev
-    return collect_window(*enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order))
+    return collect_window(*enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order,
+                                          mm_ctxs=mm_ctxs))

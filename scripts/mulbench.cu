@@ -123,11 +123,73 @@ __device__ __forceinline__ fr_t mul_u64p(const fr_t& a, const fr_t& b) {
     return fr_reduce_once(r);
 }
 
+// Variant E: a*b_i rows with 64-bit compiler carries (FMA + ALU pipes), reduction rows as PTX madc
+// chains (FMA pipe only) -- balances the two pipes.
+__device__ __forceinline__ fr_t mul_mix(const fr_t& a, const fr_t& b) {
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint64_t C = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            uint64_t uv = (uint64_t)a.v[j] * b.v[i] + t[j] + C;
+            t[j] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+        t[8] += (uint32_t)C;
+        ZK_REDC_ROW(t);
+    }
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = t[i];
+    return fr_reduce_once(r);
+}
+
+// Variant F: production product without the final conditional subtraction (output < 2p; valid as an
+// input to the next product because 4p < 2^256).
+__device__ __forceinline__ fr_t mul_lazy(const fr_t& a, const fr_t& b) {
+    const uint32_t p[8] = {ZK_P0, ZK_P1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7};
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint64_t C = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t uv = (uint64_t)a.v[j] * b.v[i] + t[j] + C;
+            t[j] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+        t[8] += (uint32_t)C;
+        const uint32_t m = t[0] * 0xffffffffu;
+        C = (uint64_t)(t[0] != 0);
+        {
+            const uint64_t uv = ((uint64_t)m << 32) + t[1] + C - m;
+            t[0] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+#pragma unroll
+        for (int j = 2; j < 8; j++) {
+            const uint64_t uv = (uint64_t)m * p[j] + t[j] + C;
+            t[j - 1] = (uint32_t)uv;
+            C = uv >> 32;
+        }
+        const uint64_t uv = (uint64_t)t[8] + C;
+        t[7] = (uint32_t)uv;
+        t[8] = (uint32_t)(uv >> 32);
+    }
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = t[i];
+    return r;
+}
+
 template <int V>
 __device__ __forceinline__ fr_t MUL(const fr_t& a, const fr_t& b) {
     if (V == 0) return fr_mul(a, b);
     if (V == 1) return mul_u64(a, b);
     if (V == 3) return mul_u64p(a, b);
+    if (V == 4) return mul_mix(a, b);
+    if (V == 5) return mul_lazy(a, b);
     return mul_sos(a, b);
 }
 
@@ -149,6 +211,7 @@ template <int V>
 __global__ void check(const fr_t* x, const fr_t* y, uint32_t n, int* bad) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         fr_t r0 = fr_mul(x[i], y[i]), r1 = MUL<V>(x[i], y[i]);
+        if (V == 5) r1 = fr_reduce_once(r1);
         if (!fr_equal(r0, r1)) atomicAdd(bad, 1);
     }
 }
@@ -189,9 +252,12 @@ static void run(const char* name, fr_t* d_seed, fr_t* d_out, int blocks, uint32_
     printf("{\"variant\": \"%s\", \"blocks\": %d, \"G_frmul_per_s\": %.2f, \"regs\": %d, \"mismatches\": %d}\n", name, blocks,
            muls / (best / 1e3) / 1e9, at.numRegs, hb);
     cudaFree(bad);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("cuda error %s\n", cudaGetErrorString(e)); exit(1); }
 }
 
 int main() {
+    setvbuf(stdout, nullptr, _IONBF, 0);
     // random canonical inputs (top limb < p7 keeps them < p) in Montgomery-agnostic form
     fr_t h[1024];
     for (int i = 0; i < 1024; i++) {
@@ -206,6 +272,9 @@ int main() {
     run<0>("ptx_cios", d_seed, d_out, blocks, 1000);
     run<1>("u64_cios", d_seed, d_out, blocks, 1000);
     run<3>("u64_cios_p01", d_seed, d_out, blocks, 1000);
+    run<4>("mix_u64_madc", d_seed, d_out, blocks, 1000);
+    run<5>("u64_p01_lazy", d_seed, d_out, blocks, 1000);
     for (int b = 148 * 2; b <= 148 * 16; b *= 2) run<3>("u64_cios_p01", d_seed, d_out, b, 1000);
+    for (int b = 148 * 2; b <= 148 * 16; b *= 2) run<4>("mix_u64_madc", d_seed, d_out, b, 1000);
     return 0;
 }
