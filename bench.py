@@ -473,7 +473,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")
-    ap.add_argument("--mm-streams", type=int, default=1,
+    ap.add_argument("--mm-streams", type=int, default=4,
                     help="streams (contexts) the matmul families are spread over, side by side")
     ap.add_argument("--prof", default="dominant", choices=["dominant", "inline", "separate"],
                     help="where per-kernel CUDA-event durations come from (see roofline.durations)")

@@ -1395,9 +1395,11 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     unsigned int* ticket = s.alloc_zero<unsigned int>(1);
     const fr_t* cur[3] = {full[0], full[1], full[2]};
     int lo_level = 0;
-    static const bool unfactored = getenv("ZKDL_IROUND_V") && atoi(getenv("ZKDL_IROUND_V")) == 0;   // A/B switch
-    // rounds with at most 2^plog pairs run in one persistent launch (k_relu_ipersist)
-    static const int plog = getenv("ZKDL_IPERSIST_LOG") ? atoi(getenv("ZKDL_IPERSIST_LOG")) : 16;
+    // A/B switches (read per call, so tests can cover every path in one process): ZKDL_IROUND_V=0 the
+    // unfactored round kernel; rounds with at most 2^ZKDL_IPERSIST_LOG pairs (default 16, < 0: none) run
+    // in one persistent launch (k_relu_ipersist)
+    const bool unfactored = getenv("ZKDL_IROUND_V") && atoi(getenv("ZKDL_IROUND_V")) == 0;
+    const int plog = getenv("ZKDL_IPERSIST_LOG") ? atoi(getenv("ZKDL_IPERSIST_LOG")) : 16;
     const uint32_t pcpb = (uint32_t)((ctx->num_sms - 1) >> hb);
     uint32_t t0 = H;
     if (!unfactored && pcpb >= 1 && plog >= 0)

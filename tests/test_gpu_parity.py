@@ -238,6 +238,23 @@ def test_relu_range_error(ctx):
         api.relu_prove(ctx, api.Transcript(ctx, bytes(32)), dev(Z), dev(np.zeros(16, np.int32)), 4, 2)
 
 
+@pytest.mark.parametrize("env", [{"ZKDL_IPERSIST_LOG": "-1"}, {"ZKDL_IPERSIST_LOG": "5"}, {"ZKDL_IPERSIST_LOG": "30"},
+                                 {"ZKDL_IROUND_V": "0"}])
+@pytest.mark.parametrize("logD", [12, 17])
+def test_relu_round_paths_vs_oracle(ctx, O, logD, env, monkeypatch):
+    """Every i-round path gives the oracle's transcript: per-round factored launches only, a switch to
+    the persistent kernel mid-way, persistent from round 1, and the unfactored A/B kernel."""
+    from paper_2307_16273_b200 import api
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    Z = uniform_range(11, 3 * logD, (1 << logD,), -(1 << 31), 1 << 31)
+    GA = uniform_range(11, 3 * logD + 1, (1 << logD,), -(1 << 31), 1 << 31)
+    seed = fs_seed(f"relu-paths-{logD}")
+    o = O.relu_prove(O.Transcript(seed), Z, GA, 16, 16)
+    g = api.relu_prove(ctx, api.Transcript(ctx, seed), dev(Z), dev(GA), 16, 16)
+    assert g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
+
+
 def test_c2_full_vs_oracle(ctx, O):
     """C2 (BASELINE configs[1]) at full size: 64 x 1024 entries, Q = R = 16, bit-exact against the dense oracle."""
     from oracle import drivers
@@ -293,6 +310,16 @@ def test_fcn_tiny_vs_oracle(ctx, O):
     assert h[-1]["window_state"] == g[-1]["window_state"]
     g2 = dfcn.prove_window(ctx, fs_seed("tiny"), fcn.fcn_header(shape), dfcn.upload_families(fams), relu_ctx=relu_ctx)
     assert [r["proof"] for r in g2] == [r["proof"] for r in g] and g2[-1]["window_state"] == g[-1]["window_state"]
+    # matmul families spread over three more streams with SM budgets (bench --mm-streams): same bytes
+    mm = [api.Context(0, torch.cuda.Stream()) for _ in range(3)]
+    for c in [ctx] + mm:
+        c.set_sm_budget(37)
+    g3 = dfcn.prove_window(ctx, fs_seed("tiny"), fcn.fcn_header(shape), dfcn.upload_families(fams), relu_ctx=relu_ctx,
+                           mm_ctxs=mm)
+    ctx.set_sm_budget(0)
+    assert [r["proof"] for r in g3] == [r["proof"] for r in g] and g3[-1]["window_state"] == g[-1]["window_state"]
+    h3 = dfcn.prove_window_from_host(ctx, fs_seed("tiny"), fcn.fcn_header(shape), host, relu_ctx=relu_ctx, mm_ctxs=mm)
+    assert [r["proof"] for r in h3] == [r["proof"] for r in g]
 
 
 def test_async_provers_match_sync(ctx):
