@@ -207,7 +207,7 @@ def by_kernel(prof: dict) -> dict:
     """Merge template instantiations: {"k<true>": (n, ms), "k<false>": ...} -> {"k": (n, ms)}."""
     out = {}
     for k, (n, t) in prof.items():
-        b = k.split("<")[0]
+        b = k.lstrip("(").split("<")[0]
         n0, t0 = out.get(b, (0, 0.0))
         out[b] = (n0 + n, t0 + t)
     return out
@@ -384,8 +384,132 @@ def run_ours(args, rank, world, local):
         "clocks": clk,
         "paper_context": {"value": 0.84, "unit": "s/update", "hardware": "A100", "note": "PT/step at T'=16, BS 64 (PAPER.md L405); includes commitments, not this metric"},
     }
+    if not args.no_c5 and not args.profile_mode:
+        # BASELINE configs[4] alongside: one 2^26 sumcheck sharded over the same ranks (strong scaling)
+        with torch.cuda.stream(stream):
+            c5 = c5_measure(ctx, rank, world, 26, 3, 1)
+        peak = 148 * IMAD_LANES_PER_SM_CLK * clock_mhz * 1e6 / IMAD_PER_FRMUL / 1e9
+        out["c5_sharded"] = {"m": 26, "G": world, "ms_per_proof": c5["ms"], "frmul_per_s": c5["frmul_per_s"],
+                             "frac_of_frmul_peak": round(c5["frmul_per_s"] / 1e9 / peak, 4), "scaling": "strong",
+                             "proof_digest": c5["digest"], "note": "whole-proof rate incl. transcript steps and "
+                             "(G > 1) NCCL all-gathers; bench.py --config C5 gives the kernel table"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_mode:
         out["cpu_baseline"] = cpu_baseline(fams, shape, sample_scale=args.cpu_sample)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- C5: one (sharded) 2^m product sumcheck
+def c5_frmul_model(m: int, tail_log: int = 16, hb: int = 5) -> dict:
+    """Algorithmic Fr-mul count of one C5 proof (K = 2, n_eq = m) by kernel, mirroring
+    sumcheck.cu: round 0 (k_sc_round2f from int32): per pair 4 embeddings (half a product each) + E'
+    times A at X = 0, 1 (2) + 3 products = 7; folding rounds: fold 4 + 2 + 3 = 9 (plus one HI product per
+    pair where the groups are too small, "flat"); the last rounds (<= 2^tail_log entries after the
+    fold) in k_sc_all: fold 4 + eq 1 + 3 x 2 = 11 per pair (7 in the last, eq-free round)."""
+    out = {"k_sc_round2f": 0, "k_sc_all": 0}
+    for t in range(m):
+        pairs = 1 << (m - t - 1)
+        if t >= 1 and m - t <= tail_log:
+            has_e = 1 if t + 1 < m else 0
+            out["k_sc_all"] += pairs * (4 + has_e + 3 * (1 + has_e))
+            continue
+        nv = m - t - 1                      # eq variables of the pair index
+        hbe = min(m - 1, hb)
+        flat = nv > hbe and nv - hbe < 10    # LO x HI with groups < 1024 pairs: per-pair HI product
+        per = 7 if t == 0 else 9
+        out["k_sc_round2f"] += pairs * (per + (1 if flat else 0))
+    out["total"] = out["k_sc_round2f"] + out["k_sc_all"]
+    return out
+
+
+def c5_measure(ctx, rank: int, world: int, m: int, steps: int, warmup: int, switch_log: int = 12) -> dict:
+    """Time the C5 statement sum_x eq(w, x) A(x) B(x) over 2^m entries (D3c: "c5/hdr", w drawn from the
+    transcript, claim computed in round 0), sharded over the `world` ranks on its last-bound variables
+    (D19; G = 1: the single-device prover).  Inputs: int32 slices generated on the device, resident
+    before the timed region; every step proves from a fresh transcript."""
+    import torch
+    from paper_2307_16273_b200 import api, shard
+    from synth.prng import DATA_SEED, fs_seed, uniform_range_torch
+    dev = torch.device("cuda", ctx.device)
+    s = world.bit_length() - 1
+    n_loc = 1 << (m - s)
+    A = uniform_range_torch(DATA_SEED, 21, n_loc, -(1 << 15), 1 << 15, dev, offset=rank * n_loc)
+    B = uniform_range_torch(DATA_SEED, 22, n_loc, -(1 << 15), 1 << 15, dev, offset=rank * n_loc)
+    comm = shard.TorchComm() if world > 1 else None
+    torch.cuda.synchronize()
+
+    def one():
+        tr = api.Transcript(ctx, fs_seed(f"C5-m{m}"))
+        tr.absorb("c5/hdr", m.to_bytes(4, "little"))
+        w = tr.challenges("c5/w", m)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        if world == 1:
+            res = api.sumcheck_prove(ctx, tr, m, m, [A, B], w)
+        else:
+            sess = shard.ShardSession(ctx, tr, m, m, [A, B], w, rank, world)
+            res = shard.prove(sess, comm, switch_log=switch_log)
+            sess.close()
+        e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        tr.close()
+        return e0.elapsed_time(e1), res
+
+    for _ in range(warmup):
+        one()
+    times = []
+    res = None
+    for _ in range(steps):
+        ms, res = one()
+        times.append(max_over_ranks(ms, world))
+    ms = statistics.median(times)
+    model = c5_frmul_model(m)
+    frmul = model["total"]
+    return {"m": m, "G": world, "ms": round(ms, 4), "ms_min": round(min(times), 4), "frmul": frmul, "model": model,
+            "frmul_per_s": frmul / (ms / 1000.0), "digest": __import__("hashlib").sha256(res["proof"]).hexdigest()[:16]}
+
+
+def run_c5(args, rank, world, local):
+    """--config C5: the sharded single sumcheck (BASELINE configs[4]), strong scaling."""
+    import torch
+    from paper_2307_16273_b200 import api, build
+    build.build(verbose=False)
+    stream = torch.cuda.Stream(device=local)
+    ctx = api.Context(local, stream)
+    with torch.cuda.stream(stream):
+        clocks = Clocks(local)
+        clocks.start()
+        r = c5_measure(ctx, rank, world, args.m, args.steps, args.warmup)
+        clk = clocks.stop()
+        prof = {}
+        if world == 1:   # per-kernel table of one more proof (every launch bracketed)
+            ctx.profile(True)
+            ctx.profile_read()
+            c5_measure(ctx, rank, world, args.m, 1, 0)
+            prof = by_kernel(ctx.profile_read())
+            ctx.profile(False)
+    clock_mhz = clk.get("sm_max_mhz") or 1965.0
+    peak = 148 * IMAD_LANES_PER_SM_CLK * clock_mhz * 1e6 / IMAD_PER_FRMUL / 1e9
+    rf = None
+    if prof:
+        n, kms = prof.get("k_sc_round2f", (0, 0.0))
+        if kms > 0:
+            ach = r["model"]["k_sc_round2f"] / (kms / 1000.0) / 1e9
+            rf = {"bound": "alu", "kernel": "k_sc_round2f", "achieved": round(ach, 3), "peak": round(peak, 3),
+                  "unit": "GFr-mul/s", "frac": round(ach / peak, 4), "traffic": None, "launches_per_proof": n,
+                  "ms_per_proof": round(kms, 4), "share_of_step": round(kms / r["ms"], 4),
+                  "durations": "CUDA events around every launch of one more proof after the timed region"}
+    out = {"metric": f"C5 sharded sumcheck: prover s per 2^{args.m} product sumcheck (K=2, eq over all variables)",
+           "value": r["ms"] / 1000.0, "unit": "s/proof", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": r["ms"], "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+           "dtype": "fr_bls12_381 (8x32-bit Montgomery)", "data": "synthetic (A, B ~ U[-2^15, 2^15) int32, counter PRNG)",
+           "config": {"workload": f"C5: sum_x eq(w,x) A(x) B(x), 2^{args.m} entries, sharded on the last-bound variables over G={world}",
+                      "m": args.m, "parallelism": f"shard x{world}", "l2": "inputs larger than L2" if args.m >= 24 else "inputs fit L2"},
+           "frmul_per_s": r["frmul_per_s"], "frmul_per_proof": r["frmul"], "proof_digest": r["digest"],
+           "roofline": rf, "kernels_ms_per_step": {k: round(t, 4) for k, (n, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])[:12]},
+           "clocks": clk}
     if rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -469,7 +593,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C4", choices=["C4"])
+    ap.add_argument("--config", default="C4", choices=["C4", "C5"])
+    ap.add_argument("--m", type=int, default=26, help="C5: log2 of the hypercube (22..30)")
+    ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")
@@ -485,7 +611,10 @@ def main():
         run_reference(args, rank, 1, 0)
         return
     rank, world, local = dist_setup(args.gpus)
-    run_ours(args, rank, world, local)
+    if args.config == "C5":
+        run_c5(args, rank, world, local)
+    else:
+        run_ours(args, rank, world, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

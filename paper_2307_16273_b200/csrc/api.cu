@@ -338,10 +338,9 @@ zk_status zk_sumcheck_prove(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt* 
     S.K = K;
     const uint64_t N = 1ull << m;
     for (uint32_t k = 0; k < K; k++) {
-        if (st->i32_mask & (1u << k)) {
-            fr_t* t = s.alloc<fr_t>(N);
-            embed_i32_dev(ctx, static_cast<const int32_t*>(d_tables[k]), N, t);
-            S.tables[k] = t;
+        if (st->i32_mask & (1u << k)) {   // embedded by the prover (fused into round 0 where it can)
+            S.tables[k] = s.alloc<fr_t>(N);
+            S.i32[k] = static_cast<const int32_t*>(d_tables[k]);
         } else {
             S.tables[k] = static_cast<const fr_t*>(d_tables[k]);
         }

@@ -112,12 +112,12 @@ zk_status zk_sc_shard_create(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt*
         e.d_point = s.alloc<uint8_t>(32ull * m);
         e.d_finals = s.alloc<fr_t>(K);
         const fr_t* tabs[3] = {nullptr, nullptr, nullptr};
+        const int32_t* i32[3] = {nullptr, nullptr, nullptr};
         for (uint32_t k = 0; k < K; k++) {
             ZK_REQUIRE(d_local_tables[k], ZK_ERR_ARG, "null table");
-            if (st->i32_mask & (1u << k)) {
-                fr_t* t = s.alloc<fr_t>(1ull << L);
-                embed_i32_dev(ctx, static_cast<const int32_t*>(d_local_tables[k]), 1ull << L, t);
-                tabs[k] = t;
+            if (st->i32_mask & (1u << k)) {   // embedded by round 0 (ScEngine::set_i32)
+                tabs[k] = s.alloc<fr_t>(1ull << L);
+                i32[k] = static_cast<const int32_t*>(d_local_tables[k]);
             } else {
                 tabs[k] = static_cast<const fr_t*>(d_local_tables[k]);
             }
@@ -133,6 +133,7 @@ zk_status zk_sc_shard_create(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt*
         }
         e.header();
         e.setup(tabs, L, 0, n_eq < L ? n_eq : L);
+        e.set_i32(i32);
     } catch (const ZkError& err) {
         ctx->err = err.msg;
         delete sh->s;
@@ -192,8 +193,7 @@ zk_status zk_sc_shard_adopt(zk_sc_shard* sh, const void* d_full) {
     }
     e.d_scale = nullptr;
     e.setup(tabs, Lf, ta, e.n_eq > ta ? e.n_eq - ta : 0);
-    while (e.t < e.m) e.round(nullptr);
-    e.finals();
+    e.run_to_end();
     sh->done = true;
     SH_END
 }

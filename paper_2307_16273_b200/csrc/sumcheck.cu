@@ -48,6 +48,46 @@ struct ScRoundArgs {
     const fr_t* scale;       // sharded mode: the rank's eq factor over its high bits (nullptr = 1)
 };
 
+// Finalizer of a product-sumcheck round (last block, warp 0): the claim of round 0 (when computed),
+// the message, the transcript step; in sharded mode the rank's (scaled) totals instead.
+__device__ __noinline__ void sc_finish(const ScRoundArgs& a, const fr_t* tot, const int K) {
+    __shared__ FsScratch fs;
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    if (a.part_out) {
+        if (lane <= K) {
+            fr_t v = tot[lane & 3];
+            if (a.scale) v = fr_mul_cold(v, fr_load(a.scale));
+            fr_store(&a.part_out[lane], v);
+        }
+        return;
+    }
+    fs_begin(fs, a.st);
+    if (a.compute_claim) {
+        __shared__ fr_t claim_sm;
+        if (lane == 0) {
+            fr_t c;
+            if (a.t < a.n_eq) {
+                fr_t w0 = fr_load(&a.w[a.t]);
+                c = fr_add(fr_mul_cold(fr_sub(fr_one(), w0), tot[0]), fr_mul_cold(w0, tot[1]));
+            } else {
+                c = fr_add(tot[0], tot[1]);
+            }
+            fr_store(a.claim, c);
+            claim_sm = c;
+        }
+        __syncwarp();
+        fs_absorb_frs(fs, "sc/claim", claim_sm, 1, a.claim_bytes);
+    }
+    fs_absorb_frs(fs, "sc/msg", lane <= K ? tot[lane & 3] : fr_zero(), K + 1, a.msg_out);
+    fr_t rt = fs_challenge(fs, "sc/r");
+    if (lane == 0) {
+        fr_store(a.r_out, rt);
+        fr_canon_to_bytes(fs.rc, a.point_out);
+    }
+    fs_end(fs, a.st);
+}
+
 template <int K, bool FOLD>
 __global__ void __launch_bounds__(256) k_sc_round(ScRoundArgs a) {
     fr_t acc[K + 1];
@@ -104,41 +144,151 @@ __global__ void __launch_bounds__(256) k_sc_round(ScRoundArgs a) {
         }
     }
     __shared__ fr_t tot[K + 1];
-    __shared__ FsScratch fs;
-    if (grid_reduce_fr_block<K + 1>(acc, a.partials, a.ticket, tot) && threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        if (a.part_out) {
-            if (lane <= K) {
-                fr_t v = tot[lane & 3];
-                if (a.scale) v = fr_mul_cold(v, fr_load(a.scale));
-                fr_store(&a.part_out[lane], v);
+    if (grid_reduce_fr_block<K + 1>(acc, a.partials, a.ticket, tot)) sc_finish(a, tot, K);
+}
+
+// Factored K = 2 round (the large statements: C5, the sharded prover).  Pairs are grouped by their
+// HI index (b >> lo_cnt): inside a group the suffix eq weight is E'(b) = LO[b mod 2^lo_cnt] * HI[group],
+// so a CTA accumulates LO-weighted sums over a slice of one group and multiplies its three totals by
+// HI[group] once (no per-pair eq product).  Per pair: y = E' A at X = 0, 1 (two products), then
+// P(0) = y0 B0, P(1) = y1 B1, P(inf) = (y1 - y0)(B1 - B0) (three products); the message evaluations are
+// f(0) = P(0), f(1) = P(1), f(2) = 2 P(1) + 2 P(inf) - P(0).  With the fold (4 products) that is 9 Fr
+// products per pair against 11 (no eq: 4 + 3 against 4 + 3).  MODE 0: round 0 from Fr tables; 1: fold
+// rounds; 2: round 0 from int32 tables, embedded on the fly (a product with a one-limb operand, half a
+// full product) and written out for round 1 — no separate embedding pass.
+struct fr4_t { fr_t a, b, c, d; };
+// four int32 -> Montgomery embeddings (each a product with a one-limb operand: half a full product)
+static __device__ __noinline__ fr4_t fr_embed4_ni(int32_t x, int32_t y, int32_t z, int32_t w) {
+    return fr4_t{fr_from_i32(x), fr_from_i32(y), fr_from_i32(z), fr_from_i32(w)};
+}
+
+struct Sc2Args {
+    ScRoundArgs r;            // tables, eq (LO = eq_cur, HI = eq_hi or null), reduction, finalize
+    const int32_t* i32[2];    // MODE 2 sources
+    fr_t* emb[2];             // MODE 2: embedded tables written here
+    uint32_t slices;          // CTAs per group when there are fewer groups than CTAs
+    int flat;                 // groups too small for a CTA: every pair applies its HI value itself
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
+    const ScRoundArgs& a = A.r;
+    constexpr bool FOLD = MODE == 1;
+    const bool has_e = a.eq_mode != 0;
+    const uint32_t lo_cnt = has_e ? a.lo_cnt : 0;
+    // pairs per group (log2): the LO range; without eq weights the whole round is one group
+    const uint32_t gsize_log = has_e ? lo_cnt : 63 - __clzll(a.n_pairs);
+    const uint64_t ngroups = a.n_pairs >> gsize_log ? a.n_pairs >> gsize_log : 1;
+    uint64_t gsize = a.n_pairs < (1ull << gsize_log) ? a.n_pairs : (1ull << gsize_log);
+    if (A.flat) gsize = a.n_pairs;   // one group; E' = LO[b mod 2^lo_cnt] * HI[b >> lo_cnt] per pair
+    const uint64_t slices = A.slices;
+    const uint64_t slice_len = (gsize + slices - 1) / slices;
+    const uint64_t next_count = lo_cnt ? (1ull << (lo_cnt - 1)) : 0;
+    const uint64_t hi_mask = (1ull << a.hb) - 1;
+    fr_t r;
+    if (FOLD) r = fr_load(a.r_prev);
+    fr_t tot0 = fr_zero(), tot1 = fr_zero(), toti = fr_zero();
+    const uint64_t nitems = (A.flat ? 1 : ngroups) * slices;
+    const uint64_t lo_mask = (1ull << lo_cnt) - 1;
+    for (uint64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const uint64_t g = item / slices, sl = item % slices;
+        const uint64_t j_end = (sl + 1) * slice_len < gsize ? (sl + 1) * slice_len : gsize;
+        fr_t s0 = fr_zero(), s1 = fr_zero(), si = fr_zero();
+        bool any = false;
+        for (uint64_t j = sl * slice_len + threadIdx.x; j < j_end; j += blockDim.x) {
+            any = true;
+            const uint64_t b = A.flat ? j : (g << gsize_log) + j;
+            // products in three-wide out-of-line groups (three independent CIOS chains per call, one
+            // ~24 KB body shared by every call site: the inlined 9-product loop missed the I-cache)
+            fr_t a0, a1, b0, b1, e;
+            const fr_t zero = fr_zero();
+            if (has_e) {
+                e = fr_load(&a.eq_cur[b & lo_mask]);
+                if (b < next_count)
+                    fr_store(&a.eq_next[b], fr_add(fr_load(&a.eq_cur[2 * b]), fr_load(&a.eq_cur[2 * b + 1])));
             }
-            return;
-        }
-        fs_begin(fs, a.st);
-        if (a.compute_claim) {
-            __shared__ fr_t claim_sm;
-            if (lane == 0) {
-                fr_t c;
-                if (a.t < a.n_eq) {
-                    fr_t w0 = fr_load(&a.w[a.t]);
-                    c = fr_add(fr_mul(fr_sub(fr_one(), w0), tot[0]), fr_mul(w0, tot[1]));
+            fr3_t q;   // second group: (r db, E' a0, E' a1) in folding rounds with eq weights
+            bool q_done = false;
+            if (FOLD) {
+                const fr_t* sa = a.src[0] + 4 * b;
+                const fr_t* sb = a.src[1] + 4 * b;
+                const fr_t x0 = fr_load_cg(sa), x1 = fr_load_cg(sa + 1), x2 = fr_load_cg(sa + 2), x3 = fr_load_cg(sa + 3);
+                const fr_t z0 = fr_load_cg(sb), z1 = fr_load_cg(sb + 1), z2 = fr_load_cg(sb + 2), z3 = fr_load_cg(sb + 3);
+                const fr3_t f = fr_mul3_ni(r, fr_sub(x1, x0), r, fr_sub(x3, x2), r, fr_sub(z1, z0));
+                a0 = fr_add(x0, f.x);
+                a1 = fr_add(x2, f.y);
+                b0 = fr_add(z0, f.z);
+                if (has_e && !(A.flat && a.eq_hi)) {
+                    q = fr_mul3_ni(r, fr_sub(z3, z2), e, a0, e, a1);
+                    b1 = fr_add(z2, q.x);
+                    q_done = true;
                 } else {
-                    c = fr_add(tot[0], tot[1]);
+                    const fr_t hh = (has_e && A.flat && a.eq_hi) ? fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]) : zero;
+                    const fr3_t g2 = fr_mul3_ni(r, fr_sub(z3, z2), e, hh, zero, zero);
+                    b1 = fr_add(z2, g2.x);
+                    if (has_e) e = g2.y;
                 }
-                fr_store(a.claim, c);
-                claim_sm = c;
+                fr_store(a.dst[0] + 2 * b, a0);
+                fr_store(a.dst[0] + 2 * b + 1, a1);
+                fr_store(a.dst[1] + 2 * b, b0);
+                fr_store(a.dst[1] + 2 * b + 1, b1);
+            } else {
+                if (MODE == 2) {
+                    const int2 ia = __ldcs(reinterpret_cast<const int2*>(A.i32[0]) + b);
+                    const int2 ib = __ldcs(reinterpret_cast<const int2*>(A.i32[1]) + b);
+                    const fr4_t em = fr_embed4_ni(ia.x, ia.y, ib.x, ib.y);
+                    a0 = em.a;
+                    a1 = em.b;
+                    b0 = em.c;
+                    b1 = em.d;
+                    fr_store(A.emb[0] + 2 * b, a0);
+                    fr_store(A.emb[0] + 2 * b + 1, a1);
+                    fr_store(A.emb[1] + 2 * b, b0);
+                    fr_store(A.emb[1] + 2 * b + 1, b1);
+                } else {
+                    a0 = fr_load_cg(a.src[0] + 2 * b);
+                    a1 = fr_load_cg(a.src[0] + 2 * b + 1);
+                    b0 = fr_load_cg(a.src[1] + 2 * b);
+                    b1 = fr_load_cg(a.src[1] + 2 * b + 1);
+                }
+                if (has_e && A.flat && a.eq_hi) e = fr_mul_ni(e, fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]));
             }
-            __syncwarp();
-            fs_absorb_frs(fs, "sc/claim", claim_sm, 1, a.claim_bytes);
+            fr_t y0 = a0, y1 = a1;
+            if (has_e) {
+                if (!q_done) q = fr_mul3_ni(e, a0, e, a1, zero, zero);
+                y0 = q.y;
+                y1 = q.z;
+                if (!q_done) {
+                    y0 = q.x;
+                    y1 = q.y;
+                }
+            }
+            const fr3_t p = fr_mul3_ni(y0, b0, y1, b1, fr_sub(y1, y0), fr_sub(b1, b0));
+            s0 = fr_add(s0, p.x);
+            s1 = fr_add(s1, p.y);
+            si = fr_add(si, p.z);
         }
-        fs_absorb_frs(fs, "sc/msg", lane <= K ? tot[lane < K + 1 ? lane : 0] : fr_zero(), K + 1, a.msg_out);
-        fr_t rt = fs_challenge(fs, "sc/r");
-        if (lane == 0) {
-            fr_store(a.r_out, rt);
-            fr_canon_to_bytes(fs.rc, a.point_out);
+        if (any && has_e && a.eq_hi && !A.flat) {   // this group's HI factor, once per CTA and group
+            const fr_t h = fr_load(&a.eq_hi[g & hi_mask]);
+            s0 = fr_mul_ni(s0, h);
+            s1 = fr_mul_ni(s1, h);
+            si = fr_mul_ni(si, h);
         }
-        fs_end(fs, a.st);
+        tot0 = fr_add(tot0, s0);
+        tot1 = fr_add(tot1, s1);
+        toti = fr_add(toti, si);
+    }
+    fr_t acc[3] = {tot0, tot1, toti};
+    __shared__ fr_t tt[3];
+    __shared__ fr_t msg[3];
+    if (grid_reduce_fr_block<3>(acc, a.partials, a.ticket, tt)) {
+        if (threadIdx.x == 0) {   // evaluations at X = 0, 1, 2 of the quadratic with P(0), P(1), P(inf)
+            msg[0] = tt[0];
+            msg[1] = tt[1];
+            msg[2] = fr_sub(fr_dbl(fr_add(tt[1], tt[2])), tt[0]);
+        }
+        __syncthreads();
+        sc_finish(a, msg, 2);
     }
 }
 
@@ -222,6 +372,8 @@ static void launch_round(zk_ctx* ctx, bool fold, unsigned int grid, const ScRoun
 
 // ---------------------------------------------------------------- engine
 void ScEngine::setup(const fr_t* const tables[3], uint32_t L_, uint32_t t0_, uint32_t n_eq_loc_) {
+    factored = !(getenv("ZKDL_SC_V") && atoi(getenv("ZKDL_SC_V")) == 0);
+    for (int k = 0; k < 3; k++) i32[k] = nullptr;   // set_i32 after setup (a continuation has none)
     L = L_;
     t0 = t0_;
     t = t0_;
@@ -234,7 +386,10 @@ void ScEngine::setup(const fr_t* const tables[3], uint32_t L_, uint32_t t0_, uin
     }
     // suffix eq tables over w[t0+1 .. t0+n_eq_loc-1]: LO (pair-summed in the round kernel) x HI (<= 10 vars)
     HI = LO[0] = LO[1] = HP[0] = HP[1] = nullptr;
-    hb = n_eq_loc >= 1 ? (n_eq_loc - 1 < 10 ? n_eq_loc - 1 : 10) : 0;
+    // HI variables: 10 for the unfactored kernel (per-pair LO x HI); 5 for the factored K = 2 kernel, whose
+    // CTAs apply HI once per group of 2^lo_cnt pairs (groups stay large while LO holds most variables)
+    const uint32_t hmax = (factored && K == 2) ? 5 : 10;
+    hb = n_eq_loc >= 1 ? (n_eq_loc - 1 < hmax ? n_eq_loc - 1 : hmax) : 0;
     lo0 = n_eq_loc >= 1 ? n_eq_loc - 1 - hb : 0;
     if (n_eq_loc >= 2) {
         HI = s->alloc<fr_t>(1ull << hb);
@@ -254,6 +409,16 @@ void ScEngine::setup(const fr_t* const tables[3], uint32_t L_, uint32_t t0_, uin
         partials = s->alloc<fr_t>((size_t)ctx->num_sms * 4 * 4);
         ticket = s->alloc_zero<unsigned int>(1);
     }
+}
+
+void ScEngine::set_i32(const int32_t* const src[3]) {
+    for (uint32_t k = 0; k < K; k++) {
+        i32[k] = src[k];
+        if (src[k] && !(factored && K == 2))
+            embed_i32_dev(ctx, src[k], 1ull << L, const_cast<fr_t*>(cur[k]));
+    }
+    if (!(factored && K == 2))
+        for (uint32_t k = 0; k < 3; k++) i32[k] = nullptr;
 }
 
 void ScEngine::round(fr_t* part_out) {
@@ -301,10 +466,45 @@ void ScEngine::round(fr_t* part_out) {
     a.point_out = d_point + 32ull * t;
     a.part_out = part_out;
     a.scale = d_scale;
-    unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
-    if (K == 1) launch_round<1>(ctx, fold, grid, a);
-    else if (K == 2) launch_round<2>(ctx, fold, grid, a);
-    else launch_round<3>(ctx, fold, grid, a);
+    if (K == 2 && factored) {
+        Sc2Args A;
+        memset(&A, 0, sizeof A);
+        A.r = a;
+        const bool from_i32 = tl == 0 && (i32[0] || i32[1]);
+        if (from_i32) {
+            ZK_REQUIRE(i32[0] && i32[1], ZK_ERR_INTERNAL, "sumcheck: mixed int32 / Fr tables in round 0");
+            for (int k = 0; k < 2; k++) {
+                A.i32[k] = i32[k];
+                A.emb[k] = const_cast<fr_t*>(cur[k]);
+            }
+        }
+        // work items: (group of pairs sharing one HI value) x slices, at most two waves of 2 CTAs per SM
+        const uint32_t glog = a.eq_mode ? a.lo_cnt : 0;
+        const uint64_t ngroups = a.eq_mode ? ((n_pairs >> glog) ? (n_pairs >> glog) : 1) : 1;
+        const uint64_t gsize = a.eq_mode ? (n_pairs < (1ull << glog) ? n_pairs : (1ull << glog)) : n_pairs;
+        const uint64_t cap = (uint64_t)ctx->num_sms * 2;
+        A.flat = a.eq_mode && gsize < 1024;   // small groups: per-pair HI product instead
+        const uint64_t ng = A.flat ? 1 : ngroups, gs = A.flat ? n_pairs : gsize;
+        // slices: enough items to fill the grid (one pair per thread at least), ~8 items per CTA when
+        // the round is large (static round robin stays balanced), never below 256 pairs per item
+        const uint64_t want = (n_pairs + 255) / 256 < cap ? (n_pairs + 255) / 256 : cap;
+        uint64_t slices = 1;
+        while (gs / (slices * 2) >= 256 && (ng * slices < want || (ng * slices * 2 <= 8 * cap && gs / (slices * 2) >= 2048)))
+            slices *= 2;
+        A.slices = (uint32_t)slices;
+        const unsigned int grid = (unsigned int)(ng * slices < cap ? ng * slices : cap);
+        if (from_i32)
+            ZK_LAUNCH(ctx, k_sc_round2f<2>, grid, 256, 0, A);
+        else if (fold)
+            ZK_LAUNCH(ctx, k_sc_round2f<1>, grid, 256, 0, A);
+        else
+            ZK_LAUNCH(ctx, k_sc_round2f<0>, grid, 256, 0, A);
+    } else {
+        unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
+        if (K == 1) launch_round<1>(ctx, fold, grid, a);
+        else if (K == 2) launch_round<2>(ctx, fold, grid, a);
+        else launch_round<3>(ctx, fold, grid, a);
+    }
     if (a.eq_mode == 1) {
         lo_level ^= 1;
     } else if (a.eq_mode == 2) {
@@ -358,6 +558,7 @@ struct ScAllArgs {
     fr_t* partials;             // gridDim.x * 4
     unsigned int* arrive;       // monotonic: blocks that finished round t = (t+1) * gridDim.x
     unsigned int* flag;         // rounds whose challenge is published
+    const fr_t* r_first;        // continuation of a larger statement: round 0 folds by this challenge
 };
 
 __device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
@@ -377,16 +578,18 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
     if (blockIdx.x == 0 && tid < 32) fs_begin(fs, a.st);
     for (uint32_t t = 0; t < m; t++) {
         const uint64_t n_pairs = 1ull << (m - t - 1);
+        const bool fold0 = a.r_first != nullptr;
+        const bool folding = t > 0 || fold0;
         const fr_t* src[K];
         fr_t* dst[K];
 #pragma unroll
         for (int k = 0; k < K; k++) {
-            src[k] = t == 0 ? a.src[k] : (t == 1 ? a.src[k] : a.buf[(t - 1) & 1][k]);
+            src[k] = (t == 0 || (t == 1 && !fold0)) ? a.src[k] : a.buf[(t - 1) & 1][k];
             dst[k] = a.buf[t & 1][k];
         }
         fr_t r;
-        if (t > 0) {
-            const uint4* q = reinterpret_cast<const uint4*>(&a.d_r[t - 1]);
+        if (folding) {
+            const uint4* q = reinterpret_cast<const uint4*>(t > 0 ? &a.d_r[t - 1] : a.r_first);
             uint4 x = __ldcg(q), y = __ldcg(q + 1);
             r = fr_t{{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w}};
         }
@@ -405,7 +608,7 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 fr_t v0, v1;
-                if (t > 0) {
+                if (folding) {
                     const fr_t* s = src[k] + 4 * b;
                     fr_t x0 = fr_load_l2(s), x1 = fr_load_l2(s + 1), x2 = fr_load_l2(s + 2), x3 = fr_load_l2(s + 3);
                     v0 = fr_add(x0, fr_mul(r, fr_sub(x1, x0)));
@@ -517,7 +720,7 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
         const int lane = tid;
         const fr_t* T = lane == 0 ? a.buf[(m - 1) & 1][0] : (lane == 1 ? a.buf[(m - 1) & 1][K > 1 ? 1 : 0]
                                                                         : a.buf[(m - 1) & 1][K > 2 ? 2 : 0]);
-        if (m == 1) T = lane == 0 ? a.src[0] : (lane == 1 ? a.src[K > 1 ? 1 : 0] : a.src[K > 2 ? 2 : 0]);
+        if (m == 1 && !a.r_first) T = lane == 0 ? a.src[0] : (lane == 1 ? a.src[K > 1 ? 1 : 0] : a.src[K > 2 ? 2 : 0]);
         fr_t f = fr_zero();
         if (lane < K) {
             fr_t rr = fr_load(&a.d_r[m - 1]);
@@ -608,6 +811,8 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
     const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
     ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
     if (m <= SC_ALL_MAX_LOG && !getenv("ZKDL_NO_PERSISTENT")) {
+        for (uint32_t k = 0; k < K; k++)
+            if (S.i32[k]) embed_i32_dev(ctx, S.i32[k], 1ull << m, const_cast<fr_t*>(S.tables[k]));
         sumcheck_prove_small(ctx, tr, S, s);
         return;
     }
@@ -628,8 +833,65 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
     e.d_finals = S.d_finals;
     e.header();
     e.setup(S.tables, m, 0, n_eq);
-    for (uint32_t t = 0; t < m; t++) e.round(nullptr);
-    e.finals();
+    e.set_i32(S.i32);
+    e.run_to_end();
+}
+
+constexpr uint32_t SC_TAIL_LOG = 16;
+
+void ScEngine::run_to_end() {
+    const bool persistent_ok = !getenv("ZKDL_NO_PERSISTENT");
+    while (t < t0 + L) {
+        const uint32_t tl = t - t0;
+        if (tl >= 1 && persistent_ok && L - tl <= SC_TAIL_LOG) {
+            persist_rest();
+            return;
+        }
+        round(nullptr);
+    }
+    finals();
+}
+
+// The remaining local rounds tl .. L-1 (tl >= 1: the tables still need the fold by r_{t-1}) as a
+// continuation statement of k_sc_all: m' = L - tl variables, eq over the remaining eq variables, the
+// same transcript, proof offsets shifted by t rounds; k_sc_all also writes the finals.
+void ScEngine::persist_rest() {
+    const uint32_t tl = t - t0, mr = L - tl;
+    ZK_REQUIRE(tl >= 1 && mr >= 1, ZK_ERR_INTERNAL, "sumcheck continuation: bad round");
+    ScAllArgs a;
+    memset(&a, 0, sizeof a);
+    for (uint32_t k = 0; k < K; k++) {
+        a.src[k] = cur[k];
+        a.buf[0][k] = s->alloc<fr_t>(1ull << mr);
+        a.buf[1][k] = s->alloc<fr_t>(mr >= 2 ? 1ull << (mr - 1) : 1);
+    }
+    const uint32_t n_eq_end = t0 + n_eq_loc;
+    const uint32_t n_rem = t < n_eq_end ? n_eq_end - t : 0;
+    if (n_rem >= 2) {
+        a.E[0] = s->alloc<fr_t>(1ull << (n_rem - 1));
+        a.E[1] = s->alloc<fr_t>(n_rem >= 3 ? 1ull << (n_rem - 2) : 1);
+        eq_table_dev(ctx, d_w + t + 1, n_rem - 1, nullptr, a.E[0], *s);
+    }
+    a.m = mr;
+    a.n_eq = n_rem;
+    a.w = d_w + t;
+    a.claim = d_claim;
+    a.compute_claim = 0;
+    a.st = tr->d_st;
+    a.proof = d_proof + 32ull * t * (K + 1);   // message of local round i at d_proof + 44 + 32 (t + i)(K + 1)
+    a.d_r = d_r + t;
+    a.d_point = d_point + 32ull * t;
+    a.d_finals = d_finals;
+    a.r_first = d_r + t - 1;
+    unsigned int grid = K == 1 ? all_grid<1>(ctx, mr) : K == 2 ? all_grid<2>(ctx, mr) : all_grid<3>(ctx, mr);
+    a.partials = s->alloc<fr_t>((size_t)grid * 4);
+    unsigned int* ctr = s->alloc_zero<unsigned int>(2);
+    a.arrive = ctr;
+    a.flag = ctr + 1;
+    if (K == 1) launch_all<1>(ctx, a, grid);
+    else if (K == 2) launch_all<2>(ctx, a, grid);
+    else launch_all<3>(ctx, a, grid);
+    t = t0 + L;
 }
 
 uint64_t sumcheck_proof_len(uint32_t m, uint32_t K) { return 12 + 32 + 32ull * m * (K + 1) + 32ull * K; }

@@ -6,7 +6,9 @@ namespace zk {
 
 struct ScStatement {
     uint32_t m, n_eq, K;
-    const fr_t* tables[3];   // Fr (Montgomery), 2^m entries each; not modified
+    const fr_t* tables[3];   // Fr (Montgomery), 2^m entries each; not modified (i32[k] set: scratch that
+                             // round 0 fills with the embedded int32 table)
+    const int32_t* i32[3];   // int32 source of table k, or null
     const fr_t* d_w;         // n_eq points (Montgomery)
     fr_t* d_claim;           // in (claim_given) or out
     bool claim_given;
@@ -40,13 +42,22 @@ struct ScEngine {
     fr_t* d_claim = nullptr;
     bool claim_given = false;
     fr_t* d_finals = nullptr;
+    const int32_t* i32[3] = {nullptr, nullptr, nullptr};   // int32 sources: round 0 embeds into cur[k]
+    bool factored = true;   // K = 2: k_sc_round2f (ZKDL_SC_V=0: the unfactored k_sc_round)
 
+    // int32 tables: round 0 of the factored kernel embeds them into the (scratch) cur tables; otherwise
+    // they are embedded here, before round 0
+    void set_i32(const int32_t* const src[3]);
     // local tables of 2^L entries entering at global round t0; eq over w[t0 .. t0 + n_eq_loc - 1]
     void setup(const fr_t* const tables[3], uint32_t L, uint32_t t0, uint32_t n_eq_loc);
     void header();                    // absorb "sc/hdr" (+ the given claim)
     void round(fr_t* part_out);       // round t: fused (part_out == nullptr) or partial-only
     void combine(const fr_t* all, uint32_t G);   // sharded: sum G partials + transcript step of round t-1
     void finals();
+    // every remaining round and the finals; the last rounds (<= 2^SC_TAIL_LOG entries left) in one
+    // persistent cooperative launch instead of one launch per round
+    void run_to_end();
+    void persist_rest();
 };
 
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s);

@@ -60,3 +60,40 @@ def uniform_range(seed: int, tensor_id: int, shape, lo: int, hi: int, dtype=np.i
     if bits == 0:
         return np.full(shape, lo, dtype=dtype)
     return uniform_bits(seed, tensor_id, n, lo, bits).astype(dtype).reshape(shape)
+
+
+# ---------------------------------------------------------------- the same generator on a torch device
+def _lsr(z, k: int):
+    """Logical right shift of int64 tensors holding uint64 bit patterns."""
+    import torch
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def _i64(u: int) -> int:
+    """uint64 constant -> the int64 with the same bits (torch integer arithmetic wraps mod 2^64)."""
+    u &= 0xFFFFFFFFFFFFFFFF
+    return u - (1 << 64) if u >> 63 else u
+
+
+def uniform_range_torch(seed: int, tensor_id: int, n: int, lo: int, hi: int, device, offset: int = 0,
+                        chunk: int = 1 << 26):
+    """int32 tensor of entries offset .. offset+n-1 of uniform_range(seed, tensor_id, ...) computed on
+    `device` (bit-identical to the numpy generator; used for inputs too large to generate on the host,
+    e.g. C5 at m = 30, and for per-rank slices of a sharded statement)."""
+    import torch
+    span = hi - lo
+    bits = span.bit_length() - 1
+    if span <= 0 or (1 << bits) != span or not 1 <= bits <= 63:
+        raise ValueError("hi - lo must be a power of two in [2, 2^63]")
+    base = (seed ^ ((tensor_id * 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+    out = torch.empty(n, dtype=torch.int32, device=device)
+    g, m1, m2 = _i64(0x9E3779B97F4A7C15), _i64(0xBF58476D1CE4E5B9), _i64(0x94D049BB133111EB)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        z = torch.arange(offset + s, offset + e, dtype=torch.int64, device=device) + _i64(base)
+        z = z + g
+        z = (z ^ _lsr(z, 30)) * m1
+        z = (z ^ _lsr(z, 27)) * m2
+        z = z ^ _lsr(z, 31)
+        out[s:e] = (_lsr(z, 64 - bits) + lo).to(torch.int32)
+    return out
