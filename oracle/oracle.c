@@ -919,20 +919,40 @@ int or_relu_verify(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t
     if (!fr_eq(P, c)) return -100;
     absorb_frs(tr, "relu/final", fin, 3);
     if (Z && GA) {   /* the three aux claims against the bits of Z and G_A (brute force) */
-        fr s0 = fr_zero(), s1 = fr_zero(), sg = fr_zero();
-        for (uint64_t i = 0; i < D; i++) {
-            fr ei = eq_at(vi, (int)logD, i);
-            uint32_t z = (uint32_t)Z[i], g = (uint32_t)GA[i];
-            fr bz = fr_zero(), bg = fr_zero();
-            for (uint32_t j = 0; j < QR; j++) {
-                fr ej = eq_at(vj, (int)logB, j);
-                if ((z >> j) & 1) bz = fr_add(bz, ej);
-                if ((g >> j) & 1) bg = fr_add(bg, ej);
+        /* aux~(s, v, w) = sum_i eq(v_i, i) sum_j eq(v_j, j) bit_j(word_s[i]); the j-factors do not depend
+           on i (computed once), the i-sum is split over threads (field addition: order-free) */
+        fr ej[64];
+        for (uint32_t j = 0; j < QR; j++) ej[j] = eq_at(vj, (int)logB, j);
+        int nt = omp_get_max_threads();
+        fr *part = (fr *)calloc((size_t)3 * nt, sizeof(fr));
+        #pragma omp parallel
+        {
+            int id = omp_get_thread_num();
+            fr a0s = fr_zero(), a1s = fr_zero(), sgs = fr_zero();
+            #pragma omp for schedule(static)
+            for (uint64_t i = 0; i < D; i++) {
+                fr ei = eq_at(vi, (int)logD, i);
+                uint32_t z = (uint32_t)Z[i], g = (uint32_t)GA[i];
+                fr bz = fr_zero(), bg = fr_zero();
+                for (uint32_t j = 0; j < QR; j++) {
+                    if ((z >> j) & 1) bz = fr_add(bz, ej[j]);
+                    if ((g >> j) & 1) bg = fr_add(bg, ej[j]);
+                }
+                a0s = fr_add(a0s, fr_mul(ei, bz));
+                a1s = fr_add(a1s, fr_mul(ei, bg));
+                if ((z >> (QR - 1)) & 1) sgs = fr_add(sgs, ei);
             }
-            s0 = fr_add(s0, fr_mul(ei, bz));
-            s1 = fr_add(s1, fr_mul(ei, bg));
-            if ((z >> (QR - 1)) & 1) sg = fr_add(sg, ei);
+            part[3 * id] = a0s;
+            part[3 * id + 1] = a1s;
+            part[3 * id + 2] = sgs;
         }
+        fr s0 = fr_zero(), s1 = fr_zero(), sg = fr_zero();
+        for (int i = 0; i < nt; i++) {
+            s0 = fr_add(s0, part[3 * i]);
+            s1 = fr_add(s1, part[3 * i + 1]);
+            sg = fr_add(sg, part[3 * i + 2]);
+        }
+        free(part);
         if (!fr_eq(s0, fin[0])) return -201;
         if (!fr_eq(s1, fin[1])) return -202;
         if (!fr_eq(sg, fin[2])) return -203;

@@ -410,3 +410,61 @@ def test_shard_nccl_single_rank(ctx, O):
         assert res["msgs"] == o["msgs"] and res["finals"] == o["finals"] and res["claim"] == o["claim"]
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- BASELINE workloads at full size
+def test_c4_window_full_size_vs_oracle(ctx, O):
+    """C4, the bench.py workload, at full size in the bench's launch configuration (zkReLU on a second
+    stream, matmul families over four budgeted streams): every matmul family is bit-exact against the
+    oracle's own proof (brute-force restriction, claim = brute-force MLE of the exact integer product),
+    the 2^23-entry zkReLU family is accepted by the oracle verifier (claims = brute-force MLEs of Z, A,
+    G_A, G_Z; finals = brute-force aux MLEs of the bits), and every family's and the window's
+    transcript state equal the oracle's (D3d)."""
+    import os
+    import torch
+    from paper_2307_16273_b200 import api
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    from synth.prng import DATA_SEED
+    O.set_threads(len(os.sched_getaffinity(0)))
+    shape = fcn.C4_SHAPE
+    fams = fcn.assemble_families(shape, fcn.generate_trace(shape, seed=DATA_SEED))
+    relu_ctx = api.Context(0, torch.cuda.Stream())
+    mm = [api.Context(0, torch.cuda.Stream()) for _ in range(3)]
+    for c in [ctx] + mm:
+        c.set_sm_budget(37)
+    g = dfcn.prove_window(ctx, fs_seed("C4-rank0"), fcn.fcn_header(shape), dfcn.upload_families(fams),
+                          relu_ctx=relu_ctx, mm_ctxs=mm)
+    ctx.set_sm_budget(0)
+    W = O.Transcript(fs_seed("C4-rank0"))
+    W.absorb("fcn/hdr", fcn.fcn_header(shape))
+    forks = []
+    for f in fams:
+        W.absorb("fcn/fam", f.name.encode())
+        forks.append(O.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    for f, T, gr in zip(fams, forks, g):
+        if hasattr(f, "A"):
+            o = O.matmul_prove(T, f.A, f.B, f.transA, f.transB)
+            assert (gr["w"], gr["u1"], gr["u3"], gr["claim"]) == (o["w"], o["u1"], o["u3"], o["claim"]), f.name
+            assert gr["msgs"] == o["msgs"] and gr["finals"] == o["finals"], f.name
+        else:
+            assert O.relu_verify(T, f.Z, f.GA, f.Q, f.R, gr["claims"], gr["msgs"], gr["finals"]) == 0, f.name
+        assert gr["state"] == T.state(), f.name
+    for T in forks:
+        W.absorb("fcn/join", T.state())
+    assert g[-1]["window_state"] == W.state()
+
+
+@pytest.mark.parametrize("m", [22])
+def test_c5_bench_size_vs_oracle(ctx, O, m):
+    """C5 at the smallest BASELINE sweep size through the path bench.py --config C5 times (int32 tables
+    embedded in round 0, grouped and flat factored rounds, persistent tail): bit-exact."""
+    from oracle import drivers
+    from paper_2307_16273_b200 import api
+    A, B = drivers.c5_inputs(m)
+    o = drivers.c5_prove(m)
+    tr = api.Transcript(ctx, fs_seed(f"C5-m{m}"))
+    tr.absorb("c5/hdr", m.to_bytes(4, "little"))
+    w = tr.challenges("c5/w", m)
+    g = api.sumcheck_prove(ctx, tr, m, m, [dev(A), dev(B)], w)
+    assert g["claim"] == o["claim"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
