@@ -57,6 +57,9 @@ def lib():
         L.or_relu_tables.argtypes = [i32p, i32p, c.c_uint64, c.c_uint32, c.c_uint32] + [vp] * 7
         L.or_relu_prove.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp]
         L.or_relu_verify.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp]
+        L.or_reindex_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp,
+                                       vp, vp, vp, vp]
+        L.or_relu_merge.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp]
         L.or_set_threads.argtypes = [c.c_int]
         L.or_get_threads.restype = c.c_int
         L.or_transcript_size.restype = c.c_uint64
@@ -275,3 +278,52 @@ def relu_verify(tr: Transcript, Z, GA, Q: int, R: int, claims, msgs, finals) -> 
     flat = [v for row in msgs for v in row]
     return lib().or_relu_verify(tr.st, None if Zc is None else _ptr(Zc), None if Gc is None else _ptr(Gc),
                                 logD, Q, R, to_bytes(claims), to_bytes(flat), to_bytes(finals))
+
+
+# ---------------------------------------------------------------- N1: re-indexing, aux-claim merge
+def reindex_prove(tr: Transcript, X: np.ndarray, views: list, u: list, claims: list, want_tables: bool = False):
+    """Eq. (sc-reindex) (D20).  X: [N][D] int32 (N, D powers of two); views: list of
+    (map: int array of 2^{n_k} slice indices or -1 for an empty slot, u_k: n_k points); u: log2 D
+    points; claims: c_k = X_k~(u, u_k).  Returns dict(rk, claim, msgs, r, finals[, C, Xu])."""
+    X = np.ascontiguousarray(X, dtype=np.int32)
+    N, D = X.shape
+    n, d = N.bit_length() - 1, D.bit_length() - 1
+    assert N == 1 << n and D == 1 << d
+    K = len(views)
+    nk = [len(m).bit_length() - 1 for m, _ in views]
+    for (mp, uk), l in zip(views, nk):
+        assert len(mp) == 1 << l and len(uk) == l
+    maps = np.concatenate([np.asarray(mp, dtype=np.int64) & 0xFFFFFFFF for mp, _ in views]).astype(np.uint32)
+    uk_all = [x for _, uk in views for x in uk]
+    rk, claim, msgs, r, fin = _buf(32 * K), _buf(32), _buf(32 * 3 * max(n, 1)), _buf(32 * max(n, 1)), _buf(64)
+    tabs = _buf(64 * N) if want_tables else None
+    s = lib().or_reindex_prove(tr.st, _ptr(X), n, d, K, (ctypes.c_uint32 * K)(*nk), _ptr(maps), to_bytes(uk_all),
+                               to_bytes(u), to_bytes(claims), rk, claim, msgs, r, fin, tabs)
+    if s:
+        raise ValueError(f"or_reindex_prove status {s}")
+    flat = from_bytes(msgs.raw[:96 * n])
+    out = dict(rk=from_bytes(rk.raw[:32 * K]), claim=from_bytes(claim.raw[:32])[0],
+               msgs=[flat[3 * t:3 * t + 3] for t in range(n)], r=from_bytes(r.raw[:32 * n], n),
+               finals=from_bytes(fin.raw[:64], 2))
+    if want_tables:
+        tv = from_bytes(tabs.raw[:64 * N])
+        out["C"], out["Xu"] = tv[:N], tv[N:]
+    return out
+
+
+def relu_merge(tr: Transcript, Z: np.ndarray, GA: np.ndarray, Q: int, R: int, point: list, finals: list):
+    """The zkReLU aux-claim merge (D21) after relu_prove on the same transcript.
+    Returns dict(rho, claim, msgs, r, finals): finals[0] = aux~(r_s, v, r_j) (the merged claim)."""
+    Z = np.ascontiguousarray(Z, dtype=np.int32).reshape(-1)
+    GA = np.ascontiguousarray(GA, dtype=np.int32).reshape(-1)
+    logD = Z.size.bit_length() - 1
+    m = relu_logB(Q, R) + 1
+    rho, claim, msgs, r, fin = _buf(32), _buf(32), _buf(96 * m), _buf(32 * m), _buf(64)
+    s = lib().or_relu_merge(tr.st, _ptr(Z), _ptr(GA), logD, Q, R, to_bytes(point), to_bytes(finals), rho, claim,
+                            msgs, r, fin)
+    if s:
+        raise ValueError(f"or_relu_merge status {s}")
+    flat = from_bytes(msgs.raw[:96 * m])
+    return dict(rho=from_bytes(rho.raw[:32])[0], claim=from_bytes(claim.raw[:32])[0],
+                msgs=[flat[3 * t:3 * t + 3] for t in range(m)], r=from_bytes(r.raw[:32 * m], m),
+                finals=from_bytes(fin.raw[:64], 2))

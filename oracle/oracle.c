@@ -960,6 +960,122 @@ int or_relu_verify(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t
     return 0;
 }
 
+/* ------------------------------------------------------------ N1: re-indexing sumcheck
+ * Eq. (sc-reindex) P:L262-270 (D20).  X: N = 2^n slices of D = 2^d int32 entries, row-major
+ * [N][D]; a point on X is (u over the D bits, then the N bits) (D2).  View k has N_k = 2^{n_k} slots,
+ * slot j holding slice map_k[j] (0xffffffff: an empty, all-zero slot); p_k(i, j) = [map_k[j] == i].
+ * Given claims c_k = X_k~(u, u_k):
+ *   sum_k r_k c_k = sum_i ( sum_k sum_j r_k beta(u_k, j) p_k(i, j) ) X~(u, i),
+ * proved by the product sumcheck over i of C(i) = sum_k sum_j r_k beta(u_k, j) p_k(i, j) and
+ * X_u(i) = X~(u, i) = sum_d beta(u, d) X[i][d].  Transcript: "rx/hdr" (n, d, K, n_k...) -> "rx/claims"
+ * -> r_k ("rx/r" x K) -> sumcheck (D3c, n_eq = 0, claim sum_k r_k c_k given). */
+int or_reindex_prove(transcript *tr, const int32_t *X, uint32_t n, uint32_t d, uint32_t K, const uint32_t *nk,
+                     const uint32_t *maps /* concatenated, 2^{n_k} each */, const uint8_t *uk_b /* concatenated */,
+                     const uint8_t *u_b /* d */, const uint8_t *claims_b /* K */, uint8_t *rk_out /* K */,
+                     uint8_t *claim_out, uint8_t *msgs_out /* n x 3 */, uint8_t *r_out /* n */, uint8_t *finals_out /* 2 */,
+                     uint8_t *tables_out /* optional: C then X_u, 2 x 2^n canonical */) {
+    init();
+    if (K < 1 || K > 64 || n > 30 || d > 34) return -1;
+    uint64_t N = 1ULL << n, D = 1ULL << d;
+    fr u[64], cl[64], rk[64];
+    if (load_point(u_b, (int)d, u)) return -3;
+    for (uint32_t k = 0; k < K; k++) if (load_canon(claims_b + 32 * k, &cl[k])) return -3;
+    uint32_t hdr[3 + 64];
+    hdr[0] = n; hdr[1] = d; hdr[2] = K;
+    for (uint32_t k = 0; k < K; k++) hdr[3 + k] = nk[k];
+    absorb_u32s(tr, "rx/hdr", hdr, (int)(3 + K));
+    absorb_frs(tr, "rx/claims", cl, (int)K);
+    for (uint32_t k = 0; k < K; k++) { rk[k] = transcript_challenge(tr, "rx/r"); store_canon(rk[k], rk_out + 32 * k); }
+    fr claim = fr_zero();
+    for (uint32_t k = 0; k < K; k++) claim = fr_add(claim, fr_mul(rk[k], cl[k]));
+    /* C(i): the definition, slot by slot */
+    fr *C = (fr *)calloc(N, sizeof(fr));
+    uint64_t off = 0, uoff = 0;
+    for (uint32_t k = 0; k < K; k++) {
+        fr uk[64];
+        if (nk[k] > 30 || load_point(uk_b + 32 * uoff, (int)nk[k], uk)) { free(C); return -3; }
+        for (uint64_t j = 0; j < (1ULL << nk[k]); j++) {
+            uint32_t i = maps[off + j];
+            if (i == 0xffffffffu) continue;
+            if (i >= N) { free(C); return -1; }
+            C[i] = fr_add(C[i], fr_mul(rk[k], eq_at(uk, (int)nk[k], j)));
+        }
+        off += 1ULL << nk[k];
+        uoff += nk[k];
+    }
+    /* X_u(i) = X~(u, i): brute-force MLE of slice i over its D entries */
+    fr *Xu = (fr *)malloc(N * sizeof(fr));
+    #pragma omp parallel for schedule(static)
+    for (uint64_t i = 0; i < N; i++) {
+        fr acc = fr_zero();
+        for (uint64_t c = 0; c < D; c++)
+            if (X[i * D + c]) acc = fr_add(acc, fr_mul(fr_from_i64(X[i * D + c]), eq_at(u, (int)d, c)));
+        Xu[i] = acc;
+    }
+    uint8_t *tb = (uint8_t *)malloc(2 * N * 32);
+    for (uint64_t i = 0; i < N; i++) { store_canon(C[i], tb + 32 * i); store_canon(Xu[i], tb + 32 * (N + i)); }
+    if (tables_out) memcpy(tables_out, tb, 2 * N * 32);
+    uint8_t cb[32];
+    store_canon(claim, cb);
+    int st = or_sumcheck_prove(tr, n, 0, 2, NULL, tb, cb, claim_out, msgs_out, r_out, finals_out);
+    free(C); free(Xu); free(tb);
+    return st;
+}
+
+/* ------------------------------------------------------------ N1: zkReLU aux-claim merge
+ * P:L470 ("they can be merged into a singular claim"), S:L459 (D21).  aux[s][i][j] = bit j of
+ * word s (s = 0: Z, s = 1: G_A) of entry i; the three claims of the zkReLU sumcheck at its point
+ * (w over the logB j-bits, v over the logD i-bits): f0 = aux~(0, v, w), f1 = aux~(1, v, w),
+ * f2 = aux~(0, v, Q+R-1).  All three share v, so with rho from the transcript
+ *   f0 + rho f1 + rho^2 f2 = sum_{s, j} T(s, j) W(s, j),   T(s, j) = sum_i beta(v, i) aux[s][i][j],
+ *   W(s, j) = [s = 0] (beta(w, j) + rho^2 [j = Q+R-1]) + [s = 1] rho beta(w, j),
+ * proved by the product sumcheck over (j, s) (j bits first, D2); its finals are T~(r) =
+ * aux~(r_s, v, r_j), the single merged claim, and W~(r).  Transcript: "relu/merge" (rho) after the
+ * zkReLU proof, then the sumcheck (D3c, n_eq = 0, claim given). */
+int or_relu_merge(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
+                  const uint8_t *point_b /* logB + logD */, const uint8_t *finals_b /* 3 */, uint8_t *rho_out,
+                  uint8_t *claim_out, uint8_t *msgs_out /* (logB + 1) x 3 */, uint8_t *r_out /* logB + 1 */,
+                  uint8_t *finals_out /* 2 */) {
+    init();
+    uint32_t QR = Q + R, logB = 0;
+    while ((1u << logB) < QR) logB++;
+    uint64_t D = 1ULL << logD, B = 1ULL << logB;
+    fr pt[96], f[3];
+    if (load_point(point_b, (int)(logB + logD), pt)) return -3;
+    for (int k = 0; k < 3; k++) if (load_canon(finals_b + 32 * k, &f[k])) return -3;
+    const fr *w = pt, *v = pt + logB;
+    fr rho = transcript_challenge(tr, "relu/merge");
+    store_canon(rho, rho_out);
+    fr rho2 = fr_mul(rho, rho);
+    fr claim = fr_add(fr_add(f[0], fr_mul(rho, f[1])), fr_mul(rho2, f[2]));
+    /* T(s, j) by brute force over the entries */
+    fr T[2][64];
+    for (int sx = 0; sx < 2; sx++) {
+        const int32_t *word = sx ? GA : Z;
+        for (uint64_t j = 0; j < B; j++) {
+            fr acc = fr_zero();
+            if (j < QR)
+                for (uint64_t i = 0; i < D; i++)
+                    if (((uint32_t)word[i] >> j) & 1) acc = fr_add(acc, eq_at(v, (int)logD, i));
+            T[sx][j] = acc;
+        }
+    }
+    uint64_t n = 2 * B;
+    uint8_t *tb = (uint8_t *)malloc(2 * n * 32);
+    for (int sx = 0; sx < 2; sx++)
+        for (uint64_t j = 0; j < B; j++) {
+            fr ew = eq_at(w, (int)logB, j);
+            fr W = sx ? fr_mul(rho, ew) : fr_add(ew, j == QR - 1 ? rho2 : fr_zero());
+            store_canon(T[sx][j], tb + 32 * (sx * B + j));
+            store_canon(W, tb + 32 * (n + sx * B + j));
+        }
+    uint8_t cb[32];
+    store_canon(claim, cb);
+    int st = or_sumcheck_prove(tr, logB + 1, 0, 2, NULL, tb, cb, claim_out, msgs_out, r_out, finals_out);
+    free(tb);
+    return st;
+}
+
 /* ------------------------------------------------------------ misc exports */
 void or_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
 int or_get_threads(void) { return omp_get_max_threads(); }
