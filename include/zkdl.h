@@ -139,6 +139,34 @@ zk_status zk_sumcheck_prove(zk_ctx* ctx, zk_transcript* tr, const zk_prod_stmt* 
                             const zk_fr* claim, zk_fr* claim_out, uint8_t* proof, uint64_t* proof_len,
                             zk_fr* point_out, zk_fr* finals_out);
 
+/* ------------------------------------------- claim reductions after the hot path
+ * zk_reindex_prove — the re-indexing sumcheck, Eq. (sc-reindex) P:L262-270 (D20).
+ *   d_X: int32 stack of N = 2^n slices of D = 2^d entries, row-major [N][D] (device, borrowed).  A
+ *   point on X is (u over the D bits, then the N bits) (D2).  views[k]: N_k = 2^{logN} slots; slot j
+ *   holds slice map[j] (host array, injective into [0, N); 0xffffffff = an all-zero slot), with the
+ *   point u_k (host, logN elements); claims[k] = X_k~(u, u_k) (host, K <= 32); u: host, d elements.
+ *   Transcript: "rx/hdr" (n, d, K, logN_0..logN_{K-1} as u32le) | "rx/claims" (K) | r_k = "rx/r" x K |
+ *   the product sumcheck (D3c) over n variables of C(i) = sum_k r_k sum_j beta(u_k, j) [map_k[j] = i]
+ *   and X~(u, i), n_eq = 0, claim sum_k r_k claims[k] given.  proof / proof_len / point_out (n) as in
+ *   zk_sumcheck_prove; finals_out (host, 2): C~(r) (the verifier recomputes it from the maps) and
+ *   X~(u, r), the single output claim on the stack.  Errors: ZK_ERR_RANGE (slot outside the stack),
+ *   ZK_ERR_ARG (non-injective map, bad shape).  Synchronises the ctx stream once.
+ * zk_relu_merge — the zkReLU aux-claim merge, P:L470 (D21), on the transcript
+ *   that just proved zk_relu_prove: point = its final point (logB + logD: the j-bits w then the
+ *   i-bits v), finals = its three finals aux~(0, v, w), aux~(1, v, w), aux~(0, v, Q+R-1).
+ *   Transcript: rho = "relu/merge" | the product sumcheck (D3c) over (j, s) (logB + 1 variables, j
+ *   first) of T(s, j) = sum_i beta(v, i) bit_j(word_s[i]) (s = 0: Z, s = 1: G_A) and W(s, j) =
+ *   [s=0](beta(w, j) + rho^2 [j = Q+R-1]) + [s=1] rho beta(w, j), claim f0 + rho f1 + rho^2 f2.
+ *   merged_out (host, 2): aux~(r_s, v, r_j) — the single merged claim — and W~(r); point_out:
+ *   logB + 1 elements (r_j, then r_s).  Synchronises the ctx stream once. */
+typedef struct { uint32_t logN; const uint32_t* map; const zk_fr* u; } zk_view;
+zk_status zk_reindex_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_X, uint32_t n, uint32_t d, uint32_t K,
+                           const zk_view* views, const zk_fr* u, const zk_fr* claims, uint8_t* proof,
+                           uint64_t* proof_len, zk_fr* point_out, zk_fr* finals_out);
+zk_status zk_relu_merge(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                        uint32_t Q, uint32_t R, const zk_fr* point, const zk_fr* finals, uint8_t* proof,
+                        uint64_t* proof_len, zk_fr* point_out, zk_fr* merged_out);
+
 /* ------------------------------------------- sharded product sumcheck (SURVEY §8(e), G = 2^s devices)
  * Rank g (of world = G, a power of two) holds entries [g 2^L, (g+1) 2^L) of every table, L = m - s:
  * the top s index bits (the last-bound variables, D2) are the rank id, so every round pair is local.

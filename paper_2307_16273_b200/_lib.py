@@ -28,6 +28,10 @@ class MmShape(ctypes.Structure):
                 ("logD3", ctypes.c_uint32), ("trans_a", ctypes.c_uint32), ("trans_b", ctypes.c_uint32)]
 
 
+class View(ctypes.Structure):
+    _fields_ = [("logN", ctypes.c_uint32), ("map", ctypes.c_void_p), ("u", ctypes.c_void_p)]
+
+
 class ProdStmt(ctypes.Structure):
     _fields_ = [("m", ctypes.c_uint32), ("n_eq", ctypes.c_uint32), ("n_tables", ctypes.c_uint32),
                 ("i32_mask", ctypes.c_uint32), ("w", ctypes.c_void_p)]
@@ -56,6 +60,8 @@ def lib():
         "zk_ctx_profile_read": ([vp, c.c_char_p, u64], i32),
         "zk_ctx_profile_filter": ([vp, c.c_char_p], i32),
         "zk_ctx_set_sm_budget": ([vp, u32], i32),
+        "zk_reindex_prove": ([vp, vp, vp, u32, u32, u32, vp, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
+        "zk_relu_merge": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_transcript_new": ([vp, vp, c.POINTER(vp)], i32),
         "zk_transcript_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_transcript_challenges": ([vp, c.c_char_p, u32, vp], i32),

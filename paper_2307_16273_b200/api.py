@@ -12,7 +12,7 @@ import ctypes
 
 import torch
 
-from ._lib import MmShape, ProdStmt, ZkError, lib
+from ._lib import MmShape, ProdStmt, View, ZkError, lib
 
 P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
 
@@ -396,3 +396,49 @@ def diag_mul_bench(ctx: Context, seed: torch.Tensor, iters: int, blocks: int) ->
     out = fr_empty(blocks * 256, seed.device)
     ctx.check(lib().zk_diag_mul_bench(ctx.h, _dev_ptr(seed), iters, blocks, out.data_ptr()))
     return out
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) N1
+def reindex_prove(ctx: Context, tr: Transcript, X: torch.Tensor, views: list, u: list, claims: list) -> dict:
+    """zk_reindex_prove (Eq. sc-reindex, D20).  X: int32 device tensor [N][D]; views: list of
+    (map: sequence of 2^n_k slice indices, -1 = empty slot, u_k: n_k field elements); u: log2 D
+    elements; claims: X_k~(u, u_k).  Returns dict(claim, msgs, r, finals, proof)."""
+    assert X.dtype == torch.int32 and X.dim() == 2 and X.is_cuda
+    N, D = X.shape
+    n, d = _log2(N), _log2(D)
+    K = len(views)
+    keep = []
+    vs = (View * K)()
+    for k, (mp, uk) in enumerate(views):
+        arr = (ctypes.c_uint32 * len(mp))(*[(int(i) & 0xFFFFFFFF) for i in mp])
+        ub = _fr_buf(uk) if len(uk) else None
+        keep += [arr, ub]
+        vs[k] = View(_log2(len(mp)), ctypes.cast(arr, ctypes.c_void_p), ctypes.cast(ub, ctypes.c_void_p) if ub else None)
+    plen = ctypes.c_uint64(12 + 32 + 32 * n * 3 + 64)
+    proof = ctypes.create_string_buffer(plen.value)
+    point = ctypes.create_string_buffer(32 * n)
+    fin = ctypes.create_string_buffer(64)
+    ctx.check(lib().zk_reindex_prove(ctx.h, tr.h, _dev_ptr(X, torch.int32), n, d, K, vs, _fr_buf(u) if d else None,
+                                     _fr_buf(claims), proof, ctypes.byref(plen), point, fin))
+    res = parse_sumcheck_proof(proof.raw[:plen.value])
+    res["r"] = _ints(point, n)
+    res["proof"] = proof.raw[:plen.value]
+    return res
+
+
+def relu_merge(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, Q: int, R: int, point: list,
+               finals: list) -> dict:
+    """zk_relu_merge (D21) after relu_prove on the same transcript.  Returns
+    dict(claim, msgs, r, finals, proof): finals[0] = aux~(r_s, v, r_j), the merged claim."""
+    logD = _log2(Z.numel())
+    m = relu_logB(Q, R) + 1
+    plen = ctypes.c_uint64(12 + 32 + 32 * m * 3 + 64)
+    proof = ctypes.create_string_buffer(plen.value)
+    pt = ctypes.create_string_buffer(32 * m)
+    fin = ctypes.create_string_buffer(64)
+    ctx.check(lib().zk_relu_merge(ctx.h, tr.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), logD, Q, R,
+                                  _fr_buf(point), _fr_buf(finals), proof, ctypes.byref(plen), pt, fin))
+    res = parse_sumcheck_proof(proof.raw[:plen.value])
+    res["r"] = _ints(pt, m)
+    res["proof"] = proof.raw[:plen.value]
+    return res

@@ -468,3 +468,86 @@ def test_c5_bench_size_vs_oracle(ctx, O, m):
     w = tr.challenges("c5/w", m)
     g = api.sumcheck_prove(ctx, tr, m, m, [dev(A), dev(B)], w)
     assert g["claim"] == o["claim"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) N1
+@pytest.mark.parametrize("n,d,nks", [(3, 2, [3, 2, 1]), (6, 5, [6, 5]), (10, 8, [10, 9, 0]), (14, 4, [13, 14])])
+def test_reindex_vs_oracle(ctx, O, n, d, nks):
+    """Re-indexing sumcheck (Eq. sc-reindex): transcript bit-exact against the oracle, views with empty
+    slots and several sizes (the larger ones through the factored round kernel)."""
+    from paper_2307_16273_b200 import api
+    rng = random.Random(1000 + n)
+    X = uniform_range(13, n + d, (1 << n, 1 << d), -(1 << 15), 1 << 15)
+    u = [rng.randrange(P) for _ in range(d)]
+    views = []
+    for nk in nks:
+        pick = rng.sample(range(1 << n), min(1 << nk, 1 << n))
+        mp = pick + [-1] * ((1 << nk) - len(pick))
+        rng.shuffle(mp)
+        views.append((mp, [rng.randrange(P) for _ in range(nk)]))
+    claims = [rng.randrange(P) for _ in views]      # any claims: the transcript is still determined
+    seed = fs_seed(f"rx-gpu-{n}-{d}")
+    o = O.reindex_prove(O.Transcript(seed), X, views, u, claims)
+    g = api.reindex_prove(ctx, api.Transcript(ctx, seed), dev(X), views, u, claims)
+    assert g["claim"] == o["claim"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"] and g["r"] == o["r"]
+
+
+def test_reindex_rejects_bad_maps(ctx):
+    from paper_2307_16273_b200 import api
+    X = dev(uniform_range(13, 1, (8, 4), -8, 8))
+    for mp in ([0, 0], [0, 9]):
+        with pytest.raises(api.ZkError):
+            api.reindex_prove(ctx, api.Transcript(ctx, bytes(32)), X, [(mp, [5])], [1, 2], [3])
+
+
+@pytest.mark.parametrize("Q,R,logD", [(4, 2, 3), (16, 16, 8), (8, 8, 12), (16, 16, 16)])
+def test_relu_merge_vs_oracle(ctx, O, Q, R, logD):
+    """zkReLU prove then the aux-claim merge on the same transcript: bit-exact against the oracle."""
+    from paper_2307_16273_b200 import api
+    half = 1 << (Q + R - 1)
+    Z = uniform_range(14, logD + Q, (1 << logD,), -half, half)
+    GA = uniform_range(14, logD + R + 1, (1 << logD,), -half, half)
+    seed = fs_seed(f"merge-gpu-{Q}-{R}-{logD}")
+    ot = O.Transcript(seed)
+    orr = O.relu_prove(ot, Z, GA, Q, R)
+    om = O.relu_merge(ot, Z, GA, Q, R, orr["point"], orr["finals"])
+    gt = api.Transcript(ctx, seed)
+    gr = api.relu_prove(ctx, gt, dev(Z), dev(GA), Q, R)
+    assert gr["finals"] == orr["finals"]
+    gm = api.relu_merge(ctx, gt, dev(Z), dev(GA), Q, R, gr["point"], gr["finals"])
+    assert gm["claim"] == om["claim"] and gm["msgs"] == om["msgs"] and gm["finals"] == om["finals"]
+    assert gt.state() == ot.state()
+
+
+def test_relu_merge_c4_size(ctx, O):
+    """The merge at the C4 zkReLU size (2^23 entries): the merged claim equals aux~(r_s, v, r_j) built
+    from the oracle's brute-force MLEs of the 64 bit planes, and the oracle verifier accepts the merge
+    sumcheck's round identities."""
+    import os
+    from paper_2307_16273_b200 import api
+    O.set_threads(len(os.sched_getaffinity(0)))
+    logD = 23
+    Z = uniform_range(15, 1, (1 << logD,), -(1 << 31), 1 << 31)
+    GA = uniform_range(15, 2, (1 << logD,), -(1 << 31), 1 << 31)
+    rng = random.Random(9)
+    point = [rng.randrange(P) for _ in range(5 + logD)]
+    w, v = point[:5], point[5:]
+    planes = [[O.mle_i32((((word.astype(np.int64) & 0xFFFFFFFF) >> j) & 1).astype(np.int32), v) for j in range(32)]
+              for word in (Z, GA)]                    # aux~(s, v, j) at Boolean j
+    beta5 = lambda x, j: O.beta(x, [(j >> t) & 1 for t in range(5)])
+    ew = [beta5(w, j) for j in range(32)]
+    f0 = sum(e * p for e, p in zip(ew, planes[0])) % P
+    f1 = sum(e * p for e, p in zip(ew, planes[1])) % P
+    f2 = planes[0][31]
+    seed = fs_seed("merge-c4")
+    gm = api.relu_merge(ctx, api.Transcript(ctx, seed), dev(Z), dev(GA), 16, 16, point, [f0, f1, f2])
+    rj, rs = gm["r"][:5], gm["r"][5]
+    ej = [beta5(rj, j) for j in range(32)]
+    t0 = sum(e * p for e, p in zip(ej, planes[0])) % P
+    t1 = sum(e * p for e, p in zip(ej, planes[1])) % P
+    assert gm["finals"][0] == ((1 - rs) * t0 + rs * t1) % P
+    tr = O.Transcript(seed)
+    rho = tr.challenges("relu/merge", 1)[0]
+    claim = (f0 + rho * f1 + rho * rho * f2) % P
+    assert gm["claim"] == claim
+    assert O.sumcheck_verify(tr, 6, 0, 2, [], claim, gm["msgs"], gm["finals"]) == 0
