@@ -413,8 +413,10 @@ def test_shard_nccl_single_rank(ctx, O):
 
 
 # ---------------------------------------------------------------- BASELINE workloads at full size
-def test_c4_window_full_size_vs_oracle(ctx, O):
-    """C4, the bench.py workload, at full size in the bench's launch configuration (zkReLU on a second
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_fcn_window_full_size_vs_oracle(ctx, O, cfg):
+    """C3 (one training step of the uniform 8 x 1024^2 FCN) and C4 (the bench.py workload: a T' = 16
+    window of the paper's 10M FCN) at full size in the bench's launch configuration (zkReLU on a second
     stream, matmul families over four budgeted streams): every matmul family is bit-exact against the
     oracle's own proof (brute-force restriction, claim = brute-force MLE of the exact integer product),
     the 2^23-entry zkReLU family is accepted by the oracle verifier (claims = brute-force MLEs of Z, A,
@@ -427,16 +429,17 @@ def test_c4_window_full_size_vs_oracle(ctx, O):
     from synth import fcn
     from synth.prng import DATA_SEED
     O.set_threads(len(os.sched_getaffinity(0)))
-    shape = fcn.C4_SHAPE
+    shape = fcn.C4_SHAPE if cfg == "C4" else fcn.C3_SHAPE
+    seed_name = "C4-rank0" if cfg == "C4" else "C3"
     fams = fcn.assemble_families(shape, fcn.generate_trace(shape, seed=DATA_SEED))
     relu_ctx = api.Context(0, torch.cuda.Stream())
     mm = [api.Context(0, torch.cuda.Stream()) for _ in range(3)]
     for c in [ctx] + mm:
         c.set_sm_budget(37)
-    g = dfcn.prove_window(ctx, fs_seed("C4-rank0"), fcn.fcn_header(shape), dfcn.upload_families(fams),
+    g = dfcn.prove_window(ctx, fs_seed(seed_name), fcn.fcn_header(shape), dfcn.upload_families(fams),
                           relu_ctx=relu_ctx, mm_ctxs=mm)
     ctx.set_sm_budget(0)
-    W = O.Transcript(fs_seed("C4-rank0"))
+    W = O.Transcript(fs_seed(seed_name))
     W.absorb("fcn/hdr", fcn.fcn_header(shape))
     forks = []
     for f in fams:
@@ -453,6 +456,30 @@ def test_c4_window_full_size_vs_oracle(ctx, O):
     for T in forks:
         W.absorb("fcn/join", T.state())
     assert g[-1]["window_state"] == W.state()
+
+
+def test_c5_bench_size_26_properties(ctx, O):
+    """C5 at m = 26 (the c5_sharded size of every bench line), too large for a full oracle run: the
+    oracle verifier replays the transcript, checks every round identity, and checks the finals
+    against brute-force MLEs of A and B at r; the claim is checked against its brute-force sum."""
+    import os
+    from oracle import drivers
+    from paper_2307_16273_b200 import api
+    O.set_threads(len(os.sched_getaffinity(0)))
+    m = 26
+    A, B = drivers.c5_inputs(m)
+    tr = api.Transcript(ctx, fs_seed(f"C5-m{m}"))
+    tr.absorb("c5/hdr", m.to_bytes(4, "little"))
+    w = tr.challenges("c5/w", m)
+    g = api.sumcheck_prove(ctx, tr, m, m, [dev(A), dev(B)], w)
+    ot = O.Transcript(fs_seed(f"C5-m{m}"))
+    ot.absorb("c5/hdr", m.to_bytes(4, "little"))
+    assert ot.challenges("c5/w", m) == w
+    assert g["finals"] == [O.mle_i32(A, g["r"]), O.mle_i32(B, g["r"])]
+    assert O.sumcheck_verify(ot, m, m, 2, w, g["claim"], g["msgs"], g["finals"]) == 0
+    assert ot.state() == tr.state()
+    # the claim: sum_x eq(w, x) A(x) B(x) = MLE of the integer product table at w
+    assert g["claim"] == O.mle_i32((A.astype(np.int64) * B).astype(np.int32), w)   # |A B| < 2^30
 
 
 @pytest.mark.parametrize("m", [22])
