@@ -383,15 +383,20 @@ void relu_bitsums_gram(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint32_
     const uint32_t lo_n = 1u << lo_bits;
     GramArgs ga;
     memset(&ga, 0, sizeof ga);
-    for (int x = 0; x < 5; x++) {
-        fr_t* lo = s.alloc<fr_t>(lo_n);
+    fr_t* los[5];
+    EqJob jobs[10];
+    for (int x = 0; x < 5; x++) {   // the ten eq tables in two launches
+        los[x] = s.alloc<fr_t>(lo_n);
         fr_t* hi = s.alloc<fr_t>(1ull << hi_bits);
-        eq_table_r2_dev(ctx, u_i[x], lo_bits, lo, s);
-        eq_table_dev(ctx, u_i[x] + lo_bits, hi_bits, nullptr, hi, s);
-        uint8_t* lot = s.alloc<uint8_t>((size_t)(lo_n / GR_CH) * GR_LBLK);
-        ZK_LAUNCH(ctx, k_lo_limbs, grid_for(ctx, lo_n, 256, 4), 256, 0, (const fr_t*)lo, lo_n, lot);
-        ga.LOT[x] = lot;
+        jobs[2 * x] = EqJob{u_i[x], lo_bits, nullptr, 1, los[x]};
+        jobs[2 * x + 1] = EqJob{u_i[x] + lo_bits, hi_bits, nullptr, 0, hi};
         ga.HI[x] = hi;
+    }
+    eq_tables_batch(ctx, 10, jobs, s);
+    for (int x = 0; x < 5; x++) {
+        uint8_t* lot = s.alloc<uint8_t>((size_t)(lo_n / GR_CH) * GR_LBLK);
+        ZK_LAUNCH(ctx, k_lo_limbs, grid_for(ctx, lo_n, 256, 4), 256, 0, (const fr_t*)los[x], lo_n, lot);
+        ga.LOT[x] = lot;
     }
     ga.Z = Z;
     ga.GA = GA;

@@ -1262,10 +1262,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     tr_challenges_dev(tr, "relu/uGZ", logD, U + 3 * logD, nullptr);
     // claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) with A, G_Z formed on the fly (Lemma 1)
     fr_t* claims = s.alloc<fr_t>(4);
-    mle_i32_plain(ctx, Z, logD, U, claims, s);
-    mle_i32_relu(ctx, 0, Z, GA, R, logD, U + logD, claims + 1, s);
-    mle_i32_plain(ctx, GA, logD, U + 2 * logD, claims + 2, s);
-    mle_i32_relu(ctx, 1, Z, GA, R, logD, U + 3 * logD, claims + 3, s);
+    mle_i32_relu4(ctx, Z, GA, R, logD, U, claims, s);
     ZK_LAUNCH(ctx, k_tr_absorb_frs, 1, 32, 0, tr->d_st, make_tag("relu/claims"), (const fr_t*)claims, 4u, proof + 12);
     // r, r', u_bin
     fr_t* rr = s.alloc<fr_t>(2);
@@ -1371,20 +1368,23 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     const uint32_t H = logD - hb;
     fr_t* HIs[6];
     fr_t* LOs[5][2];
+    EqJob jobs[11];
+    uint32_t nj = 0;
     for (int x = 0; x < 5; x++) {
         HIs[x] = s.alloc<fr_t>(1ull << hb);
-        eq_table_dev(ctx, u_i[x] + H, hb, kappa + (x < 4 ? x : 4), HIs[x], s);
+        jobs[nj++] = EqJob{u_i[x] + H, hb, kappa + (x < 4 ? x : 4), 0, HIs[x]};
         if (x == 4) {   // E_b' = r' E_b for the a1 side of the AIVP
             HIs[5] = s.alloc<fr_t>(1ull << hb);
-            eq_table_dev(ctx, u_i[4] + H, hb, kappa + 7, HIs[5], s);
+            jobs[nj++] = EqJob{u_i[4] + H, hb, kappa + 7, 0, HIs[5]};
         }
         LOs[x][0] = LOs[x][1] = nullptr;
         if (H) {
             LOs[x][0] = s.alloc<fr_t>(1ull << H);
             LOs[x][1] = s.alloc<fr_t>(1ull << (H - 1));
-            eq_table_dev(ctx, u_i[x], H, nullptr, LOs[x][0], s);
+            jobs[nj++] = EqJob{u_i[x], H, nullptr, 0, LOs[x][0]};
         }
     }
+    eq_tables_batch(ctx, nj, jobs, s);   // 11 tables in two launches
     fr_t* buf[2][3];
     for (int k = 0; k < 3; k++) {
         buf[1][k] = s.alloc<fr_t>(D >> 1);

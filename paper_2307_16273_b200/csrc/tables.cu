@@ -103,6 +103,97 @@ void eq_table_dev(zk_ctx* ctx, const fr_t* d_u, uint32_t k, const fr_t* d_scale,
 
 __global__ void k_set_const(fr_t* out, fr_t v) { fr_store(out, v); }
 
+// ---------------------------------------------------------------- batched eq tables
+// Phase 1: every direct table of the batch (the small tables whole, the large ones' lo and hi halves)
+// in one launch; phase 2: every lo x hi combine in one launch.  Entry x of part p belongs to the part
+// whose [start, start + 2^k) range contains the flat index (binary search over <= 2 EQB_MAX parts).
+struct EqParts {
+    uint32_t n;
+    uint64_t start[2 * EQB_MAX + 1];
+    const fr_t* u[2 * EQB_MAX];
+    const fr_t* scale[2 * EQB_MAX];
+    fr_t* out[2 * EQB_MAX];
+    uint32_t k[2 * EQB_MAX];
+    int r2[2 * EQB_MAX];   // scale is R (the "double Montgomery" tables of the lazy int32 dot products)
+};
+__global__ void k_eq_direct_batch(EqParts P) {
+    const uint64_t total = P.start[P.n];
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = P.n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (P.start[mid] <= g) lo = mid; else hi = mid;
+        }
+        const uint64_t x = g - P.start[lo];
+        fr_t acc = P.r2[lo] ? ZK_R2 : (P.scale[lo] ? fr_load(P.scale[lo]) : fr_one());
+        for (uint32_t t = 0; t < P.k[lo]; t++) {
+            const fr_t ut = fr_load(&P.u[lo][t]);
+            acc = fr_mul(acc, ((x >> t) & 1) ? ut : fr_sub(fr_one(), ut));
+        }
+        fr_store(&P.out[lo][x], acc);
+    }
+}
+struct EqCombines {
+    uint32_t n;
+    uint64_t start[EQB_MAX + 1];
+    const fr_t* lo[EQB_MAX];
+    const fr_t* hi[EQB_MAX];
+    fr_t* out[EQB_MAX];
+    uint32_t klo[EQB_MAX];
+};
+__global__ void k_eq_combine_batch(EqCombines C) {
+    const uint64_t total = C.start[C.n];
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = C.n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (C.start[mid] <= g) lo = mid; else hi = mid;
+        }
+        const uint64_t x = g - C.start[lo];
+        const uint64_t mask = (1ull << C.klo[lo]) - 1;
+        fr_store(&C.out[lo][x], fr_mul(fr_load(&C.lo[lo][x & mask]), fr_load(&C.hi[lo][x >> C.klo[lo]])));
+    }
+}
+
+void eq_tables_batch(zk_ctx* ctx, uint32_t n, const EqJob* jobs, Scratch& s) {
+    for (uint32_t b0 = 0; b0 < n; b0 += EQB_MAX) {
+        const uint32_t nb = n - b0 < EQB_MAX ? n - b0 : EQB_MAX;
+        EqParts P;
+        EqCombines C;
+        memset(&P, 0, sizeof P);
+        memset(&C, 0, sizeof C);
+        for (uint32_t i = 0; i < nb; i++) {
+            const EqJob& J = jobs[b0 + i];
+            auto part = [&](const fr_t* u, uint32_t k, const fr_t* sc, int r2, fr_t* out) {
+                P.u[P.n] = u;
+                P.k[P.n] = k;
+                P.scale[P.n] = sc;
+                P.r2[P.n] = r2;
+                P.out[P.n] = out;
+                P.start[P.n + 1] = P.start[P.n] + (1ull << k);
+                P.n++;
+            };
+            if (J.k <= 10) {
+                part(J.u, J.k, J.scale, J.r2, J.out);
+            } else {
+                const uint32_t klo = (J.k + 1) / 2, khi = J.k - klo;
+                fr_t* lo = s.alloc<fr_t>(1ull << klo);
+                fr_t* hi = s.alloc<fr_t>(1ull << khi);
+                part(J.u, klo, nullptr, 0, lo);
+                part(J.u + klo, khi, J.scale, J.r2, hi);
+                C.lo[C.n] = lo;
+                C.hi[C.n] = hi;
+                C.out[C.n] = J.out;
+                C.klo[C.n] = klo;
+                C.start[C.n + 1] = C.start[C.n] + (1ull << J.k);
+                C.n++;
+            }
+        }
+        ZK_LAUNCH(ctx, k_eq_direct_batch, grid_for(ctx, P.start[P.n], 128, 8), 128, 0, P);
+        if (C.n) ZK_LAUNCH(ctx, k_eq_combine_batch, grid_for(ctx, C.start[C.n], 256, 8), 256, 0, C);
+    }
+}
+
 void eq_table_r2_dev(zk_ctx* ctx, const fr_t* d_u, uint32_t k, fr_t* d_out, Scratch& s) {
     fr_t* sc = s.alloc<fr_t>(1);
     ZK_LAUNCH(ctx, k_set_const, 1, 1, 0, sc, ZK_R2);   // the Montgomery form of the field element R
@@ -172,6 +263,38 @@ void mle_i32_relu(zk_ctx* ctx, int kind, const int32_t* d_z, const int32_t* d_g,
         mle_i32_generic(ctx, LoadReluA{d_z, R}, m, d_u, d_out, s);
     else
         mle_i32_generic(ctx, LoadReluGZ{d_z, d_g, R}, m, d_u, d_out, s);
+}
+
+// The four zkReLU claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) (A, G_Z formed on the fly, Lemma 1):
+// the eight eq tables in one batch, then a row-dot and a dot per claim.
+void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,
+                   fr_t* d_out, Scratch& s) {
+    uint32_t lo, hi;
+    split_bits(m, lo, hi);
+    fr_t* E2[4];
+    fr_t* H[4];
+    EqJob jobs[8];
+    uint32_t nj = 0;
+    for (int c = 0; c < 4; c++) {
+        E2[c] = s.alloc<fr_t>(1ull << lo);
+        jobs[nj++] = EqJob{d_U + (uint64_t)c * m, lo, nullptr, 1, E2[c]};
+        H[c] = nullptr;
+        if (hi) {
+            H[c] = s.alloc<fr_t>(1ull << hi);
+            jobs[nj++] = EqJob{d_U + (uint64_t)c * m + lo, hi, nullptr, 0, H[c]};
+        }
+    }
+    eq_tables_batch(ctx, nj, jobs, s);
+    const uint64_t rows = 1ull << hi;
+    const unsigned int g = grid_for(ctx, rows * 32, 256, 8);
+    for (int c = 0; c < 4; c++) {
+        fr_t* V = hi ? s.alloc<fr_t>(rows) : d_out + c;
+        if (c == 0) ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, g, 256, 0, LoadPlain{d_z}, rows, 1u << lo, (const fr_t*)E2[c], V, rows, hi, (uint64_t)1);
+        if (c == 1) ZK_LAUNCH(ctx, k_rowdot_i32<LoadReluA>, g, 256, 0, LoadReluA{d_z, R}, rows, 1u << lo, (const fr_t*)E2[c], V, rows, hi, (uint64_t)1);
+        if (c == 2) ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, g, 256, 0, LoadPlain{d_g}, rows, 1u << lo, (const fr_t*)E2[c], V, rows, hi, (uint64_t)1);
+        if (c == 3) ZK_LAUNCH(ctx, k_rowdot_i32<LoadReluGZ>, g, 256, 0, LoadReluGZ{d_z, d_g, R}, rows, 1u << lo, (const fr_t*)E2[c], V, rows, hi, (uint64_t)1);
+        if (hi) dot_dev(ctx, V, H[c], rows, d_out + c, s);
+    }
 }
 
 void mle_fr_dev(zk_ctx* ctx, const fr_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s) {

@@ -147,9 +147,22 @@ __global__ void k_dot_fr(const fr_t* a, const fr_t* b, uint64_t n, fr_t* partial
 void mle_i32_plain(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s);
 void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ*/, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m,
                   const fr_t* d_u, fr_t* d_out, Scratch& s);
+void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,
+                   fr_t* d_out, Scratch& s);
 void mle_fr_dev(zk_ctx* ctx, const fr_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s);
 // eq table scaled by R (for the lazy accumulators)
 void eq_table_r2_dev(zk_ctx* ctx, const fr_t* d_u, uint32_t k, fr_t* d_out, Scratch& s);
+// Several eq tables in two launches (direct parts, then lo x hi combines): out = scale * beta(u, .)
+// over k variables; r2 = 1: scale = R (Montgomery form of R), as eq_table_r2_dev.
+constexpr uint32_t EQB_MAX = 16;
+struct EqJob {
+    const fr_t* u;
+    uint32_t k;
+    const fr_t* scale;
+    int r2;
+    fr_t* out;
+};
+void eq_tables_batch(zk_ctx* ctx, uint32_t n, const EqJob* jobs, Scratch& s);
 void embed_i32_dev(zk_ctx* ctx, const int32_t* d_in, uint64_t n, fr_t* d_out);
 
 }  // namespace zk
