@@ -240,7 +240,7 @@ def run_ours(args, rank, world, local):
     mm_ctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.mm_streams - 1)]
     if args.mm_streams > 1:
         for c in [ctx] + mm_ctxs:
-            c.set_sm_budget(max(8, 148 // args.mm_streams))
+            c.set_sm_budget(args.mm_budget or max(8, 148 // args.mm_streams))
     ctxs = [ctx] + ([relu_ctx] if relu_ctx else []) + mm_ctxs
     header = fcn.fcn_header(shape)
     seed = fs_seed(f"C4-rank{rank}")
@@ -372,7 +372,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps, "
                                "9 families (F x3, GA x2, GW x3, ReLU D=2^23), one transcript",
                    "updates_per_step": shape.steps, "input_bytes_per_step": in_bytes,
-                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams},
+                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams, "mm_budget": args.mm_budget or max(8, 148 // args.mm_streams)},
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "fcn.prove_window_from_host: pinned host stacks -> HBM per family on a copy stream "
@@ -599,8 +599,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")
-    ap.add_argument("--mm-streams", type=int, default=4,
+    ap.add_argument("--mm-streams", type=int, default=2,
                     help="streams (contexts) the matmul families are spread over, side by side")
+    ap.add_argument("--mm-budget", type=int, default=37,
+                    help="SM budget of each matmul stream's persistent sumcheck grid (0: 148 / mm-streams)")
     ap.add_argument("--prof", default="dominant", choices=["dominant", "inline", "separate"],
                     help="where per-kernel CUDA-event durations come from (see roofline.durations)")
     ap.add_argument("--profile-mode", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")
