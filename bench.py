@@ -265,13 +265,13 @@ def run_ours(args, rank, world, local):
         """K windows, one stream, CUDA events around every launch: the per-kernel table."""
         prof_on(None)
         for _ in range(args.steps):
-            dfcn.enqueue_window(ctx, seed, header, dev_fams)
+            dfcn.enqueue_window(ctx, seed, header, dev_fams, merge_aux=args.merge_aux)
         torch.cuda.synchronize()
         return prof_off()
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
+            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
         torch.cuda.synchronize()
         # kernel table first (outside the timed region) -> the dominant kernel
         prof_table = profiled_pass() if args.prof == "dominant" else None
@@ -287,7 +287,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs) for _ in range(args.steps)]
+        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux) for _ in range(args.steps)]
         ev1.record(stream)   # each window joins the zkReLU stream back into this one before its end
         torch.cuda.synchronize()
         res = dfcn.collect_window(*pending[-1])   # outputs stay in HBM until here (outside the timed region)
@@ -302,6 +302,22 @@ def run_ours(args, rank, world, local):
             prof_table = profiled_pass()
             prof_live = prof_table
     prof = prof_table
+    n1 = None
+    if not args.merge_aux and not args.profile_mode:
+        # SURVEY 8(f) N1 beside the headline: the same windows with every zkReLU family ending in the
+        # aux-claim merge (D21), timed the same way
+        with torch.cuda.stream(stream):
+            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pend = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=True)
+                    for _ in range(args.steps)]
+            e1.record(stream)
+            torch.cuda.synchronize()
+            del pend
+        n1 = {"ms_per_step": max_over_ranks(e0.elapsed_time(e1), world) / args.steps,
+              "what": "the same window with the zkReLU aux-claim merge (one aux claim per ReLU family)"}
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
     updates = world * args.steps * shape.steps
@@ -321,7 +337,7 @@ def run_ours(args, rank, world, local):
     copy_stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         if e2e_steps:   # one untimed end-to-end window: allocator warm-up for the upload buffers
-            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
+            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -329,11 +345,11 @@ def run_ours(args, rank, world, local):
         for _ in range(e2e_steps):
             # pinned host -> HBM per family on a copy stream, overlapped with the earlier families'
             # proofs; proof bytes come back to the host
-            out = dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
+            out = dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     h2d = sum(t.numel() * t.element_size() for t in pinned.values())   # distinct stacks, copied once each
-    d2h = dfcn.window_out_bytes(dev_fams) + 4                           # proofs, points, states + range flag
+    d2h = dfcn.window_out_bytes(dev_fams, bool(args.merge_aux)) + 4     # proofs, points, states + range flag
     e2e_value = e2e_s / (world * e2e_steps * shape.steps) if e2e_steps else None
     # ---- roofline of the dominant kernel (live CUDA-event durations over the timed region)
     per_step = {k: (n / args.steps, t / args.steps) for k, (n, t) in prof.items()}
@@ -372,12 +388,13 @@ def run_ours(args, rank, world, local):
         "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps, "
                                "9 families (F x3, GA x2, GW x3, ReLU D=2^23), one transcript",
                    "updates_per_step": shape.steps, "input_bytes_per_step": in_bytes,
-                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams, "mm_budget": args.mm_budget or max(8, 148 // args.mm_streams)},
+                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams, "mm_budget": args.mm_budget or max(8, 148 // args.mm_streams), "relu_aux_merge": bool(args.merge_aux)},
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "fcn.prove_window_from_host: pinned host stacks -> HBM per family on a copy stream "
                         "(shared stacks once), overlapped with the proofs; proofs back to the host"},
         "roofline": rf,
+        "n1_relu_aux_merge": n1,
         "kernels_ms_per_step": {k: round(t, 4) for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:16]},
         "kernel_launches_per_step": {k: n for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:16]},
         "kernel_ms_total_per_step": round(total_kernel_ms, 4),
@@ -601,6 +618,8 @@ def main():
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")
     ap.add_argument("--mm-streams", type=int, default=2,
                     help="streams (contexts) the matmul families are spread over, side by side")
+    ap.add_argument("--merge-aux", type=int, default=0, choices=[0, 1],
+                    help="1: every zkReLU family ends with the aux-claim merge (P:L470, DESIGN.md D21)")
     ap.add_argument("--mm-budget", type=int, default=37,
                     help="SM budget of each matmul stream's persistent sumcheck grid (0: 148 / mm-streams)")
     ap.add_argument("--prof", default="dominant", choices=["dominant", "inline", "separate"],

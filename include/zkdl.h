@@ -166,6 +166,12 @@ zk_status zk_reindex_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_X, u
 zk_status zk_relu_merge(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
                         uint32_t Q, uint32_t R, const zk_fr* point, const zk_fr* finals, uint8_t* proof,
                         uint64_t* proof_len, zk_fr* point_out, zk_fr* merged_out);
+/* zk_relu_merge_dev: the same merge, asynchronous, reading the point and finals from d_relu_out (the
+ * zk_relu_prove_dev output of the same statement, device) and writing d_out = merge sumcheck proof
+ * (zk_sumcheck_prove layout; finals = merged claim, W~(r)) | pad to 16 bytes | point (logB + 1
+ * elements, canonical); d_out 16-byte aligned; d_out == NULL with out_len != NULL is a size query. */
+zk_status zk_relu_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                            uint32_t Q, uint32_t R, const uint8_t* d_relu_out, uint8_t* d_out, uint64_t* out_len);
 
 /* ------------------------------------------- sharded product sumcheck (SURVEY §8(e), G = 2^s devices)
  * Rank g (of world = G, a power of two) holds entries [g 2^L, (g+1) 2^L) of every table, L = m - s:

@@ -84,7 +84,7 @@ def c5_prove(m: int):
     return res
 
 
-def fcn_prove(shape, families, seed_name: str, only=None):
+def fcn_prove(shape, families, seed_name: str, only=None, merge_aux: bool = False):
     """D3d: window transcript W: "fcn/hdr"; per family (in order) "fcn/fam" <name> and a fork: the family
     transcript T_f is seeded with the canonical bytes of W's challenge "fcn/fork"; each family's protocol
     runs on its own T_f; finally W absorbs "fcn/join" <T_f state> for every family (in order).
@@ -104,6 +104,8 @@ def fcn_prove(shape, families, seed_name: str, only=None):
             res = O.matmul_prove(T, f.A, f.B, f.transA, f.transB)
         else:
             res = O.relu_prove(T, f.Z, f.GA, f.Q, f.R)
+            if merge_aux:   # DESIGN.md D21: the aux-claim merge on the family transcript
+                res["merge"] = O.relu_merge(T, f.Z, f.GA, f.Q, f.R, res["point"], res["finals"])
         res["name"] = f.name
         res["state"] = T.state()
         out.append(res)

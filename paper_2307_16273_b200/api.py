@@ -442,3 +442,32 @@ def relu_merge(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, 
     res["r"] = _ints(pt, m)
     res["proof"] = proof.raw[:plen.value]
     return res
+
+
+def relu_merge_len(Q: int, R: int) -> int:
+    m = relu_logB(Q, R) + 1
+    return _a16(12 + 32 + 96 * m + 64) + 32 * m
+
+
+def relu_merge_dev(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, Q: int, R: int,
+                   relu_out: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_relu_merge_dev: the aux-claim merge from a zk_relu_prove_dev output, into a device buffer."""
+    logD = _log2(Z.numel())
+    n = relu_merge_len(Q, R)
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=Z.device)
+    assert out.dtype == torch.uint8 and out.numel() >= n and out.is_contiguous()
+    ln = ctypes.c_uint64(out.numel())
+    ctx.check(lib().zk_relu_merge_dev(ctx.h, tr.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), logD, Q, R,
+                                      relu_out.data_ptr(), out.data_ptr(), ctypes.byref(ln)))
+    return out
+
+
+def parse_relu_merge_out(raw: bytes, Q: int, R: int) -> dict:
+    m = relu_logB(Q, R) + 1
+    plen = 12 + 32 + 96 * m + 64
+    res = parse_sumcheck_proof(raw[:plen])
+    res["proof"] = raw[:plen]
+    o = _a16(plen)
+    res["r"] = [int.from_bytes(raw[o + 32 * i:o + 32 * i + 32], "little") for i in range(m)]
+    return res

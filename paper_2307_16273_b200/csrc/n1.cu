@@ -70,50 +70,118 @@ __device__ __forceinline__ fr_t lazy_finish9(const uint32_t (&a)[9]) {
     return fr_mul(fr_redc_wide(w), ZK_R2);
 }
 
-// T(s, j) partial sums: each warp walks chunks of 32 consecutive entries; lane l loads entry
-// i0 + l (eq weight, both words), then for each of the 32 entries the words and the weight are
-// broadcast and lane j adds the weight when bit j is set.  Block partials (2 x 32 Fr) to out.
-__global__ void __launch_bounds__(256) k_aux_colsum(const int32_t* Z, const int32_t* GA, const fr_t* E, uint64_t D,
-                                                    uint32_t qr_mask, fr_t* partials) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// T(s, j) partial sums without a 2^logD eq table: beta(v, i) = LO[i mod 2^lo] * HI[i >> lo], one block
+// per HI value h.  Each warp stages 32 entries (LO weight, both words) in shared memory, then lane j
+// walks them (broadcast reads) and adds the LO weight lazily (9-limb, no reduction) when bit j is set;
+// the lazy sums are closed once per warp, added over the block and multiplied by HI[h] once.
+__global__ void __launch_bounds__(256) k_aux_colsum(const int32_t* Z, const int32_t* GA, const fr_t* LO,
+                                                    const fr_t* HI, uint32_t lo, uint32_t qr_mask, fr_t* partials) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ fr_t se[8][32];
+    __shared__ uint2 sw[8][32];
     uint32_t az[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, ag[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; c * 32 < D; c += nwarps) {
-        const uint64_t i = c * 32 + lane;
-        const bool ok = i < D;
-        const uint32_t zw = ok ? ((uint32_t)__ldg(Z + i) & qr_mask) : 0u;
-        const uint32_t gw = ok ? ((uint32_t)__ldg(GA + i) & qr_mask) : 0u;
-        const fr_t e = ok ? fr_load(&E[i]) : fr_zero();
+    const uint64_t base = (uint64_t)blockIdx.x << lo, n = 1ull << lo;
+    for (uint64_t c = (uint64_t)wid * 32; c < n; c += (uint64_t)nw * 32) {
+        const uint64_t x = c + lane;
+        if (x < n) {
+            se[wid][lane] = fr_load(&LO[x]);
+            sw[wid][lane] = make_uint2((uint32_t)__ldg(Z + base + x) & qr_mask, (uint32_t)__ldg(GA + base + x) & qr_mask);
+        } else {
+            se[wid][lane] = fr_zero();
+            sw[wid][lane] = make_uint2(0u, 0u);
+        }
+        __syncwarp();
 #pragma unroll 4
         for (int k = 0; k < 32; k++) {
-            const uint32_t z = __shfl_sync(0xffffffffu, zw, k), g = __shfl_sync(0xffffffffu, gw, k);
-            fr_t ek;
-#pragma unroll
-            for (int l = 0; l < 8; l++) ek.v[l] = __shfl_sync(0xffffffffu, e.v[l], k);
-            if ((z >> lane) & 1) lazy_add9(az, ek);
-            if ((g >> lane) & 1) lazy_add9(ag, ek);
+            const uint2 w = sw[wid][k];
+            if (((w.x | w.y) >> lane) & 1) {
+                const fr_t e = se[wid][k];
+                if ((w.x >> lane) & 1) lazy_add9(az, e);
+                if ((w.y >> lane) & 1) lazy_add9(ag, e);
+            }
         }
+        __syncwarp();
     }
     __shared__ fr_t sm[8][64];
     sm[wid][lane] = lazy_finish9(az);
     sm[wid][32 + lane] = lazy_finish9(ag);
     __syncthreads();
     if (threadIdx.x < 64) {
-        fr_t s = sm[0][threadIdx.x];
-        for (int w = 1; w < (int)(blockDim.x >> 5); w++) s = fr_add(s, sm[w][threadIdx.x]);
-        fr_store(&partials[blockIdx.x * 64 + threadIdx.x], s);
+        fr_t acc = sm[0][threadIdx.x];
+        for (int w = 1; w < nw; w++) acc = fr_add(acc, sm[w][threadIdx.x]);
+        fr_store(&partials[blockIdx.x * 64ull + threadIdx.x], fr_mul(acc, fr_load(&HI[blockIdx.x])));
     }
 }
 
-// T[s * B + j] = sum over blocks (j < 32; zero for 32 <= j < B)
+// T[s * B + j] = sum over blocks (j < 32; zero for 32 <= j < B): 4 warps per output cell
 __global__ void k_aux_colsum_reduce(const fr_t* partials, uint32_t nblocks, uint32_t B, fr_t* T) {
-    const uint32_t t = threadIdx.x;
-    if (t >= 2 * B) return;
-    const uint32_t s = t / B, j = t % B;
+    const uint32_t cell = blockIdx.x, s = cell / B, j = cell % B;
+    __shared__ fr_t sm[4];
     fr_t acc = fr_zero();
     if (j < 32)
-        for (uint32_t b = 0; b < nblocks; b++) acc = fr_add(acc, fr_load(&partials[b * 64 + s * 32 + j]));
-    fr_store(&T[t], acc);
+        for (uint32_t b = threadIdx.x; b < nblocks; b += blockDim.x) acc = fr_add(acc, fr_load(&partials[b * 64ull + s * 32 + j]));
+    for (int off = 16; off > 0; off >>= 1) acc = fr_add(acc, fr_shfl_down(acc, off));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < blockDim.x / 32; w++) acc = fr_add(acc, sm[w]);
+        fr_store(&T[cell], acc);
+    }
+}
+
+// canonical 32-byte encodings (already checked < p by the producer) -> Montgomery
+__global__ void k_canon_to_mont(const uint8_t* in, uint32_t n, fr_t* out) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        fr_t x;
+        for (int l = 0; l < 8; l++)
+            x.v[l] = (uint32_t)in[32 * i + 4 * l] | ((uint32_t)in[32 * i + 4 * l + 1] << 8) |
+                     ((uint32_t)in[32 * i + 4 * l + 2] << 16) | ((uint32_t)in[32 * i + 4 * l + 3] << 24);
+        fr_store(&out[i], fr_from_canonical(x));
+    }
+}
+
+// The merge (D21) from device-resident point and finals (Montgomery); proof and point to device memory.
+static void relu_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                           uint32_t Q, uint32_t R, const fr_t* pt, const fr_t* f, uint8_t* d_proof, uint8_t* d_point,
+                           Scratch& s) {
+    const uint32_t QR = Q + R;
+    uint32_t logB = 0;
+    while ((1u << logB) < QR) logB++;
+    const uint32_t B = 1u << logB, m = logB + 1;
+    const uint64_t D = 1ull << logD;
+    fr_t* rho = s.alloc<fr_t>(1);
+    tr_challenges_dev(tr, "relu/merge", 1, rho, nullptr);
+    ScStatement S;
+    memset(&S, 0, sizeof S);
+    S.m = m;
+    S.n_eq = 0;
+    S.K = 2;
+    S.d_claim = s.alloc<fr_t>(1);
+    S.claim_given = true;
+    // beta(v, i) = LO[i mod 2^lo] HI[i >> lo]: 2^lo entries per block of k_aux_colsum
+    const uint32_t lo = logD < 12 ? logD : 12, hi = logD - lo;
+    fr_t* Ew = s.alloc<fr_t>(B);
+    fr_t* LO = s.alloc<fr_t>(1ull << lo);
+    fr_t* HI = s.alloc<fr_t>(1ull << hi);
+    EqJob jobs[3] = {EqJob{pt, logB, nullptr, 0, Ew}, EqJob{pt + logB, lo, nullptr, 0, LO},
+                     EqJob{pt + logB + lo, hi, nullptr, 0, HI}};
+    eq_tables_batch(ctx, 3, jobs, s);
+    fr_t* W = s.alloc<fr_t>(2 * B);
+    ZK_LAUNCH(ctx, k_merge_setup, 1, 64, 0, f, (const fr_t*)rho, (const fr_t*)Ew, B, QR, S.d_claim, W);
+    // T(s, j) = sum_i beta(v, i) bit_j(word_s[i])
+    const unsigned int grid = 1u << hi;
+    fr_t* part = s.alloc<fr_t>((size_t)grid * 64);
+    const uint32_t qr_mask = QR >= 32 ? 0xffffffffu : ((1u << QR) - 1);
+    ZK_LAUNCH(ctx, k_aux_colsum, grid, 256, 0, d_Z, d_GA, (const fr_t*)LO, (const fr_t*)HI, lo, qr_mask, part);
+    fr_t* T = s.alloc<fr_t>(2 * B);
+    ZK_LAUNCH(ctx, k_aux_colsum_reduce, 2 * B, 128, 0, (const fr_t*)part, grid, B, T);
+    (void)D;
+    S.tables[0] = T;
+    S.tables[1] = W;
+    S.d_proof = d_proof;
+    S.d_r = s.alloc<fr_t>(m);
+    S.d_point = d_point;
+    sumcheck_prove_dev(ctx, tr, S, s);
 }
 
 static void copy_proof_out(zk_ctx* ctx, const ScStatement& S, uint32_t m, uint8_t* proof, zk_fr* point_out,
@@ -243,44 +311,50 @@ zk_status zk_relu_merge(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
     ZK_REQUIRE(Q >= 1 && R >= 1 && QR <= 32 && logD >= 1 && logD <= 32, ZK_ERR_ARG, "bad zkReLU shape");
     uint32_t logB = 0;
     while ((1u << logB) < QR) logB++;
-    const uint32_t B = 1u << logB, m = logB + 1;
+    const uint32_t m = logB + 1;
     if (proof_len_check(sumcheck_proof_len(m, 2), proof, proof_len)) return ZK_OK;
-    const uint64_t D = 1ull << logD;
     Scratch s(ctx);
     fr_t* pt = s.alloc<fr_t>(logB + logD);
     upload_points(ctx, point, logB + logD, pt, s);
     fr_t* f = s.alloc<fr_t>(3);
     upload_points(ctx, finals, 3, f, s);
-    // rho ("relu/merge"), claim, W
-    fr_t* rho = s.alloc<fr_t>(1);
-    tr_challenges_dev(tr, "relu/merge", 1, rho, nullptr);
-    fr_t* Ew = s.alloc<fr_t>(B);
-    eq_table_dev(ctx, pt, logB, nullptr, Ew, s);
     ScStatement S;
     memset(&S, 0, sizeof S);
-    S.m = m;
-    S.n_eq = 0;
-    S.K = 2;
-    S.d_claim = s.alloc<fr_t>(1);
-    S.claim_given = true;
-    fr_t* W = s.alloc<fr_t>(2 * B);
-    ZK_LAUNCH(ctx, k_merge_setup, 1, 64, 0, (const fr_t*)f, (const fr_t*)rho, (const fr_t*)Ew, B, QR, S.d_claim, W);
-    // T(s, j) = sum_i beta(v, i) bit_j(word_s[i])
-    fr_t* Ev = s.alloc<fr_t>(D);
-    eq_table_dev(ctx, pt + logB, logD, nullptr, Ev, s);
-    const unsigned int grid = grid_for(ctx, D, 256, 4);
-    fr_t* part = s.alloc<fr_t>((size_t)grid * 64);
-    const uint32_t qr_mask = QR >= 32 ? 0xffffffffu : ((1u << QR) - 1);
-    ZK_LAUNCH(ctx, k_aux_colsum, grid, 256, 0, d_Z, d_GA, (const fr_t*)Ev, D, qr_mask, part);
-    fr_t* T = s.alloc<fr_t>(2 * B);
-    ZK_LAUNCH(ctx, k_aux_colsum_reduce, 1, 64, 0, (const fr_t*)part, grid, B, T);
-    S.tables[0] = T;
-    S.tables[1] = W;
     S.d_proof = s.alloc<uint8_t>(sumcheck_proof_len(m, 2));
-    S.d_r = s.alloc<fr_t>(m);
     S.d_point = s.alloc<uint8_t>(32ull * m);
-    sumcheck_prove_dev(ctx, tr, S, s);
+    relu_merge_dev(ctx, tr, d_Z, d_GA, logD, Q, R, pt, f, S.d_proof, S.d_point, s);
     copy_proof_out(ctx, S, m, proof, point_out, merged_out);
+    N1_END(ctx)
+}
+
+zk_status zk_relu_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                            uint32_t Q, uint32_t R, const uint8_t* d_relu_out, uint8_t* d_out, uint64_t* out_len) {
+    N1_BEGIN(ctx)
+    ZK_REQUIRE(tr && d_Z && d_GA && d_relu_out, ZK_ERR_ARG, "null argument");
+    const uint32_t QR = Q + R;
+    ZK_REQUIRE(Q >= 1 && R >= 1 && QR <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
+    uint32_t logB = 0;
+    while ((1u << logB) < QR) logB++;
+    const uint32_t m = logB + 1;
+    const uint64_t plen = sumcheck_proof_len(m, 2), off_pt = (plen + 15) & ~15ull;
+    if (out_len) {
+        const bool query = !d_out;
+        if (d_out && *out_len < off_pt + 32ull * m) {
+            *out_len = off_pt + 32ull * m;
+            throw ZkError{ZK_ERR_ARG, "output buffer too small"};
+        }
+        *out_len = off_pt + 32ull * m;
+        if (query) return ZK_OK;
+    }
+    ZK_REQUIRE(d_out && ((uintptr_t)d_out & 15) == 0, ZK_ERR_ARG, "d_out must be 16-byte aligned");
+    // the zkReLU output (zk_relu_prove_dev layout): proof | pad | point; its finals end the proof
+    const uint64_t rplen = 12 + 128 + 128ull * (logB + logD) + 96, roff = (rplen + 15) & ~15ull;
+    Scratch s(ctx);
+    fr_t* pt = s.alloc<fr_t>(logB + logD);
+    fr_t* f = s.alloc<fr_t>(3);
+    ZK_LAUNCH(ctx, k_canon_to_mont, 1, 64, 0, d_relu_out + roff, logB + logD, pt);
+    ZK_LAUNCH(ctx, k_canon_to_mont, 1, 64, 0, d_relu_out + rplen - 96, 3u, f);
+    relu_merge_dev(ctx, tr, d_Z, d_GA, logD, Q, R, pt, f, d_out, d_out + off_pt, s);
     N1_END(ctx)
 }
 

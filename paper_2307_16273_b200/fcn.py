@@ -57,21 +57,24 @@ def upload_families(families, device="cuda", pin: bool = False) -> list:
     return out
 
 
-def _layout(f: DeviceFamily):
+def _layout(f: DeviceFamily, merge_aux: bool = False):
     if f.kind == "matmul":
         logs = api._mm_logs(f.A, f.B, f.trans_a, f.trans_b)
         return logs, api.matmul_prove_len(logs)
     logD = api._log2(f.Z.numel())
-    return logD, api.relu_prove_len(logD, f.Q, f.R)
+    n = api.relu_prove_len(logD, f.Q, f.R)
+    if merge_aux:   # the aux-claim merge output follows at the next 16-byte offset
+        n = api._a16(n) + api.relu_merge_len(f.Q, f.R)
+    return logD, n
 
 
 def _slot(n: int) -> int:
     return (n + 32 + 255) & ~255   # family output + 32-byte state, every family 256-byte aligned
 
 
-def window_out_bytes(families: list) -> int:
+def window_out_bytes(families: list, merge_aux: bool = False) -> int:
     """Size of a window's device output buffer (what collect_window copies back)."""
-    return sum(_slot(_layout(f)[1]) for f in families) + 256   # + the window transcript's final state
+    return sum(_slot(_layout(f, merge_aux)[1]) for f in families) + 256   # + the window's final state
 
 
 def _family_work(f: DeviceFamily) -> int:
@@ -82,7 +85,7 @@ def _family_work(f: DeviceFamily) -> int:
 
 def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list, ready: list | None = None,
                    relu_ctx: api.Context | None = None, proof_order: list | None = None,
-                   mm_ctxs: list | None = None):
+                   mm_ctxs: list | None = None, merge_aux: bool = False):
     """Enqueue one window's proofs without synchronising.
 
     Transcripts (D3d): the window transcript W absorbs "fcn/hdr", then per family "fcn/fam"
@@ -102,7 +105,7 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
     lay = []
     off = 0
     for f in families:
-        info, n = _layout(f)
+        info, n = _layout(f, merge_aux)
         lay.append((f, info, off, n))
         off += _slot(n)
     out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
@@ -137,7 +140,11 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
         if f.kind == "matmul":
             api.matmul_prove(c, T, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
         else:
-            api.relu_prove_dev(c, T, f.Z, f.GA, f.Q, f.R, flag, out=out[o:o + n])
+            rn = api.relu_prove_len(info, f.Q, f.R)
+            api.relu_prove_dev(c, T, f.Z, f.GA, f.Q, f.R, flag, out=out[o:o + rn])
+            if merge_aux:
+                mo = o + api._a16(rn)
+                api.relu_merge_dev(c, T, f.Z, f.GA, f.Q, f.R, out[o:o + rn], out=out[mo:o + n])
         T.state_dev(out[o + n:o + n + 32])
     for c in side:
         ev = torch.cuda.Event()
@@ -171,9 +178,12 @@ def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
             res = dict(name=f.name, kind="matmul", w=r["w"], u1=r["u1"], u3=r["u3"], claim=r["claim"],
                        msgs=r["msgs"], r=r["r"], finals=r["finals"], proof=r["proof"])
         else:
-            r = api.parse_relu_out(blob, info, f.Q, f.R)
+            rn = api.relu_prove_len(info, f.Q, f.R)
+            r = api.parse_relu_out(blob[:rn], info, f.Q, f.R)
             res = dict(name=f.name, kind="relu", claims=r["claims"], msgs=r["msgs"], point=r["point"],
                        finals=r["finals"], proof=r["proof"])
+            if len(blob) > rn:
+                res["merge"] = api.parse_relu_merge_out(blob[api._a16(rn):], f.Q, f.R)
         res["state"] = raw[o + n:o + n + 32]
         results.append(res)
     end = len(raw) - 256
@@ -182,13 +192,15 @@ def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
 
 
 def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
-                 relu_ctx: api.Context | None = None, mm_ctxs: list | None = None) -> list:
+                 relu_ctx: api.Context | None = None, mm_ctxs: list | None = None, merge_aux: bool = False) -> list:
     """Prove every family of one window (D3d transcripts); returns per-family results."""
-    return collect_window(*enqueue_window(ctx, seed, header, families, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs))
+    return collect_window(*enqueue_window(ctx, seed, header, families, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
+                                          merge_aux=merge_aux))
 
 
 def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None,
-                           relu_ctx: api.Context | None = None, mm_ctxs: list | None = None) -> list:
+                           relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
+                           merge_aux: bool = False) -> list:
     """The user-facing end-to-end call: families given as host (ideally pinned) int32 tensors.
 
     Each family's stacks are copied host->device on `copy_stream` (one is created if None) and its
@@ -230,4 +242,4 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
             fams[i] = g
             ready[i] = ev
     return collect_window(*enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order,
-                                          mm_ctxs=mm_ctxs))
+                                          mm_ctxs=mm_ctxs, merge_aux=merge_aux))

@@ -322,6 +322,40 @@ def test_fcn_tiny_vs_oracle(ctx, O):
     assert [r["proof"] for r in h3] == [r["proof"] for r in g]
 
 
+def test_fcn_tiny_merge_aux_vs_oracle(ctx, O):
+    """The window with the aux-claim merge in every zkReLU family (D21): bit-exact against the oracle
+    driver, and the synchronous zk_relu_merge gives the same bytes as the device-output one."""
+    import torch
+    from oracle import drivers
+    from paper_2307_16273_b200 import api
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=3, width=16, batch=8, din=8, dout=4)
+    trace = fcn.generate_trace(shape, x_bits=4, w_bits=4, y_bits=3)
+    fams = fcn.assemble_families(shape, trace)
+    o = drivers.fcn_prove(shape, fams, "tiny-merge", merge_aux=True)
+    relu_ctx = api.Context(0, torch.cuda.Stream())
+    g = dfcn.prove_window(ctx, fs_seed("tiny-merge"), fcn.fcn_header(shape), dfcn.upload_families(fams),
+                          relu_ctx=relu_ctx, merge_aux=True)
+    for gr, orr in zip(g, o):
+        assert gr["msgs"] == orr["msgs"] and gr["finals"] == orr["finals"] and gr["state"] == orr["state"], gr["name"]
+        if gr["kind"] == "relu":
+            gm, om = gr["merge"], orr["merge"]
+            assert gm["claim"] == om["claim"] and gm["msgs"] == om["msgs"] and gm["finals"] == om["finals"]
+            assert gm["r"] == om["r"]
+    assert g[-1]["window_state"] == o[-1]["window_state"]
+    f = next(f for f in fams if not hasattr(f, "A"))
+    t1 = api.Transcript(ctx, bytes(32))
+    r1 = api.relu_prove(ctx, t1, dev(f.Z), dev(f.GA), f.Q, f.R)
+    m1 = api.relu_merge(ctx, t1, dev(f.Z), dev(f.GA), f.Q, f.R, r1["point"], r1["finals"])
+    t2 = api.Transcript(ctx, bytes(32))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ro = api.relu_prove_dev(ctx, t2, dev(f.Z), dev(f.GA), f.Q, f.R, flag)
+    mo = api.relu_merge_dev(ctx, t2, dev(f.Z), dev(f.GA), f.Q, f.R, ro)
+    pm = api.parse_relu_merge_out(mo.cpu().numpy().tobytes(), f.Q, f.R)
+    assert pm["proof"] == m1["proof"] and pm["r"] == m1["r"] and t1.state() == t2.state()
+
+
 def test_async_provers_match_sync(ctx):
     """zk_matmul_prove / zk_relu_prove_dev (device outputs, no host sync) give the bytes of the
     synchronous calls, back to back on one transcript; the range flag replaces ZK_ERR_RANGE."""
@@ -436,8 +470,9 @@ def test_fcn_window_full_size_vs_oracle(ctx, O, cfg):
     mm = [api.Context(0, torch.cuda.Stream()) for _ in range(3)]
     for c in [ctx] + mm:
         c.set_sm_budget(37)
+    merge = cfg == "C4"   # C4 also with the aux-claim merge of N1 (D21) in the zkReLU family
     g = dfcn.prove_window(ctx, fs_seed(seed_name), fcn.fcn_header(shape), dfcn.upload_families(fams),
-                          relu_ctx=relu_ctx, mm_ctxs=mm)
+                          relu_ctx=relu_ctx, mm_ctxs=mm, merge_aux=merge)
     ctx.set_sm_budget(0)
     W = O.Transcript(fs_seed(seed_name))
     W.absorb("fcn/hdr", fcn.fcn_header(shape))
@@ -452,6 +487,12 @@ def test_fcn_window_full_size_vs_oracle(ctx, O, cfg):
             assert gr["msgs"] == o["msgs"] and gr["finals"] == o["finals"], f.name
         else:
             assert O.relu_verify(T, f.Z, f.GA, f.Q, f.R, gr["claims"], gr["msgs"], gr["finals"]) == 0, f.name
+            if merge:   # the merge's claim from the verified finals, then its round identities
+                gm = gr["merge"]
+                rho = T.challenges("relu/merge", 1)[0]
+                f0, f1, f2 = gr["finals"]
+                assert gm["claim"] == (f0 + rho * f1 + rho * rho * f2) % P
+                assert O.sumcheck_verify(T, 6, 0, 2, [], gm["claim"], gm["msgs"], gm["finals"]) == 0
         assert gr["state"] == T.state(), f.name
     for T in forks:
         W.absorb("fcn/join", T.state())
