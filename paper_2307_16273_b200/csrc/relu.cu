@@ -1390,7 +1390,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         buf[1][k] = s.alloc<fr_t>(D >> 1);
         buf[0][k] = s.alloc<fr_t>(D >= 4 ? D >> 2 : 1);
     }
-    unsigned int max_grid = (unsigned int)ctx->num_sms * 4;
+    unsigned int max_grid = (unsigned int)ctx->num_sms * 4;   // >= the factored kernel's grid (cap above)
     fr_t* partials = s.alloc<fr_t>((size_t)max_grid * 13);
     unsigned int* ticket = s.alloc_zero<unsigned int>(1);
     const fr_t* cur[3] = {full[0], full[1], full[2]};
@@ -1442,18 +1442,21 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
             else
                 ZK_LAUNCH(ctx, k_relu_iround<false>, grid, 256, 0, a);
         } else {
-            // grid = 2^hb HI blocks x cpb CTAs each, at most two CTAs per SM
+            // grid = 2^hb HI blocks x cpb CTAs each, two 256-thread CTAs per SM (ZKDL_IROUND_T=128: four
+            // 128-thread CTAs; measured no better in the C4 window)
+            const char* te = getenv("ZKDL_IROUND_T");
+            const uint32_t ithreads = (te && atoi(te) == 128) ? 128u : 256u;
             const uint64_t per_blk = a.n_pairs >> hb;
-            uint64_t cpb = (per_blk + 127) / 128;
-            const uint64_t cap = ((uint64_t)ctx->num_sms * 2) >> hb;
+            uint64_t cpb = (per_blk + ithreads / 2 - 1) / (ithreads / 2);
+            const uint64_t cap = ((uint64_t)ctx->num_sms * (512 / ithreads)) >> hb;
             if (cpb > cap) cpb = cap;
             if (cpb < 1) cpb = 1;
             a.cpb = (uint32_t)cpb;
             const unsigned int grid = (unsigned int)(cpb << hb);
             if (fold)
-                ZK_LAUNCH(ctx, k_relu_iround_f<true>, grid, 256, 0, a);
+                ZK_LAUNCH(ctx, k_relu_iround_f<true>, grid, ithreads, 0, a);
             else
-                ZK_LAUNCH(ctx, k_relu_iround_f<false>, grid, 256, 0, a);
+                ZK_LAUNCH(ctx, k_relu_iround_f<false>, grid, ithreads, 0, a);
         }
         lo_level ^= 1;
         if (fold)

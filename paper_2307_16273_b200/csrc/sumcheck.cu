@@ -733,6 +733,13 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
     }
 }
 
+// CTA size of the persistent small-statement prover (ZKDL_SCALL_T=128 for experiments: measured no
+// better in the C4 window, 11.80 vs 11.65 ms)
+static int sc_all_threads() {
+    const char* e = getenv("ZKDL_SCALL_T");
+    return (e && atoi(e) == 128) ? 128 : 256;
+}
+
 template <int K>
 static void launch_all(zk_ctx* ctx, const ScAllArgs& a, unsigned int grid) {
     void* args[] = {(void*)&a};
@@ -743,7 +750,7 @@ static void launch_all(zk_ctx* ctx, const ScAllArgs& a, unsigned int grid) {
         ev_b = ctx->take_event();
         cudaEventRecord(ev_a, ctx->stream);
     }
-    ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_sc_all<K>, dim3(grid), dim3(256), args, 0, ctx->stream));
+    ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_sc_all<K>, dim3(grid), dim3(sc_all_threads()), args, 0, ctx->stream));
     after_launch(ctx, "k_sc_all");
     if (prof) {
         cudaEventRecord(ev_b, ctx->stream);
@@ -754,7 +761,7 @@ static void launch_all(zk_ctx* ctx, const ScAllArgs& a, unsigned int grid) {
 template <int K>
 static unsigned int all_grid(zk_ctx* ctx, uint32_t m) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sc_all<K>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sc_all<K>, sc_all_threads(), 0);
     if (per_sm < 1) per_sm = 1;
     // at most one block per SM: the rounds are latency-bound after the first few, and a persistent
     // grid that fills the GPU would crowd out the zkReLU kernels running on the other stream
@@ -762,7 +769,8 @@ static unsigned int all_grid(zk_ctx* ctx, uint32_t m) {
     if (cap > (uint64_t)ctx->num_sms) cap = (uint64_t)ctx->num_sms;
     if (ctx->sm_budget > 0 && cap > (uint64_t)ctx->sm_budget) cap = (uint64_t)ctx->sm_budget;
     if (cap < 2) cap = 2;   // one worker + the reducer block
-    uint64_t need = ((1ull << (m - 1)) + 255) / 256 + 1;   // + the reducer block
+    const uint64_t T = (uint64_t)sc_all_threads();
+    uint64_t need = ((1ull << (m - 1)) + T - 1) / T + 1;   // + the reducer block
     if (need < 2) need = 2;
     return (unsigned int)(need < cap ? need : cap);
 }
