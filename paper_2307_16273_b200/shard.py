@@ -101,12 +101,15 @@ class TorchComm:
         self.world = dist.get_world_size(group)
 
     def allgather(self, t: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         if self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        else:
-            self.dist.all_gather(list(out.unbind(0)), t.contiguous(), group=self.group)
-        return out
+            return out
+        # gloo (tests, CPU hosts of the multi-rank logic): exchange through host memory
+        src = t.contiguous().cpu()
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype)
+        self.dist.all_gather(list(out.unbind(0)), src, group=self.group)
+        return out.to(t.device)
 
 
 def prove(session, comm, switch_log: int = 12) -> dict:
