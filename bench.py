@@ -542,6 +542,65 @@ def run_c5(args, rank, world, local):
         print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------- T' x BS sweep (SURVEY §8(f) N3's workload)
+def run_sweep(args, rank, world, local):
+    """--config sweep: the C4 network at T' in --sweep-T and BS in --sweep-BS, one line with per-update
+    proving time and per-update sumcheck proof bytes per point -- the shape of the paper's Table 1
+    (PT and PS per step fall with T' until they plateau), for this hot path only (no
+    commitments, so CS and the commitment part of PS are not comparable)."""
+    import dataclasses
+
+    import torch
+    from paper_2307_16273_b200 import api, build
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    from synth.prng import DATA_SEED, fs_seed
+    build.build(verbose=False)
+    stream = torch.cuda.Stream(device=local)
+    ctx = api.Context(local, stream)
+    relu_ctx = api.Context(local, torch.cuda.Stream(device=local))
+    mm = [api.Context(local, torch.cuda.Stream(device=local))]
+    for c in [ctx] + mm:
+        c.set_sm_budget(37)
+    rows = []
+    for T in args.sweep_T:
+        for bs in args.sweep_BS:
+            shape = dataclasses.replace(fcn.C4_SHAPE, name=f"C4-T{T}-BS{bs}", batch=bs, steps=T)
+            t0 = time.time()
+            fams = fcn.assemble_families(shape, fcn.generate_trace(shape, seed=DATA_SEED + rank))
+            gen_s = time.time() - t0
+            dev_fams = dfcn.upload_families(fams, device=f"cuda:{local}")
+            header = fcn.fcn_header(shape)
+            seed = fs_seed(shape.name)
+            with torch.cuda.stream(stream):
+                res = dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                pend = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm)
+                        for _ in range(args.steps)]
+                e1.record(stream)
+                torch.cuda.synchronize()
+                del pend
+            ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+            proof_bytes = sum(len(r["proof"]) for r in res)
+            rows.append({"T": T, "BS": bs, "s_per_update": ms / 1000.0 / T, "ms_per_window": round(ms, 3),
+                         "proof_kB_per_update": round(proof_bytes / 1024.0 / T, 3),
+                         "families": len(fams), "trace_gen_s": round(gen_s, 1)})
+            log(f"[sweep] T'={T} BS={bs}: {ms / T:.3f} ms/update, {proof_bytes / 1024 / T:.2f} kB/update")
+            del dev_fams, fams
+            torch.cuda.empty_cache()
+    out = {"metric": "prover s per batch update vs T' (aggregated steps) and BS (Table 1 shape, hot path only)",
+           "value": rows[-1]["s_per_update"] if rows else None, "unit": "s/update", "n_gpus": world,
+           "steps": args.steps, "warmup": 1, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+           "dtype": "fr_bls12_381 (8x32-bit Montgomery)", "data": "synthetic (seeded quantized FCN training trace)",
+           "config": {"workload": "C4 network (3072(->4096)-1024x8-10(->16)) at each (T', BS)", "sweep": rows},
+           "paper_context": {"table": "P:L391-416", "PT_s_per_step_A100": {"1": 6.2, "4": 1.9, "16": 0.84, "64": 0.85},
+                             "note": "paper PT includes commitments and openings (excluded here)"}}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 # ---------------------------------------------------------------- oracle (CPU) arm
 def oracle_window_sample(fams, shape, frac_inst: int, relu_instances: int):
     """Time the oracle on a sub-stack of every family; return (seconds for the full window, sample note)."""
@@ -621,7 +680,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C4", choices=["C4", "C5"])
+    ap.add_argument("--config", default="C4", choices=["C4", "C5", "sweep"])
+    ap.add_argument("--sweep-T", type=int, nargs="+", default=[1, 4, 16, 64])
+    ap.add_argument("--sweep-BS", type=int, nargs="+", default=[16, 32, 64])
     ap.add_argument("--c5-log", type=int, default=26, help="C5: log2 m of the 2^m hypercube (22..30)")
     ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -645,6 +706,8 @@ def main():
     rank, world, local = dist_setup(args.gpus)
     if args.config == "C5":
         run_c5(args, rank, world, local)
+    elif args.config == "sweep":
+        run_sweep(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
     if world > 1:
