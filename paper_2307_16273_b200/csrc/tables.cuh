@@ -99,6 +99,7 @@ struct LoadReluGZ {
 // One warp per row r of an int32 matrix viewed through `load` (row-major, `cols` entries per row,
 // rows < nrows): out[map(r)] = sum_c M[r][c] * eq[c], with E2 = eq table scaled by R (double Montgomery).
 // map(r) = (r & (inner - 1)) * outer + (r >> log_inner)   (restriction layout [k][n]); inner = nrows gives identity.
+// (Measured: unrolling eight loads per lane, or four rows per warp sharing the eq loads, were slower.)
 template <class Load>
 __global__ void __launch_bounds__(256) k_rowdot_i32(Load load, uint64_t nrows, uint32_t cols, const fr_t* E2,
                                                     fr_t* out, uint64_t inner, uint32_t log_inner, uint64_t outer) {
@@ -130,7 +131,18 @@ __global__ void __launch_bounds__(256) k_colsum_i32(Load load, uint64_t N, uint3
         const uint64_t n = t / cols, c = t % cols;
         uint32_t acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         const uint64_t base = n * (uint64_t)rows * cols + c;
-        for (uint32_t r = 0; r < rows; r++) {
+        uint32_t r = 0;
+        for (; r + 7 < rows; r += 8) {   // eight loads in flight (see k_rowdot_i32)
+            uint32_t u[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) u[k] = (uint32_t)load(base + (uint64_t)(r + k) * cols) + 0x80000000u;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const fr_t e = fr_load(&E2[r + k]);
+                ZK_MAC_WIDE(acc, e, u[k]);
+            }
+        }
+        for (; r < rows; r++) {
             uint32_t u = (uint32_t)load(base + (uint64_t)r * cols) + 0x80000000u;
             fr_t e = fr_load(&E2[r]);
             ZK_MAC_WIDE(acc, e, u);
