@@ -243,3 +243,46 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
             ready[i] = ev
     return collect_window(*enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order,
                                           mm_ctxs=mm_ctxs, merge_aux=merge_aux))
+
+
+def prove_windows_from_host(ctx: api.Context, windows: list, copy_stream=None, relu_ctx: api.Context | None = None,
+                            mm_ctxs: list | None = None, merge_aux: bool = False) -> list:
+    """Several windows end to end, pipelined: windows = [(seed, header, host_families), ...].  Every
+    window's uploads are enqueued on the copy stream behind the previous window's, and its proofs wait
+    only for their own uploads, so the copy engine streams without gaps while earlier windows prove;
+    the proofs of all windows come back with one synchronisation at the end.  Same bytes as
+    prove_window_from_host per window."""
+    dev = torch.device("cuda", ctx.device)
+    cs = copy_stream if copy_stream is not None else torch.cuda.Stream(device=dev)
+    pending = []
+    for seed, header, host_families in windows:
+        uploaded = {}
+
+        def upload(t):
+            key = (t.data_ptr(), t.numel(), t.dtype)
+            if key not in uploaded:
+                uploaded[key] = t.to(dev, non_blocking=True)
+            return uploaded[key]
+
+        def nbytes(f):
+            ts = (f.A, f.B) if f.kind == "matmul" else (f.Z, f.GA)
+            return sum(t.numel() * t.element_size() for t in ts)
+        order = sorted(range(len(host_families)),
+                       key=lambda i: (host_families[i].kind != "relu", -nbytes(host_families[i]), i))
+        fams, ready = [None] * len(host_families), [None] * len(host_families)
+        with torch.cuda.stream(cs):
+            for i in order:
+                f = host_families[i]
+                up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
+                fams[i] = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
+                readers = [relu_ctx.stream] if (relu_ctx is not None and f.kind == "relu") else \
+                    [ctx.stream] + [c.stream for c in (mm_ctxs or [])]
+                for t in up.values():
+                    for st in readers:
+                        t.record_stream(st)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                ready[i] = ev
+        pending.append(enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order,
+                                      mm_ctxs=mm_ctxs, merge_aux=merge_aux))
+    return [collect_window(*p) for p in pending]

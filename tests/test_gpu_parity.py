@@ -306,6 +306,8 @@ def test_fcn_tiny_vs_oracle(ctx, O):
     host = dfcn.upload_families(fams, device="cpu")
     h = dfcn.prove_window_from_host(ctx, fs_seed("tiny"), fcn.fcn_header(shape), host, relu_ctx=relu_ctx)
     assert [r["proof"] for r in h] == [r["proof"] for r in g]
+    hh = dfcn.prove_windows_from_host(ctx, [(fs_seed("tiny"), fcn.fcn_header(shape), host)] * 3, relu_ctx=relu_ctx)
+    assert all([r["proof"] for r in w] == [r["proof"] for r in g] for w in hh)
     assert [r["state"] for r in h] == [r["state"] for r in g]
     assert h[-1]["window_state"] == g[-1]["window_state"]
     g2 = dfcn.prove_window(ctx, fs_seed("tiny"), fcn.fcn_header(shape), dfcn.upload_families(fams), relu_ctx=relu_ctx)
