@@ -383,6 +383,16 @@ def run_ours(args, rank, world, local):
               "unit": "GFr-mul/s", "frac": None, "traffic": None, "ms_per_step": round(dom_ms, 4),
               "share_of_step": round(dom_ms / ms_local * args.steps, 4) if ms_local else None}
     rf["launches_per_step"] = dom_launches
+    try:   # DRAM traffic of the dominant kernel's captured launch (ncu --set full, committed under profiles/)
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r1h.json")))
+        base = dom_name.split("<")[0]
+        if base in tj:
+            L0 = tj[base]["launches"][0]
+            rf["traffic"] = L0["dram_read"] + L0["dram_write"]
+            rf["traffic_note"] = (f"bytes of one captured launch ({L0['launch']}) against {L0['algorithmic']} "
+                                  f"algorithmic bytes ({L0['algorithmic_note']}); {tj['source']}")
+    except (OSError, ValueError, KeyError):
+        pass
     rf["durations"] = {
         "dominant": "CUDA events on the launch stream around each launch of this kernel only, inside the timed "
                     "region; the kernel table comes from an identical K-window pass with every launch bracketed",
