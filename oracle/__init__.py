@@ -60,6 +60,7 @@ def lib():
         L.or_reindex_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp,
                                        vp, vp, vp, vp]
         L.or_relu_merge.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp]
+        L.or_zero_sumcheck_prove.argtypes = [vp, c.c_uint32, i32p, i32p, i32p, vp, vp, vp, vp]
         L.or_set_threads.argtypes = [c.c_int]
         L.or_get_threads.restype = c.c_int
         L.or_transcript_size.restype = c.c_uint64
@@ -327,3 +328,19 @@ def relu_merge(tr: Transcript, Z: np.ndarray, GA: np.ndarray, Q: int, R: int, po
     return dict(rho=from_bytes(rho.raw[:32])[0], claim=from_bytes(claim.raw[:32])[0],
                 msgs=[flat[3 * t:3 * t + 3] for t in range(m)], r=from_bytes(r.raw[:32 * m], m),
                 finals=from_bytes(fin.raw[:64], 2))
+
+
+# ---------------------------------------------------------------- N2: Protocol 2 zero form
+def zero_sumcheck_prove(tr: Transcript, Y: np.ndarray, A: np.ndarray, B: np.ndarray):
+    """0 = sum_x beta(w, x) (Y(x) - A(x) B(x)) (Eq. tensor-op-aggr + Protocol 2, D22); int32
+    tables of 2^m entries.  Returns dict(w, msgs[m][3], r, finals (Y~, A~, B~ at r))."""
+    Y, A, B = (np.ascontiguousarray(t, dtype=np.int32).reshape(-1) for t in (Y, A, B))
+    m = Y.size.bit_length() - 1
+    assert Y.size == 1 << m and A.size == Y.size and B.size == Y.size
+    w, msgs, r, fin = _buf(32 * m), _buf(96 * m), _buf(32 * m), _buf(96)
+    s = lib().or_zero_sumcheck_prove(tr.st, m, _ptr(Y), _ptr(A), _ptr(B), w, msgs, r, fin)
+    if s:
+        raise ValueError(f"or_zero_sumcheck_prove status {s}")
+    flat = from_bytes(msgs.raw[:96 * m])
+    return dict(w=from_bytes(w.raw[:32 * m], m), msgs=[flat[3 * t:3 * t + 3] for t in range(m)],
+                r=from_bytes(r.raw[:32 * m], m), finals=from_bytes(fin.raw[:96], 3))

@@ -1076,6 +1076,71 @@ int or_relu_merge(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t 
     return st;
 }
 
+/* ------------------------------------------------------------ N2: Protocol 2's zero form
+ * Eq. (tensor-op-aggr) P:L229-234 with Protocol 2 P:L476-502 for the aggregated Hadamard product
+ * (every index of Y is an output index, D_in = 1, f = X_0 X_1), D22:
+ *   0 = sum_x beta(w, x) (Y(x) - A(x) B(x)),   x over the m = log2 N + log2 D_out variables,
+ * w (the paper's (w, u)) drawn from the transcript.  Per round t the prover sends f_t at v = 0, 1, 2 with
+ * beta(w_{<=t}, .) divided out (D4: the verifier checks (1 - w_t) f_t(0) + w_t f_t(1) = c_t, c_0 = 0,
+ * c_{t+1} = f_t(r_t)).  Transcript: "hd/hdr" (m) | w = "hd/w" x m | per round "sc/msg" (3 values) then
+ * "sc/r" | "sc/final" (Y~(r), A~(r), B~(r)).  Tables int32, embedded (negatives -> p - |v|). */
+int or_zero_sumcheck_prove(transcript *tr, uint32_t m, const int32_t *Y, const int32_t *A, const int32_t *B,
+                           uint8_t *w_out /* m */, uint8_t *msgs_out /* m x 3 */, uint8_t *r_out /* m */,
+                           uint8_t *finals_out /* 3 */) {
+    init();
+    if (m < 1 || m > 32) return -1;
+    uint64_t n = 1ULL << m;
+    absorb_u32s(tr, "hd/hdr", &m, 1);
+    fr w[64];
+    for (uint32_t t = 0; t < m; t++) { w[t] = transcript_challenge(tr, "hd/w"); store_canon(w[t], w_out + 32 * t); }
+    fr *T[3];
+    const int32_t *src[3] = {Y, A, B};
+    for (int k = 0; k < 3; k++) {
+        T[k] = (fr *)malloc(n * sizeof(fr));
+        for (uint64_t i = 0; i < n; i++) T[k][i] = fr_from_i64(src[k][i]);
+    }
+    int nt = omp_get_max_threads();
+    for (uint32_t t = 0; t < m; t++) {
+        uint64_t half = n >> (t + 1);
+        fr *part = (fr *)calloc((size_t)nt * 3, sizeof(fr));
+        #pragma omp parallel
+        {
+            int id = omp_get_thread_num();
+            fr acc[3] = {fr_zero(), fr_zero(), fr_zero()};
+            #pragma omp for schedule(static)
+            for (uint64_t b = 0; b < half; b++) {
+                int rest = (int)(m - t - 1);   /* beta(w_{t+1..m-1}, b) */
+                fr e = eq_at(w + t + 1, rest, b);
+                for (uint32_t X = 0; X < 3; X++) {
+                    fr x = fr_from_u64(X);
+                    fr y = fr_add(T[0][2 * b], fr_mul(x, fr_sub(T[0][2 * b + 1], T[0][2 * b])));
+                    fr a = fr_add(T[1][2 * b], fr_mul(x, fr_sub(T[1][2 * b + 1], T[1][2 * b])));
+                    fr c = fr_add(T[2][2 * b], fr_mul(x, fr_sub(T[2][2 * b + 1], T[2][2 * b])));
+                    acc[X] = fr_add(acc[X], fr_mul(e, fr_sub(y, fr_mul(a, c))));
+                }
+            }
+            for (int X = 0; X < 3; X++) part[id * 3 + X] = acc[X];
+        }
+        fr ev[3];
+        for (int X = 0; X < 3; X++) {
+            ev[X] = fr_zero();
+            for (int i = 0; i < nt; i++) ev[X] = fr_add(ev[X], part[i * 3 + X]);
+            store_canon(ev[X], msgs_out + 32 * (t * 3 + X));
+        }
+        free(part);
+        absorb_frs(tr, "sc/msg", ev, 3);
+        fr r = transcript_challenge(tr, "sc/r");
+        store_canon(r, r_out + 32 * t);
+        for (int k = 0; k < 3; k++)
+            for (uint64_t b = 0; b < half; b++)
+                T[k][b] = fr_add(T[k][2 * b], fr_mul(r, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
+    }
+    fr fin[3];
+    for (int k = 0; k < 3; k++) { fin[k] = T[k][0]; store_canon(fin[k], finals_out + 32 * k); free(T[k]); }
+    absorb_frs(tr, "sc/final", fin, 3);
+    return 0;
+}
+
 /* ------------------------------------------------------------ misc exports */
 void or_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
 int or_get_threads(void) { return omp_get_max_threads(); }

@@ -1,0 +1,77 @@
+"""Pins for the oracle's SURVEY §8(f) N2 step (-m "not gpu"): Protocol 2's zero form for the aggregated
+Hadamard product (Eq. tensor-op-aggr, Protocol 2 P:L476-502; D22).
+
+The verifier is written here from Protocol 2 (g_t = beta(w_t, .) f_t, g_0(0) + g_0(1) = 0,
+g_t(0) + g_t(1) = f_{t-1}(v_{t-1}), the last claim against Y~ - A~ B~ at the final point) with every
+multilinear extension evaluated by Python-int brute force; tampering with one entry of Y must break
+the first identity.
+"""
+import numpy as np
+
+from synth.prng import fs_seed, uniform_range
+
+P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+
+
+def mle(vals, point):
+    acc = 0
+    for b, v in enumerate(vals):
+        w = 1
+        for t, x in enumerate(point):
+            w = w * (x if (b >> t) & 1 else 1 - x) % P
+        acc = (acc + int(v) * w) % P
+    return acc
+
+
+def lagrange3(e, x):
+    inv2 = pow(2, P - 2, P)
+    return (e[0] * (x - 1) * (x - 2) * inv2 - e[1] * x * (x - 2) + e[2] * x * (x - 1) * inv2) % P
+
+
+def verify(O, seed, m, res, Y, A, B):
+    """Protocol 2 verifier; returns 0 = accept, t + 1 = the failing round, -1 = the final check."""
+    tr = O.Transcript(seed)
+    tr.absorb("hd/hdr", m.to_bytes(4, "little"))
+    w = tr.challenges("hd/w", m)
+    assert w == res["w"]
+    c = 0
+    for t, e in enumerate(res["msgs"]):
+        if ((1 - w[t]) * e[0] + w[t] * e[1]) % P != c:
+            return t + 1
+        tr.absorb("sc/msg", O.to_bytes(e))
+        r = tr.challenges("sc/r", 1)[0]
+        assert r == res["r"][t]
+        c = lagrange3(e, r)
+    y, a, b = (mle(list(T), res["r"]) for T in (Y, A, B))
+    if res["finals"] != [y, a, b] or c != (y - a * b) % P:
+        return -1
+    return 0
+
+
+def test_zero_form_honest_hadamard_accepted(oracle_lib):
+    O = oracle_lib
+    for m in (1, 2, 3, 5, 7):
+        A = uniform_range(31, m, (1 << m,), -(1 << 15), 1 << 15)
+        B = uniform_range(31, m + 40, (1 << m,), -(1 << 15), 1 << 15)
+        Y = (A.astype(np.int64) * B).astype(np.int32)
+        seed = fs_seed(f"hd-{m}")
+        res = O.zero_sumcheck_prove(O.Transcript(seed), Y, A, B)
+        assert verify(O, seed, m, res, Y, A, B) == 0
+        # the statement itself: sum_x beta(w, x) (Y - A B) = 0, and f_0 folds to it
+        w = res["w"]
+        total = sum(mle([1 if i == x else 0 for i in range(1 << m)], w) * (int(Y[x]) - int(A[x]) * int(B[x]))
+                    for x in range(1 << m)) % P
+        assert total == 0
+
+
+def test_zero_form_rejects_a_wrong_product(oracle_lib):
+    O = oracle_lib
+    m = 6
+    A = uniform_range(32, 1, (1 << m,), -(1 << 15), 1 << 15)
+    B = uniform_range(32, 2, (1 << m,), -(1 << 15), 1 << 15)
+    for pos in (0, 17, 63):
+        Y = (A.astype(np.int64) * B).astype(np.int32)
+        Y[pos] += 1
+        seed = fs_seed(f"hd-bad-{pos}")
+        res = O.zero_sumcheck_prove(O.Transcript(seed), Y, A, B)
+        assert verify(O, seed, m, res, Y, A, B) == 1
