@@ -612,6 +612,46 @@ def run_sweep(args, rank, world, local):
         print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------- N2: Protocol 2's zero form
+def run_hadamard(args, rank, world, local):
+    """--config hadamard: Protocol 2's zero form for the aggregated Hadamard product (SURVEY §8(f) N2,
+    DESIGN.md D22): 0 = sum_x beta(w, x) (Y - A B) over 2^m entries, A, B ~ U[-2^15, 2^15), Y = A (.) B."""
+    import torch
+    from paper_2307_16273_b200 import api, build
+    from synth.prng import DATA_SEED, fs_seed, uniform_range_torch
+    build.build(verbose=False)
+    stream = torch.cuda.Stream(device=local)
+    ctx = api.Context(local, stream)
+    m = args.c5_log
+    dev = torch.device("cuda", local)
+    A = uniform_range_torch(DATA_SEED, 21, 1 << m, -(1 << 15), 1 << 15, dev)
+    B = uniform_range_torch(DATA_SEED, 22, 1 << m, -(1 << 15), 1 << 15, dev)
+    Y = (A.to(torch.int64) * B.to(torch.int64)).to(torch.int32)
+    times = []
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup + args.steps):
+            tr = api.Transcript(ctx, fs_seed(f"HD-m{m}"))
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g = api.hadamard_zero_prove(ctx, tr, Y, A, B)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tr.close()
+            if i >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+    ms = statistics.median(times)
+    first_ok = ((1 - g["w"][0]) * g["msgs"][0][0] + g["w"][0] * g["msgs"][0][1]) % 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001 == 0
+    out = {"metric": f"N2: prover s per 2^{m} aggregated Hadamard product, Protocol 2 zero form", "value": ms / 1000.0,
+           "unit": "s/proof", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+           "dtype": "fr_bls12_381 (8x32-bit Montgomery)", "data": "synthetic (A, B ~ U[-2^15, 2^15), Y = A B)",
+           "config": {"workload": f"0 = sum_x beta(w,x) (Y - A B), 2^{m} entries", "m": m},
+           "frmul_per_pair_model": "fold 6 + eq 1 + 3 x 2 = 13", "first_round_identity_holds": first_ok}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 # ---------------------------------------------------------------- oracle (CPU) arm
 def oracle_window_sample(fams, shape, frac_inst: int, relu_instances: int):
     """Time the oracle on a sub-stack of every family; return (seconds for the full window, sample note)."""
@@ -691,7 +731,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C4", choices=["C4", "C5", "sweep"])
+    ap.add_argument("--config", default="C4", choices=["C4", "C5", "sweep", "hadamard"])
     ap.add_argument("--sweep-T", type=int, nargs="+", default=[1, 4, 16, 64])
     ap.add_argument("--sweep-BS", type=int, nargs="+", default=[16, 32, 64])
     ap.add_argument("--c5-log", type=int, default=26, help="C5: log2 m of the 2^m hypercube (22..30)")
@@ -719,6 +759,8 @@ def main():
         run_c5(args, rank, world, local)
     elif args.config == "sweep":
         run_sweep(args, rank, world, local)
+    elif args.config == "hadamard":
+        run_hadamard(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
     if world > 1:

@@ -173,6 +173,19 @@ zk_status zk_relu_merge(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
 zk_status zk_relu_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
                             uint32_t Q, uint32_t R, const uint8_t* d_relu_out, uint8_t* d_out, uint64_t* out_len);
 
+/* zk_hadamard_zero_prove — SURVEY §8(f) N2: Protocol 2's zero form (Eq. tensor-op-aggr P:L229-234,
+ *   Protocol 2 P:L476-502) for the aggregated Hadamard product Y = A (.) B, D22:
+ *     0 = sum_x beta(w, x) (Y(x) - A(x) B(x)),  x over m variables (the stack and the output index).
+ *   d_Y, d_A, d_B: int32 tables of 2^m entries (device, borrowed; embedded mod p).  Transcript: "hd/hdr"
+ *   (m as u32le) | w = "hd/w" x m | per round "sc/msg" (f_t at 0, 1, 2; beta(w_{<=t}) divided out, D4)
+ *   then "sc/r" | "sc/final" (Y~(r), A~(r), B~(r)).  proof (host): u32le m | m x 3 evaluations |
+ *   3 finals; proof_len in/out (proof == NULL: size query).  w_out (m), point_out (m), finals_out (3):
+ *   host, may be NULL.  A false statement is not an error: the proof simply fails verification
+ *   ((1 - w_0) f_0(0) + w_0 f_0(1) != 0).  Synchronises the ctx stream once. */
+zk_status zk_hadamard_zero_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Y, const int32_t* d_A,
+                                 const int32_t* d_B, uint32_t m, uint8_t* proof, uint64_t* proof_len, zk_fr* w_out,
+                                 zk_fr* point_out, zk_fr* finals_out);
+
 /* ------------------------------------------- sharded product sumcheck (SURVEY §8(e), G = 2^s devices)
  * Rank g (of world = G, a power of two) holds entries [g 2^L, (g+1) 2^L) of every table, L = m - s:
  * the top s index bits (the last-bound variables, D2) are the rank id, so every round pair is local.

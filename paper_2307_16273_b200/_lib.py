@@ -63,6 +63,7 @@ def lib():
         "zk_reindex_prove": ([vp, vp, vp, u32, u32, u32, vp, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_relu_merge": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_relu_merge_dev": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, c.POINTER(u64)], i32),
+        "zk_hadamard_zero_prove": ([vp, vp, vp, vp, vp, u32, vp, c.POINTER(u64), vp, vp, vp], i32),
         "zk_transcript_new": ([vp, vp, c.POINTER(vp)], i32),
         "zk_transcript_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_transcript_challenges": ([vp, c.c_char_p, u32, vp], i32),

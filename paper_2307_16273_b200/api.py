@@ -471,3 +471,20 @@ def parse_relu_merge_out(raw: bytes, Q: int, R: int) -> dict:
     o = _a16(plen)
     res["r"] = [int.from_bytes(raw[o + 32 * i:o + 32 * i + 32], "little") for i in range(m)]
     return res
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) N2
+def hadamard_zero_prove(ctx: Context, tr: Transcript, Y: torch.Tensor, A: torch.Tensor, B: torch.Tensor) -> dict:
+    """zk_hadamard_zero_prove (Protocol 2's zero form, D22): int32 device tables of 2^m entries.
+    Returns dict(w, msgs[m][3], r, finals (Y~, A~, B~ at r), proof)."""
+    m = _log2(Y.numel())
+    assert A.numel() == Y.numel() and B.numel() == Y.numel()
+    plen = ctypes.c_uint64(4 + 96 * m + 96)
+    proof = ctypes.create_string_buffer(plen.value)
+    w, pt, fin = ctypes.create_string_buffer(32 * m), ctypes.create_string_buffer(32 * m), ctypes.create_string_buffer(96)
+    ctx.check(lib().zk_hadamard_zero_prove(ctx.h, tr.h, _dev_ptr(Y, torch.int32), _dev_ptr(A, torch.int32),
+                                           _dev_ptr(B, torch.int32), m, proof, ctypes.byref(plen), w, pt, fin))
+    raw = proof.raw[:plen.value]
+    vals = [int.from_bytes(raw[4 + 32 * i:36 + 32 * i], "little") for i in range(3 * m + 3)]
+    return dict(w=_ints(w, m), msgs=[vals[3 * t:3 * t + 3] for t in range(m)], r=_ints(pt, m), finals=vals[3 * m:],
+                proof=raw)

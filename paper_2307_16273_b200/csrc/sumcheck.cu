@@ -292,6 +292,54 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     }
 }
 
+// N2 (D22): Protocol 2's zero form for the aggregated Hadamard product.  Tables (Y, A, B); per pair the
+// term p(X) = Y(X) - A(X) B(X) times the suffix eq weight (f_t form, D4) at X = 0, 1, 2; the claim is 0.
+template <bool FOLD>
+__global__ void __launch_bounds__(256) k_sc_zero_round(ScRoundArgs a) {
+    fr_t acc[3] = {fr_zero(), fr_zero(), fr_zero()};
+    fr_t r;
+    if (FOLD) r = fr_load(a.r_prev);
+    const uint64_t lo_mask = (1ull << a.lo_cnt) - 1, hi_mask = (1ull << a.hb) - 1;
+    const uint64_t next_count = a.lo_cnt ? (1ull << (a.lo_cnt - 1)) : 0;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < a.n_pairs; b += (uint64_t)gridDim.x * blockDim.x) {
+        fr_t lo[3], d[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            fr_t v0, v1;
+            if (FOLD) {
+                const fr_t* s = a.src[k] + 4 * b;
+                const fr_t x0 = fr_load_cg(s), x1 = fr_load_cg(s + 1), x2 = fr_load_cg(s + 2), x3 = fr_load_cg(s + 3);
+                v0 = fr_add(x0, fr_mul_ni(r, fr_sub(x1, x0)));
+                v1 = fr_add(x2, fr_mul_ni(r, fr_sub(x3, x2)));
+                fr_store(a.dst[k] + 2 * b, v0);
+                fr_store(a.dst[k] + 2 * b + 1, v1);
+            } else {
+                v0 = fr_load_cg(a.src[k] + 2 * b);
+                v1 = fr_load_cg(a.src[k] + 2 * b + 1);
+            }
+            lo[k] = v0;
+            d[k] = fr_sub(v1, v0);
+        }
+        fr_t e = fr_one();
+        const bool has_e = a.eq_mode != 0;
+        if (a.eq_mode == 1) e = fr_mul_ni(fr_load(&a.eq_cur[b & lo_mask]), fr_load(&a.eq_hi[(b >> a.lo_cnt) & hi_mask]));
+        else if (a.eq_mode == 2) e = fr_load(&a.eq_cur[b & lo_mask]);
+        if (a.eq_mode && b < next_count)
+            fr_store(&a.eq_next[b], fr_add(fr_load(&a.eq_cur[2 * b]), fr_load(&a.eq_cur[2 * b + 1])));
+#pragma unroll
+        for (int x = 0; x < 3; x++) {
+            fr_t p = fr_sub(lo[0], fr_mul_ni(lo[1], lo[2]));
+            if (has_e) p = fr_mul_ni(p, e);
+            acc[x] = fr_add(acc[x], p);
+            if (x < 2)
+#pragma unroll
+                for (int k = 0; k < 3; k++) lo[k] = fr_add(lo[k], d[k]);
+        }
+    }
+    __shared__ fr_t tot[3];
+    if (grid_reduce_fr_block<3>(acc, a.partials, a.ticket, tot)) sc_finish(a, tot, 2);
+}
+
 // header (+ provided claim) before round 0; one warp
 __global__ void k_sc_header(uint8_t* st, Bytes256 hdr, const fr_t* claim, int absorb_claim, uint8_t* claim_bytes) {
     __shared__ FsScratch fs;
@@ -461,12 +509,18 @@ void ScEngine::round(fr_t* part_out) {
     a.claim = d_claim;
     a.compute_claim = (t == 0 && !claim_given) ? 1 : 0;
     a.claim_bytes = d_proof + 12;
-    a.msg_out = d_proof + 44 + 32ull * t * (K + 1);
+    a.msg_out = d_proof + 44 + 32ull * t * nev();
     a.r_out = d_r + t;
     a.point_out = d_point + 32ull * t;
     a.part_out = part_out;
     a.scale = d_scale;
-    if (K == 2 && factored) {
+    if (zero) {
+        const unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
+        if (fold)
+            ZK_LAUNCH(ctx, k_sc_zero_round<true>, grid, 256, 0, a);
+        else
+            ZK_LAUNCH(ctx, k_sc_zero_round<false>, grid, 256, 0, a);
+    } else if (K == 2 && factored) {
         Sc2Args A;
         memset(&A, 0, sizeof A);
         A.r = a;
@@ -531,7 +585,7 @@ void ScEngine::header() {
 
 void ScEngine::finals() {
     ZK_LAUNCH(ctx, k_sc_finals, 1, 32, 0, cur[0], K > 1 ? cur[1] : cur[0], K > 2 ? cur[2] : cur[0], (int)K, d_r + (m - 1),
-              tr->d_st, d_proof + 44 + 32ull * m * (K + 1), d_finals);
+              tr->d_st, d_proof + 44 + 32ull * m * nev(), d_finals);
 }
 
 // ---------------------------------------------------------------- persistent small-statement prover
@@ -848,7 +902,7 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
 constexpr uint32_t SC_TAIL_LOG = 16;
 
 void ScEngine::run_to_end() {
-    const bool persistent_ok = !getenv("ZKDL_NO_PERSISTENT");
+    const bool persistent_ok = !getenv("ZKDL_NO_PERSISTENT") && !zero;
     while (t < t0 + L) {
         const uint32_t tl = t - t0;
         if (tl >= 1 && persistent_ok && L - tl <= SC_TAIL_LOG) {

@@ -44,6 +44,8 @@ struct ScEngine {
     fr_t* d_finals = nullptr;
     const int32_t* i32[3] = {nullptr, nullptr, nullptr};   // int32 sources: round 0 embeds into cur[k]
     bool factored = true;   // K = 2: k_sc_round2f (ZKDL_SC_V=0: the unfactored k_sc_round)
+    bool zero = false;      // N2 zero form (D22): K = 3 tables (Y, A, B), terms Y - A B, 3 evaluations
+    uint32_t nev() const { return zero ? 3 : K + 1; }   // evaluations per round message
 
     // int32 tables: round 0 of the factored kernel embeds them into the (scratch) cur tables; otherwise
     // they are embedded here, before round 0

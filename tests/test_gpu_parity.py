@@ -621,3 +621,23 @@ def test_relu_merge_c4_size(ctx, O):
     claim = (f0 + rho * f1 + rho * rho * f2) % P
     assert gm["claim"] == claim
     assert O.sumcheck_verify(tr, 6, 0, 2, [], claim, gm["msgs"], gm["finals"]) == 0
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) N2
+@pytest.mark.parametrize("m", [1, 5, 12, 17, 20])
+def test_hadamard_zero_vs_oracle(ctx, O, m):
+    """Protocol 2's zero form (D22): bit-exact against the oracle, for a true statement Y = A (.) B and for a
+    false one (one entry of Y off by one: the proof is still determined and must match)."""
+    from paper_2307_16273_b200 import api
+    A = uniform_range(33, m, (1 << m,), -(1 << 15), 1 << 15)
+    B = uniform_range(33, m + 50, (1 << m,), -(1 << 15), 1 << 15)
+    for bad in (False, True):
+        Y = (A.astype(np.int64) * B).astype(np.int32)
+        if bad:
+            Y[(1 << m) // 3] += 1
+        seed = fs_seed(f"hd-gpu-{m}-{bad}")
+        o = O.zero_sumcheck_prove(O.Transcript(seed), Y, A, B)
+        g = api.hadamard_zero_prove(ctx, api.Transcript(ctx, seed), dev(Y), dev(A), dev(B))
+        assert g["w"] == o["w"] and g["msgs"] == o["msgs"] and g["r"] == o["r"] and g["finals"] == o["finals"]
+        first = ((1 - g["w"][0]) * g["msgs"][0][0] + g["w"][0] * g["msgs"][0][1]) % P
+        assert (first == 0) == (not bad)
