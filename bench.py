@@ -243,7 +243,9 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.Stream(device=local)
     ctx = api.Context(local, stream)
     # zkReLU families on a second stream, concurrent with the matmul families (D3d transcripts)
-    relu_ctx = api.Context(local, torch.cuda.Stream(device=local)) if args.streams == 2 else None
+    # the zkReLU family is the window's critical path: its stream gets the higher scheduling priority, so
+    # the matmul families' CTAs fill the SMs it leaves idle instead of delaying it
+    relu_ctx = api.Context(local, torch.cuda.Stream(device=local, priority=args.relu_priority)) if args.streams == 2 else None
     # matmul families spread over --mm-streams contexts (one stream each), persistent grids budgeted
     mm_ctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.mm_streams - 1)]
     if args.mm_streams > 1:
@@ -743,6 +745,7 @@ def main():
                     help="streams (contexts) the matmul families are spread over, side by side")
     ap.add_argument("--merge-aux", type=int, default=0, choices=[0, 1],
                     help="1: every zkReLU family ends with the aux-claim merge (P:L470, DESIGN.md D21)")
+    ap.add_argument("--relu-priority", type=int, default=-1, help="CUDA stream priority of the zkReLU stream (lower = higher)")
     ap.add_argument("--mm-budget", type=int, default=37,
                     help="SM budget of each matmul stream's persistent sumcheck grid (0: 148 / mm-streams)")
     ap.add_argument("--prof", default="dominant", choices=["dominant", "inline", "separate"],
