@@ -264,6 +264,10 @@ zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
  *   products on register-resident values (d_seed: 1024 elements; d_out: blocks*256 elements);
  *   bench.py times it to measure this implementation's sustained Fr-mul rate. */
 zk_status zk_diag_fr_op(zk_ctx* ctx, int op, const void* d_a, const void* d_b, uint64_t n, void* d_out);
+/* zk_diag_rowdot: out[r] = sum_c M[r][c] beta(point, c) (Montgomery, d_out: nrows Fr) through the CUDA-core
+ * (use_tc = 0) or the tensor-core (use_tc = 1) row-dot kernel of the matmul restriction; cols a power of two. */
+zk_status zk_diag_rowdot(zk_ctx* ctx, const int32_t* d_M, uint64_t nrows, uint32_t cols, const zk_fr* point,
+                         void* d_out, int use_tc);
 zk_status zk_diag_mul_bench(zk_ctx* ctx, const void* d_seed, uint32_t iters, uint32_t blocks, void* d_out);
 /* zk_diag_fs_bench: n sequential transcript steps on one warp (mode 0: absorb 3 elements + squeeze,
  * 1: transcript-hash (BLAKE2s) compressions only, 2: out-of-line Montgomery products); d_out receives one element. */

@@ -95,6 +95,7 @@ def lib():
         "zk_sc_shard_free": ([vp], None),
         "zk_diag_fr_op": ([vp, i32, vp, vp, u64, vp], i32),
         "zk_diag_mul_bench": ([vp, vp, u32, u32, vp], i32),
+        "zk_diag_rowdot": ([vp, vp, u64, u32, vp, vp, i32], i32),
         "zk_diag_fs_bench": ([vp, u32, i32, vp], i32),
     }
     for name, (args, res) in sig.items():

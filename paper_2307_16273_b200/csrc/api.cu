@@ -495,6 +495,30 @@ zk_status zk_diag_fr_op(zk_ctx* ctx, int op, const void* d_a, const void* d_b, u
     ZK_API_END(ctx)
 }
 
+zk_status zk_diag_rowdot(zk_ctx* ctx, const int32_t* d_M, uint64_t nrows, uint32_t cols, const zk_fr* point,
+                         void* d_out, int use_tc) {
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(d_M && d_out && point && cols && (cols & (cols - 1)) == 0, ZK_ERR_ARG, "bad argument");
+    uint32_t k = 0;
+    while ((1u << k) < cols) k++;
+    Scratch s(ctx);
+    fr_t* u = s.alloc<fr_t>(k ? k : 1);
+    if (k) upload_points(ctx, point, k, u, s);
+    fr_t* E2 = s.alloc<fr_t>(cols);
+    eq_table_r2_dev(ctx, u, k, E2, s);
+    uint32_t ln = 0;
+    while ((1ull << ln) < nrows) ln++;
+    if (use_tc) {
+        ZK_REQUIRE(rowdot_tc_ok(nrows, cols), ZK_ERR_ARG, "shape not supported by the tensor-core row dot");
+        rowdot_tc(ctx, d_M, nrows, cols, E2, static_cast<fr_t*>(d_out), 1ull << ln, ln, 1, s);
+    } else {
+        ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, grid_for(ctx, nrows * 32, 256, 8), 256, 0, LoadPlain{d_M}, nrows, cols,
+                  (const fr_t*)E2, static_cast<fr_t*>(d_out), 1ull << ln, ln, (uint64_t)1);
+    }
+    ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    ZK_API_END(ctx)
+}
+
 zk_status zk_diag_mul_bench(zk_ctx* ctx, const void* d_seed /* 1024 Fr */, uint32_t iters, uint32_t blocks, void* d_out) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(d_seed && d_out && blocks, ZK_ERR_ARG, "bad argument");

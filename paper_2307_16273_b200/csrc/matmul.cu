@@ -48,12 +48,16 @@ void matmul_reduce_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* A, const i
     if (!sh.trans_a) {   // A stored [N][D1][D2]: column sums over a
         ZK_LAUNCH(ctx, k_colsum_i32<LoadPlain>, grid_for(ctx, N * D2, 256, 8), 256, 0, LoadPlain{A}, N, (uint32_t)D1,
                   (uint32_t)D2, E1, At);
-    } else {             // A stored [N][D2][D1]: one warp per (n, k) row
+    } else if (rowdot_tc_ok(N * D2, (uint32_t)D1)) {   // A stored [N][D2][D1]: row dots on the tensor cores
+        rowdot_tc(ctx, A, N * D2, (uint32_t)D1, E1, At, D2, l2, N, s);
+    } else {             // one warp per (n, k) row
         ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, grid_for(ctx, N * D2 * 32, 256, 8), 256, 0, LoadPlain{A}, N * D2,
                   (uint32_t)D1, E1, At, D2, l2, N);
     }
     // Bt[k][n]
-    if (!sh.trans_b) {   // B stored [N][D2][D3]: row dots over c
+    if (!sh.trans_b && rowdot_tc_ok(N * D2, (uint32_t)D3)) {   // B stored [N][D2][D3]: row dots over c, tensor cores
+        rowdot_tc(ctx, B, N * D2, (uint32_t)D3, E3, Bt, D2, l2, N, s);
+    } else if (!sh.trans_b) {
         ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, grid_for(ctx, N * D2 * 32, 256, 8), 256, 0, LoadPlain{B}, N * D2,
                   (uint32_t)D3, E3, Bt, D2, l2, N);
     } else {             // B stored [N][D3][D2]: column sums over c

@@ -159,6 +159,12 @@ __global__ void k_dot_fr(const fr_t* a, const fr_t* b, uint64_t n, fr_t* partial
 void mle_i32_plain(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s);
 void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ*/, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m,
                   const fr_t* d_u, fr_t* d_out, Scratch& s);
+// Row dots out[map(r)] = sum_c M[r][c] E2[c] of an int32 matrix on the tensor cores (restrict_tc.cu): same
+// results as k_rowdot_i32<LoadPlain>; rowdot_tc_ok says whether the shape is supported (cols % 8 == 0,
+// cols <= 4096, >= 1024 rows; ZKDL_ROWDOT_TC=0 disables it).
+bool rowdot_tc_ok(uint64_t nrows, uint32_t cols);
+void rowdot_tc(zk_ctx* ctx, const int32_t* M, uint64_t nrows, uint32_t cols, const fr_t* E2, fr_t* out, uint64_t inner,
+               uint32_t log_inner, uint64_t outer, Scratch& s);
 void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,
                    fr_t* d_out, Scratch& s);
 void mle_fr_dev(zk_ctx* ctx, const fr_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s);

@@ -193,6 +193,24 @@ __device__ __forceinline__ fr_t MUL(const fr_t& a, const fr_t& b) {
     return mul_sos(a, b);
 }
 
+// Variant 6: three products per call through the production out-of-line fr_mul3_ni (k_relu_iround_f,
+// k_sc_round2f); variant 7: one product per call (fr_mul_ni)
+template <int V>
+__global__ void __launch_bounds__(256) bench3(const fr_t* seed, uint32_t iters, fr_t* out) {
+    uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    fr_t a = seed[tid & 1023], b = seed[(tid + 1) & 1023], c = seed[(tid + 2) & 1023];
+    fr_t k = seed[(tid + 7) & 1023];
+    for (uint32_t i = 0; i < iters; i++) {
+        if (V == 6) {
+            fr3_t r = fr_mul3_ni(a, k, b, k, c, k);
+            a = r.x; b = r.y; c = r.z;
+        } else {
+            a = fr_mul_ni(a, k); b = fr_mul_ni(b, k); c = fr_mul_ni(c, k);
+        }
+    }
+    out[tid] = fr_add(fr_add(a, b), c);
+}
+
 template <int V>
 __global__ void __launch_bounds__(256) bench(const fr_t* seed, uint32_t iters, fr_t* out) {
     uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -256,6 +274,28 @@ static void run(const char* name, fr_t* d_seed, fr_t* d_out, int blocks, uint32_
     if (e != cudaSuccess) { printf("cuda error %s\n", cudaGetErrorString(e)); exit(1); }
 }
 
+template <int V>
+static void run3(const char* name, fr_t* d_seed, fr_t* d_out, int blocks, uint32_t iters) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    bench3<V><<<blocks, 256>>>(d_seed, 10, d_out);
+    float best = 1e30f;
+    for (int r = 0; r < 3; r++) {
+        cudaEventRecord(e0);
+        bench3<V><<<blocks, 256>>>(d_seed, iters, d_out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    cudaFuncAttributes at;
+    cudaFuncGetAttributes(&at, bench3<V>);
+    printf("{\"variant\": \"%s\", \"blocks\": %d, \"G_frmul_per_s\": %.2f, \"regs\": %d}\n", name, blocks,
+           (double)blocks * 256 * 3 * iters / (best / 1e3) / 1e9, at.numRegs);
+}
+
 int main() {
     setvbuf(stdout, nullptr, _IONBF, 0);
     // random canonical inputs (top limb < p7 keeps them < p) in Montgomery-agnostic form
@@ -274,7 +314,7 @@ int main() {
     run<3>("u64_cios_p01", d_seed, d_out, blocks, 1000);
     run<4>("mix_u64_madc", d_seed, d_out, blocks, 1000);
     run<5>("u64_p01_lazy", d_seed, d_out, blocks, 1000);
-    for (int b = 148 * 2; b <= 148 * 16; b *= 2) run<3>("u64_cios_p01", d_seed, d_out, b, 1000);
-    for (int b = 148 * 2; b <= 148 * 16; b *= 2) run<4>("mix_u64_madc", d_seed, d_out, b, 1000);
+    for (int b = 148 * 2; b <= 148 * 8; b *= 2) run3<6>("fr_mul3_ni", d_seed, d_out, b, 1000);
+    for (int b = 148 * 2; b <= 148 * 8; b *= 2) run3<7>("fr_mul_ni x3", d_seed, d_out, b, 1000);
     return 0;
 }

@@ -641,3 +641,23 @@ def test_hadamard_zero_vs_oracle(ctx, O, m):
         assert g["w"] == o["w"] and g["msgs"] == o["msgs"] and g["r"] == o["r"] and g["finals"] == o["finals"]
         first = ((1 - g["w"][0]) * g["msgs"][0][0] + g["w"][0] * g["msgs"][0][1]) % P
         assert (first == 0) == (not bad)
+
+
+@pytest.mark.parametrize("nrows,cols", [(1024, 8), (1024 + 24, 16), (18944, 64), (4096, 1024), (131072, 1024), (3000, 4096)])
+def test_rowdot_tensor_cores_match_cuda_cores(ctx, nrows, cols):
+    """The matmul restriction's row dots on the tensor cores (int8 GEMM over the bytes of the int32 matrix,
+    restrict_tc.cu) give the CUDA-core kernel's field elements bit for bit, full int32 range, ragged row
+    counts, several tiles per CTA."""
+    from paper_2307_16273_b200._lib import lib
+    from paper_2307_16273_b200 import api
+    rng = random.Random(nrows + cols)
+    M = torch.randint(-2 ** 31, 2 ** 31, (nrows, cols), dtype=torch.int64, generator=torch.Generator().manual_seed(nrows)).to(torch.int32).cuda()
+    M[0, :] = -2 ** 31
+    M[1, :] = 2 ** 31 - 1
+    pt = api._fr_buf([rng.randrange(P) for _ in range(cols.bit_length() - 1)])
+    outs = []
+    for tc in (0, 1):
+        o = torch.zeros((nrows, 32), dtype=torch.uint8, device="cuda")
+        ctx.check(lib().zk_diag_rowdot(ctx.h, M.data_ptr(), nrows, cols, pt, o.data_ptr(), tc))
+        outs.append(o.cpu())
+    assert torch.equal(outs[0], outs[1])
