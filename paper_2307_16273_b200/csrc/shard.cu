@@ -171,6 +171,7 @@ zk_status zk_sc_shard_export(zk_sc_shard* sh, void* d_out) {
     ScEngine& e = sh->e;
     const uint64_t n = 1ull << (e.L - e.t);   // local entries after folding by r_{t-1}
     fr_t* out = static_cast<fr_t*>(d_out);
+    e.materialize();
     for (uint32_t k = 0; k < e.K; k++)
         ZK_LAUNCH(ctx, k_fold_copy, grid_for(ctx, n, 256, 8), 256, 0, e.cur[k], n, e.t ? e.d_r + (e.t - 1) : nullptr,
                   out + k * n);

@@ -170,10 +170,135 @@ struct Sc2Args {
     int flat;                 // groups too small for a CTA: every pair applies its HI value itself
 };
 
+// ---- integer round 0 for int32 tables (C5, the sharded prover): the pair products are exact integers
+// P(0) = a0 b0, P(1) = a1 b1, P(inf) = (a1 - a0)(b1 - b0) (|P| < 2^64), so round 0 needs no field product
+// per pair: E' P is accumulated lazily as a 352-bit integer (u = P + 2^64 in [0, 2^65): 16 IMAD.WIDE),
+// the bias 2^64 sum E' is removed once per work item, and one Montgomery reduction closes each sum.
+__device__ __forceinline__ void mac65(uint32_t (&acc)[11], const fr_t& e, unsigned __int128 u) {
+    const uint32_t lo = (uint32_t)u, hi = (uint32_t)(u >> 32), top = (uint32_t)(u >> 64);
+    uint64_t C = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t t = (uint64_t)e.v[j] * lo + acc[j] + C;
+        acc[j] = (uint32_t)t;
+        C = t >> 32;
+    }
+#pragma unroll
+    for (int j = 8; j < 11; j++) {
+        const uint64_t t = (uint64_t)acc[j] + C;
+        acc[j] = (uint32_t)t;
+        C = t >> 32;
+    }
+    C = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t t = (uint64_t)e.v[j] * hi + acc[j + 1] + C;
+        acc[j + 1] = (uint32_t)t;
+        C = t >> 32;
+    }
+#pragma unroll
+    for (int j = 9; j < 11; j++) {
+        const uint64_t t = (uint64_t)acc[j] + C;
+        acc[j] = (uint32_t)t;
+        C = t >> 32;
+    }
+    if (top) {
+        C = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t t = (uint64_t)e.v[j] + acc[j + 2] + C;
+            acc[j + 2] = (uint32_t)t;
+            C = t >> 32;
+        }
+        acc[10] += (uint32_t)C;
+    }
+}
+__device__ __forceinline__ void add9(uint32_t (&s)[9], const fr_t& e) {
+    uint64_t C = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t t = (uint64_t)s[j] + e.v[j] + C;
+        s[j] = (uint32_t)t;
+        C = t >> 32;
+    }
+    s[8] += (uint32_t)C;
+}
+// Montgomery reduction of an 11-limb integer T < 2^352 (< p 2^256): T R^{-1} mod p
+__device__ __noinline__ fr_t fr_redc11(const uint32_t (&w)[11]) {
+    // T = lo10 + w10 2^320:  REDC(T) = REDC(lo10) + w10 2^64 (2^320 R^{-1} = 2^64)
+    const uint32_t lo[10] = {w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], w[9]};
+    const fr_t x = fr_redc_wide(lo);
+    return fr_add(x, fr_t{{0, 0, w[10], 0, 0, 0, 0, 0}});   // w10 2^64 < p, already reduced
+}
+
+// Montgomery form of 2^64 (= 2^64 R mod p), derived with Python integers
+#define ZK_MONT_2_64 fr_const(0x0121c884u, 0xc98da28eu, 0xc7363c67u, 0xe6f4f4a0u, 0xe92e7df1u, 0xb2d6ebc4u, 0x9d26242au, 0x19ae5794u)
+
+// Round 0 from int32 tables, grouped eq weights (E' = LO[j], HI[group] once per item): the sums of E' P(0),
+// E' P(1), E' P(inf) as exact lazy integers.  Writes nothing but the next LO level; round 1 folds from the
+// int32 tables (MODE 3 of k_sc_round2f).
+__global__ void __launch_bounds__(256, 2) k_sc_round0_int(Sc2Args A) {
+    const ScRoundArgs& a = A.r;
+    const uint32_t lo_cnt = a.lo_cnt;
+    const uint64_t ngroups = a.n_pairs >> lo_cnt ? a.n_pairs >> lo_cnt : 1;
+    const uint64_t gsize = a.n_pairs < (1ull << lo_cnt) ? a.n_pairs : (1ull << lo_cnt);
+    const uint64_t slices = A.slices;
+    const uint64_t slice_len = (gsize + slices - 1) / slices;
+    const uint64_t next_count = lo_cnt ? (1ull << (lo_cnt - 1)) : 0;
+    const uint64_t hi_mask = (1ull << a.hb) - 1, lo_mask = (1ull << lo_cnt) - 1;
+    const int2* ia = reinterpret_cast<const int2*>(A.i32[0]);
+    const int2* ib = reinterpret_cast<const int2*>(A.i32[1]);
+    fr_t tot[3] = {fr_zero(), fr_zero(), fr_zero()};
+    for (uint64_t item = blockIdx.x; item < ngroups * slices; item += gridDim.x) {
+        const uint64_t g = item / slices, sl = item % slices;
+        const uint64_t j_end = (sl + 1) * slice_len < gsize ? (sl + 1) * slice_len : gsize;
+        uint32_t acc[3][11], S[9];
+#pragma unroll
+        for (int v = 0; v < 3; v++)
+#pragma unroll
+            for (int i = 0; i < 11; i++) acc[v][i] = 0;
+#pragma unroll
+        for (int i = 0; i < 9; i++) S[i] = 0;
+        bool any = false;
+        for (uint64_t j = sl * slice_len + threadIdx.x; j < j_end; j += blockDim.x) {
+            any = true;
+            const uint64_t b = (g << lo_cnt) + j;
+            const int2 x = __ldcs(ia + b), y = __ldcs(ib + b);
+            const fr_t e = fr_load(&a.eq_cur[b & lo_mask]);
+            if (b < next_count)
+                fr_store(&a.eq_next[b], fr_add(fr_load(&a.eq_cur[2 * b]), fr_load(&a.eq_cur[2 * b + 1])));
+            const unsigned __int128 bias = (unsigned __int128)1 << 64;
+            const __int128 p0 = (__int128)((int64_t)x.x * y.x), p1 = (__int128)((int64_t)x.y * y.y);
+            const __int128 pi = (__int128)((int64_t)x.y - x.x) * (__int128)((int64_t)y.y - y.x);
+            mac65(acc[0], e, (unsigned __int128)p0 + bias);
+            mac65(acc[1], e, (unsigned __int128)p1 + bias);
+            mac65(acc[2], e, (unsigned __int128)pi + bias);
+            add9(S, e);
+        }
+        if (any) {   // sum E' P = REDC(acc) - 2^64 REDC(S), to Montgomery form (x R^2), times HI[group]
+            const uint32_t s10[10] = {S[0], S[1], S[2], S[3], S[4], S[5], S[6], S[7], S[8], 0};
+            const fr_t sb = fr_mul(fr_redc_wide(s10), ZK_MONT_2_64);   // 2^64 sum E' (plain)
+            const fr_t h = a.eq_hi ? fr_mul(fr_load(&a.eq_hi[g & hi_mask]), ZK_R2) : ZK_R2;   // HI R (or R)
+#pragma unroll
+            for (int v = 0; v < 3; v++) tot[v] = fr_add(tot[v], fr_mul(fr_sub(fr_redc11(acc[v]), sb), h));
+        }
+    }
+    __shared__ fr_t tt[3];
+    __shared__ fr_t msg[3];
+    if (grid_reduce_fr_block<3>(tot, a.partials, a.ticket, tt)) {
+        if (threadIdx.x == 0) {   // evaluations at X = 0, 1, 2 of the quadratic with P(0), P(1), P(inf)
+            msg[0] = tt[0];
+            msg[1] = tt[1];
+            msg[2] = fr_sub(fr_dbl(fr_add(tt[1], tt[2])), tt[0]);
+        }
+        __syncthreads();
+        sc_finish(a, msg, 2);
+    }
+}
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     const ScRoundArgs& a = A.r;
-    constexpr bool FOLD = MODE == 1;
+    constexpr bool FOLD = MODE == 1 || MODE == 3;   // MODE 3: round 1 folding straight from the int32 tables
     const bool has_e = a.eq_mode != 0;
     const uint32_t lo_cnt = has_e ? a.lo_cnt : 0;
     // pairs per group (log2): the LO range; without eq weights the whole round is one group
@@ -185,8 +310,9 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     const uint64_t slice_len = (gsize + slices - 1) / slices;
     const uint64_t next_count = lo_cnt ? (1ull << (lo_cnt - 1)) : 0;
     const uint64_t hi_mask = (1ull << a.hb) - 1;
-    fr_t r;
+    fr_t r, r2;
     if (FOLD) r = fr_load(a.r_prev);
+    if (MODE == 3) r2 = fr_mul(r, ZK_R2);   // r R^2: fr_mul(r2, k) = Montgomery(r k) for a one-limb integer k
     fr_t tot0 = fr_zero(), tot1 = fr_zero(), toti = fr_zero();
     const uint64_t nitems = (A.flat ? 1 : ngroups) * slices;
     const uint64_t lo_mask = (1ull << lo_cnt) - 1;
@@ -210,10 +336,32 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
             fr3_t q;   // second group: (r db, E' a0, E' a1) in folding rounds with eq weights
             bool q_done = false;
             if (FOLD) {
+                fr_t x0, x1, x2, x3, z0, z1, z2, z3;
+                if constexpr (MODE == 3) {
+                    // v0 + r (v1 - v0) from int32: the embedding of v0 and r |v1 - v0| are products with a
+                    // one-limb operand (half a full product each); x1 / x3 carry r (v1 - v0) directly
+                    const int4 ia = __ldcs(reinterpret_cast<const int4*>(A.i32[0]) + b);
+                    const int4 ib = __ldcs(reinterpret_cast<const int4*>(A.i32[1]) + b);
+                    const int32_t va[4] = {ia.x, ia.y, ia.z, ia.w}, vb[4] = {ib.x, ib.y, ib.z, ib.w};
+                    fr_t fa[2], fb[2];
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const int64_t da = (int64_t)va[2 * h + 1] - va[2 * h], db = (int64_t)vb[2 * h + 1] - vb[2 * h];
+                        const fr_t ra = fr_mul(r2, fr_t{{(uint32_t)(da < 0 ? -da : da), 0, 0, 0, 0, 0, 0, 0}});
+                        const fr_t rb = fr_mul(r2, fr_t{{(uint32_t)(db < 0 ? -db : db), 0, 0, 0, 0, 0, 0, 0}});
+                        fa[h] = fr_add(fr_from_i32(va[2 * h]), da < 0 ? fr_neg(ra) : ra);
+                        fb[h] = fr_add(fr_from_i32(vb[2 * h]), db < 0 ? fr_neg(rb) : rb);
+                    }
+                    a0 = fa[0];
+                    a1 = fa[1];
+                    b0 = fb[0];
+                    b1 = fb[1];
+                    (void)x0; (void)x1; (void)x2; (void)x3; (void)z0; (void)z1; (void)z2; (void)z3;
+                } else {
                 const fr_t* sa = a.src[0] + 4 * b;
                 const fr_t* sb = a.src[1] + 4 * b;
-                const fr_t x0 = fr_load_cg(sa), x1 = fr_load_cg(sa + 1), x2 = fr_load_cg(sa + 2), x3 = fr_load_cg(sa + 3);
-                const fr_t z0 = fr_load_cg(sb), z1 = fr_load_cg(sb + 1), z2 = fr_load_cg(sb + 2), z3 = fr_load_cg(sb + 3);
+                x0 = fr_load_cg(sa); x1 = fr_load_cg(sa + 1); x2 = fr_load_cg(sa + 2); x3 = fr_load_cg(sa + 3);
+                z0 = fr_load_cg(sb); z1 = fr_load_cg(sb + 1); z2 = fr_load_cg(sb + 2); z3 = fr_load_cg(sb + 3);
                 const fr3_t f = fr_mul3_ni(r, fr_sub(x1, x0), r, fr_sub(x3, x2), r, fr_sub(z1, z0));
                 a0 = fr_add(x0, f.x);
                 a1 = fr_add(x2, f.y);
@@ -227,6 +375,10 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                     const fr3_t g2 = fr_mul3_ni(r, fr_sub(z3, z2), e, hh, zero, zero);
                     b1 = fr_add(z2, g2.x);
                     if (has_e) e = g2.y;
+                }
+                }
+                if constexpr (MODE == 3) {
+                    if (has_e && A.flat && a.eq_hi) e = fr_mul_ni(e, fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]));
                 }
                 fr_store(a.dst[0] + 2 * b, a0);
                 fr_store(a.dst[0] + 2 * b + 1, a1);
@@ -422,6 +574,7 @@ static void launch_round(zk_ctx* ctx, bool fold, unsigned int grid, const ScRoun
 void ScEngine::setup(const fr_t* const tables[3], uint32_t L_, uint32_t t0_, uint32_t n_eq_loc_) {
     factored = !(getenv("ZKDL_SC_V") && atoi(getenv("ZKDL_SC_V")) == 0);
     for (int k = 0; k < 3; k++) i32[k] = nullptr;   // set_i32 after setup (a continuation has none)
+    int0_used = false;
     L = L_;
     t0 = t0_;
     t = t0_;
@@ -467,6 +620,15 @@ void ScEngine::set_i32(const int32_t* const src[3]) {
     }
     if (!(factored && K == 2))
         for (uint32_t k = 0; k < 3; k++) i32[k] = nullptr;
+}
+
+void ScEngine::materialize() {
+    const uint32_t tl = t - t0;
+    if (!(tl == 0 || (tl == 1 && int0_used))) return;
+    for (uint32_t k = 0; k < K; k++)
+        if (i32[k]) embed_i32_dev(ctx, i32[k], 1ull << L, const_cast<fr_t*>(cur[k]));
+    for (uint32_t k = 0; k < 3; k++) i32[k] = nullptr;
+    int0_used = false;
 }
 
 void ScEngine::round(fr_t* part_out) {
@@ -525,13 +687,7 @@ void ScEngine::round(fr_t* part_out) {
         memset(&A, 0, sizeof A);
         A.r = a;
         const bool from_i32 = tl == 0 && (i32[0] || i32[1]);
-        if (from_i32) {
-            ZK_REQUIRE(i32[0] && i32[1], ZK_ERR_INTERNAL, "sumcheck: mixed int32 / Fr tables in round 0");
-            for (int k = 0; k < 2; k++) {
-                A.i32[k] = i32[k];
-                A.emb[k] = const_cast<fr_t*>(cur[k]);
-            }
-        }
+        if (from_i32) ZK_REQUIRE(i32[0] && i32[1], ZK_ERR_INTERNAL, "sumcheck: mixed int32 / Fr tables in round 0");
         // work items: (group of pairs sharing one HI value) x slices, at most two waves of 2 CTAs per SM
         const uint32_t glog = a.eq_mode ? a.lo_cnt : 0;
         const uint64_t ngroups = a.eq_mode ? ((n_pairs >> glog) ? (n_pairs >> glog) : 1) : 1;
@@ -547,12 +703,26 @@ void ScEngine::round(fr_t* part_out) {
             slices *= 2;
         A.slices = (uint32_t)slices;
         const unsigned int grid = (unsigned int)(ng * slices < cap ? ng * slices : cap);
-        if (from_i32)
+        // int32 round 0 in exact integers (grouped eq weights only; ZKDL_SC_INT0=0 disables it)
+        static const bool int0_off = getenv("ZKDL_SC_INT0") && atoi(getenv("ZKDL_SC_INT0")) == 0;
+        const bool int0 = from_i32 && a.eq_mode != 0 && !A.flat && !int0_off;
+        if (from_i32 || (tl == 1 && int0_used))
+            for (int k = 0; k < 2; k++) {
+                A.i32[k] = i32[k];
+                A.emb[k] = const_cast<fr_t*>(cur[k]);
+            }
+        if (int0) {
+            ZK_LAUNCH(ctx, k_sc_round0_int, grid, 256, 0, A);
+            int0_used = true;
+        } else if (from_i32) {
             ZK_LAUNCH(ctx, k_sc_round2f<2>, grid, 256, 0, A);
-        else if (fold)
+        } else if (fold && tl == 1 && int0_used) {
+            ZK_LAUNCH(ctx, k_sc_round2f<3>, grid, 256, 0, A);
+        } else if (fold) {
             ZK_LAUNCH(ctx, k_sc_round2f<1>, grid, 256, 0, A);
-        else
+        } else {
             ZK_LAUNCH(ctx, k_sc_round2f<0>, grid, 256, 0, A);
+        }
     } else {
         unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
         if (K == 1) launch_round<1>(ctx, fold, grid, a);
@@ -920,6 +1090,7 @@ void ScEngine::run_to_end() {
 void ScEngine::persist_rest() {
     const uint32_t tl = t - t0, mr = L - tl;
     ZK_REQUIRE(tl >= 1 && mr >= 1, ZK_ERR_INTERNAL, "sumcheck continuation: bad round");
+    materialize();
     ScAllArgs a;
     memset(&a, 0, sizeof a);
     for (uint32_t k = 0; k < K; k++) {

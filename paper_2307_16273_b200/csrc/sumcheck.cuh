@@ -45,11 +45,16 @@ struct ScEngine {
     const int32_t* i32[3] = {nullptr, nullptr, nullptr};   // int32 sources: round 0 embeds into cur[k]
     bool factored = true;   // K = 2: k_sc_round2f (ZKDL_SC_V=0: the unfactored k_sc_round)
     bool zero = false;      // N2 zero form (D22): K = 3 tables (Y, A, B), terms Y - A B, 3 evaluations
+    bool int0_used = false; // round 0 ran on the int32 tables in integers (cur[] not embedded; round 1 folds
+                            // from the int32 tables)
     uint32_t nev() const { return zero ? 3 : K + 1; }   // evaluations per round message
 
     // int32 tables: round 0 of the factored kernel embeds them into the (scratch) cur tables; otherwise
     // they are embedded here, before round 0
     void set_i32(const int32_t* const src[3]);
+    // make cur[] hold the Fr tables the next round expects (embeds int32 tables round 0 left in
+    // integers); for consumers other than round(): persist_rest, the shard export
+    void materialize();
     // local tables of 2^L entries entering at global round t0; eq over w[t0 .. t0 + n_eq_loc - 1]
     void setup(const fr_t* const tables[3], uint32_t L, uint32_t t0, uint32_t n_eq_loc);
     void header();                    // absorb "sc/hdr" (+ the given claim)
