@@ -44,7 +44,8 @@ typedef enum {
     ZK_ERR_CUDA = -5,
     ZK_ERR_NCCL = -6,
     ZK_ERR_UNIMPLEMENTED = -7,
-    ZK_ERR_INTERNAL = -8
+    ZK_ERR_INTERNAL = -8,
+    ZK_REJECT = 1               /* host verifiers: a well-formed proof that does not verify */
 } zk_status;
 
 /* ------------------------------------------------------------------ context */
@@ -256,6 +257,37 @@ zk_status zk_matmul_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, co
 zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
                             uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag);
 zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
+
+/* ------------------------------------------- host verifiers (D23)
+ * Verification replays the same sequence of rounds as proving with O(degree) field
+ * operations per round: plain host code (verify.cu), no device, no context, callable anywhere.
+ * st: a 32-byte transcript state (D3), in/out: the verifier's copy of the transcript before the
+ * proof; on return the state after it (on accept equal to the prover's zk_transcript_state).
+ * zk_htr_*: the D3 transcript on such a state (init from a seed, absorb, n challenges).
+ * Every verifier returns ZK_OK (accept), ZK_REJECT with *fail = the failing 1-based round, -100 (final
+ * identity), -1 (claim mismatch) or -101 (merge weight final), ZK_ERR_ARG (malformed proof bytes) or
+ * ZK_ERR_NONCANONICAL.  The finals in the proof are claims on the committed tensors: the caller checks
+ * them against the commitments (out of scope) or against the tensors themselves.
+ * zk_verify_sumcheck: a zk_sumcheck_prove proof (Protocol 3, D3c transcript, D4 messages); w: the
+ *   statement's n_eq eq point (host); claim: the claim the verifier expects, or NULL to take the
+ *   proof's; point_out: m elements (host, may be NULL).
+ * zk_verify_hadamard_zero: a zk_hadamard_zero_prove proof (Protocol 2 zero form, D22): round identities
+ *   from c_0 = 0, final Y~(r) - A~(r) B~(r); w_out, point_out: m elements (may be NULL).
+ * zk_verify_relu: a zk_relu_prove proof (App. A, D3b): the final identity of the six statements at the
+ *   final point with the verifier's own beta, s, s' evaluations; point_out: logB + logD elements.
+ * zk_verify_relu_merge: a zk_relu_merge proof (D21) following the zkReLU proof whose point and finals
+ *   are given: the verifier forms the claim and checks the weight final W~(r); point_out: logB + 1. */
+zk_status zk_htr_init(const uint8_t seed[32], uint8_t st[32]);
+zk_status zk_htr_absorb(uint8_t st[32], const char* tag, const void* msg, uint64_t len);
+zk_status zk_htr_challenges(uint8_t st[32], const char* tag, uint32_t n, zk_fr* out);
+zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const zk_fr* w,
+                             const zk_fr* claim, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* w_out,
+                                  zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_relu_merge(uint8_t st[32], uint32_t logD, uint32_t Q, uint32_t R, const zk_fr* relu_point,
+                               const zk_fr* relu_finals, const uint8_t* proof, uint64_t proof_len, zk_fr* point_out,
+                               int32_t* fail);
 
 /* ----------------------------------------------------------------- diagnostics
  * zk_diag_fr_op: element-wise d_out[i] = op(d_a[i], d_b[i]) on Montgomery tables, op 0 add, 1 sub,

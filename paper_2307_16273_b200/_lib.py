@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libzkdl.so")
 
 STATUS = {0: "ZK_OK", -1: "ZK_ERR_ARG", -2: "ZK_ERR_RANGE", -3: "ZK_ERR_NONCANONICAL", -4: "ZK_ERR_OOM",
-          -5: "ZK_ERR_CUDA", -6: "ZK_ERR_NCCL", -7: "ZK_ERR_UNIMPLEMENTED", -8: "ZK_ERR_INTERNAL"}
+          -5: "ZK_ERR_CUDA", -6: "ZK_ERR_NCCL", -7: "ZK_ERR_UNIMPLEMENTED", -8: "ZK_ERR_INTERNAL",
+          1: "ZK_REJECT"}
 
 
 class ZkError(RuntimeError):
@@ -97,6 +98,13 @@ def lib():
         "zk_diag_mul_bench": ([vp, vp, u32, u32, vp], i32),
         "zk_diag_rowdot": ([vp, vp, u64, u32, vp, vp, i32], i32),
         "zk_diag_fs_bench": ([vp, u32, i32, vp], i32),
+        "zk_htr_init": ([vp, vp], i32),
+        "zk_htr_absorb": ([vp, c.c_char_p, vp, u64], i32),
+        "zk_htr_challenges": ([vp, c.c_char_p, u32, vp], i32),
+        "zk_verify_sumcheck": ([vp, vp, u64, vp, vp, vp, vp], i32),
+        "zk_verify_hadamard_zero": ([vp, vp, u64, vp, vp, vp], i32),
+        "zk_verify_relu": ([vp, vp, u64, vp, vp], i32),
+        "zk_verify_relu_merge": ([vp, u32, u32, u32, vp, vp, vp, u64, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

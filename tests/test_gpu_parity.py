@@ -268,7 +268,7 @@ def test_c2_full_vs_oracle(ctx, O):
 
 
 # ---------------------------------------------------------------- C5 single sumcheck
-@pytest.mark.parametrize("m", [12, 19])
+@pytest.mark.parametrize("m", [12, 17, 19])
 def test_c5_vs_oracle(ctx, O, m):
     from oracle import drivers
     from paper_2307_16273_b200 import api
@@ -280,6 +280,32 @@ def test_c5_vs_oracle(ctx, O, m):
     g = api.sumcheck_prove(ctx, tr, m, m, [dev(A), dev(B)], w, None)
     assert g["claim"] == o["claim"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
     assert tr.state() == o["state"]
+
+
+@pytest.mark.parametrize("m,switch", [(17, None), (18, None), (18, 40), (18, 17)])
+def test_int_round0_extreme_values_vs_oracle(ctx, O, m, switch):
+    """The integer round 0 (k_sc_round0_int) and the int32 fold of round 1 at the extremes of int32:
+    P(inf) = (a1 - a0)(b1 - b0) reaches (2^32 - 1)^2 > 2^63, P(0), P(1) reach 2^62; m = 17 hands round 1
+    to the persistent tail (the int32 tables are embedded first); through the shard session, switch = 40
+    exports before round 0, switch = m - 1 exports the int32 fold after the integer round 0."""
+    from paper_2307_16273_b200 import api, shard
+    rng = random.Random(77 + m)
+    A = uniform_range(14, m, (1 << m,), -(1 << 31), 1 << 31)
+    B = uniform_range(14, m + 50, (1 << m,), -(1 << 31), 1 << 31)
+    lo, hi = np.int32(-(1 << 31)), np.int32((1 << 31) - 1)
+    A[0::4], A[1::4], B[0::4], B[1::4] = lo, hi, hi, lo        # maximal |a1 - a0|, |b1 - b0|, opposite signs
+    A[2::8], B[2::8] = lo, lo                                    # (-2^31)^2 = 2^62
+    w = [rng.randrange(P) for _ in range(m)]
+    seed = fs_seed(f"int0-{m}")
+    o = O.sumcheck_prove(O.Transcript(seed), m, m, [[int(v) % P for v in t] for t in (A, B)], w, None)
+    if switch is None:
+        g = api.sumcheck_prove(ctx, api.Transcript(ctx, seed), m, m, [dev(A), dev(B)], w, None)
+        assert g["claim"] == o["claim"] and g["msgs"] == o["msgs"] and g["finals"] == o["finals"]
+    else:
+        sess = shard.ShardSession(ctx, api.Transcript(ctx, seed), m, m, [dev(A), dev(B)], w, 0, 1)
+        r = shard.prove_virtual([sess], switch_log=switch)
+        assert r[0]["msgs"] == o["msgs"] and r[0]["finals"] == o["finals"]
+        sess.close()
 
 
 # ---------------------------------------------------------------- FCN family driver (row a9)
@@ -499,6 +525,10 @@ def test_fcn_window_full_size_vs_oracle(ctx, O, cfg):
     for T in forks:
         W.absorb("fcn/join", T.state())
     assert g[-1]["window_state"] == W.state()
+    # the library's own host verifier (N3, D23) accepts the GPU window: every family, the joins
+    from paper_2307_16273_b200 import verify
+    vo = verify.verify_window(fs_seed(seed_name), fcn.fcn_header(shape), fams, g)
+    assert [v["point"] for v in vo] == [gr["r"] if hasattr(f, "A") else gr["point"] for f, gr in zip(fams, g)]
 
 
 def test_c5_bench_size_26_properties(ctx, O):
@@ -523,6 +553,11 @@ def test_c5_bench_size_26_properties(ctx, O):
     assert ot.state() == tr.state()
     # the claim: sum_x eq(w, x) A(x) B(x) = MLE of the integer product table at w
     assert g["claim"] == O.mle_i32((A.astype(np.int64) * B).astype(np.int32), w)   # |A B| < 2^30
+    from paper_2307_16273_b200 import verify   # and the library's host verifier (N3, D23)
+    H = verify.HostTranscript(seed=fs_seed(f"C5-m{m}"))
+    H.absorb("c5/hdr", m.to_bytes(4, "little"))
+    assert H.challenges("c5/w", m) == w
+    assert verify.verify_sumcheck(H, g["proof"], w) == g["r"] and H.state() == tr.state()
 
 
 @pytest.mark.parametrize("m", [22])

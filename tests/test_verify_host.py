@@ -1,0 +1,189 @@
+"""The host verifiers of libzkdl (D23; verify.cu) on CPU (-m "not gpu").
+
+The verifiers share no code with the oracle; here they are run on the ORACLE's proofs (the GPU
+proofs are bit-identical to them, tests/test_gpu_parity.py) and must accept them, end in the oracle
+prover's transcript state, and reject tampered proofs at the round the tampering breaks.  The host
+transcript is pinned to the oracle's (itself pinned to RFC 7693 vectors, test_oracle_field.py).
+"""
+import random
+
+import numpy as np
+import pytest
+
+from synth.prng import fs_seed, uniform_range
+
+P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+
+
+@pytest.fixture(scope="module")
+def V():
+    from paper_2307_16273_b200 import build
+    build.build(verbose=False)
+    from paper_2307_16273_b200 import verify
+    return verify
+
+
+def u32s(*v):
+    return b"".join(int(x).to_bytes(4, "little") for x in v)
+
+
+def frs(vals):
+    return b"".join(int(x).to_bytes(32, "little") for x in vals)
+
+
+def sc_proof(m, n_eq, K, res):
+    return u32s(m, n_eq, K) + frs([res["claim"]]) + frs([v for row in res["msgs"] for v in row]) + frs(res["finals"])
+
+
+def relu_proof(logD, Q, R, res):
+    return u32s(logD, Q, R) + frs(res["claims"]) + frs([v for row in res["msgs"] for v in row]) + frs(res["finals"])
+
+
+def test_host_transcript_matches_oracle(V, oracle_lib):
+    O = oracle_lib
+    for seed in (b"\0" * 32, fs_seed("htr")):
+        a, b = V.HostTranscript(seed=seed), O.Transcript(seed)
+        assert a.state() == b.state()
+        for n, tag, msg in ((1, "x", b""), (3, "a/b", b"\x01" * 63), (2, "t" * 40, bytes(range(200)))):
+            a.absorb(tag, msg)
+            b.absorb(tag, msg)
+            assert a.state() == b.state()
+            assert a.challenges(tag, n) == b.challenges(tag, n)
+            assert a.state() == b.state()
+
+
+@pytest.mark.parametrize("m,n_eq,K", [(1, 0, 1), (4, 4, 2), (6, 3, 2), (5, 0, 3), (7, 7, 3)])
+def test_sumcheck_verifier_on_oracle_proofs(V, oracle_lib, m, n_eq, K):
+    O = oracle_lib
+    rng = random.Random(11 * m + K)
+    tabs = [[rng.randrange(P) for _ in range(1 << m)] for _ in range(K)]
+    w = [rng.randrange(P) for _ in range(n_eq)]
+    seed = fs_seed(f"vsc-{m}-{n_eq}-{K}")
+    T = O.Transcript(seed)
+    res = O.sumcheck_prove(T, m, n_eq, tabs, w)
+    proof = sc_proof(m, n_eq, K, res)
+    H = V.HostTranscript(seed=seed)
+    assert V.verify_sumcheck(H, proof, w) == res["r"]
+    assert H.state() == T.state()
+    assert V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, claim=res["claim"]) == res["r"]
+    # finals are the MLEs of the tables at r (what a commitment opening would close)
+    assert res["finals"] == [O.mle_fr(t, res["r"]) for t in tabs]
+    with pytest.raises(V.Rejected) as e:   # another claim
+        V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, claim=(res["claim"] + 1) % P)
+    assert e.value.where == -1
+    for t in range(m):                       # one evaluation of round t changed: round t fails
+        bad = bytearray(proof)
+        o = 44 + 32 * (t * (K + 1))
+        bad[o:o + 32] = ((int.from_bytes(bad[o:o + 32], "little") + 1) % P).to_bytes(32, "little")
+        with pytest.raises(V.Rejected) as e:
+            V.verify_sumcheck(V.HostTranscript(seed=seed), bytes(bad), w)
+        assert e.value.where == t + 1
+    bad = bytearray(proof)                   # a final changed: the final identity fails
+    bad[-1] ^= 0x01
+    with pytest.raises(V.Rejected) as e:
+        V.verify_sumcheck(V.HostTranscript(seed=seed), bytes(bad), w)
+    assert e.value.where == -100
+    with pytest.raises(ValueError):          # malformed
+        V.verify_sumcheck(V.HostTranscript(seed=seed), proof[:-1], w)
+
+
+def test_hadamard_zero_verifier(V, oracle_lib):
+    O = oracle_lib
+    m = 6
+    A = uniform_range(41, 1, (1 << m,), -(1 << 15), 1 << 15)
+    B = uniform_range(41, 2, (1 << m,), -(1 << 15), 1 << 15)
+    Y = (A.astype(np.int64) * B).astype(np.int32)
+    for bad_at in (None, 5):
+        Yx = Y.copy()
+        if bad_at is not None:
+            Yx[bad_at] += 1
+        seed = fs_seed(f"vhd-{bad_at}")
+        T = O.Transcript(seed)
+        res = O.zero_sumcheck_prove(T, Yx, A, B)
+        proof = u32s(m) + frs([v for row in res["msgs"] for v in row]) + frs(res["finals"])
+        H = V.HostTranscript(seed=seed)
+        if bad_at is None:
+            out = V.verify_hadamard_zero(H, proof)
+            assert out["w"] == res["w"] and out["r"] == res["r"] and H.state() == T.state()
+        else:
+            with pytest.raises(V.Rejected) as e:
+                V.verify_hadamard_zero(H, proof)
+            assert e.value.where == 1        # the zero claim breaks in the first round
+
+
+@pytest.mark.parametrize("logD,Q,R", [(4, 16, 16), (6, 8, 8), (5, 12, 4)])
+def test_relu_verifier_and_merge(V, oracle_lib, logD, Q, R):
+    O = oracle_lib
+    lim = 1 << (Q + R - 1)
+    Z = uniform_range(42, logD, (1 << logD,), -lim, lim)
+    GA = uniform_range(42, logD + 9, (1 << logD,), -lim, lim)
+    seed = fs_seed(f"vrelu-{logD}-{Q}-{R}")
+    T = O.Transcript(seed)
+    res = O.relu_prove(T, Z, GA, Q, R)
+    mg = O.relu_merge(T, Z, GA, Q, R, res["point"], res["finals"])
+    proof = relu_proof(logD, Q, R, res)
+    H = V.HostTranscript(seed=seed)
+    assert V.verify_relu(H, proof) == res["point"]
+    mproof = u32s(len(mg["r"]), 0, 2) + frs([mg["claim"]]) + frs([v for row in mg["msgs"] for v in row]) + frs(mg["finals"])
+    assert V.verify_relu_merge(H, logD, Q, R, res["point"], res["finals"], mproof) == mg["r"]
+    assert H.state() == T.state()
+    m = len(res["point"])
+    for t in (0, m // 2, m - 1):
+        bad = bytearray(proof)
+        o = 12 + 128 + 128 * t + 32
+        bad[o:o + 32] = ((int.from_bytes(bad[o:o + 32], "little") + 7) % P).to_bytes(32, "little")
+        with pytest.raises(V.Rejected) as e:
+            V.verify_relu(V.HostTranscript(seed=seed), bytes(bad))
+        assert e.value.where == t + 1
+    bad = bytearray(proof)                   # sigma final changed: the six-statement identity fails
+    bad[-32] ^= 0x01
+    with pytest.raises(V.Rejected) as e:
+        V.verify_relu(V.HostTranscript(seed=seed), bytes(bad))
+    assert e.value.where == -100
+    bad = bytearray(proof)                   # a claim changed: round 1 fails
+    bad[12] ^= 0x01
+    with pytest.raises(V.Rejected) as e:
+        V.verify_relu(V.HostTranscript(seed=seed), bytes(bad))
+    assert e.value.where == 1
+    H2 = V.HostTranscript(seed=seed)         # the merge's weight final
+    V.verify_relu(H2, proof)
+    badm = bytearray(mproof)
+    badm[-32] ^= 0x01
+    with pytest.raises(V.Rejected) as e:
+        V.verify_relu_merge(H2, logD, Q, R, res["point"], res["finals"], bytes(badm))
+    assert e.value.where in (-100, -101)
+
+
+def test_window_verifier_on_oracle_window(V, oracle_lib):
+    """D3d: a tiny FAC4DNN window proved by the oracle, verified family by family on forked host
+    transcripts, joins replayed; a changed family proof is caught."""
+    from oracle import drivers
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4)
+    trace = fcn.generate_trace(shape, x_bits=4, w_bits=4, y_bits=3)
+    fams = fcn.assemble_families(shape, trace)
+    o = drivers.fcn_prove(shape, fams, "vwin", merge_aux=True)
+    results = []
+    for f, r in zip(fams, o):
+        r = dict(r)
+        if hasattr(f, "A"):
+            lN, l1, l2, l3 = r["logs"]
+            r["proof"] = sc_proof(lN + l2, lN, 2, r)
+        else:
+            logD = int(f.Z.size).bit_length() - 1
+            r["proof"] = relu_proof(logD, f.Q, f.R, r)
+            mg = r["merge"]
+            r["merge"] = dict(mg, proof=u32s(len(mg["r"]), 0, 2) + frs([mg["claim"]]) +
+                              frs([v for row in mg["msgs"] for v in row]) + frs(mg["finals"]))
+        results.append(r)
+    out = V.verify_window(fs_seed("vwin"), fcn.fcn_header(shape), fams, results)
+    assert [x["name"] for x in out] == [f.name for f in fams]
+    for x, r in zip(out, o):
+        assert x["point"] == (r["r"] if "r" in r and "point" not in r else r["point"])
+    k = next(i for i, f in enumerate(fams) if hasattr(f, "A"))
+    bad = dict(results[k])
+    pb = bytearray(bad["proof"])
+    pb[44] ^= 0x01
+    bad["proof"] = bytes(pb)
+    with pytest.raises(V.Rejected):
+        V.verify_window(fs_seed("vwin"), fcn.fcn_header(shape), fams, results[:k] + [bad] + results[k + 1:])
