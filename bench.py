@@ -445,11 +445,12 @@ def c5_frmul_model(m: int, tail_log: int = 16, hb: int = 5) -> dict:
     """Algorithmic Fr-mul count of one C5 proof (K = 2, n_eq = m) by kernel, mirroring
     sumcheck.cu: round 0 (k_sc_round0_int, grouped eq weights): no Fr product per pair -- three exact
     integer multiply-accumulates E' x (P + 2^64) into 352-bit accumulators, reduced once per CTA and
-    group ("int_mac_per_pair"); round 1 (k_sc_round2f folding from int32): 4 embeddings + 4 r |d|
-    (half a product each) + E' a (2) + 3 = 9; folding rounds: fold 4 + 2 + 3 = 9 (plus one HI product
+    group ("int_mac_per_pair"); round 1 (k_sc_round2f folding from int32): 4 folds, each two 32 x 256-bit
+    multiply-accumulates and one reduction (3/4 of a product) + E' a (2) + 3 = 8; folding rounds: fold 4 + 2 + 3 = 9 (plus one HI product
     per pair where the groups are too small, "flat"); the last rounds (<= 2^tail_log entries after the
     fold) in k_sc_all: fold 4 + eq 1 + 3 x 2 = 11 per pair (7 in the last, eq-free round)."""
     out = {"k_sc_round2f": 0, "k_sc_all": 0, "k_sc_round0_int": 0}
+    int0 = False
     for t in range(m):
         pairs = 1 << (m - t - 1)
         if t >= 1 and m - t <= tail_log:
@@ -461,8 +462,9 @@ def c5_frmul_model(m: int, tail_log: int = 16, hb: int = 5) -> dict:
         flat = nv > hbe and nv - hbe < 10    # LO x HI with groups < 1024 pairs: per-pair HI product
         if t == 0 and nv > hbe and not flat:
             out["int_mac_per_pair"] = 3
+            int0 = True
             continue
-        per = 7 if t == 0 else 9
+        per = 7 if t == 0 else (8 if t == 1 and int0 else 9)
         out["k_sc_round2f"] += pairs * (per + (1 if flat else 0))
     out["total"] = out["k_sc_round2f"] + out["k_sc_all"]
     return out

@@ -223,12 +223,42 @@ __device__ __forceinline__ void add9(uint32_t (&s)[9], const fr_t& e) {
     }
     s[8] += (uint32_t)C;
 }
-// Montgomery reduction of an 11-limb integer T < 2^352 (< p 2^256): T R^{-1} mod p
+// Montgomery reduction of an 11-limb integer T (< p 2^256): T R^{-1} mod p.  T = lo9 + w9 2^288 + w10 2^320 and
+// 2^288 R^{-1} = 2^32, 2^320 R^{-1} = 2^64, so REDC(T) = REDC(lo9) + (w9 2^32 + w10 2^64) (the second term
+// < 2^96 < p; fr_redc_wide's top limb stays zero, so its carry into t[8] cannot wrap)
 __device__ __noinline__ fr_t fr_redc11(const uint32_t (&w)[11]) {
-    // T = lo10 + w10 2^320:  REDC(T) = REDC(lo10) + w10 2^64 (2^320 R^{-1} = 2^64)
-    const uint32_t lo[10] = {w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], w[9]};
+    const uint32_t lo[10] = {w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], w[8], 0};
     const fr_t x = fr_redc_wide(lo);
-    return fr_add(x, fr_t{{0, 0, w[10], 0, 0, 0, 0, 0}});   // w10 2^64 < p, already reduced
+    return fr_add(x, fr_t{{0, w[9], w[10], 0, 0, 0, 0, 0}});
+}
+
+// Round 1 after the integer round 0: the fold v0 + r (v1 - v0) of an int32 pair, straight to Montgomery
+// form.  With u = v + 2^31 in [0, 2^32):  x = (1 - r) u0 + r u1 - 2^31, so
+//     I = u0 [(1 - r) R^2] + u1 [r R^2] + [-2^31 R^2]     (residues < p; I < 2^33 p < 2^300)
+// and REDC(I) = x R: two 32 x 256-bit multiply-accumulates and one reduction per value instead of two
+// half products.  Four values per call, out of line (one body for every call site: I-cache).
+struct FoldI32 { fr_t omr2, r2, cneg; };
+__device__ __forceinline__ void mac32(uint32_t (&w)[10], const fr_t& e, uint32_t u) {
+    uint64_t C = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t t = (uint64_t)e.v[j] * u + w[j] + C;
+        w[j] = (uint32_t)t;
+        C = t >> 32;
+    }
+    const uint64_t t = (uint64_t)w[8] + C;
+    w[8] = (uint32_t)t;
+    w[9] += (uint32_t)(t >> 32);
+}
+__device__ __forceinline__ fr_t fold_i32(const FoldI32& f, int32_t v0, int32_t v1) {
+    uint32_t w[10] = {f.cneg.v[0], f.cneg.v[1], f.cneg.v[2], f.cneg.v[3], f.cneg.v[4], f.cneg.v[5], f.cneg.v[6],
+                      f.cneg.v[7], 0, 0};
+    mac32(w, f.omr2, (uint32_t)v0 ^ 0x80000000u);
+    mac32(w, f.r2, (uint32_t)v1 ^ 0x80000000u);
+    return fr_redc_wide(w);
+}
+static __device__ __noinline__ fr4_t fold4_i32_ni(const FoldI32& f, int4 x, int4 y) {
+    return fr4_t{fold_i32(f, x.x, x.y), fold_i32(f, x.z, x.w), fold_i32(f, y.x, y.y), fold_i32(f, y.z, y.w)};
 }
 
 // Montgomery form of 2^64 (= 2^64 R mod p), derived with Python integers
@@ -310,9 +340,14 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     const uint64_t slice_len = (gsize + slices - 1) / slices;
     const uint64_t next_count = lo_cnt ? (1ull << (lo_cnt - 1)) : 0;
     const uint64_t hi_mask = (1ull << a.hb) - 1;
-    fr_t r, r2;
+    fr_t r;
     if (FOLD) r = fr_load(a.r_prev);
-    if (MODE == 3) r2 = fr_mul(r, ZK_R2);   // r R^2: fr_mul(r2, k) = Montgomery(r k) for a one-limb integer k
+    FoldI32 fi;
+    if (MODE == 3) {   // residues (1 - r) R^2, r R^2, -2^31 R^2 (fr_mul(x R, R^2) = x R^2)
+        fi.r2 = fr_mul(r, ZK_R2);
+        fi.omr2 = fr_mul(fr_sub(fr_one(), r), ZK_R2);
+        fi.cneg = fr_mul(fr_neg(fr_from_u32(0x80000000u)), ZK_R2);
+    }
     fr_t tot0 = fr_zero(), tot1 = fr_zero(), toti = fr_zero();
     const uint64_t nitems = (A.flat ? 1 : ngroups) * slices;
     const uint64_t lo_mask = (1ull << lo_cnt) - 1;
@@ -337,25 +372,14 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
             bool q_done = false;
             if (FOLD) {
                 fr_t x0, x1, x2, x3, z0, z1, z2, z3;
-                if constexpr (MODE == 3) {
-                    // v0 + r (v1 - v0) from int32: the embedding of v0 and r |v1 - v0| are products with a
-                    // one-limb operand (half a full product each); x1 / x3 carry r (v1 - v0) directly
+                if constexpr (MODE == 3) {   // fold straight from the int32 tables (fold4_i32_ni)
                     const int4 ia = __ldcs(reinterpret_cast<const int4*>(A.i32[0]) + b);
                     const int4 ib = __ldcs(reinterpret_cast<const int4*>(A.i32[1]) + b);
-                    const int32_t va[4] = {ia.x, ia.y, ia.z, ia.w}, vb[4] = {ib.x, ib.y, ib.z, ib.w};
-                    fr_t fa[2], fb[2];
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        const int64_t da = (int64_t)va[2 * h + 1] - va[2 * h], db = (int64_t)vb[2 * h + 1] - vb[2 * h];
-                        const fr_t ra = fr_mul(r2, fr_t{{(uint32_t)(da < 0 ? -da : da), 0, 0, 0, 0, 0, 0, 0}});
-                        const fr_t rb = fr_mul(r2, fr_t{{(uint32_t)(db < 0 ? -db : db), 0, 0, 0, 0, 0, 0, 0}});
-                        fa[h] = fr_add(fr_from_i32(va[2 * h]), da < 0 ? fr_neg(ra) : ra);
-                        fb[h] = fr_add(fr_from_i32(vb[2 * h]), db < 0 ? fr_neg(rb) : rb);
-                    }
-                    a0 = fa[0];
-                    a1 = fa[1];
-                    b0 = fb[0];
-                    b1 = fb[1];
+                    const fr4_t fv = fold4_i32_ni(fi, ia, ib);
+                    a0 = fv.a;
+                    a1 = fv.b;
+                    b0 = fv.c;
+                    b1 = fv.d;
                     (void)x0; (void)x1; (void)x2; (void)x3; (void)z0; (void)z1; (void)z2; (void)z3;
                 } else {
                 const fr_t* sa = a.src[0] + 4 * b;
