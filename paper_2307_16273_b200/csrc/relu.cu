@@ -596,6 +596,10 @@ struct IRoundArgs {
     uint8_t* msg_out;
     fr_t* r_out;
     uint8_t* point_out;
+    // MODE 2 / 3 of k_relu_iround_f: the int32 words (Z, G_A) and the byte table of k_relu_jrounds
+    const int32_t* words[2];
+    const fr_t* byte_tab;
+    uint32_t qr_mask, sig_bit, nbytes;
 };
 
 // Finalizer of an i-round (last block, after the grid reduction), in two parts so that the persistent
@@ -803,11 +807,26 @@ struct IPtrs {   // one side's view of a round (L2 loads: the persistent kernel 
     fr_t* nxA;
     fr_t* nxC;
     fr_t* nxB;   // null on side 1
+    // SRC = 1 (rounds 0 and 1 from the int32 words, no materialised tables): this side's word (Z or G_A),
+    // the Z words (sign bits), the byte tables in shared memory ([nbytes][256]; round 1: (1 - r_0) T then
+    // r_0 T), the masks
+    const int32_t* W;
+    const int32_t* Zw;
+    const fr_t* tb;
+    uint32_t qr_mask, sig_bit, nbytes;
 };
+
+// a(i) = sum_j beta(r_j, j) bit_j(w_i) as byte-table lookups (the table rows of k_relu_materialize)
+__device__ __forceinline__ fr_t byte_sum(const fr_t* tb, uint32_t w, const IPtrs& q) {
+    const uint32_t x = w & q.qr_mask;
+    fr_t acc = tb[x & 255];
+    for (uint32_t k = 1; k < q.nbytes; k++) acc = fr_add(acc, tb[k * 256 + ((x >> (8 * k)) & 255)]);
+    return acc;
+}
 
 // Accumulate this thread's pairs j = j0, j0 + js, ... < P_blk of HI block h into T[0..7] =
 // (T_a(0), T_a(1), T_c(0), T_c(1), T_c(inf), T_b(0), T_b(1), T_b(inf)) of its side.
-template <bool FOLD>
+template <bool FOLD, int SRC = 0>
 __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint32_t h, uint32_t pb, uint64_t j0,
                                              uint64_t js, const int side, fr_t (&T)[8]) {
     const fr_t one = fr_one();
@@ -816,7 +835,31 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
         const uint64_t b = ((uint64_t)h << pb) + j;
         fr_t a0, a1, om0, om1;
         int o0 = 0, o1 = 0;
-        if (FOLD) {
+        if constexpr (SRC == 1 && FOLD) {
+            // round 1 from the words: the fold by r_0 of entries (4b, 4b+1) and (4b+2, 4b+3) is a sum of
+            // lookups in (1 - r_0) T and r_0 T; oms folds to 0, 1 - r_0, r_0 or 1
+            const int4 w4 = __ldcs(reinterpret_cast<const int4*>(q.W) + b);
+            const int4 z4 = side ? __ldcs(reinterpret_cast<const int4*>(q.Zw) + b) : w4;
+            const fr_t* t1 = q.tb + q.nbytes * 256;
+            a0 = fr_add(byte_sum(q.tb, (uint32_t)w4.x, q), byte_sum(t1, (uint32_t)w4.y, q));
+            a1 = fr_add(byte_sum(q.tb, (uint32_t)w4.z, q), byte_sum(t1, (uint32_t)w4.w, q));
+            const uint32_t zA = (uint32_t)(side ? z4.z : z4.x), zB = (uint32_t)(side ? z4.w : z4.y);
+            const bool oA = !((zA >> q.sig_bit) & 1), oB = !((zB >> q.sig_bit) & 1);
+            const fr_t mine = oA ? (oB ? fr_one() : fr_sub(fr_one(), r)) : (oB ? r : fr_zero());
+            fr_store(q.dstA + 2 * b, a0);
+            fr_store(q.dstA + 2 * b + 1, a1);
+            fr_store(q.dstO + 2 * b + side, mine);
+            const fr_t other = fr_shfl_xor(mine, 1, __activemask());
+            om0 = side ? other : mine;
+            om1 = side ? mine : other;
+        } else if constexpr (SRC == 1) {   // round 0 from the words
+            const int2 w2 = __ldcs(reinterpret_cast<const int2*>(q.W) + b);
+            const int2 z2 = side ? __ldcs(reinterpret_cast<const int2*>(q.Zw) + b) : w2;
+            a0 = byte_sum(q.tb, (uint32_t)w2.x, q);
+            a1 = byte_sum(q.tb, (uint32_t)w2.y, q);
+            o0 = !(((uint32_t)z2.x >> q.sig_bit) & 1);
+            o1 = !(((uint32_t)z2.y >> q.sig_bit) & 1);
+        } else if (FOLD) {
             const fr_t* s = q.srcA + 4 * b;
             const fr_t y0 = fr_load_l2(s), y1 = fr_load_l2(s + 1), y2 = fr_load_l2(s + 2), y3 = fr_load_l2(s + 3);
             // oms fold shared by the pair's two lanes: side s folds entry s and stores it
@@ -963,8 +1006,11 @@ __device__ __noinline__ void iround_g(const fr_t* tot, const fr_t* const* u, uin
     __syncthreads();
 }
 
-template <bool FOLD>
+// MODE: bit 0 = FOLD, bit 1 = SRC (rounds 0 / 1 from the int32 words through byte tables in shared memory)
+template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_relu_iround_f(IRoundArgs a) {
+    constexpr bool FOLD = MODE & 1;
+    constexpr int SRC = MODE >> 1;
     const int side = threadIdx.x & 1;
     const uint32_t pb = a.lo_cnt - 1;   // log2 of the pairs per HI block
     const uint32_t h = blockIdx.x / a.cpb, cib = blockIdx.x % a.cpb;
@@ -981,11 +1027,32 @@ __global__ void __launch_bounds__(256, 2) k_relu_iround_f(IRoundArgs a) {
     q.nxB = side ? nullptr : a.lo_next[4];
     fr_t r;
     if (FOLD) r = fr_load(a.r_prev);
+    if constexpr (SRC == 1) {   // byte tables into shared memory (round 1: scaled by 1 - r_0 and r_0)
+        extern __shared__ fr_t tbs[];
+        const uint32_t n = a.nbytes * 256;
+        const fr_t omr = fr_sub(fr_one(), r);
+        for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+            const fr_t v = fr_load(&a.byte_tab[e]);
+            if (FOLD) {
+                tbs[e] = fr_mul_ni(v, omr);
+                tbs[n + e] = fr_mul_ni(v, r);
+            } else {
+                tbs[e] = v;
+            }
+        }
+        __syncthreads();
+        q.W = side ? a.words[1] : a.words[0];
+        q.Zw = a.words[0];
+        q.tb = tbs;
+        q.qr_mask = a.qr_mask;
+        q.sig_bit = a.sig_bit;
+        q.nbytes = a.nbytes;
+    }
     fr_t T[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) T[k] = fr_zero();
     const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
-    iround_pairs<FOLD>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+    iround_pairs<FOLD, SRC>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
     fr_t v[16];
     iround_scale_scatter(T, a.hi, h, side, j0 < (1ull << pb), v);
     __shared__ fr_t sm[8 * 16];
@@ -1359,11 +1426,6 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     ja.kappa = kappa;
     ZK_LAUNCH(ctx, k_relu_jrounds, 1, 256, 0, ja);
 
-    // ---- i-phase tables
-    fr_t* full[3];
-    for (int k = 0; k < 3; k++) full[k] = s.alloc<fr_t>(D);
-    ZK_LAUNCH(ctx, k_relu_materialize, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, qr_mask, QR - 1, nbytes,
-              (const fr_t*)byte_tab, full[0], full[1], full[2]);
     const uint32_t hb = logD < 5 ? logD : 5;
     const uint32_t H = logD - hb;
     fr_t* HIs[6];
@@ -1393,7 +1455,6 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     unsigned int max_grid = (unsigned int)ctx->num_sms * 4;   // >= the factored kernel's grid (cap above)
     fr_t* partials = s.alloc<fr_t>((size_t)max_grid * 13);
     unsigned int* ticket = s.alloc_zero<unsigned int>(1);
-    const fr_t* cur[3] = {full[0], full[1], full[2]};
     int lo_level = 0;
     // A/B switches (read per call, so tests can cover every path in one process): ZKDL_IROUND_V=0 the
     // unfactored round kernel; rounds with at most 2^ZKDL_IPERSIST_LOG pairs (default 16, < 0: none) run
@@ -1408,6 +1469,23 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
                 t0 = t;
                 break;
             }
+    // ---- i-phase tables: rounds 0 and 1 of the factored kernel read the int32 words through the byte table
+    // (MODE 2 / 3 of k_relu_iround_f); the Fr tables a0, a1, oms are materialised only for the other paths
+    // (ZKDL_RELU_WORDS=0 forces them)
+    static const bool words_off = getenv("ZKDL_RELU_WORDS") && atoi(getenv("ZKDL_RELU_WORDS")) == 0;
+    const bool words = !unfactored && t0 >= 2 && !words_off;
+    fr_t* full[3] = {nullptr, nullptr, nullptr};
+    if (!words) {
+        for (int k = 0; k < 3; k++) full[k] = s.alloc<fr_t>(D);
+        ZK_LAUNCH(ctx, k_relu_materialize, grid_for(ctx, D, 256, 8), 256, 0, Z, GA, D, qr_mask, QR - 1, nbytes,
+                  (const fr_t*)byte_tab, full[0], full[1], full[2]);
+    }
+    const fr_t* cur[3] = {full[0], full[1], full[2]};
+    const size_t tb_smem = 2ull * nbytes * 256 * sizeof(fr_t);
+    if (words) {
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
+    }
     for (uint32_t t = 0; t < t0; t++) {
         IRoundArgs a;
         memset(&a, 0, sizeof a);
@@ -1453,10 +1531,22 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
             if (cpb < 1) cpb = 1;
             a.cpb = (uint32_t)cpb;
             const unsigned int grid = (unsigned int)(cpb << hb);
-            if (fold)
-                ZK_LAUNCH(ctx, k_relu_iround_f<true>, grid, ithreads, 0, a);
-            else
-                ZK_LAUNCH(ctx, k_relu_iround_f<false>, grid, ithreads, 0, a);
+            if (words && t <= 1) {
+                a.words[0] = Z;
+                a.words[1] = GA;
+                a.byte_tab = byte_tab;
+                a.qr_mask = qr_mask;
+                a.sig_bit = QR - 1;
+                a.nbytes = nbytes;
+                if (fold)
+                    ZK_LAUNCH(ctx, k_relu_iround_f<3>, grid, ithreads, tb_smem, a);
+                else
+                    ZK_LAUNCH(ctx, k_relu_iround_f<2>, grid, ithreads, tb_smem / 2, a);
+            } else if (fold) {
+                ZK_LAUNCH(ctx, k_relu_iround_f<1>, grid, ithreads, 0, a);
+            } else {
+                ZK_LAUNCH(ctx, k_relu_iround_f<0>, grid, ithreads, 0, a);
+            }
         }
         lo_level ^= 1;
         if (fold)
