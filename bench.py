@@ -197,10 +197,12 @@ def frmul_model(fams, persist_log: int = 16, hb: int = 5) -> dict:
         H = logD - min(hb, logD)
         t0 = next((t for t in range(1, H) if (D >> (t + 1)) <= (1 << persist_log)), H)
         # factored i-round, per pair (two sides): first round 2 x (6 E'a + 3 T_b) = 18; folding rounds
-        # 2 x (3 fold + 6 E'a + 3 T_c + 3 T_b) = 30; plus 8 HI' products per thread and launch (not counted)
+        # 2 x (3 fold + 6 E'a + 3 T_c + 3 T_b) = 30, round 1 from the words (t0 >= 2) without the 3 fold
+        # products (byte tables scaled by 1 - r_0, r_0) = 24; plus 8 HI' products per thread and launch
+        # (not counted)
         for t in range(H):
             pairs = D >> (t + 1)
-            per = 18 if t == 0 else 30
+            per = 18 if t == 0 else (24 if t == 1 and t0 >= 2 else 30)
             out["k_relu_iround_f" if t < t0 else "k_relu_ipersist"] += per * pairs
     for f in fams:
         if hasattr(f, "A"):
@@ -386,7 +388,7 @@ def run_ours(args, rank, world, local):
               "share_of_step": round(dom_ms / ms_local * args.steps, 4) if ms_local else None}
     rf["launches_per_step"] = dom_launches
     try:   # DRAM traffic of the dominant kernel's captured launch (ncu --set full, committed under profiles/)
-        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r1h.json")))
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r1j.json")))
         base = dom_name.split("<")[0]
         if base in tj:
             L0 = tj[base]["launches"][0]
@@ -549,6 +551,14 @@ def run_c5(args, rank, world, local):
                   "unit": "GFr-mul/s", "frac": round(ach / peak, 4), "traffic": None, "launches_per_proof": n,
                   "ms_per_proof": round(kms, 4), "share_of_step": round(kms / r["ms"], 4),
                   "durations": "CUDA events around every launch of one more proof after the timed region"}
+            try:   # DRAM traffic of a captured launch at m = 26 (ncu --set full, committed under profiles/)
+                L0 = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r1j.json")))["k_sc_round2f"]["launches"][0]
+                if args.c5_log == 26:
+                    rf["traffic"] = L0["dram_read"] + L0["dram_write"]
+                    rf["traffic_note"] = (f"bytes of one captured launch ({L0['launch']}) against {L0['algorithmic']} "
+                                          f"algorithmic bytes ({L0['algorithmic_note']})")
+            except (OSError, ValueError, KeyError):
+                pass
     out = {"metric": f"C5 sharded sumcheck: prover s per 2^{args.c5_log} product sumcheck (K=2, eq over all variables)",
            "value": r["ms"] / 1000.0, "unit": "s/proof", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": r["ms"], "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
