@@ -236,7 +236,7 @@ __device__ __noinline__ fr_t fr_redc11(const uint32_t (&w)[11]) {
 // form.  With u = v + 2^31 in [0, 2^32):  x = (1 - r) u0 + r u1 - 2^31, so
 //     I = u0 [(1 - r) R^2] + u1 [r R^2] + [-2^31 R^2]     (residues < p; I < 2^33 p < 2^300)
 // and REDC(I) = x R: two 32 x 256-bit multiply-accumulates and one reduction per value instead of two
-// half products.  Four values per call, out of line (one body for every call site: I-cache).
+// half products.  Out of line, two values per call (a small body shared by both call sites: I-cache).
 struct FoldI32 { fr_t omr2, r2, cneg; };
 __device__ __forceinline__ void mac32(uint32_t (&w)[10], const fr_t& e, uint32_t u) {
     uint64_t C = 0;
@@ -257,8 +257,9 @@ __device__ __forceinline__ fr_t fold_i32(const FoldI32& f, int32_t v0, int32_t v
     mac32(w, f.r2, (uint32_t)v1 ^ 0x80000000u);
     return fr_redc_wide(w);
 }
-static __device__ __noinline__ fr4_t fold4_i32_ni(const FoldI32& f, int4 x, int4 y) {
-    return fr4_t{fold_i32(f, x.x, x.y), fold_i32(f, x.z, x.w), fold_i32(f, y.x, y.y), fold_i32(f, y.z, y.w)};
+struct fr2_t { fr_t a, b; };
+static __device__ __noinline__ fr2_t fold2_i32_ni(const FoldI32& f, int4 x) {   // two values per call: a small body
+    return fr2_t{fold_i32(f, x.x, x.y), fold_i32(f, x.z, x.w)};
 }
 
 // Montgomery form of 2^64 (= 2^64 R mod p), derived with Python integers
@@ -375,11 +376,11 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                 if constexpr (MODE == 3) {   // fold straight from the int32 tables (fold4_i32_ni)
                     const int4 ia = __ldcs(reinterpret_cast<const int4*>(A.i32[0]) + b);
                     const int4 ib = __ldcs(reinterpret_cast<const int4*>(A.i32[1]) + b);
-                    const fr4_t fv = fold4_i32_ni(fi, ia, ib);
-                    a0 = fv.a;
-                    a1 = fv.b;
-                    b0 = fv.c;
-                    b1 = fv.d;
+                    const fr2_t fa = fold2_i32_ni(fi, ia), fb = fold2_i32_ni(fi, ib);
+                    a0 = fa.a;
+                    a1 = fa.b;
+                    b0 = fb.a;
+                    b1 = fb.b;
                     (void)x0; (void)x1; (void)x2; (void)x3; (void)z0; (void)z1; (void)z2; (void)z3;
                 } else {
                 const fr_t* sa = a.src[0] + 4 * b;
