@@ -46,8 +46,7 @@ void matmul_reduce_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* A, const i
     eq_table_r2_dev(ctx, u3, l3, E3, s);
     // At[k][n]
     if (!sh.trans_a) {   // A stored [N][D1][D2]: column sums over a
-        ZK_LAUNCH(ctx, k_colsum_i32<LoadPlain>, grid_for(ctx, N * D2, 256, 8), 256, 0, LoadPlain{A}, N, (uint32_t)D1,
-                  (uint32_t)D2, E1, At);
+        colsum_i32(ctx, A, N, (uint32_t)D1, (uint32_t)D2, E1, At, s);
     } else if (rowdot_tc_ok(N * D2, (uint32_t)D1)) {   // A stored [N][D2][D1]: row dots on the tensor cores
         rowdot_tc(ctx, A, N * D2, (uint32_t)D1, E1, At, D2, l2, N, s);
     } else {             // one warp per (n, k) row
@@ -61,8 +60,7 @@ void matmul_reduce_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* A, const i
         ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, grid_for(ctx, N * D2 * 32, 256, 8), 256, 0, LoadPlain{B}, N * D2,
                   (uint32_t)D3, E3, Bt, D2, l2, N);
     } else {             // B stored [N][D3][D2]: column sums over c
-        ZK_LAUNCH(ctx, k_colsum_i32<LoadPlain>, grid_for(ctx, N * D2, 256, 8), 256, 0, LoadPlain{B}, N, (uint32_t)D3,
-                  (uint32_t)D2, E3, Bt);
+        colsum_i32(ctx, B, N, (uint32_t)D3, (uint32_t)D2, E3, Bt, s);
     }
     // claim
     fr_t* Ew = s.alloc<fr_t>(N);

@@ -353,4 +353,35 @@ void mul_bench_dev(zk_ctx* ctx, const fr_t* seed, uint32_t iters, uint32_t block
     ZK_LAUNCH(ctx, k_mul_bench, blocks, 256, 0, seed, iters, out);
 }
 
+__global__ void k_colsum_finish(const uint32_t* partials, uint64_t N, uint32_t cols, uint32_t S, fr_t* out) {
+    const uint64_t outputs = N * cols;
+    for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < outputs; o += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t acc[10];
+#pragma unroll
+        for (int k = 0; k < 10; k++) acc[k] = partials[o * 10 + k];
+        for (uint32_t sp = 1; sp < S; sp++) {
+            uint32_t b[10];
+#pragma unroll
+            for (int k = 0; k < 10; k++) b[k] = partials[(sp * outputs + o) * 10 + k];
+            wide_add10(acc, b);
+        }
+        const uint64_t n = o / cols, c = o % cols;
+        fr_store(&out[c * N + n], wide_finish(acc));
+    }
+}
+
+void colsum_i32(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
+                Scratch& s) {
+    // 128-thread CTAs, up to 7 resident per SM (70 registers): size the work to about one wave
+    const uint64_t outputs = N * cols, slots = (uint64_t)ctx->num_sms * 7 * 128;
+    uint32_t S = 1;
+    while ((uint64_t)S * 2 * outputs <= slots && rows / (S * 2) >= 32 && rows % (S * 2) == 0) S *= 2;
+    uint32_t* partials = S > 1 ? s.alloc<uint32_t>(outputs * S * 10) : nullptr;
+    const uint64_t items = outputs * S;
+    const uint64_t blocks = (items + 127) / 128;
+    const unsigned int grid = (unsigned int)(blocks < (uint64_t)ctx->num_sms * 7 ? blocks : (uint64_t)ctx->num_sms * 7);
+    ZK_LAUNCH(ctx, k_colsum_i32<LoadPlain>, grid, 128, 0, LoadPlain{M}, N, rows, cols, E2, out, S, partials);
+    if (S > 1) ZK_LAUNCH(ctx, k_colsum_finish, grid_for(ctx, outputs, 256, 4), 256, 0, (const uint32_t*)partials, N, cols, S, out);
+}
+
 }  // namespace zk

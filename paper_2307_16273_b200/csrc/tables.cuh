@@ -122,34 +122,49 @@ __global__ void __launch_bounds__(256) k_rowdot_i32(Load load, uint64_t nrows, u
     }
 }
 
-// One thread per (n, c) of M[N][rows][cols]: out[c * N + n] = sum_r eq[r] * M[n][r][c] (E2 double Montgomery).
+// Work item (s, n, c) of M[N][rows][cols] (c fastest): the lazy sum over rows [s rows/S, (s+1) rows/S) of
+// eq[r] * M[n][r][c] (E2 double Montgomery).  S = 1: out[c * N + n] directly; S > 1: the 10-limb partial
+// to partials[item] (exact integers, summed by k_colsum_finish).  Sixteen loads in flight per thread and
+// two lazy accumulators (even / odd rows), so consecutive MACs are independent carry chains.
 template <class Load>
-__global__ void __launch_bounds__(256) k_colsum_i32(Load load, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2,
-                                                    fr_t* out) {
-    const uint64_t total = N * cols;
+__global__ void __launch_bounds__(128) k_colsum_i32(Load load, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2,
+                                                    fr_t* out, uint32_t S, uint32_t* partials) {
+    const uint64_t outputs = N * cols, total = outputs * S;
+    const uint32_t chunk = rows / S;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t n = t / cols, c = t % cols;
+        const uint64_t o = t % outputs, n = o / cols, c = o % cols;
+        const uint32_t sp = (uint32_t)(t / outputs), r0 = sp * chunk, r1 = r0 + chunk;
         uint32_t acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t acc2[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         const uint64_t base = n * (uint64_t)rows * cols + c;
-        uint32_t r = 0;
-        for (; r + 7 < rows; r += 8) {   // eight loads in flight (see k_rowdot_i32)
-            uint32_t u[8];
+        uint32_t r = r0;
+        for (; r + 15 < r1; r += 16) {
+            uint32_t u[16];
 #pragma unroll
-            for (int k = 0; k < 8; k++) u[k] = (uint32_t)load(base + (uint64_t)(r + k) * cols) + 0x80000000u;
+            for (int k = 0; k < 16; k++) u[k] = (uint32_t)load(base + (uint64_t)(r + k) * cols) + 0x80000000u;
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const fr_t e = fr_load(&E2[r + k]);
-                ZK_MAC_WIDE(acc, e, u[k]);
+            for (int k = 0; k < 16; k += 2) {
+                const fr_t e0 = fr_load(&E2[r + k]), e1 = fr_load(&E2[r + k + 1]);
+                ZK_MAC_WIDE(acc, e0, u[k]);
+                ZK_MAC_WIDE(acc2, e1, u[k + 1]);
             }
         }
-        for (; r < rows; r++) {
+        for (; r < r1; r++) {
             uint32_t u = (uint32_t)load(base + (uint64_t)r * cols) + 0x80000000u;
             fr_t e = fr_load(&E2[r]);
             ZK_MAC_WIDE(acc, e, u);
         }
-        fr_store(&out[c * N + n], wide_finish(acc));
+        wide_add10(acc, acc2);
+        if (S == 1) {
+            fr_store(&out[c * N + n], wide_finish(acc));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 10; k++) partials[t * 10 + k] = acc[k];
+        }
     }
 }
+// out[c * N + n] = finish(sum_s partials[(s, n, c)])
+__global__ void k_colsum_finish(const uint32_t* partials, uint64_t N, uint32_t cols, uint32_t S, fr_t* out);
 
 // Grid reduction of sum_i a[i] * b[i] (Fr); the last block writes the result to *out.
 __global__ void k_dot_fr(const fr_t* a, const fr_t* b, uint64_t n, fr_t* partials, unsigned int* ticket, fr_t* out);
@@ -157,6 +172,10 @@ __global__ void k_dot_fr(const fr_t* a, const fr_t* b, uint64_t n, fr_t* partial
 // Host helpers (tables.cu)
 // MLE of an int32 table viewed through a loader, at a device point (Montgomery); result to d_out (Montgomery).
 void mle_i32_plain(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s);
+// Column sums out[c * N + n] = sum_r E2[r] M[n][r][c] of an int32 stack (k_colsum_i32): one wave of 128-thread
+// CTAs, the rows split into S chunks (partials summed by k_colsum_finish) when there are few outputs.
+void colsum_i32(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
+                Scratch& s);
 void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ*/, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m,
                   const fr_t* d_u, fr_t* d_out, Scratch& s);
 // Row dots out[map(r)] = sum_c M[r][c] E2[c] of an int32 matrix on the tensor cores (restrict_tc.cu): same
