@@ -56,6 +56,7 @@ def lib():
                                        c.c_int, c.c_int, vp, vp, vp, vp]
         L.or_relu_tables.argtypes = [i32p, i32p, c.c_uint64, c.c_uint32, c.c_uint32] + [vp] * 7
         L.or_relu_prove.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp]
+        L.or_loss_grad_prove.argtypes = [vp, c.c_uint32, i32p, i32p, i32p, vp, vp]
         L.or_relu_verify.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp]
         L.or_reindex_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp,
                                        vp, vp, vp, vp]
@@ -344,3 +345,16 @@ def zero_sumcheck_prove(tr: Transcript, Y: np.ndarray, A: np.ndarray, B: np.ndar
     flat = from_bytes(msgs.raw[:96 * m])
     return dict(w=from_bytes(w.raw[:32 * m], m), msgs=[flat[3 * t:3 * t + 3] for t in range(m)],
                 r=from_bytes(r.raw[:32 * m], m), finals=from_bytes(fin.raw[:96], 3))
+
+
+# ---------------------------------------------------------------- N2: the loss-gradient family
+def loss_grad_prove(tr: Transcript, GZ: np.ndarray, Z: np.ndarray, Y: np.ndarray):
+    """Eq. (fcnn-GZ-last) G_Z = Z - Y (D24): returns dict(u, claims = [G_Z~(u), Z~(u), Y~(u)])."""
+    GZ, Z, Y = (np.ascontiguousarray(t, dtype=np.int32).reshape(-1) for t in (GZ, Z, Y))
+    m = Z.size.bit_length() - 1
+    assert Z.size == 1 << m and GZ.size == Z.size and Y.size == Z.size
+    u, cl = _buf(32 * m), _buf(96)
+    s = lib().or_loss_grad_prove(tr.st, m, _ptr(GZ), _ptr(Z), _ptr(Y), u, cl)
+    if s:
+        raise ValueError(f"or_loss_grad_prove status {s}")
+    return dict(u=from_bytes(u.raw[:32 * m], m), claims=from_bytes(cl.raw[:96], 3))

@@ -1141,6 +1141,26 @@ int or_zero_sumcheck_prove(transcript *tr, uint32_t m, const int32_t *Y, const i
     return 0;
 }
 
+/* ------------------------------------------------------------ N2: the loss-gradient family
+ * Eq. (fcnn-GZ-last): G_Z^(L) = Z^(L) - Y, a linear relation, so its aggregated form over the
+ * stacked instances needs no sumcheck: at a verifier point u (m = log2 of the stacked size) the claims
+ * G_Z~(u), Z~(u), Y~(u) satisfy G_Z~(u) = Z~(u) - Y~(u) by linearity of the multilinear extension
+ * (P:L144-149); the verifier checks that identity and the three claims go to the commitments
+ * (D24).  Transcript: "lg/hdr" (m) | u = "lg/u" x m | "lg/claims" (G_Z~(u), Z~(u), Y~(u)).
+ * Tables int32, embedded (negatives -> p - |v|); MLEs by the plain definition (mle_i32). */
+int or_loss_grad_prove(transcript *tr, uint32_t m, const int32_t *GZ, const int32_t *Z, const int32_t *Y,
+                       uint8_t *u_out /* m */, uint8_t *claims_out /* 3 */) {
+    init();
+    if (m < 1 || m > 32) return -1;
+    absorb_u32s(tr, "lg/hdr", &m, 1);
+    fr u[64];
+    for (uint32_t t = 0; t < m; t++) { u[t] = transcript_challenge(tr, "lg/u"); store_canon(u[t], u_out + 32 * t); }
+    fr cl[3] = {mle_i32(GZ, (int)m, u), mle_i32(Z, (int)m, u), mle_i32(Y, (int)m, u)};
+    for (int k = 0; k < 3; k++) store_canon(cl[k], claims_out + 32 * k);
+    absorb_frs(tr, "lg/claims", cl, 3);
+    return 0;
+}
+
 /* ------------------------------------------------------------ misc exports */
 void or_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
 int or_get_threads(void) { return omp_get_max_threads(); }

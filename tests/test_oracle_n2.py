@@ -75,3 +75,28 @@ def test_zero_form_rejects_a_wrong_product(oracle_lib):
         seed = fs_seed(f"hd-bad-{pos}")
         res = O.zero_sumcheck_prove(O.Transcript(seed), Y, A, B)
         assert verify(O, seed, m, res, Y, A, B) == 1
+
+
+# ---------------------------------------------------------------- the loss-gradient family (D24)
+def test_loss_grad_claims_brute_force_and_linearity(oracle_lib):
+    """Eq. (fcnn-GZ-last): the three claims are the brute-force MLEs at the transcript's u
+    (drawn "lg/u" after "lg/hdr"), G_Z~(u) = Z~(u) - Y~(u) for G_Z = Z - Y, and a changed entry of G_Z
+    breaks the identity (its MLE moves by beta(u, x) != 0)."""
+    O = oracle_lib
+    for m in (1, 3, 6):
+        Z = uniform_range(33, m, (1 << m,), -(1 << 20), 1 << 20)
+        Y = uniform_range(33, m + 20, (1 << m,), -(1 << 20), 1 << 20)
+        G = (Z.astype(np.int64) - Y).astype(np.int32)
+        seed = fs_seed(f"lg-{m}")
+        res = O.loss_grad_prove(O.Transcript(seed), G, Z, Y)
+        T = O.Transcript(seed)
+        T.absorb("lg/hdr", m.to_bytes(4, "little"))
+        u = T.challenges("lg/u", m)
+        assert res["u"] == u
+        g, z, y = res["claims"]
+        assert [g, z, y] == [mle(list(G), u), mle(list(Z), u), mle(list(Y), u)]
+        assert g == (z - y) % P
+        Gb = G.copy()
+        Gb[(1 << m) - 1] += 1
+        gb = O.loss_grad_prove(O.Transcript(seed), Gb, Z, Y)["claims"][0]
+        assert gb != (z - y) % P
