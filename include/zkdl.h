@@ -187,6 +187,16 @@ zk_status zk_hadamard_zero_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* 
                                  const int32_t* d_B, uint32_t m, uint8_t* proof, uint64_t* proof_len, zk_fr* w_out,
                                  zk_fr* point_out, zk_fr* finals_out);
 
+/* zk_loss_grad_prove — SURVEY §8(f) N2: the loss-gradient family, Eq. (fcnn-GZ-last) P:L299-302,
+ *   G_Z^(L) = Z^(L) - Y over the stacked instances (D24).  The relation is linear, so no
+ *   sumcheck: at the verifier's point u the claims G_Z~(u), Z~(u), Y~(u) satisfy G_Z~(u) = Z~(u) - Y~(u)
+ *   (linearity of the MLE); the three claims go to the commitments.  d_GZ, d_Z, d_Y: int32
+ *   tables of 2^m entries (device, borrowed).  Transcript: "lg/hdr" (m as u32le) | u = "lg/u" x m |
+ *   "lg/claims" (3 canonical values).  point_out (m) and claims_out (3): host, may be NULL.  A false
+ *   statement is not an error: the claims simply fail the identity.  Synchronises the ctx stream once. */
+zk_status zk_loss_grad_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_GZ, const int32_t* d_Z,
+                             const int32_t* d_Y, uint32_t m, zk_fr* point_out, zk_fr* claims_out);
+
 /* ------------------------------------------- sharded product sumcheck (SURVEY §8(e), G = 2^s devices)
  * Rank g (of world = G, a power of two) holds entries [g 2^L, (g+1) 2^L) of every table, L = m - s:
  * the top s index bits (the last-bound variables, D2) are the rank id, so every round pair is local.
@@ -275,6 +285,8 @@ zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
  *   from c_0 = 0, final Y~(r) - A~(r) B~(r); w_out, point_out: m elements (may be NULL).
  * zk_verify_relu: a zk_relu_prove proof (App. A, D3b): the final identity of the six statements at the
  *   final point with the verifier's own beta, s, s' evaluations; point_out: logB + logD elements.
+ * zk_verify_loss_grad: the loss-gradient claims (D24): replays "lg/hdr", u, "lg/claims" and checks
+ *   G_Z~(u) = Z~(u) - Y~(u) (fail = -100); point_out: m elements.
  * zk_verify_relu_merge: a zk_relu_merge proof (D21) following the zkReLU proof whose point and finals
  *   are given: the verifier forms the claim and checks the weight final W~(r); point_out: logB + 1. */
 zk_status zk_htr_init(const uint8_t seed[32], uint8_t st[32]);
@@ -285,6 +297,7 @@ zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proo
 zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* w_out,
                                   zk_fr* point_out, int32_t* fail);
 zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_loss_grad(uint8_t st[32], uint32_t m, const zk_fr* claims, zk_fr* point_out, int32_t* fail);
 zk_status zk_verify_relu_merge(uint8_t st[32], uint32_t logD, uint32_t Q, uint32_t R, const zk_fr* relu_point,
                                const zk_fr* relu_finals, const uint8_t* proof, uint64_t proof_len, zk_fr* point_out,
                                int32_t* fail);

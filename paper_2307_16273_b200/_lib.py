@@ -104,6 +104,8 @@ def lib():
         "zk_verify_sumcheck": ([vp, vp, u64, vp, vp, vp, vp], i32),
         "zk_verify_hadamard_zero": ([vp, vp, u64, vp, vp, vp], i32),
         "zk_verify_relu": ([vp, vp, u64, vp, vp], i32),
+        "zk_loss_grad_prove": ([vp, vp, vp, vp, vp, u32, vp, vp], i32),
+        "zk_verify_loss_grad": ([vp, u32, vp, vp, vp], i32),
         "zk_verify_relu_merge": ([vp, u32, u32, u32, vp, vp, vp, u64, vp, vp], i32),
     }
     for name, (args, res) in sig.items():

@@ -488,3 +488,14 @@ def hadamard_zero_prove(ctx: Context, tr: Transcript, Y: torch.Tensor, A: torch.
     vals = [int.from_bytes(raw[4 + 32 * i:36 + 32 * i], "little") for i in range(3 * m + 3)]
     return dict(w=_ints(w, m), msgs=[vals[3 * t:3 * t + 3] for t in range(m)], r=_ints(pt, m), finals=vals[3 * m:],
                 proof=raw)
+
+
+def loss_grad_prove(ctx: Context, tr: Transcript, GZ: torch.Tensor, Z: torch.Tensor, Y: torch.Tensor) -> dict:
+    """zk_loss_grad_prove (Eq. fcnn-GZ-last, D24): int32 device tables of 2^m entries.
+    Returns dict(u, claims = [G_Z~(u), Z~(u), Y~(u)])."""
+    m = _log2(Z.numel())
+    assert GZ.numel() == Z.numel() and Y.numel() == Z.numel()
+    pt, cl = ctypes.create_string_buffer(32 * m), ctypes.create_string_buffer(96)
+    ctx.check(lib().zk_loss_grad_prove(ctx.h, tr.h, _dev_ptr(GZ, torch.int32), _dev_ptr(Z, torch.int32),
+                                       _dev_ptr(Y, torch.int32), m, pt, cl))
+    return dict(u=_ints(pt, m), claims=_ints(cl, 3))

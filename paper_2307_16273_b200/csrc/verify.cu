@@ -494,6 +494,21 @@ zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_le
     });
 }
 
+// The loss-gradient family (Eq. fcnn-GZ-last, D24): the claims at the transcript's point u satisfy the
+// linear identity G_Z~(u) = Z~(u) - Y~(u).
+zk_status zk_verify_loss_grad(uint8_t st[32], uint32_t m, const zk_fr* claims, zk_fr* point_out, int32_t* fail) {
+    return guarded(fail, [&] {
+        need(st && claims && m >= 1 && m <= 64);
+        tr_absorb_u32s(st, "lg/hdr", &m, 1);
+        F u[64], cl[3];
+        for (uint32_t t = 0; t < m; t++) u[t] = tr_challenge(st, "lg/u");
+        for (int k = 0; k < 3; k++) cl[k] = ld(claims[k].b);
+        if (!eq(cl[0], sub(cl[1], cl[2]))) throw Reject{-100};
+        tr_absorb_frs(st, "lg/claims", cl, 3);
+        out_points(u, m, point_out);
+    });
+}
+
 // The zkReLU aux-claim merge (D21): rho, then the product sumcheck over (j, s) with n_eq = 0
 // and the claim f0 + rho f1 + rho^2 f2 the verifier forms itself; the second final W~(r) is checked
 // against the verifier's own evaluation of W, the first is the single merged claim aux~(r_s, v, r_j).

@@ -98,6 +98,13 @@ def verify_relu(tr: HostTranscript, proof: bytes) -> list:
     return _ints(pt, m)
 
 
+def verify_loss_grad(tr: HostTranscript, m: int, claims: list) -> list:
+    """zk_verify_loss_grad (D24): returns the point u; raises Rejected unless G_Z~(u) = Z~(u) - Y~(u)."""
+    pt = ctypes.create_string_buffer(32 * m)
+    _run("loss gradient", lib().zk_verify_loss_grad, tr.st, m, _fr(claims), pt)
+    return _ints(pt, m)
+
+
 def verify_relu_merge(tr: HostTranscript, logD: int, Q: int, R: int, relu_point: list, relu_finals: list,
                       proof: bytes) -> list:
     m = max(0, (Q + R - 1).bit_length()) + 1

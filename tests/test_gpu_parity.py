@@ -696,3 +696,24 @@ def test_rowdot_tensor_cores_match_cuda_cores(ctx, nrows, cols):
         ctx.check(lib().zk_diag_rowdot(ctx.h, M.data_ptr(), nrows, cols, pt, o.data_ptr(), tc))
         outs.append(o.cpu())
     assert torch.equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------- N2: the loss-gradient family (D24)
+@pytest.mark.parametrize("m", [1, 10, 16])
+def test_loss_grad_vs_oracle(ctx, O, m):
+    """zk_loss_grad_prove against the oracle: the point, the three claims and the transcript state
+    bit-exact; the library's host verifier accepts; the identity fails for a false G_Z."""
+    from paper_2307_16273_b200 import api, verify
+    Z = uniform_range(44, m, (1 << m,), -(1 << 30), 1 << 30)
+    Y = uniform_range(44, m + 30, (1 << m,), -(1 << 30), 1 << 30)
+    G = (Z.astype(np.int64) - Y).astype(np.int32)
+    seed = fs_seed(f"lg-gpu-{m}")
+    T = O.Transcript(seed)
+    o = O.loss_grad_prove(T, G, Z, Y)
+    tr = api.Transcript(ctx, seed)
+    g = api.loss_grad_prove(ctx, tr, dev(G), dev(Z), dev(Y))
+    assert g == o and tr.state() == T.state()
+    assert verify.verify_loss_grad(verify.HostTranscript(seed=seed), m, g["claims"]) == g["u"]
+    G[0] += 1
+    gb = api.loss_grad_prove(ctx, api.Transcript(ctx, seed), dev(G), dev(Z), dev(Y))
+    assert gb["claims"][0] != (gb["claims"][1] - gb["claims"][2]) % P

@@ -187,3 +187,23 @@ def test_window_verifier_on_oracle_window(V, oracle_lib):
     bad["proof"] = bytes(pb)
     with pytest.raises(V.Rejected):
         V.verify_window(fs_seed("vwin"), fcn.fcn_header(shape), fams, results[:k] + [bad] + results[k + 1:])
+
+
+def test_loss_grad_verifier(V, oracle_lib):
+    """D24: the oracle's loss-gradient claims are accepted (end state = the oracle's), a false statement
+    (one entry of G_Z changed) is rejected by the linear identity."""
+    O = oracle_lib
+    m = 7
+    Z = uniform_range(43, 1, (1 << m,), -(1 << 20), 1 << 20)
+    Y = uniform_range(43, 2, (1 << m,), -(1 << 20), 1 << 20)
+    G = (Z.astype(np.int64) - Y).astype(np.int32)
+    seed = fs_seed("vlg")
+    T = O.Transcript(seed)
+    res = O.loss_grad_prove(T, G, Z, Y)
+    H = V.HostTranscript(seed=seed)
+    assert V.verify_loss_grad(H, m, res["claims"]) == res["u"] and H.state() == T.state()
+    G[3] -= 1
+    bad = O.loss_grad_prove(O.Transcript(seed), G, Z, Y)
+    with pytest.raises(V.Rejected) as e:
+        V.verify_loss_grad(V.HostTranscript(seed=seed), m, bad["claims"])
+    assert e.value.where == -100
