@@ -370,8 +370,101 @@ __global__ void k_colsum_finish(const uint32_t* partials, uint64_t N, uint32_t c
     }
 }
 
+// Row-streaming column sums for wide stacks (cols = 256 CS, CS in {2, 4}): the row units (n, r) of the
+// whole stack are cut into one contiguous range per CTA; a CTA streams its rows whole (4 KB contiguous at
+// cols = 1024; the column-strip kernel above reads 512-byte strips of 4 KB-strided rows) with thread t
+// owning columns t + 256 j, and flushes one 10-limb partial per instance it touches (slot = n - first
+// instance of its range); k_colsum_rows_finish adds the partials of the CTAs that cover each instance.
+template <int CS>
+__global__ void __launch_bounds__(256) k_colsum_rows(const int32_t* M, uint64_t N, uint32_t rows, const fr_t* E2,
+                                                     uint32_t* partials, uint32_t slots) {
+    constexpr uint32_t cols = 256 * CS;
+    const uint64_t units = N * rows, R = gridDim.x;
+    const uint64_t lo = blockIdx.x * units / R, hi = (blockIdx.x + 1) * units / R;
+    const uint64_t n_first = lo / rows;
+    uint64_t u = lo;
+    while (u < hi) {
+        const uint64_t n = u / rows, end = (n + 1) * rows < hi ? (n + 1) * rows : hi;
+        uint32_t acc[CS][10];
+#pragma unroll
+        for (int j = 0; j < CS; j++)
+#pragma unroll
+            for (int k = 0; k < 10; k++) acc[j][k] = 0;
+        const fr_t* Er = E2 + (u - n * rows);   // eq weight of the current row (no per-row modulo)
+        const int32_t* Mr = M + u * cols + threadIdx.x;
+        for (; u + 3 < end; u += 4, Er += 4, Mr += 4 * cols) {   // 4 rows x CS columns of loads in flight
+            uint32_t v[4][CS];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < CS; j++) v[i][j] = (uint32_t)__ldcs(Mr + i * cols + 256 * j);
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const fr_t e = fr_load(&Er[i]);
+#pragma unroll
+                for (int j = 0; j < CS; j++) ZK_MAC_WIDE(acc[j], e, v[i][j] + 0x80000000u);
+            }
+        }
+        for (; u < end; u++, Er++, Mr += cols) {
+            const fr_t e = fr_load(Er);
+#pragma unroll
+            for (int j = 0; j < CS; j++) ZK_MAC_WIDE(acc[j], e, (uint32_t)__ldcs(Mr + 256 * j) + 0x80000000u);
+        }
+        uint32_t* P = partials + ((uint64_t)blockIdx.x * slots + (n - n_first)) * cols * 10;
+#pragma unroll
+        for (int j = 0; j < CS; j++)
+#pragma unroll
+            for (int k = 0; k < 10; k++) P[(uint64_t)(threadIdx.x + 256 * j) * 10 + k] = acc[j][k];
+    }
+}
+__global__ void k_colsum_rows_finish(const uint32_t* partials, uint64_t N, uint32_t rows, uint32_t cols, uint32_t R,
+                                     uint32_t slots, fr_t* out) {
+    const uint64_t units = N * rows;
+    for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < N * cols; o += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t n = o / cols, c = o % cols;
+        // CTAs whose unit range [b units / R, (b + 1) units / R) meets [n rows, (n + 1) rows)
+        uint64_t b = n * rows * R / units;
+        while (b > 0 && b * units / R > n * rows) b--;
+        while ((b + 1) * units / R <= n * rows) b++;
+        uint32_t acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (; b < R && b * units / R < (n + 1) * rows; b++) {
+            const uint64_t n_first = (b * units / R) / rows;
+            const uint32_t* P = partials + ((b * slots + (n - n_first)) * cols + c) * 10;
+            uint32_t x[10];
+#pragma unroll
+            for (int k = 0; k < 10; k++) x[k] = P[k];
+            wide_add10(acc, x);
+        }
+        fr_store(&out[c * N + n], wide_finish(acc));
+    }
+}
+
 void colsum_i32(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
                 Scratch& s) {
+    // wide stacks with many row units: the row-streaming kernel (ZKDL_COLSUM_ROWS=0 disables it)
+    static const bool rows_off = getenv("ZKDL_COLSUM_ROWS") && atoi(getenv("ZKDL_COLSUM_ROWS")) == 0;
+    if (!rows_off && (cols == 512 || cols == 1024) && N * rows >= 64ull * ctx->num_sms) {
+        static int per_sm[2] = {0, 0};
+        const int ci = cols == 1024;
+        if (!per_sm[ci]) {
+            if (ci)
+                ZK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ci], k_colsum_rows<4>, 256, 0));
+            else
+                ZK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ci], k_colsum_rows<2>, 256, 0));
+            if (per_sm[ci] < 1) per_sm[ci] = 1;
+        }
+        const uint32_t R = (uint32_t)ctx->num_sms * per_sm[ci];
+        const uint64_t units = N * rows, span = (units + R - 1) / R;
+        const uint32_t slots = (uint32_t)((span + rows - 1) / rows + 1);   // instances one unit range can touch
+        uint32_t* partials = s.alloc<uint32_t>((uint64_t)R * slots * cols * 10);
+        if (ci)
+            ZK_LAUNCH(ctx, k_colsum_rows<4>, R, 256, 0, M, N, rows, E2, partials, slots);
+        else
+            ZK_LAUNCH(ctx, k_colsum_rows<2>, R, 256, 0, M, N, rows, E2, partials, slots);
+        ZK_LAUNCH(ctx, k_colsum_rows_finish, grid_for(ctx, N * cols, 256, 4), 256, 0, (const uint32_t*)partials, N, rows,
+                  cols, R, slots, out);
+        return;
+    }
     // 128-thread CTAs, up to 7 resident per SM (70 registers): size the work to about one wave
     const uint64_t outputs = N * cols, slots = (uint64_t)ctx->num_sms * 7 * 128;
     uint32_t S = 1;

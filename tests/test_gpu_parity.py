@@ -151,7 +151,9 @@ def test_sumcheck_vs_oracle(ctx, O, m, n_eq, K):
 
 # ---------------------------------------------------------------- matmul (row a3)
 MM_CASES = [(0, 5, 6, 6, False, False), (2, 3, 4, 2, False, False), (3, 4, 5, 3, True, False),
-            (2, 6, 7, 5, False, True), (1, 6, 6, 10, True, True), (4, 2, 9, 12, False, True), (3, 10, 6, 4, True, False)]
+            (2, 6, 7, 5, False, True), (1, 6, 6, 10, True, True), (4, 2, 9, 12, False, True), (3, 10, 6, 4, True, False),
+            # the row-streaming column sums (k_colsum_rows: 512 / 1024 columns, CTA ranges straddling instances)
+            (4, 10, 9, 0, False, False), (3, 0, 10, 11, False, True)]
 
 
 @pytest.mark.parametrize("lN,l1,l2,l3,ta,tb", MM_CASES)
