@@ -267,8 +267,93 @@ void mle_i32_relu(zk_ctx* ctx, int kind, const int32_t* d_z, const int32_t* d_g,
 
 // The four zkReLU claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) (A, G_Z formed on the fly, Lemma 1):
 // the eight eq tables in one batch, then a row-dot and a dot per claim.
+// The four zkReLU claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) (D3b) in one pass over Z and G_A: the
+// tables viewed as [2^hi rows][256 columns] (entry i = 256 r + c, so the low 8 point coordinates index the
+// column, D2); thread c of a CTA owns column c and streams a contiguous range of rows, accumulating the
+// four lazy sums sum_r H_k[r] u_k[r][c] (u = v + 2^31, H_k = eq over the high coordinates, R-scaled);
+// each CTA writes the four column partials as Fr (REDC without the bias); k_mle4_finish adds the CTAs'
+// partials, weights column c by E_k[c] (eq over the low coordinates) and removes the bias once:
+// sum_c E_k[c] sum_r H_k[r] 2^31 = 2^31.  (The former path: four row-dot launches, one warp per row and a
+// 32-byte eq load per element, ~0.24 ms at C4; this one reads each word once.)
+__global__ void __launch_bounds__(256) k_mle4_rows(const int32_t* Z, const int32_t* GA, uint32_t R, uint64_t rows,
+                                                   const fr_t* H0, const fr_t* H1, const fr_t* H2, const fr_t* H3,
+                                                   fr_t* partials) {
+    const uint64_t r0 = blockIdx.x * rows / gridDim.x, r1 = (blockIdx.x + 1) * rows / gridDim.x;
+    const uint32_t c = threadIdx.x;
+    uint32_t acc[4][10];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int l = 0; l < 10; l++) acc[k][l] = 0;
+    const int64_t half = 1ll << (R - 1);
+    uint64_t r = r0;
+    for (; r + 3 < r1; r += 4) {   // 8 loads in flight per thread
+        int32_t z[4], g[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            z[i] = __ldcs(Z + (r + i) * 256 + c);
+            g[i] = __ldcs(GA + (r + i) * 256 + c);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int32_t a = z[i] >= 0 ? (int32_t)(((int64_t)z[i] + half) >> R) : 0;      // A = 1{Z >= 0} round(Z / 2^R)
+            const int32_t gz = z[i] >= 0 ? (int32_t)(((int64_t)g[i] + half) >> R) : 0;     // G_Z = 1{Z >= 0} round(G_A / 2^R)
+            ZK_MAC_WIDE(acc[0], fr_load(&H0[r + i]), (uint32_t)z[i] + 0x80000000u);
+            ZK_MAC_WIDE(acc[1], fr_load(&H1[r + i]), (uint32_t)a + 0x80000000u);
+            ZK_MAC_WIDE(acc[2], fr_load(&H2[r + i]), (uint32_t)g[i] + 0x80000000u);
+            ZK_MAC_WIDE(acc[3], fr_load(&H3[r + i]), (uint32_t)gz + 0x80000000u);
+        }
+    }
+    for (; r < r1; r++) {
+        const int32_t z = __ldcs(Z + r * 256 + c), g = __ldcs(GA + r * 256 + c);
+        const int32_t a = z >= 0 ? (int32_t)(((int64_t)z + half) >> R) : 0;
+        const int32_t gz = z >= 0 ? (int32_t)(((int64_t)g + half) >> R) : 0;
+        ZK_MAC_WIDE(acc[0], fr_load(&H0[r]), (uint32_t)z + 0x80000000u);
+        ZK_MAC_WIDE(acc[1], fr_load(&H1[r]), (uint32_t)a + 0x80000000u);
+        ZK_MAC_WIDE(acc[2], fr_load(&H2[r]), (uint32_t)g + 0x80000000u);
+        ZK_MAC_WIDE(acc[3], fr_load(&H3[r]), (uint32_t)gz + 0x80000000u);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) fr_store(&partials[((uint64_t)blockIdx.x * 4 + k) * 256 + c], fr_redc_wide(acc[k]));
+}
+// block k (claim k), thread c: sum_b partials[b][k][c] * E_k[c], block-summed, minus the bias 2^31
+__global__ void __launch_bounds__(256) k_mle4_finish(const fr_t* partials, uint32_t nb, const fr_t* E0, const fr_t* E1,
+                                                     const fr_t* E2, const fr_t* E3, fr_t* out) {
+    __shared__ fr_t sm[32];
+    const uint32_t k = blockIdx.x, c = threadIdx.x;
+    fr_t s = fr_zero();
+    for (uint32_t b = 0; b < nb; b++) s = fr_add(s, fr_load(&partials[((uint64_t)b * 4 + k) * 256 + c]));
+    const fr_t* E = k == 0 ? E0 : k == 1 ? E1 : k == 2 ? E2 : E3;
+    fr_t v[1] = {fr_mul(s, fr_load(&E[c]))};
+    block_reduce_fr<1>(v, sm);
+    if (threadIdx.x == 0) fr_store(&out[k], fr_sub(v[0], ZK_TWO31_MONT));
+}
+
 void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,
                    fr_t* d_out, Scratch& s) {
+    static const bool fused_off = getenv("ZKDL_MLE4_FUSED") && atoi(getenv("ZKDL_MLE4_FUSED")) == 0;
+    if (!fused_off && m >= 16 && R >= 1) {
+        const uint32_t lo = 8, hi = m - 8;
+        fr_t* E[4];
+        fr_t* H[4];
+        EqJob jobs[8];
+        for (int c = 0; c < 4; c++) {
+            E[c] = s.alloc<fr_t>(256);
+            H[c] = s.alloc<fr_t>(1ull << hi);
+            jobs[2 * c] = EqJob{d_U + (uint64_t)c * m, lo, nullptr, 0, E[c]};
+            jobs[2 * c + 1] = EqJob{d_U + (uint64_t)c * m + lo, hi, nullptr, 1, H[c]};   // R-scaled: lazy MACs
+        }
+        eq_tables_batch(ctx, 8, jobs, s);
+        const uint64_t rows = 1ull << hi;
+        uint32_t nb = (uint32_t)ctx->num_sms * 2;
+        if ((uint64_t)nb > rows / 4) nb = (uint32_t)(rows / 4);
+        fr_t* P = s.alloc<fr_t>((uint64_t)nb * 4 * 256);
+        ZK_LAUNCH(ctx, k_mle4_rows, nb, 256, 0, d_z, d_g, R, rows, (const fr_t*)H[0], (const fr_t*)H[1],
+                  (const fr_t*)H[2], (const fr_t*)H[3], P);
+        ZK_LAUNCH(ctx, k_mle4_finish, 4, 256, 0, (const fr_t*)P, nb, (const fr_t*)E[0], (const fr_t*)E[1],
+                  (const fr_t*)E[2], (const fr_t*)E[3], d_out);
+        return;
+    }
     uint32_t lo, hi;
     split_bits(m, lo, hi);
     fr_t* E2[4];
