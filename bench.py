@@ -348,8 +348,12 @@ def run_ours(args, rank, world, local):
     e2e_steps = 0 if args.profile_mode else max(1, min(args.steps, 3))
     copy_stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
-        if e2e_steps:   # one untimed end-to-end window: allocator warm-up for the upload buffers
-            dfcn.prove_window_from_host(ctx, seed, header, host_fams, copy_stream, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
+        for _ in range(2 if e2e_steps else 0):   # untimed warm-up with the timed call's shape: the caching
+            # allocator then holds upload buffers for e2e_steps windows in flight (a cudaMalloc inside the
+            # timed region synchronises the device and showed up as 20-60 ms outliers)
+            dfcn.prove_windows_from_host(ctx, [(seed, header, host_fams)] * e2e_steps, copy_stream,
+                                         relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
+            torch.cuda.synchronize()
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
