@@ -183,6 +183,50 @@ __device__ __forceinline__ fr_t mul_lazy(const fr_t& a, const fr_t& b) {
     return r;
 }
 
+// Variant 8: the production CIOS with every carry folded into the 64-bit addend of the product
+// (x + C as a 33-bit value from PTX add.cc / addc, meant for the ALU pipe), so IMAD.WIDE.U32 carries no
+// separate high-word carry add (the IMAD.X the compiler puts on the FMA pipe)
+__device__ __forceinline__ uint64_t add33(uint32_t x, uint32_t y) {
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, 0, 0;" : "=r"(lo), "=r"(hi) : "r"(x), "r"(y));
+    return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ fr_t mul_alu(const fr_t& a, const fr_t& b) {
+    const uint32_t p[8] = {ZK_P0, ZK_P1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7};
+    uint32_t t[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        uint32_t C = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t uv = (uint64_t)a.v[j] * b.v[i] + add33(t[j], C);
+            t[j] = (uint32_t)uv;
+            C = (uint32_t)(uv >> 32);
+        }
+        t[8] += C;
+        const uint32_t m = t[0] * 0xffffffffu;
+        uint64_t C2 = (uint64_t)(t[0] != 0);
+        {
+            const uint64_t uv = ((uint64_t)m << 32) + t[1] + C2 - m;
+            t[0] = (uint32_t)uv;
+            C = (uint32_t)(uv >> 32);
+        }
+#pragma unroll
+        for (int j = 2; j < 8; j++) {
+            const uint64_t uv = (uint64_t)m * p[j] + add33(t[j], C);
+            t[j - 1] = (uint32_t)uv;
+            C = (uint32_t)(uv >> 32);
+        }
+        const uint64_t uv = (uint64_t)t[8] + C;
+        t[7] = (uint32_t)uv;
+        t[8] = (uint32_t)(uv >> 32);
+    }
+    fr_t r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.v[i] = t[i];
+    return fr_reduce_once(r);
+}
+
 template <int V>
 __device__ __forceinline__ fr_t MUL(const fr_t& a, const fr_t& b) {
     if (V == 0) return fr_mul(a, b);
@@ -190,6 +234,7 @@ __device__ __forceinline__ fr_t MUL(const fr_t& a, const fr_t& b) {
     if (V == 3) return mul_u64p(a, b);
     if (V == 4) return mul_mix(a, b);
     if (V == 5) return mul_lazy(a, b);
+    if (V == 8) return mul_alu(a, b);
     return mul_sos(a, b);
 }
 
@@ -314,6 +359,7 @@ int main() {
     run<3>("u64_cios_p01", d_seed, d_out, blocks, 1000);
     run<4>("mix_u64_madc", d_seed, d_out, blocks, 1000);
     run<5>("u64_p01_lazy", d_seed, d_out, blocks, 1000);
+    run<8>("u64_p01_alucarry", d_seed, d_out, blocks, 1000);
     for (int b = 148 * 2; b <= 148 * 8; b *= 2) run3<6>("fr_mul3_ni", d_seed, d_out, b, 1000);
     for (int b = 148 * 2; b <= 148 * 8; b *= 2) run3<7>("fr_mul_ni x3", d_seed, d_out, b, 1000);
     return 0;
