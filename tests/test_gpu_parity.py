@@ -719,3 +719,23 @@ def test_loss_grad_vs_oracle(ctx, O, m):
     G[0] += 1
     gb = api.loss_grad_prove(ctx, api.Transcript(ctx, seed), dev(G), dev(Z), dev(Y))
     assert gb["claims"][0] != (gb["claims"][1] - gb["claims"][2]) % P
+
+
+def test_readme_flow_host_verified(ctx, O):
+    """The README's usage: a matmul reduction + product sumcheck and a zkReLU proof on one transcript,
+    then the host verifiers replaying the same transcript accept both and end in the prover's state."""
+    from paper_2307_16273_b200 import api, verify
+    A = uniform_range(9, 1, (4, 8, 16), -(1 << 15), 1 << 15)
+    B = uniform_range(9, 2, (4, 16, 32), -(1 << 15), 1 << 15)
+    Z = uniform_range(9, 3, (1 << 12,), -(1 << 31), 1 << 31)
+    GA = uniform_range(9, 4, (1 << 12,), -(1 << 31), 1 << 31)
+    tr = api.Transcript(ctx, b"\0" * 32)
+    red = api.matmul_reduce(ctx, tr, dev(A), dev(B))
+    logN, logD2 = len(red["w"]), 4
+    proof = api.sumcheck_prove(ctx, tr, logN + logD2, logN, [red["At"], red["Bt"]], red["w"], red["claim"])
+    relu = api.relu_prove(ctx, tr, dev(Z), dev(GA), 16, 16)
+    H = verify.HostTranscript(seed=b"\0" * 32)
+    logs = (logN, len(red["u1"]), logD2, len(red["u3"]))
+    assert verify.verify_matmul(H, logs, dict(red, proof=proof["proof"])) == proof["r"]
+    assert verify.verify_relu(H, relu["proof"]) == relu["point"]
+    assert H.state() == tr.state()
