@@ -229,6 +229,13 @@ static __device__ __noinline__ fr3_t fr_mul3_ni(fr_t a0, fr_t b0, fr_t a1, fr_t 
     return fr3_t{fr_mul(a0, b0), fr_mul(a1, b1), fr_mul(a2, b2)};
 }
 
+// Two independent products in one out-of-line body (for the groups with only two products: a wasted
+// third slot of fr_mul3_ni costs a whole product)
+struct fr2p_t { fr_t x, y; };
+static __device__ __noinline__ fr2p_t fr_mul2_ni(fr_t a0, fr_t b0, fr_t a1, fr_t b1) {
+    return fr2p_t{fr_mul(a0, b0), fr_mul(a1, b1)};
+}
+
 // One out-of-line copy for cold code (finalizers, single-CTA round kernels): the inlined product is
 // ~560 SASS instructions, and cold code that inlines dozens of them runs out of the instruction
 // cache (ncu: stall_no_inst dominated the round kernels' finalize).

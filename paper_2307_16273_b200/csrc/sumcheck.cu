@@ -432,12 +432,13 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
             }
             fr_t y0 = a0, y1 = a1;
             if (has_e) {
-                if (!q_done) q = fr_mul3_ni(e, a0, e, a1, zero, zero);
-                y0 = q.y;
-                y1 = q.z;
-                if (!q_done) {
-                    y0 = q.x;
-                    y1 = q.y;
+                if (q_done) {
+                    y0 = q.y;
+                    y1 = q.z;
+                } else {   // two products only: the two-product body (no wasted third slot)
+                    const fr2p_t q2 = fr_mul2_ni(e, a0, e, a1);
+                    y0 = q2.x;
+                    y1 = q2.y;
                 }
             }
             const fr3_t p = fr_mul3_ni(y0, b0, y1, b1, fr_sub(y1, y0), fr_sub(b1, b0));
