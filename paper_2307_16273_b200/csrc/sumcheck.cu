@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                     q_done = true;
                 } else {
                     const fr_t hh = (has_e && A.flat && a.eq_hi) ? fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]) : zero;
-                    const fr3_t g2 = fr_mul3_ni(r, fr_sub(z3, z2), e, hh, zero, zero);
+                    const fr2p_t g2 = fr_mul2_ni(r, fr_sub(z3, z2), e, hh);
                     b1 = fr_add(z2, g2.x);
                     if (has_e) e = g2.y;
                 }
