@@ -533,29 +533,42 @@ def test_fcn_window_full_size_vs_oracle(ctx, O, cfg):
     assert [v["point"] for v in vo] == [gr["r"] if hasattr(f, "A") else gr["point"] for f, gr in zip(fams, g)]
 
 
-def test_c5_bench_size_26_properties(ctx, O):
-    """C5 at m = 26 (the c5_sharded size of every bench line), too large for a full oracle run: the
-    oracle verifier replays the transcript, checks every round identity, and checks the finals
-    against brute-force MLEs of A and B at r; the claim is checked against its brute-force sum."""
+@pytest.mark.slow
+@pytest.mark.parametrize("m", [24, 26, 28, 30])
+def test_c5_large_properties(ctx, O, m):
+    """C5 (BASELINE configs[4]: the aggregated Hadamard statement sum_x eq(w,x) A(x) B(x)) at
+    the sweep sizes 2^24 ... 2^30, too large for a full oracle prover run: inputs generated on the device
+    by the counter PRNG (checked against the numpy generator at both ends), the oracle verifier replays
+    the transcript and checks every round identity, the finals are checked against
+    brute-force MLEs of A and B at r, and the claim against the brute-force MLE of the integer
+    product table at w (|A B| < 2^30); the library's host verifier ends in the prover's state."""
     import os
-    from oracle import drivers
-    from paper_2307_16273_b200 import api
+    from paper_2307_16273_b200 import api, verify
+    from synth.prng import DATA_SEED, uniform_bits, uniform_range_torch
     O.set_threads(len(os.sched_getaffinity(0)))
-    m = 26
-    A, B = drivers.c5_inputs(m)
+    n = 1 << m
+    dA = uniform_range_torch(DATA_SEED, 21, n, -(1 << 15), 1 << 15, "cuda")
+    dB = uniform_range_torch(DATA_SEED, 22, n, -(1 << 15), 1 << 15, "cuda")
+    for tid, d in ((21, dA), (22, dB)):
+        ref = uniform_range(DATA_SEED, tid, (1 << 12,), -(1 << 15), 1 << 15)
+        assert np.array_equal(d[:1 << 12].cpu().numpy(), ref)
+        end = uniform_bits(DATA_SEED, tid, 1 << 12, -(1 << 15), 16, offset=n - (1 << 12)).astype(np.int32)
+        assert np.array_equal(d[n - (1 << 12):].cpu().numpy(), end)
     tr = api.Transcript(ctx, fs_seed(f"C5-m{m}"))
     tr.absorb("c5/hdr", m.to_bytes(4, "little"))
     w = tr.challenges("c5/w", m)
-    g = api.sumcheck_prove(ctx, tr, m, m, [dev(A), dev(B)], w)
+    g = api.sumcheck_prove(ctx, tr, m, m, [dA, dB], w)
+    A, B = dA.cpu().numpy(), dB.cpu().numpy()
+    del dA, dB
+    torch.cuda.empty_cache()
     ot = O.Transcript(fs_seed(f"C5-m{m}"))
     ot.absorb("c5/hdr", m.to_bytes(4, "little"))
     assert ot.challenges("c5/w", m) == w
     assert g["finals"] == [O.mle_i32(A, g["r"]), O.mle_i32(B, g["r"])]
     assert O.sumcheck_verify(ot, m, m, 2, w, g["claim"], g["msgs"], g["finals"]) == 0
     assert ot.state() == tr.state()
-    # the claim: sum_x eq(w, x) A(x) B(x) = MLE of the integer product table at w
-    assert g["claim"] == O.mle_i32((A.astype(np.int64) * B).astype(np.int32), w)   # |A B| < 2^30
-    from paper_2307_16273_b200 import verify   # and the library's host verifier (N3, D23)
+    np.multiply(A, B, out=A)                     # |A B| <= 2^30: exact in int32
+    assert g["claim"] == O.mle_i32(A, w)
     H = verify.HostTranscript(seed=fs_seed(f"C5-m{m}"))
     H.absorb("c5/hdr", m.to_bytes(4, "little"))
     assert H.challenges("c5/w", m) == w
@@ -681,23 +694,28 @@ def test_hadamard_zero_vs_oracle(ctx, O, m):
 
 
 @pytest.mark.parametrize("nrows,cols", [(1024, 8), (1024 + 24, 16), (18944, 64), (4096, 1024), (131072, 1024), (3000, 4096)])
-def test_rowdot_tensor_cores_match_cuda_cores(ctx, nrows, cols):
-    """The matmul restriction's row dots on the tensor cores (int8 GEMM over the bytes of the int32 matrix,
-    restrict_tc.cu) give the CUDA-core kernel's field elements bit for bit, full int32 range, ragged row
-    counts, several tiles per CTA."""
+def test_rowdot_tensor_cores_vs_oracle(ctx, O, nrows, cols):
+    """The matmul restriction's row dots (row r of M against eq(u, .)) on the tensor cores
+    (int8 GEMM over the bytes of the int32 matrix, restrict_tc.cu) and on the CUDA cores, each against
+    the oracle's brute-force MLE of the row: the full int32 range (rows 0/1 at -2^31 and 2^31-1), ragged
+    row counts, several tiles per CTA; every row up to 4096 rows, else the first/last 512 and 512 random."""
     from paper_2307_16273_b200._lib import lib
     from paper_2307_16273_b200 import api
     rng = random.Random(nrows + cols)
-    M = torch.randint(-2 ** 31, 2 ** 31, (nrows, cols), dtype=torch.int64, generator=torch.Generator().manual_seed(nrows)).to(torch.int32).cuda()
+    M = torch.randint(-2 ** 31, 2 ** 31, (nrows, cols), dtype=torch.int64, generator=torch.Generator().manual_seed(nrows)).to(torch.int32)
     M[0, :] = -2 ** 31
     M[1, :] = 2 ** 31 - 1
-    pt = api._fr_buf([rng.randrange(P) for _ in range(cols.bit_length() - 1)])
-    outs = []
+    Mh = M.numpy()
+    pt = [rng.randrange(P) for _ in range(cols.bit_length() - 1)]
+    rows = list(range(nrows)) if nrows <= 4096 else sorted(set(range(512)) | set(range(nrows - 512, nrows))
+                                                           | set(rng.sample(range(nrows), 512)))
+    O.set_threads(1)
+    want = [O.mle_i32(Mh[r], pt) for r in rows]
     for tc in (0, 1):
         o = torch.zeros((nrows, 32), dtype=torch.uint8, device="cuda")
-        ctx.check(lib().zk_diag_rowdot(ctx.h, M.data_ptr(), nrows, cols, pt, o.data_ptr(), tc))
-        outs.append(o.cpu())
-    assert torch.equal(outs[0], outs[1])
+        ctx.check(lib().zk_diag_rowdot(ctx.h, M.cuda().data_ptr(), nrows, cols, api._fr_buf(pt), o.data_ptr(), tc))
+        got = api.fr_table_to_ints(ctx, o)
+        assert [got[r] for r in rows] == want, f"use_tc={tc}"
 
 
 # ---------------------------------------------------------------- N2: the loss-gradient family (D24)
