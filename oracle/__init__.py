@@ -57,6 +57,9 @@ def lib():
         L.or_relu_tables.argtypes = [i32p, i32p, c.c_uint64, c.c_uint32, c.c_uint32] + [vp] * 7
         L.or_relu_prove.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp]
         L.or_loss_grad_prove.argtypes = [vp, c.c_uint32, i32p, i32p, i32p, vp, vp]
+        L.or_relu_prove_pts.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp]
+        L.or_claim_merge_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp,
+                                           vp, vp, vp, vp, vp, vp]
         L.or_relu_verify.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp]
         L.or_reindex_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp,
                                        vp, vp, vp, vp]
@@ -254,7 +257,9 @@ def relu_logB(Q: int, R: int) -> int:
     return max(0, (Q + R - 1).bit_length())
 
 
-def relu_prove(tr: Transcript, Z: np.ndarray, GA: np.ndarray, Q: int, R: int):
+def relu_prove(tr: Transcript, Z: np.ndarray, GA: np.ndarray, Q: int, R: int, points=None):
+    """App. A zkReLU (D3b).  points: None (u_Z, u_A, u_GA, u_GZ drawn from the transcript) or the chained
+    form (D25): the four logD-element points given (the window's merged claims)."""
     Z = np.ascontiguousarray(Z, dtype=np.int32).reshape(-1)
     GA = np.ascontiguousarray(GA, dtype=np.int32).reshape(-1)
     logD = Z.size.bit_length() - 1
@@ -262,7 +267,12 @@ def relu_prove(tr: Transcript, Z: np.ndarray, GA: np.ndarray, Q: int, R: int):
     logB = relu_logB(Q, R)
     m = logB + logD
     claims, chal, msgs, pt, fin = _buf(128), _buf(32 * (2 + m)), _buf(128 * m), _buf(32 * m), _buf(96)
-    s = lib().or_relu_prove(tr.st, _ptr(Z), _ptr(GA), logD, Q, R, claims, chal, msgs, pt, fin)
+    if points is None:
+        s = lib().or_relu_prove(tr.st, _ptr(Z), _ptr(GA), logD, Q, R, claims, chal, msgs, pt, fin)
+    else:
+        assert len(points) == 4 and all(len(u) == logD for u in points)
+        s = lib().or_relu_prove_pts(tr.st, _ptr(Z), _ptr(GA), logD, Q, R, to_bytes([x for u in points for x in u]),
+                                    claims, chal, msgs, pt, fin)
     if s:
         raise ValueError(f"or_relu_prove status {s}")
     flat = from_bytes(msgs.raw[:128 * m])
@@ -358,3 +368,36 @@ def loss_grad_prove(tr: Transcript, GZ: np.ndarray, Z: np.ndarray, Y: np.ndarray
     if s:
         raise ValueError(f"or_loss_grad_prove status {s}")
     return dict(u=from_bytes(u.raw[:32 * m], m), claims=from_bytes(cl.raw[:96], 3))
+
+
+# ---------------------------------------------------------------- N3: the claim merge (D25)
+def claim_merge_prove(tr: Transcript, X: np.ndarray, claims: list):
+    """General Eq. (sc-reindex) (D25).  X: [N][D] int32 (powers of two).  claims: list of
+    dicts(map = 2^{n_k} slice indices (-1: empty slot), u = n_k slot points, v = log2 D inner points,
+    c = the claimed value X_k~(v, u)).  Returns dict(rho, A = dict(msgs, r, finals), B = dict(msgs, r,
+    finals), point = r_B || r_A[:n], claim = finals_B[1]): the one claim X~(point) left on the stack."""
+    X = np.ascontiguousarray(X, dtype=np.int32)
+    N, D = X.shape
+    n, d = N.bit_length() - 1, D.bit_length() - 1
+    assert N == 1 << n and D == 1 << d
+    K = len(claims)
+    kap = max(0, (K - 1).bit_length())
+    nk = [len(c["map"]).bit_length() - 1 for c in claims]
+    for c, l in zip(claims, nk):
+        assert len(c["map"]) == 1 << l and len(c["u"]) == l and len(c["v"]) == d
+    maps = np.concatenate([np.asarray(c["map"], dtype=np.int64) & 0xFFFFFFFF for c in claims]).astype(np.uint32)
+    mA = n + kap
+    rho, mgA, rA, fA = _buf(32 * K), _buf(96 * mA), _buf(32 * mA), _buf(64)
+    mgB, rB, fB = _buf(96 * d), _buf(32 * d), _buf(64)
+    s = lib().or_claim_merge_prove(tr.st, _ptr(X), n, d, K, (ctypes.c_uint32 * K)(*nk), _ptr(maps),
+                                   to_bytes([x for c in claims for x in c["u"]]),
+                                   to_bytes([x for c in claims for x in c["v"]]), to_bytes([c["c"] for c in claims]),
+                                   rho, mgA, rA, fA, mgB, rB, fB)
+    if s:
+        raise ValueError(f"or_claim_merge_prove status {s}")
+    fa, fb = from_bytes(mgA.raw[:96 * mA]), from_bytes(mgB.raw[:96 * d])
+    A = dict(msgs=[fa[3 * t:3 * t + 3] for t in range(mA)], r=from_bytes(rA.raw[:32 * mA], mA),
+             finals=from_bytes(fA.raw[:64], 2))
+    B = dict(msgs=[fb[3 * t:3 * t + 3] for t in range(d)], r=from_bytes(rB.raw[:32 * d], d),
+             finals=from_bytes(fB.raw[:64], 2))
+    return dict(rho=from_bytes(rho.raw[:32 * K], K), A=A, B=B, point=B["r"] + A["r"][:n], claim=B["finals"][1])

@@ -766,10 +766,28 @@ enum { T_A0, T_A1, T_OMS, T_EZ, T_EA, T_EGA, T_EGZ, T_EB, T_S, T_SP, T_NT };
  * "relu/x" | "relu/final" (aux~(0,v,w), aux~(1,v,w), aux~(0,v,Q+R-1)).
  * Variables x = (j, i): flat index i*B + j, j bound first (D2).
  */
+/* pts_in: NULL (the points are drawn as above), or the chained form (N3, D25): the four
+ * points u_Z, u_A, u_GA, u_GZ (logD each, concatenated) are given — the single claims the window's
+ * claim merges left on the Z, A, G_A, G_Z stacks ("we presuppose that the proof's execution
+ * over other components yields the claimed evaluations") — and nothing is drawn for them. */
+static int relu_prove_impl(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q,
+                           uint32_t R, const uint8_t *pts_in, uint8_t *claims_out, uint8_t *chal_out,
+                           uint8_t *msgs_out, uint8_t *rpt_out, uint8_t *finals_out);
 int or_relu_prove(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
                   uint8_t *claims_out /* 4 */, uint8_t *chal_out /* 2 + logB + logD: r, r', u_bin */,
                   uint8_t *msgs_out /* (logB+logD) x 4 */, uint8_t *rpt_out /* logB+logD */,
                   uint8_t *finals_out /* 3 */) {
+    return relu_prove_impl(tr, Z, GA, logD, Q, R, NULL, claims_out, chal_out, msgs_out, rpt_out, finals_out);
+}
+int or_relu_prove_pts(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
+                      const uint8_t *pts_in /* 4 x logD */, uint8_t *claims_out, uint8_t *chal_out, uint8_t *msgs_out,
+                      uint8_t *rpt_out, uint8_t *finals_out) {
+    if (!pts_in) return -1;
+    return relu_prove_impl(tr, Z, GA, logD, Q, R, pts_in, claims_out, chal_out, msgs_out, rpt_out, finals_out);
+}
+static int relu_prove_impl(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q,
+                           uint32_t R, const uint8_t *pts_in, uint8_t *claims_out, uint8_t *chal_out,
+                           uint8_t *msgs_out, uint8_t *rpt_out, uint8_t *finals_out) {
     init();
     uint64_t D = 1ULL << logD;
     uint32_t QR = Q + R;
@@ -784,10 +802,18 @@ int or_relu_prove(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t 
     uint32_t hdr[3] = {logD, Q, R};
     absorb_u32s(tr, "relu/hdr", hdr, 3);
     fr uZ[64], uA[64], uGA[64], uGZ[64], ub[64];
-    for (uint32_t i = 0; i < logD; i++) uZ[i] = transcript_challenge(tr, "relu/uZ");
-    for (uint32_t i = 0; i < logD; i++) uA[i] = transcript_challenge(tr, "relu/uA");
-    for (uint32_t i = 0; i < logD; i++) uGA[i] = transcript_challenge(tr, "relu/uGA");
-    for (uint32_t i = 0; i < logD; i++) uGZ[i] = transcript_challenge(tr, "relu/uGZ");
+    if (pts_in) {
+        if (load_point(pts_in, (int)logD, uZ) || load_point(pts_in + 32 * logD, (int)logD, uA) ||
+            load_point(pts_in + 64 * logD, (int)logD, uGA) || load_point(pts_in + 96 * logD, (int)logD, uGZ)) {
+            free(A); free(GZ); free(sg);
+            return -3;
+        }
+    } else {
+        for (uint32_t i = 0; i < logD; i++) uZ[i] = transcript_challenge(tr, "relu/uZ");
+        for (uint32_t i = 0; i < logD; i++) uA[i] = transcript_challenge(tr, "relu/uA");
+        for (uint32_t i = 0; i < logD; i++) uGA[i] = transcript_challenge(tr, "relu/uGA");
+        for (uint32_t i = 0; i < logD; i++) uGZ[i] = transcript_challenge(tr, "relu/uGZ");
+    }
     fr cl[4] = {mle_i32(Z, (int)logD, uZ), mle_i32(A, (int)logD, uA), mle_i32(GA, (int)logD, uGA),
                 mle_i32(GZ, (int)logD, uGZ)};
     for (int i = 0; i < 4; i++) store_canon(cl[i], claims_out + 32 * i);
@@ -1162,6 +1188,109 @@ int or_loss_grad_prove(transcript *tr, uint32_t m, const int32_t *GZ, const int3
 }
 
 /* ------------------------------------------------------------ misc exports */
+/* ------------------------------------------------------------ N3: the claim merge (D25)
+ * Protocol 1 line 8 ends every family's sumcheck with Eq. (sc-reindex) so that
+ * one claim S_i~(u_i) per tensor family remains.  The claims a window leaves on a tensor family come
+ * from different operation families and carry different points on the inner (non-stack) dimensions
+ * as well, so (sc-reindex) is applied in its general form: X is a stack of N = 2^n slices of D = 2^d
+ * int32 entries ([N][D], a point is (inner bits y, then slice bits i), D2).  Claim k is on a view of X
+ * (N_k = 2^{n_k} slots, slot j holding slice map_k[j], 0xffffffff = an all-zero slot) at the point
+ * (v_k over y, u_k over the slots):  c_k = X_k~(v_k, u_k) = sum_j beta(u_k, j) X_{map_k[j]}~(v_k).
+ * With rho_k from the transcript and S_k(i) = sum_j beta(u_k, j) [map_k[j] = i] (p_k of Eq. sc-reindex)
+ *   sum_k rho_k c_k = sum_{i, k} P(i, k) Rt(i, k),   P(i, k) = rho_k S_k(i),  Rt(i, k) = X_i~(v_k)
+ * (k padded with zero terms to 2^kappa).  Phase A: the product sumcheck over the n + kappa variables
+ * (i, then k), claim sum_k rho_k c_k; its finals are P~(r_i, r_k) (the verifier recomputes it from the
+ * maps) and Rt~(r_i, r_k) = sum_k beta(r_k, k) X~(v_k, r_i).  Phase B: the product sumcheck over the d
+ * inner variables of Wy(y) = sum_k beta(r_k, k) beta(v_k, y) and Xr(y) = sum_i beta(r_i, i) X(i, y)
+ * with that claim; its finals are Wy~(r_y) (verifier-computable) and Xr~(r_y) = X~(r_y, r_i), the one
+ * claim left on the stack.  Transcript: "cm/hdr" (n, d, K, n_k...) | "cm/claims" (K) | rho = "cm/rho" x K
+ * | phase A (D3c, n_eq = 0, claim given) | phase B (D3c, n_eq = 0, claim given). */
+int or_claim_merge_prove(transcript *tr, const int32_t *X, uint32_t n, uint32_t d, uint32_t K, const uint32_t *nk,
+                         const uint32_t *maps /* concatenated, 2^{n_k} each */,
+                         const uint8_t *uk_b /* concatenated slot points, n_k each */,
+                         const uint8_t *vk_b /* K x d inner points */, const uint8_t *claims_b /* K */,
+                         uint8_t *rho_out /* K */, uint8_t *msgsA_out /* (n + kappa) x 3 */,
+                         uint8_t *rA_out /* n + kappa */, uint8_t *finA_out /* 2 */, uint8_t *msgsB_out /* d x 3 */,
+                         uint8_t *rB_out /* d */, uint8_t *finB_out /* 2 */) {
+    init();
+    if (K < 1 || K > 16 || n > 24 || d < 1 || d > 30) return -1;
+    uint32_t kap = 0;
+    while ((1u << kap) < K) kap++;
+    if (n + kap < 1) return -1;
+    uint64_t N = 1ULL << n, D = 1ULL << d, NA = N << kap;
+    fr cl[16], rho[16], vk[16][32];
+    for (uint32_t k = 0; k < K; k++) {
+        if (load_canon(claims_b + 32 * k, &cl[k]) || load_point(vk_b + 32ull * d * k, (int)d, vk[k])) return -3;
+        if (nk[k] > 24) return -1;
+    }
+    uint32_t hdr[3 + 16];
+    hdr[0] = n; hdr[1] = d; hdr[2] = K;
+    for (uint32_t k = 0; k < K; k++) hdr[3 + k] = nk[k];
+    absorb_u32s(tr, "cm/hdr", hdr, (int)(3 + K));
+    absorb_frs(tr, "cm/claims", cl, (int)K);
+    for (uint32_t k = 0; k < K; k++) { rho[k] = transcript_challenge(tr, "cm/rho"); store_canon(rho[k], rho_out + 32 * k); }
+    fr claimA = fr_zero();
+    for (uint32_t k = 0; k < K; k++) claimA = fr_add(claimA, fr_mul(rho[k], cl[k]));
+    /* phase A tables, flat index k * N + i */
+    fr *Pt = (fr *)calloc(NA, sizeof(fr)), *Rt = (fr *)calloc(NA, sizeof(fr)), *E = (fr *)malloc(D * sizeof(fr));
+    uint64_t off = 0, uoff = 0;
+    for (uint32_t k = 0; k < K; k++) {
+        fr uk[32];
+        if (load_point(uk_b + 32 * uoff, (int)nk[k], uk)) { free(Pt); free(Rt); free(E); return -3; }
+        for (uint64_t j = 0; j < (1ULL << nk[k]); j++) {     /* S_k(i): the definition, slot by slot */
+            uint32_t i = maps[off + j];
+            if (i == 0xffffffffu) continue;
+            if (i >= N) { free(Pt); free(Rt); free(E); return -1; }
+            Pt[k * N + i] = fr_add(Pt[k * N + i], fr_mul(rho[k], eq_at(uk, (int)nk[k], j)));
+        }
+        off += 1ULL << nk[k];
+        uoff += nk[k];
+        #pragma omp parallel for schedule(static)      /* beta(v_k, y), each entry the direct product */
+        for (uint64_t y = 0; y < D; y++) E[y] = eq_at(vk[k], (int)d, y);
+        #pragma omp parallel for schedule(static)      /* Rt(i, k) = X_i~(v_k): brute-force MLE of slice i */
+        for (uint64_t i = 0; i < N; i++) {
+            fr acc = fr_zero();
+            for (uint64_t y = 0; y < D; y++)
+                if (X[i * D + y]) acc = fr_add(acc, fr_mul(fr_from_i64(X[i * D + y]), E[y]));
+            Rt[k * N + i] = acc;
+        }
+    }
+    uint8_t *tb = (uint8_t *)malloc(2 * NA * 32);
+    for (uint64_t x = 0; x < NA; x++) { store_canon(Pt[x], tb + 32 * x); store_canon(Rt[x], tb + 32 * (NA + x)); }
+    uint8_t cb[32], cout[32];
+    store_canon(claimA, cb);
+    int st = or_sumcheck_prove(tr, n + kap, 0, 2, NULL, tb, cb, cout, msgsA_out, rA_out, finA_out);
+    free(Pt); free(Rt); free(tb);
+    if (st) { free(E); return st; }
+    /* phase B: r_i = rA[0..n), r_k = rA[n..n+kappa) */
+    fr ri[32], rk[8], claimB;
+    if (load_point(rA_out, (int)n, ri) || load_point(rA_out + 32 * n, (int)kap, rk) || load_canon(finA_out + 32, &claimB)) {
+        free(E);
+        return -3;
+    }
+    fr *Wy = (fr *)calloc(D, sizeof(fr)), *Xr = (fr *)calloc(D, sizeof(fr));
+    for (uint32_t k = 0; k < K; k++) {
+        fr bk = eq_at(rk, (int)kap, k);
+        #pragma omp parallel for schedule(static)
+        for (uint64_t y = 0; y < D; y++) Wy[y] = fr_add(Wy[y], fr_mul(bk, eq_at(vk[k], (int)d, y)));
+    }
+    fr *Ei = (fr *)malloc(N * sizeof(fr));
+    for (uint64_t i = 0; i < N; i++) Ei[i] = eq_at(ri, (int)n, i);
+    #pragma omp parallel for schedule(static)
+    for (uint64_t y = 0; y < D; y++) {
+        fr acc = fr_zero();
+        for (uint64_t i = 0; i < N; i++)
+            if (X[i * D + y]) acc = fr_add(acc, fr_mul(Ei[i], fr_from_i64(X[i * D + y])));
+        Xr[y] = acc;
+    }
+    tb = (uint8_t *)malloc(2 * D * 32);
+    for (uint64_t y = 0; y < D; y++) { store_canon(Wy[y], tb + 32 * y); store_canon(Xr[y], tb + 32 * (D + y)); }
+    store_canon(claimB, cb);
+    st = or_sumcheck_prove(tr, d, 0, 2, NULL, tb, cb, cout, msgsB_out, rB_out, finB_out);
+    free(Wy); free(Xr); free(Ei); free(E); free(tb);
+    return st;
+}
+
 void or_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
 int or_get_threads(void) { return omp_get_max_threads(); }
 uint64_t or_transcript_size(void) { return sizeof(transcript); }

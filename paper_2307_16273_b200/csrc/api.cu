@@ -374,7 +374,7 @@ zk_status zk_relu_tables(zk_ctx* ctx, const int32_t* d_Z, const int32_t* d_GA, u
                          int32_t* d_RGA) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(d_Z && d_GA && d_sign && d_A && d_GZ, ZK_ERR_ARG, "null argument");
-    ZK_REQUIRE(Q >= 1 && R >= 1 && Q + R <= 32, ZK_ERR_ARG, "need 1 <= Q, R and Q + R <= 32");
+    ZK_REQUIRE(Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && Q + R <= 32, ZK_ERR_ARG, "need 1 <= Q, R and Q + R <= 32");
     Scratch s(ctx);
     bool ok = relu_tables_dev(ctx, d_Z, d_GA, D, Q, R, d_sign, d_A, d_GZ, d_Zp, d_GAp, d_RZ, d_RGA, s);
     ZK_REQUIRE(ok, ZK_ERR_RANGE, "Z or G_A outside the (Q+R)-bit range");
@@ -386,7 +386,7 @@ zk_status zk_relu_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
                         zk_fr* finals_out) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(tr && d_Z && d_GA, ZK_ERR_ARG, "null argument");
-    ZK_REQUIRE(Q >= 1 && R >= 1 && Q + R <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
+    ZK_REQUIRE(Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && Q + R <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
     const uint32_t logB = relu_logB(Q, R);
     const uint64_t plen = relu_proof_len(logD, logB);
     if (proof_len) {
@@ -418,10 +418,18 @@ zk_status zk_relu_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
 }
 
 // ------------------------------------------------------------------ device-output provers
+// d_out == NULL: size query (*out_len = need).  Otherwise *out_len is the caller's capacity and must
+// hold `need` bytes (else ZK_ERR_ARG, nothing written); on return it is the size written.
 static bool size_query(uint8_t* d_out, uint64_t* out_len, uint64_t need) {
-    if (out_len) *out_len = need;
     ZK_REQUIRE(d_out || out_len, ZK_ERR_ARG, "null output");
-    return d_out == nullptr;
+    if (!d_out) {
+        *out_len = need;
+        return true;
+    }
+    ZK_REQUIRE(out_len, ZK_ERR_ARG, "out_len (the capacity of d_out) is required");
+    ZK_REQUIRE(*out_len >= need, ZK_ERR_ARG, "d_out too small (*out_len < the required size)");
+    *out_len = need;
+    return false;
 }
 
 zk_status zk_matmul_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, const int32_t* d_B, zk_mm_shape shape,
@@ -465,7 +473,7 @@ zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, 
                             uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(tr && d_Z && d_GA && d_range_flag, ZK_ERR_ARG, "null argument");
-    ZK_REQUIRE(Q >= 1 && R >= 1 && Q + R <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
+    ZK_REQUIRE(Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && Q + R <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
     const uint32_t logB = relu_logB(Q, R);
     const uint64_t plen = relu_proof_len(logD, logB);
     const uint64_t off_pt = (plen + 15) & ~15ull;

@@ -308,7 +308,7 @@ zk_status zk_relu_merge(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, cons
     N1_BEGIN(ctx)
     ZK_REQUIRE(tr && d_Z && d_GA && point && finals, ZK_ERR_ARG, "null argument");
     const uint32_t QR = Q + R;
-    ZK_REQUIRE(Q >= 1 && R >= 1 && QR <= 32 && logD >= 1 && logD <= 32, ZK_ERR_ARG, "bad zkReLU shape");
+    ZK_REQUIRE(Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && QR <= 32 && logD >= 1 && logD <= 32, ZK_ERR_ARG, "bad zkReLU shape");
     uint32_t logB = 0;
     while ((1u << logB) < QR) logB++;
     const uint32_t m = logB + 1;
@@ -332,7 +332,7 @@ zk_status zk_relu_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, 
     N1_BEGIN(ctx)
     ZK_REQUIRE(tr && d_Z && d_GA && d_relu_out, ZK_ERR_ARG, "null argument");
     const uint32_t QR = Q + R;
-    ZK_REQUIRE(Q >= 1 && R >= 1 && QR <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
+    ZK_REQUIRE(Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && QR <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
     uint32_t logB = 0;
     while ((1u << logB) < QR) logB++;
     const uint32_t m = logB + 1;

@@ -436,7 +436,7 @@ zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_le
     return guarded(fail, [&] {
         need(st && proof && proof_len >= 12);
         const uint32_t logD = rd32(proof), Q = rd32(proof + 4), R = rd32(proof + 8), QR = Q + R;
-        need(logD >= 1 && logD <= 40 && Q >= 1 && R >= 1 && QR <= 32);
+        need(logD >= 1 && logD <= 40 && Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && QR <= 32);
         uint32_t logB = 0;
         while ((1u << logB) < QR) logB++;
         const uint32_t m = logB + logD;
@@ -517,7 +517,7 @@ zk_status zk_verify_relu_merge(uint8_t st[32], uint32_t logD, uint32_t Q, uint32
                                int32_t* fail) {
     return guarded(fail, [&] {
         const uint32_t QR = Q + R;
-        need(st && relu_point && relu_finals && proof && Q >= 1 && R >= 1 && QR <= 32 && logD >= 1 && logD <= 40);
+        need(st && relu_point && relu_finals && proof && Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && QR <= 32 && logD >= 1 && logD <= 40);
         uint32_t logB = 0;
         while ((1u << logB) < QR) logB++;
         const uint32_t m = logB + 1;
