@@ -267,6 +267,40 @@ zk_status zk_matmul_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, co
 zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
                             uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag);
 zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
+/* zk_relu_prove_chained_dev: zk_relu_prove_dev in the chained window (N3, D25): the points
+ *   u_Z, u_A, u_GA, u_GZ are NOT drawn — they are given (d_pts: device, 4 x logD canonical elements, in
+ *   that order), the points of the single claims the window's claim merges left on the Z, A, G_A, G_Z
+ *   stacks.  The transcript is D3b without the four point draws; the proof's claims are the
+ *   MLEs at the given points (the verifier checks them against the merged claims). */
+zk_status zk_relu_prove_chained_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA,
+                                    uint32_t logD, uint32_t Q, uint32_t R, const uint8_t* d_pts, uint8_t* d_out,
+                                    uint64_t* out_len, uint32_t* d_range_flag);
+
+/* ------------------------------------------- the claim merge (D25)
+ * zk_claim_merge_dev — Protocol 1 line 8: the claims a window's operation families leave on
+ *   views of one tensor family are reduced to ONE claim on its stack by Eq. (sc-reindex) in
+ *   its general form (every claim with its own inner point).  The stack: N = 2^n slices of
+ *   2^log_rows x 2^log_cols int32 entries, row-major (a point on it: col bits, row bits, slice bits; D2),
+ *   read through `source`: 0 = d_X itself, 1 = A = 1{Z >= 0} round(Z / 2^R) formed from d_X = the Z
+ *   words, 2 = G_Z = 1{Z >= 0} round(G_A / 2^R) from d_X = Z and d_X2 = G_A (Lemma 1; the
+ *   tensors anchored by aux).  views[k] (host): 2^logN slots, map[j] = the slice slot j holds
+ *   (0xffffffff: an all-zero slot; injective).  d_pts (device, canonical): per claim, in order, its inner
+ *   point v_k (log_rows + log_cols elements) then its slot point u_k (logN elements); d_claims (device,
+ *   canonical): c_k = X_k~(v_k, u_k).  Transcript: "cm/hdr" (n, d, K, logN_k... u32le) | "cm/claims" |
+ *   rho = "cm/rho" x K | phase A product sumcheck (D3c) over n + kappa variables (kappa = ceil log2 K)
+ *   of P(i, k) = rho_k sum_j beta(u_k, j) [map_k[j] = i] and Rt(i, k) = X_i~(v_k), claim sum rho_k c_k |
+ *   phase B product sumcheck over d = log_rows + log_cols variables of Wy(y) = sum_k beta(r_k, k)
+ *   beta(v_k, y) and Xr(y) = sum_i beta(r_i, i) X(i, y), claim Rt~(r_i, r_k).
+ *   d_out (device, 16-byte aligned, *out_len = capacity in / size out; NULL: size query): proof A |
+ *   proof B (zk_sumcheck_prove layout each) | pad to 16 | point A (n + kappa) | point B (d) | the stack
+ *   point (point B, then point A's first n elements) | the claim X~(stack point) (32 B).  Asynchronous.
+ *   Errors: ZK_ERR_ARG (shape: K <= 8, n <= 16, log_rows, log_cols <= 16, d <= 30, at most 2048 view
+ *   slots in all, n + kappa >= 1; map not injective), ZK_ERR_RANGE (slot outside the stack). */
+typedef struct { uint32_t logN; const uint32_t* map; } zk_cm_view;
+zk_status zk_claim_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_X, const int32_t* d_X2, uint32_t source,
+                             uint32_t R, uint32_t n, uint32_t log_rows, uint32_t log_cols, uint32_t K,
+                             const zk_cm_view* views, const uint8_t* d_pts, const uint8_t* d_claims, uint8_t* d_out,
+                             uint64_t* out_len);
 
 /* ------------------------------------------- host verifiers (D23)
  * Verification replays the same sequence of rounds as proving with O(degree) field
@@ -278,13 +312,20 @@ zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
  * identity), -1 (claim mismatch) or -101 (merge weight final), ZK_ERR_ARG (malformed proof bytes) or
  * ZK_ERR_NONCANONICAL.  The finals in the proof are claims on the committed tensors: the caller checks
  * them against the commitments (out of scope) or against the tensors themselves.
+ * The statement's shape is the verifier's: every verifier takes the expected header (expect = (m, n_eq,
+ *   K), (logD, Q, R), or m) and rejects a proof whose header differs (fail = -2) before reading further.
  * zk_verify_sumcheck: a zk_sumcheck_prove proof (Protocol 3, D3c transcript, D4 messages); w: the
- *   statement's n_eq eq point (host); claim: the claim the verifier expects, or NULL to take the
- *   proof's; point_out: m elements (host, may be NULL).
+ *   statement's n_eq = expect[1] eq point (host); claim: the claim the verifier expects, or NULL to take
+ *   the proof's; point_out: m elements (host, may be NULL).
  * zk_verify_hadamard_zero: a zk_hadamard_zero_prove proof (Protocol 2 zero form, D22): round identities
  *   from c_0 = 0, final Y~(r) - A~(r) B~(r); w_out, point_out: m elements (may be NULL).
  * zk_verify_relu: a zk_relu_prove proof (App. A, D3b): the final identity of the six statements at the
  *   final point with the verifier's own beta, s, s' evaluations; point_out: logB + logD elements.
+ *   pts: NULL (the points are drawn, D3b) or the chained form's given points (4 x logD, D25).
+ * zk_verify_claim_merge: a zk_claim_merge_dev proof (proof A | proof B bytes, D25) for the verifier's own
+ *   statement: n, d, the views (maps), per claim its point (v_k then u_k, host) and claimed value; checks
+ *   both phases, P~ (fail -101) and Wy~ (fail -102) from the maps and points; point_out (d + n) and
+ *   claim_out (1): the one claim left on the stack.
  * zk_verify_loss_grad: the loss-gradient claims (D24): replays "lg/hdr", u, "lg/claims" and checks
  *   G_Z~(u) = Z~(u) - Y~(u) (fail = -100); point_out: m elements.
  * zk_verify_relu_merge: a zk_relu_merge proof (D21) following the zkReLU proof whose point and finals
@@ -292,12 +333,16 @@ zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out);
 zk_status zk_htr_init(const uint8_t seed[32], uint8_t st[32]);
 zk_status zk_htr_absorb(uint8_t st[32], const char* tag, const void* msg, uint64_t len);
 zk_status zk_htr_challenges(uint8_t st[32], const char* tag, uint32_t n, zk_fr* out);
-zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const zk_fr* w,
-                             const zk_fr* claim, zk_fr* point_out, int32_t* fail);
-zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* w_out,
-                                  zk_fr* point_out, int32_t* fail);
-zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const uint32_t expect[3],
+                             const zk_fr* w, const zk_fr* claim, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, uint32_t expect_m,
+                                  zk_fr* w_out, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const uint32_t expect[3],
+                         const zk_fr* pts, zk_fr* point_out, int32_t* fail);
 zk_status zk_verify_loss_grad(uint8_t st[32], uint32_t m, const zk_fr* claims, zk_fr* point_out, int32_t* fail);
+zk_status zk_verify_claim_merge(uint8_t st[32], uint32_t n, uint32_t d, uint32_t K, const zk_cm_view* views,
+                                const zk_fr* pts, const zk_fr* claims, const uint8_t* proof, uint64_t proof_len,
+                                zk_fr* point_out, zk_fr* claim_out, int32_t* fail);
 zk_status zk_verify_relu_merge(uint8_t st[32], uint32_t logD, uint32_t Q, uint32_t R, const zk_fr* relu_point,
                                const zk_fr* relu_finals, const uint8_t* proof, uint64_t proof_len, zk_fr* point_out,
                                int32_t* fail);

@@ -60,6 +60,7 @@ def lib():
         L.or_relu_prove_pts.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp]
         L.or_claim_merge_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp,
                                            vp, vp, vp, vp, vp, vp]
+        L.or_relu_verify_pts.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp]
         L.or_relu_verify.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp]
         L.or_reindex_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp,
                                        vp, vp, vp, vp]
@@ -282,12 +283,16 @@ def relu_prove(tr: Transcript, Z: np.ndarray, GA: np.ndarray, Q: int, R: int, po
                 finals=from_bytes(fin.raw[:96]))
 
 
-def relu_verify(tr: Transcript, Z, GA, Q: int, R: int, claims, msgs, finals) -> int:
+def relu_verify(tr: Transcript, Z, GA, Q: int, R: int, claims, msgs, finals, points=None) -> int:
     Zc = None if Z is None else np.ascontiguousarray(Z, dtype=np.int32).reshape(-1)
     Gc = None if GA is None else np.ascontiguousarray(GA, dtype=np.int32).reshape(-1)
     m = len(msgs)
     logD = m - relu_logB(Q, R)
     flat = [v for row in msgs for v in row]
+    if points is not None:
+        return lib().or_relu_verify_pts(tr.st, None if Zc is None else _ptr(Zc), None if Gc is None else _ptr(Gc),
+                                        logD, Q, R, to_bytes([x for u in points for x in u]), to_bytes(claims),
+                                        to_bytes(flat), to_bytes(finals))
     return lib().or_relu_verify(tr.st, None if Zc is None else _ptr(Zc), None if Gc is None else _ptr(Gc),
                                 logD, Q, R, to_bytes(claims), to_bytes(flat), to_bytes(finals))
 

@@ -114,3 +114,116 @@ def fcn_prove(shape, families, seed_name: str, only=None, merge_aux: bool = Fals
     if out:
         out[-1]["window_state"] = W.state()
     return out
+
+
+# ---------------------------------------------------------------- N3: the claim-chained window (D25)
+def _matmul_family_claims(f, res):
+    """The three claims a matmul family's proof leaves (Eq. exm-matmul-batched): Y~(w, u1, u3) (the
+    claim it started from) and the operand finals A~(r_n, u1, r_k), B~(r_n, r_k, u3), each as a claim on a
+    view of a tensor family: (role, ref, inner point over the stored [rows][cols] slice (col bits, row
+    bits, D2), slot point, value)."""
+    lN = res["logs"][0]
+    rn, rk = res["r"][:lN], res["r"][lN:]
+    vA = res["u1"] + rk if f.transA else rk + res["u1"]
+    vB = rk + res["u3"] if f.transB else res["u3"] + rk
+    return [("Y", f.refs["Y"], res["u3"] + res["u1"], res["w"], res["claim"]),
+            ("A", f.refs["A"], vA, rn, res["finals"][0]),
+            ("B", f.refs["B"], vB, rn, res["finals"][1])]
+
+
+def _is_whole(t, cl):
+    """One claim whose view is the whole stack (slot j -> j; an empty slot only where the stack pads)."""
+    if len(cl) != 1 or len(cl[0]["map"]) != len(t.slots):
+        return False
+    return all((i == j) if i >= 0 else t.slots[j] is None for j, i in enumerate(cl[0]["map"]))
+
+
+def _tensor_values(t, families):
+    """The int32 stack [N][rows * cols] of a tensor family; the ReLU-bound ones from the words (Lemma 1)."""
+    N = len(t.slots)
+    if t.relu is None:
+        return np.ascontiguousarray(t.array.reshape(N, -1))
+    f = next(g for g in families if g.name == t.relu)
+    if t.kind in ("Z", "GA"):
+        v = f.Z if t.kind == "Z" else f.GA
+    else:
+        tb = O.relu_tables(f.Z, f.GA, f.Q, f.R)
+        v = tb["A"] if t.kind == "A" else tb["GZ"]
+    return np.ascontiguousarray(np.asarray(v, dtype=np.int32).reshape(N, -1))
+
+
+def fcn_prove_chained(shape, families, tensors, seed_name: str):
+    """The claim-chained window (Protocol 1 lines 7-8; D25).  Window transcript W:
+    "fcn/chdr" (header) | stage 1: per matmul family "fcn/fam" <name> and a fork; each family proved on
+    its fork (D3a) | "fcn/join" per family | stage 2: per tensor family whose claims need merging (more
+    than one claim, or one claim on a view that is not the whole stack) "fcn/tfam" <name> and a fork; the
+    claim merge (D25) on it | joins | stage 3: per ReLU family "fcn/fam" <name> and a fork; the chained
+    zkReLU (points = the merged claims of its Z, A, G_A, G_Z stacks) and the aux merge (D21) on it
+    | joins.  Returns dict(matmul, merges, relu (per family name), opened: tensor family -> (point, value)
+    for every committed stack and "aux:<ReLU family>" (one claim per tensor family, Protocol 1 line 10),
+    window_state)."""
+    W = O.Transcript(fs_seed(seed_name))
+    W.absorb("fcn/chdr", fcn_header(shape))
+    mms = [f for f in families if isinstance(f, MatmulFamily)]
+    relus = [f for f in families if isinstance(f, ReluFamily)]
+
+    def fork():
+        return O.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little"))
+
+    kids = []
+    for f in mms:
+        W.absorb("fcn/fam", f.name.encode())
+        kids.append(fork())
+    mres = {}
+    for f, T in zip(mms, kids):
+        r = O.matmul_prove(T, f.A, f.B, f.transA, f.transB)
+        r["state"] = T.state()
+        mres[f.name] = r
+    for T in kids:
+        W.absorb("fcn/join", T.state())
+    claims = {t.name: [] for t in tensors}
+    for f in mms:
+        for role, ref, v, u, c in _matmul_family_claims(f, mres[f.name]):
+            claims[ref.tensor].append(dict(map=list(ref.map), u=list(u), v=list(v), c=c, src=(f.name, role)))
+    opened = {}
+    to_merge = []
+    for t in tensors:
+        cl = claims[t.name]
+        if not cl:
+            continue
+        if _is_whole(t, cl):
+            opened[t.name] = (cl[0]["v"] + cl[0]["u"], cl[0]["c"])
+        else:
+            to_merge.append(t)
+    mk = []
+    for t in to_merge:
+        W.absorb("fcn/tfam", t.name.encode())
+        mk.append(fork())
+    merges = {}
+    for t, T in zip(to_merge, mk):
+        r = O.claim_merge_prove(T, _tensor_values(t, families), claims[t.name])
+        r["state"] = T.state()
+        r["claims_in"] = claims[t.name]
+        merges[t.name] = r
+        opened[t.name] = (r["point"], r["claim"])
+    for T in mk:
+        W.absorb("fcn/join", T.state())
+    rk = []
+    for f in relus:
+        W.absorb("fcn/fam", f.name.encode())
+        rk.append(fork())
+    rres = {}
+    for f, T in zip(relus, rk):
+        names = [f.tensors[k] for k in ("Z", "A", "GA", "GZ")]
+        r = O.relu_prove(T, f.Z, f.GA, f.Q, f.R, points=[opened[n][0] for n in names])
+        r["merge"] = O.relu_merge(T, f.Z, f.GA, f.Q, f.R, r["point"], r["finals"])
+        r["state"] = T.state()
+        rres[f.name] = r
+        for n in names:          # bound by the aux commitment through zkReLU (P:L274): not opened
+            opened.pop(n)
+        logB = O.relu_logB(f.Q, f.R)
+        rj, rs = r["merge"]["r"][:logB], r["merge"]["r"][logB:]
+        opened["aux:" + f.name] = (rj + r["point"][logB:] + rs, r["merge"]["finals"][0])
+    for T in rk:
+        W.absorb("fcn/join", T.state())
+    return dict(matmul=mres, merges=merges, relu=rres, opened=opened, window_state=W.state())

@@ -881,8 +881,22 @@ static int relu_prove_impl(transcript *tr, const int32_t *Z, const int32_t *GA, 
  * round identity g(0)+g(1) = c, and the final identity using the verifier's
  * own beta / s / s' evaluations, then the three aux finals against the
  * brute-force MLE of the bits of Z and G_A.  Returns 0 on accept. */
+static int relu_verify_impl(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q,
+                            uint32_t R, const uint8_t *pts_in, const uint8_t *claims_b, const uint8_t *msgs_b,
+                            const uint8_t *finals_b);
 int or_relu_verify(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
                    const uint8_t *claims_b, const uint8_t *msgs_b, const uint8_t *finals_b) {
+    return relu_verify_impl(tr, Z, GA, logD, Q, R, NULL, claims_b, msgs_b, finals_b);
+}
+/* the chained form (D25): the four points are given, not drawn */
+int or_relu_verify_pts(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q, uint32_t R,
+                       const uint8_t *pts_in, const uint8_t *claims_b, const uint8_t *msgs_b, const uint8_t *finals_b) {
+    if (!pts_in) return -1;
+    return relu_verify_impl(tr, Z, GA, logD, Q, R, pts_in, claims_b, msgs_b, finals_b);
+}
+static int relu_verify_impl(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t logD, uint32_t Q,
+                            uint32_t R, const uint8_t *pts_in, const uint8_t *claims_b, const uint8_t *msgs_b,
+                            const uint8_t *finals_b) {
     init();
     uint32_t QR = Q + R, logB = 0;
     while ((1u << logB) < QR) logB++;
@@ -890,10 +904,16 @@ int or_relu_verify(transcript *tr, const int32_t *Z, const int32_t *GA, uint32_t
     uint32_t hdr[3] = {logD, Q, R};
     absorb_u32s(tr, "relu/hdr", hdr, 3);
     fr uZ[64], uA[64], uGA[64], uGZ[64], ub[64], cl[4], fin[3], ev[4], pt[64];
-    for (uint32_t i = 0; i < logD; i++) uZ[i] = transcript_challenge(tr, "relu/uZ");
-    for (uint32_t i = 0; i < logD; i++) uA[i] = transcript_challenge(tr, "relu/uA");
-    for (uint32_t i = 0; i < logD; i++) uGA[i] = transcript_challenge(tr, "relu/uGA");
-    for (uint32_t i = 0; i < logD; i++) uGZ[i] = transcript_challenge(tr, "relu/uGZ");
+    if (pts_in) {
+        if (load_point(pts_in, (int)logD, uZ) || load_point(pts_in + 32 * logD, (int)logD, uA) ||
+            load_point(pts_in + 64 * logD, (int)logD, uGA) || load_point(pts_in + 96 * logD, (int)logD, uGZ))
+            return -3;
+    } else {
+        for (uint32_t i = 0; i < logD; i++) uZ[i] = transcript_challenge(tr, "relu/uZ");
+        for (uint32_t i = 0; i < logD; i++) uA[i] = transcript_challenge(tr, "relu/uA");
+        for (uint32_t i = 0; i < logD; i++) uGA[i] = transcript_challenge(tr, "relu/uGA");
+        for (uint32_t i = 0; i < logD; i++) uGZ[i] = transcript_challenge(tr, "relu/uGZ");
+    }
     for (int i = 0; i < 4; i++) if (load_canon(claims_b + 32 * i, &cl[i])) return -3;
     if (Z && GA) {
         int32_t *A = (int32_t *)malloc(D * 4), *GZ = (int32_t *)malloc(D * 4);

@@ -33,6 +33,10 @@ class View(ctypes.Structure):
     _fields_ = [("logN", ctypes.c_uint32), ("map", ctypes.c_void_p), ("u", ctypes.c_void_p)]
 
 
+class CmView(ctypes.Structure):
+    _fields_ = [("logN", ctypes.c_uint32), ("map", ctypes.c_void_p)]
+
+
 class ProdStmt(ctypes.Structure):
     _fields_ = [("m", ctypes.c_uint32), ("n_eq", ctypes.c_uint32), ("n_tables", ctypes.c_uint32),
                 ("i32_mask", ctypes.c_uint32), ("w", ctypes.c_void_p)]
@@ -101,9 +105,12 @@ def lib():
         "zk_htr_init": ([vp, vp], i32),
         "zk_htr_absorb": ([vp, c.c_char_p, vp, u64], i32),
         "zk_htr_challenges": ([vp, c.c_char_p, u32, vp], i32),
-        "zk_verify_sumcheck": ([vp, vp, u64, vp, vp, vp, vp], i32),
-        "zk_verify_hadamard_zero": ([vp, vp, u64, vp, vp, vp], i32),
-        "zk_verify_relu": ([vp, vp, u64, vp, vp], i32),
+        "zk_verify_sumcheck": ([vp, vp, u64, vp, vp, vp, vp, vp], i32),
+        "zk_verify_hadamard_zero": ([vp, vp, u64, u32, vp, vp, vp], i32),
+        "zk_verify_relu": ([vp, vp, u64, vp, vp, vp, vp], i32),
+        "zk_verify_claim_merge": ([vp, u32, u32, u32, vp, vp, vp, vp, u64, vp, vp, vp], i32),
+        "zk_claim_merge_dev": ([vp, vp, vp, vp, u32, u32, u32, u32, u32, u32, vp, vp, vp, vp, c.POINTER(u64)], i32),
+        "zk_relu_prove_chained_dev": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, c.POINTER(u64), vp], i32),
         "zk_loss_grad_prove": ([vp, vp, vp, vp, vp, u32, vp, vp], i32),
         "zk_verify_loss_grad": ([vp, u32, vp, vp, vp], i32),
         "zk_verify_relu_merge": ([vp, u32, u32, u32, vp, vp, vp, u64, vp, vp], i32),

@@ -12,7 +12,7 @@ import ctypes
 
 import torch
 
-from ._lib import MmShape, ProdStmt, View, ZkError, lib
+from ._lib import CmView, MmShape, ProdStmt, View, ZkError, lib
 
 P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
 
@@ -499,3 +499,67 @@ def loss_grad_prove(ctx: Context, tr: Transcript, GZ: torch.Tensor, Z: torch.Ten
     ctx.check(lib().zk_loss_grad_prove(ctx.h, tr.h, _dev_ptr(GZ, torch.int32), _dev_ptr(Z, torch.int32),
                                        _dev_ptr(Y, torch.int32), m, pt, cl))
     return dict(u=_ints(pt, m), claims=_ints(cl, 3))
+
+
+# ---------------------------------------------------------------- N3: the claim merge (D25)
+CM_SOURCE = {"plain": 0, "relu_A": 1, "relu_GZ": 2}
+
+
+def claim_merge_layout(n: int, K: int, d: int) -> dict:
+    """Byte offsets of a zk_claim_merge_dev output (include/zkdl.h)."""
+    kap = max(0, (K - 1).bit_length())
+    la, lb = 12 + 32 + 96 * (n + kap) + 64, 12 + 32 + 96 * d + 64
+    off_pa = _a16(la + lb)
+    off_pb = off_pa + 32 * (n + kap)
+    off_pt = off_pb + 32 * d
+    off_c = off_pt + 32 * (d + n)
+    return dict(kappa=kap, la=la, lb=lb, off_pa=off_pa, off_pb=off_pb, off_pt=off_pt, off_c=off_c, total=off_c + 32)
+
+
+def claim_merge_dev(ctx: Context, tr: Transcript, X: torch.Tensor, n: int, log_rows: int, log_cols: int, maps: list,
+                    d_pts: torch.Tensor, d_claims: torch.Tensor, source: str = "plain", X2: torch.Tensor | None = None,
+                    R: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_claim_merge_dev: maps = one slot->slice list per claim (-1: empty slot); d_pts / d_claims: device
+    canonical bytes (per claim its inner point then its slot point; the claimed values).  Asynchronous;
+    returns the uint8 output buffer (layout: claim_merge_layout)."""
+    K = len(maps)
+    lay = claim_merge_layout(n, K, log_rows + log_cols)
+    if out is None:
+        out = torch.empty(lay["total"], dtype=torch.uint8, device=X.device)
+    assert out.dtype == torch.uint8 and out.numel() >= lay["total"] and out.is_contiguous()
+    arrs = [(ctypes.c_uint32 * len(m))(*[int(i) & 0xFFFFFFFF for i in m]) for m in maps]
+    views = (CmView * K)(*[CmView(len(m).bit_length() - 1, ctypes.cast(a, ctypes.c_void_p)) for m, a in zip(maps, arrs)])
+    ln = ctypes.c_uint64(out.numel())
+    ctx.check(lib().zk_claim_merge_dev(ctx.h, tr.h, _dev_ptr(X, torch.int32), None if X2 is None else _dev_ptr(X2, torch.int32),
+                                       CM_SOURCE[source], R, n, log_rows, log_cols, K, views, _dev_ptr(d_pts, torch.uint8),
+                                       _dev_ptr(d_claims, torch.uint8), out.data_ptr(), ctypes.byref(ln)))
+    return out
+
+
+def parse_claim_merge_out(raw: bytes, n: int, K: int, d: int) -> dict:
+    lay = claim_merge_layout(n, K, d)
+    A = parse_sumcheck_proof(raw[:lay["la"]])
+    B = parse_sumcheck_proof(raw[lay["la"]:lay["la"] + lay["lb"]])
+    mA = n + lay["kappa"]
+
+    def pts(o, k):
+        return [int.from_bytes(raw[o + 32 * i:o + 32 * i + 32], "little") for i in range(k)]
+    A["r"], B["r"] = pts(lay["off_pa"], mA), pts(lay["off_pb"], d)
+    return dict(A=A, B=B, proof=raw[:lay["la"] + lay["lb"]], point=pts(lay["off_pt"], d + n),
+                claim=pts(lay["off_c"], 1)[0])
+
+
+def relu_prove_chained_dev(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: torch.Tensor, Q: int, R: int,
+                           d_pts: torch.Tensor, range_flag: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_relu_prove_chained_dev: the zkReLU proof at given points (device canonical, 4 x logD)."""
+    logD = _log2(Z.numel())
+    n = relu_prove_len(logD, Q, R)
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=Z.device)
+    assert out.dtype == torch.uint8 and out.numel() >= n and out.is_contiguous()
+    assert d_pts.numel() == 128 * logD
+    ln = ctypes.c_uint64(out.numel())
+    ctx.check(lib().zk_relu_prove_chained_dev(ctx.h, tr.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), logD, Q, R,
+                                              _dev_ptr(d_pts, torch.uint8), out.data_ptr(), ctypes.byref(ln),
+                                              range_flag.data_ptr()))
+    return out

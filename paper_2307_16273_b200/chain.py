@@ -1,0 +1,259 @@
+"""The claim-chained FAC4DNN window on the device (Protocol 1 lines 7-8, P:L320-333;
+DESIGN.md D25).  Sequencing of library calls only (no arithmetic here).
+
+Window transcript W ("fcn/chdr" header), three stages, each a set of forked transcripts joined back:
+  1. every matmul family (zk_matmul_prove on its fork, spread over the matmul streams);
+  2. every tensor family whose claims need merging (zk_claim_merge_dev: the claims of stage 1 on views of
+     it -> one claim on its stack), spread over all streams;
+  3. every ReLU family: zk_relu_prove_chained_dev at the merged points of its Z, A, G_A, G_Z stacks
+     (P:L186), then the aux-claim merge (zk_relu_merge_dev, D21).
+The window ends with one claim per committed tensor family and one on each aux (verify.verify_window_chained
+returns exactly those).  The claims of stage 1 travel to stage 2 as device bytes (slices of the window's
+output buffer gathered on the consuming stream), so the whole window is one stream-ordered program with
+a single host synchronisation.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import api
+from .fcn import DeviceFamily
+from .plan import RELU_ROLES, is_whole, matmul_claim_pieces
+
+
+@dataclass
+class DeviceTensor:
+    """A tensor family on the device: N slots of rows x cols int32 (pad[j]: slot j is zero padding);
+    committed ones hold their stack, ReLU-bound ones name the ReLU family whose words they are formed from."""
+    name: str
+    kind: str
+    pad: list
+    rows: int
+    cols: int
+    relu: str | None = None
+    array: torch.Tensor | None = None
+
+
+@dataclass
+class ChainedFamily(DeviceFamily):
+    refs: dict = field(default_factory=dict)      # matmul: role -> (tensor name, map)
+    tensors: dict = field(default_factory=dict)   # ReLU: role -> tensor name
+
+
+def upload_plan(families, tensors, device="cuda") -> tuple:
+    """synth.fcn families + plan_window tensor families -> device records; an array shared by several
+    families or tensor families (same numpy object) is copied once."""
+    seen = {}
+
+    def dev(a):
+        if id(a) not in seen:
+            seen[id(a)] = torch.from_numpy(a).to(device)
+        return seen[id(a)]
+
+    fams = []
+    for f in families:
+        if hasattr(f, "A"):
+            fams.append(ChainedFamily(f.name, "matmul", A=dev(f.A), B=dev(f.B), trans_a=f.transA, trans_b=f.transB,
+                                      refs={k: (r.tensor, list(r.map)) for k, r in f.refs.items()}))
+        else:
+            fams.append(ChainedFamily(f.name, "relu", Z=dev(f.Z), GA=dev(f.GA), Q=f.Q, R=f.R, tensors=dict(f.tensors)))
+    ts = [DeviceTensor(t.name, t.kind, [s is None for s in t.slots], t.rows, t.cols, t.relu,
+                       None if t.array is None else dev(t.array)) for t in tensors]
+    return fams, ts
+
+
+def _slot(n: int) -> int:
+    return (n + 32 + 255) & ~255
+
+
+def _log2(n: int) -> int:
+    return api._log2(n)
+
+
+def _mm_pieces(logs) -> dict:
+    """Byte ranges (offset, elements) of the named pieces in a zk_matmul_prove output."""
+    lN, l1, l2, l3 = logs
+    np_, m = lN + l1 + l3, lN + l2
+    off = 32 * np_ + 32
+    plen = 12 + 32 + 96 * m + 64
+    o_r = api._a16(off + plen)
+    return dict(w=(0, lN), u1=(32 * lN, l1), u3=(32 * (lN + l1), l3), claim=(32 * np_, 1),
+                fA=(off + plen - 64, 1), fB=(off + plen - 32, 1), rn=(o_r, lN), rk=(o_r + 32 * lN, l2))
+
+
+class _Lanes:
+    """Streams a stage spreads its proofs over (least-loaded first)."""
+
+    def __init__(self, ctxs):
+        self.ctxs, self.load = ctxs, [0] * len(ctxs)
+
+    def pick(self, work: int):
+        j = min(range(len(self.ctxs)), key=lambda j: self.load[j])
+        self.load[j] += work
+        return self.ctxs[j]
+
+
+def _fence(src, dsts):
+    ev = torch.cuda.Event()
+    ev.record(src.stream)
+    for c in dsts:
+        if c.stream != src.stream:
+            c.stream.wait_event(ev)
+
+
+def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
+                           relu_ctx: api.Context | None = None, mm_ctxs: list | None = None):
+    """Enqueue one chained window without synchronising; returns a handle for collect_window_chained."""
+    dev = next(f.A for f in families if f.kind == "matmul").device
+    mms = [f for f in families if f.kind == "matmul"]
+    relus = [f for f in families if f.kind == "relu"]
+    tmap = {t.name: t for t in tensors}
+    lanes1 = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
+    rctx = relu_ctx if relu_ctx is not None else ctx
+    lanes2 = lanes1 + ([rctx] if rctx.stream not in [c.stream for c in lanes1] else [])
+    # ---- layout of the window's output buffer
+    off = 0
+    lay1 = []
+    for f in mms:
+        logs = api._mm_logs(f.A, f.B, f.trans_a, f.trans_b)
+        n = api.matmul_prove_len(logs)
+        lay1.append((f, logs, off, n))
+        off += _slot(n)
+    # the claims stage 1 leaves, per tensor family (in family order, roles Y, A, B)
+    claims = {t.name: [] for t in tensors}
+    for f, logs, o, n in lay1:
+        pieces = _mm_pieces(logs)
+        for role, vp, up, cp in matmul_claim_pieces(f.trans_a, f.trans_b):
+            tname, mp = f.refs[role]
+            rng = lambda names: [(o + pieces[p][0], pieces[p][1]) for p in names]
+            claims[tname].append(dict(map=mp, v=rng(vp), u=rng(up), c=rng([cp]), src=(f.name, role)))
+    merges = [t for t in tensors if claims[t.name] and not is_whole(t.pad, [c["map"] for c in claims[t.name]])]
+    lay2 = []
+    for t in merges:
+        n = _log2(len(t.pad))
+        cl = claims[t.name]
+        L = api.claim_merge_layout(n, len(cl), _log2(t.rows) + _log2(t.cols))
+        lay2.append((t, n, cl, off, L))
+        off += _slot(L["total"])
+    lay3 = []
+    for f in relus:
+        logD = _log2(f.Z.numel())
+        rn = api.relu_prove_len(logD, f.Q, f.R)
+        n = api._a16(rn) + api.relu_merge_len(f.Q, f.R)
+        lay3.append((f, logD, rn, off, n))
+        off += _slot(n)
+    out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    keep = []   # device temporaries in use by enqueued work
+
+    def gather(c, ranges):
+        with torch.cuda.stream(c.stream):
+            g = torch.cat([out[a:a + 32 * k] for a, k in ranges if k]) if any(k for _, k in ranges) else \
+                torch.zeros(0, dtype=torch.uint8, device=dev)
+        keep.append(g)
+        return g
+
+    W = api.Transcript(ctx, seed)
+    W.absorb("fcn/chdr", header)
+    # ---- stage 1: the matmul families
+    L1 = _Lanes(lanes1)
+    home1 = {}
+    for i in sorted(range(len(mms)), key=lambda i: -(mms[i].A.numel() + mms[i].B.numel())):
+        home1[i] = L1.pick(mms[i].A.numel() + mms[i].B.numel())
+    kids1 = []
+    for i, f in enumerate(mms):
+        W.absorb("fcn/fam", f.name.encode())
+        kids1.append(W.fork("fcn/fork", home1[i]))
+    _fence(ctx, lanes1)
+    for i, (f, logs, o, n) in enumerate(lay1):
+        c, T = home1[i], kids1[i]
+        api.matmul_prove(c, T, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
+        T.state_dev(out[o + n:o + n + 32])
+    for c in lanes1[1:]:
+        _fence(c, [ctx])
+    for T in kids1:
+        W.absorb_state("fcn/join", T)
+    # ---- stage 2: one claim per tensor family
+    L2 = _Lanes(lanes2)
+    home2 = [L2.pick(len(t.pad) * t.rows * t.cols) for t, *_ in lay2]
+    kids2 = []
+    for (t, *_), c in zip(lay2, home2):
+        W.absorb("fcn/tfam", t.name.encode())
+        kids2.append(W.fork("fcn/fork", c))
+    _fence(ctx, lanes2)
+    for (t, n, cl, o, L), c, T in zip(lay2, home2, kids2):
+        d_pts = gather(c, [r for x in cl for r in x["v"] + x["u"]])
+        d_cl = gather(c, [r for x in cl for r in x["c"]])
+        maps = [x["map"] for x in cl]
+        lr, lc = _log2(t.rows), _log2(t.cols)
+        if t.relu is None:
+            api.claim_merge_dev(c, T, t.array, n, lr, lc, maps, d_pts, d_cl, out=out[o:o + L["total"]])
+        else:
+            f = next(g for g in relus if g.name == t.relu)
+            src = {"Z": ("plain", f.Z, None), "GA": ("plain", f.GA, None), "A": ("relu_A", f.Z, None),
+                   "GZ": ("relu_GZ", f.Z, f.GA)}[t.kind]
+            api.claim_merge_dev(c, T, src[1], n, lr, lc, maps, d_pts, d_cl, source=src[0], X2=src[2], R=f.R,
+                                out=out[o:o + L["total"]])
+        T.state_dev(out[o + L["total"]:o + L["total"] + 32])
+    for c in lanes2[1:]:
+        _fence(c, [ctx])
+    for T in kids2:
+        W.absorb_state("fcn/join", T)
+    # ---- stage 3: the chained zkReLU families and their aux merges
+    pos2 = {t.name: (o, L) for t, n, cl, o, L in lay2}
+    kids3 = []
+    for f in relus:
+        W.absorb("fcn/fam", f.name.encode())
+        kids3.append(W.fork("fcn/fork", rctx))
+    _fence(ctx, [rctx])
+    for (f, logD, rn, o, n), T in zip(lay3, kids3):
+        rngs = []
+        for role in RELU_ROLES:
+            to, tl = pos2[f.tensors[role]]
+            rngs.append((to + tl["off_pt"], logD))
+        d_pts = gather(rctx, rngs)
+        api.relu_prove_chained_dev(rctx, T, f.Z, f.GA, f.Q, f.R, d_pts, flag, out=out[o:o + rn])
+        mo = o + api._a16(rn)
+        api.relu_merge_dev(rctx, T, f.Z, f.GA, f.Q, f.R, out[o:o + rn], out=out[mo:o + n])
+        T.state_dev(out[o + n:o + n + 32])
+    _fence(rctx, [ctx])
+    for T in kids3:
+        W.absorb_state("fcn/join", T)
+    W.state_dev(out[off:off + 32])
+    _fence(ctx, lanes2)      # the children are freed on their own streams: after the joins
+    for T in kids1 + kids2 + kids3:
+        T.close()
+    W.close()
+    return dict(out=out, flag=flag, lay1=lay1, lay2=lay2, lay3=lay3, end=off, keep=keep, claims=claims)
+
+
+def collect_window_chained(h: dict) -> dict:
+    """The one synchronisation: copy the window's outputs back and parse them.  Returns dict(matmul:
+    name -> result, merges: tensor name -> result, relu: name -> result, window_state)."""
+    raw = h["out"].cpu().numpy().tobytes()
+    if int(h["flag"].item()) & 1:
+        raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")
+    res = dict(matmul={}, merges={}, relu={})
+    for f, logs, o, n in h["lay1"]:
+        r = api.parse_matmul_out(raw[o:o + n], logs)
+        res["matmul"][f.name] = dict(logs=logs, w=r["w"], u1=r["u1"], u3=r["u3"], claim=r["claim"], msgs=r["msgs"],
+                                     r=r["r"], finals=r["finals"], proof=r["proof"], state=raw[o + n:o + n + 32])
+    for t, n, cl, o, L in h["lay2"]:
+        d = _log2(t.rows) + _log2(t.cols)
+        r = api.parse_claim_merge_out(raw[o:o + L["total"]], n, len(cl), d)
+        r["state"] = raw[o + L["total"]:o + L["total"] + 32]
+        res["merges"][t.name] = r
+    for f, logD, rn, o, n in h["lay3"]:
+        r = api.parse_relu_out(raw[o:o + rn], logD, f.Q, f.R)
+        r["merge"] = api.parse_relu_merge_out(raw[o + api._a16(rn):o + n], f.Q, f.R)
+        r["state"] = raw[o + n:o + n + 32]
+        res["relu"][f.name] = r
+    res["window_state"] = raw[h["end"]:h["end"] + 32]
+    return res
+
+
+def prove_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
+                         relu_ctx: api.Context | None = None, mm_ctxs: list | None = None) -> dict:
+    return collect_window_chained(enqueue_window_chained(ctx, seed, header, families, tensors, relu_ctx, mm_ctxs))

@@ -469,8 +469,8 @@ zk_status zk_matmul_prove(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_A, co
     ZK_API_END(ctx)
 }
 
-zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
-                            uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag) {
+static zk_status relu_prove_dev_entry(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                            uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag, const uint8_t* d_pts) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(tr && d_Z && d_GA && d_range_flag, ZK_ERR_ARG, "null argument");
     ZK_REQUIRE(Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && Q + R <= 32 && logD >= 1 && logD <= 30, ZK_ERR_ARG, "bad zkReLU shape");
@@ -483,8 +483,20 @@ zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, 
     ReluOutputs o;
     o.d_proof = d_out;
     o.d_point = d_out + off_pt;
-    relu_prove_dev(ctx, tr, d_Z, d_GA, logD, Q, R, o, d_range_flag, s);
+    relu_prove_dev(ctx, tr, d_Z, d_GA, logD, Q, R, o, d_range_flag, s, d_pts);
     ZK_API_END(ctx)
+}
+
+zk_status zk_relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA, uint32_t logD,
+                            uint32_t Q, uint32_t R, uint8_t* d_out, uint64_t* out_len, uint32_t* d_range_flag) {
+    return relu_prove_dev_entry(ctx, tr, d_Z, d_GA, logD, Q, R, d_out, out_len, d_range_flag, nullptr);
+}
+
+zk_status zk_relu_prove_chained_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, const int32_t* d_GA,
+                                    uint32_t logD, uint32_t Q, uint32_t R, const uint8_t* d_pts, uint8_t* d_out,
+                                    uint64_t* out_len, uint32_t* d_range_flag) {
+    if (!d_pts && d_out) return ZK_ERR_ARG;
+    return relu_prove_dev_entry(ctx, tr, d_Z, d_GA, logD, Q, R, d_out, out_len, d_range_flag, d_pts);
 }
 
 zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out) {

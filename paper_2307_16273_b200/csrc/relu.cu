@@ -1306,8 +1306,10 @@ __global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
 }
 
 // ---------------------------------------------------------------- driver
+__global__ void k_canon_to_mont(const uint8_t* in, uint32_t n, fr_t* out);   // n1.cu
+
 void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,
-                    uint32_t R, ReluOutputs& out, unsigned int* range_flag, Scratch& s) {
+                    uint32_t R, ReluOutputs& out, unsigned int* range_flag, Scratch& s, const uint8_t* d_pts) {
     const uint32_t QR = Q + R;
     const uint32_t logB = relu_logB(Q, R), B = 1u << logB;
     const uint64_t D = 1ull << logD;
@@ -1323,10 +1325,14 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     tr_absorb_host(tr, "relu/hdr", hdr, 12, proof);
     // points u_Z, u_A, u_GA, u_GZ
     fr_t* U = s.alloc<fr_t>(4ull * logD);
-    tr_challenges_dev(tr, "relu/uZ", logD, U, nullptr);
-    tr_challenges_dev(tr, "relu/uA", logD, U + logD, nullptr);
-    tr_challenges_dev(tr, "relu/uGA", logD, U + 2 * logD, nullptr);
-    tr_challenges_dev(tr, "relu/uGZ", logD, U + 3 * logD, nullptr);
+    if (d_pts) {   // chained (D25): the window's merged claims give the points; nothing is drawn
+        ZK_LAUNCH(ctx, k_canon_to_mont, 1, 128, 0, d_pts, 4 * logD, U);
+    } else {
+        tr_challenges_dev(tr, "relu/uZ", logD, U, nullptr);
+        tr_challenges_dev(tr, "relu/uA", logD, U + logD, nullptr);
+        tr_challenges_dev(tr, "relu/uGA", logD, U + 2 * logD, nullptr);
+        tr_challenges_dev(tr, "relu/uGZ", logD, U + 3 * logD, nullptr);
+    }
     // claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) with A, G_Z formed on the fly (Lemma 1)
     fr_t* claims = s.alloc<fr_t>(4);
     mle_i32_relu4(ctx, Z, GA, R, logD, U, claims, s);

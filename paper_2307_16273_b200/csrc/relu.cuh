@@ -27,6 +27,7 @@ void relu_bitsums_gram(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint32_
 // Enqueues the whole proof; bit 0 of *range_flag (device word, not cleared here) is set if an input
 // lies outside the (Q+R)-bit range (never for Q+R = 32: every int32 is in range).
 void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int32_t* GA, uint32_t logD, uint32_t Q,
-                    uint32_t R, ReluOutputs& out, unsigned int* range_flag, Scratch& s);
+                    uint32_t R, ReluOutputs& out, unsigned int* range_flag, Scratch& s,
+                    const uint8_t* d_pts = nullptr /* chained (D25): 4 x logD canonical points, device */);
 
 }  // namespace zk

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "zkdl.h"
 
@@ -383,11 +384,13 @@ zk_status zk_htr_challenges(uint8_t st[32], const char* tag, uint32_t n, zk_fr* 
     return ZK_OK;
 }
 
-zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const zk_fr* w,
-                             const zk_fr* claim, zk_fr* point_out, int32_t* fail) {
+zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const uint32_t expect[3],
+                             const zk_fr* w, const zk_fr* claim, zk_fr* point_out, int32_t* fail) {
     return guarded(fail, [&] {
-        need(st && proof && proof_len >= 12);
+        need(st && proof && expect && proof_len >= 12);
         const uint32_t m = rd32(proof), n_eq = rd32(proof + 4), K = rd32(proof + 8);
+        // the statement's shape is the verifier's, not the prover's: the header must match it
+        if (m != expect[0] || n_eq != expect[1] || K != expect[2]) throw Reject{-2};
         need(m >= 1 && m <= 64 && n_eq <= m && K >= 1 && K <= 3 && (n_eq == 0 || w));
         need(proof_len == 12 + 32 + 32ull * m * (K + 1) + 32ull * K);
         F wf[64], r[64];
@@ -402,11 +405,12 @@ zk_status zk_verify_sumcheck(uint8_t st[32], const uint8_t* proof, uint64_t proo
     });
 }
 
-zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* w_out,
-                                  zk_fr* point_out, int32_t* fail) {
+zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, uint32_t expect_m,
+                                  zk_fr* w_out, zk_fr* point_out, int32_t* fail) {
     return guarded(fail, [&] {
         need(st && proof && proof_len >= 4);
         const uint32_t m = rd32(proof);
+        if (m != expect_m) throw Reject{-2};
         need(m >= 1 && m <= 64 && proof_len == 4 + 96ull * m + 96);
         tr_absorb_u32s(st, "hd/hdr", &m, 1);
         F w[64], r[64];
@@ -432,11 +436,14 @@ zk_status zk_verify_hadamard_zero(uint8_t st[32], const uint8_t* proof, uint64_t
 
 // zkReLU (App. A; transcript D3b).  The final identity is the six statements of
 // Eq. (zkrelu-*-sc) at the final point, with the verifier's own beta, s and s' evaluations.
-zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, zk_fr* point_out, int32_t* fail) {
+zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const uint32_t expect[3],
+                         const zk_fr* pts, zk_fr* point_out, int32_t* fail) {
     return guarded(fail, [&] {
-        need(st && proof && proof_len >= 12);
-        const uint32_t logD = rd32(proof), Q = rd32(proof + 4), R = rd32(proof + 8), QR = Q + R;
-        need(logD >= 1 && logD <= 40 && Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && QR <= 32);
+        need(st && proof && expect && proof_len >= 12);
+        const uint32_t logD = rd32(proof), Q = rd32(proof + 4), R = rd32(proof + 8);
+        if (logD != expect[0] || Q != expect[1] || R != expect[2]) throw Reject{-2};
+        need(logD >= 1 && logD <= 40 && Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && Q + R <= 32);
+        const uint32_t QR = Q + R;
         uint32_t logB = 0;
         while ((1u << logB) < QR) logB++;
         const uint32_t m = logB + logD;
@@ -444,10 +451,19 @@ zk_status zk_verify_relu(uint8_t st[32], const uint8_t* proof, uint64_t proof_le
         const uint32_t hdr[3] = {logD, Q, R};
         tr_absorb_u32s(st, "relu/hdr", hdr, 3);
         F uZ[40], uA[40], uGA[40], uGZ[40], ub[72], cl[4], pt[72], fin[3];
-        for (uint32_t i = 0; i < logD; i++) uZ[i] = tr_challenge(st, "relu/uZ");
-        for (uint32_t i = 0; i < logD; i++) uA[i] = tr_challenge(st, "relu/uA");
-        for (uint32_t i = 0; i < logD; i++) uGA[i] = tr_challenge(st, "relu/uGA");
-        for (uint32_t i = 0; i < logD; i++) uGZ[i] = tr_challenge(st, "relu/uGZ");
+        if (pts) {   // chained (D25): the points of the window's merged claims, nothing drawn
+            for (uint32_t i = 0; i < logD; i++) {
+                uZ[i] = ld(pts[i].b);
+                uA[i] = ld(pts[logD + i].b);
+                uGA[i] = ld(pts[2 * logD + i].b);
+                uGZ[i] = ld(pts[3 * logD + i].b);
+            }
+        } else {
+            for (uint32_t i = 0; i < logD; i++) uZ[i] = tr_challenge(st, "relu/uZ");
+            for (uint32_t i = 0; i < logD; i++) uA[i] = tr_challenge(st, "relu/uA");
+            for (uint32_t i = 0; i < logD; i++) uGA[i] = tr_challenge(st, "relu/uGA");
+            for (uint32_t i = 0; i < logD; i++) uGZ[i] = tr_challenge(st, "relu/uGZ");
+        }
         for (int i = 0; i < 4; i++) cl[i] = ld(proof + 12 + 32 * i);
         tr_absorb_frs(st, "relu/claims", cl, 4);
         const F r = tr_challenge(st, "relu/r"), rp = tr_challenge(st, "relu/rp");
@@ -537,6 +553,81 @@ zk_status zk_verify_relu_merge(uint8_t st[32], uint32_t logD, uint32_t Q, uint32
         const F W = add(mul(one_minus(rs), add(bw, mul(rho2, beta_at(r, logB, QR - 1)))), mul(rs, mul(rho, bw)));
         if (!eq(ld(proof + 44 + 96ull * m + 32), W)) throw Reject{-101};
         out_points(r, m, point_out);
+    });
+}
+
+// The claim merge (N3, D25; Eq. sc-reindex P:L262-270 in its general form): the verifier forms the
+// phase-A claim sum_k rho_k c_k itself, recomputes P~(r_i, r_k) = sum_k beta(r_k, k) rho_k sum_j
+// beta(u_k, j) beta(map_k[j], r_i) from the maps and Wy~(r_y) = sum_k beta(r_k, k) beta(v_k, r_y); the
+// phase-B claim is phase A's second final.  Output: the stack point (r_y, r_i) and the claim X~ there.
+zk_status zk_verify_claim_merge(uint8_t st[32], uint32_t n, uint32_t d, uint32_t K, const zk_cm_view* views,
+                                const zk_fr* pts, const zk_fr* claims, const uint8_t* proof, uint64_t proof_len,
+                                zk_fr* point_out, zk_fr* claim_out, int32_t* fail) {
+    return guarded(fail, [&] {
+        need(st && views && pts && claims && proof && K >= 1 && K <= 8 && n <= 16 && d >= 1 && d <= 40);
+        uint32_t kap = 0;
+        while ((1u << kap) < K) kap++;
+        const uint32_t mA = n + kap;
+        need(mA >= 1);
+        const uint64_t la = 12 + 32 + 96ull * mA + 64, lb = 12 + 32 + 96ull * d + 64;
+        need(proof_len == la + lb);
+        if (rd32(proof) != mA || rd32(proof + 4) != 0 || rd32(proof + 8) != 2) throw Reject{-2};
+        if (rd32(proof + la) != d || rd32(proof + la + 4) != 0 || rd32(proof + la + 8) != 2) throw Reject{-2};
+        std::vector<uint32_t> hdr = {n, d, K};
+        std::vector<F> cl(K), v(K * (size_t)d);
+        std::vector<std::vector<F>> u(K);
+        size_t po = 0;
+        for (uint32_t k = 0; k < K; k++) {
+            need(views[k].logN <= 16 && views[k].map);
+            hdr.push_back(views[k].logN);
+            cl[k] = ld(claims[k].b);
+            for (uint32_t t = 0; t < d; t++) v[k * (size_t)d + t] = ld(pts[po++].b);
+            for (uint32_t t = 0; t < views[k].logN; t++) u[k].push_back(ld(pts[po++].b));
+            for (uint64_t j = 0; j < (1ull << views[k].logN); j++) {
+                const uint32_t i = views[k].map[j];
+                need(i == 0xffffffffu || (n < 32 && i < (1u << n)), ZK_ERR_RANGE);
+            }
+        }
+        tr_absorb_u32s(st, "cm/hdr", hdr.data(), (uint32_t)hdr.size());
+        tr_absorb_frs(st, "cm/claims", cl.data(), K);
+        std::vector<F> rho(K);
+        F cA = zero();
+        for (uint32_t k = 0; k < K; k++) {
+            rho[k] = tr_challenge(st, "cm/rho");
+            cA = add(cA, mul(rho[k], cl[k]));
+        }
+        if (!eq(ld(proof + 12), cA)) throw Reject{-1};
+        const uint32_t hA[3] = {mA, 0, 2};
+        tr_absorb_u32s(st, "sc/hdr", hA, 3);
+        tr_absorb_frs(st, "sc/claim", &cA, 1);
+        F rA[64], rB[64];
+        sumcheck_rounds(st, mA, 0, 2, nullptr, cA, proof + 44, proof + 44 + 96ull * mA, rA);
+        const F* ri = rA;
+        const F* rk = rA + n;
+        F Pv = zero();
+        for (uint32_t k = 0; k < K; k++) {
+            F sk = zero();
+            for (uint64_t j = 0; j < (1ull << views[k].logN); j++) {
+                const uint32_t i = views[k].map[j];
+                if (i == 0xffffffffu) continue;
+                sk = add(sk, mul(beta_at(u[k].data(), views[k].logN, j), beta_at(ri, n, i)));
+            }
+            Pv = add(Pv, mul(beta_at(rk, kap, k), mul(rho[k], sk)));
+        }
+        if (!eq(ld(proof + 44 + 96ull * mA), Pv)) throw Reject{-101};
+        const F cB = ld(proof + 44 + 96ull * mA + 32);
+        const uint8_t* pb = proof + la;
+        if (!eq(ld(pb + 12), cB)) throw Reject{-1};
+        const uint32_t hB[3] = {d, 0, 2};
+        tr_absorb_u32s(st, "sc/hdr", hB, 3);
+        tr_absorb_frs(st, "sc/claim", &cB, 1);
+        sumcheck_rounds(st, d, 0, 2, nullptr, cB, pb + 44, pb + 44 + 96ull * d, rB);
+        F Wv = zero();
+        for (uint32_t k = 0; k < K; k++) Wv = add(Wv, mul(beta_at(rk, kap, k), beta(&v[k * (size_t)d], rB, d)));
+        if (!eq(ld(pb + 44 + 96ull * d), Wv)) throw Reject{-102};
+        out_points(rB, d, point_out);
+        if (point_out) out_points(ri, n, point_out + d);
+        if (claim_out) store(ld(pb + 44 + 96ull * d + 32), claim_out->b);
     });
 }
 

@@ -3,9 +3,11 @@ zk_htr_* (verify.cu, plain host code), and the window verifier that replays the 
 transcripts of a FAC4DNN proving window.
 
 Verification replays the prover's rounds; every round identity and each protocol's final
-identity is checked here.  The finals are claims on the committed tensors (commitments: out of scope,
-SURVEY §8(f) N4); `verify_window` returns them per family so a caller holding the tensors (tests) or
-their commitments can close them.
+identity is checked here.  The statement's shape is always the verifier's own (a proof whose header
+differs is rejected before anything else is read).  Every value returned — claims, finals, points — is
+read from the verified proof bytes or drawn by the verifier itself, never taken from the prover's
+result dicts: those values are the claims left for the commitments (out of scope), so
+a caller holding the tensors (tests) or their commitments closes them.
 """
 from __future__ import annotations
 
@@ -74,28 +76,53 @@ def _run(what: str, fn, *args) -> None:
         raise Rejected(what, fail.value)
 
 
-def verify_sumcheck(tr: HostTranscript, proof: bytes, w: list, claim: int | None = None) -> list:
-    """zk_verify_sumcheck: returns the point r; raises Rejected."""
-    m = int.from_bytes(proof[:4], "little")
-    pt = ctypes.create_string_buffer(32 * m)
-    _run("sumcheck", lib().zk_verify_sumcheck, tr.st, proof, len(proof), _fr(w),
+def _fin(proof: bytes, k: int) -> list:
+    """The last k field elements of a proof (its finals), as bytes the verifier has just checked."""
+    return [int.from_bytes(proof[len(proof) - 32 * (k - i):len(proof) - 32 * (k - i - 1)], "little") for i in range(k)]
+
+
+def verify_sumcheck(tr: HostTranscript, proof: bytes, w: list, claim: int | None = None, *, shape) -> list:
+    """zk_verify_sumcheck for the statement shape = (m, n_eq, K): returns the point r; raises Rejected."""
+    m, n_eq, K = (int(v) for v in shape)
+    if len(w) != n_eq:
+        raise ValueError("w must have n_eq elements")
+    pt = ctypes.create_string_buffer(32 * max(1, m))
+    _run("sumcheck", lib().zk_verify_sumcheck, tr.st, proof, len(proof), (ctypes.c_uint32 * 3)(m, n_eq, K), _fr(w),
          None if claim is None else _fr([claim]), pt)
     return _ints(pt, m)
 
 
-def verify_hadamard_zero(tr: HostTranscript, proof: bytes) -> dict:
-    m = int.from_bytes(proof[:4], "little")
-    w, pt = ctypes.create_string_buffer(32 * m), ctypes.create_string_buffer(32 * m)
-    _run("hadamard zero", lib().zk_verify_hadamard_zero, tr.st, proof, len(proof), w, pt)
-    return dict(w=_ints(w, m), r=_ints(pt, m))
+def sumcheck_finals(proof: bytes) -> list:
+    K = int.from_bytes(proof[8:12], "little")
+    return _fin(proof, K)
 
 
-def verify_relu(tr: HostTranscript, proof: bytes) -> list:
-    logD, Q, R = (int.from_bytes(proof[4 * i:4 * i + 4], "little") for i in range(3))
+def verify_hadamard_zero(tr: HostTranscript, proof: bytes, m: int) -> dict:
+    w, pt = ctypes.create_string_buffer(32 * max(1, m)), ctypes.create_string_buffer(32 * max(1, m))
+    _run("hadamard zero", lib().zk_verify_hadamard_zero, tr.st, proof, len(proof), m, w, pt)
+    return dict(w=_ints(w, m), r=_ints(pt, m), finals=_fin(proof, 3))
+
+
+def relu_points(tr: HostTranscript, logD: int, Q: int, R: int) -> list:
+    """The four points D3b draws (u_Z, u_A, u_GA, u_GZ) — drawn on a copy of the transcript."""
+    T = HostTranscript(state=tr.state())
+    T.absorb("relu/hdr", b"".join(int(v).to_bytes(4, "little") for v in (logD, Q, R)))
+    return [T.challenges(t, logD) for t in ("relu/uZ", "relu/uA", "relu/uGA", "relu/uGZ")]
+
+
+def verify_relu(tr: HostTranscript, proof: bytes, shape, points: list | None = None) -> dict:
+    """zk_verify_relu for shape = (logD, Q, R); points: None (D3b draws them) or the chained form's given
+    points (D25).  Returns dict(points, claims, point, finals) from the verified proof."""
+    logD, Q, R = (int(v) for v in shape)
+    if not (1 <= logD <= 40 and 1 <= Q <= 32 and 1 <= R <= 32 and Q + R <= 32):
+        raise ValueError("bad zkReLU shape")
     m = max(0, (Q + R - 1).bit_length()) + logD
+    pts = relu_points(tr, logD, Q, R) if points is None else [list(u) for u in points]
     pt = ctypes.create_string_buffer(32 * m)
-    _run("zkReLU", lib().zk_verify_relu, tr.st, proof, len(proof), pt)
-    return _ints(pt, m)
+    _run("zkReLU", lib().zk_verify_relu, tr.st, proof, len(proof), (ctypes.c_uint32 * 3)(logD, Q, R),
+         None if points is None else _fr([x for u in points for x in u]), pt)
+    claims = [int.from_bytes(proof[12 + 32 * i:44 + 32 * i], "little") for i in range(4)]
+    return dict(points=pts, claims=claims, point=_ints(pt, m), finals=_fin(proof, 3))
 
 
 def verify_loss_grad(tr: HostTranscript, m: int, claims: list) -> list:
@@ -106,32 +133,63 @@ def verify_loss_grad(tr: HostTranscript, m: int, claims: list) -> list:
 
 
 def verify_relu_merge(tr: HostTranscript, logD: int, Q: int, R: int, relu_point: list, relu_finals: list,
-                      proof: bytes) -> list:
+                      proof: bytes) -> dict:
+    """zk_verify_relu_merge (D21): returns dict(point = (r_j, r_s), claim = aux~(r_s, v, r_j), weight)."""
     m = max(0, (Q + R - 1).bit_length()) + 1
     pt = ctypes.create_string_buffer(32 * m)
     _run("zkReLU merge", lib().zk_verify_relu_merge, tr.st, logD, Q, R, _fr(relu_point), _fr(relu_finals), proof,
          len(proof), pt)
-    return _ints(pt, m)
+    f = _fin(proof, 2)
+    return dict(point=_ints(pt, m), claim=f[0], weight=f[1])
 
 
-def verify_matmul(tr: HostTranscript, logs, res: dict) -> list:
+def verify_claim_merge(tr: HostTranscript, n: int, d: int, claims: list, proof: bytes) -> tuple:
+    """zk_verify_claim_merge (D25).  claims: dicts(map, v (d elements), u (log2 len(map)), c).
+    Returns (point (d + n), claim): the one claim left on the stack."""
+    from ._lib import CmView
+    K = len(claims)
+    arrs = [(ctypes.c_uint32 * len(c["map"]))(*[int(i) & 0xFFFFFFFF for i in c["map"]]) for c in claims]
+    views = (CmView * K)(*[CmView(len(c["map"]).bit_length() - 1, ctypes.cast(a, ctypes.c_void_p))
+                           for c, a in zip(claims, arrs)])
+    pts = [x for c in claims for x in list(c["v"]) + list(c["u"])]
+    pt, cl = ctypes.create_string_buffer(32 * (d + n)), ctypes.create_string_buffer(32)
+    _run("claim merge", lib().zk_verify_claim_merge, tr.st, n, d, K, views, _fr(pts), _fr([c["c"] for c in claims]),
+         proof, len(proof), pt, cl)
+    return _ints(pt, d + n), _ints(cl, 1)[0]
+
+
+def verify_matmul(tr: HostTranscript, logs, res: dict) -> dict:
     """A matmul family (rows a3-a6): the verifier draws w, u1, u3 itself (D3a), checks they are the
-    prover's, then verifies the product sumcheck (n_eq = logN) of the claim Y~(w, u1, u3)."""
+    prover's, then verifies the product sumcheck (m = logN + logD2, n_eq = logN, K = 2) of the proof's
+    claim Y~(w, u1, u3).  Returns dict(w, u1, u3, claim, r, finals) — claim and finals from the proof."""
     lN, l1, l2, l3 = logs
     tr.absorb("mm/hdr", b"".join(int(v).to_bytes(4, "little") for v in (lN, l1, l2, l3)))
     w, u1, u3 = tr.challenges("mm/w", lN), tr.challenges("mm/u1", l1), tr.challenges("mm/u3", l3)
     if (w, u1, u3) != (res["w"], res["u1"], res["u3"]):
         raise Rejected("matmul points", -2)
-    return verify_sumcheck(tr, res["proof"], w, res["claim"])
+    proof = res["proof"]
+    r = verify_sumcheck(tr, proof, w, shape=(lN + l2, lN, 2))
+    return dict(w=w, u1=u1, u3=u3, claim=int.from_bytes(proof[12:44], "little"), r=r, finals=_fin(proof, 2))
+
+
+def _family_logs(f):
+    from .api import _mm_logs
+    ta, tb = getattr(f, "trans_a", getattr(f, "transA", False)), getattr(f, "trans_b", getattr(f, "transB", False))
+    return _mm_logs(f.A, f.B, ta, tb), ta, tb
+
+
+def _relu_shape(f):
+    return int(f.Z.size if hasattr(f.Z, "size") and not callable(f.Z.size) else f.Z.numel()).bit_length() - 1, f.Q, f.R
 
 
 def verify_window(seed: bytes, header: bytes, families: list, results: list) -> list:
-    """Replays a window (D3d): W absorbs "fcn/hdr", per family "fcn/fam" and forks "fcn/fork"; each
+    """Replays a D3d window: W absorbs "fcn/hdr", per family "fcn/fam" and forks "fcn/fork"; each
     family's proof is verified on its own forked transcript and must end in the state the prover
     reported; W absorbs "fcn/join" of every family and must end in the reported window state.
     families: the window's family records (shapes only are read); results: fcn.prove_window's output.
-    Returns per family the claims left for the commitments: {name, point, finals}."""
-    from .api import _mm_logs
+    Returns per family every claim it leaves open (the D3d window binds no claim to another family's):
+    matmul: the claim Y~(w, u1, u3) with (w, u1, u3), the point r and the finals A~, B~ there; ReLU: the
+    four claims with their points, the final point and the aux finals (+ the aux merge)."""
     W = HostTranscript(seed=seed)
     W.absorb("fcn/hdr", header)
     kids = []
@@ -141,16 +199,17 @@ def verify_window(seed: bytes, header: bytes, families: list, results: list) -> 
     out = []
     for f, T, res in zip(families, kids, results):
         if hasattr(f, "A"):   # a matmul family (device record or host synth.fcn record: shapes only)
-            ta, tb = getattr(f, "trans_a", getattr(f, "transA", False)), getattr(f, "trans_b", getattr(f, "transB", False))
-            r = verify_matmul(T, _mm_logs(f.A, f.B, ta, tb), res)
-            out.append(dict(name=f.name, point=r, finals=res["finals"]))
+            logs, _, _ = _family_logs(f)
+            v = verify_matmul(T, logs, res)
+            out.append(dict(name=f.name, w=v["w"], u1=v["u1"], u3=v["u3"], claim=v["claim"], point=v["r"],
+                            finals=v["finals"]))
         else:
-            logD = int.from_bytes(res["proof"][:4], "little")
-            r = verify_relu(T, res["proof"])
-            item = dict(name=f.name, point=r, finals=res["finals"])
+            shape = _relu_shape(f)
+            v = verify_relu(T, res["proof"], shape)
+            item = dict(name=f.name, points=v["points"], claims=v["claims"], point=v["point"], finals=v["finals"])
             if "merge" in res:
-                item["merge_point"] = verify_relu_merge(T, logD, f.Q, f.R, r, res["finals"], res["merge"]["proof"])
-                item["merge_finals"] = res["merge"]["finals"]
+                mg = verify_relu_merge(T, shape[0], f.Q, f.R, v["point"], v["finals"], res["merge"]["proof"])
+                item["merge_point"], item["merge_claim"] = mg["point"], mg["claim"]
             out.append(item)
         if T.state() != res["state"]:
             raise Rejected(f"family {f.name} transcript state", -3)
@@ -159,3 +218,98 @@ def verify_window(seed: bytes, header: bytes, families: list, results: list) -> 
     if W.state() != results[-1]["window_state"]:
         raise Rejected("window transcript state", -3)
     return out
+
+
+def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: list, res: dict) -> dict:
+    """Replays a claim-chained window (Protocol 1 lines 7-8, D25; chain.prove_window_chained's
+    output `res`).  families: records with shapes and refs (synth.fcn after plan_window, or
+    chain.ChainedFamily); tensors: the plan's tensor families (name, slots/pad, rows, cols, relu).
+    Every matmul family is verified on its fork; the claims it leaves are routed by the plan to their
+    tensor families; every tensor family with more than one claim (or one on a partial view) must carry a
+    verified claim merge of exactly those claims; every ReLU family is verified at the merged points of
+    its Z, A, G_A, G_Z stacks and its four claims must EQUAL the merged claims (nothing unbound); its aux
+    merge gives the aux claim.  Returns {tensor family: (point, value)} for every committed stack and
+    {"aux:<ReLU>": (point over (j, i, s), value)} — exactly the claims left for the commitments."""
+    from .plan import RELU_ROLES, is_whole, matmul_claim_pieces
+    W = HostTranscript(seed=seed)
+    W.absorb("fcn/chdr", header)
+    mms = [f for f in families if getattr(f, "A", None) is not None]
+    relus = [f for f in families if getattr(f, "A", None) is None]
+
+    def refs(f):
+        return {k: (v.tensor, list(v.map)) if hasattr(v, "tensor") else (v[0], list(v[1])) for k, v in f.refs.items()}
+
+    def pad_of(t):
+        return list(t.pad) if hasattr(t, "pad") else [s is None for s in t.slots]
+
+    kids = []
+    for f in mms:
+        W.absorb("fcn/fam", f.name.encode())
+        kids.append(W.fork("fcn/fork"))
+    claims = {t.name: [] for t in tensors}
+    for f, T in zip(mms, kids):
+        r = res["matmul"][f.name]
+        logs, ta, tb = _family_logs(f)
+        v = verify_matmul(T, logs, r)
+        if T.state() != r["state"]:
+            raise Rejected(f"family {f.name} transcript state", -3)
+        lN = logs[0]
+        val = dict(w=v["w"], u1=v["u1"], u3=v["u3"], claim=[v["claim"]], fA=[v["finals"][0]], fB=[v["finals"][1]],
+                   rn=v["r"][:lN], rk=v["r"][lN:])
+        rf = refs(f)
+        for role, vp, up, cp in matmul_claim_pieces(ta, tb):
+            tname, mp = rf[role]
+            claims[tname].append(dict(map=mp, v=[x for p in vp for x in val[p]], u=[x for p in up for x in val[p]],
+                                      c=val[cp][0]))
+    for T in kids:
+        W.absorb("fcn/join", T.state())
+    opened = {}
+    merged = []
+    for t in tensors:
+        cl = claims[t.name]
+        if not cl:
+            continue
+        if is_whole(pad_of(t), [c["map"] for c in cl]):
+            opened[t.name] = (cl[0]["v"] + cl[0]["u"], cl[0]["c"])
+        else:
+            merged.append(t)
+    if set(res["merges"]) != {t.name for t in merged}:
+        raise Rejected("claim merges do not match the window plan", -4)
+    kids2 = []
+    for t in merged:
+        W.absorb("fcn/tfam", t.name.encode())
+        kids2.append(W.fork("fcn/fork"))
+    for t, T in zip(merged, kids2):
+        n = len(pad_of(t)).bit_length() - 1
+        d = (t.rows * t.cols).bit_length() - 1
+        mr = res["merges"][t.name]
+        opened[t.name] = verify_claim_merge(T, n, d, claims[t.name], mr["proof"])
+        if T.state() != mr["state"]:
+            raise Rejected(f"claim merge {t.name} transcript state", -3)
+    for T in kids2:
+        W.absorb("fcn/join", T.state())
+    kids3 = []
+    for f in relus:
+        W.absorb("fcn/fam", f.name.encode())
+        kids3.append(W.fork("fcn/fork"))
+    for f, T in zip(relus, kids3):
+        r = res["relu"][f.name]
+        names = [f.tensors[k] for k in RELU_ROLES]
+        if any(nm not in opened for nm in names):
+            raise Rejected(f"{f.name}: a ReLU-bound stack without a claim", -4)
+        shape = _relu_shape(f)
+        v = verify_relu(T, r["proof"], shape, points=[opened[nm][0] for nm in names])
+        if v["claims"] != [opened[nm][1] for nm in names]:
+            raise Rejected(f"{f.name}: zkReLU claims differ from the merged claims", -1)
+        mg = verify_relu_merge(T, shape[0], f.Q, f.R, v["point"], v["finals"], r["merge"]["proof"])
+        if T.state() != r["state"]:
+            raise Rejected(f"family {f.name} transcript state", -3)
+        for nm in names:            # bound through zkReLU by the aux commitment (P:L274): not opened
+            del opened[nm]
+        logB = max(0, (f.Q + f.R - 1).bit_length())
+        opened["aux:" + f.name] = (mg["point"][:logB] + v["point"][logB:] + mg["point"][logB:], mg["claim"])
+    for T in kids3:
+        W.absorb("fcn/join", T.state())
+    if W.state() != res["window_state"]:
+        raise Rejected("window transcript state", -3)
+    return opened

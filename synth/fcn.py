@@ -162,6 +162,8 @@ class MatmulFamily:
     transA: bool
     transB: bool
     n_real: int
+    insts: list = field(default_factory=list)   # (step, layer) per stack slot
+    refs: dict = field(default_factory=dict)    # plan_window: role "A" / "B" / "Y" -> TensorRef
 
     @property
     def logs(self):
@@ -181,6 +183,8 @@ class ReluFamily:
     Q: int
     R: int
     n_real: int
+    insts: list = field(default_factory=list)
+    tensors: dict = field(default_factory=dict)  # plan_window: "Z" / "A" / "GA" / "GZ" -> tensor family name
 
 
 def assemble_families(shape: FcnShape, trace):
@@ -214,34 +218,36 @@ def assemble_families(shape: FcnShape, trace):
         for i, (s, l) in enumerate(insts):
             Z[i * per:(i + 1) * per] = trace[s].Z[l].reshape(-1)
             G[i * per:(i + 1) * per] = trace[s].GA[l].reshape(-1)
-        fam.append(ReluFamily(f"ReLU[{','.join(map(str, ls))}]", Z, G, Q_BITS, R_BITS, len(insts)))
-    # forward: Z^(l) = A^(l-1) W^(l)
-    for key, ls in group("F", range(1, L + 1), lambda l: (shape.dims[l - 1], shape.dims[l])):
+        fam.append(ReluFamily(f"ReLU[{','.join(map(str, ls))}]", Z, G, Q_BITS, R_BITS, len(insts), insts))
+    # forward: Z^(l) = A^(l-1) W^(l).  The key also separates the first layer (its input is the data X)
+    # and the top layer (its output is not ReLU'd), so every operand stack of a family is a view of ONE
+    # tensor family (plan_window)
+    for key, ls in group("F", range(1, L + 1), lambda l: (shape.dims[l - 1], shape.dims[l], l == 1, l == L)):
         insts = [(s, l) for s in range(shape.steps) for l in ls]
         N = _next_pow2(len(insts))
         fam.append(MatmulFamily(
             f"F[{','.join(map(str, ls))}]",
             stk("A", [(s, l - 1) for s, l in insts], N),
             stk("W", [(s, l) for s, l in insts], N),
-            stk("Z", [(s, l) for s, l in insts], N), False, False, len(insts)))
+            stk("Z", [(s, l) for s, l in insts], N), False, False, len(insts), insts))
     # input gradients: G_A^(l) = G_Z^(l+1) W^(l+1)^T
-    for key, ls in group("GA", range(1, L), lambda l: (shape.dims[l + 1], shape.dims[l])):
+    for key, ls in group("GA", range(1, L), lambda l: (shape.dims[l + 1], shape.dims[l], l + 1 == L)):
         insts = [(s, l) for s in range(shape.steps) for l in ls]
         N = _next_pow2(len(insts))
         fam.append(MatmulFamily(
             f"GA[{','.join(map(str, ls))}]",
             stk("GZ", [(s, l + 1) for s, l in insts], N),
             stk("W", [(s, l + 1) for s, l in insts], N),
-            stk("GA", [(s, l) for s, l in insts], N), False, True, len(insts)))
+            stk("GA", [(s, l) for s, l in insts], N), False, True, len(insts), insts))
     # weight gradients: G_W^(l) = G_Z^(l)^T A^(l-1)
-    for key, ls in group("GW", range(1, L + 1), lambda l: (shape.dims[l], shape.dims[l - 1])):
+    for key, ls in group("GW", range(1, L + 1), lambda l: (shape.dims[l], shape.dims[l - 1], l == 1, l == L)):
         insts = [(s, l) for s in range(shape.steps) for l in ls]
         N = _next_pow2(len(insts))
         fam.append(MatmulFamily(
             f"GW[{','.join(map(str, ls))}]",
             stk("GZ", [(s, l) for s, l in insts], N),
             stk("A", [(s, l - 1) for s, l in insts], N),
-            stk("GW", [(s, l) for s, l in insts], N), True, False, len(insts)))
+            stk("GW", [(s, l) for s, l in insts], N), True, False, len(insts), insts))
     return fam
 
 
@@ -249,3 +255,146 @@ def fcn_header(shape: FcnShape) -> bytes:
     """Bytes absorbed under tag "fcn/hdr" before the first family (D3d)."""
     words = [len(shape.dims) - 1, shape.batch, shape.steps] + list(shape.dims)
     return b"".join(int(w).to_bytes(4, "little") for w in words)
+
+
+# ---------------------------------------------------------------- tensor families (Protocol 1, P:L287)
+@dataclass
+class TensorFamily:
+    """A stack S_i of same-kind, same-shape tensors of the window (Protocol 1 line 4): slot j holds
+    the tensor of (step, layer) slots[j] (None: an all-zero slot), each stored [rows][cols] as the trace
+    holds it.  relu: the ReLU family whose aux binds the tensor (Z, A, G_A, G_Z: P:L274) — its values are
+    then formed from that family's Z / G_A words — else None (a committed tensor, array = its stack)."""
+    name: str
+    kind: str
+    slots: list
+    rows: int
+    cols: int
+    relu: str | None = None
+    array: np.ndarray | None = None
+
+
+@dataclass
+class TensorRef:
+    """A family operand as a view of a tensor family: family slot n holds tensor slot map[n] (-1: zero)."""
+    tensor: str
+    map: list
+
+
+# (field, layer) -> tensor-family kind
+def _kind(field_: str, l: int, L: int) -> str:
+    if field_ == "A":
+        return "X" if l == 0 else "A"
+    if field_ in ("Z", "GZ"):
+        return field_ + ("out" if l == L else "")
+    return field_                      # GA (hidden only), W, GW
+
+
+def plan_window(shape: FcnShape, trace, families: list) -> list:
+    """Tensor families of a window and the views the operation families take of them (input structure
+    only: which stored tensor each stack slot is).  Sets f.refs (matmul families: roles "A", "B", "Y")
+    and f.tensors (ReLU families) and returns the tensor families in a fixed order: X, then per ReLU
+    family its Z, A, G_A, G_Z, then Zout, GZout, W and GW groups (in family order)."""
+    L = len(shape.dims) - 1
+    relus = [f for f in families if not hasattr(f, "A")]
+    mms = [f for f in families if hasattr(f, "A")]
+    tf = {}
+    order = []
+
+    def add(name, kind, slots, rows, cols, relu=None, array=None):
+        if name not in tf:
+            tf[name] = TensorFamily(name, kind, slots, rows, cols, relu, array)
+            order.append(name)
+        return tf[name]
+
+    def stack(field_, slots, rows, cols):
+        out = np.zeros((len(slots), rows, cols), dtype=np.int32)
+        for j, sl in enumerate(slots):
+            if sl is not None:
+                out[j] = getattr(trace[sl[0]], field_)[sl[1]]
+        return out
+
+    def pad(slots):
+        return slots + [None] * (_next_pow2(len(slots)) - len(slots))
+
+    def same(slots, f, role):    # the family's own operand stack when it holds exactly these slots
+        if f is None or len(slots) != getattr(f, role).shape[0]:
+            return None
+        want = [None] * len(slots)
+        for j, (s, l) in enumerate(f.insts):
+            want[j] = {"F": {"A": (s, l - 1), "B": (s, l), "Y": (s, l)},
+                       "GA": {"A": (s, l + 1), "B": (s, l + 1), "Y": (s, l)},
+                       "GW": {"A": (s, l), "B": (s, l - 1), "Y": (s, l)}}[f.name.split("[")[0]][role]
+        return getattr(f, role) if want == slots else None
+
+    def first(pred):
+        return next((f for f in mms if pred(f)), None)
+
+    B = shape.batch
+    xs = pad([(s, 0) for s in range(shape.steps)])
+    f1 = first(lambda f: f.name.startswith("F[") and min(l for _, l in f.insts) == 1)
+    xa = same(xs, f1, "A")
+    add("X", "X", xs, B, shape.dims[0], array=xa if xa is not None else stack("A", xs, B, shape.dims[0]))
+    home = {}                     # (kind, layer) -> tensor family name
+    for f in relus:
+        lay = sorted({l for _, l in f.insts})
+        tag = ",".join(map(str, lay))
+        slots = pad(list(f.insts))
+        w = shape.dims[lay[0]]
+        f.tensors = {}
+        for k in ("Z", "A", "GA", "GZ"):
+            nm = f"{k}[{tag}]"
+            add(nm, k, slots, B, w, relu=f.name)
+            f.tensors[k] = nm
+            for l in lay:
+                home[(k, l)] = nm
+    zs = pad([(s, L) for s in range(shape.steps)])
+    fL = first(lambda f: f.name.startswith("F[") and max(l for _, l in f.insts) == L)
+    gL = first(lambda f: f.name.startswith("GA[") and max(l for _, l in f.insts) == L - 1)
+    za, ga = same(zs, fL, "Y"), same(zs, gL, "A")
+    add("Zout", "Zout", zs, B, shape.dims[L], array=za if za is not None else stack("Z", zs, B, shape.dims[L]))
+    add("GZout", "GZout", zs, B, shape.dims[L], array=ga if ga is not None else stack("GZ", zs, B, shape.dims[L]))
+    for f in mms:
+        if f.name.startswith("F["):
+            ls = sorted({l for _, l in f.insts})
+            nm = f"W[{','.join(map(str, ls))}]"
+            sl = pad(list(f.insts))
+            a = same(sl, f, "B")
+            add(nm, "W", sl, shape.dims[ls[0] - 1], shape.dims[ls[0]],
+                array=a if a is not None else stack("W", sl, shape.dims[ls[0] - 1], shape.dims[ls[0]]))
+            for l in ls:
+                home[("W", l)] = nm
+    for f in mms:
+        if f.name.startswith("GW["):
+            ls = sorted({l for _, l in f.insts})
+            nm = f"GW[{','.join(map(str, ls))}]"
+            sl = pad(list(f.insts))
+            a = same(sl, f, "Y")
+            add(nm, "GW", sl, shape.dims[ls[0]], shape.dims[ls[0] - 1],
+                array=a if a is not None else stack("GW", sl, shape.dims[ls[0]], shape.dims[ls[0] - 1]))
+            for l in ls:
+                home[("GW", l)] = nm
+    home[("X", 0)] = "X"
+    home[("Zout", L)] = "Zout"
+    home[("GZout", L)] = "GZout"
+
+    def ref(keys, N):
+        names = {home[(_kind(fl, l, L), l)] for fl, s, l in keys}
+        assert len(names) == 1, f"a family operand spans several tensor families: {names}"
+        nm = names.pop()
+        where = {sl: j for j, sl in enumerate(tf[nm].slots) if sl is not None}
+        mp = [where[(s, l)] for fl, s, l in keys] + [-1] * (N - len(keys))
+        return TensorRef(nm, mp)
+
+    for f in mms:
+        N = f.A.shape[0]
+        if f.name.startswith("F["):
+            keys = dict(A=[("A", s, l - 1) for s, l in f.insts], B=[("W", s, l) for s, l in f.insts],
+                        Y=[("Z", s, l) for s, l in f.insts])
+        elif f.name.startswith("GA["):
+            keys = dict(A=[("GZ", s, l + 1) for s, l in f.insts], B=[("W", s, l + 1) for s, l in f.insts],
+                        Y=[("GA", s, l) for s, l in f.insts])
+        else:
+            keys = dict(A=[("GZ", s, l) for s, l in f.insts], B=[("A", s, l - 1) for s, l in f.insts],
+                        Y=[("GW", s, l) for s, l in f.insts])
+        f.refs = {role: ref(k, N) for role, k in keys.items()}
+    return [tf[n] for n in order]

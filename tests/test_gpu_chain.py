@@ -1,0 +1,163 @@
+"""GPU parity of the claim-chained window (Protocol 1 lines 7-8; DESIGN.md
+D25): chain.prove_window_chained against the oracle's drivers.fcn_prove_chained, bit-exact (D18), and
+the library's host verifier (verify.verify_window_chained) on the GPU's bytes, with every opened claim
+checked against the brute-force MLE of its tensor."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from synth.prng import DATA_SEED, fs_seed
+
+pytestmark = pytest.mark.gpu
+P = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2307_16273_b200 import build
+    build.build(verbose=False)
+    from paper_2307_16273_b200 import api
+    return api.Context(0)
+
+
+@pytest.fixture(scope="module")
+def O():
+    import oracle
+    oracle.build()
+    oracle.set_threads(len(os.sched_getaffinity(0)))
+    return oracle
+
+
+def _compare(g, o, fams):
+    for f in fams:
+        if hasattr(f, "A"):
+            a, b = g["matmul"][f.name], o["matmul"][f.name]
+            assert (a["w"], a["u1"], a["u3"], a["claim"]) == (b["w"], b["u1"], b["u3"], b["claim"]), f.name
+            assert a["msgs"] == b["msgs"] and a["finals"] == b["finals"] and a["state"] == b["state"], f.name
+    assert set(g["merges"]) == set(o["merges"])
+    for name, b in o["merges"].items():
+        a = g["merges"][name]
+        assert a["A"]["msgs"] == b["A"]["msgs"] and a["A"]["finals"] == b["A"]["finals"], name
+        assert a["B"]["msgs"] == b["B"]["msgs"] and a["B"]["finals"] == b["B"]["finals"], name
+        assert a["point"] == b["point"] and a["claim"] == b["claim"] and a["state"] == b["state"], name
+
+
+def _run(ctx, O, shape, seed_name, streams, x_bits=11, w_bits=12, y_bits=10, full_oracle=True):
+    from paper_2307_16273_b200 import api, chain, verify
+    from oracle import drivers
+    from synth import fcn
+    trace = fcn.generate_trace(shape, seed=DATA_SEED, x_bits=x_bits, w_bits=w_bits, y_bits=y_bits)
+    fams = fcn.assemble_families(shape, trace)
+    tensors = fcn.plan_window(shape, trace, fams)
+    dfams, dts = chain.upload_plan(fams, tensors)
+    relu_ctx = api.Context(0, torch.cuda.Stream()) if streams else None
+    mm = [api.Context(0, torch.cuda.Stream()) for _ in range(streams)]
+    g = chain.prove_window_chained(ctx, fs_seed(seed_name), fcn.fcn_header(shape), dfams, dts, relu_ctx=relu_ctx,
+                                   mm_ctxs=mm)
+    opened = verify.verify_window_chained(fs_seed(seed_name), fcn.fcn_header(shape), fams, tensors, g)
+    return fams, tensors, g, opened
+
+
+def test_chained_window_tiny_vs_oracle(ctx, O):
+    """A tiny window (2 steps, 3 layers): every family, merge and the chained zkReLU bit-exact against
+    the oracle; the opened claims equal the oracle's and are true on the tensors."""
+    from oracle import drivers
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4)
+    for streams in (0, 2):
+        fams, tensors, g, opened = _run(ctx, O, shape, "chain-tiny", streams, x_bits=4, w_bits=4, y_bits=3)
+        o = drivers.fcn_prove_chained(shape, fams, tensors, "chain-tiny")
+        _compare(g, o, fams)
+        for f in fams:
+            if not hasattr(f, "A"):
+                a, b = g["relu"][f.name], o["relu"][f.name]
+                assert a["claims"] == b["claims"] and a["msgs"] == b["msgs"] and a["finals"] == b["finals"]
+                assert a["merge"]["msgs"] == b["merge"]["msgs"] and a["state"] == b["state"]
+        assert g["window_state"] == o["window_state"]
+        assert opened == o["opened"]
+
+
+@pytest.mark.parametrize("layers,width", [(4, 64), (3, 256)])
+def test_chained_window_mid_vs_oracle(ctx, O, layers, width):
+    """Wider windows (several tiles per kernel, padded stacks: 3 ReLU layers x 2 steps = 6 -> 8 slots)."""
+    from oracle import drivers
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=layers, width=width, batch=16, din=width * 2, dout=16)
+    fams, tensors, g, opened = _run(ctx, O, shape, f"chain-{layers}-{width}", 2)
+    o = drivers.fcn_prove_chained(shape, fams, tensors, f"chain-{layers}-{width}")
+    _compare(g, o, fams)
+    for f in fams:
+        if not hasattr(f, "A"):
+            assert g["relu"][f.name]["msgs"] == o["relu"][f.name]["msgs"]
+    assert g["window_state"] == o["window_state"] and opened == o["opened"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_chained_window_full_size(ctx, O, cfg):
+    """C3 and C4 (the bench workload) chained, in the bench's stream configuration: every matmul family
+    and every claim merge bit-exact against the oracle; the chained zkReLU accepted by the oracle's
+    verifier at the merged points (claims = brute-force MLEs there); the library's host verifier accepts
+    the window; every opened committed claim equals the brute-force MLE of its stack."""
+    from oracle import drivers
+    from synth import fcn
+    shape = fcn.C4_SHAPE if cfg == "C4" else fcn.C3_SHAPE
+    fams, tensors, g, opened = _run(ctx, O, shape, f"{cfg}-chained", 2)
+    # the oracle: stage 1 and 2 in full (drivers' functions with the dense zkReLU left out), then the
+    # zkReLU through the oracle's verifier at the merged points
+    import oracle as Ol
+    W = Ol.Transcript(fs_seed(f"{cfg}-chained"))
+    W.absorb("fcn/chdr", fcn.fcn_header(shape))
+    mms = [f for f in fams if hasattr(f, "A")]
+    kids = []
+    for f in mms:
+        W.absorb("fcn/fam", f.name.encode())
+        kids.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    om = {}
+    for f, T in zip(mms, kids):
+        r = Ol.matmul_prove(T, f.A, f.B, f.transA, f.transB)
+        r["state"] = T.state()
+        om[f.name] = r
+    _compare(dict(matmul=g["matmul"], merges={}), dict(matmul=om, merges={}), fams)
+    for T in kids:
+        W.absorb("fcn/join", T.state())
+    claims = {t.name: [] for t in tensors}
+    for f in mms:
+        for role, ref, v, u, c in drivers._matmul_family_claims(f, om[f.name]):
+            claims[ref.tensor].append(dict(map=list(ref.map), u=list(u), v=list(v), c=c))
+    merged = [t for t in tensors if claims[t.name] and not drivers._is_whole(t, claims[t.name])]
+    assert sorted(t.name for t in merged) == sorted(g["merges"])
+    mk = []
+    for t in merged:
+        W.absorb("fcn/tfam", t.name.encode())
+        mk.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    for t, T in zip(merged, mk):
+        r = Ol.claim_merge_prove(T, drivers._tensor_values(t, fams), claims[t.name])
+        a = g["merges"][t.name]
+        assert a["A"]["msgs"] == r["A"]["msgs"] and a["B"]["msgs"] == r["B"]["msgs"], t.name
+        assert a["point"] == r["point"] and a["claim"] == r["claim"] and a["state"] == T.state(), t.name
+    for T in mk:
+        W.absorb("fcn/join", T.state())
+    for f in fams:
+        if hasattr(f, "A"):
+            continue
+        W.absorb("fcn/fam", f.name.encode())
+        T = Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little"))
+        gr = g["relu"][f.name]
+        pts = [g["merges"][f.tensors[k]]["point"] for k in ("Z", "A", "GA", "GZ")]
+        assert Ol.relu_verify(T, f.Z, f.GA, f.Q, f.R, gr["claims"], gr["msgs"], gr["finals"], points=pts) == 0
+        assert gr["claims"] == [g["merges"][f.tensors[k]]["claim"] for k in ("Z", "A", "GA", "GZ")]
+        rho = T.challenges("relu/merge", 1)[0]
+        f0, f1, f2 = gr["finals"]
+        assert gr["merge"]["claim"] == (f0 + rho * f1 + rho * rho * f2) % P
+        assert Ol.sumcheck_verify(T, len(gr["merge"]["r"]), 0, 2, [], gr["merge"]["claim"], gr["merge"]["msgs"],
+                                  gr["merge"]["finals"]) == 0
+        assert gr["state"] == T.state()
+        W.absorb("fcn/join", T.state())
+    assert g["window_state"] == W.state()
+    for t in tensors:
+        if t.relu is None and t.name in opened:
+            pt, val = opened[t.name]
+            assert val == Ol.mle_i32(np.ascontiguousarray(t.array).reshape(-1), pt), t.name

@@ -572,7 +572,7 @@ def test_c5_large_properties(ctx, O, m):
     H = verify.HostTranscript(seed=fs_seed(f"C5-m{m}"))
     H.absorb("c5/hdr", m.to_bytes(4, "little"))
     assert H.challenges("c5/w", m) == w
-    assert verify.verify_sumcheck(H, g["proof"], w) == g["r"] and H.state() == tr.state()
+    assert verify.verify_sumcheck(H, g["proof"], w, shape=(m, m, 2)) == g["r"] and H.state() == tr.state()
 
 
 @pytest.mark.parametrize("m", [22])
@@ -754,6 +754,6 @@ def test_readme_flow_host_verified(ctx, O):
     relu = api.relu_prove(ctx, tr, dev(Z), dev(GA), 16, 16)
     H = verify.HostTranscript(seed=b"\0" * 32)
     logs = (logN, len(red["u1"]), logD2, len(red["u3"]))
-    assert verify.verify_matmul(H, logs, dict(red, proof=proof["proof"])) == proof["r"]
-    assert verify.verify_relu(H, relu["proof"]) == relu["point"]
+    assert verify.verify_matmul(H, logs, dict(red, proof=proof["proof"]))["r"] == proof["r"]
+    assert verify.verify_relu(H, relu["proof"], (12, 16, 16))["point"] == relu["point"]
     assert H.state() == tr.state()

@@ -63,28 +63,38 @@ def test_sumcheck_verifier_on_oracle_proofs(V, oracle_lib, m, n_eq, K):
     res = O.sumcheck_prove(T, m, n_eq, tabs, w)
     proof = sc_proof(m, n_eq, K, res)
     H = V.HostTranscript(seed=seed)
-    assert V.verify_sumcheck(H, proof, w) == res["r"]
+    assert V.verify_sumcheck(H, proof, w, shape=(m, n_eq, K)) == res["r"]
     assert H.state() == T.state()
-    assert V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, claim=res["claim"]) == res["r"]
+    assert V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, claim=res["claim"], shape=(m, n_eq, K)) == res["r"]
+    assert V.sumcheck_finals(proof) == res["finals"]
     # finals are the MLEs of the tables at r (what a commitment opening would close)
     assert res["finals"] == [O.mle_fr(t, res["r"]) for t in tabs]
     with pytest.raises(V.Rejected) as e:   # another claim
-        V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, claim=(res["claim"] + 1) % P)
+        V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, claim=(res["claim"] + 1) % P, shape=(m, n_eq, K))
     assert e.value.where == -1
     for t in range(m):                       # one evaluation of round t changed: round t fails
         bad = bytearray(proof)
         o = 44 + 32 * (t * (K + 1))
         bad[o:o + 32] = ((int.from_bytes(bad[o:o + 32], "little") + 1) % P).to_bytes(32, "little")
         with pytest.raises(V.Rejected) as e:
-            V.verify_sumcheck(V.HostTranscript(seed=seed), bytes(bad), w)
+            V.verify_sumcheck(V.HostTranscript(seed=seed), bytes(bad), w, shape=(m, n_eq, K))
         assert e.value.where == t + 1
     bad = bytearray(proof)                   # a final changed: the final identity fails
     bad[-1] ^= 0x01
     with pytest.raises(V.Rejected) as e:
-        V.verify_sumcheck(V.HostTranscript(seed=seed), bytes(bad), w)
+        V.verify_sumcheck(V.HostTranscript(seed=seed), bytes(bad), w, shape=(m, n_eq, K))
     assert e.value.where == -100
     with pytest.raises(ValueError):          # malformed
-        V.verify_sumcheck(V.HostTranscript(seed=seed), proof[:-1], w)
+        V.verify_sumcheck(V.HostTranscript(seed=seed), proof[:-1], w, shape=(m, n_eq, K))
+    # the statement's shape is the verifier's: another header is rejected before anything is read
+    # (a proof for (m=1, n_eq=0, K=1) passed for any family)
+    with pytest.raises(V.Rejected) as e:
+        V.verify_sumcheck(V.HostTranscript(seed=seed), proof, w, shape=(m + 1, n_eq, K))
+    assert e.value.where == -2
+    fake = (u32s(1, 0, 1) if (m, n_eq, K) != (1, 0, 1) else u32s(2, 0, 1)) + frs([5, 2, 3, 4])
+    with pytest.raises(V.Rejected) as e:
+        V.verify_sumcheck(V.HostTranscript(seed=seed), fake, w, shape=(m, n_eq, K))
+    assert e.value.where == -2
 
 
 def test_hadamard_zero_verifier(V, oracle_lib):
@@ -103,11 +113,11 @@ def test_hadamard_zero_verifier(V, oracle_lib):
         proof = u32s(m) + frs([v for row in res["msgs"] for v in row]) + frs(res["finals"])
         H = V.HostTranscript(seed=seed)
         if bad_at is None:
-            out = V.verify_hadamard_zero(H, proof)
+            out = V.verify_hadamard_zero(H, proof, m)
             assert out["w"] == res["w"] and out["r"] == res["r"] and H.state() == T.state()
         else:
             with pytest.raises(V.Rejected) as e:
-                V.verify_hadamard_zero(H, proof)
+                V.verify_hadamard_zero(H, proof, m)
             assert e.value.where == 1        # the zero claim breaks in the first round
 
 
@@ -123,9 +133,14 @@ def test_relu_verifier_and_merge(V, oracle_lib, logD, Q, R):
     mg = O.relu_merge(T, Z, GA, Q, R, res["point"], res["finals"])
     proof = relu_proof(logD, Q, R, res)
     H = V.HostTranscript(seed=seed)
-    assert V.verify_relu(H, proof) == res["point"]
+    v = V.verify_relu(H, proof, (logD, Q, R))
+    assert v["point"] == res["point"] and v["claims"] == res["claims"] and v["finals"] == res["finals"]
+    t = O.relu_tables(Z, GA, Q, R)          # the returned points are the ones the claims are at
+    assert v["claims"] == [O.mle_i32(Z, v["points"][0]), O.mle_i32(t["A"], v["points"][1]),
+                           O.mle_i32(GA, v["points"][2]), O.mle_i32(t["GZ"], v["points"][3])]
     mproof = u32s(len(mg["r"]), 0, 2) + frs([mg["claim"]]) + frs([v for row in mg["msgs"] for v in row]) + frs(mg["finals"])
-    assert V.verify_relu_merge(H, logD, Q, R, res["point"], res["finals"], mproof) == mg["r"]
+    vm = V.verify_relu_merge(H, logD, Q, R, res["point"], res["finals"], mproof)
+    assert vm["point"] == mg["r"] and vm["claim"] == mg["finals"][0]
     assert H.state() == T.state()
     m = len(res["point"])
     for t in (0, m // 2, m - 1):
@@ -133,20 +148,25 @@ def test_relu_verifier_and_merge(V, oracle_lib, logD, Q, R):
         o = 12 + 128 + 128 * t + 32
         bad[o:o + 32] = ((int.from_bytes(bad[o:o + 32], "little") + 7) % P).to_bytes(32, "little")
         with pytest.raises(V.Rejected) as e:
-            V.verify_relu(V.HostTranscript(seed=seed), bytes(bad))
+            V.verify_relu(V.HostTranscript(seed=seed), bytes(bad), (logD, Q, R))
         assert e.value.where == t + 1
     bad = bytearray(proof)                   # sigma final changed: the six-statement identity fails
     bad[-32] ^= 0x01
     with pytest.raises(V.Rejected) as e:
-        V.verify_relu(V.HostTranscript(seed=seed), bytes(bad))
+        V.verify_relu(V.HostTranscript(seed=seed), bytes(bad), (logD, Q, R))
     assert e.value.where == -100
     bad = bytearray(proof)                   # a claim changed: round 1 fails
     bad[12] ^= 0x01
     with pytest.raises(V.Rejected) as e:
-        V.verify_relu(V.HostTranscript(seed=seed), bytes(bad))
+        V.verify_relu(V.HostTranscript(seed=seed), bytes(bad), (logD, Q, R))
     assert e.value.where == 1
+    with pytest.raises(V.Rejected) as e:     # another statement shape
+        V.verify_relu(V.HostTranscript(seed=seed), proof, (logD + 1, Q, R))
+    assert e.value.where == -2
+    with pytest.raises(ValueError):          # Q + R overflow guard
+        V.verify_relu(V.HostTranscript(seed=seed), proof, (logD, 0xFFFFFFFF, 2))
     H2 = V.HostTranscript(seed=seed)         # the merge's weight final
-    V.verify_relu(H2, proof)
+    V.verify_relu(H2, proof, (logD, Q, R))
     badm = bytearray(mproof)
     badm[-32] ^= 0x01
     with pytest.raises(V.Rejected) as e:
@@ -178,8 +198,13 @@ def test_window_verifier_on_oracle_window(V, oracle_lib):
         results.append(r)
     out = V.verify_window(fs_seed("vwin"), fcn.fcn_header(shape), fams, results)
     assert [x["name"] for x in out] == [f.name for f in fams]
-    for x, r in zip(out, o):
+    for x, r, f in zip(out, o, fams):
         assert x["point"] == (r["r"] if "r" in r and "point" not in r else r["point"])
+        assert x["finals"] == r["finals"]
+        if hasattr(f, "A"):   # the matmul claim and its point are returned (open claims of the D3d window)
+            assert (x["w"], x["u1"], x["u3"], x["claim"]) == (r["w"], r["u1"], r["u3"], r["claim"])
+        else:
+            assert x["claims"] == r["claims"] and x["merge_claim"] == r["merge"]["finals"][0]
     k = next(i for i, f in enumerate(fams) if hasattr(f, "A"))
     bad = dict(results[k])
     pb = bytearray(bad["proof"])
@@ -207,3 +232,94 @@ def test_loss_grad_verifier(V, oracle_lib):
     with pytest.raises(V.Rejected) as e:
         V.verify_loss_grad(V.HostTranscript(seed=seed), m, bad["claims"])
     assert e.value.where == -100
+
+
+def _chained_results(o, fams, tensors):
+    """The oracle's chained window in the device driver's result layout (proof bytes)."""
+    from paper_2307_16273_b200.api import relu_logB
+    res = dict(matmul={}, merges={}, relu={}, window_state=o["window_state"])
+    for f in fams:
+        if hasattr(f, "A"):
+            r = dict(o["matmul"][f.name])
+            lN, l1, l2, l3 = r["logs"]
+            r["proof"] = sc_proof(lN + l2, lN, 2, r)
+            res["matmul"][f.name] = r
+        else:
+            r = dict(o["relu"][f.name])
+            logD = int(f.Z.size).bit_length() - 1
+            r["proof"] = relu_proof(logD, f.Q, f.R, r)
+            mg = r["merge"]
+            r["merge"] = dict(mg, proof=u32s(len(mg["r"]), 0, 2) + frs([mg["claim"]]) +
+                              frs([v for row in mg["msgs"] for v in row]) + frs(mg["finals"]))
+            res["relu"][f.name] = r
+    for name, mr in o["merges"].items():
+        A, B = mr["A"], mr["B"]
+        cA = sum(rh * c["c"] for rh, c in zip(mr["rho"], mr["claims_in"])) % P
+        proof = (u32s(len(A["r"]), 0, 2) + frs([cA]) + frs([v for row in A["msgs"] for v in row]) + frs(A["finals"]) +
+                 u32s(len(B["r"]), 0, 2) + frs([A["finals"][1]]) + frs([v for row in B["msgs"] for v in row]) +
+                 frs(B["finals"]))
+        res["merges"][name] = dict(mr, proof=proof)
+    return res
+
+
+def _aux_mle(f, pt):
+    """Brute-force MLE of the aux bit tensor aux[s][i][j] (s: Z / G_A words, j: bit, padded to B)."""
+    from oracle import drivers  # noqa: F401
+    import oracle as O
+    QR = f.Q + f.R
+    B = 1 << max(0, (QR - 1).bit_length())
+    bits = []
+    for w in (f.Z, f.GA):
+        for v in np.asarray(w).reshape(-1):
+            x = int(v) & 0xFFFFFFFF
+            bits += [(x >> j) & 1 if j < QR else 0 for j in range(B)]
+    return O.mle_fr(bits, pt)
+
+
+def test_chained_window_verifier_on_oracle_window(V, oracle_lib):
+    """N3 (D25): a tiny claim-chained window proved by the oracle; the host verifier accepts it and
+    returns exactly one claim per committed tensor family plus the aux claim, each TRUE on the tensors
+    (brute-force MLE); the zkReLU claims are bound to the merged claims; tampering anywhere is caught."""
+    from oracle import drivers
+    from synth import fcn
+    O = oracle_lib
+    O.set_threads(1)
+    shape = fcn.tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4)
+    trace = fcn.generate_trace(shape, x_bits=4, w_bits=4, y_bits=3)
+    fams = fcn.assemble_families(shape, trace)
+    tensors = fcn.plan_window(shape, trace, fams)
+    o = drivers.fcn_prove_chained(shape, fams, tensors, "vchain")
+    res = _chained_results(o, fams, tensors)
+    hdr = fcn.fcn_header(shape)
+    opened = V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, res)
+    assert opened == o["opened"]
+    committed = [t for t in tensors if t.relu is None]
+    relus = [f for f in fams if not hasattr(f, "A")]
+    assert sorted(opened) == sorted([t.name for t in committed] + ["aux:" + f.name for f in relus])
+    for t in committed:
+        pt, val = opened[t.name]
+        assert val == O.mle_i32(t.array.reshape(-1), pt), t.name
+    for f in relus:
+        pt, val = opened["aux:" + f.name]
+        assert val == _aux_mle(f, pt)
+    # a zkReLU proof whose claims are not the merged ones (a different Z claim) is rejected
+    bad = dict(res, relu=dict(res["relu"]))
+    f = relus[0]
+    rr = dict(res["relu"][f.name])
+    pb = bytearray(rr["proof"])
+    pb[12] ^= 1
+    rr["proof"] = bytes(pb)
+    bad["relu"][f.name] = rr
+    with pytest.raises(V.Rejected):
+        V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, bad)
+    # a merge proof for other claims, and a missing merge
+    name = next(iter(res["merges"]))
+    bad = dict(res, merges=dict(res["merges"]))
+    mb = bytearray(bad["merges"][name]["proof"])
+    mb[20] ^= 1
+    bad["merges"][name] = dict(bad["merges"][name], proof=bytes(mb))
+    with pytest.raises(V.Rejected):
+        V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, bad)
+    bad = dict(res, merges={k: v for k, v in res["merges"].items() if k != name})
+    with pytest.raises(V.Rejected):
+        V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, bad)
