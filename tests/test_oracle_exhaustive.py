@@ -114,7 +114,7 @@ def _run(m, K, vals, n_eq_mode):
     ntab = len(vals) ** (1 << m)
     nproc = max(1, min(16, os.cpu_count() or 1))
     chunks = [list(range(i, ntab, nproc * 4)) for i in range(nproc * 4)]
-    with mp.get_context("fork").Pool(nproc) as pool:
+    with mp.get_context("spawn").Pool(nproc) as pool:
         out = pool.map(_work, [(m, K, vals, c, n_eq_mode) for c in chunks])
     total = sum(o[0] for o in out)
     bad = [b for o in out for b in o[1]]
