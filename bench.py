@@ -174,8 +174,9 @@ def c4_workload(rank: int):
     t0 = time.time()
     trace = fcn.generate_trace(fcn.C4_SHAPE, seed=DATA_SEED + rank)
     fams = fcn.assemble_families(fcn.C4_SHAPE, trace)
+    tensors = fcn.plan_window(fcn.C4_SHAPE, trace, fams)
     log(f"[bench] rank {rank}: C4 trace + families generated in {time.time() - t0:.1f}s")
-    return fcn.C4_SHAPE, fams
+    return fcn.C4_SHAPE, fams, tensors
 
 
 def family_bytes(fams) -> int:
@@ -238,7 +239,7 @@ def run_ours(args, rank, world, local):
     from synth.prng import fs_seed
 
     build.build(verbose=False)
-    shape, fams = c4_workload(rank)
+    shape, fams, tensors = c4_workload(rank)
     in_bytes = family_bytes(fams)
     dev_fams = dfcn.upload_families(fams, device=f"cuda:{local}")
     torch.cuda.synchronize()
@@ -330,6 +331,35 @@ def run_ours(args, rank, world, local):
             del pend
         n1 = {"ms_per_step": max_over_ranks(e0.elapsed_time(e1), world) / args.steps,
               "what": "the same window with the zkReLU aux-claim merge (one aux claim per ReLU family)"}
+    chained = None
+    if not args.profile_mode and not args.no_chained:
+        # SURVEY 8(f) N3 beside the headline: the claim-chained window (Protocol 1 lines 7-8, DESIGN.md
+        # D25) -- matmul families, the claim merges that leave one claim per tensor family, the chained
+        # zkReLU at the merged points and its aux merge -- timed the same way
+        from paper_2307_16273_b200 import chain
+        cfams, cts = chain.upload_plan(fams, tensors, device=f"cuda:{local}")
+        cseed = fs_seed(f"C4-chained-rank{rank}")
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
+            torch.cuda.synchronize()
+            barrier(world)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            pend = [chain.enqueue_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs)
+                    for _ in range(args.steps)]
+            c1.record(stream)
+            torch.cuda.synchronize()
+            cres = chain.collect_window_chained(pend[-1])
+            del pend
+        cms = max_over_ranks(c0.elapsed_time(c1), world) / args.steps
+        chained = {"ms_per_step": round(cms, 4), "s_per_update": cms / 1000.0 / shape.steps,
+                   "claim_merges": sorted(cres["merges"]), "window_state": cres["window_state"].hex()[:16],
+                   "what": "the claim-chained window: every matmul family, one claim merge per tensor family "
+                           "with several claims, the zkReLU at the merged points + aux merge; ends with one "
+                           "claim per committed tensor family and one on aux"}
+        del cfams, cts
+        torch.cuda.empty_cache()
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
     updates = world * args.steps * shape.steps
@@ -422,6 +452,7 @@ def run_ours(args, rank, world, local):
                         "overlapped with the proofs; proofs back to the host", "windows": e2e_steps},
         "roofline": rf,
         "n1_relu_aux_merge": n1,
+        "n3_chained_window": chained,
         "kernels_ms_per_step": {k: round(t, 4) for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:16]},
         "kernel_launches_per_step": {k: n for k, (n, t) in sorted(per_step.items(), key=lambda kv: -kv[1][1])[:16]},
         "kernel_ms_total_per_step": round(total_kernel_ms, 4),
@@ -441,7 +472,9 @@ def run_ours(args, rank, world, local):
         except Exception as e:   # never lose the headline line to the auxiliary measurement
             out["c5_sharded"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_mode:
-        out["cpu_baseline"] = cpu_baseline(fams, shape, sample_scale=args.cpu_sample)
+        with torch.cuda.stream(stream):
+            gfull = gpu_full_families(ctx, dev_fams, FULL_FAMILIES)
+        out["cpu_baseline"] = cpu_baseline(fams, shape, sample_scale=args.cpu_sample, gpu_full_ms=round(gfull, 4))
     if rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -708,22 +741,72 @@ def oracle_window_sample(fams, shape, frac_inst: int, relu_instances: int):
     return est, "oracle on sub-stacks " + ", ".join(parts) + " (time scaled linearly in the instance count)"
 
 
-def cpu_baseline(fams, shape, sample_scale: int = 16):
+def oracle_full_families(fams, names):
+    """The oracle on complete families (every instance, nothing extrapolated): seconds."""
+    import numpy as np
+    import oracle as O
+    from synth.prng import fs_seed
+    t0 = time.perf_counter()
+    for f in fams:
+        if f.name in names:
+            O.matmul_prove(O.Transcript(fs_seed("C4-oracle-full-" + f.name)), np.ascontiguousarray(f.A),
+                           np.ascontiguousarray(f.B), f.transA, f.transB)
+    return time.perf_counter() - t0
+
+
+def gpu_full_families(ctx, dev_fams, names, reps: int = 5) -> float:
+    """The same complete families on the GPU (zk_matmul_prove, one stream, CUDA events): ms per pass."""
+    import torch
+    from paper_2307_16273_b200 import api
+    from synth.prng import fs_seed
+    sel = [f for f in dev_fams if f.name in names]
+
+    def once():
+        for f in sel:
+            api.matmul_prove(ctx, api.Transcript(ctx, fs_seed("C4-oracle-full-" + f.name)), f.A, f.B, f.trans_a, f.trans_b)
+    once()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    for _ in range(reps):
+        once()
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+FULL_FAMILIES = ("F[9]", "GA[8]")   # two complete families of the C4 window (16 instances each)
+
+
+def cpu_baseline(fams, shape, sample_scale: int = 16, gpu_full_ms: float | None = None):
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     O.set_threads(cores)
     t0 = time.perf_counter()
     est, note = oracle_window_sample(fams, shape, frac_inst=sample_scale, relu_instances=4)
     wall = time.perf_counter() - t0
-    return {"value": est / shape.steps, "unit": UNIT, "cores": O.threads(), "kind": "oracle",
-            "sample": note + f"; sample wall {wall:.1f}s"}
+    full_all = oracle_full_families(fams, FULL_FAMILIES)
+    O.set_threads(1)
+    t1 = time.perf_counter()
+    est1, note1 = oracle_window_sample(fams, shape, frac_inst=4 * sample_scale, relu_instances=1)
+    wall1 = time.perf_counter() - t1
+    full_one = oracle_full_families(fams, FULL_FAMILIES)
+    O.set_threads(cores)
+    return {"value": est / shape.steps, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": note + f"; sample wall {wall:.1f}s",
+            "threads_1": {"value": est1 / shape.steps, "unit": UNIT, "cores": 1,
+                          "sample": note1 + f"; sample wall {wall1:.1f}s"},
+            "unextrapolated": {"families": list(FULL_FAMILIES), "what": "complete families of the window, every "
+                               "instance proved by the oracle, nothing scaled", "s_all_cores": round(full_all, 4),
+                               "s_1_thread": round(full_one, 4), "gpu_ms": gpu_full_ms,
+                               "gpu_note": "the same families through zk_matmul_prove on one stream (CUDA events)"}}
 
 
 def run_reference(args, rank, world, local):
     if rank != 0:
         return
     import oracle as O
-    shape, fams = c4_workload(0)
+    shape, fams, _ = c4_workload(0)
     cores = len(os.sched_getaffinity(0))
     O.set_threads(cores)
     for _ in range(args.warmup):
@@ -759,6 +842,7 @@ def main():
     ap.add_argument("--sweep-BS", type=int, nargs="+", default=[16, 32, 64])
     ap.add_argument("--c5-log", type=int, default=26, help="C5: log2 m of the 2^m hypercube (22..30)")
     ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
+    ap.add_argument("--no-chained", action="store_true", help="C4 line without the chained-window (N3) measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")

@@ -18,6 +18,9 @@ SO = os.path.join(HERE, "libzkdl.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "177"]
+# ZKDL_FR64=0 builds the hot product bodies with the integer CIOS instead of the FP64-pipe product (A/B)
+if os.environ.get("ZKDL_FR64") is not None:
+    FLAGS += [f"-DZKDL_FR64={int(os.environ['ZKDL_FR64'])}"]
 
 
 def _deps():

@@ -216,24 +216,41 @@ __device__ __forceinline__ fr_t fr_mul(const fr_t& a, const fr_t& b) {
 }
 __device__ __forceinline__ fr_t fr_sqr(const fr_t& a) { return fr_mul(a, a); }
 
+}  // namespace zk
+#include "fr64.cuh"
+namespace zk {
+
+// The product of the hot out-of-line bodies below: the FP64-pipe product (fr64.cuh) unless the build
+// selects the integer CIOS (ZKDL_FR64=0); both give identical bits.
+#ifndef ZKDL_FR64
+#define ZKDL_FR64 1
+#endif
+__device__ __forceinline__ fr_t fr_mul_hot(const fr_t& a, const fr_t& b) {
+#if ZKDL_FR64
+    return fr_mul_f64(a, b);
+#else
+    return fr_mul(a, b);
+#endif
+}
+
 // Out-of-line but fully unrolled product for hot loops with many multiplications: one ~560-instruction
 // body shared by every call site keeps the loop inside the instruction cache (the inlined k_relu_iround
 // body was > 100 KB of SASS; ncu stall_no_inst 36%).
-static __device__ __noinline__ fr_t fr_mul_ni(fr_t a, fr_t b) { return fr_mul(a, b); }
+static __device__ __noinline__ fr_t fr_mul_ni(fr_t a, fr_t b) { return fr_mul_hot(a, b); }
 
 // Three independent products in one out-of-line body: the scheduler interleaves the three CIOS
 // chains, so a warp has three-way instruction-level parallelism inside the product (the single
 // product is a dependent chain that leaves the pipes idle at low occupancy).
 struct fr3_t { fr_t x, y, z; };
 static __device__ __noinline__ fr3_t fr_mul3_ni(fr_t a0, fr_t b0, fr_t a1, fr_t b1, fr_t a2, fr_t b2) {
-    return fr3_t{fr_mul(a0, b0), fr_mul(a1, b1), fr_mul(a2, b2)};
+    return fr3_t{fr_mul_hot(a0, b0), fr_mul_hot(a1, b1), fr_mul_hot(a2, b2)};
 }
 
 // Two independent products in one out-of-line body (for the groups with only two products: a wasted
 // third slot of fr_mul3_ni costs a whole product)
 struct fr2p_t { fr_t x, y; };
 static __device__ __noinline__ fr2p_t fr_mul2_ni(fr_t a0, fr_t b0, fr_t a1, fr_t b1) {
-    return fr2p_t{fr_mul(a0, b0), fr_mul(a1, b1)};
+    return fr2p_t{fr_mul_hot(a0, b0), fr_mul_hot(a1, b1)};
 }
 
 // One out-of-line copy for cold code (finalizers, single-CTA round kernels): the inlined product is

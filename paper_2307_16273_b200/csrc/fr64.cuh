@@ -16,7 +16,7 @@
 // Per product: 185 FP64-pipe operations (DFMA/DADD) and ~200 ALU operations (limb extraction, 64-bit
 // column sums), against ~376 fmaheavy slots for the integer CIOS.
 #pragma once
-#include "fr.cuh"
+// included by fr.cuh after fr_t and fr_reduce_once
 
 namespace zk {
 

@@ -6,7 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "../paper_2307_16273_b200/csrc/fr64.cuh"
+#include "../paper_2307_16273_b200/csrc/fr.cuh"
 
 using namespace zk;
 
