@@ -174,9 +174,10 @@ def c4_workload(rank: int):
     t0 = time.time()
     trace = fcn.generate_trace(fcn.C4_SHAPE, seed=DATA_SEED + rank)
     fams = fcn.assemble_families(fcn.C4_SHAPE, trace)
-    tensors = fcn.plan_window(fcn.C4_SHAPE, trace, fams)
+    top = fcn.assemble_top_families(fcn.C4_SHAPE, trace, fams)
+    tensors = fcn.plan_window(fcn.C4_SHAPE, trace, fams, top)
     log(f"[bench] rank {rank}: C4 trace + families generated in {time.time() - t0:.1f}s")
-    return fcn.C4_SHAPE, fams, tensors
+    return fcn.C4_SHAPE, fams, (top, tensors)
 
 
 def family_bytes(fams) -> int:
@@ -337,7 +338,8 @@ def run_ours(args, rank, world, local):
         # D25) -- matmul families, the claim merges that leave one claim per tensor family, the chained
         # zkReLU at the merged points and its aux merge -- timed the same way
         from paper_2307_16273_b200 import chain
-        cfams, cts = chain.upload_plan(fams, tensors, device=f"cuda:{local}")
+        top, ptens = tensors
+        cfams, cts = chain.upload_plan(fams, ptens, device=f"cuda:{local}", top=top)
         cseed = fs_seed(f"C4-chained-rank{rank}")
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -355,9 +357,10 @@ def run_ours(args, rank, world, local):
         cms = max_over_ranks(c0.elapsed_time(c1), world) / args.steps
         chained = {"ms_per_step": round(cms, 4), "s_per_update": cms / 1000.0 / shape.steps,
                    "claim_merges": sorted(cres["merges"]), "window_state": cres["window_state"].hex()[:16],
-                   "what": "the claim-chained window: every matmul family, one claim merge per tensor family "
-                           "with several claims, the zkReLU at the merged points + aux merge; ends with one "
-                           "claim per committed tensor family and one on aux"}
+                   "what": "the claim-chained window (N3) with the top layer (N2): every matmul family and the "
+                           "loss family, one claim merge per tensor family with several claims, the zkReLU at "
+                           "the merged points + aux merge, the top-layer rescale + its aux merge; ends with one "
+                           "claim per committed tensor family and one on each aux"}
         del cfams, cts
         torch.cuda.empty_cache()
     ms_local = ev0.elapsed_time(ev1)

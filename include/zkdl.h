@@ -283,7 +283,8 @@ zk_status zk_relu_prove_chained_dev(zk_ctx* ctx, zk_transcript* tr, const int32_
  *   2^log_rows x 2^log_cols int32 entries, row-major (a point on it: col bits, row bits, slice bits; D2),
  *   read through `source`: 0 = d_X itself, 1 = A = 1{Z >= 0} round(Z / 2^R) formed from d_X = the Z
  *   words, 2 = G_Z = 1{Z >= 0} round(G_A / 2^R) from d_X = Z and d_X2 = G_A (Lemma 1; the
- *   tensors anchored by aux).  views[k] (host): 2^logN slots, map[j] = the slice slot j holds
+ *   tensors anchored by aux), 3 = the bits of d_X (aux(i, j) = bit j of X[i], j < R = the bit
+ *   count, 2^log_cols columns, n = 0: the rescale's aux, D26).  views[k] (host): 2^logN slots, map[j] = the slice slot j holds
  *   (0xffffffff: an all-zero slot; injective).  d_pts (device, canonical): per claim, in order, its inner
  *   point v_k (log_rows + log_cols elements) then its slot point u_k (logN elements); d_claims (device,
  *   canonical): c_k = X_k~(v_k, u_k).  Transcript: "cm/hdr" (n, d, K, logN_k... u32le) | "cm/claims" |
@@ -346,6 +347,29 @@ zk_status zk_verify_claim_merge(uint8_t st[32], uint32_t n, uint32_t d, uint32_t
 zk_status zk_verify_relu_merge(uint8_t st[32], uint32_t logD, uint32_t Q, uint32_t R, const zk_fr* relu_point,
                                const zk_fr* relu_finals, const uint8_t* proof, uint64_t proof_len, zk_fr* point_out,
                                int32_t* fail);
+
+/* ------------------------------------------- the top layer (D24, D26)
+ * zk_loss_grad_prove_dev: zk_loss_grad_prove with device outputs, d_out = u (m canonical) | G_Z~(u),
+ *   Z~(u), Y~(u) (canonical); asynchronous (the chained window's loss family).
+ * zk_rescale_prove_dev — the top layer's rescale Z = 2^R Z' + R_Z, Z' = round(Z / 2^R) (half-up, D9),
+ *   through the bits of Z (Eqs. aux-Z, zkrelu-Z and the Z' relation), at given points
+ *   (d_pts: device, u_Z then u_P, logD canonical elements each: the window's claims on Z and Z', D25).
+ *   Transcript (D26): "rs/hdr" (logD, Q, R) | "rs/claims" (Z~(u_Z), Z'~(u_P)) | r = "rs/r" | product
+ *   sumcheck A (D3c, m = logB + logD, n_eq = 0, K = 2: W(i, j) = r beta(u_Z, i) s(j) + beta(u_P, i) s'(j)
+ *   and aux(i, j), claim r Z~ + Z'~) | w = "rs/w" x m | product sumcheck B (D3c, n_eq = m, K = 2: aux and
+ *   aux - 1, claim 0).  d_out (16-byte aligned): proof = u32le logD, Q, R | 2 claims | proof A | proof B,
+ *   then pad to 16 | point A (m) | point B (m).  Bit 0 of *d_range_flag is set when Z leaves Q+R bits. */
+zk_status zk_loss_grad_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_GZ, const int32_t* d_Z,
+                                 const int32_t* d_Y, uint32_t m, uint8_t* d_out, uint64_t* out_len);
+zk_status zk_rescale_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_Z, uint32_t logD, uint32_t Q,
+                               uint32_t R, const uint8_t* d_pts, uint8_t* d_out, uint64_t* out_len,
+                               uint32_t* d_range_flag);
+/* zk_verify_rescale: a zk_rescale_prove_dev proof for expect = (logD, Q, R) at the given points (pts: u_Z then
+ *   u_P, host): A's round identities from r Z~ + Z'~ and its weight final W~(r_A) (fail -101), B's from 0 in
+ *   the eq form and its second final = first - 1 (fail -102).  claims_out (2): the proof's Z~(u_Z),
+ *   Z'~(u_P); aux_out (2): aux~(r_A), aux~(r_B); point_out (2m): r_A then r_B. */
+zk_status zk_verify_rescale(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const uint32_t expect[3],
+                            const zk_fr* pts, zk_fr* claims_out, zk_fr* aux_out, zk_fr* point_out, int32_t* fail);
 
 /* ----------------------------------------------------------------- diagnostics
  * zk_diag_fr_op: element-wise d_out[i] = op(d_a[i], d_b[i]) on Montgomery tables, op 0 add, 1 sub,

@@ -61,6 +61,7 @@ def lib():
         L.or_claim_merge_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp,
                                            vp, vp, vp, vp, vp, vp]
         L.or_relu_verify_pts.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp]
+        L.or_rescale_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.or_relu_verify.argtypes = [vp, i32p, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp]
         L.or_reindex_prove.argtypes = [vp, i32p, c.c_uint32, c.c_uint32, c.c_uint32, vp, vp, vp, vp, vp, vp, vp,
                                        vp, vp, vp, vp]
@@ -406,3 +407,25 @@ def claim_merge_prove(tr: Transcript, X: np.ndarray, claims: list):
     B = dict(msgs=[fb[3 * t:3 * t + 3] for t in range(d)], r=from_bytes(rB.raw[:32 * d], d),
              finals=from_bytes(fB.raw[:64], 2))
     return dict(rho=from_bytes(rho.raw[:32 * K], K), A=A, B=B, point=B["r"] + A["r"][:n], claim=B["finals"][1])
+
+
+# ---------------------------------------------------------------- N2: the top-layer rescale (D26)
+def rescale_prove(tr: Transcript, Z: np.ndarray, Q: int, R: int, points):
+    """Z = 2^R Z' + R_Z through the bits of Z (D26) at the given points (u_Z, u_P).
+    Returns dict(claims = [Z~(u_Z), Z'~(u_P)], r, A = dict(msgs, r, finals), w, B = dict(msgs, r, finals))."""
+    Z = np.ascontiguousarray(Z, dtype=np.int32).reshape(-1)
+    logD = Z.size.bit_length() - 1
+    assert Z.size == 1 << logD and len(points) == 2 and all(len(u) == logD for u in points)
+    m = relu_logB(Q, R) + logD
+    cl, r, w = _buf(64), _buf(32), _buf(32 * m)
+    mA, rA, fA, mB, rB, fB = _buf(96 * m), _buf(32 * m), _buf(64), _buf(96 * m), _buf(32 * m), _buf(64)
+    s = lib().or_rescale_prove(tr.st, _ptr(Z), logD, Q, R, to_bytes(points[0] + points[1]), cl, r, mA, rA, fA, w,
+                               mB, rB, fB)
+    if s:
+        raise ValueError(f"or_rescale_prove status {s}")
+    fa, fb = from_bytes(mA.raw[:96 * m]), from_bytes(mB.raw[:96 * m])
+    return dict(claims=from_bytes(cl.raw[:64], 2), r=from_bytes(r.raw[:32])[0], w=from_bytes(w.raw[:32 * m], m),
+                A=dict(msgs=[fa[3 * t:3 * t + 3] for t in range(m)], r=from_bytes(rA.raw[:32 * m], m),
+                       finals=from_bytes(fA.raw[:64], 2)),
+                B=dict(msgs=[fb[3 * t:3 * t + 3] for t in range(m)], r=from_bytes(rB.raw[:32 * m], m),
+                       finals=from_bytes(fB.raw[:64], 2)))

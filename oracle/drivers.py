@@ -9,7 +9,7 @@ from __future__ import annotations
 import numpy as np
 
 import oracle as O
-from synth.fcn import MatmulFamily, ReluFamily, fcn_header
+from synth.fcn import LossFamily, MatmulFamily, ReluFamily, RescaleFamily, fcn_header
 from synth.prng import DATA_SEED, fs_seed, uniform_range
 
 P = O.P
@@ -139,11 +139,15 @@ def _is_whole(t, cl):
 
 
 def _tensor_values(t, families):
-    """The int32 stack [N][rows * cols] of a tensor family; the ReLU-bound ones from the words (Lemma 1)."""
+    """The int32 stack [N][rows * cols] of a tensor family; the ReLU-bound ones from the words (Lemma 1),
+    the rescaled top output Z' from the rescale family's Z (D9)."""
     N = len(t.slots)
-    if t.relu is None:
+    if t.array is not None:
         return np.ascontiguousarray(t.array.reshape(N, -1))
     f = next(g for g in families if g.name == t.relu)
+    if t.kind == "Zp":
+        z = np.asarray(f.Z, dtype=np.int64)
+        return np.ascontiguousarray(((z + (1 << (f.R - 1))) >> f.R).astype(np.int32).reshape(N, -1))
     if t.kind in ("Z", "GA"):
         v = f.Z if t.kind == "Z" else f.GA
     else:
@@ -152,7 +156,15 @@ def _tensor_values(t, families):
     return np.ascontiguousarray(np.asarray(v, dtype=np.int32).reshape(N, -1))
 
 
-def fcn_prove_chained(shape, families, tensors, seed_name: str):
+def _loss_family_claims(f, res):
+    """The loss family's three claims (D24) at its point u = (inner bits, slot bits) of the stacked
+    [N][B][d_L] tensors."""
+    d = (f.GZ.shape[1] * f.GZ.shape[2]).bit_length() - 1
+    u = res["u"]
+    return [(role, f.refs[role], u[:d], u[d:], c) for role, c in zip(("GZ", "Zp", "Y"), res["claims"])]
+
+
+def fcn_prove_chained(shape, families, tensors, seed_name: str, top=None):
     """The claim-chained window (Protocol 1 lines 7-8; D25).  Window transcript W:
     "fcn/chdr" (header) | stage 1: per matmul family "fcn/fam" <name> and a fork; each family proved on
     its fork (D3a) | "fcn/join" per family | stage 2: per tensor family whose claims need merging (more
@@ -164,26 +176,33 @@ def fcn_prove_chained(shape, families, tensors, seed_name: str):
     window_state)."""
     W = O.Transcript(fs_seed(seed_name))
     W.absorb("fcn/chdr", fcn_header(shape))
+    top = list(top or [])
     mms = [f for f in families if isinstance(f, MatmulFamily)]
     relus = [f for f in families if isinstance(f, ReluFamily)]
+    losses = [f for f in top if isinstance(f, LossFamily)]
+    rescales = [f for f in top if isinstance(f, RescaleFamily)]
 
     def fork():
         return O.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little"))
 
     kids = []
-    for f in mms:
+    for f in mms + losses:
         W.absorb("fcn/fam", f.name.encode())
         kids.append(fork())
     mres = {}
-    for f, T in zip(mms, kids):
-        r = O.matmul_prove(T, f.A, f.B, f.transA, f.transB)
+    for f, T in zip(mms + losses, kids):
+        if isinstance(f, LossFamily):
+            r = O.loss_grad_prove(T, f.GZ, f.Zp, f.Y)
+        else:
+            r = O.matmul_prove(T, f.A, f.B, f.transA, f.transB)
         r["state"] = T.state()
         mres[f.name] = r
     for T in kids:
         W.absorb("fcn/join", T.state())
     claims = {t.name: [] for t in tensors}
-    for f in mms:
-        for role, ref, v, u, c in _matmul_family_claims(f, mres[f.name]):
+    for f in mms + losses:
+        fc = _loss_family_claims(f, mres[f.name]) if isinstance(f, LossFamily) else _matmul_family_claims(f, mres[f.name])
+        for role, ref, v, u, c in fc:
             claims[ref.tensor].append(dict(map=list(ref.map), u=list(u), v=list(v), c=c, src=(f.name, role)))
     opened = {}
     to_merge = []
@@ -209,11 +228,27 @@ def fcn_prove_chained(shape, families, tensors, seed_name: str):
     for T in mk:
         W.absorb("fcn/join", T.state())
     rk = []
-    for f in relus:
+    for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
         rk.append(fork())
     rres = {}
-    for f, T in zip(relus, rk):
+    for f, T in zip(relus + rescales, rk):
+        if isinstance(f, RescaleFamily):   # D26, then the claim merge (D25) of its two aux claims
+            names = [f.tensors["Z"], f.tensors["Zp"]]
+            r = O.rescale_prove(T, f.Z, f.Q, f.R, [opened[n][0] for n in names])
+            logB = O.relu_logB(f.Q, f.R)
+            D = f.Z.size
+            bits = ((f.Z.astype(np.int64).reshape(-1, 1) & 0xFFFFFFFF) >> np.arange(1 << logB)) & 1
+            bits[:, f.Q + f.R:] = 0
+            aux = [dict(map=[0], u=[], v=r["A"]["r"], c=r["A"]["finals"][1]),
+                   dict(map=[0], u=[], v=r["B"]["r"], c=r["B"]["finals"][0])]
+            r["aux_merge"] = O.claim_merge_prove(T, np.ascontiguousarray(bits.astype(np.int32).reshape(1, D << logB)), aux)
+            r["state"] = T.state()
+            rres[f.name] = r
+            for n in names:
+                opened.pop(n)
+            opened["aux:" + f.name] = (r["aux_merge"]["point"], r["aux_merge"]["claim"])
+            continue
         names = [f.tensors[k] for k in ("Z", "A", "GA", "GZ")]
         r = O.relu_prove(T, f.Z, f.GA, f.Q, f.R, points=[opened[n][0] for n in names])
         r["merge"] = O.relu_merge(T, f.Z, f.GA, f.Q, f.R, r["point"], r["finals"])

@@ -1207,6 +1207,79 @@ int or_loss_grad_prove(transcript *tr, uint32_t m, const int32_t *GZ, const int3
     return 0;
 }
 
+/* ------------------------------------------------------------ N2: the top-layer rescale (D26)
+ * Eq. (fcnn-GZ-last) uses the top layer's output at the activations' scale; as for every
+ * pre-activation (Eqs. zkrelu-Z, and the aux relations P:L188-199) that is the rescaled
+ * Z' = round(Z / 2^R) (half-up, D9) with Z = 2^R Z' + R_Z, proved through the bits of Z: aux(i, j) = bit j
+ * of Z[i] (two's complement, zero for j >= Q+R), Z = aux s_{Q+R} (Eq. aux-Z) and Z' = aux[:, R:Q+R] s_Q +
+ * aux[:, R-1], aux binary (Eq. aux-bin).  Given claims c_Z = Z~(u_Z), c_P = Z'~(u_P) (points
+ * given: the window's claims on Z and Z', D25) and r from the transcript:
+ *   A: r c_Z + c_P = sum_{i,j} W(i, j) aux(i, j),  W = r beta(u_Z, i) s(j) + beta(u_P, i) s'(j)
+ *   B: 0 = sum_x beta(w, x) aux(x) (aux(x) - 1)        (w drawn after A)
+ * two product sumchecks (D3c; x = (j, i), j bound first); the verifier recomputes W~ and checks the
+ * second final of B is the first minus one; the two aux claims aux~(r_A), aux~(r_B) remain.
+ * Transcript: "rs/hdr" (logD, Q, R) | "rs/claims" (c_Z, c_P) | r = "rs/r" | A (n_eq = 0, claim given) |
+ * w = "rs/w" x m | B (n_eq = m, claim 0). */
+int or_rescale_prove(transcript *tr, const int32_t *Z, uint32_t logD, uint32_t Q, uint32_t R,
+                     const uint8_t *pts_in /* u_Z, u_P: 2 x logD */, uint8_t *claims_out /* 2 */, uint8_t *r_out,
+                     uint8_t *msgsA /* m x 3 */, uint8_t *rA /* m */, uint8_t *finA /* 2 */, uint8_t *w_out /* m */,
+                     uint8_t *msgsB /* m x 3 */, uint8_t *rB /* m */, uint8_t *finB /* 2 */) {
+    init();
+    uint32_t QR = Q + R;
+    if (Q < 1 || R < 1 || Q > 32 || R > 32 || QR > 32 || logD < 1 || logD > 26) return -1;
+    uint32_t logB = 0;
+    while ((1u << logB) < QR) logB++;
+    uint64_t D = 1ULL << logD, B = 1ULL << logB, n = D << logB;
+    uint32_t m = logB + logD;
+    fr uZ[32], uP[32];
+    if (load_point(pts_in, (int)logD, uZ) || load_point(pts_in + 32 * logD, (int)logD, uP)) return -3;
+    const int64_t lim = 1LL << (QR - 1);
+    int32_t *Zp = (int32_t *)malloc(D * 4);
+    for (uint64_t i = 0; i < D; i++) {
+        if ((int64_t)Z[i] < -lim || (int64_t)Z[i] >= lim) { free(Zp); return -2; }
+        Zp[i] = (int32_t)(((int64_t)Z[i] + (1LL << (R - 1))) >> R);      /* round(Z / 2^R), half-up (D9) */
+    }
+    fr cl[2] = {mle_i32(Z, (int)logD, uZ), mle_i32(Zp, (int)logD, uP)};
+    free(Zp);
+    for (int k = 0; k < 2; k++) store_canon(cl[k], claims_out + 32 * k);
+    uint32_t hdr[3] = {logD, Q, R};
+    absorb_u32s(tr, "rs/hdr", hdr, 3);
+    absorb_frs(tr, "rs/claims", cl, 2);
+    fr r = transcript_challenge(tr, "rs/r");
+    store_canon(r, r_out);
+    /* tables, flat x = i * B + j */
+    uint8_t *tb = (uint8_t *)malloc(2 * n * 32);
+    #pragma omp parallel for schedule(static)
+    for (uint64_t i = 0; i < D; i++) {
+        fr ez = fr_mul(r, eq_at(uZ, (int)logD, i)), ep = eq_at(uP, (int)logD, i);
+        uint32_t z = (uint32_t)Z[i];
+        for (uint64_t j = 0; j < B; j++) {
+            fr w = fr_add(fr_mul(ez, s_weight((int)j, (int)Q, (int)R)), fr_mul(ep, sp_weight((int)j, (int)Q, (int)R)));
+            fr a = (j < QR && ((z >> j) & 1)) ? fr_one() : fr_zero();
+            store_canon(w, tb + 32 * (i * B + j));
+            store_canon(a, tb + 32 * (n + i * B + j));
+        }
+    }
+    uint8_t cb[32], cout[32];
+    store_canon(fr_add(fr_mul(r, cl[0]), cl[1]), cb);
+    int st = or_sumcheck_prove(tr, m, 0, 2, NULL, tb, cb, cout, msgsA, rA, finA);
+    if (st) { free(tb); return st; }
+    fr w[64];
+    for (uint32_t t = 0; t < m; t++) { w[t] = transcript_challenge(tr, "rs/w"); store_canon(w[t], w_out + 32 * t); }
+    /* B: tables aux and aux - 1 */
+    #pragma omp parallel for schedule(static)
+    for (uint64_t x = 0; x < n; x++) {
+        fr a;
+        load_canon(tb + 32 * (n + x), &a);
+        memcpy(tb + 32 * x, tb + 32 * (n + x), 32);
+        store_canon(fr_sub(a, fr_one()), tb + 32 * (n + x));
+    }
+    store_canon(fr_zero(), cb);
+    st = or_sumcheck_prove(tr, m, m, 2, w_out, tb, cb, cout, msgsB, rB, finB);
+    free(tb);
+    return st;
+}
+
 /* ------------------------------------------------------------ misc exports */
 /* ------------------------------------------------------------ N3: the claim merge (D25)
  * Protocol 1 line 8 ends every family's sumcheck with Eq. (sc-reindex) so that

@@ -110,6 +110,9 @@ def lib():
         "zk_verify_relu": ([vp, vp, u64, vp, vp, vp, vp], i32),
         "zk_verify_claim_merge": ([vp, u32, u32, u32, vp, vp, vp, vp, u64, vp, vp, vp], i32),
         "zk_claim_merge_dev": ([vp, vp, vp, vp, u32, u32, u32, u32, u32, u32, vp, vp, vp, vp, c.POINTER(u64)], i32),
+        "zk_loss_grad_prove_dev": ([vp, vp, vp, vp, vp, u32, vp, c.POINTER(u64)], i32),
+        "zk_rescale_prove_dev": ([vp, vp, vp, u32, u32, u32, vp, vp, c.POINTER(u64), vp], i32),
+        "zk_verify_rescale": ([vp, vp, u64, vp, vp, vp, vp, vp, vp], i32),
         "zk_relu_prove_chained_dev": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, c.POINTER(u64), vp], i32),
         "zk_loss_grad_prove": ([vp, vp, vp, vp, vp, u32, vp, vp], i32),
         "zk_verify_loss_grad": ([vp, u32, vp, vp, vp], i32),

@@ -502,7 +502,7 @@ def loss_grad_prove(ctx: Context, tr: Transcript, GZ: torch.Tensor, Z: torch.Ten
 
 
 # ---------------------------------------------------------------- N3: the claim merge (D25)
-CM_SOURCE = {"plain": 0, "relu_A": 1, "relu_GZ": 2}
+CM_SOURCE = {"plain": 0, "relu_A": 1, "relu_GZ": 2, "bits": 3}
 
 
 def claim_merge_layout(n: int, K: int, d: int) -> dict:
@@ -562,4 +562,37 @@ def relu_prove_chained_dev(ctx: Context, tr: Transcript, Z: torch.Tensor, GA: to
     ctx.check(lib().zk_relu_prove_chained_dev(ctx.h, tr.h, _dev_ptr(Z, torch.int32), _dev_ptr(GA, torch.int32), logD, Q, R,
                                               _dev_ptr(d_pts, torch.uint8), out.data_ptr(), ctypes.byref(ln),
                                               range_flag.data_ptr()))
+    return out
+
+
+# ---------------------------------------------------------------- N2: the top layer (D24, D26)
+def loss_grad_prove_dev(ctx: Context, tr: Transcript, GZ: torch.Tensor, Z: torch.Tensor, Y: torch.Tensor,
+                        out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_loss_grad_prove_dev: out = u (m canonical) | G_Z~(u), Z~(u), Y~(u) (canonical); asynchronous."""
+    m = _log2(Z.numel())
+    n = 32 * m + 96
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=Z.device)
+    ln = ctypes.c_uint64(out.numel())
+    ctx.check(lib().zk_loss_grad_prove_dev(ctx.h, tr.h, _dev_ptr(GZ, torch.int32), _dev_ptr(Z, torch.int32),
+                                           _dev_ptr(Y, torch.int32), m, out.data_ptr(), ctypes.byref(ln)))
+    return out
+
+
+def rescale_prove_len(logD: int, Q: int, R: int) -> int:
+    m = relu_logB(Q, R) + logD
+    return _a16(12 + 64 + 2 * (12 + 32 + 96 * m + 64)) + 64 * m
+
+
+def rescale_prove_dev(ctx: Context, tr: Transcript, Z: torch.Tensor, Q: int, R: int, d_pts: torch.Tensor,
+                      range_flag: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_rescale_prove_dev (D26) at the points d_pts (device canonical: u_Z then u_P)."""
+    logD = _log2(Z.numel())
+    n = rescale_prove_len(logD, Q, R)
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=Z.device)
+    assert d_pts.numel() == 64 * logD
+    ln = ctypes.c_uint64(out.numel())
+    ctx.check(lib().zk_rescale_prove_dev(ctx.h, tr.h, _dev_ptr(Z, torch.int32), logD, Q, R, _dev_ptr(d_pts, torch.uint8),
+                                         out.data_ptr(), ctypes.byref(ln), range_flag.data_ptr()))
     return out

@@ -2,11 +2,13 @@
 DESIGN.md D25).  Sequencing of library calls only (no arithmetic here).
 
 Window transcript W ("fcn/chdr" header), three stages, each a set of forked transcripts joined back:
-  1. every matmul family (zk_matmul_prove on its fork, spread over the matmul streams);
+  1. every matmul family (zk_matmul_prove on its fork, spread over the matmul streams) and the loss family
+     (zk_loss_grad_prove_dev, D24);
   2. every tensor family whose claims need merging (zk_claim_merge_dev: the claims of stage 1 on views of
      it -> one claim on its stack), spread over all streams;
   3. every ReLU family: zk_relu_prove_chained_dev at the merged points of its Z, A, G_A, G_Z stacks
-     (P:L186), then the aux-claim merge (zk_relu_merge_dev, D21).
+     (P:L186), then the aux-claim merge (zk_relu_merge_dev, D21); the top layer's rescale
+     (zk_rescale_prove_dev, D26) at the claims on Z^(L) and Z^(L)', then the merge of its two aux claims.
 The window ends with one claim per committed tensor family and one on each aux (verify.verify_window_chained
 returns exactly those).  The claims of stage 1 travel to stage 2 as device bytes (slices of the window's
 output buffer gathered on the consuming stream), so the whole window is one stream-ordered program with
@@ -20,7 +22,7 @@ import torch
 
 from . import api
 from .fcn import DeviceFamily
-from .plan import RELU_ROLES, is_whole, matmul_claim_pieces
+from .plan import RELU_ROLES, family_kind, is_whole, matmul_claim_pieces
 
 
 @dataclass
@@ -38,11 +40,14 @@ class DeviceTensor:
 
 @dataclass
 class ChainedFamily(DeviceFamily):
-    refs: dict = field(default_factory=dict)      # matmul: role -> (tensor name, map)
-    tensors: dict = field(default_factory=dict)   # ReLU: role -> tensor name
+    refs: dict = field(default_factory=dict)      # matmul / loss: role -> (tensor name, map)
+    tensors: dict = field(default_factory=dict)   # ReLU / rescale: role -> tensor name
+    GZ: torch.Tensor = None                       # loss family (D24): G_Z^(L), Z^(L)', Y stacks
+    Zp: torch.Tensor = None
+    Y: torch.Tensor = None
 
 
-def upload_plan(families, tensors, device="cuda") -> tuple:
+def upload_plan(families, tensors, device="cuda", top=None) -> tuple:
     """synth.fcn families + plan_window tensor families -> device records; an array shared by several
     families or tensor families (same numpy object) is copied once."""
     seen = {}
@@ -53,10 +58,16 @@ def upload_plan(families, tensors, device="cuda") -> tuple:
         return seen[id(a)]
 
     fams = []
-    for f in families:
-        if hasattr(f, "A"):
+    for f in list(families) + list(top or []):
+        k = family_kind(f)
+        if k == "matmul":
             fams.append(ChainedFamily(f.name, "matmul", A=dev(f.A), B=dev(f.B), trans_a=f.transA, trans_b=f.transB,
                                       refs={k: (r.tensor, list(r.map)) for k, r in f.refs.items()}))
+        elif k == "loss":
+            fams.append(ChainedFamily(f.name, "loss", GZ=dev(f.GZ), Zp=dev(f.Zp), Y=dev(f.Y),
+                                      refs={k: (r.tensor, list(r.map)) for k, r in f.refs.items()}))
+        elif k == "rescale":
+            fams.append(ChainedFamily(f.name, "rescale", Z=dev(f.Z), Q=f.Q, R=f.R, tensors=dict(f.tensors)))
         else:
             fams.append(ChainedFamily(f.name, "relu", Z=dev(f.Z), GA=dev(f.GA), Q=f.Q, R=f.R, tensors=dict(f.tensors)))
     ts = [DeviceTensor(t.name, t.kind, [s is None for s in t.slots], t.rows, t.cols, t.relu,
@@ -108,7 +119,9 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     """Enqueue one chained window without synchronising; returns a handle for collect_window_chained."""
     dev = next(f.A for f in families if f.kind == "matmul").device
     mms = [f for f in families if f.kind == "matmul"]
+    losses = [f for f in families if f.kind == "loss"]
     relus = [f for f in families if f.kind == "relu"]
+    rescales = [f for f in families if f.kind == "rescale"]
     tmap = {t.name: t for t in tensors}
     lanes1 = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
     rctx = relu_ctx if relu_ctx is not None else ctx
@@ -121,7 +134,12 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         n = api.matmul_prove_len(logs)
         lay1.append((f, logs, off, n))
         off += _slot(n)
-    # the claims stage 1 leaves, per tensor family (in family order, roles Y, A, B)
+    layL = []
+    for f in losses:
+        m = _log2(f.GZ.numel())
+        layL.append((f, m, off, 32 * m + 96))
+        off += _slot(32 * m + 96)
+    # the claims stage 1 leaves, per tensor family (in family order, roles Y, A, B; then G_Z, Z', Y)
     claims = {t.name: [] for t in tensors}
     for f, logs, o, n in lay1:
         pieces = _mm_pieces(logs)
@@ -129,6 +147,12 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
             tname, mp = f.refs[role]
             rng = lambda names: [(o + pieces[p][0], pieces[p][1]) for p in names]
             claims[tname].append(dict(map=mp, v=rng(vp), u=rng(up), c=rng([cp]), src=(f.name, role)))
+    for f, m, o, n in layL:
+        d = _log2(f.GZ.shape[1] * f.GZ.shape[2])
+        for k, role in enumerate(("GZ", "Zp", "Y")):
+            tname, mp = f.refs[role]
+            claims[tname].append(dict(map=mp, v=[(o, d)], u=[(o + 32 * d, m - d)], c=[(o + 32 * m + 32 * k, 1)],
+                                      src=(f.name, role)))
     merges = [t for t in tensors if claims[t.name] and not is_whole(t.pad, [c["map"] for c in claims[t.name]])]
     lay2 = []
     for t in merges:
@@ -144,6 +168,14 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         n = api._a16(rn) + api.relu_merge_len(f.Q, f.R)
         lay3.append((f, logD, rn, off, n))
         off += _slot(n)
+    layR = []
+    for f in rescales:
+        logD = _log2(f.Z.numel())
+        logB = api.relu_logB(f.Q, f.R)
+        rl = api.rescale_prove_len(logD, f.Q, f.R)
+        L = api.claim_merge_layout(0, 2, logD + logB)
+        layR.append((f, logD, logB, rl, L, off, api._a16(rl) + L["total"]))
+        off += _slot(api._a16(rl) + L["total"])
     out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
     flag = torch.zeros(1, dtype=torch.int32, device=dev)
     keep = []   # device temporaries in use by enqueued work
@@ -162,14 +194,20 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     home1 = {}
     for i in sorted(range(len(mms)), key=lambda i: -(mms[i].A.numel() + mms[i].B.numel())):
         home1[i] = L1.pick(mms[i].A.numel() + mms[i].B.numel())
+    for i in range(len(losses)):
+        home1[len(mms) + i] = L1.pick(losses[i].GZ.numel() * 3)
     kids1 = []
-    for i, f in enumerate(mms):
+    for i, f in enumerate(mms + losses):
         W.absorb("fcn/fam", f.name.encode())
         kids1.append(W.fork("fcn/fork", home1[i]))
     _fence(ctx, lanes1)
     for i, (f, logs, o, n) in enumerate(lay1):
         c, T = home1[i], kids1[i]
         api.matmul_prove(c, T, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
+        T.state_dev(out[o + n:o + n + 32])
+    for i, (f, m, o, n) in enumerate(layL):
+        c, T = home1[len(mms) + i], kids1[len(mms) + i]
+        api.loss_grad_prove_dev(c, T, f.GZ, f.Zp, f.Y, out=out[o:o + n])
         T.state_dev(out[o + n:o + n + 32])
     for c in lanes1[1:]:
         _fence(c, [ctx])
@@ -188,8 +226,10 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         d_cl = gather(c, [r for x in cl for r in x["c"]])
         maps = [x["map"] for x in cl]
         lr, lc = _log2(t.rows), _log2(t.cols)
-        if t.relu is None:
+        if t.array is not None:
             api.claim_merge_dev(c, T, t.array, n, lr, lc, maps, d_pts, d_cl, out=out[o:o + L["total"]])
+        elif t.kind == "Zp":
+            raise NotImplementedError("a claim merge on Z' (one loss claim on it is the whole stack)")
         else:
             f = next(g for g in relus if g.name == t.relu)
             src = {"Z": ("plain", f.Z, None), "GA": ("plain", f.GA, None), "A": ("relu_A", f.Z, None),
@@ -201,18 +241,36 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         _fence(c, [ctx])
     for T in kids2:
         W.absorb_state("fcn/join", T)
-    # ---- stage 3: the chained zkReLU families and their aux merges
+    # ---- stage 3: the chained zkReLU families and their aux merges; the top layer's rescale
     pos2 = {t.name: (o, L) for t, n, cl, o, L in lay2}
+
+    def point_ranges(tname):   # the one claim on a tensor family: its merge output, or its single claim
+        if tname in pos2:
+            to, tl = pos2[tname]
+            d = _log2(tmap[tname].rows) + _log2(tmap[tname].cols)
+            return [(to + tl["off_pt"], d + _log2(len(tmap[tname].pad)))]
+        c0 = claims[tname][0]
+        return c0["v"] + c0["u"]
     kids3 = []
-    for f in relus:
+    for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
         kids3.append(W.fork("fcn/fork", rctx))
     _fence(ctx, [rctx])
+    for (f, logD, logB, rl, L, o, n), T in zip(layR, kids3[len(relus):]):
+        d_pts = gather(rctx, point_ranges(f.tensors["Z"]) + point_ranges(f.tensors["Zp"]))
+        api.rescale_prove_dev(rctx, T, f.Z, f.Q, f.R, d_pts, flag, out=out[o:o + rl])
+        # the two aux claims -> one (claim merge, D25, on the bits of Z: one slice [D][B])
+        po = o + api._a16(12 + 64 + 2 * (12 + 32 + 96 * (logD + logB) + 64))
+        pla = o + 76 + (12 + 32 + 96 * (logD + logB) + 64) - 32          # A's second final: aux~(r_A)
+        plb = o + 76 + 2 * (12 + 32 + 96 * (logD + logB) + 64) - 64      # B's first final: aux~(r_B)
+        d_apts = gather(rctx, [(po, logD + logB), (po + 32 * (logD + logB), logD + logB)])
+        d_acl = gather(rctx, [(pla, 1), (plb, 1)])
+        mo = o + api._a16(rl)
+        api.claim_merge_dev(rctx, T, f.Z, 0, logD, logB, [[0], [0]], d_apts, d_acl, source="bits", R=f.Q + f.R,
+                            out=out[mo:mo + L["total"]])
+        T.state_dev(out[o + n:o + n + 32])
     for (f, logD, rn, o, n), T in zip(lay3, kids3):
-        rngs = []
-        for role in RELU_ROLES:
-            to, tl = pos2[f.tensors[role]]
-            rngs.append((to + tl["off_pt"], logD))
+        rngs = [r for role in RELU_ROLES for r in point_ranges(f.tensors[role])]
         d_pts = gather(rctx, rngs)
         api.relu_prove_chained_dev(rctx, T, f.Z, f.GA, f.Q, f.R, d_pts, flag, out=out[o:o + rn])
         mo = o + api._a16(rn)
@@ -226,7 +284,8 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     for T in kids1 + kids2 + kids3:
         T.close()
     W.close()
-    return dict(out=out, flag=flag, lay1=lay1, lay2=lay2, lay3=lay3, end=off, keep=keep, claims=claims)
+    return dict(out=out, flag=flag, lay1=lay1, layL=layL, lay2=lay2, lay3=lay3, layR=layR, end=off, keep=keep,
+                claims=claims)
 
 
 def collect_window_chained(h: dict) -> dict:
@@ -235,7 +294,14 @@ def collect_window_chained(h: dict) -> dict:
     raw = h["out"].cpu().numpy().tobytes()
     if int(h["flag"].item()) & 1:
         raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")
-    res = dict(matmul={}, merges={}, relu={})
+    res = dict(matmul={}, merges={}, relu={}, loss={}, rescale={})
+    for f, m, o, n in h["layL"]:
+        vals = [int.from_bytes(raw[o + 32 * i:o + 32 * i + 32], "little") for i in range(m + 3)]
+        res["loss"][f.name] = dict(u=vals[:m], claims=vals[m:], state=raw[o + n:o + n + 32])
+    for f, logD, logB, rl, L, o, n in h["layR"]:
+        am = api.parse_claim_merge_out(raw[o + api._a16(rl):o + api._a16(rl) + L["total"]], 0, 2, logD + logB)
+        res["rescale"][f.name] = dict(proof=raw[o:o + 12 + 64 + 2 * (12 + 32 + 96 * (logD + logB) + 64)],
+                                      aux_merge=am, state=raw[o + n:o + n + 32])
     for f, logs, o, n in h["lay1"]:
         r = api.parse_matmul_out(raw[o:o + n], logs)
         res["matmul"][f.name] = dict(logs=logs, w=r["w"], u1=r["u1"], u3=r["u3"], claim=r["claim"], msgs=r["msgs"],

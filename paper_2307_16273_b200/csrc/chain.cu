@@ -222,8 +222,9 @@ zk_status zk_claim_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_X,
         *out_len = L.total;
         ZK_REQUIRE(((uintptr_t)d_out & 15) == 0, ZK_ERR_ARG, "d_out must be 16-byte aligned");
         ZK_REQUIRE(tr && d_X && views && d_pts && d_claims, ZK_ERR_ARG, "null argument");
-        ZK_REQUIRE(source <= 2 && (source != 2 || d_X2) && (source == 0 || (R >= 1 && R <= 31)), ZK_ERR_ARG,
-                   "bad source");
+        ZK_REQUIRE(source <= 3 && (source != 2 || d_X2) && (source == 0 || (R >= 1 && R <= 32)) &&
+                       (source != 3 || n == 0),
+                   ZK_ERR_ARG, "bad source");
         CmMaps M;
         memset(&M, 0, sizeof M);
         M.K = K;
@@ -251,9 +252,12 @@ zk_status zk_claim_merge_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* d_X,
             claim_merge_dev(ctx, tr, LoadPlain{d_X}, n, log_rows, log_cols, M, nk.data(), d_pts, d_claims, d_out, s);
         else if (source == 1)
             claim_merge_dev(ctx, tr, LoadReluA{d_X, R}, n, log_rows, log_cols, M, nk.data(), d_pts, d_claims, d_out, s);
-        else
+        else if (source == 2)
             claim_merge_dev(ctx, tr, LoadReluGZ{d_X, d_X2, R}, n, log_rows, log_cols, M, nk.data(), d_pts, d_claims,
                             d_out, s);
+        else   // the rescale's aux bits (D26): one slice of 2^log_rows entries x 2^log_cols bit columns
+            claim_merge_dev(ctx, tr, LoadBits{d_X, log_cols, R}, n, log_rows, log_cols, M, nk.data(), d_pts,
+                            d_claims, d_out, s);
     } catch (const ::zk::ZkError& e) {
         ctx->err = e.msg;
         return e.st;

@@ -261,6 +261,8 @@ void mle_i32_relu(zk_ctx* ctx, int kind, const int32_t* d_z, const int32_t* d_g,
                   fr_t* d_out, Scratch& s) {
     if (kind == 0)
         mle_i32_generic(ctx, LoadReluA{d_z, R}, m, d_u, d_out, s);
+    else if (kind == 2)
+        mle_i32_generic(ctx, LoadRound{d_z, R}, m, d_u, d_out, s);
     else
         mle_i32_generic(ctx, LoadReluGZ{d_z, d_g, R}, m, d_u, d_out, s);
 }

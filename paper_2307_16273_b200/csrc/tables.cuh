@@ -96,6 +96,25 @@ struct LoadReluGZ {
     }
 };
 
+// Z' = round(Z / 2^R) (half-up D9), the rescale of the top layer (D26)
+struct LoadRound {
+    const int32_t* z;
+    uint32_t R;
+    __device__ __forceinline__ int32_t operator()(uint64_t i) const {
+        const int64_t v = __ldg(z + i);
+        return (int32_t)((v + (1ll << (R - 1))) >> R);
+    }
+};
+// aux(i, j) = bit j of Z[i] (zero for j >= QR), flat index i * 2^logB + j (the rescale's aux bits, D26)
+struct LoadBits {
+    const int32_t* z;
+    uint32_t logB, QR;
+    __device__ __forceinline__ int32_t operator()(uint64_t x) const {
+        const uint32_t j = (uint32_t)(x & ((1ull << logB) - 1));
+        return j < QR ? (int32_t)(((uint32_t)__ldg(z + (x >> logB)) >> j) & 1u) : 0;
+    }
+};
+
 // One warp per row r of an int32 matrix viewed through `load` (row-major, `cols` entries per row,
 // rows < nrows): out[map(r)] = sum_c M[r][c] * eq[c], with E2 = eq table scaled by R (double Montgomery).
 // map(r) = (r & (inner - 1)) * outer + (r >> log_inner)   (restriction layout [k][n]); inner = nrows gives identity.
@@ -176,7 +195,7 @@ void mle_i32_plain(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const fr_t* d_
 // CTAs, the rows split into S chunks (partials summed by k_colsum_finish) when there are few outputs.
 void colsum_i32(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
                 Scratch& s);
-void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ*/, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m,
+void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ, 2 Z' = round(Z / 2^R)*/, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m,
                   const fr_t* d_u, fr_t* d_out, Scratch& s);
 // Row dots out[map(r)] = sum_c M[r][c] E2[c] of an int32 matrix on the tensor cores (restrict_tc.cu): same
 // results as k_rowdot_i32<LoadPlain>; rowdot_tc_ok says whether the shape is supported (cols % 8 == 0,

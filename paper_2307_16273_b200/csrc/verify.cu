@@ -631,4 +631,76 @@ zk_status zk_verify_claim_merge(uint8_t st[32], uint32_t n, uint32_t d, uint32_t
     });
 }
 
+// The top-layer rescale (D26): A from the claim r Z~(u_Z) + Z'~(u_P) with the weight final recomputed from
+// the verifier's own beta, s and s' evaluations; B from 0 in the eq form (Protocol 3) with its second
+// final = the first minus one (the MLE of aux - 1).
+zk_status zk_verify_rescale(uint8_t st[32], const uint8_t* proof, uint64_t proof_len, const uint32_t expect[3],
+                            const zk_fr* pts, zk_fr* claims_out, zk_fr* aux_out, zk_fr* point_out, int32_t* fail) {
+    return guarded(fail, [&] {
+        need(st && proof && expect && pts && proof_len >= 12);
+        const uint32_t logD = rd32(proof), Q = rd32(proof + 4), R = rd32(proof + 8);
+        if (logD != expect[0] || Q != expect[1] || R != expect[2]) throw Reject{-2};
+        need(logD >= 1 && logD <= 40 && Q >= 1 && R >= 1 && Q <= 32 && R <= 32 && Q + R <= 32);
+        const uint32_t QR = Q + R;
+        uint32_t logB = 0;
+        while ((1u << logB) < QR) logB++;
+        const uint32_t m = logB + logD;
+        const uint64_t lp = 12 + 32 + 96ull * m + 64;
+        need(proof_len == 12 + 64 + 2 * lp);
+        const uint8_t *pa = proof + 76, *pb = proof + 76 + lp;
+        if (rd32(pa) != m || rd32(pa + 4) != 0 || rd32(pa + 8) != 2) throw Reject{-2};
+        if (rd32(pb) != m || rd32(pb + 4) != m || rd32(pb + 8) != 2) throw Reject{-2};
+        const uint32_t hdr[3] = {logD, Q, R};
+        tr_absorb_u32s(st, "rs/hdr", hdr, 3);
+        F uZ[40], uP[40], cl[2];
+        for (uint32_t i = 0; i < logD; i++) {
+            uZ[i] = ld(pts[i].b);
+            uP[i] = ld(pts[logD + i].b);
+        }
+        cl[0] = ld(proof + 12);
+        cl[1] = ld(proof + 44);
+        tr_absorb_frs(st, "rs/claims", cl, 2);
+        const F r = tr_challenge(st, "rs/r");
+        const F cA = add(mul(r, cl[0]), cl[1]);
+        if (!eq(ld(pa + 12), cA)) throw Reject{-1};
+        const uint32_t hA[3] = {m, 0, 2};
+        tr_absorb_u32s(st, "sc/hdr", hA, 3);
+        tr_absorb_frs(st, "sc/claim", &cA, 1);
+        F rA[80], rB[80], w[80];
+        sumcheck_rounds(st, m, 0, 2, nullptr, cA, pa + 44, pa + 44 + 96ull * m, rA);
+        const F* vj = rA;
+        const F* vi = rA + logB;
+        F sv = zero(), spv = zero();
+        for (uint32_t j = 0; j < QR; j++) {
+            const F e = beta_at(vj, logB, j);
+            sv = add(sv, mul(e, j == QR - 1 ? neg(from_u64(1ull << (QR - 1))) : from_u64(1ull << j)));
+            if (j + 1 >= R) {
+                const F spw = j == R - 1 ? ONE : (j == QR - 1 ? neg(from_u64(1ull << (Q - 1))) : from_u64(1ull << (j - R)));
+                spv = add(spv, mul(e, spw));
+            }
+        }
+        const F Wv = add(mul(r, mul(beta(uZ, vi, logD), sv)), mul(beta(uP, vi, logD), spv));
+        if (!eq(ld(pa + 44 + 96ull * m), Wv)) throw Reject{-101};
+        for (uint32_t t = 0; t < m; t++) w[t] = tr_challenge(st, "rs/w");
+        if (!eq(ld(pb + 12), zero())) throw Reject{-1};
+        const uint32_t hB[3] = {m, m, 2};
+        tr_absorb_u32s(st, "sc/hdr", hB, 3);
+        const F z = zero();
+        tr_absorb_frs(st, "sc/claim", &z, 1);
+        sumcheck_rounds(st, m, m, 2, w, z, pb + 44, pb + 44 + 96ull * m, rB);
+        const F b0 = ld(pb + 44 + 96ull * m), b1 = ld(pb + 44 + 96ull * m + 32);
+        if (!eq(b1, sub(b0, ONE))) throw Reject{-102};
+        if (claims_out) {
+            store(cl[0], claims_out[0].b);
+            store(cl[1], claims_out[1].b);
+        }
+        if (aux_out) {
+            store(ld(pa + 44 + 96ull * m + 32), aux_out[0].b);
+            store(b0, aux_out[1].b);
+        }
+        out_points(rA, m, point_out);
+        if (point_out) out_points(rB, m, point_out + m);
+    });
+}
+
 }  // extern "C"

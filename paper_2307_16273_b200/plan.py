@@ -28,3 +28,15 @@ def is_whole(pad: list, maps: list) -> bool:
 
 
 RELU_ROLES = ("Z", "A", "GA", "GZ")   # the order of zkReLU's points u_Z, u_A, u_GA, u_GZ (D3b)
+
+
+def family_kind(f) -> str:
+    """"matmul", "relu", "loss" or "rescale" for a synth.fcn family record or a device record."""
+    k = getattr(f, "kind", None)
+    if k:
+        return k
+    if getattr(f, "A", None) is not None:
+        return "matmul"
+    if getattr(f, "Zp", None) is not None and getattr(f, "GZ", None) is not None:
+        return "loss"
+    return "relu" if getattr(f, "GA", None) is not None else "rescale"

@@ -143,6 +143,20 @@ def verify_relu_merge(tr: HostTranscript, logD: int, Q: int, R: int, relu_point:
     return dict(point=_ints(pt, m), claim=f[0], weight=f[1])
 
 
+def verify_rescale(tr: HostTranscript, proof: bytes, shape, points: list) -> dict:
+    """zk_verify_rescale (D26) for shape = (logD, Q, R) at the given points (u_Z, u_P).  Returns dict(claims =
+    [Z~(u_Z), Z'~(u_P)], aux = [aux~(r_A), aux~(r_B)], rA, rB) from the verified proof."""
+    logD, Q, R = (int(v) for v in shape)
+    if not (1 <= logD <= 40 and 1 <= Q <= 32 and 1 <= R <= 32 and Q + R <= 32):
+        raise ValueError("bad rescale shape")
+    m = max(0, (Q + R - 1).bit_length()) + logD
+    cl, aux, pt = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64), ctypes.create_string_buffer(64 * m)
+    _run("rescale", lib().zk_verify_rescale, tr.st, proof, len(proof), (ctypes.c_uint32 * 3)(logD, Q, R),
+         _fr([x for u in points for x in u]), cl, aux, pt)
+    p2 = _ints(pt, 2 * m)
+    return dict(claims=_ints(cl, 2), aux=_ints(aux, 2), rA=p2[:m], rB=p2[m:])
+
+
 def verify_claim_merge(tr: HostTranscript, n: int, d: int, claims: list, proof: bytes) -> tuple:
     """zk_verify_claim_merge (D25).  claims: dicts(map, v (d elements), u (log2 len(map)), c).
     Returns (point (d + n), claim): the one claim left on the stack."""
@@ -230,11 +244,13 @@ def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: l
     its Z, A, G_A, G_Z stacks and its four claims must EQUAL the merged claims (nothing unbound); its aux
     merge gives the aux claim.  Returns {tensor family: (point, value)} for every committed stack and
     {"aux:<ReLU>": (point over (j, i, s), value)} — exactly the claims left for the commitments."""
-    from .plan import RELU_ROLES, is_whole, matmul_claim_pieces
+    from .plan import RELU_ROLES, family_kind, is_whole, matmul_claim_pieces
     W = HostTranscript(seed=seed)
     W.absorb("fcn/chdr", header)
-    mms = [f for f in families if getattr(f, "A", None) is not None]
-    relus = [f for f in families if getattr(f, "A", None) is None]
+    mms = [f for f in families if family_kind(f) == "matmul"]
+    losses = [f for f in families if family_kind(f) == "loss"]
+    relus = [f for f in families if family_kind(f) == "relu"]
+    rescales = [f for f in families if family_kind(f) == "rescale"]
 
     def refs(f):
         return {k: (v.tensor, list(v.map)) if hasattr(v, "tensor") else (v[0], list(v[1])) for k, v in f.refs.items()}
@@ -243,7 +259,7 @@ def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: l
         return list(t.pad) if hasattr(t, "pad") else [s is None for s in t.slots]
 
     kids = []
-    for f in mms:
+    for f in mms + losses:
         W.absorb("fcn/fam", f.name.encode())
         kids.append(W.fork("fcn/fork"))
     claims = {t.name: [] for t in tensors}
@@ -261,6 +277,17 @@ def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: l
             tname, mp = rf[role]
             claims[tname].append(dict(map=mp, v=[x for p in vp for x in val[p]], u=[x for p in up for x in val[p]],
                                       c=val[cp][0]))
+    for f, T in zip(losses, kids[len(mms):]):
+        r = res["loss"][f.name]
+        n = int(f.GZ.size if not callable(f.GZ.size) else f.GZ.numel())
+        d = int(f.GZ.shape[1] * f.GZ.shape[2]).bit_length() - 1
+        u = verify_loss_grad(T, n.bit_length() - 1, r["claims"])
+        if T.state() != r["state"]:
+            raise Rejected(f"family {f.name} transcript state", -3)
+        rf = refs(f)
+        for role, c in zip(("GZ", "Zp", "Y"), r["claims"]):
+            tname, mp = rf[role]
+            claims[tname].append(dict(map=mp, v=u[:d], u=u[d:], c=c))
     for T in kids:
         W.absorb("fcn/join", T.state())
     opened = {}
@@ -289,9 +316,26 @@ def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: l
     for T in kids2:
         W.absorb("fcn/join", T.state())
     kids3 = []
-    for f in relus:
+    for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
         kids3.append(W.fork("fcn/fork"))
+    for f, T in zip(rescales, kids3[len(relus):]):
+        r = res["rescale"][f.name]
+        names = [f.tensors["Z"], f.tensors["Zp"]]
+        if any(nm not in opened for nm in names):
+            raise Rejected(f"{f.name}: a rescale-bound stack without a claim", -4)
+        n = int(f.Z.size if not callable(f.Z.size) else f.Z.numel())
+        logB = max(0, (f.Q + f.R - 1).bit_length())
+        v = verify_rescale(T, r["proof"], (n.bit_length() - 1, f.Q, f.R), [opened[nm][0] for nm in names])
+        if v["claims"] != [opened[nm][1] for nm in names]:
+            raise Rejected(f"{f.name}: rescale claims differ from the window's claims", -1)
+        aux = [dict(map=[0], u=[], v=v["rA"], c=v["aux"][0]), dict(map=[0], u=[], v=v["rB"], c=v["aux"][1])]
+        pt, cl = verify_claim_merge(T, 0, (n.bit_length() - 1) + logB, aux, r["aux_merge"]["proof"])
+        if T.state() != r["state"]:
+            raise Rejected(f"family {f.name} transcript state", -3)
+        for nm in names:
+            del opened[nm]
+        opened["aux:" + f.name] = (pt, cl)
     for f, T in zip(relus, kids3):
         r = res["relu"][f.name]
         names = [f.tensors[k] for k in RELU_ROLES]

@@ -75,6 +75,8 @@ class StepTrace:
     GZ: list = field(default_factory=list)   # G_Z[l] for l=1..L
     GA: list = field(default_factory=list)   # G_A[l] for l=1..L-1
     GW: list = field(default_factory=list)   # G_W[l] [d_l, d_{l-1}] for l=1..L
+    Zp: np.ndarray = None                     # round(Z^(L) / 2^R) (D16) [B, d_L]
+    Y: np.ndarray = None                      # labels: Zp - G_Z^(L) [B, d_L]
 
 
 def _pad_mask(shape: FcnShape, l: int):
@@ -128,6 +130,8 @@ def generate_trace(shape: FcnShape, seed: int = DATA_SEED, x_bits=11, w_bits=12,
         tr.GZ = [None] + [_to_i32(g, "G_Z") for g in GZ[1:]]
         tr.GA = [None] + [_to_i32(GA[l], "G_A") for l in range(1, L)]
         tr.GW = [None] + [_to_i32(g, "G_W") for g in GW[1:]]
+        tr.Zp = _to_i32(_round_half_up(Z[L], R_BITS), "Z'^L")
+        tr.Y = _to_i32(tr.Zp.astype(np.int64) - GZ[L], "Y")
         steps.append(tr)
         for l in range(1, L + 1):
             W[l] = W[l] - _round_half_up(GW[l].T.astype(np.int64), LR_SHIFT)
@@ -251,6 +255,45 @@ def assemble_families(shape: FcnShape, trace):
     return fam
 
 
+@dataclass
+class LossFamily:
+    """Eq. (fcnn-GZ-last) at the activations' scale (D16): G_Z^(L) = Z^(L)' - Y, stacked over the
+    window's steps (D24); GZ, Zp, Y: [N][B][d_L]."""
+    name: str
+    GZ: np.ndarray
+    Zp: np.ndarray
+    Y: np.ndarray
+    insts: list = field(default_factory=list)
+    refs: dict = field(default_factory=dict)    # plan_window: "GZ" / "Zp" / "Y" -> TensorRef
+
+
+@dataclass
+class RescaleFamily:
+    """The top layer's Z^(L) = 2^R Z^(L)' + R_Z, proved through the bits of Z^(L) (DESIGN.md D26);
+    Z: the stacked Z^(L) flattened, [N * B * d_L]."""
+    name: str
+    Z: np.ndarray
+    Q: int
+    R: int
+    insts: list = field(default_factory=list)
+    tensors: dict = field(default_factory=dict)  # plan_window: "Z" -> "Zout", "Zp" -> "Zp"
+
+
+def assemble_top_families(shape: FcnShape, trace, families: list) -> list:
+    """The loss-gradient and rescale families of the top layer (N2), stacked over the steps like every
+    family; the G_Z^(L) stack is the one the GA family of the top layer already holds."""
+    L = len(shape.dims) - 1
+    insts = [(s, L) for s in range(shape.steps)]
+    N = _next_pow2(len(insts))
+    ga_top = next((f for f in families if f.name.startswith("GA[") and max(l for _, l in f.insts) == L - 1), None)
+    gz = ga_top.A if ga_top is not None and ga_top.A.shape[0] == N else _stack([trace[s].GZ[L] for s, _ in insts], N)
+    zp = _stack([trace[s].Zp for s, _ in insts], N)
+    y = _stack([trace[s].Y for s, _ in insts], N)
+    f_top = next((f for f in families if f.name.startswith("F[") and max(l for _, l in f.insts) == L), None)
+    z = f_top.Y if f_top is not None and f_top.Y.shape[0] == N else _stack([trace[s].Z[L] for s, _ in insts], N)
+    return [LossFamily(f"Loss[{L}]", gz, zp, y, insts), RescaleFamily(f"Rescale[{L}]", z.reshape(-1), Q_BITS, R_BITS, insts)]
+
+
 def fcn_header(shape: FcnShape) -> bytes:
     """Bytes absorbed under tag "fcn/hdr" before the first family (D3d)."""
     words = [len(shape.dims) - 1, shape.batch, shape.steps] + list(shape.dims)
@@ -289,14 +332,16 @@ def _kind(field_: str, l: int, L: int) -> str:
     return field_                      # GA (hidden only), W, GW
 
 
-def plan_window(shape: FcnShape, trace, families: list) -> list:
+def plan_window(shape: FcnShape, trace, families: list, top: list | None = None) -> list:
     """Tensor families of a window and the views the operation families take of them (input structure
     only: which stored tensor each stack slot is).  Sets f.refs (matmul families: roles "A", "B", "Y")
     and f.tensors (ReLU families) and returns the tensor families in a fixed order: X, then per ReLU
     family its Z, A, G_A, G_Z, then Zout, GZout, W and GW groups (in family order)."""
     L = len(shape.dims) - 1
-    relus = [f for f in families if not hasattr(f, "A")]
+    relus = [f for f in families if isinstance(f, ReluFamily)]
     mms = [f for f in families if hasattr(f, "A")]
+    loss = next((f for f in (top or []) if isinstance(f, LossFamily)), None)
+    resc = next((f for f in (top or []) if isinstance(f, RescaleFamily)), None)
     tf = {}
     order = []
 
@@ -351,8 +396,17 @@ def plan_window(shape: FcnShape, trace, families: list) -> list:
     fL = first(lambda f: f.name.startswith("F[") and max(l for _, l in f.insts) == L)
     gL = first(lambda f: f.name.startswith("GA[") and max(l for _, l in f.insts) == L - 1)
     za, ga = same(zs, fL, "Y"), same(zs, gL, "A")
-    add("Zout", "Zout", zs, B, shape.dims[L], array=za if za is not None else stack("Z", zs, B, shape.dims[L]))
+    add("Zout", "Zout", zs, B, shape.dims[L], array=za if za is not None else stack("Z", zs, B, shape.dims[L]),
+        relu=resc.name if resc is not None else None)
     add("GZout", "GZout", zs, B, shape.dims[L], array=ga if ga is not None else stack("GZ", zs, B, shape.dims[L]))
+    if loss is not None:   # the top layer's rescaled output (bound by the rescale's aux) and the labels
+        add("Zp", "Zp", zs, B, shape.dims[L], relu=resc.name if resc is not None else None,
+            array=loss.Zp if resc is None else None)
+        add("Y", "Y", zs, B, shape.dims[L], array=loss.Y)
+        loss.refs = {"GZ": TensorRef("GZout", list(range(len(zs)))), "Zp": TensorRef("Zp", list(range(len(zs)))),
+                     "Y": TensorRef("Y", list(range(len(zs))))}
+    if resc is not None:
+        resc.tensors = {"Z": "Zout", "Zp": "Zp"}
     for f in mms:
         if f.name.startswith("F["):
             ls = sorted({l for _, l in f.insts})

@@ -30,7 +30,15 @@ def O():
     return oracle
 
 
-def _compare(g, o, fams):
+def _compare(g, o, fams, top=()):
+    for f in top:
+        if hasattr(f, "Y"):
+            a, b = g["loss"][f.name], o["matmul"][f.name]
+            assert a["u"] == b["u"] and a["claims"] == b["claims"] and a["state"] == b["state"], f.name
+        else:
+            a, b = g["rescale"][f.name], o["relu"][f.name]
+            assert a["state"] == b["state"], f.name
+            assert a["aux_merge"]["point"] == b["aux_merge"]["point"] and a["aux_merge"]["claim"] == b["aux_merge"]["claim"]
     for f in fams:
         if hasattr(f, "A"):
             a, b = g["matmul"][f.name], o["matmul"][f.name]
@@ -50,14 +58,15 @@ def _run(ctx, O, shape, seed_name, streams, x_bits=11, w_bits=12, y_bits=10, ful
     from synth import fcn
     trace = fcn.generate_trace(shape, seed=DATA_SEED, x_bits=x_bits, w_bits=w_bits, y_bits=y_bits)
     fams = fcn.assemble_families(shape, trace)
-    tensors = fcn.plan_window(shape, trace, fams)
-    dfams, dts = chain.upload_plan(fams, tensors)
+    top = fcn.assemble_top_families(shape, trace, fams)
+    tensors = fcn.plan_window(shape, trace, fams, top)
+    dfams, dts = chain.upload_plan(fams, tensors, top=top)
     relu_ctx = api.Context(0, torch.cuda.Stream()) if streams else None
     mm = [api.Context(0, torch.cuda.Stream()) for _ in range(streams)]
     g = chain.prove_window_chained(ctx, fs_seed(seed_name), fcn.fcn_header(shape), dfams, dts, relu_ctx=relu_ctx,
                                    mm_ctxs=mm)
-    opened = verify.verify_window_chained(fs_seed(seed_name), fcn.fcn_header(shape), fams, tensors, g)
-    return fams, tensors, g, opened
+    opened = verify.verify_window_chained(fs_seed(seed_name), fcn.fcn_header(shape), fams + top, tensors, g)
+    return fams, top, tensors, g, opened
 
 
 def test_chained_window_tiny_vs_oracle(ctx, O):
@@ -67,9 +76,9 @@ def test_chained_window_tiny_vs_oracle(ctx, O):
     from synth import fcn
     shape = fcn.tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4)
     for streams in (0, 2):
-        fams, tensors, g, opened = _run(ctx, O, shape, "chain-tiny", streams, x_bits=4, w_bits=4, y_bits=3)
-        o = drivers.fcn_prove_chained(shape, fams, tensors, "chain-tiny")
-        _compare(g, o, fams)
+        fams, top, tensors, g, opened = _run(ctx, O, shape, "chain-tiny", streams, x_bits=4, w_bits=4, y_bits=3)
+        o = drivers.fcn_prove_chained(shape, fams, tensors, "chain-tiny", top=top)
+        _compare(g, o, fams, top)
         for f in fams:
             if not hasattr(f, "A"):
                 a, b = g["relu"][f.name], o["relu"][f.name]
@@ -85,9 +94,9 @@ def test_chained_window_mid_vs_oracle(ctx, O, layers, width):
     from oracle import drivers
     from synth import fcn
     shape = fcn.tiny_shape(steps=2, layers=layers, width=width, batch=16, din=width * 2, dout=16)
-    fams, tensors, g, opened = _run(ctx, O, shape, f"chain-{layers}-{width}", 2)
-    o = drivers.fcn_prove_chained(shape, fams, tensors, f"chain-{layers}-{width}")
-    _compare(g, o, fams)
+    fams, top, tensors, g, opened = _run(ctx, O, shape, f"chain-{layers}-{width}", 2)
+    o = drivers.fcn_prove_chained(shape, fams, tensors, f"chain-{layers}-{width}", top=top)
+    _compare(g, o, fams, top)
     for f in fams:
         if not hasattr(f, "A"):
             assert g["relu"][f.name]["msgs"] == o["relu"][f.name]["msgs"]
@@ -104,15 +113,16 @@ def test_chained_window_full_size(ctx, O, cfg):
     from oracle import drivers
     from synth import fcn
     shape = fcn.C4_SHAPE if cfg == "C4" else fcn.C3_SHAPE
-    fams, tensors, g, opened = _run(ctx, O, shape, f"{cfg}-chained", 2)
-    # the oracle: stage 1 and 2 in full (drivers' functions with the dense zkReLU left out), then the
-    # zkReLU through the oracle's verifier at the merged points
+    fams, top, tensors, g, opened = _run(ctx, O, shape, f"{cfg}-chained", 2)
+    # the oracle: stages 1 and 2 in full (the driver's pieces), then the zkReLU through the oracle's verifier
+    # at the merged points (the dense oracle zkReLU of 2^28 entries is out of reach), the rescale in full
     import oracle as Ol
     W = Ol.Transcript(fs_seed(f"{cfg}-chained"))
     W.absorb("fcn/chdr", fcn.fcn_header(shape))
     mms = [f for f in fams if hasattr(f, "A")]
+    loss, resc = top
     kids = []
-    for f in mms:
+    for f in mms + [loss]:
         W.absorb("fcn/fam", f.name.encode())
         kids.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
     om = {}
@@ -120,35 +130,57 @@ def test_chained_window_full_size(ctx, O, cfg):
         r = Ol.matmul_prove(T, f.A, f.B, f.transA, f.transB)
         r["state"] = T.state()
         om[f.name] = r
-    _compare(dict(matmul=g["matmul"], merges={}), dict(matmul=om, merges={}), fams)
+    ol = Ol.loss_grad_prove(kids[-1], loss.GZ, loss.Zp, loss.Y)
+    ol["state"] = kids[-1].state()
+    _compare(dict(matmul=g["matmul"], merges={}, loss=g["loss"]), dict(matmul=dict(om, **{loss.name: ol}), merges={}),
+             fams, [loss])
     for T in kids:
         W.absorb("fcn/join", T.state())
     claims = {t.name: [] for t in tensors}
     for f in mms:
         for role, ref, v, u, c in drivers._matmul_family_claims(f, om[f.name]):
             claims[ref.tensor].append(dict(map=list(ref.map), u=list(u), v=list(v), c=c))
+    for role, ref, v, u, c in drivers._loss_family_claims(loss, ol):
+        claims[ref.tensor].append(dict(map=list(ref.map), u=list(u), v=list(v), c=c))
     merged = [t for t in tensors if claims[t.name] and not drivers._is_whole(t, claims[t.name])]
     assert sorted(t.name for t in merged) == sorted(g["merges"])
     mk = []
     for t in merged:
         W.absorb("fcn/tfam", t.name.encode())
         mk.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    one = {}
+    for t in tensors:
+        if claims[t.name] and t not in merged:
+            one[t.name] = (claims[t.name][0]["v"] + claims[t.name][0]["u"], claims[t.name][0]["c"])
     for t, T in zip(merged, mk):
-        r = Ol.claim_merge_prove(T, drivers._tensor_values(t, fams), claims[t.name])
+        r = Ol.claim_merge_prove(T, drivers._tensor_values(t, fams + top), claims[t.name])
         a = g["merges"][t.name]
         assert a["A"]["msgs"] == r["A"]["msgs"] and a["B"]["msgs"] == r["B"]["msgs"], t.name
         assert a["point"] == r["point"] and a["claim"] == r["claim"] and a["state"] == T.state(), t.name
+        one[t.name] = (r["point"], r["claim"])
     for T in mk:
         W.absorb("fcn/join", T.state())
-    for f in fams:
-        if hasattr(f, "A"):
-            continue
+    for f in [f for f in fams if not hasattr(f, "A")] + [resc]:
         W.absorb("fcn/fam", f.name.encode())
         T = Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little"))
+        if f is resc:
+            r = Ol.rescale_prove(T, f.Z, f.Q, f.R, [one[f.tensors["Z"]][0], one[f.tensors["Zp"]][0]])
+            assert r["claims"] == [one[f.tensors["Z"]][1], one[f.tensors["Zp"]][1]]
+            logB = Ol.relu_logB(f.Q, f.R)
+            bits = ((f.Z.astype(np.int64).reshape(-1, 1) & 0xFFFFFFFF) >> np.arange(1 << logB)) & 1
+            bits[:, f.Q + f.R:] = 0
+            am = Ol.claim_merge_prove(T, np.ascontiguousarray(bits.astype(np.int32).reshape(1, -1)),
+                                      [dict(map=[0], u=[], v=r["A"]["r"], c=r["A"]["finals"][1]),
+                                       dict(map=[0], u=[], v=r["B"]["r"], c=r["B"]["finals"][0])])
+            ga = g["rescale"][f.name]
+            assert ga["aux_merge"]["point"] == am["point"] and ga["aux_merge"]["claim"] == am["claim"]
+            assert ga["state"] == T.state()
+            W.absorb("fcn/join", T.state())
+            continue
         gr = g["relu"][f.name]
-        pts = [g["merges"][f.tensors[k]]["point"] for k in ("Z", "A", "GA", "GZ")]
+        pts = [one[f.tensors[k]][0] for k in ("Z", "A", "GA", "GZ")]
         assert Ol.relu_verify(T, f.Z, f.GA, f.Q, f.R, gr["claims"], gr["msgs"], gr["finals"], points=pts) == 0
-        assert gr["claims"] == [g["merges"][f.tensors[k]]["claim"] for k in ("Z", "A", "GA", "GZ")]
+        assert gr["claims"] == [one[f.tensors[k]][1] for k in ("Z", "A", "GA", "GZ")]
         rho = T.challenges("relu/merge", 1)[0]
         f0, f1, f2 = gr["finals"]
         assert gr["merge"]["claim"] == (f0 + rho * f1 + rho * rho * f2) % P

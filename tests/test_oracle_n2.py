@@ -7,6 +7,7 @@ multilinear extension evaluated by Python-int brute force; tampering with one en
 the first identity.
 """
 import numpy as np
+import pytest
 
 from synth.prng import fs_seed, uniform_range
 
@@ -100,3 +101,87 @@ def test_loss_grad_claims_brute_force_and_linearity(oracle_lib):
         Gb[(1 << m) - 1] += 1
         gb = O.loss_grad_prove(O.Transcript(seed), Gb, Z, Y)["claims"][0]
         assert gb != (z - y) % P
+
+
+# ---------------------------------------------------------------- the top-layer rescale (D26)
+def _beta_pt(u, v):
+    e = 1
+    for a, b in zip(u, v):
+        e = e * (a * b + (1 - a) * (1 - b)) % P
+    return e
+
+
+def _lag(ev, x):
+    K = len(ev) - 1
+    tot = 0
+    for i in range(K + 1):
+        num, den = 1, 1
+        for j in range(K + 1):
+            if j != i:
+                num, den = num * (x - j) % P, den * (i - j) % P
+        tot += ev[i] * num * pow(den, -1, P)
+    return tot % P
+
+
+def _rescale_check(Z, Q, R, pts, res, claims=None):
+    """D26 verifier in Python integers: A's and B's round identities, A's weight final recomputed, B's
+    second final = first - 1, both aux finals = brute-force MLEs of the bits of Z."""
+    D = len(Z)
+    logD = D.bit_length() - 1
+    QR = Q + R
+    logB = (QR - 1).bit_length()
+    Bc = 1 << logB
+    cz, cp = res["claims"] if claims is None else claims
+    r = res["r"]
+    c = (r * cz + cp) % P
+    A = res["A"]
+    for ev, x in zip(A["msgs"], A["r"]):
+        assert (ev[0] + ev[1]) % P == c, "A round"
+        c = _lag(ev, x)
+    assert c == A["finals"][0] * A["finals"][1] % P
+    rj, ri = A["r"][:logB], A["r"][logB:]
+    s = [1 << j for j in range(QR - 1)] + [-(1 << (QR - 1))] + [0] * (Bc - QR)
+    sp = [0] * (R - 1) + [1] + [1 << k for k in range(Q - 1)] + [-(1 << (Q - 1))] + [0] * (Bc - QR)
+    sw, spw = mle([x % P for x in s], rj), mle([x % P for x in sp], rj)
+    assert A["finals"][0] == (r * _beta_pt(pts[0], ri) * sw + _beta_pt(pts[1], ri) * spw) % P, "W final"
+    bits = [((int(z) & 0xFFFFFFFF) >> j) & 1 if j < QR else 0 for z in Z for j in range(Bc)]
+    assert A["finals"][1] == mle(bits, A["r"])
+    B = res["B"]
+    c, w = 0, res["w"]
+    for t, (ev, x) in enumerate(zip(B["msgs"], B["r"])):
+        assert ((1 - w[t]) * ev[0] + w[t] * ev[1]) % P == c, "B round"
+        c = _lag(ev, x)
+    assert c == B["finals"][0] * B["finals"][1] % P
+    assert B["finals"][1] == (B["finals"][0] - 1) % P
+    assert B["finals"][0] == mle(bits, B["r"])
+
+
+@pytest.mark.parametrize("Q,R,logD", [(4, 2, 3), (16, 16, 4), (8, 8, 5)])
+def test_rescale_claims_identities_and_finals(oracle_lib, Q, R, logD):
+    import random
+    O = oracle_lib
+    rng = random.Random(logD * 7 + Q)
+    half = 1 << (Q + R - 1)
+    Z = uniform_range(45, logD, (1 << logD,), -half, half)
+    Z[0], Z[1] = half - 1, -half                    # both ends of the range (the D11 edge included)
+    pts = [[rng.randrange(P) for _ in range(logD)] for _ in range(2)]
+    res = O.rescale_prove(O.Transcript(bytes(32)), Z, Q, R, pts)
+    Zp = [(int(z) + (1 << (R - 1))) >> R for z in Z]   # round(Z / 2^R), half-up (D9)
+    assert res["claims"] == [mle(Z, pts[0]), mle(Zp, pts[1])]
+    _rescale_check(Z, Q, R, pts, res)
+
+
+def test_rescale_rejects_other_rounding(oracle_lib):
+    """A claim on round-toward-zero (or floor) instead of the half-up Z' of D9 fails A's first round."""
+    import random
+    O = oracle_lib
+    rng = random.Random(9)
+    Q, R, logD = 4, 2, 4
+    Z = np.array([-7, -6, -5, -3, -2, -1, 0, 1, 2, 3, 5, 6, 7, 9, 10, 13], dtype=np.int32)
+    pts = [[rng.randrange(P) for _ in range(logD)] for _ in range(2)]
+    res = O.rescale_prove(O.Transcript(bytes(32)), Z, Q, R, pts)
+    trunc = [int(np.trunc(int(z) / 4)) for z in Z]
+    floor_ = [int(z) >> R for z in Z]
+    for other in (trunc, floor_):
+        with pytest.raises(AssertionError):
+            _rescale_check(Z, Q, R, pts, res, claims=[res["claims"][0], mle(other, pts[1])])

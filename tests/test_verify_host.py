@@ -234,10 +234,32 @@ def test_loss_grad_verifier(V, oracle_lib):
     assert e.value.where == -100
 
 
-def _chained_results(o, fams, tensors):
+def _merge_proof(mr):
+    A, B = mr["A"], mr["B"]
+    cA = sum(rh * c["c"] for rh, c in zip(mr["rho"], mr["claims_in"])) % P
+    return (u32s(len(A["r"]), 0, 2) + frs([cA]) + frs([v for row in A["msgs"] for v in row]) + frs(A["finals"]) +
+            u32s(len(B["r"]), 0, 2) + frs([A["finals"][1]]) + frs([v for row in B["msgs"] for v in row]) +
+            frs(B["finals"]))
+
+
+def _chained_results(o, fams, tensors, top=()):
     """The oracle's chained window in the device driver's result layout (proof bytes)."""
-    from paper_2307_16273_b200.api import relu_logB
-    res = dict(matmul={}, merges={}, relu={}, window_state=o["window_state"])
+    res = dict(matmul={}, merges={}, relu={}, loss={}, rescale={}, window_state=o["window_state"])
+    for f in top:
+        r = dict(o["matmul"].get(f.name) or o["relu"][f.name])
+        if hasattr(f, "Y"):
+            res["loss"][f.name] = dict(u=r["u"], claims=r["claims"], state=r["state"])
+        else:
+            logD = int(f.Z.size).bit_length() - 1
+            A, B = r["A"], r["B"]
+            proof = (u32s(logD, f.Q, f.R) + frs(r["claims"]) +
+                     u32s(len(A["r"]), 0, 2) + frs([(r["r"] * r["claims"][0] + r["claims"][1]) % P]) +
+                     frs([v for row in A["msgs"] for v in row]) + frs(A["finals"]) +
+                     u32s(len(B["r"]), len(B["r"]), 2) + frs([0]) + frs([v for row in B["msgs"] for v in row]) +
+                     frs(B["finals"]))
+            am = dict(r["aux_merge"])
+            am["claims_in"] = [dict(c=A["finals"][1]), dict(c=B["finals"][0])]
+            res["rescale"][f.name] = dict(proof=proof, aux_merge=dict(proof=_merge_proof(am)), state=r["state"])
     for f in fams:
         if hasattr(f, "A"):
             r = dict(o["matmul"][f.name])
@@ -253,12 +275,7 @@ def _chained_results(o, fams, tensors):
                               frs([v for row in mg["msgs"] for v in row]) + frs(mg["finals"]))
             res["relu"][f.name] = r
     for name, mr in o["merges"].items():
-        A, B = mr["A"], mr["B"]
-        cA = sum(rh * c["c"] for rh, c in zip(mr["rho"], mr["claims_in"])) % P
-        proof = (u32s(len(A["r"]), 0, 2) + frs([cA]) + frs([v for row in A["msgs"] for v in row]) + frs(A["finals"]) +
-                 u32s(len(B["r"]), 0, 2) + frs([A["finals"][1]]) + frs([v for row in B["msgs"] for v in row]) +
-                 frs(B["finals"]))
-        res["merges"][name] = dict(mr, proof=proof)
+        res["merges"][name] = dict(mr, proof=_merge_proof(mr))
     return res
 
 
@@ -287,21 +304,28 @@ def test_chained_window_verifier_on_oracle_window(V, oracle_lib):
     shape = fcn.tiny_shape(steps=2, layers=3, width=8, batch=4, din=8, dout=4)
     trace = fcn.generate_trace(shape, x_bits=4, w_bits=4, y_bits=3)
     fams = fcn.assemble_families(shape, trace)
-    tensors = fcn.plan_window(shape, trace, fams)
-    o = drivers.fcn_prove_chained(shape, fams, tensors, "vchain")
-    res = _chained_results(o, fams, tensors)
+    top = fcn.assemble_top_families(shape, trace, fams)
+    tensors = fcn.plan_window(shape, trace, fams, top)
+    o = drivers.fcn_prove_chained(shape, fams, tensors, "vchain", top=top)
+    res = _chained_results(o, fams, tensors, top)
     hdr = fcn.fcn_header(shape)
-    opened = V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, res)
+    opened = V.verify_window_chained(fs_seed("vchain"), hdr, fams + top, tensors, res)
     assert opened == o["opened"]
     committed = [t for t in tensors if t.relu is None]
     relus = [f for f in fams if not hasattr(f, "A")]
-    assert sorted(opened) == sorted([t.name for t in committed] + ["aux:" + f.name for f in relus])
+    assert sorted(opened) == sorted([t.name for t in committed] + ["aux:" + f.name for f in relus + top[1:]])
+    assert "Y" in opened and "Zout" not in opened and "Zp" not in opened      # the labels are data; Z^(L), Z' bound
     for t in committed:
         pt, val = opened[t.name]
         assert val == O.mle_i32(t.array.reshape(-1), pt), t.name
     for f in relus:
         pt, val = opened["aux:" + f.name]
         assert val == _aux_mle(f, pt)
+    rs = top[1]                                  # the rescale's aux: the bits of Z^(L), [D][B]
+    pt, val = opened["aux:" + rs.name]
+    QR = rs.Q + rs.R
+    bits = [((int(z) & 0xFFFFFFFF) >> j) & 1 if j < QR else 0 for z in rs.Z for j in range(32)]
+    assert val == O.mle_fr(bits, pt)
     # a zkReLU proof whose claims are not the merged ones (a different Z claim) is rejected
     bad = dict(res, relu=dict(res["relu"]))
     f = relus[0]
@@ -311,7 +335,7 @@ def test_chained_window_verifier_on_oracle_window(V, oracle_lib):
     rr["proof"] = bytes(pb)
     bad["relu"][f.name] = rr
     with pytest.raises(V.Rejected):
-        V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, bad)
+        V.verify_window_chained(fs_seed("vchain"), hdr, fams + top, tensors, bad)
     # a merge proof for other claims, and a missing merge
     name = next(iter(res["merges"]))
     bad = dict(res, merges=dict(res["merges"]))
@@ -319,7 +343,7 @@ def test_chained_window_verifier_on_oracle_window(V, oracle_lib):
     mb[20] ^= 1
     bad["merges"][name] = dict(bad["merges"][name], proof=bytes(mb))
     with pytest.raises(V.Rejected):
-        V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, bad)
+        V.verify_window_chained(fs_seed("vchain"), hdr, fams + top, tensors, bad)
     bad = dict(res, merges={k: v for k, v in res["merges"].items() if k != name})
     with pytest.raises(V.Rejected):
-        V.verify_window_chained(fs_seed("vchain"), hdr, fams, tensors, bad)
+        V.verify_window_chained(fs_seed("vchain"), hdr, fams + top, tensors, bad)
