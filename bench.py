@@ -525,7 +525,8 @@ def c5_measure(ctx, rank: int, world: int, m: int, steps: int, warmup: int, swit
     n_loc = 1 << (m - s)
     A = uniform_range_torch(DATA_SEED, 21, n_loc, -(1 << 15), 1 << 15, dev, offset=rank * n_loc)
     B = uniform_range_torch(DATA_SEED, 22, n_loc, -(1 << 15), 1 << 15, dev, offset=rank * n_loc)
-    comm = shard.TorchComm() if world > 1 else None
+    if world > 1:   # the exchange owned by the library: one NCCL communicator per context
+        shard.attach_nccl(ctx)
     torch.cuda.synchronize()
 
     def one():
@@ -540,7 +541,7 @@ def c5_measure(ctx, rank: int, world: int, m: int, steps: int, warmup: int, swit
             res = api.sumcheck_prove(ctx, tr, m, m, [A, B], w)
         else:
             sess = shard.ShardSession(ctx, tr, m, m, [A, B], w, rank, world)
-            res = shard.prove(sess, comm, switch_log=switch_log)
+            res = shard.prove_nccl(sess, switch_log=switch_log)
             sess.close()
         e1.record(ctx.stream)
         torch.cuda.synchronize()

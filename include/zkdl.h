@@ -221,6 +221,21 @@ uint32_t zk_sc_shard_rounds_done(const zk_sc_shard* sh);
 uint32_t zk_sc_shard_local_log(const zk_sc_shard* sh);
 zk_status zk_sc_shard_export(zk_sc_shard* sh, void* d_out);
 zk_status zk_sc_shard_adopt(zk_sc_shard* sh, const void* d_full);
+/* The exchange owned by the library (the context's NCCL communicator):
+ * zk_nccl_unique_id: rank 0 creates the 128-byte communicator id (the caller broadcasts it, e.g. through
+ *   torch.distributed); ZK_ERR_NCCL when libnccl.so.2 cannot be loaded.
+ * zk_ctx_attach_nccl: every rank creates the communicator of `world` ranks (a power of two) on the
+ *   context's device (collective: all ranks call it); the context owns it (zk_ctx_detach_nccl or
+ *   zk_ctx_destroy frees it).
+ * zk_sc_shard_prove_nccl: every remaining round of a shard created on an attached context with the same
+ *   rank / world: per round this rank's K+1 partials are all-gathered as (K+1)*32 raw bytes (ncclUint8)
+ *   on the context stream, added mod p and put through the transcript step on the device; below
+ *   2^switch_log local entries the folded tables are all-gathered and every rank finishes alone.
+ *   Asynchronous (no host synchronisation); then zk_sc_shard_result. */
+zk_status zk_nccl_unique_id(uint8_t out[128]);
+zk_status zk_ctx_attach_nccl(zk_ctx* ctx, const uint8_t id[128], int rank, int world);
+zk_status zk_ctx_detach_nccl(zk_ctx* ctx);
+zk_status zk_sc_shard_prove_nccl(zk_sc_shard* sh, uint32_t switch_log);
 zk_status zk_sc_shard_result(zk_sc_shard* sh, uint8_t* proof, uint64_t* proof_len, zk_fr* point_out, zk_fr* finals_out,
                              zk_fr* claim_out);
 void zk_sc_shard_free(zk_sc_shard* sh);

@@ -98,6 +98,10 @@ def lib():
         "zk_sc_shard_adopt": ([vp, vp], i32),
         "zk_sc_shard_result": ([vp, vp, c.POINTER(u64), vp, vp, vp], i32),
         "zk_sc_shard_free": ([vp], None),
+        "zk_nccl_unique_id": ([vp], i32),
+        "zk_ctx_attach_nccl": ([vp, vp, i32, i32], i32),
+        "zk_ctx_detach_nccl": ([vp], i32),
+        "zk_sc_shard_prove_nccl": ([vp, u32], i32),
         "zk_diag_fr_op": ([vp, i32, vp, vp, u64, vp], i32),
         "zk_diag_mul_bench": ([vp, vp, u32, u32, vp], i32),
         "zk_diag_rowdot": ([vp, vp, u64, u32, vp, vp, i32], i32),

@@ -596,3 +596,15 @@ def rescale_prove_dev(ctx: Context, tr: Transcript, Z: torch.Tensor, Q: int, R: 
     ctx.check(lib().zk_rescale_prove_dev(ctx.h, tr.h, _dev_ptr(Z, torch.int32), logD, Q, R, _dev_ptr(d_pts, torch.uint8),
                                          out.data_ptr(), ctypes.byref(ln), range_flag.data_ptr()))
     return out
+
+
+def parse_rescale_out(raw: bytes, logD: int, Q: int, R: int) -> dict:
+    m = relu_logB(Q, R) + logD
+    lp = 12 + 32 + 96 * m + 64
+    plen = 12 + 64 + 2 * lp
+    A, B = parse_sumcheck_proof(raw[76:76 + lp]), parse_sumcheck_proof(raw[76 + lp:plen])
+    o = _a16(plen)
+    A["r"] = [int.from_bytes(raw[o + 32 * i:o + 32 * i + 32], "little") for i in range(m)]
+    B["r"] = [int.from_bytes(raw[o + 32 * (m + i):o + 32 * (m + i) + 32], "little") for i in range(m)]
+    claims = [int.from_bytes(raw[12 + 32 * i:44 + 32 * i], "little") for i in range(2)]
+    return dict(claims=claims, A=A, B=B, proof=raw[:plen])

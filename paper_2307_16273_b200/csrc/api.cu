@@ -65,6 +65,7 @@ void zk_ctx_destroy(zk_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    zk_ctx_detach_nccl(ctx);
     delete ctx;
 }
 

@@ -11,10 +11,51 @@
 // challenges agree without a broadcast and the transcript equals the single-device one for every G.
 // When the local slice gets small the folded tables are exported, all-gathered, and the remaining
 // rounds run on every rank from the full tables (continuation: no second header).
+#include <dlfcn.h>
+
+#include <mutex>
+
 #include "sumcheck.cuh"
 #include "tables.cuh"
 
 using namespace zk;
+
+// NCCL, loaded at run time (the library loads without it; the process's libnccl.so.2 — torch's — is used
+// when already loaded).  Only the five entry points the exchange needs; ABI types as in nccl.h.
+namespace {
+struct NcclUid {
+    char internal[128];
+};
+struct Nccl {
+    int (*get_unique_id)(NcclUid*) = nullptr;
+    int (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
+    int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+    int (*comm_destroy)(void*) = nullptr;
+    const char* (*error_string)(int) = nullptr;
+    bool ok = false;
+};
+Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        n.get_unique_id = reinterpret_cast<int (*)(NcclUid*)>(dlsym(h, "ncclGetUniqueId"));
+        n.comm_init_rank = reinterpret_cast<int (*)(void**, int, NcclUid, int)>(dlsym(h, "ncclCommInitRank"));
+        n.all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(dlsym(h, "ncclAllGather"));
+        n.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+        n.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+        n.ok = n.get_unique_id && n.comm_init_rank && n.all_gather && n.comm_destroy && n.error_string;
+    });
+    return n;
+}
+constexpr int NCCL_UINT8 = 1;   // ncclUint8
+#define ZK_NCCL(call)                                                                                  \
+    do {                                                                                               \
+        const int r_ = (call);                                                                         \
+        if (r_ != 0) throw ZkError{ZK_ERR_NCCL, std::string("NCCL: ") + nccl().error_string(r_)};      \
+    } while (0)
+}  // namespace
 
 struct zk_sc_shard {
     zk_ctx* ctx = nullptr;
@@ -218,6 +259,102 @@ zk_status zk_sc_shard_result(zk_sc_shard* sh, uint8_t* proof, uint64_t* proof_le
                                 ctx->stream));
     if (claim_out) ZK_CUDA(cudaMemcpyAsync(claim_out, e.d_proof + 12, 32, cudaMemcpyDeviceToHost, ctx->stream));
     ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+    SH_END
+}
+
+// ---- the exchange owned by the library (SURVEY §8(b) zk_ctx_attach_nccl; north star "allgathers partial
+// round-polynomial coefficients as raw bytes via NCCL, adds them mod p on the device")
+zk_status zk_nccl_unique_id(uint8_t out[128]) {
+    if (!out) return ZK_ERR_ARG;
+    Nccl& n = nccl();
+    if (!n.ok) return ZK_ERR_NCCL;
+    NcclUid id;
+    if (n.get_unique_id(&id) != 0) return ZK_ERR_NCCL;
+    memcpy(out, id.internal, 128);
+    return ZK_OK;
+}
+
+zk_status zk_ctx_attach_nccl(zk_ctx* ctx, const uint8_t id[128], int rank, int world) {
+    if (!ctx) return ZK_ERR_ARG;
+    try {
+        ZK_CUDA(cudaSetDevice(ctx->device));
+        ZK_REQUIRE(id && world >= 1 && rank >= 0 && rank < world && (world & (world - 1)) == 0, ZK_ERR_ARG,
+                   "need 0 <= rank < world, world a power of two");
+        Nccl& n = nccl();
+        ZK_REQUIRE(n.ok, ZK_ERR_NCCL, "libnccl.so.2 not found");
+        if (ctx->nccl_comm) ZK_NCCL(n.comm_destroy(ctx->nccl_comm));
+        ctx->nccl_comm = nullptr;
+        NcclUid uid;
+        memcpy(uid.internal, id, 128);
+        void* comm = nullptr;
+        ZK_NCCL(n.comm_init_rank(&comm, world, uid, rank));
+        ctx->nccl_comm = comm;
+        ctx->nccl_rank = rank;
+        ctx->nccl_world = world;
+    } catch (const ZkError& e) {
+        ctx->err = e.msg;
+        return e.st;
+    }
+    return ZK_OK;
+}
+
+zk_status zk_ctx_detach_nccl(zk_ctx* ctx) {
+    if (!ctx) return ZK_ERR_ARG;
+    if (ctx->nccl_comm) {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        nccl().comm_destroy(ctx->nccl_comm);
+        ctx->nccl_comm = nullptr;
+    }
+    return ZK_OK;
+}
+
+// Every remaining round of a sharded statement with the exchange inside the library: per round the
+// K+1 partials (32-byte elements) are all-gathered as raw bytes (ncclUint8) on the context stream and
+// added mod p on the device with the transcript step; below 2^switch_log local entries the folded
+// tables are all-gathered and every rank finishes alone.  No host synchronisation, no per-round host
+// logic beyond the round counter; collect the proof with zk_sc_shard_result.
+zk_status zk_sc_shard_prove_nccl(zk_sc_shard* sh, uint32_t switch_log) {
+    SH_BEGIN(sh)
+    ZK_REQUIRE(ctx->nccl_comm && ctx->nccl_world == (int)sh->world && ctx->nccl_rank == (int)sh->rank, ZK_ERR_ARG,
+               "context not attached to an NCCL communicator of this shard's rank and world");
+    ScEngine& e = sh->e;
+    Nccl& n = nccl();
+    const uint64_t pbytes = 32ull * (e.K + 1);
+    fr_t* part = sh->s->alloc<fr_t>(e.K + 1);
+    fr_t* all = sh->s->alloc<fr_t>((uint64_t)sh->world * (e.K + 1));
+    while (!sh->done && e.t0 == 0 && e.t < sh->L && (e.L - e.t) > switch_log) {
+        e.round(part);
+        ZK_NCCL(n.all_gather(part, all, pbytes, NCCL_UINT8, ctx->nccl_comm, ctx->stream));
+        e.combine(all, sh->world);
+        if (e.t == e.m) {
+            e.finals();
+            sh->done = true;
+        }
+    }
+    if (!sh->done) {
+        const uint64_t nloc = 1ull << (e.L - e.t);
+        fr_t* loc = sh->s->alloc<fr_t>(e.K * nloc);
+        fr_t* full = sh->s->alloc<fr_t>((uint64_t)sh->world * e.K * nloc);
+        e.materialize();
+        for (uint32_t k = 0; k < e.K; k++)
+            ZK_LAUNCH(ctx, k_fold_copy, grid_for(ctx, nloc, 256, 8), 256, 0, e.cur[k], nloc,
+                      e.t ? e.d_r + (e.t - 1) : nullptr, loc + k * nloc);
+        ZK_NCCL(n.all_gather(loc, full, 32ull * e.K * nloc, NCCL_UINT8, ctx->nccl_comm, ctx->stream));
+        const uint32_t ta = e.t;
+        const uint32_t Lf = e.m - ta;
+        const fr_t* tabs[3] = {nullptr, nullptr, nullptr};
+        for (uint32_t k = 0; k < e.K; k++) {
+            fr_t* t = sh->s->alloc<fr_t>(1ull << Lf);
+            ZK_LAUNCH(ctx, k_unshard, grid_for(ctx, (uint64_t)sh->world * nloc, 256, 8), 256, 0, (const fr_t*)full,
+                      sh->world, e.K, nloc, k, t);
+            tabs[k] = t;
+        }
+        e.d_scale = nullptr;
+        e.setup(tabs, Lf, ta, e.n_eq > ta ? e.n_eq - ta : 0);
+        e.run_to_end();
+        sh->done = true;
+    }
     SH_END
 }
 

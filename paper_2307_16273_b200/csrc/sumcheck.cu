@@ -639,12 +639,15 @@ void ScEngine::setup(const fr_t* const tables[3], uint32_t L_, uint32_t t0_, uin
 }
 
 void ScEngine::set_i32(const int32_t* const src[3]) {
+    // the factored K = 2 kernels take round 0 from int32 tables only when both are int32: one int32 table
+    // next to an Fr table (the rescale's W and aux, D26) is embedded here like the other paths
+    const bool fused = factored && K == 2 && ((src[0] != nullptr) == (src[1] != nullptr));
     for (uint32_t k = 0; k < K; k++) {
         i32[k] = src[k];
-        if (src[k] && !(factored && K == 2))
+        if (src[k] && !fused)
             embed_i32_dev(ctx, src[k], 1ull << L, const_cast<fr_t*>(cur[k]));
     }
-    if (!(factored && K == 2))
+    if (!fused)
         for (uint32_t k = 0; k < 3; k++) i32[k] = nullptr;
 }
 

@@ -2,7 +2,10 @@
 
 Each round the library computes this rank's partial evaluations (zk_sc_shard_partial), the ranks
 all-gather them, and the library adds them and runs the identical transcript step on every rank
-(zk_sc_shard_finish).  Below `switch_log` local entries the folded tables are all-gathered and the
+(zk_sc_shard_finish).  The production path keeps the exchange inside the library: attach_nccl gives the
+context its own NCCL communicator (zk_ctx_attach_nccl, the id broadcast through torch.distributed) and
+prove_nccl runs every round with the all-gathers on the context stream (zk_sc_shard_prove_nccl: no
+per-round Python, no host synchronisation).  Below `switch_log` local entries the folded tables are all-gathered and the
 remaining rounds run on every rank (zk_sc_shard_export / zk_sc_shard_adopt).  The exchange is
 behind a tiny `Comm` interface so the same driver runs over NCCL (one process per GPU), gloo (CPU
 tests of the host logic with a mock backend) or sequential virtual shards on one device.
@@ -134,3 +137,26 @@ def prove_virtual(sessions: list, switch_log: int = 12) -> list:
         for s in sessions:
             s.adopt(full)
     return [s.result() for s in sessions]
+
+
+def attach_nccl(ctx: api.Context, group=None) -> tuple:
+    """Give ctx its own NCCL communicator over the ranks of `group` (collective).  Rank 0 of the group
+    creates the id (zk_nccl_unique_id), torch.distributed broadcasts it, every rank attaches."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [None]
+    if rank == 0:
+        buf = ctypes.create_string_buffer(128)
+        ctx.check(lib().zk_nccl_unique_id(buf))
+        obj[0] = buf.raw[:128]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    ctx.check(lib().zk_ctx_attach_nccl(ctx.h, obj[0], rank, world))
+    return rank, world
+
+
+def prove_nccl(session: ShardSession, switch_log: int = 12) -> dict:
+    """Every remaining round with the library-owned exchange (the session's context attached)."""
+    session.ctx.check(lib().zk_sc_shard_prove_nccl(session.h, switch_log))
+    session.done = True
+    return session.result()

