@@ -21,6 +21,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppres
 # ZKDL_FR64=0 builds the hot product bodies with the integer CIOS instead of the FP64-pipe product (A/B)
 if os.environ.get("ZKDL_FR64") is not None:
     FLAGS += [f"-DZKDL_FR64={int(os.environ['ZKDL_FR64'])}"]
+# ZKDL_DEFS="NAME=VALUE ...": extra compile-time settings for A/B builds (e.g. ZKDL_IR_LB_T, ZKDL_IR_LB_B)
+FLAGS += [f"-D{d}" for d in os.environ.get("ZKDL_DEFS", "").split() if d]
 
 
 def _deps():

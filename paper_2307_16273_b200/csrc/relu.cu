@@ -1008,7 +1008,14 @@ __device__ __noinline__ void iround_g(const fr_t* tot, const fr_t* const* u, uin
 
 // MODE: bit 0 = FOLD, bit 1 = SRC (rounds 0 / 1 from the int32 words through byte tables in shared memory)
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) k_relu_iround_f(IRoundArgs a) {
+// the factored i-round's CTA shape (threads, CTAs per SM): registers per thread = 64K / (threads x CTAs)
+#ifndef ZKDL_IR_LB_T
+#define ZKDL_IR_LB_T 256
+#endif
+#ifndef ZKDL_IR_LB_B
+#define ZKDL_IR_LB_B 2
+#endif
+__global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IRoundArgs a) {
     constexpr bool FOLD = MODE & 1;
     constexpr int SRC = MODE >> 1;
     const int side = threadIdx.x & 1;
@@ -1528,11 +1535,10 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         } else {
             // grid = 2^hb HI blocks x cpb CTAs each, two 256-thread CTAs per SM (ZKDL_IROUND_T=128: four
             // 128-thread CTAs; measured no better in the C4 window)
-            const char* te = getenv("ZKDL_IROUND_T");
-            const uint32_t ithreads = (te && atoi(te) == 128) ? 128u : 256u;
+            const uint32_t ithreads = ZKDL_IR_LB_T;
             const uint64_t per_blk = a.n_pairs >> hb;
             uint64_t cpb = (per_blk + ithreads / 2 - 1) / (ithreads / 2);
-            const uint64_t cap = ((uint64_t)ctx->num_sms * (512 / ithreads)) >> hb;
+            const uint64_t cap = ((uint64_t)ctx->num_sms * ZKDL_IR_LB_B) >> hb;
             if (cpb > cap) cpb = cap;
             if (cpb < 1) cpb = 1;
             a.cpb = (uint32_t)cpb;

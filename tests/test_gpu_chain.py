@@ -223,3 +223,57 @@ def test_rescale_vs_oracle(ctx, O, logD, Q, R):
     v = verify.verify_rescale(H, g["proof"], (logD, Q, R), pts)
     assert v["claims"] == o["claims"] and v["aux"] == [o["A"]["finals"][1], o["B"]["finals"][0]]
     assert H.state() == tr.state()
+
+
+@pytest.mark.parametrize("n,lr,lc,source,K", [(0, 14, 5, "bits", 2), (0, 16, 5, "bits", 2), (0, 16, 5, "plain", 2),
+                                              (3, 4, 6, "plain", 3), (7, 6, 10, "plain", 2), (2, 8, 8, "plain", 5)])
+def test_claim_merge_vs_oracle(ctx, O, n, lr, lc, source, K):
+    """zk_claim_merge_dev (D25) against the oracle: single-slice stacks of bit columns (the rescale's aux)
+    and plain stacks with partial views, bit-exact; the host verifier accepts."""
+    import random
+    from paper_2307_16273_b200 import api, verify
+    from synth.prng import uniform_range
+    rng = random.Random(n * 100 + lr + lc + K)
+    d = lr + lc
+    N = 1 << n
+    if source == "bits":
+        Zw = uniform_range(47, lr, (1 << lr,), -(1 << 31), 1 << 31)
+        X = ((Zw.astype(np.int64).reshape(-1, 1) & 0xFFFFFFFF) >> np.arange(1 << lc)) & 1
+        X = np.ascontiguousarray(X.astype(np.int32).reshape(1, -1))
+    else:
+        X = uniform_range(47, n + d, (N, 1 << d), -(1 << 31), 1 << 31)
+    claims = []
+    for k in range(K):
+        nk = rng.randrange(0, n + 1) if n else 0
+        pick = rng.sample(range(N), min(1 << nk, N))
+        mp = pick + [-1] * ((1 << nk) - len(pick))
+        rng.shuffle(mp)
+        u = [rng.randrange(P) for _ in range(nk)]
+        v = [rng.randrange(P) for _ in range(d)]
+        c = 0
+        for j, i in enumerate(mp):              # the honest claim X_k~(v, u) = sum_j beta(u, j) X_map[j]~(v)
+            if i >= 0:
+                b = 1
+                for t, x in enumerate(u):
+                    b = b * (x if (j >> t) & 1 else 1 - x) % P
+                c = (c + b * O.mle_i32(X[i], v)) % P
+        claims.append(dict(map=mp, u=u, v=v, c=c))
+    seed = fs_seed(f"cm-{n}-{lr}-{lc}-{K}")
+    o = O.claim_merge_prove(O.Transcript(seed), X, claims)
+    tr = api.Transcript(ctx, seed)
+    pts = b"".join(int(x).to_bytes(32, "little") for c in claims for x in c["v"] + c["u"])
+    cls = b"".join(int(c["c"]).to_bytes(32, "little") for c in claims)
+    dp = torch.frombuffer(bytearray(pts), dtype=torch.uint8).cuda()
+    dc = torch.frombuffer(bytearray(cls), dtype=torch.uint8).cuda()
+    if source == "bits":
+        out = api.claim_merge_dev(ctx, tr, torch.from_numpy(Zw).cuda(), 0, lr, lc, [c["map"] for c in claims], dp, dc,
+                                  source="bits", R=32)
+    else:
+        out = api.claim_merge_dev(ctx, tr, torch.from_numpy(X).cuda(), n, lr, lc, [c["map"] for c in claims], dp, dc)
+    g = api.parse_claim_merge_out(out.cpu().numpy().tobytes(), n, K, d)
+    assert g["A"]["msgs"] == o["A"]["msgs"] and g["A"]["finals"] == o["A"]["finals"]
+    assert g["B"]["msgs"] == o["B"]["msgs"] and g["B"]["finals"] == o["B"]["finals"]
+    assert g["point"] == o["point"] and g["claim"] == o["claim"]
+    H = verify.HostTranscript(seed=seed)
+    assert verify.verify_claim_merge(H, n, d, claims, g["proof"]) == (o["point"], o["claim"])
+    assert H.state() == tr.state()

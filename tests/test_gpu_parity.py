@@ -480,9 +480,8 @@ def test_shard_nccl_single_rank(ctx, O):
             s2 = shard.ShardSession(c2, tr2, m, n_eq, [dev(A), dev(B)], w, 0, 1)
             r2 = shard.prove_nccl(s2, switch_log=sw)
             assert r2["msgs"] == o["msgs"] and r2["finals"] == o["finals"] and r2["claim"] == o["claim"]
-            assert tr2.state() == O.Transcript(seed).state() or True
             s2.close()
-        c2.close()
+            tr2.close()
     finally:
         dist.destroy_process_group()
 
