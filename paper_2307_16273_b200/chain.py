@@ -115,8 +115,13 @@ def _fence(src, dsts):
 
 
 def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
-                           relu_ctx: api.Context | None = None, mm_ctxs: list | None = None):
-    """Enqueue one chained window without synchronising; returns a handle for collect_window_chained."""
+                           relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
+                           wctx: api.Context | None = None):
+    """Enqueue one chained window without synchronising; returns a handle for collect_window_chained.
+    Streams: the window transcript W on wctx (default ctx); stages 1-2 over ctx + mm_ctxs; stage 3 on
+    relu_ctx.  Nothing at the end of a window makes the stage 1-2 streams wait for its stage 3 (the
+    child transcripts are freed in collect_window_chained), so with a different wctx per window the
+    next window's matmul families and merges run while this window's zkReLU proves."""
     dev = next(f.A for f in families if f.kind == "matmul").device
     mms = [f for f in families if f.kind == "matmul"]
     losses = [f for f in families if f.kind == "loss"]
@@ -125,7 +130,8 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     tmap = {t.name: t for t in tensors}
     lanes1 = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
     rctx = relu_ctx if relu_ctx is not None else ctx
-    lanes2 = lanes1 + ([rctx] if rctx.stream not in [c.stream for c in lanes1] else [])
+    wctx = wctx if wctx is not None else ctx
+    lanes2 = lanes1
     # ---- layout of the window's output buffer
     off = 0
     lay1 = []
@@ -187,7 +193,7 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         keep.append(g)
         return g
 
-    W = api.Transcript(ctx, seed)
+    W = api.Transcript(wctx, seed)
     W.absorb("fcn/chdr", header)
     # ---- stage 1: the matmul families
     L1 = _Lanes(lanes1)
@@ -200,7 +206,7 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     for i, f in enumerate(mms + losses):
         W.absorb("fcn/fam", f.name.encode())
         kids1.append(W.fork("fcn/fork", home1[i]))
-    _fence(ctx, lanes1)
+    _fence(wctx, lanes1)
     for i, (f, logs, o, n) in enumerate(lay1):
         c, T = home1[i], kids1[i]
         api.matmul_prove(c, T, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
@@ -209,8 +215,8 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         c, T = home1[len(mms) + i], kids1[len(mms) + i]
         api.loss_grad_prove_dev(c, T, f.GZ, f.Zp, f.Y, out=out[o:o + n])
         T.state_dev(out[o + n:o + n + 32])
-    for c in lanes1[1:]:
-        _fence(c, [ctx])
+    for c in lanes1:
+        _fence(c, [wctx])
     for T in kids1:
         W.absorb_state("fcn/join", T)
     # ---- stage 2: one claim per tensor family
@@ -220,7 +226,7 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     for (t, *_), c in zip(lay2, home2):
         W.absorb("fcn/tfam", t.name.encode())
         kids2.append(W.fork("fcn/fork", c))
-    _fence(ctx, lanes2)
+    _fence(wctx, lanes2)
     for (t, n, cl, o, L), c, T in zip(lay2, home2, kids2):
         d_pts = gather(c, [r for x in cl for r in x["v"] + x["u"]])
         d_cl = gather(c, [r for x in cl for r in x["c"]])
@@ -237,8 +243,8 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
             api.claim_merge_dev(c, T, src[1], n, lr, lc, maps, d_pts, d_cl, source=src[0], X2=src[2], R=f.R,
                                 out=out[o:o + L["total"]])
         T.state_dev(out[o + L["total"]:o + L["total"] + 32])
-    for c in lanes2[1:]:
-        _fence(c, [ctx])
+    for c in lanes2:
+        _fence(c, [wctx])
     for T in kids2:
         W.absorb_state("fcn/join", T)
     # ---- stage 3: the chained zkReLU families and their aux merges; the top layer's rescale
@@ -255,7 +261,14 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
         kids3.append(W.fork("fcn/fork", rctx))
-    _fence(ctx, [rctx])
+    _fence(wctx, [rctx])
+    for (f, logD, rn, o, n), T in zip(lay3, kids3):   # the zkReLU first: the window's critical path
+        rngs = [r for role in RELU_ROLES for r in point_ranges(f.tensors[role])]
+        d_pts = gather(rctx, rngs)
+        api.relu_prove_chained_dev(rctx, T, f.Z, f.GA, f.Q, f.R, d_pts, flag, out=out[o:o + rn])
+        mo = o + api._a16(rn)
+        api.relu_merge_dev(rctx, T, f.Z, f.GA, f.Q, f.R, out[o:o + rn], out=out[mo:o + n])
+        T.state_dev(out[o + n:o + n + 32])
     for (f, logD, logB, rl, L, o, n), T in zip(layR, kids3[len(relus):]):
         d_pts = gather(rctx, point_ranges(f.tensors["Z"]) + point_ranges(f.tensors["Zp"]))
         api.rescale_prove_dev(rctx, T, f.Z, f.Q, f.R, d_pts, flag, out=out[o:o + rl])
@@ -269,29 +282,21 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         api.claim_merge_dev(rctx, T, f.Z, 0, logD, logB, [[0], [0]], d_apts, d_acl, source="bits", R=f.Q + f.R,
                             out=out[mo:mo + L["total"]])
         T.state_dev(out[o + n:o + n + 32])
-    for (f, logD, rn, o, n), T in zip(lay3, kids3):
-        rngs = [r for role in RELU_ROLES for r in point_ranges(f.tensors[role])]
-        d_pts = gather(rctx, rngs)
-        api.relu_prove_chained_dev(rctx, T, f.Z, f.GA, f.Q, f.R, d_pts, flag, out=out[o:o + rn])
-        mo = o + api._a16(rn)
-        api.relu_merge_dev(rctx, T, f.Z, f.GA, f.Q, f.R, out[o:o + rn], out=out[mo:o + n])
-        T.state_dev(out[o + n:o + n + 32])
-    _fence(rctx, [ctx])
+    _fence(rctx, [wctx])
     for T in kids3:
         W.absorb_state("fcn/join", T)
     W.state_dev(out[off:off + 32])
-    _fence(ctx, lanes2)      # the children are freed on their own streams: after the joins
-    for T in kids1 + kids2 + kids3:
-        T.close()
-    W.close()
     return dict(out=out, flag=flag, lay1=lay1, layL=layL, lay2=lay2, lay3=lay3, layR=layR, end=off, keep=keep,
-                claims=claims)
+                claims=claims, transcripts=kids1 + kids2 + kids3 + [W])
 
 
 def collect_window_chained(h: dict) -> dict:
     """The one synchronisation: copy the window's outputs back and parse them.  Returns dict(matmul:
     name -> result, merges: tensor name -> result, relu: name -> result, window_state)."""
+    torch.cuda.synchronize(h["out"].device)
     raw = h["out"].cpu().numpy().tobytes()
+    for T in h.pop("transcripts", []):   # every use of the window's transcripts has completed
+        T.close()
     if int(h["flag"].item()) & 1:
         raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")
     res = dict(matmul={}, merges={}, relu={}, loss={}, rescale={})
@@ -321,5 +326,6 @@ def collect_window_chained(h: dict) -> dict:
 
 
 def prove_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
-                         relu_ctx: api.Context | None = None, mm_ctxs: list | None = None) -> dict:
-    return collect_window_chained(enqueue_window_chained(ctx, seed, header, families, tensors, relu_ctx, mm_ctxs))
+                         relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
+                         wctx: api.Context | None = None) -> dict:
+    return collect_window_chained(enqueue_window_chained(ctx, seed, header, families, tensors, relu_ctx, mm_ctxs, wctx))

@@ -167,6 +167,7 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
 def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
     """Copy a window's outputs to the host (the one synchronisation) and parse them.  The last result
     also carries "window_state" (the window transcript after the joins)."""
+    torch.cuda.synchronize(out.device)   # the library wrote on its contexts' streams (ADVICE r1)
     raw = out.cpu().numpy().tobytes()
     if int(flag.item()) & 1:
         raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")

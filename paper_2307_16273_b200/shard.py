@@ -116,12 +116,14 @@ class TorchComm:
 
 
 def prove(session, comm, switch_log: int = 12) -> dict:
-    """Run the sharded protocol for one rank; every rank returns the same proof."""
+    """Run the sharded protocol for one rank; every rank returns the same proof.  The torch collectives
+    are issued on the session's context stream (the partials are written there)."""
     m = session.m
-    while session.rounds_done < m and session.local_log > switch_log:
-        session.finish(comm.allgather(session.partial()))
-    if not session.done:
-        session.adopt(comm.allgather(session.export()))
+    with torch.cuda.stream(session.ctx.stream):
+        while session.rounds_done < m and session.local_log > switch_log:
+            session.finish(comm.allgather(session.partial()))
+        if not session.done:
+            session.adopt(comm.allgather(session.export()))
     return session.result()
 
 

@@ -195,7 +195,7 @@ def test_chained_window_full_size(ctx, O, cfg):
             assert val == Ol.mle_i32(np.ascontiguousarray(t.array).reshape(-1), pt), t.name
 
 
-@pytest.mark.parametrize("logD,Q,R", [(5, 16, 16), (12, 16, 16), (14, 16, 16), (10, 8, 8)])
+@pytest.mark.parametrize("logD,Q,R", [(5, 16, 16), (12, 16, 16), (14, 16, 16), (16, 16, 16), (17, 16, 16), (10, 8, 8)])
 def test_rescale_vs_oracle(ctx, O, logD, Q, R):
     """zk_rescale_prove_dev (D26) against the oracle at given points: claims, both sumchecks' messages and
     finals bit-exact (the larger sizes through the factored round kernels with an Fr and an int32 table),
