@@ -344,20 +344,28 @@ def run_ours(args, rank, world, local):
         # each window's transcript on its own stream (two alternate), so a window's matmul families and
         # merges overlap the previous window's zkReLU
         wctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(2)]
-        streams_all = [c.stream for c in ctxs + wctxs]
+        # stage 2's claim merges (latency-bound sumchecks) side by side on budgeted streams
+        mctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.merge_streams)]
+        for c in mctxs:
+            c.set_sm_budget(max(4, 148 // max(1, args.merge_streams)))
+        streams_all = [c.stream for c in ctxs + wctxs + mctxs]
         with torch.cuda.stream(stream):
             for i in range(2):
                 chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                           wctx=wctxs[i % 2])
+                                           wctx=wctxs[i % 2], merge_ctxs=mctxs)
             torch.cuda.synchronize()
             # the kernel table of one window (every launch bracketed, outside the timed region)
             prof_on(None)
             for c in wctxs:
                 c.profile(True)
                 c.profile_read()
-            chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, wctx=wctxs[0])
+            for c in mctxs:
+                c.profile(True)
+                c.profile_read()
+            chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, wctx=wctxs[0],
+                                       merge_ctxs=mctxs)
             ctab = prof_off()
-            for c in wctxs:
+            for c in wctxs + mctxs:
                 for k, v in c.profile_read().items():
                     n0, t0 = ctab.get(k, (0, 0.0))
                     ctab[k] = (n0 + v[0], t0 + v[1])
@@ -367,7 +375,7 @@ def run_ours(args, rank, world, local):
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
             pend = [chain.enqueue_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                                 wctx=wctxs[i % 2]) for i in range(args.steps)]
+                                                 wctx=wctxs[i % 2], merge_ctxs=mctxs) for i in range(args.steps)]
             for st in streams_all:   # the region ends when every stream of every window has
                 ev = torch.cuda.Event()
                 ev.record(st)
@@ -381,6 +389,7 @@ def run_ours(args, rank, world, local):
         cms = max_over_ranks(c0.elapsed_time(c1), world) / args.steps
         cby = by_kernel(ctab)
         chained = {"ms_per_step": round(cms, 4), "s_per_update": cms / 1000.0 / shape.steps,
+                   "merge_streams": args.merge_streams,
                    "kernels_ms_one_window_serialised": {k: round(t, 4) for k, (n, t) in
                                                         sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
                    "claim_merges": sorted(cres["merges"]), "window_state": cres["window_state"].hex()[:16],
@@ -874,6 +883,7 @@ def main():
     ap.add_argument("--c5-log", type=int, default=26, help="C5: log2 m of the 2^m hypercube (22..30)")
     ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
     ap.add_argument("--no-chained", action="store_true", help="C4 line without the chained-window (N3) measurement")
+    ap.add_argument("--merge-streams", type=int, default=8, help="chained window: streams for the claim merges")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")

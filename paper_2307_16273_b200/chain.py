@@ -116,12 +116,14 @@ def _fence(src, dsts):
 
 def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
                            relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
-                           wctx: api.Context | None = None):
+                           wctx: api.Context | None = None, merge_ctxs: list | None = None):
     """Enqueue one chained window without synchronising; returns a handle for collect_window_chained.
     Streams: the window transcript W on wctx (default ctx); stages 1-2 over ctx + mm_ctxs; stage 3 on
     relu_ctx.  Nothing at the end of a window makes the stage 1-2 streams wait for its stage 3 (the
     child transcripts are freed in collect_window_chained), so with a different wctx per window the
-    next window's matmul families and merges run while this window's zkReLU proves."""
+    next window's matmul families and merges run while this window's zkReLU proves.  merge_ctxs
+    (optional): the streams stage 2 spreads its claim merges over (latency-bound sumchecks: many
+    budgeted streams side by side), default ctx + mm_ctxs."""
     dev = next(f.A for f in families if f.kind == "matmul").device
     mms = [f for f in families if f.kind == "matmul"]
     losses = [f for f in families if f.kind == "loss"]
@@ -131,7 +133,7 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     lanes1 = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
     rctx = relu_ctx if relu_ctx is not None else ctx
     wctx = wctx if wctx is not None else ctx
-    lanes2 = lanes1
+    lanes2 = list(merge_ctxs) if merge_ctxs else lanes1
     # ---- layout of the window's output buffer
     off = 0
     lay1 = []
@@ -327,5 +329,6 @@ def collect_window_chained(h: dict) -> dict:
 
 def prove_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
                          relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
-                         wctx: api.Context | None = None) -> dict:
-    return collect_window_chained(enqueue_window_chained(ctx, seed, header, families, tensors, relu_ctx, mm_ctxs, wctx))
+                         wctx: api.Context | None = None, merge_ctxs: list | None = None) -> dict:
+    return collect_window_chained(enqueue_window_chained(ctx, seed, header, families, tensors, relu_ctx, mm_ctxs, wctx,
+                                                         merge_ctxs))

@@ -160,9 +160,12 @@ def test_chained_window_full_size(ctx, O, cfg):
         one[t.name] = (r["point"], r["claim"])
     for T in mk:
         W.absorb("fcn/join", T.state())
-    for f in [f for f in fams if not hasattr(f, "A")] + [resc]:
+    st3 = [f for f in fams if not hasattr(f, "A")] + [resc]
+    forks3 = []
+    for f in st3:                      # D25 stage 3: every fork first, then the proofs, then the joins
         W.absorb("fcn/fam", f.name.encode())
-        T = Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little"))
+        forks3.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    for f, T in zip(st3, forks3):
         if f is resc:
             r = Ol.rescale_prove(T, f.Z, f.Q, f.R, [one[f.tensors["Z"]][0], one[f.tensors["Zp"]][0]])
             assert r["claims"] == [one[f.tensors["Z"]][1], one[f.tensors["Zp"]][1]]
@@ -175,7 +178,6 @@ def test_chained_window_full_size(ctx, O, cfg):
             ga = g["rescale"][f.name]
             assert ga["aux_merge"]["point"] == am["point"] and ga["aux_merge"]["claim"] == am["claim"]
             assert ga["state"] == T.state()
-            W.absorb("fcn/join", T.state())
             continue
         gr = g["relu"][f.name]
         pts = [one[f.tensors[k]][0] for k in ("Z", "A", "GA", "GZ")]
@@ -187,6 +189,7 @@ def test_chained_window_full_size(ctx, O, cfg):
         assert Ol.sumcheck_verify(T, len(gr["merge"]["r"]), 0, 2, [], gr["merge"]["claim"], gr["merge"]["msgs"],
                                   gr["merge"]["finals"]) == 0
         assert gr["state"] == T.state()
+    for T in forks3:
         W.absorb("fcn/join", T.state())
     assert g["window_state"] == W.state()
     for t in tensors:
