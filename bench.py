@@ -460,8 +460,20 @@ def run_ours(args, rank, world, local):
               "unit": "GFr-mul/s", "frac": None, "traffic": None, "ms_per_step": round(dom_ms, 4),
               "share_of_step": round(dom_ms / ms_local * args.steps, 4) if ms_local else None}
     rf["launches_per_step"] = dom_launches
+    try:   # the committed product-rate measurements (profiles/r2/frmul_peaks.json) as second denominators
+        pk = json.load(open(os.path.join(ROOT, "profiles", "r2", "frmul_peaks.json")))
+        if rf.get("achieved"):
+            meas = pk["products_per_s"]["fp64_pipe_product"] / 1e9
+            ana = pk["analytic_bounds_per_s"]["fp64_product_issue"]["value"] / 1e9
+            rf["frac_of_measured_product_rate"] = round(rf["achieved"] / meas, 4)
+            rf["frac_of_fp64_product_issue_bound"] = round(rf["achieved"] / ana, 4)
+            rf["measured_peaks_basis"] = ("profiles/r2/frmul_peaks.json: the kernel's product (FP64 pipe, fr64.cuh) "
+                                          f"register-resident {meas:.1f} G/s measured; its issue bound {ana:.1f} G/s; "
+                                          "'peak' stays the IMAD-pipe bound of the north star's wording")
+    except (OSError, ValueError, KeyError):
+        pass
     try:   # DRAM traffic of the dominant kernel's captured launch (ncu --set full, committed under profiles/)
-        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic_r1j.json")))
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r2", "ncu_traffic_r2.json")))
         base = dom_name.split("<")[0]
         if base in tj:
             L0 = tj[base]["launches"][0]
