@@ -256,6 +256,14 @@ def run_ours(args, rank, world, local):
         for c in [ctx] + mm_ctxs:
             c.set_sm_budget(args.mm_budget or max(8, 148 // args.mm_streams))
     ctxs = [ctx] + ([relu_ctx] if relu_ctx else []) + mm_ctxs
+    # --pipeline: consecutive windows on alternating zkReLU and window-transcript streams, so a window's
+    # zkReLU starts while the previous one finishes its latency-bound tail rounds (no cross-window waits)
+    pipe = bool(args.pipeline) and relu_ctx is not None
+    relu_ctxs = [relu_ctx] + ([api.Context(local, torch.cuda.Stream(device=local, priority=args.relu_priority))]
+                              if pipe else [])
+    wctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(2)] if pipe else [None, None]
+    ctxs = ctxs + relu_ctxs[1:] + [c for c in wctxs if c is not None]
+    ctxs_all = ctxs
     header = fcn.fcn_header(shape)
     seed = fs_seed(f"C4-rank{rank}")
 
@@ -284,8 +292,9 @@ def run_ours(args, rank, world, local):
         return prof_off()
 
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            dfcn.prove_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
+        for i in range(args.warmup):
+            dfcn.collect_window(*dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctxs[i % len(relu_ctxs)],
+                                                     mm_ctxs=mm_ctxs, merge_aux=args.merge_aux, wctx=wctxs[i % 2]))
         torch.cuda.synchronize()
         # kernel table first (outside the timed region) -> the dominant kernel
         prof_table = profiled_pass() if args.prof == "dominant" else None
@@ -301,10 +310,17 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux) for _ in range(args.steps)]
-        ev1.record(stream)   # each window joins the zkReLU stream back into this one before its end
+        pending = [dfcn.enqueue_window(ctx, seed, header, dev_fams, relu_ctx=relu_ctxs[i % len(relu_ctxs)],
+                                       mm_ctxs=mm_ctxs, merge_aux=args.merge_aux, wctx=wctxs[i % 2])
+                   for i in range(args.steps)]
+        for c in ctxs_all:   # the region ends when every stream of every window has
+            ev_ = torch.cuda.Event()
+            ev_.record(c.stream)
+            stream.wait_event(ev_)
+        ev1.record(stream)
         torch.cuda.synchronize()
-        res = dfcn.collect_window(*pending[-1])   # outputs stay in HBM until here (outside the timed region)
+        for p_ in pending:   # outputs stay in HBM until here (outside the timed region)
+            res = dfcn.collect_window(*p_)
         del pending
         barrier(world)
         launches = sum(c.launches for c in ctxs) - launches0
@@ -343,29 +359,29 @@ def run_ours(args, rank, world, local):
         cseed = fs_seed(f"C4-chained-rank{rank}")
         # each window's transcript on its own stream (two alternate), so a window's matmul families and
         # merges overlap the previous window's zkReLU
-        wctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(2)]
+        cwctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(2)]
         # stage 2's claim merges (latency-bound sumchecks) side by side on budgeted streams
         mctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.merge_streams)]
         for c in mctxs:
             c.set_sm_budget(max(4, 148 // max(1, args.merge_streams)))
-        streams_all = [c.stream for c in ctxs + wctxs + mctxs]
+        streams_all = [c.stream for c in ctxs + cwctxs + mctxs]
         with torch.cuda.stream(stream):
             for i in range(2):
                 chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                           wctx=wctxs[i % 2], merge_ctxs=mctxs)
+                                           wctx=cwctxs[i % 2], merge_ctxs=mctxs)
             torch.cuda.synchronize()
             # the kernel table of one window (every launch bracketed, outside the timed region)
             prof_on(None)
-            for c in wctxs:
+            for c in cwctxs:
                 c.profile(True)
                 c.profile_read()
             for c in mctxs:
                 c.profile(True)
                 c.profile_read()
-            chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, wctx=wctxs[0],
+            chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, wctx=cwctxs[0],
                                        merge_ctxs=mctxs)
             ctab = prof_off()
-            for c in wctxs + mctxs:
+            for c in cwctxs + mctxs:
                 for k, v in c.profile_read().items():
                     n0, t0 = ctab.get(k, (0, 0.0))
                     ctab[k] = (n0 + v[0], t0 + v[1])
@@ -375,7 +391,7 @@ def run_ours(args, rank, world, local):
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
             pend = [chain.enqueue_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                                 wctx=wctxs[i % 2], merge_ctxs=mctxs) for i in range(args.steps)]
+                                                 wctx=cwctxs[i % 2], merge_ctxs=mctxs) for i in range(args.steps)]
             for st in streams_all:   # the region ends when every stream of every window has
                 ev = torch.cuda.Event()
                 ev.record(st)
@@ -495,7 +511,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": "C4: FAC4DNN window of the 3072(->4096)-1024x8-10(->16) FCN, batch 64, T'=16 steps, "
                                "9 families (F x3, GA x2, GW x3, ReLU D=2^23), one transcript",
                    "updates_per_step": shape.steps, "input_bytes_per_step": in_bytes,
-                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams, "mm_budget": args.mm_budget or max(8, 148 // args.mm_streams), "relu_aux_merge": bool(args.merge_aux)},
+                   "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams, "pipelined_windows": pipe, "mm_budget": args.mm_budget or max(8, 148 // args.mm_streams), "relu_aux_merge": bool(args.merge_aux)},
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "fcn.prove_windows_from_host: pinned host stacks -> HBM per family on a copy stream "
@@ -896,6 +912,8 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
     ap.add_argument("--no-chained", action="store_true", help="C4 line without the chained-window (N3) measurement")
     ap.add_argument("--merge-streams", type=int, default=8, help="chained window: streams for the claim merges")
+    ap.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
+                    help="1: consecutive windows on alternating zkReLU / transcript streams (windows overlap)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")

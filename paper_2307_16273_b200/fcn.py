@@ -85,7 +85,7 @@ def _family_work(f: DeviceFamily) -> int:
 
 def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list, ready: list | None = None,
                    relu_ctx: api.Context | None = None, proof_order: list | None = None,
-                   mm_ctxs: list | None = None, merge_aux: bool = False):
+                   mm_ctxs: list | None = None, merge_aux: bool = False, wctx: api.Context | None = None):
     """Enqueue one window's proofs without synchronising.
 
     Transcripts (D3d): the window transcript W absorbs "fcn/hdr", then per family "fcn/fam"
@@ -99,6 +99,10 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
     mm_ctxs (optional): extra contexts (own streams, typically with an SM budget) over which the matmul
     families are spread, largest first onto the least-loaded one, so their latency-bound sumchecks run
     side by side; ctx keeps its share.
+    wctx (optional): the context of the window transcript W (default ctx).  With a wctx of its own per
+    window (alternating), nothing in a window waits for the previous window's families, so windows
+    enqueued back to back pipeline (a window's latency-bound tail overlaps the next one's rounds); the
+    child transcripts are then released by collect_window.
     Returns (out, flag, layout): `out` holds, per family, its proof output followed by the family
     transcript's final state, then W's final state; `flag` is the int32 range flag."""
     dev = (families[0].A if families[0].kind == "matmul" else families[0].Z).device
@@ -120,8 +124,11 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
             home[i] = lanes[j]
             load[j] += _family_work(families[i])
     ctx_of_i = lambda i: relu_ctx if (two and families[i].kind == "relu") else home.get(i, ctx)
-    side = ([relu_ctx] if two else []) + lanes[1:]   # streams that fork from and join back into ctx
-    W = api.Transcript(ctx, seed)
+    own_w = wctx is not None and wctx.stream != ctx.stream
+    wc = wctx if own_w else ctx
+    # streams that fork from and join back into the window transcript's stream
+    side = ([relu_ctx] if two else []) + (lanes if own_w else lanes[1:])
+    W = api.Transcript(wc, seed)
     W.absorb("fcn/hdr", header)
     kids = []
     for i, f in enumerate(families):
@@ -129,7 +136,7 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
         kids.append(W.fork("fcn/fork", ctx_of_i(i)))
     if side:
         ev = torch.cuda.Event()
-        ev.record(ctx.stream)
+        ev.record(wc.stream)
         for c in side:
             c.stream.wait_event(ev)
     for i in (proof_order if proof_order is not None else range(len(lay))):
@@ -149,10 +156,13 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
     for c in side:
         ev = torch.cuda.Event()
         ev.record(c.stream)
-        ctx.stream.wait_event(ev)
+        wc.stream.wait_event(ev)
     for T in kids:
         W.absorb_state("fcn/join", T)
     W.state_dev(out[off:off + 32])
+    if own_w:   # pipelined windows: the transcripts are released by collect_window, after the device work
+        lay.append(("transcripts", kids + [W]))
+        return out, flag, lay
     if side:   # the children are freed on their own streams: after the joins
         ev = torch.cuda.Event()
         ev.record(ctx.stream)
@@ -169,6 +179,10 @@ def collect_window(out: torch.Tensor, flag: torch.Tensor, lay) -> list:
     also carries "window_state" (the window transcript after the joins)."""
     torch.cuda.synchronize(out.device)   # the library wrote on its contexts' streams (ADVICE r1)
     raw = out.cpu().numpy().tobytes()
+    if lay and lay[-1][0] == "transcripts":
+        for T in lay[-1][1]:
+            T.close()
+        lay = lay[:-1]
     if int(flag.item()) & 1:
         raise api.ZkError(-2, "zkReLU input outside the (Q+R)-bit range")
     results = []
