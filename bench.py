@@ -233,6 +233,7 @@ def dominant_kernel(prof: dict):
 
 # ---------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local):
+    import numpy as np
     import torch
     from paper_2307_16273_b200 import api, build
     from paper_2307_16273_b200 import fcn as dfcn
@@ -422,9 +423,12 @@ def run_ours(args, rank, world, local):
     # ---- e2e: host (pinned) -> device copies of the window's inputs inside the timed region
     pinned = {}
 
-    def pin(a):   # one pinned buffer per distinct stack (shared stacks are uploaded once per window)
+    def pin(a):   # one pinned buffer per distinct stack (shared stacks are uploaded once per window); a stack
+        # whose entries fit 16 bits (the matmul operands: X, W, A, G_Z) travels as int16 and is widened on
+        # the device (zk_widen_i16): the same int32 tensor, half the PCIe bytes
         if id(a) not in pinned:
-            pinned[id(a)] = torch.from_numpy(a).pin_memory()
+            small = args.e2e_i16 and a.size and int(a.max()) < (1 << 15) and int(a.min()) >= -(1 << 15)
+            pinned[id(a)] = torch.from_numpy(a.astype(np.int16) if small else a).pin_memory()
         return pinned[id(a)]
 
     host_fams = [dfcn.DeviceFamily(f.name, "matmul", A=pin(f.A), B=pin(f.B), trans_a=f.transA, trans_b=f.transB)
@@ -912,9 +916,12 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
     ap.add_argument("--no-chained", action="store_true", help="C4 line without the chained-window (N3) measurement")
     ap.add_argument("--merge-streams", type=int, default=8, help="chained window: streams for the claim merges")
-    ap.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
-                    help="1: consecutive windows on alternating zkReLU / transcript streams (windows overlap)")
+    ap.add_argument("--pipeline", type=int, default=0, choices=[0, 1],
+                    help="1: consecutive windows on alternating zkReLU / transcript streams (measured 171 ms per "
+                         "window against 11.2: two windows' persistent spin-waiting kernels interleave on the SMs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-i16", type=int, default=1, choices=[0, 1],
+                    help="1: e2e uploads stacks whose entries fit 16 bits as int16 (widened on the device)")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
                     help="2: zkReLU families on a second stream, concurrent with the matmul families")
     ap.add_argument("--mm-streams", type=int, default=2,

@@ -102,6 +102,10 @@ void zk_transcript_free(zk_transcript* tr);
  * zk_fr_table_to_canonical: d_out[i] = canonical 32-byte encoding of d_in[i] (may alias).
  * zk_fr_table_from_canonical: the inverse; returns ZK_ERR_NONCANONICAL if any input >= p. */
 zk_status zk_embed_i32(zk_ctx* ctx, const int32_t* d_in, uint64_t n, void* d_out);
+/* zk_widen_i16: d_out[i] = d_in[i] (int16 -> int32, sign-extended), asynchronous; both 16-byte aligned.
+ *   The end-to-end transport of stacks whose entries fit 16 bits (the matmul operands of the FCN trace):
+ *   half the host-to-device bytes, the int32 tensor the provers read is rebuilt on the device. */
+zk_status zk_widen_i16(zk_ctx* ctx, const int16_t* d_in, uint64_t n, int32_t* d_out);
 zk_status zk_eq_table(zk_ctx* ctx, const zk_fr* point, uint32_t k, const zk_fr* scale, void* d_out);
 zk_status zk_mle_eval_i32(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const zk_fr* point, zk_fr* out);
 zk_status zk_mle_eval_fr(zk_ctx* ctx, const void* d_tab, uint32_t m, const zk_fr* point, zk_fr* out);

@@ -77,6 +77,7 @@ def lib():
         "zk_transcript_absorb_state": ([vp, c.c_char_p, vp], i32),
         "zk_transcript_free": ([vp], None),
         "zk_embed_i32": ([vp, vp, u64, vp], i32),
+        "zk_widen_i16": ([vp, vp, u64, vp], i32),
         "zk_eq_table": ([vp, vp, u32, vp, vp], i32),
         "zk_mle_eval_i32": ([vp, vp, u32, vp, vp], i32),
         "zk_mle_eval_fr": ([vp, vp, u32, vp, vp], i32),

@@ -608,3 +608,12 @@ def parse_rescale_out(raw: bytes, logD: int, Q: int, R: int) -> dict:
     B["r"] = [int.from_bytes(raw[o + 32 * (m + i):o + 32 * (m + i) + 32], "little") for i in range(m)]
     claims = [int.from_bytes(raw[12 + 32 * i:44 + 32 * i], "little") for i in range(2)]
     return dict(claims=claims, A=A, B=B, proof=raw[:plen])
+
+
+def widen_i16(ctx: Context, t16: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """zk_widen_i16: an int16 device tensor -> int32 (same shape), on the context stream."""
+    assert t16.dtype == torch.int16 and t16.is_cuda and t16.is_contiguous()
+    if out is None:
+        out = torch.empty(t16.shape, dtype=torch.int32, device=t16.device)
+    ctx.check(lib().zk_widen_i16(ctx.h, t16.data_ptr(), t16.numel(), out.data_ptr()))
+    return out

@@ -228,6 +228,28 @@ zk_status zk_embed_i32(zk_ctx* ctx, const int32_t* d_in, uint64_t n, void* d_out
     ZK_API_END(ctx)
 }
 
+// int16 -> int32 (the end-to-end transport of small-range stacks: half the host-to-device bytes)
+__global__ void k_widen_i16(const int16_t* in, uint64_t n, int32_t* out) {
+    const uint64_t n8 = n / 8;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n8; i += (uint64_t)gridDim.x * blockDim.x) {
+        const int4 v = __ldcs(reinterpret_cast<const int4*>(in) + i);
+        const int16_t* h = reinterpret_cast<const int16_t*>(&v);
+        int4* o = reinterpret_cast<int4*>(out) + 2 * i;
+        __stcs(o, make_int4(h[0], h[1], h[2], h[3]));
+        __stcs(o + 1, make_int4(h[4], h[5], h[6], h[7]));
+    }
+    for (uint64_t i = 8 * n8 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+zk_status zk_widen_i16(zk_ctx* ctx, const int16_t* d_in, uint64_t n, int32_t* d_out) {
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE((d_in && d_out) || !n, ZK_ERR_ARG, "null argument");
+    ZK_REQUIRE(((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_out & 15) == 0, ZK_ERR_ARG, "buffers must be 16-byte aligned");
+    if (n) ZK_LAUNCH(ctx, k_widen_i16, grid_for(ctx, (n + 7) / 8, 256, 8), 256, 0, d_in, n, d_out);
+    ZK_API_END(ctx)
+}
+
 zk_status zk_eq_table(zk_ctx* ctx, const zk_fr* point, uint32_t k, const zk_fr* scale, void* d_out) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE(d_out && (point || !k) && k <= 32, ZK_ERR_ARG, "bad argument");

@@ -213,6 +213,14 @@ def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
                                           merge_aux=merge_aux))
 
 
+def _upload_i32(t: torch.Tensor, dev, cctx: api.Context) -> torch.Tensor:
+    """Host stack -> int32 device tensor on the copy stream (the current stream): int16 host stacks (the
+    end-to-end transport of entries that fit 16 bits) are copied as int16 and widened on the device."""
+    if t.dtype == torch.int16:
+        return api.widen_i16(cctx, t.to(dev, non_blocking=True))
+    return t.to(dev, non_blocking=True)
+
+
 def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None,
                            relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
                            merge_aux: bool = False) -> list:
@@ -222,16 +230,18 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
     proof waits only for its own upload, so the transfers of later families overlap the proofs of
     earlier ones.  A host buffer shared by several families (the weight stack W[2..8] is the B operand
     of F[2..8] and of GA[1..7]) is copied once.  The proof bytes come back to the host (one
-    synchronisation).  host_families: DeviceFamily records whose tensors live on the host."""
+    synchronisation).  host_families: DeviceFamily records whose tensors live on the host (int32, or int16
+    for stacks whose entries fit 16 bits: copied as int16 and widened on the device, zk_widen_i16)."""
     dev = torch.device("cuda", ctx.device)
     cs = copy_stream if copy_stream is not None else torch.cuda.Stream(device=dev)
+    cctx = api.Context(ctx.device, cs)
     fams, ready = [], []
     uploaded = {}   # host buffer -> device tensor: a stack shared by several families is copied once
 
     def upload(t):
         key = (t.data_ptr(), t.numel(), t.dtype)
         if key not in uploaded:
-            uploaded[key] = t.to(dev, non_blocking=True)
+            uploaded[key] = _upload_i32(t, dev, cctx)
         return uploaded[key]
 
     # upload (and proof) order: zkReLU families first (least data, most work), then the matmul
@@ -269,6 +279,7 @@ def prove_windows_from_host(ctx: api.Context, windows: list, copy_stream=None, r
     prove_window_from_host per window."""
     dev = torch.device("cuda", ctx.device)
     cs = copy_stream if copy_stream is not None else torch.cuda.Stream(device=dev)
+    cctx = api.Context(ctx.device, cs)
     pending = []
     for seed, header, host_families in windows:
         uploaded = {}
@@ -276,7 +287,7 @@ def prove_windows_from_host(ctx: api.Context, windows: list, copy_stream=None, r
         def upload(t):
             key = (t.data_ptr(), t.numel(), t.dtype)
             if key not in uploaded:
-                uploaded[key] = t.to(dev, non_blocking=True)
+                uploaded[key] = _upload_i32(t, dev, cctx)
             return uploaded[key]
 
         def nbytes(f):

@@ -767,3 +767,29 @@ def test_readme_flow_host_verified(ctx, O):
     assert verify.verify_matmul(H, logs, dict(red, proof=proof["proof"]))["r"] == proof["r"]
     assert verify.verify_relu(H, relu["proof"], (12, 16, 16))["point"] == relu["point"]
     assert H.state() == tr.state()
+
+
+def test_e2e_int16_transport_same_proofs(ctx):
+    """prove_windows_from_host with the stacks whose entries fit 16 bits shipped as int16 (zk_widen_i16 on
+    the device) gives the bytes of the device-resident window (the same int32 tensors are proved)."""
+    import numpy as np
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=4, width=64, batch=16, din=128, dout=16)
+    fams = fcn.assemble_families(shape, fcn.generate_trace(shape))
+    seed, hdr = fs_seed("e2e-i16"), fcn.fcn_header(shape)
+    g = dfcn.prove_window(ctx, seed, hdr, dfcn.upload_families(fams))
+
+    def host(a):
+        small = int(a.max()) < (1 << 15) and int(a.min()) >= -(1 << 15)
+        return torch.from_numpy(a.astype(np.int16) if small else a).pin_memory()
+    hf = [dfcn.DeviceFamily(f.name, "matmul", A=host(f.A), B=host(f.B), trans_a=f.transA, trans_b=f.transB)
+          if hasattr(f, "A") else dfcn.DeviceFamily(f.name, "relu", Z=host(f.Z), GA=host(f.GA), Q=f.Q, R=f.R) for f in fams]
+    assert any(t.dtype == torch.int16 for f in hf for t in (f.A, f.B, f.Z, f.GA) if t is not None)
+    h = dfcn.prove_windows_from_host(ctx, [(seed, hdr, hf)])[0]
+    assert [r["proof"] for r in h] == [r["proof"] for r in g]
+    assert h[-1]["window_state"] == g[-1]["window_state"]
+    x = torch.arange(-(1 << 15), (1 << 15), 37, dtype=torch.int16)
+    from paper_2307_16273_b200 import api
+    y = api.widen_i16(ctx, x.cuda())
+    assert torch.equal(y.cpu(), x.to(torch.int32))
