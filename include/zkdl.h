@@ -398,7 +398,8 @@ zk_status zk_verify_rescale(uint8_t st[32], const uint8_t* proof, uint64_t proof
  *   bench.py times it to measure this implementation's sustained Fr-mul rate. */
 zk_status zk_diag_fr_op(zk_ctx* ctx, int op, const void* d_a, const void* d_b, uint64_t n, void* d_out);
 /* zk_diag_rowdot: out[r] = sum_c M[r][c] beta(point, c) (Montgomery, d_out: nrows Fr) through the CUDA-core
- * (use_tc = 0) or the tensor-core (use_tc = 1) row-dot kernel of the matmul restriction; cols a power of two. */
+ * (use_tc = 0) or the tensor-core row-dot kernel of the matmul restriction with its cp.async producer
+ * (use_tc = 1) or its TMA producer (use_tc = 2, the default path); cols a power of two. */
 zk_status zk_diag_rowdot(zk_ctx* ctx, const int32_t* d_M, uint64_t nrows, uint32_t cols, const zk_fr* point,
                          void* d_out, int use_tc);
 zk_status zk_diag_mul_bench(zk_ctx* ctx, const void* d_seed, uint32_t iters, uint32_t blocks, void* d_out);

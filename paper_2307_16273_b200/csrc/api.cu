@@ -553,7 +553,7 @@ zk_status zk_diag_rowdot(zk_ctx* ctx, const int32_t* d_M, uint64_t nrows, uint32
     while ((1ull << ln) < nrows) ln++;
     if (use_tc) {
         ZK_REQUIRE(rowdot_tc_ok(nrows, cols), ZK_ERR_ARG, "shape not supported by the tensor-core row dot");
-        rowdot_tc(ctx, d_M, nrows, cols, E2, static_cast<fr_t*>(d_out), 1ull << ln, ln, 1, s);
+        rowdot_tc(ctx, d_M, nrows, cols, E2, static_cast<fr_t*>(d_out), 1ull << ln, ln, 1, s, use_tc == 2 ? 1 : 0);
     } else {
         ZK_LAUNCH(ctx, k_rowdot_i32<LoadPlain>, grid_for(ctx, nrows * 32, 256, 8), 256, 0, LoadPlain{d_M}, nrows, cols,
                   (const fr_t*)E2, static_cast<fr_t*>(d_out), 1ull << ln, ln, (uint64_t)1);

@@ -18,6 +18,9 @@
 // latency-bound: every stage reads a 128 B (RT_KS = 4) piece of 4 KB-strided rows; 3 stages of 8 K steps
 // (256 B of every row per stage) cut the window's row dots 0.74 -> 0.67 ms (serial kernel tables).  A TMA
 // (128-byte swizzle) producer is the next step (a first attempt stalled when a CTA owned several tiles).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 
 #include "tables.cuh"
@@ -276,13 +279,201 @@ __global__ void __launch_bounds__(RT_THREADS, 1) k_rowdot_tc(RtArgs a) {
     if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
+// ---------------------------------------------------------------- the TMA producer (round 2)
+// The same GEMM with the A operand moved by the tensor-memory accelerator: a 2D tensor map over M's bytes
+// (rows x 4 cols), boxes of 128 rows x 128 bytes (4 K steps) in the 128-byte-swizzled K-major layout the
+// MMA reads directly (SW128 descriptor, SBO = 1024 B; the K step within a box advances the start address by
+// 32 B); rows past the end and bytes past a row are zero-filled by the TMA unit.  One thread issues a
+// stage (two boxes + one bulk copy of the B images) against one transaction-counted barrier, so the
+// producer costs no issue slots; the MMA and epilogue warps are the kernel above.
+constexpr int RM_STAGES = 3;
+struct __align__(1024) RmSmem {
+    uint8_t A[RM_STAGES][RT_KS / 4][128 * 128];
+    uint8_t B[RM_STAGES][RT_KS][2][RT_BBYTES];
+    uint64_t full[RM_STAGES], empty[RM_STAGES], accfull[2], accempty[2];
+    uint32_t tmem;
+};
+
+__device__ __forceinline__ uint64_t adesc_sw128(const void* p) {
+    return (uint64_t)((su32(p) >> 4) & 0x3fff) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(RT_THREADS, 1) k_rowdot_tma(RtArgs a, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(1024) uint8_t rm_raw[];
+    RmSmem& S = *reinterpret_cast<RmSmem*>(rm_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t KS = a.cols / 8;
+    const uint32_t KSS = (KS + RT_KS - 1) / RT_KS;
+    const uint64_t ntiles = (a.nrows + 127) / 128;
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&S.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (lane == 0) {
+            for (int i = 0; i < RM_STAGES; i++) {
+                mbar_init(&S.full[i], 1);
+                mbar_init(&S.empty[i], 1);
+            }
+            for (int i = 0; i < 2; i++) {
+                mbar_init(&S.accfull[i], 1);
+                mbar_init(&S.accempty[i], 4);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+    }
+    if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+    if (warp == 0) {
+        // ---------------- producer: one thread, one barrier transaction per stage
+        if (lane == 0) {
+            uint64_t it = 0;
+            for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (uint32_t sg = 0; sg < KSS; sg++, it++) {
+                    const uint32_t st = it % RM_STAGES;
+                    if (it >= RM_STAGES) rt_wait(&S.empty[st], ((it / RM_STAGES) - 1) & 1, 11);
+                    const uint32_t k0 = sg * RT_KS, nk = KS - k0 < (uint32_t)RT_KS ? KS - k0 : (uint32_t)RT_KS;
+                    const uint32_t nbox = (nk + 3) / 4;
+                    mbar_expect_tx(&S.full[st], nbox * 128 * 128 + nk * 2 * RT_BBYTES);
+                    for (uint32_t b = 0; b < nbox; b++)
+                        tma_load_2d(S.A[st][b], &tmap, (int32_t)((k0 + 4 * b) * 32), (int32_t)(tile * 128), &S.full[st]);
+                    bulk_g2s(S.B[st][0][0], a.Bimg + (uint64_t)k0 * 2 * RT_BBYTES, nk * 2 * RT_BBYTES, &S.full[st]);
+                }
+            }
+        }
+    } else if (warp == 8) {
+        // ---------------- MMA issuer
+        uint64_t it = 0, ti = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+            const uint32_t buf = ti & 1;
+            if (ti >= 2) rt_wait(&S.accempty[buf], ((ti / 2) - 1) & 1, 12);
+            tc_fence_after();
+            for (uint32_t sg = 0; sg < KSS; sg++, it++) {
+                const uint32_t st = it % RM_STAGES;
+                rt_wait(&S.full[st], (it / RM_STAGES) & 1, 13);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t k0 = sg * RT_KS, nk = KS - k0 < (uint32_t)RT_KS ? KS - k0 : (uint32_t)RT_KS;
+                    for (uint32_t kk = 0; kk < nk; kk++) {
+                        const uint64_t ad = adesc_sw128(S.A[st][kk >> 2] + 32 * (kk & 3));
+                        mma_i8_ss(tmem + 64 * buf, ad, bdesc(S.B[st][kk][0]), RT_IDESC_U, (k0 + kk) > 0);
+                        mma_i8_ss(tmem + 64 * buf, ad, bdesc(S.B[st][kk][1]), RT_IDESC_S, 1u);
+                    }
+                    mma_commit(&S.empty[st]);
+                    if (sg + 1 == KSS) mma_commit(&S.accfull[buf]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 9) {
+        // ---------------- epilogue: warp w drains TMEM lanes 32 (w mod 4) .. + 31
+        const uint32_t q = warp & 3;
+        uint32_t bias[10];
+#pragma unroll
+        for (int i = 0; i < 10; i++) bias[i] = __ldg(&a.bias[i]);
+        uint64_t ti = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+            const uint32_t buf = ti & 1;
+            rt_wait(&S.accfull[buf], (ti / 2) & 1, 14);
+            tc_fence_after();
+            uint32_t d[40];
+            const uint32_t taddr = tmem + ((32 * q) << 16) + 64 * buf;
+            {
+                uint32_t v32[32];
+                tmem_ld32(taddr, v32);
+#pragma unroll
+                for (int i = 0; i < 32; i++) d[i] = v32[i];
+                uint32_t v8[8];
+                tmem_ld8(taddr + 32, v8);
+#pragma unroll
+                for (int i = 0; i < 8; i++) d[32 + i] = v8[i];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.accempty[buf]);
+            const uint64_t row = tile * 128 + 32 * q + lane;
+            if (row < a.nrows) {
+                int64_t acc[10];
+#pragma unroll
+                for (int i = 0; i < 10; i++) acc[i] = (int64_t)bias[i];
+#pragma unroll
+                for (int s = 0; s < 35; s++) acc[s >> 2] += (int64_t)(int32_t)d[s] << (8 * (s & 3));
+                uint32_t w[10];
+                int64_t carry = 0;
+#pragma unroll
+                for (int i = 0; i < 10; i++) {
+                    const int64_t v = acc[i] + carry;
+                    w[i] = (uint32_t)v;
+                    carry = v >> 32;
+                }
+                const uint64_t o = (row & (a.inner - 1)) * a.outer + (row >> a.log_inner);
+                fr_store(&a.out[o], wide_finish(w));
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 1: the TMA producer (default), 0: the cp.async producer (ZKDL_ROWDOT_TMA=0)
+static bool rowdot_tma_on() {
+    static const bool off = getenv("ZKDL_ROWDOT_TMA") && atoi(getenv("ZKDL_ROWDOT_TMA")) == 0;
+    return !off;
+}
+
+static void rowdot_tma_launch(zk_ctx* ctx, const RtArgs& a) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    ZK_REQUIRE(enc != nullptr, ZK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)a.cols * 4, (cuuint64_t)a.nrows};
+    const cuuint64_t strides[1] = {(cuuint64_t)a.cols * 4};
+    const cuuint32_t box[2] = {128, 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int32_t*>(a.M), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    ZK_REQUIRE(r == CUDA_SUCCESS, ZK_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    const size_t smem = sizeof(RmSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        ZK_CUDA(cudaFuncSetAttribute(k_rowdot_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const uint64_t ntiles = (a.nrows + 127) / 128;
+    const unsigned int grid = (unsigned int)(ntiles < (uint64_t)ctx->num_sms ? ntiles : (uint64_t)ctx->num_sms);
+    ZK_LAUNCH(ctx, k_rowdot_tma, grid, RT_THREADS, smem, a, map);
+}
+
 bool rowdot_tc_ok(uint64_t nrows, uint32_t cols) {
     static const bool off = getenv("ZKDL_ROWDOT_TC") && atoi(getenv("ZKDL_ROWDOT_TC")) == 0;
     return !off && cols % 8 == 0 && cols >= 8 && cols <= 4096 && nrows >= 1024;
 }
 
 void rowdot_tc(zk_ctx* ctx, const int32_t* M, uint64_t nrows, uint32_t cols, const fr_t* E2, fr_t* out, uint64_t inner,
-               uint32_t log_inner, uint64_t outer, Scratch& s) {
+               uint32_t log_inner, uint64_t outer, Scratch& s, int use_tma) {
     const uint32_t KS = cols / 8;
     uint8_t* Bimg = s.alloc<uint8_t>((size_t)KS * 2 * RT_BBYTES);
     ZK_LAUNCH(ctx, k_rt_bimg, grid_for(ctx, (uint64_t)KS * 2 * RT_BBYTES, 256, 4), 256, 0, E2, cols, Bimg);
@@ -298,6 +489,10 @@ void rowdot_tc(zk_ctx* ctx, const int32_t* M, uint64_t nrows, uint32_t cols, con
     a.inner = inner;
     a.outer = outer;
     a.log_inner = log_inner;
+    if (use_tma < 0 ? rowdot_tma_on() : use_tma != 0) {
+        rowdot_tma_launch(ctx, a);
+        return;
+    }
     const size_t smem = sizeof(RtSmem) + 1024;
     static bool attr = false;
     if (!attr) {

@@ -202,7 +202,7 @@ void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ, 2 Z' = round(Z / 2^R)*/, co
 // cols <= 4096, >= 1024 rows; ZKDL_ROWDOT_TC=0 disables it).
 bool rowdot_tc_ok(uint64_t nrows, uint32_t cols);
 void rowdot_tc(zk_ctx* ctx, const int32_t* M, uint64_t nrows, uint32_t cols, const fr_t* E2, fr_t* out, uint64_t inner,
-               uint32_t log_inner, uint64_t outer, Scratch& s);
+               uint32_t log_inner, uint64_t outer, Scratch& s, int use_tma = -1 /* -1: default (ZKDL_ROWDOT_TMA), 0: cp.async producer, 1: TMA */);
 void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,
                    fr_t* d_out, Scratch& s);
 void mle_fr_dev(zk_ctx* ctx, const fr_t* d_tab, uint32_t m, const fr_t* d_u, fr_t* d_out, Scratch& s);

@@ -721,7 +721,7 @@ def test_rowdot_tensor_cores_vs_oracle(ctx, O, nrows, cols):
                                                            | set(rng.sample(range(nrows), 512)))
     O.set_threads(1)
     want = [O.mle_i32(Mh[r], pt) for r in rows]
-    for tc in (0, 1):
+    for tc in (0, 1, 2):   # CUDA cores; tensor cores with the cp.async producer; with the TMA producer
         o = torch.zeros((nrows, 32), dtype=torch.uint8, device="cuda")
         ctx.check(lib().zk_diag_rowdot(ctx.h, M.cuda().data_ptr(), nrows, cols, api._fr_buf(pt), o.data_ptr(), tc))
         got = api.fr_table_to_ints(ctx, o)
