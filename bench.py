@@ -434,7 +434,7 @@ def run_ours(args, rank, world, local):
     host_fams = [dfcn.DeviceFamily(f.name, "matmul", A=pin(f.A), B=pin(f.B), trans_a=f.transA, trans_b=f.transB)
                  if hasattr(f, "A") else dfcn.DeviceFamily(f.name, "relu", Z=pin(f.Z), GA=pin(f.GA), Q=f.Q, R=f.R)
                  for f in fams]
-    e2e_steps = 0 if args.profile_mode else max(1, min(args.steps, 3))
+    e2e_steps = 0 if args.profile_mode else max(1, args.steps)   # the same K windows as the device-timed value
     copy_stream = torch.cuda.Stream(device=local)
     with torch.cuda.stream(stream):
         for _ in range(2 if e2e_steps else 0):   # untimed warm-up with the timed call's shape: the caching
