@@ -794,6 +794,7 @@ void ScEngine::finals() {
 // counter; block 0 reduces them, runs the transcript step on its warp 0 and publishes r_t through a
 // round flag).  Eq suffix levels E_t = beta(w_{t+1..n_eq-1}, .) are pair-summed one level ahead.
 constexpr uint32_t SC_ALL_MAX_LOG = 18;
+constexpr uint64_t SC_SOLO_PAIRS = 512;   // rounds with at most this many pairs: the reducer block alone
 
 struct ScAllArgs {
     const fr_t* src[3];
@@ -831,6 +832,11 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
     if (blockIdx.x == 0 && tid < 32) fs_begin(fs, a.st);
     for (uint32_t t = 0; t < m; t++) {
         const uint64_t n_pairs = 1ull << (m - t - 1);
+        // the last rounds (<= SC_SOLO_PAIRS pairs) run on the reducer block alone: no partials, arrival
+        // counter or round flag, one __syncthreads per round (the workers' last folds are visible: they
+        // fenced before their final arrival, which block 0 waited for)
+        const bool solo = gridDim.x == 1 || n_pairs <= SC_SOLO_PAIRS;
+        if (solo && blockIdx.x != 0) return;
         const bool fold0 = a.r_first != nullptr;
         const bool folding = t > 0 || fold0;
         const fr_t* src[K];
@@ -855,8 +861,9 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
 #pragma unroll
         for (int x = 0; x <= K; x++) acc[x] = fr_zero();
         const uint64_t nworkers = gridDim.x - 1;
-        for (uint64_t b = blockIdx.x == 0 ? n_pairs : (blockIdx.x - 1) * (uint64_t)blockDim.x + tid; b < n_pairs;
-             b += nworkers * blockDim.x) {
+        const uint64_t b0 = solo ? (uint64_t)tid : (blockIdx.x == 0 ? n_pairs : (blockIdx.x - 1) * (uint64_t)blockDim.x + tid);
+        const uint64_t bs = solo ? (uint64_t)blockDim.x : nworkers * blockDim.x;
+        for (uint64_t b = b0; b < n_pairs; b += bs) {
             fr_t lo[K], d[K];
 #pragma unroll
             for (int k = 0; k < K; k++) {
@@ -902,7 +909,13 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
                     for (int k = 0; k < K; k++) v[k] = fr_add(v[k], d[k]);
             }
         }
-        if (blockIdx.x != 0) {   // worker: publish the block partial
+        if (solo) {   // block 0 alone: its own sums are the round totals
+            block_reduce_fr<K + 1>(acc, sm_red);
+            if (tid == 0)
+#pragma unroll
+                for (int x = 0; x <= K; x++) tot[x] = acc[x];
+            __syncthreads();
+        } else if (blockIdx.x != 0) {   // worker: publish the block partial
             block_reduce_fr<K + 1>(acc, sm_red);
             if (tid == 0) {
 #pragma unroll
@@ -912,27 +925,29 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
             }
         }
         if (blockIdx.x == 0) {   // dedicated reducer + transcript block (its I-cache keeps only this code)
-            if (tid == 0) {
-                while (ld_volatile(a.arrive) < (t + 1) * (gridDim.x - 1)) {
+            if (!solo) {
+                if (tid == 0) {
+                    while (ld_volatile(a.arrive) < (t + 1) * (gridDim.x - 1)) {
+                    }
+                    __threadfence();
                 }
-                __threadfence();
+                __syncthreads();
+                fr_t s_[K + 1];
+#pragma unroll
+                for (int x = 0; x <= K; x++) s_[x] = fr_zero();
+                for (unsigned int bb = tid; bb < gridDim.x - 1; bb += blockDim.x)
+#pragma unroll
+                    for (int x = 0; x <= K; x++) {
+                        const uint4* q = reinterpret_cast<const uint4*>(&a.partials[bb * (K + 1) + x]);
+                        uint4 xx = __ldcg(q), yy = __ldcg(q + 1);
+                        s_[x] = fr_add(s_[x], fr_t{{xx.x, xx.y, xx.z, xx.w, yy.x, yy.y, yy.z, yy.w}});
+                    }
+                block_reduce_fr<K + 1>(s_, sm_red);
+                if (tid == 0)
+#pragma unroll
+                    for (int x = 0; x <= K; x++) tot[x] = s_[x];
+                __syncthreads();
             }
-            __syncthreads();
-            fr_t s_[K + 1];
-#pragma unroll
-            for (int x = 0; x <= K; x++) s_[x] = fr_zero();
-            for (unsigned int bb = tid; bb < gridDim.x - 1; bb += blockDim.x)
-#pragma unroll
-                for (int x = 0; x <= K; x++) {
-                    const uint4* q = reinterpret_cast<const uint4*>(&a.partials[bb * (K + 1) + x]);
-                    uint4 xx = __ldcg(q), yy = __ldcg(q + 1);
-                    s_[x] = fr_add(s_[x], fr_t{{xx.x, xx.y, xx.z, xx.w, yy.x, yy.y, yy.z, yy.w}});
-                }
-            block_reduce_fr<K + 1>(s_, sm_red);
-            if (tid == 0)
-#pragma unroll
-                for (int x = 0; x <= K; x++) tot[x] = s_[x];
-            __syncthreads();
             if (tid < 32) {
                 const int lane = tid;
                 if (t == 0 && a.compute_claim) {
@@ -956,7 +971,7 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
                     fr_store(&a.d_r[t], rt);
                     fr_canon_to_bytes(fs.rc, a.d_point + 32ull * t);
                     __threadfence();
-                    atomicExch(a.flag, t + 1);
+                    if (!solo) atomicExch(a.flag, t + 1);
                 }
             }
         } else {
