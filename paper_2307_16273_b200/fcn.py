@@ -213,9 +213,39 @@ def prove_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
                                           merge_aux=merge_aux))
 
 
-def _upload_i32(t: torch.Tensor, dev, cctx: api.Context) -> torch.Tensor:
+class HostStack:
+    """A host stack whose trailing slots are zero padding (the stack axis padded to a power of two,
+    P:L144): only the leading `data.shape[0]` slots travel over PCIe; the device tensor has `shape` and its
+    padding slots are zero-filled on the device."""
+
+    def __init__(self, data: torch.Tensor, shape):
+        self.data, self.shape = data, tuple(shape)
+        self.dtype = data.dtype
+
+    def data_ptr(self) -> int:
+        return self.data.data_ptr()
+
+    def numel(self) -> int:
+        return self.data.numel()
+
+    def element_size(self) -> int:
+        return self.data.element_size()
+
+
+def _upload_i32(t, dev, cctx: api.Context) -> torch.Tensor:
     """Host stack -> int32 device tensor on the copy stream (the current stream): int16 host stacks (the
-    end-to-end transport of entries that fit 16 bits) are copied as int16 and widened on the device."""
+    end-to-end transport of entries that fit 16 bits) are copied as int16 and widened on the device;
+    a HostStack's padding slots are zero-filled on the device instead of copied."""
+    if isinstance(t, HostStack):
+        out = torch.empty(t.shape, dtype=torch.int32, device=dev)
+        n = t.data.shape[0]
+        if n < t.shape[0]:
+            out[n:].zero_()
+        if t.data.dtype == torch.int16:
+            api.widen_i16(cctx, t.data.to(dev, non_blocking=True), out=out[:n])
+        else:
+            out[:n].copy_(t.data, non_blocking=True)
+        return out
     if t.dtype == torch.int16:
         return api.widen_i16(cctx, t.to(dev, non_blocking=True))
     return t.to(dev, non_blocking=True)

@@ -775,17 +775,26 @@ def test_e2e_int16_transport_same_proofs(ctx):
     import numpy as np
     from paper_2307_16273_b200 import fcn as dfcn
     from synth import fcn
-    shape = fcn.tiny_shape(steps=2, layers=4, width=64, batch=16, din=128, dout=16)
+    shape = fcn.tiny_shape(steps=2, layers=5, width=64, batch=16, din=128, dout=16)
     fams = fcn.assemble_families(shape, fcn.generate_trace(shape))
     seed, hdr = fs_seed("e2e-i16"), fcn.fcn_header(shape)
     g = dfcn.prove_window(ctx, seed, hdr, dfcn.upload_families(fams))
+    padded = []
 
-    def host(a):
+    def host(a):   # as bench.py: int16 where the entries fit, trailing zero slots not shipped (HostStack)
         small = int(a.max()) < (1 << 15) and int(a.min()) >= -(1 << 15)
-        return torch.from_numpy(a.astype(np.int16) if small else a).pin_memory()
+        nz = np.flatnonzero(a.reshape(a.shape[0], -1).any(axis=1)) if a.ndim > 1 else np.array([0])
+        n = int(nz[-1]) + 1 if nz.size else 1
+        body = a[:n] if a.ndim > 1 else a
+        t = torch.from_numpy(np.ascontiguousarray(body.astype(np.int16) if small else body)).pin_memory()
+        if a.ndim > 1 and n < a.shape[0]:
+            padded.append(a.shape)
+            return dfcn.HostStack(t, a.shape)
+        return t
     hf = [dfcn.DeviceFamily(f.name, "matmul", A=host(f.A), B=host(f.B), trans_a=f.transA, trans_b=f.transB)
           if hasattr(f, "A") else dfcn.DeviceFamily(f.name, "relu", Z=host(f.Z), GA=host(f.GA), Q=f.Q, R=f.R) for f in fams]
     assert any(t.dtype == torch.int16 for f in hf for t in (f.A, f.B, f.Z, f.GA) if t is not None)
+    assert padded   # some stacks travel without their zero padding slots
     h = dfcn.prove_windows_from_host(ctx, [(seed, hdr, hf)])[0]
     assert [r["proof"] for r in h] == [r["proof"] for r in g]
     assert h[-1]["window_state"] == g[-1]["window_state"]
