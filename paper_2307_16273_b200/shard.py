@@ -12,6 +12,7 @@ tests of the host logic with a mock backend) or sequential virtual shards on one
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import torch
@@ -119,7 +120,8 @@ def prove(session, comm, switch_log: int = 12) -> dict:
     """Run the sharded protocol for one rank; every rank returns the same proof.  The torch collectives
     are issued on the session's context stream (the partials are written there)."""
     m = session.m
-    with torch.cuda.stream(session.ctx.stream):
+    ctx = getattr(session, "ctx", None)  # None: a host-side session (the gloo tests' CPU mock)
+    with torch.cuda.stream(ctx.stream) if ctx is not None else contextlib.nullcontext():
         while session.rounds_done < m and session.local_log > switch_log:
             session.finish(comm.allgather(session.partial()))
         if not session.done:
