@@ -232,23 +232,47 @@ class HostStack:
         return self.data.element_size()
 
 
-def _upload_i32(t, dev, cctx: api.Context) -> torch.Tensor:
-    """Host stack -> int32 device tensor on the copy stream (the current stream): int16 host stacks (the
-    end-to-end transport of entries that fit 16 bits) are copied as int16 and widened on the device;
-    a HostStack's padding slots are zero-filled on the device instead of copied."""
-    if isinstance(t, HostStack):
-        out = torch.empty(t.shape, dtype=torch.int32, device=dev)
-        n = t.data.shape[0]
-        if n < t.shape[0]:
-            out[n:].zero_()
-        if t.data.dtype == torch.int16:
-            api.widen_i16(cctx, t.data.to(dev, non_blocking=True), out=out[:n])
-        else:
-            out[:n].copy_(t.data, non_blocking=True)
+class _Uploader:
+    """Host stacks -> int32 device tensors.  The copy stream `cs` carries only the host->device DMA, so the
+    copy engine streams without gaps; the device-side work of an upload (widening an int16 stack,
+    zk_widen_i16, and zero-filling a HostStack's padding slots) runs on a second stream `ws` behind an
+    event per copy.  (On one stream a widen kernel queued behind a long proof kernel holding every SM
+    stalled the DMA of all later stacks.)  ready() gives an event after every upload enqueued so far."""
+
+    def __init__(self, dev, cs):
+        self.dev, self.cs = dev, cs
+        self.ws = torch.cuda.Stream(device=dev)
+        self.wctx = api.Context(dev.index if dev.index is not None else torch.cuda.current_device(), self.ws)
+
+    def upload(self, t) -> torch.Tensor:
+        hs = isinstance(t, HostStack)
+        data = t.data if hs else t
+        if not hs and data.dtype == torch.int32:   # nothing to do on the device: the copy is the upload
+            with torch.cuda.stream(self.cs):
+                out = data.to(self.dev, non_blocking=True)
+            self.ws.wait_stream(self.cs)
+            out.record_stream(self.ws)
+            return out
+        with torch.cuda.stream(self.cs):
+            stage = data.to(self.dev, non_blocking=True)
+        self.ws.wait_stream(self.cs)
+        stage.record_stream(self.ws)
+        with torch.cuda.stream(self.ws):
+            shape = t.shape if hs else tuple(data.shape)
+            out = torch.empty(shape, dtype=torch.int32, device=self.dev)
+            n = data.shape[0]
+            if n < shape[0]:
+                out[n:].zero_()
+            if data.dtype == torch.int16:
+                api.widen_i16(self.wctx, stage, out=out[:n])
+            else:
+                out[:n].copy_(stage)
         return out
-    if t.dtype == torch.int16:
-        return api.widen_i16(cctx, t.to(dev, non_blocking=True))
-    return t.to(dev, non_blocking=True)
+
+    def ready(self) -> torch.cuda.Event:
+        ev = torch.cuda.Event()
+        ev.record(self.ws)
+        return ev
 
 
 def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_families, copy_stream=None,
@@ -264,14 +288,14 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
     for stacks whose entries fit 16 bits: copied as int16 and widened on the device, zk_widen_i16)."""
     dev = torch.device("cuda", ctx.device)
     cs = copy_stream if copy_stream is not None else torch.cuda.Stream(device=dev)
-    cctx = api.Context(ctx.device, cs)
+    up_ = _Uploader(dev, cs)
     fams, ready = [], []
     uploaded = {}   # host buffer -> device tensor: a stack shared by several families is copied once
 
     def upload(t):
         key = (t.data_ptr(), t.numel(), t.dtype)
         if key not in uploaded:
-            uploaded[key] = _upload_i32(t, dev, cctx)
+            uploaded[key] = up_.upload(t)
         return uploaded[key]
 
     # upload (and proof) order: zkReLU families first (least data, most work), then the matmul
@@ -282,20 +306,17 @@ def prove_window_from_host(ctx: api.Context, seed: bytes, header: bytes, host_fa
     order = sorted(range(len(host_families)),
                    key=lambda i: (host_families[i].kind != "relu", -nbytes(host_families[i]), i))
     fams, ready = [None] * len(host_families), [None] * len(host_families)
-    with torch.cuda.stream(cs):
-        for i in order:
-            f = host_families[i]
-            up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
-            g = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
-            readers = [relu_ctx.stream] if (relu_ctx is not None and f.kind == "relu") else \
-                [ctx.stream] + [c.stream for c in (mm_ctxs or [])]
-            for t in up.values():   # the proof reads it on its family's stream
-                for st in readers:
-                    t.record_stream(st)
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            fams[i] = g
-            ready[i] = ev
+    for i in order:
+        f = host_families[i]
+        up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
+        g = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
+        readers = [relu_ctx.stream] if (relu_ctx is not None and f.kind == "relu") else \
+            [ctx.stream] + [c.stream for c in (mm_ctxs or [])]
+        for t in up.values():   # the proof reads it on its family's stream
+            for st in readers:
+                t.record_stream(st)
+        fams[i] = g
+        ready[i] = up_.ready()
     return collect_window(*enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order,
                                           mm_ctxs=mm_ctxs, merge_aux=merge_aux))
 
@@ -309,7 +330,7 @@ def prove_windows_from_host(ctx: api.Context, windows: list, copy_stream=None, r
     prove_window_from_host per window."""
     dev = torch.device("cuda", ctx.device)
     cs = copy_stream if copy_stream is not None else torch.cuda.Stream(device=dev)
-    cctx = api.Context(ctx.device, cs)
+    up_ = _Uploader(dev, cs)
     pending = []
     for seed, header, host_families in windows:
         uploaded = {}
@@ -317,7 +338,7 @@ def prove_windows_from_host(ctx: api.Context, windows: list, copy_stream=None, r
         def upload(t):
             key = (t.data_ptr(), t.numel(), t.dtype)
             if key not in uploaded:
-                uploaded[key] = _upload_i32(t, dev, cctx)
+                uploaded[key] = up_.upload(t)
             return uploaded[key]
 
         def nbytes(f):
@@ -326,19 +347,16 @@ def prove_windows_from_host(ctx: api.Context, windows: list, copy_stream=None, r
         order = sorted(range(len(host_families)),
                        key=lambda i: (host_families[i].kind != "relu", -nbytes(host_families[i]), i))
         fams, ready = [None] * len(host_families), [None] * len(host_families)
-        with torch.cuda.stream(cs):
-            for i in order:
-                f = host_families[i]
-                up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
-                fams[i] = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
-                readers = [relu_ctx.stream] if (relu_ctx is not None and f.kind == "relu") else \
-                    [ctx.stream] + [c.stream for c in (mm_ctxs or [])]
-                for t in up.values():
-                    for st in readers:
-                        t.record_stream(st)
-                ev = torch.cuda.Event()
-                ev.record(cs)
-                ready[i] = ev
+        for i in order:
+            f = host_families[i]
+            up = {k: upload(getattr(f, k)) for k in (("A", "B") if f.kind == "matmul" else ("Z", "GA"))}
+            fams[i] = DeviceFamily(f.name, f.kind, trans_a=f.trans_a, trans_b=f.trans_b, Q=f.Q, R=f.R, **up)
+            readers = [relu_ctx.stream] if (relu_ctx is not None and f.kind == "relu") else \
+                [ctx.stream] + [c.stream for c in (mm_ctxs or [])]
+            for t in up.values():
+                for st in readers:
+                    t.record_stream(st)
+            ready[i] = up_.ready()
         pending.append(enqueue_window(ctx, seed, header, fams, ready, relu_ctx=relu_ctx, proof_order=order,
                                       mm_ctxs=mm_ctxs, merge_aux=merge_aux))
     return [collect_window(*p) for p in pending]
