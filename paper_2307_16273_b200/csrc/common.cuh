@@ -169,6 +169,31 @@ __device__ __forceinline__ void block_reduce_fr(fr_t (&acc)[NV], fr_t* sm /* >= 
     __syncthreads();
 }
 
+// The same with the shuffle levels rolled (~5x less code): for the persistent kernels' once-per-round
+// reductions, whose code must stay in the instruction cache next to the transcript step.
+template <int NV>
+__device__ __forceinline__ void warp_reduce_fr_rolled(fr_t (&acc)[NV]) {
+#pragma unroll 1
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int v = 0; v < NV; v++) acc[v] = fr_add(acc[v], fr_shfl_down(acc[v], off));
+}
+template <int NV>
+__device__ __forceinline__ void block_reduce_fr_rolled(fr_t (&acc)[NV], fr_t* sm /* >= 32*NV */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    warp_reduce_fr_rolled<NV>(acc);
+    if (lane == 0)
+#pragma unroll
+        for (int v = 0; v < NV; v++) sm[wid * NV + v] = acc[v];
+    __syncthreads();
+    if (wid == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; v++) acc[v] = lane < nw ? sm[lane * NV + v] : fr_zero();
+        warp_reduce_fr_rolled<NV>(acc);
+    }
+    __syncthreads();
+}
+
 template <int NV>
 __device__ bool grid_reduce_fr(fr_t (&acc)[NV], fr_t* partials, unsigned int* ticket, fr_t (&out)[NV]) {
     __shared__ fr_t sm[32 * NV];

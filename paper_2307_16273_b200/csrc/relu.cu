@@ -816,6 +816,30 @@ struct IPtrs {   // one side's view of a round (L2 loads: the persistent kernel 
     uint32_t qr_mask, sig_bit, nbytes;
 };
 
+// i-round input prefetch (ZKDL_IR_PREFETCH): one prefetch.global.L2 per 64-byte piece of the next pair
+#ifndef ZKDL_IR_PREFETCH
+#define ZKDL_IR_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// the i-round's three-product groups (ZKDL_IR_MULW): 3 = one three-product body (three interleaved
+// chains, ~21 KB of code), 1 = three calls of the single-product body (~7 KB: inside the L0 I-cache)
+#ifndef ZKDL_IR_MULW
+#define ZKDL_IR_MULW 1
+#endif
+__device__ __forceinline__ fr3_t ir_mul3(const fr_t& a0, const fr_t& b0, const fr_t& a1, const fr_t& b1, const fr_t& a2,
+                                         const fr_t& b2) {
+#if ZKDL_IR_MULW == 3
+    return fr_mul3_ni(a0, b0, a1, b1, a2, b2);
+#else
+    fr3_t r;
+    r.x = fr_mul_ni(a0, b0);
+    r.y = fr_mul_ni(a1, b1);
+    r.z = fr_mul_ni(a2, b2);
+    return r;
+#endif
+}
+
 // a(i) = sum_j beta(r_j, j) bit_j(w_i) as byte-table lookups (the table rows of k_relu_materialize)
 __device__ __forceinline__ fr_t byte_sum(const fr_t* tb, uint32_t w, const IPtrs& q) {
     const uint32_t x = w & q.qr_mask;
@@ -833,6 +857,25 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
     const uint64_t P_blk = 1ull << pb;
     for (uint64_t j = j0; j < P_blk; j += js) {
         const uint64_t b = ((uint64_t)h << pb) + j;
+#if ZKDL_IR_PREFETCH
+        if (j + js < P_blk) {   // the next pair's inputs into L2 (HBM latency off the loop's critical path)
+            const uint64_t bn = b + js;
+            if constexpr (SRC == 1 && FOLD) {
+                prefetch_l2(reinterpret_cast<const int4*>(q.W) + bn);
+                if (side) prefetch_l2(reinterpret_cast<const int4*>(q.Zw) + bn);
+            } else if constexpr (SRC == 1) {
+                prefetch_l2(reinterpret_cast<const int2*>(q.W) + bn);
+                if (side) prefetch_l2(reinterpret_cast<const int2*>(q.Zw) + bn);
+            } else if (FOLD) {
+                prefetch_l2(q.srcA + 4 * bn);
+                prefetch_l2(q.srcA + 4 * bn + 2);
+                prefetch_l2(q.srcO + 4 * bn + 2 * side);
+            } else {
+                prefetch_l2(q.srcA + 2 * bn);
+                prefetch_l2(q.srcO + 2 * bn);
+            }
+        }
+#endif
         fr_t a0, a1, om0, om1;
         int o0 = 0, o1 = 0;
         if constexpr (SRC == 1 && FOLD) {
@@ -865,7 +908,7 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             // oms fold shared by the pair's two lanes: side s folds entry s and stores it
             const fr_t* so = q.srcO + 4 * b + 2 * side;
             const fr_t z0 = fr_load_l2(so), z1 = fr_load_l2(so + 1);
-            const fr3_t f = fr_mul3_ni(r, fr_sub(y1, y0), r, fr_sub(y3, y2), r, fr_sub(z1, z0));
+            const fr3_t f = ir_mul3(r, fr_sub(y1, y0), r, fr_sub(y3, y2), r, fr_sub(z1, z0));
             a0 = fr_add(y0, f.x);
             a1 = fr_add(y2, f.y);
             const fr_t mine = fr_add(z0, f.z);
@@ -889,13 +932,13 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             fr_store(&q.nxC[j], eC);
             if (q.nxB) fr_store(&q.nxB[j], eB);
         }
-        const fr3_t p = fr_mul3_ni(eA, a0, eA, a1, eC, a0);
-        const fr3_t pq = fr_mul3_ni(eC, a1, eB, a0, eB, a1);
+        const fr3_t p = ir_mul3(eA, a0, eA, a1, eC, a0);
+        const fr3_t pq = ir_mul3(eC, a1, eB, a0, eB, a1);
         T[0] = fr_add(T[0], p.x);
         T[1] = fr_add(T[1], p.y);
         const fr_t yC0 = p.z, yC1 = pq.x, zB0 = pq.y, zB1 = pq.z;
         if (FOLD) {
-            const fr3_t c = fr_mul3_ni(yC0, om0, yC1, om1, fr_sub(yC1, yC0), fr_sub(om1, om0));
+            const fr3_t c = ir_mul3(yC0, om0, yC1, om1, fr_sub(yC1, yC0), fr_sub(om1, om0));
             T[2] = fr_add(T[2], c.x);
             T[3] = fr_add(T[3], c.y);
             T[4] = fr_add(T[4], c.z);
@@ -906,7 +949,7 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             T[3] = fr_add(T[3], o1 ? yC1 : zero);
             T[4] = fr_add(T[4], o1 == o0 ? zero : (o1 ? yd : fr_neg(yd)));
         }
-        const fr3_t d = fr_mul3_ni(zB0, fr_sub(a0, one), zB1, fr_sub(a1, one), fr_sub(zB1, zB0), fr_sub(a1, a0));
+        const fr3_t d = ir_mul3(zB0, fr_sub(a0, one), zB1, fr_sub(a1, one), fr_sub(zB1, zB0), fr_sub(a1, a0));
         T[5] = fr_add(T[5], d.x);
         T[6] = fr_add(T[6], d.y);
         T[7] = fr_add(T[7], d.z);

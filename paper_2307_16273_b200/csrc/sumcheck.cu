@@ -14,6 +14,8 @@
 // beta(w_s, 0) + beta(w_s, 1) = 1, LO_{t+1}[c] = LO_t[2c] + LO_t[2c+1]: the round kernel writes the next
 // LO level with additions only.  Once LO is exhausted the HI table is pair-summed the same way.
 #include <cstdlib>
+#include <cstdio>
+#include <vector>
 
 #include "sumcheck.cuh"
 #include "tables.cuh"
@@ -813,8 +815,14 @@ struct ScAllArgs {
     unsigned int* arrive;       // monotonic: blocks that finished round t = (t+1) * gridDim.x
     unsigned int* flag;         // rounds whose challenge is published
     const fr_t* r_first;        // continuation of a larger statement: round 0 folds by this challenge
+    unsigned long long* trace;  // diagnostics (ZKDL_SCALL_TRACE): 4 timestamps per round (block 0), or null
 };
 
+__device__ __forceinline__ unsigned long long sc_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
     unsigned int v;
     asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -830,8 +838,11 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
     const uint32_t m = a.m, n_eq = a.n_eq;
     const int tid = threadIdx.x;
     if (blockIdx.x == 0 && tid < 32) fs_begin(fs, a.st);
+    const long long c_start = clock64();
+    const unsigned long long g_start = a.trace ? sc_globaltimer() : 0ull;
     for (uint32_t t = 0; t < m; t++) {
         const uint64_t n_pairs = 1ull << (m - t - 1);
+        if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[10 * t] = sc_globaltimer();
         // the last rounds (<= SC_SOLO_PAIRS pairs) run on the reducer block alone: no partials, arrival
         // counter or round flag, one __syncthreads per round (the workers' last folds are visible: they
         // fenced before their final arrival, which block 0 waited for)
@@ -865,14 +876,34 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
         const uint64_t bs = solo ? (uint64_t)blockDim.x : nworkers * blockDim.x;
         for (uint64_t b = b0; b < n_pairs; b += bs) {
             fr_t lo[K], d[K];
+            // out-of-line product bodies: the kernel's code stays inside the instruction cache (the inlined
+            // products made k_sc_all ~290 KB of SASS, every round re-fetched from L2); K = 2 groups its
+            // independent products in pairs / triples (shorter per-pair latency in the small rounds)
+            if (K == 2 && folding) {
+                const fr_t* s0 = src[0] + 4 * b;
+                const fr_t* s1 = src[K - 1] + 4 * b;
+                const fr_t x0 = fr_load_l2(s0), x1 = fr_load_l2(s0 + 1), x2 = fr_load_l2(s0 + 2), x3 = fr_load_l2(s0 + 3);
+                const fr_t y0 = fr_load_l2(s1), y1 = fr_load_l2(s1 + 1), y2 = fr_load_l2(s1 + 2), y3 = fr_load_l2(s1 + 3);
+                const fr2p_t f = fr_mul2_ni(r, fr_sub(x1, x0), r, fr_sub(x3, x2));
+                const fr2p_t g = fr_mul2_ni(r, fr_sub(y1, y0), r, fr_sub(y3, y2));
+                const fr_t v0 = fr_add(x0, f.x), v1 = fr_add(x2, f.y), w0 = fr_add(y0, g.x), w1 = fr_add(y2, g.y);
+                fr_store(dst[0] + 2 * b, v0);
+                fr_store(dst[0] + 2 * b + 1, v1);
+                fr_store(dst[K - 1] + 2 * b, w0);
+                fr_store(dst[K - 1] + 2 * b + 1, w1);
+                lo[0] = v0;
+                d[0] = fr_sub(v1, v0);
+                lo[K - 1] = w0;
+                d[K - 1] = fr_sub(w1, w0);
+            } else
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 fr_t v0, v1;
                 if (folding) {
                     const fr_t* s = src[k] + 4 * b;
                     fr_t x0 = fr_load_l2(s), x1 = fr_load_l2(s + 1), x2 = fr_load_l2(s + 2), x3 = fr_load_l2(s + 3);
-                    v0 = fr_add(x0, fr_mul(r, fr_sub(x1, x0)));
-                    v1 = fr_add(x2, fr_mul(r, fr_sub(x3, x2)));
+                    v0 = fr_add(x0, fr_mul_ni(r, fr_sub(x1, x0)));
+                    v1 = fr_add(x2, fr_mul_ni(r, fr_sub(x3, x2)));
                     fr_store(dst[k] + 2 * b, v0);
                     fr_store(dst[k] + 2 * b + 1, v1);
                 } else {
@@ -894,29 +925,41 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
                                                fr_t{{b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w}}));
                 }
             }
-            fr_t v[K];
+            if (K == 2) {   // the three evaluations (X = 0, 1, 2), then their eq weights, as triples
+                const fr_t a1 = fr_add(lo[0], d[0]), b1 = fr_add(lo[K - 1], d[K - 1]);
+                const fr3_t p = fr_mul3_ni(lo[0], lo[K - 1], a1, b1, fr_add(a1, d[0]), fr_add(b1, d[K - 1]));
+                fr3_t q = p;
+                if (has_e) q = fr_mul3_ni(p.x, e, p.y, e, p.z, e);
+                acc[0] = fr_add(acc[0], q.x);
+                acc[1] = fr_add(acc[1], q.y);
+                acc[K] = fr_add(acc[K], q.z);
+            } else {
+                fr_t v[K];
 #pragma unroll
-            for (int k = 0; k < K; k++) v[k] = lo[k];
+                for (int k = 0; k < K; k++) v[k] = lo[k];
 #pragma unroll
-            for (int x = 0; x <= K; x++) {
-                fr_t p = v[0];
+                for (int x = 0; x <= K; x++) {
+                    fr_t p = v[0];
 #pragma unroll
-                for (int k = 1; k < K; k++) p = fr_mul(p, v[k]);
-                if (has_e) p = fr_mul(p, e);
-                acc[x] = fr_add(acc[x], p);
-                if (x < K)
+                    for (int k = 1; k < K; k++) p = fr_mul_ni(p, v[k]);
+                    if (has_e) p = fr_mul_ni(p, e);
+                    acc[x] = fr_add(acc[x], p);
+                    if (x < K)
 #pragma unroll
-                    for (int k = 0; k < K; k++) v[k] = fr_add(v[k], d[k]);
+                        for (int k = 0; k < K; k++) v[k] = fr_add(v[k], d[k]);
+                }
             }
         }
         if (solo) {   // block 0 alone: its own sums are the round totals
-            block_reduce_fr<K + 1>(acc, sm_red);
+            block_reduce_fr_rolled<K + 1>(acc, sm_red);
             if (tid == 0)
 #pragma unroll
                 for (int x = 0; x <= K; x++) tot[x] = acc[x];
             __syncthreads();
         } else if (blockIdx.x != 0) {   // worker: publish the block partial
-            block_reduce_fr<K + 1>(acc, sm_red);
+            if (a.trace && blockIdx.x == 1 && tid == 0) a.trace[10 * t + 6] = sc_globaltimer();
+            block_reduce_fr_rolled<K + 1>(acc, sm_red);
+            if (a.trace && blockIdx.x == 1 && tid == 0) a.trace[10 * t + 7] = sc_globaltimer();
             if (tid == 0) {
 #pragma unroll
                 for (int x = 0; x <= K; x++) fr_store(&a.partials[(blockIdx.x - 1) * (K + 1) + x], acc[x]);
@@ -930,6 +973,7 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
                     while (ld_volatile(a.arrive) < (t + 1) * (gridDim.x - 1)) {
                     }
                     __threadfence();
+                    if (a.trace) a.trace[10 * t + 1] = sc_globaltimer();
                 }
                 __syncthreads();
                 fr_t s_[K + 1];
@@ -942,12 +986,13 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
                         uint4 xx = __ldcg(q), yy = __ldcg(q + 1);
                         s_[x] = fr_add(s_[x], fr_t{{xx.x, xx.y, xx.z, xx.w, yy.x, yy.y, yy.z, yy.w}});
                     }
-                block_reduce_fr<K + 1>(s_, sm_red);
+                block_reduce_fr_rolled<K + 1>(s_, sm_red);
                 if (tid == 0)
 #pragma unroll
                     for (int x = 0; x <= K; x++) tot[x] = s_[x];
                 __syncthreads();
             }
+            if (a.trace && tid == 0) a.trace[10 * t + 2] = sc_globaltimer();
             if (tid < 32) {
                 const int lane = tid;
                 if (t == 0 && a.compute_claim) {
@@ -965,13 +1010,23 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
                     __syncwarp();
                     fs_absorb_frs(fs, "sc/claim", claim_sm, 1, a.proof + 12);
                 }
+                const long long ca = clock64();
                 fs_absorb_frs(fs, "sc/msg", lane <= K ? tot[lane & 3] : fr_zero(), K + 1, a.proof + 44 + 32ull * t * (K + 1));
+                const long long cb = clock64();
+                if (a.trace && lane == 0) a.trace[10 * t + 3] = sc_globaltimer();
                 fr_t rt = fs_challenge(fs, "sc/r");
+                const long long cc = clock64();
+                if (a.trace && lane == 0) {
+                    a.trace[10 * t + 4] = sc_globaltimer();
+                    a.trace[10 * t + 8] = (unsigned long long)(cb - ca);
+                    a.trace[10 * t + 9] = (unsigned long long)(cc - cb);
+                }
                 if (lane == 0) {
                     fr_store(&a.d_r[t], rt);
                     fr_canon_to_bytes(fs.rc, a.d_point + 32ull * t);
                     __threadfence();
                     if (!solo) atomicExch(a.flag, t + 1);
+                    if (a.trace) a.trace[10 * t + 5] = sc_globaltimer();
                 }
             }
         } else {
@@ -998,6 +1053,10 @@ __global__ void __launch_bounds__(256) k_sc_all(ScAllArgs a) {
         }
         fs_absorb_frs(fs, "sc/final", f, K, a.proof + 44 + 32ull * m * (K + 1));
         fs_end(fs, a.st);
+        if (a.trace && lane == 0) {   // SM clock of the reducer block over the launch
+            a.trace[10ull * m] = (unsigned long long)(clock64() - c_start);
+            a.trace[10ull * m + 1] = sc_globaltimer() - g_start;
+        }
     }
 }
 
@@ -1078,9 +1137,26 @@ static void sumcheck_prove_small(zk_ctx* ctx, zk_transcript* tr, const ScStateme
     unsigned int* ctr = s.alloc_zero<unsigned int>(2);
     a.arrive = ctr;
     a.flag = ctr + 1;
+    static const bool trace = getenv("ZKDL_SCALL_TRACE") != nullptr;
+    if (trace) a.trace = s.alloc_zero<unsigned long long>(10ull * m + 2);
     if (K == 1) launch_all<1>(ctx, a, grid);
     else if (K == 2) launch_all<2>(ctx, a, grid);
     else launch_all<3>(ctx, a, grid);
+    if (trace) {
+        std::vector<unsigned long long> h(10ull * m + 2);
+        ZK_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        ZK_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (uint32_t t = 0; t < m; t++) {
+            const unsigned long long* q = &h[10ull * t];
+            const unsigned long long nx = t + 1 < m ? h[10ull * (t + 1)] : q[5];
+            auto us = [](unsigned long long a, unsigned long long b) { return a && b ? ((long long)b - (long long)a) / 1e3 : 0.0; };
+            fprintf(stderr, "sc_all m=%u grid=%u t=%u arrive %.1f us, reduce %.1f, absorb %.1f, challenge %.1f, publish %.1f, "
+                    "next %.1f | worker1 compute done %.1f, block reduce %.1f | absorb %llu cycles, challenge %llu\n", m, grid, t, us(q[0], q[1]),
+                    q[1] ? us(q[1], q[2]) : us(q[0], q[2]), us(q[2], q[3]), us(q[3], q[4]), us(q[4], q[5]), us(q[5], nx),
+                    us(q[0], q[6]), us(q[6], q[7]), q[8], q[9]);
+        }
+        fprintf(stderr, "sc_all m=%u: reducer block SM clock %.3f GHz\n", m, (double)h[10ull * m] / (double)h[10ull * m + 1]);
+    }
 }
 
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {

@@ -45,7 +45,7 @@ __global__ void k_check(uint64_t n, unsigned long long* bad, fr_t* first_bad) {
     }
 }
 
-template <int C, int MODE>   // MODE 0: integer CIOS, 1: FP64, 2: half the chains each
+template <int C, int MODE>   // MODE 0: integer CIOS, 1: FP64, 2: half the chains each, 3: odd warps integer, even warps FP64
 __global__ void __launch_bounds__(256) k_rate(const fr_t* seed, uint32_t iters, fr_t* out) {
     fr_t x[C];
     const fr_t y = seed[(threadIdx.x + 1) & 1023];
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_rate(const fr_t* seed, uint32_t iters, 
     for (uint32_t i = 0; i < iters; i++) {
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            if (MODE == 0 || (MODE == 2 && (c & 1))) x[c] = fr_mul(x[c], y);
+            if (MODE == 0 || (MODE == 2 && (c & 1)) || (MODE == 3 && ((threadIdx.x >> 5) & 1))) x[c] = fr_mul(x[c], y);
             else x[c] = fr_mul_f64(x[c], y);
         }
     }
@@ -119,6 +119,11 @@ int main() {
     rate<2, 2>("mixed", seed, out, 0);
     rate<4, 2>("mixed", seed, out, 0);
     for (int bps : {1, 2, 3, 4}) rate<2, 1>("fp64", seed, out, bps);
+    rate<1, 3>("per_warp_mixed", seed, out, 0);
+    rate<2, 3>("per_warp_mixed", seed, out, 0);
+    rate<3, 3>("per_warp_mixed", seed, out, 0);
+    rate<3, 1>("fp64", seed, out, 0);
+    rate<3, 0>("int_cios", seed, out, 0);
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("cuda error %s\n", cudaGetErrorString(e)); return 1; }
     return 0;
