@@ -458,6 +458,15 @@ def run_ours(args, rank, world, local):
                                            relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, merge_aux=args.merge_aux)
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    uploads_ms = None
+    if e2e_steps:   # the transport alone (same uploads, no proofs): what the e2e value is bound by
+        with torch.cuda.stream(stream):
+            dfcn.upload_windows([host_fams] * e2e_steps, copy_stream, local)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dfcn.upload_windows([host_fams] * e2e_steps, copy_stream, local)
+            torch.cuda.synchronize()
+            uploads_ms = 1e3 * (time.perf_counter() - t0) / e2e_steps
     h2d = sum(t.numel() * t.element_size() for t in pinned.values())   # distinct stacks (real slots), copied once each
     d2h = dfcn.window_out_bytes(dev_fams, bool(args.merge_aux)) + 4     # proofs, points, states + range flag
     e2e_value = e2e_s / (world * e2e_steps * shape.steps) if e2e_steps else None
@@ -525,7 +534,8 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "fcn.prove_windows_from_host: pinned host stacks -> HBM per family on a copy stream "
                         "(shared stacks once per window), each window's uploads behind the previous window's and "
-                        "overlapped with the proofs; proofs back to the host", "windows": e2e_steps},
+                        "overlapped with the proofs; proofs back to the host", "windows": e2e_steps,
+                "uploads_alone_ms_per_window": None if uploads_ms is None else round(uploads_ms, 3)},
         "roofline": rf,
         "n1_relu_aux_merge": n1,
         "n3_chained_window": chained,

@@ -44,13 +44,15 @@ zk_status zk_ctx_create(int device, void* cuda_stream, zk_ctx** out) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device || device < 0) return ZK_ERR_CUDA;
     if (cudaSetDevice(device) != cudaSuccess) return ZK_ERR_CUDA;
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return ZK_ERR_CUDA;
-    if (prop.major != 10) return ZK_ERR_CUDA;   // built for sm_100a only
+    int major = 0, sms = 0;   // (two attribute queries: cudaGetDeviceProperties costs milliseconds)
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+        return ZK_ERR_CUDA;
+    if (major != 10) return ZK_ERR_CUDA;   // built for sm_100a only
     zk_ctx* c = new zk_ctx();
     c->device = device;
     c->stream = (cudaStream_t)cuda_stream;
-    c->num_sms = prop.multiProcessorCount;
+    c->num_sms = sms;
     // keep freed scratch in the pool (no release back to the OS between calls)
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
