@@ -467,6 +467,232 @@ static void rowdot_tma_launch(zk_ctx* ctx, const RtArgs& a) {
     ZK_LAUNCH(ctx, k_rowdot_tma, grid, RT_THREADS, smem, a, map);
 }
 
+// ---------------------------------------------------------------- column sums on the tensor cores (round 2)
+// out[c * N + n] = sum_r E2[r] M[n][r][c] (colsum_i32) for an int32 stack M[N][rows][cols]: the contraction
+// index r is the row index of the stored matrix, so the A operand is MN-major — M = 128 byte columns
+// (32 int32 columns x 4 byte positions, contiguous in memory), K = 32 matrix rows — and the TMA unit moves
+// it untransformed: a box of 32 rows x 128 bytes with 128-byte swizzle is exactly the MN-major SW128 layout
+// (instruction descriptor bit 15; validated by scripts/tc_mn_probe.cu for u8 and s8).  B = the 32 limb bytes
+// of E2 for those 32 rows (K-major, one 1 KB image per K step), N = 32:
+//     D[4 c + l][q] = sum_r byte_l(M[n][r][c]) e_q(r),   X_c = sum_{l, q} 2^{8 (l + q)} D[4 c + l][q]
+// with the top byte signed (a second MMA reads A as s8; lane 4c+3 takes that result).  |D| < rows 2^16, so
+// rows <= 4096.  The epilogue forms each lane's 320-bit two's-complement partial, shifts it by 8 l, adds the
+// four byte lanes of a column by shuffles, adds the bias 2^31 S (S = sum_r E2[r]) and reduces (wide_finish),
+// as k_colsum_i32 does with u = v + 2^31.  Roles: warp 0 the TMA producer, warp 1 the MMA issuer, warps 2-5
+// the epilogue over a double-buffered accumulator (64 TMEM columns each: u8 result, s8 result).
+constexpr int CT_SKS = 8;                  // K steps (32 rows each) per stage
+constexpr int CT_STAGES = 4;
+constexpr uint32_t CT_IDESC_U = (2u << 4) | (1u << 15) | ((32u >> 3) << 17) | ((128u >> 4) << 24);   // A MN-major
+constexpr uint32_t CT_IDESC_S = CT_IDESC_U | (1u << 7);
+constexpr int CT_THREADS = 6 * 32;
+
+struct __align__(1024) CtSmem {
+    uint8_t A[CT_STAGES][CT_SKS][32 * 128];
+    uint8_t B[CT_STAGES][CT_SKS][1024];
+    uint64_t full[CT_STAGES], empty[CT_STAGES], accfull[2], accempty[2];
+    uint32_t tmem;
+};
+
+struct CtArgs {
+    uint64_t N;
+    uint32_t rows, cols;
+    const uint8_t* Bimg;     // [rows / 32][1024]: limb q of E2[32 ks + kb] at rt_off(q, kb)
+    const uint32_t* bias;
+    fr_t* out;
+};
+
+// B images of the column sums: K step ks holds E2[32 ks .. 32 ks + 31] as 32 limb rows (K-major, no swizzle)
+__global__ void k_ct_bimg(const fr_t* E2, uint32_t rows, uint8_t* Bimg) {
+    const uint64_t total = (uint64_t)rows * 32;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t q = (uint32_t)(g % 32), r = (uint32_t)(g / 32);
+        const uint32_t limb = __ldg(&E2[r].v[q >> 2]);
+        Bimg[(uint64_t)(r / 32) * 1024 + rt_off(q, r % 32)] = (uint8_t)(limb >> (8 * (q & 3)));
+    }
+}
+
+__global__ void __launch_bounds__(CT_THREADS, 1) k_colsum_tma(CtArgs a, const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(1024) uint8_t ct_raw[];
+    CtSmem& S = *reinterpret_cast<CtSmem*>(ct_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t KS = a.rows / 32, KSS = (KS + CT_SKS - 1) / CT_SKS, CB = a.cols / 32;
+    const uint64_t ntiles = a.N * CB;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(su32(&S.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (lane == 0) {
+            for (int i = 0; i < CT_STAGES; i++) {
+                mbar_init(&S.full[i], 1);
+                mbar_init(&S.empty[i], 1);
+            }
+            for (int i = 0; i < 2; i++) {
+                mbar_init(&S.accfull[i], 1);
+                mbar_init(&S.accempty[i], 4);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;");
+        }
+    }
+    if (warp == 0 && lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = S.tmem;
+    if (warp == 0) {
+        // ---------------- producer: one thread, one transaction-counted barrier per stage
+        if (lane == 0) {
+            uint64_t it = 0;
+            for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const uint64_t n = tile / CB, cb = tile % CB;
+                for (uint32_t sg = 0; sg < KSS; sg++, it++) {
+                    const uint32_t st = it % CT_STAGES;
+                    if (it >= CT_STAGES) rt_wait(&S.empty[st], ((it / CT_STAGES) - 1) & 1, 21);
+                    const uint32_t k0 = sg * CT_SKS, nk = KS - k0 < (uint32_t)CT_SKS ? KS - k0 : (uint32_t)CT_SKS;
+                    mbar_expect_tx(&S.full[st], nk * (32 * 128 + 1024));
+                    for (uint32_t kk = 0; kk < nk; kk++)
+                        tma_load_2d(S.A[st][kk], &tmap, (int32_t)(cb * 128), (int32_t)(n * a.rows + 32 * (k0 + kk)), &S.full[st]);
+                    bulk_g2s(S.B[st][0], a.Bimg + (uint64_t)k0 * 1024, nk * 1024, &S.full[st]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        uint64_t it = 0, ti = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+            const uint32_t buf = ti & 1;
+            if (ti >= 2) rt_wait(&S.accempty[buf], ((ti / 2) - 1) & 1, 22);
+            tc_fence_after();
+            for (uint32_t sg = 0; sg < KSS; sg++, it++) {
+                const uint32_t st = it % CT_STAGES;
+                rt_wait(&S.full[st], (it / CT_STAGES) & 1, 23);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t k0 = sg * CT_SKS, nk = KS - k0 < (uint32_t)CT_SKS ? KS - k0 : (uint32_t)CT_SKS;
+                    for (uint32_t kk = 0; kk < nk; kk++) {
+                        const uint64_t ad = adesc_sw128(S.A[st][kk]), bd = bdesc(S.B[st][kk]);
+                        mma_i8_ss(tmem + 64 * buf, ad, bd, CT_IDESC_U, (k0 + kk) > 0);
+                        mma_i8_ss(tmem + 64 * buf + 32, ad, bd, CT_IDESC_S, (k0 + kk) > 0);
+                    }
+                    mma_commit(&S.empty[st]);
+                    if (sg + 1 == KSS) mma_commit(&S.accfull[buf]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- epilogue: warp w drains TMEM lanes 32 (w mod 4) .. + 31 (lane = byte column 4 c + l)
+        const uint32_t q = warp & 3, l = lane & 3;
+        uint32_t bias[10];
+#pragma unroll
+        for (int i = 0; i < 10; i++) bias[i] = l == 0 ? __ldg(&a.bias[i]) : 0u;
+        uint64_t ti = 0;
+        for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+            const uint32_t buf = ti & 1;
+            rt_wait(&S.accfull[buf], (ti / 2) & 1, 24);
+            tc_fence_after();
+            uint32_t d[32];
+            {
+                const uint32_t taddr = tmem + ((32 * q) << 16) + 64 * buf;
+                uint32_t du[32], ds[32];
+                tmem_ld32(taddr, du);
+                tmem_ld32(taddr + 32, ds);
+#pragma unroll
+                for (int i = 0; i < 32; i++) d[i] = l == 3 ? ds[i] : du[i];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.accempty[buf]);
+            // this lane's partial sum_q 2^{8 q} D[q] as 320-bit two's complement
+            int64_t acc[10];
+#pragma unroll
+            for (int i = 0; i < 10; i++) acc[i] = 0;
+#pragma unroll
+            for (int s = 0; s < 32; s++) acc[s >> 2] += (int64_t)(int32_t)d[s] << (8 * (s & 3));
+            uint32_t w[10];
+            int64_t carry = 0;
+#pragma unroll
+            for (int i = 0; i < 10; i++) {
+                const int64_t v = acc[i] + carry;
+                w[i] = (uint32_t)v;
+                carry = v >> 32;
+            }
+            // times 2^{8 l}, then the four byte lanes of the column added by shuffles (mod 2^320), + bias
+            if (l) {
+                const uint32_t sh = 8 * l;
+#pragma unroll
+                for (int i = 9; i > 0; i--) w[i] = (w[i] << sh) | (w[i - 1] >> (32 - sh));
+                w[0] <<= sh;
+            }
+            uint32_t c0 = 0;
+#pragma unroll
+            for (int i = 0; i < 10; i++) {   // + bias (lane l = 0 only; the others add zero)
+                const uint64_t v = (uint64_t)w[i] + bias[i] + c0;
+                w[i] = (uint32_t)v;
+                c0 = (uint32_t)(v >> 32);
+            }
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                uint32_t o[10];
+#pragma unroll
+                for (int i = 0; i < 10; i++) o[i] = __shfl_xor_sync(0xffffffffu, w[i], off);
+                uint32_t cc = 0;
+#pragma unroll
+                for (int i = 0; i < 10; i++) {
+                    const uint64_t v = (uint64_t)w[i] + o[i] + cc;
+                    w[i] = (uint32_t)v;
+                    cc = (uint32_t)(v >> 32);
+                }
+            }
+            if (l == 0) {
+                const uint64_t n = tile / CB, c = (tile % CB) * 32 + 8 * q + (lane >> 2);
+                fr_store(&a.out[c * a.N + n], wide_finish(w));
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+bool colsum_tc_ok(uint64_t N, uint32_t rows, uint32_t cols) {
+    static const bool off = getenv("ZKDL_COLSUM_TC") && atoi(getenv("ZKDL_COLSUM_TC")) == 0;
+    return !off && cols % 32 == 0 && rows % 32 == 0 && rows >= 32 && rows <= 4096 && N * (cols / 32) >= 148 &&
+           N * rows * 4ull * cols >= (8ull << 20);
+}
+
+void colsum_tc(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
+               Scratch& s) {
+    uint8_t* Bimg = s.alloc<uint8_t>((size_t)rows * 32);
+    ZK_LAUNCH(ctx, k_ct_bimg, grid_for(ctx, (uint64_t)rows * 32, 256, 4), 256, 0, E2, rows, Bimg);
+    uint32_t* bias = s.alloc<uint32_t>(10);
+    ZK_LAUNCH(ctx, k_rt_bias, 1, 1024, 0, E2, rows, bias);
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    ZK_REQUIRE(enc != nullptr, ZK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols * 4, (cuuint64_t)N * rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    const cuuint32_t box[2] = {128, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int32_t*>(M), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    ZK_REQUIRE(r == CUDA_SUCCESS, ZK_ERR_CUDA, "cuTensorMapEncodeTiled failed (column sums)");
+    CtArgs a;
+    a.N = N;
+    a.rows = rows;
+    a.cols = cols;
+    a.Bimg = Bimg;
+    a.bias = bias;
+    a.out = out;
+    const size_t smem = sizeof(CtSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        ZK_CUDA(cudaFuncSetAttribute(k_colsum_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const uint64_t ntiles = N * (cols / 32);
+    const unsigned int grid = (unsigned int)(ntiles < (uint64_t)ctx->num_sms ? ntiles : (uint64_t)ctx->num_sms);
+    ZK_LAUNCH(ctx, k_colsum_tma, grid, CT_THREADS, smem, a, map);
+}
+
 bool rowdot_tc_ok(uint64_t nrows, uint32_t cols) {
     static const bool off = getenv("ZKDL_ROWDOT_TC") && atoi(getenv("ZKDL_ROWDOT_TC")) == 0;
     return !off && cols % 8 == 0 && cols >= 8 && cols <= 4096 && nrows >= 1024;

@@ -546,6 +546,10 @@ __global__ void k_colsum_rows_finish(const uint32_t* partials, uint64_t N, uint3
 
 void colsum_i32(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
                 Scratch& s) {
+    if (colsum_tc_ok(N, rows, cols)) {   // tensor cores (TMA + MN-major int8 MMAs)
+        colsum_tc(ctx, M, N, rows, cols, E2, out, s);
+        return;
+    }
     // wide stacks with many row units: the row-streaming kernel (ZKDL_COLSUM_ROWS=0 disables it)
     static const bool rows_off = getenv("ZKDL_COLSUM_ROWS") && atoi(getenv("ZKDL_COLSUM_ROWS")) == 0;
     if (!rows_off && (cols == 512 || cols == 1024) && N * rows >= 64ull * ctx->num_sms) {

@@ -201,6 +201,12 @@ void mle_i32_relu(zk_ctx* ctx, int kind /*0 A, 1 GZ, 2 Z' = round(Z / 2^R)*/, co
 // results as k_rowdot_i32<LoadPlain>; rowdot_tc_ok says whether the shape is supported (cols % 8 == 0,
 // cols <= 4096, >= 1024 rows; ZKDL_ROWDOT_TC=0 disables it).
 bool rowdot_tc_ok(uint64_t nrows, uint32_t cols);
+// Column sums on the tensor cores (restrict_tc.cu: MN-major int8 MMAs fed by TMA), the same results as
+// colsum_i32; colsum_tc_ok: cols % 32 == 0, rows % 32 == 0, 32 <= rows <= 4096, at least one tile per SM
+// (ZKDL_COLSUM_TC=0 disables it)
+bool colsum_tc_ok(uint64_t N, uint32_t rows, uint32_t cols);
+void colsum_tc(zk_ctx* ctx, const int32_t* M, uint64_t N, uint32_t rows, uint32_t cols, const fr_t* E2, fr_t* out,
+               Scratch& s);
 void rowdot_tc(zk_ctx* ctx, const int32_t* M, uint64_t nrows, uint32_t cols, const fr_t* E2, fr_t* out, uint64_t inner,
                uint32_t log_inner, uint64_t outer, Scratch& s, int use_tma = -1 /* -1: default (ZKDL_ROWDOT_TMA), 0: cp.async producer, 1: TMA */);
 void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,

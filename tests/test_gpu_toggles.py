@@ -4,7 +4,8 @@ alternative path a switch selects is run in a subprocess and compared with the o
     ZKDL_SC_INT0=0       C5 round 0 through the embedding kernel instead of the integer round 0
     ZKDL_RELU_WORDS=0    zkReLU i-rounds 0/1 from materialised tables instead of the words
     ZKDL_MLE4_FUSED=0    the four zkReLU claims through four row-dot launches
-    ZKDL_COLSUM_ROWS=0   wide column sums through the column-strip kernel
+    ZKDL_COLSUM_TC=0     column sums on the CUDA cores instead of the tensor cores (TMA + MN-major int8 MMAs)
+    ZKDL_COLSUM_ROWS=0   wide CUDA-core column sums through the column-strip kernel
     ZKDL_ROWDOT_TC=0     restriction row dots on the CUDA cores instead of the tensor cores
 """
 import json
@@ -88,11 +89,12 @@ def test_relu_paths(oracle_lib, env):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("ta,tb,env", [(0, 1, {"ZKDL_COLSUM_ROWS": "0"}), (0, 1, {}),
+@pytest.mark.parametrize("ta,tb,env", [(0, 1, {"ZKDL_COLSUM_TC": "0", "ZKDL_COLSUM_ROWS": "0"}),
+                                       (0, 1, {"ZKDL_COLSUM_TC": "0"}), (0, 1, {}),
                                        (1, 0, {"ZKDL_ROWDOT_TC": "0"}), (1, 0, {})])
 def test_restriction_paths(oracle_lib, ta, tb, env):
-    """The row-streaming and column-strip column sums (A, B^T stacks: column sums over 1024 rows of 512
-    columns), and the tensor-core and CUDA-core row dots (A^T, B stacks): the restricted tables At, Bt
+    """The tensor-core, row-streaming and column-strip column sums (A, B^T stacks: column sums over 1024 rows
+    of 512 columns), and the tensor-core and CUDA-core row dots (A^T, B stacks): the restricted tables At, Bt
     ([D2][N], every entry) and the claim equal the oracle's (or_matmul_reduce)."""
     from synth.prng import fs_seed, uniform_range
     N, D1, D2, D3 = 16, 1024, 512, 1024
