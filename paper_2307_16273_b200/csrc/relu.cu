@@ -1195,6 +1195,8 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
         const int lv = t & 1, hv = (t - a.t0) & 1;
         if (blockIdx.x != 0) {
             if (t > a.t0) wait_counter(a.flag, t);   // r_{t-1}, the LO level and the folded tables
+            unsigned long long* wtr = (a.trace && blockIdx.x == 1 && threadIdx.x == 0) ? a.trace + 4ull * (a.t1 - a.t0) + 4ull * (t - a.t0) : nullptr;
+            if (wtr) wtr[0] = globaltimer_ns();
             const uint32_t w = blockIdx.x - 1, h = w / a.cpb, cib = w % a.cpb;
             IPtrs q;
             const fr_t* const* src = t == 1 ? a.full : (const fr_t* const*)a.buf[(t - 1) & 1];
@@ -1214,7 +1216,9 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
             for (int k = 0; k < 8; k++) T[k] = fr_zero();
             const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
             iround_pairs<true>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+            if (wtr) wtr[1] = globaltimer_ns();
             if (t > a.t0) wait_counter(a.hiflag, t);   // HI' rescaled by round t-1
+            if (wtr) wtr[2] = globaltimer_ns();
             fr_t v[16];
             iround_scale_scatter(T, a.hi[hv], h, side, j0 < (1ull << pb), v);
             block_transpose_sum16(v, sm);
@@ -1223,6 +1227,7 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
             if (threadIdx.x == 0) {
                 __threadfence();
                 atomicAdd(a.arrive, 1u);
+                if (wtr) wtr[3] = globaltimer_ns();
             }
         } else {
             wait_counter(a.arrive, (t - a.t0 + 1) * nworkers);
@@ -1641,7 +1646,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         pa.flag = ctr + 1;
         pa.hiflag = ctr + 2;
         static const bool trace = getenv("ZKDL_IPERSIST_TRACE") != nullptr;
-        if (trace) pa.trace = s.alloc_zero<unsigned long long>(4ull * (H - t0) + 1);
+        if (trace) pa.trace = s.alloc_zero<unsigned long long>(8ull * (H - t0) + 1);
         void* args[] = {(void*)&pa};
         cudaEvent_t ev_a = nullptr, ev_b = nullptr;
         const bool prof = ctx->prof_match("k_relu_ipersist");
@@ -1660,14 +1665,18 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         if ((H - t0) & 1)   // the last persistent round rescaled HI' into the second buffer
             for (int x = 0; x < 6; x++) HIs[x] = pa.hi[1][x];
         if (trace) {
-            std::vector<unsigned long long> h(4ull * (H - t0));
+            std::vector<unsigned long long> h(8ull * (H - t0));
             ZK_CUDA(cudaMemcpyAsync(h.data(), pa.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
             ZK_CUDA(cudaStreamSynchronize(ctx->stream));
             for (uint32_t t = t0; t < H; t++) {
                 const unsigned long long* q = &h[4ull * (t - t0)];
                 const unsigned long long prev = t > t0 ? h[4ull * (t - t0) - 2] : q[0];
-                fprintf(stderr, "ipersist t=%u workers %.1f us, reduce %.1f, g+transcript %.1f, update %.1f\n", t,
-                        (q[0] - prev) / 1e3, (q[1] - q[0]) / 1e3, (q[2] - q[1]) / 1e3, (q[3] - q[2]) / 1e3);
+                const unsigned long long* wq = &h[4ull * (H - t0) + 4ull * (t - t0)];
+                fprintf(stderr, "ipersist t=%u workers %.1f us, reduce %.1f, g+transcript %.1f, update %.1f | worker1: "
+                        "woke +%.1f, pairs %.1f, hi wait %.1f, reduce+publish %.1f\n", t,
+                        (q[0] - prev) / 1e3, (q[1] - q[0]) / 1e3, (q[2] - q[1]) / 1e3, (q[3] - q[2]) / 1e3,
+                        ((long long)wq[0] - (long long)prev) / 1e3, (wq[1] - wq[0]) / 1e3, (wq[2] - wq[1]) / 1e3,
+                        (wq[3] - wq[2]) / 1e3);
             }
         }
     }
