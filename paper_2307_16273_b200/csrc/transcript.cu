@@ -1,5 +1,7 @@
 // transcript.cu — Fiat-Shamir transcript kernels and host wrappers (D3; row a6).
 // Every kernel here is launched with one warp (or a block whose warp 0 runs the transcript).
+#include <cstring>
+
 #include "common.cuh"
 
 namespace zk {
@@ -28,8 +30,19 @@ __global__ void k_tr_absorb(uint8_t* st, Tag32 tag, Bytes256 msg, uint8_t* copy_
     fs_end(s, st);
 }
 
-// long messages from device memory (lane 0 streams the blocks)
+// messages from device memory: up to 256 bytes through the warp-assembled path (fs_absorb_bytes: the 32
+// lanes build the blocks in shared memory, lane 0 compresses); longer ones streamed by lane 0
 __global__ void k_tr_absorb_dev(uint8_t* st, Tag32 tag, const uint8_t* msg, uint64_t len) {
+    if (len <= 256) {
+        __shared__ FsScratch s;
+        __shared__ uint8_t m[256];
+        for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) m[i] = msg[i];
+        __syncwarp();
+        fs_begin(s, st);
+        fs_absorb_bytes(s, tag.s, m, (uint32_t)len);
+        fs_end(s, st);
+        return;
+    }
     if (threadIdx.x != 0) return;
     __shared__ uint32_t buf[32];
     uint8_t* b = reinterpret_cast<uint8_t*>(buf);
@@ -86,49 +99,59 @@ __global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t 
     fs_end(s, st);
 }
 
-// Squeeze x = LE512(H(st||0) || H(st||1)) mod p for one challenge state (one thread).
-__device__ void squeeze_from_state(const uint8_t* st, uint32_t* scratch /* 32 words */, fr_t& mont, fr_t& canon) {
-    uint8_t* b = reinterpret_cast<uint8_t*>(scratch);
-    fr_t half[2];
-    for (int k = 0; k < 2; k++) {
-        for (int i = 0; i < 32; i++) b[i] = st[i];
-        b[32] = (uint8_t)k;
-        uint32_t d[8];
-        hash_buf(b, 33, d);
-        for (int i = 0; i < 8; i++) half[k].v[i] = d[i];   // little-endian digest words = limbs
-    }
-    mont = fr_add(fr_mul(ZK_R2, half[0]), fr_mul(ZK_R3, half[1]));
-    canon = fr_add(fr_reduce_once(fr_reduce_once(half[0])), fr_mul(ZK_R2, half[1]));
-}
-
-// n challenges with one tag: lane 0 advances the state chain, all threads squeeze in parallel.
-// blockDim.x >= 32; n <= 256 per launch (the host splits larger requests)
+// n challenges with one tag (D3: st_{i+1} = H(st_i || 0x02 || u8(|tag|) || tag), x_i = LE512(H(st_{i+1} || 0) ||
+// H(st_{i+1} || 1)) mod p).  Thread 0 advances the state chain word-wise (the block's tail after the state
+// is the same for every step: built once), then thread j < 2n computes squeeze half j & 1 of challenge
+// j / 2, and thread i < n converts.  blockDim.x >= max(32, 2n); n <= 256 per launch.
 __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mont, uint8_t* out_canon) {
-    __shared__ uint8_t states[256][32];
-    __shared__ uint32_t scratch[256][32];
+    __shared__ uint32_t states[256][8];
+    __shared__ fr_t half[256][2];
+    __shared__ uint32_t m[16];   // the chain's message block (shared memory: the compression reads it in place)
     if (threadIdx.x == 0) {
-        uint8_t* b = reinterpret_cast<uint8_t*>(scratch[0]);
-        uint32_t tl = zk_strlen(tag.s);
-        uint8_t cur[32];
-        for (int i = 0; i < 32; i++) cur[i] = st[i];
+        const uint32_t tl = zk_strlen(tag.s);
+#pragma unroll
+        for (int k = 8; k < 16; k++) m[k] = 0;
+        // bytes 32.. of the block: 0x02, |tag|, tag (|tag| <= 30)
+        uint8_t* tb = reinterpret_cast<uint8_t*>(m + 8);
+        tb[0] = 0x02;
+        tb[1] = (uint8_t)tl;
+        for (uint32_t k = 0; k < tl; k++) tb[2 + k] = (uint8_t)tag.s[k];
+        uint32_t cur[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            cur[k] = (uint32_t)st[4 * k] | ((uint32_t)st[4 * k + 1] << 8) | ((uint32_t)st[4 * k + 2] << 16) |
+                     ((uint32_t)st[4 * k + 3] << 24);
         for (uint32_t i = 0; i < n; i++) {
-            for (int k = 0; k < 32; k++) b[k] = cur[k];
-            b[32] = 0x02;
-            b[33] = (uint8_t)tl;
-            for (uint32_t k = 0; k < tl; k++) b[34 + k] = (uint8_t)tag.s[k];
-            uint32_t d[8];
-            hash_buf(b, 34 + tl, d);
-            st_words_to_bytes(d, cur);
-            for (int k = 0; k < 32; k++) states[i][k] = cur[k];
+#pragma unroll
+            for (int k = 0; k < 8; k++) m[k] = cur[k];
+            hash_init(cur);
+            hash_compress(cur, m, 34 + tl, true);
+#pragma unroll
+            for (int k = 0; k < 8; k++) states[i][k] = cur[k];
         }
-        for (int i = 0; i < 32; i++) st[i] = cur[i];
+        st_words_to_bytes(cur, st);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * n) {   // one squeeze compression per thread: H(st_i || k), 33 bytes
+        const uint32_t i = threadIdx.x >> 1, k = threadIdx.x & 1;
+        uint32_t q[16], d[8];
+#pragma unroll
+        for (int w = 0; w < 8; w++) q[w] = states[i][w];
+        q[8] = k;
+#pragma unroll
+        for (int w = 9; w < 16; w++) q[w] = 0;
+        hash_init(d);
+        hash_compress(d, q, 33, true);
+        fr_t x;
+#pragma unroll
+        for (int w = 0; w < 8; w++) x.v[w] = d[w];   // little-endian digest words = limbs
+        half[i][k] = x;
     }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        fr_t x, c;
-        squeeze_from_state(states[i], scratch[threadIdx.x], x, c);
-        if (out_mont) fr_store(&out_mont[i], x);
-        if (out_canon) fr_canon_to_bytes(c, out_canon + 32 * i);
+        const fr_t lo = half[i][0], hi = half[i][1];
+        if (out_mont) fr_store(&out_mont[i], fr_add(fr_mul(ZK_R2, lo), fr_mul(ZK_R3, hi)));
+        if (out_canon) fr_canon_to_bytes(fr_add(fr_reduce_once(fr_reduce_once(lo)), fr_mul(ZK_R2, hi)), out_canon + 32 * i);
     }
 }
 
@@ -148,10 +171,11 @@ void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t 
 
 void tr_challenges_dev(zk_transcript* tr, const char* tag, uint32_t n, fr_t* d_out_mont, uint8_t* d_out_canon) {
     zk_ctx* ctx = tr->ctx;
+    ZK_REQUIRE(strlen(tag) <= 30, ZK_ERR_ARG, "challenge tag longer than 30 bytes (one-block chain step)");
     Tag32 t = make_tag(tag);
     for (uint32_t off = 0; off < n; off += 256) {
         uint32_t c = n - off < 256 ? n - off : 256;
-        uint32_t threads = (c + 31) / 32 * 32;
+        uint32_t threads = (2 * c + 31) / 32 * 32;
         ZK_LAUNCH(ctx, k_tr_challenges, 1, threads, 0, tr->d_st, t, c, d_out_mont ? d_out_mont + off : nullptr,
                   d_out_canon ? d_out_canon + 32 * (size_t)off : nullptr);
     }
