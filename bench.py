@@ -409,6 +409,8 @@ def run_ours(args, rank, world, local):
                    "merge_streams": args.merge_streams,
                    "kernels_ms_one_window_serialised": {k: round(t, 4) for k, (n, t) in
                                                         sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
+                   "kernel_launches_one_window": {k: n for k, (n, t) in sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
+                   "launches_one_window": sum(n for n, t in cby.values()),
                    "claim_merges": sorted(cres["merges"]), "window_state": cres["window_state"].hex()[:16],
                    "what": "the claim-chained window (N3) with the top layer (N2): every matmul family and the "
                            "loss family, one claim merge per tensor family with several claims, the zkReLU at "
