@@ -48,14 +48,6 @@ __global__ void k_cm_scatter(CmMaps M, const fr_t* E, const fr_t* rho, fr_t* P) 
     }
 }
 
-// Wy[y] += scale[k] * E[y]
-__global__ void k_fr_axpy(const fr_t* scale, const fr_t* E, uint64_t n, fr_t* W, int first) {
-    const fr_t a = fr_load(scale);
-    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < n; y += (uint64_t)gridDim.x * blockDim.x) {
-        const fr_t v = fr_mul(a, fr_load(&E[y]));
-        fr_store(&W[y], first ? v : fr_add(fr_load(&W[y]), v));
-    }
-}
 
 // Xr[y] = sum_i beta(r_i, i) X(i, y): the column sums of the [N][D] stack (E2 = beta(r_i) scaled by R)
 template <class Load>
@@ -74,20 +66,28 @@ static inline uint32_t n_log(uint64_t N) {
 }
 
 // Rt(i, k) for one claim: T[i * rows + row] = sum_col beta(v.cols)[col] X[i][row][col]; Rt = T . beta(v.rows)
+// (Ec = beta(v.cols) scaled by R, Er = beta(v.rows): built by the caller's batched eq-table launches)
 template <class Load>
-static void cm_slice_mles(zk_ctx* ctx, Load load, uint64_t N, uint32_t lr, uint32_t lc, const fr_t* v, fr_t* out,
-                          Scratch& s) {
+static void cm_slice_mles(zk_ctx* ctx, Load load, uint64_t N, uint32_t lr, uint32_t lc, const fr_t* Ec, const fr_t* Er,
+                          fr_t* out, Scratch& s) {
     const uint64_t rows = 1ull << lr, cols = 1ull << lc;
-    fr_t* Ec = s.alloc<fr_t>(cols);
-    eq_table_r2_dev(ctx, v, lc, Ec, s);
     fr_t* T = s.alloc<fr_t>(N * rows);
     ZK_LAUNCH(ctx, k_rowdot_i32<Load>, grid_for(ctx, N * rows * 32, 256, 8), 256, 0, load, N * rows, (uint32_t)cols,
-              (const fr_t*)Ec, T, N * rows, (uint32_t)(n_log(N) + lr), (uint64_t)1);
+              Ec, T, N * rows, (uint32_t)(n_log(N) + lr), (uint64_t)1);
     // the row dots are in natural order (inner = nrows: identity map)
-    fr_t* Er = s.alloc<fr_t>(rows);
-    eq_table_dev(ctx, v + lc, lr, nullptr, Er, s);
-    ZK_LAUNCH(ctx, k_rowdot_fr, grid_for(ctx, N * 32, 256, 8), 256, 0, (const fr_t*)T, N, (uint32_t)rows,
-              (const fr_t*)Er, out);
+    ZK_LAUNCH(ctx, k_rowdot_fr, grid_for(ctx, N * 32, 256, 8), 256, 0, (const fr_t*)T, N, (uint32_t)rows, Er, out);
+}
+
+// W[y] = sum_k T_k[y] over K tables of D entries (phase B's sum of the scaled eq tables)
+struct CmTabs {
+    const fr_t* t[64];
+};
+__global__ void k_cm_sum_tables(CmTabs T, uint32_t K, uint64_t D, fr_t* W) {
+    for (uint64_t y = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; y < D; y += (uint64_t)gridDim.x * blockDim.x) {
+        fr_t acc = fr_load(&T.t[0][y]);
+        for (uint32_t k = 1; k < K; k++) acc = fr_add(acc, fr_load(&T.t[k][y]));
+        fr_store(&W[y], acc);
+    }
 }
 
 struct CmLayout {
@@ -141,10 +141,19 @@ static void claim_merge_dev(zk_ctx* ctx, zk_transcript* tr, Load load, uint32_t 
     fr_t* P = s.alloc_zero<fr_t>(NA);
     fr_t* Rt = s.alloc_zero<fr_t>(NA);
     fr_t* E = s.alloc<fr_t>(M.off[K] ? M.off[K] : 1);
+    // every eq table of phase A in batched launches: per claim the slot table, and the column (R-scaled) and
+    // row tables of its inner point
+    std::vector<EqJob> jobs;
+    std::vector<fr_t*> Ec(K), Er(K);
     for (uint32_t k = 0; k < K; k++) {
-        eq_table_dev(ctx, pts + poff[k] + d, nk[k], nullptr, E + M.off[k], s);
-        cm_slice_mles(ctx, load, N, lr, lc, pts + poff[k], Rt + (uint64_t)k * N, s);
+        Ec[k] = s.alloc<fr_t>(1ull << lc);
+        Er[k] = s.alloc<fr_t>(1ull << lr);
+        jobs.push_back(EqJob{pts + poff[k] + d, nk[k], nullptr, 0, E + M.off[k]});
+        jobs.push_back(EqJob{pts + poff[k], lc, nullptr, 1, Ec[k]});
+        jobs.push_back(EqJob{pts + poff[k] + lc, lr, nullptr, 0, Er[k]});
     }
+    eq_tables_batch(ctx, (uint32_t)jobs.size(), jobs.data(), s);
+    for (uint32_t k = 0; k < K; k++) cm_slice_mles(ctx, load, N, lr, lc, Ec[k], Er[k], Rt + (uint64_t)k * N, s);
     ZK_LAUNCH(ctx, k_cm_scatter, grid_for(ctx, M.off[K], 128, 1), 128, 0, M, (const fr_t*)E, (const fr_t*)rho, P);
     ScStatement A;
     memset(&A, 0, sizeof A);
@@ -168,12 +177,17 @@ static void claim_merge_dev(zk_ctx* ctx, zk_transcript* tr, Load load, uint32_t 
     fr_t* Bk = s.alloc<fr_t>(1ull << kap);
     eq_table_dev(ctx, A.d_r + n, kap, nullptr, Bk, s);
     fr_t* Wy = s.alloc<fr_t>(D);
-    fr_t* Ev = s.alloc<fr_t>(D);
+    // Wy = sum_k beta(r_k, k) beta(v_k, .): the K tables scaled by beta(r_k, k) in batched launches, then summed
+    ZK_REQUIRE(K <= 64, ZK_ERR_ARG, "claim merge: at most 64 claims");
+    CmTabs tabs;
+    std::vector<EqJob> bj;
     for (uint32_t k = 0; k < K; k++) {
-        eq_table_dev(ctx, pts + poff[k], d, nullptr, Ev, s);
-        ZK_LAUNCH(ctx, k_fr_axpy, grid_for(ctx, D, 256, 4), 256, 0, (const fr_t*)(Bk + k), (const fr_t*)Ev, D, Wy,
-                  (int)(k == 0));
+        fr_t* Ev = s.alloc<fr_t>(D);
+        tabs.t[k] = Ev;
+        bj.push_back(EqJob{pts + poff[k], d, Bk + k, 0, Ev});
     }
+    eq_tables_batch(ctx, K, bj.data(), s);
+    ZK_LAUNCH(ctx, k_cm_sum_tables, grid_for(ctx, D, 256, 4), 256, 0, tabs, K, D, Wy);
     ScStatement B;
     memset(&B, 0, sizeof B);
     B.m = d;

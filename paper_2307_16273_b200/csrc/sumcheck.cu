@@ -328,6 +328,27 @@ __global__ void __launch_bounds__(256, 2) k_sc_round0_int(Sc2Args A) {
         sc_finish(a, msg, 2);
     }
 }
+// the factored K = 2 rounds' product groups (ZKDL_SC_MULW): 3 = the two- and three-product bodies
+// (interleaved chains), 1 = single-product body calls (the smaller body stays in the L0 instruction cache)
+#ifndef ZKDL_SC_MULW
+#define ZKDL_SC_MULW 3
+#endif
+__device__ __forceinline__ fr3_t sc_mul3(const fr_t& a0, const fr_t& b0, const fr_t& a1, const fr_t& b1, const fr_t& a2,
+                                         const fr_t& b2) {
+#if ZKDL_SC_MULW == 3
+    return fr_mul3_ni(a0, b0, a1, b1, a2, b2);
+#else
+    return fr3_t{fr_mul_ni(a0, b0), fr_mul_ni(a1, b1), fr_mul_ni(a2, b2)};
+#endif
+}
+__device__ __forceinline__ fr2p_t sc_mul2(const fr_t& a0, const fr_t& b0, const fr_t& a1, const fr_t& b1) {
+#if ZKDL_SC_MULW == 3
+    return fr_mul2_ni(a0, b0, a1, b1);
+#else
+    return fr2p_t{fr_mul_ni(a0, b0), fr_mul_ni(a1, b1)};
+#endif
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     const ScRoundArgs& a = A.r;
@@ -389,17 +410,17 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                 const fr_t* sb = a.src[1] + 4 * b;
                 x0 = fr_load_cg(sa); x1 = fr_load_cg(sa + 1); x2 = fr_load_cg(sa + 2); x3 = fr_load_cg(sa + 3);
                 z0 = fr_load_cg(sb); z1 = fr_load_cg(sb + 1); z2 = fr_load_cg(sb + 2); z3 = fr_load_cg(sb + 3);
-                const fr3_t f = fr_mul3_ni(r, fr_sub(x1, x0), r, fr_sub(x3, x2), r, fr_sub(z1, z0));
+                const fr3_t f = sc_mul3(r, fr_sub(x1, x0), r, fr_sub(x3, x2), r, fr_sub(z1, z0));
                 a0 = fr_add(x0, f.x);
                 a1 = fr_add(x2, f.y);
                 b0 = fr_add(z0, f.z);
                 if (has_e && !(A.flat && a.eq_hi)) {
-                    q = fr_mul3_ni(r, fr_sub(z3, z2), e, a0, e, a1);
+                    q = sc_mul3(r, fr_sub(z3, z2), e, a0, e, a1);
                     b1 = fr_add(z2, q.x);
                     q_done = true;
                 } else {
                     const fr_t hh = (has_e && A.flat && a.eq_hi) ? fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]) : zero;
-                    const fr2p_t g2 = fr_mul2_ni(r, fr_sub(z3, z2), e, hh);
+                    const fr2p_t g2 = sc_mul2(r, fr_sub(z3, z2), e, hh);
                     b1 = fr_add(z2, g2.x);
                     if (has_e) e = g2.y;
                 }
@@ -438,12 +459,12 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                     y0 = q.y;
                     y1 = q.z;
                 } else {   // two products only: the two-product body (no wasted third slot)
-                    const fr2p_t q2 = fr_mul2_ni(e, a0, e, a1);
+                    const fr2p_t q2 = sc_mul2(e, a0, e, a1);
                     y0 = q2.x;
                     y1 = q2.y;
                 }
             }
-            const fr3_t p = fr_mul3_ni(y0, b0, y1, b1, fr_sub(y1, y0), fr_sub(b1, b0));
+            const fr3_t p = sc_mul3(y0, b0, y1, b1, fr_sub(y1, y0), fr_sub(b1, b0));
             s0 = fr_add(s0, p.x);
             s1 = fr_add(s1, p.y);
             si = fr_add(si, p.z);

@@ -195,9 +195,9 @@ void eq_tables_batch(zk_ctx* ctx, uint32_t n, const EqJob* jobs, Scratch& s) {
 }
 
 void eq_table_r2_dev(zk_ctx* ctx, const fr_t* d_u, uint32_t k, fr_t* d_out, Scratch& s) {
-    fr_t* sc = s.alloc<fr_t>(1);
-    ZK_LAUNCH(ctx, k_set_const, 1, 1, 0, sc, ZK_R2);   // the Montgomery form of the field element R
-    eq_table_dev(ctx, d_u, k, sc, d_out, s);
+    // the batch kernel's r2 start value (the Montgomery form of the field element R): no constant to upload
+    const EqJob j{d_u, k, nullptr, 1, d_out};
+    eq_tables_batch(ctx, 1, &j, s);
 }
 
 // ---------------------------------------------------------------- dot products and MLE
