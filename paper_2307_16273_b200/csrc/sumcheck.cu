@@ -329,9 +329,10 @@ __global__ void __launch_bounds__(256, 2) k_sc_round0_int(Sc2Args A) {
     }
 }
 // the factored K = 2 rounds' product groups (ZKDL_SC_MULW): 3 = the two- and three-product bodies
-// (interleaved chains), 1 = single-product body calls (the smaller body stays in the L0 instruction cache)
+// (interleaved chains), 1 = single-product body calls (the smaller body stays in the L0 instruction cache:
+// C5 m = 26 10.1 -> 9.0 ms, m = 24 3.64 -> 3.34 ms, same proofs)
 #ifndef ZKDL_SC_MULW
-#define ZKDL_SC_MULW 3
+#define ZKDL_SC_MULW 1
 #endif
 __device__ __forceinline__ fr3_t sc_mul3(const fr_t& a0, const fr_t& b0, const fr_t& a1, const fr_t& b1, const fr_t& a2,
                                          const fr_t& b2) {
