@@ -226,7 +226,9 @@ namespace zk {
 #define ZKDL_FR64 1
 #endif
 __device__ __forceinline__ fr_t fr_mul_hot(const fr_t& a, const fr_t& b) {
-#if ZKDL_FR64
+#if ZKDL_FR64 == 2
+    return fr_mul_f64r(a, b);   // the rolled (CIOS-order) FP64 product: a ~5x smaller body
+#elif ZKDL_FR64
     return fr_mul_f64(a, b);
 #else
     return fr_mul(a, b);

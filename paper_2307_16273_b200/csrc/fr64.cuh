@@ -92,4 +92,55 @@ __device__ __forceinline__ fr_t fr_mul_f64(const fr_t& a, const fr_t& b) {
     return fr_reduce_once(r);
 }
 
+// The same product with the reduction interleaved row by row (CIOS order) in a rolled loop: the six live
+// columns shift down one limb per row (the column entering at the top starts at its pre-bias, which the
+// constants above give: 0x3960.. + i 0x1340.. for columns 6..9), and A's limbs shift with them, so every
+// index is static and the body is ~5x smaller (~1.8 KB against ~7 KB: inside the L0 instruction cache).
+// Every column receives the same terms as in fr_mul_f64, so the result is the same bits.
+__device__ __forceinline__ fr_t fr_mul_f64r(const fr_t& a, const fr_t& b) {
+    const double P0 = 4503595332403201.0, P1 = 52776117727231.0, P2 = 2711223964777892.0,
+                 P3 = 2203984808738944.0, P4 = 127464551688605.0;
+    const double PINV = 4503595332403199.0;
+    double A[5] = {fr64_limb(a, -4), fr64_limb(a, 48), fr64_limb(a, 100), fr64_limb(a, 152), fr64_limb(a, 204)};
+    const double B[5] = {fr64_limb(b, 0), fr64_limb(b, 52), fr64_limb(b, 104), fr64_limb(b, 156), fr64_limb(b, 208)};
+    const double Pl[5] = {P0, P1, P2, P3, P4};
+    uint64_t c[6] = {0x79a0000000000000ull, 0x6660000000000000ull, 0x5320000000000000ull, 0x3fe0000000000000ull,
+                     0x2ca0000000000000ull, 0x2620000000000000ull};
+#pragma unroll 1
+    for (int i = 0; i < 5; i++) {
+        const double ai = A[0];
+#pragma unroll
+        for (int j = 0; j < 5; j++) ZK_F64_MAC(ai, B[j], c[j], c[j + 1]);
+        const double x = __dsub_rn(zk_f64((c[0] & ZK_F52_MASK) | ZK_F52_EXP), ZK_TWO52);
+        const double h = __fma_rz(x, PINV, ZK_TWO104);
+        const double q = __dsub_rn(__fma_rz(x, PINV, __dsub_rn(ZK_C2, h)), ZK_TWO52);
+#pragma unroll
+        for (int j = 0; j < 5; j++) ZK_F64_MAC(q, Pl[j], c[j], c[j + 1]);
+        const uint64_t carry = c[0] >> 52;
+        c[0] = c[1] + carry;
+        c[1] = c[2];
+        c[2] = c[3];
+        c[3] = c[4];
+        c[4] = c[5];
+        c[5] = i < 4 ? 0x3960000000000000ull + (uint64_t)i * 0x1340000000000000ull : 0ull;
+        A[0] = A[1];
+        A[1] = A[2];
+        A[2] = A[3];
+        A[3] = A[4];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        c[k + 1] += c[k] >> 52;
+        c[k] &= ZK_F52_MASK;
+    }
+    const uint64_t u0 = c[0] | (c[1] << 52), u1 = (c[1] >> 12) | (c[2] << 40), u2 = (c[2] >> 24) | (c[3] << 28),
+                   u3 = (c[3] >> 36) | (c[4] << 16);
+    fr_t r;
+    r.v[0] = (uint32_t)u0; r.v[1] = (uint32_t)(u0 >> 32);
+    r.v[2] = (uint32_t)u1; r.v[3] = (uint32_t)(u1 >> 32);
+    r.v[4] = (uint32_t)u2; r.v[5] = (uint32_t)(u2 >> 32);
+    r.v[6] = (uint32_t)u3; r.v[7] = (uint32_t)(u3 >> 32);
+    return fr_reduce_once(r);
+}
+
 }  // namespace zk

@@ -831,6 +831,9 @@ __device__ __forceinline__ fr3_t ir_mul3(const fr_t& a0, const fr_t& b0, const f
                                          const fr_t& b2) {
 #if ZKDL_IR_MULW == 3
     return fr_mul3_ni(a0, b0, a1, b1, a2, b2);
+#elif ZKDL_IR_MULW == 2
+    const fr2p_t p = fr_mul2_ni(a0, b0, a1, b1);
+    return fr3_t{p.x, p.y, fr_mul_ni(a2, b2)};
 #else
     fr3_t r;
     r.x = fr_mul_ni(a0, b0);

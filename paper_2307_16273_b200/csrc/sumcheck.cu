@@ -338,12 +338,15 @@ __device__ __forceinline__ fr3_t sc_mul3(const fr_t& a0, const fr_t& b0, const f
                                          const fr_t& b2) {
 #if ZKDL_SC_MULW == 3
     return fr_mul3_ni(a0, b0, a1, b1, a2, b2);
+#elif ZKDL_SC_MULW == 2
+    const fr2p_t p = fr_mul2_ni(a0, b0, a1, b1);
+    return fr3_t{p.x, p.y, fr_mul_ni(a2, b2)};
 #else
     return fr3_t{fr_mul_ni(a0, b0), fr_mul_ni(a1, b1), fr_mul_ni(a2, b2)};
 #endif
 }
 __device__ __forceinline__ fr2p_t sc_mul2(const fr_t& a0, const fr_t& b0, const fr_t& a1, const fr_t& b1) {
-#if ZKDL_SC_MULW == 3
+#if ZKDL_SC_MULW >= 2
     return fr_mul2_ni(a0, b0, a1, b1);
 #else
     return fr2p_t{fr_mul_ni(a0, b0), fr_mul_ni(a1, b1)};

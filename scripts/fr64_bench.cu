@@ -38,14 +38,15 @@ __global__ void k_check(uint64_t n, unsigned long long* bad, fr_t* first_bad) {
         if (e == 2) a = fr_zero();
         if (e == 3) { a = fr_const(ZK_P0 - 1, ZK_P1, ZK_P2, ZK_P3, ZK_P4, ZK_P5, ZK_P6, ZK_P7); b = fr_const(~0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u, ~0u); }
         if (e == 4) { a.v[0] = 1; for (int i = 1; i < 8; i++) a.v[i] = 0; }
-        const fr_t x = fr_mul(a, b), y = fr_mul_f64(a, b);
-        if (!fr_equal(x, y)) {
+        const fr_t x = fr_mul(a, b), y = fr_mul_f64(a, b), z = fr_mul_f64r(a, b);
+        if (!fr_equal(x, y) || !fr_equal(x, z)) {
             if (atomicAdd(bad, 1ull) == 0) { first_bad[0] = a; first_bad[1] = b; first_bad[2] = x; first_bad[3] = y; }
         }
     }
 }
 
-template <int C, int MODE>   // MODE 0: integer CIOS, 1: FP64, 2: half the chains each, 3: odd warps integer, even warps FP64
+template <int C, int MODE>   // MODE 0: integer CIOS, 1: FP64, 2: half the chains each, 3: odd warps integer, even warps FP64,
+                             // 4: FP64 rolled (CIOS order)
 __global__ void __launch_bounds__(256) k_rate(const fr_t* seed, uint32_t iters, fr_t* out) {
     fr_t x[C];
     const fr_t y = seed[(threadIdx.x + 1) & 1023];
@@ -54,7 +55,8 @@ __global__ void __launch_bounds__(256) k_rate(const fr_t* seed, uint32_t iters, 
     for (uint32_t i = 0; i < iters; i++) {
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            if (MODE == 0 || (MODE == 2 && (c & 1)) || (MODE == 3 && ((threadIdx.x >> 5) & 1))) x[c] = fr_mul(x[c], y);
+            if (MODE == 4) x[c] = fr_mul_f64r(x[c], y);
+            else if (MODE == 0 || (MODE == 2 && (c & 1)) || (MODE == 3 && ((threadIdx.x >> 5) & 1))) x[c] = fr_mul(x[c], y);
             else x[c] = fr_mul_f64(x[c], y);
         }
     }
@@ -119,6 +121,8 @@ int main() {
     rate<2, 2>("mixed", seed, out, 0);
     rate<4, 2>("mixed", seed, out, 0);
     for (int bps : {1, 2, 3, 4}) rate<2, 1>("fp64", seed, out, bps);
+    rate<1, 4>("fp64_rolled", seed, out, 0);
+    rate<2, 4>("fp64_rolled", seed, out, 0);
     rate<1, 3>("per_warp_mixed", seed, out, 0);
     rate<2, 3>("per_warp_mixed", seed, out, 0);
     rate<3, 3>("per_warp_mixed", seed, out, 0);
