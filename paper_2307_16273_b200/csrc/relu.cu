@@ -460,18 +460,23 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
     for (uint32_t t = 0; t < a.logB; t++) {
         const int n = B >> t, np = n >> 1;
         // evaluations: item (b, X)
-        if (tid < 4 * np) {
+        if (tid < 4 * np) {   // independent products in three-product out-of-line bodies (latency: this
+                              // single-CTA kernel is on the zkReLU family's critical path)
             const int b = tid >> 2, X = tid & 3;
             const fr_t x = fr_from_u32((uint32_t)X), omx = fr_sub(fr_one(), x);
-#define LIN(v) fr_add(v[2 * b], fr_mul_cold(x, fr_sub(v[2 * b + 1], v[2 * b])))
-            fr_t sv = LIN(S), spv = LIN(SP), ebv = LIN(EB), lsv = LIN(LS), lspv = LIN(LSP), lqv = LIN(LQ);
-#undef LIN
+#define DIF(v) fr_sub(v[2 * b + 1], v[2 * b])
+            const fr3_t l1 = fr_mul3_ni(x, DIF(S), x, DIF(SP), x, DIF(EB));
+            const fr3_t l2 = fr_mul3_ni(x, DIF(LS), x, DIF(LSP), x, DIF(LQ));
+#undef DIF
+            const fr_t sv = fr_add(S[2 * b], l1.x), spv = fr_add(SP[2 * b], l1.y), ebv = fr_add(EB[2 * b], l1.z);
+            const fr_t lsv = fr_add(LS[2 * b], l2.x), lspv = fr_add(LSP[2 * b], l2.y), lqv = fr_add(LQ[2 * b], l2.z);
             // bilinear: sum_{x1,x2} l(x1) l(x2) CQ[2b+x1][2b+x2]
             fr_t c00 = CQ[2 * b][2 * b], c01 = CQ[2 * b][2 * b + 1], c10 = CQ[2 * b + 1][2 * b], c11 = CQ[2 * b + 1][2 * b + 1];
-            fr_t cq = fr_add(fr_mul_cold(fr_mul_cold(omx, omx), c00),
-                             fr_add(fr_mul_cold(fr_mul_cold(omx, x), fr_add(c01, c10)), fr_mul_cold(fr_mul_cold(x, x), c11)));
-            fr_t v = fr_add(fr_add(fr_mul_cold(sv, lsv), fr_mul_cold(spv, lspv)), fr_mul_cold(ebv, fr_sub(cq, lqv)));
-            vals[tid] = v;
+            const fr3_t w = fr_mul3_ni(omx, omx, omx, x, x, x);
+            const fr3_t q = fr_mul3_ni(w.x, c00, w.y, fr_add(c01, c10), w.z, c11);
+            const fr_t cq = fr_add(q.x, fr_add(q.y, q.z));
+            const fr3_t t3 = fr_mul3_ni(sv, lsv, spv, lspv, ebv, fr_sub(cq, lqv));
+            vals[tid] = fr_add(fr_add(t3.x, t3.y), t3.z);
         }
         __syncthreads();
         if (tid < 4) {
@@ -499,16 +504,19 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_t nv[6];
         if (tid < np) {
             const int b = tid;
-#define FOLD(v) fr_add(v[2 * b], fr_mul_cold(rt, fr_sub(v[2 * b + 1], v[2 * b])))
-            nv[0] = FOLD(S); nv[1] = FOLD(SP); nv[2] = FOLD(EB); nv[3] = FOLD(LS); nv[4] = FOLD(LSP); nv[5] = FOLD(LQ);
-#undef FOLD
+#define DIF(v) fr_sub(v[2 * b + 1], v[2 * b])
+            const fr3_t f1 = fr_mul3_ni(rt, DIF(S), rt, DIF(SP), rt, DIF(EB));
+            const fr3_t f2 = fr_mul3_ni(rt, DIF(LS), rt, DIF(LSP), rt, DIF(LQ));
+#undef DIF
+            nv[0] = fr_add(S[2 * b], f1.x); nv[1] = fr_add(SP[2 * b], f1.y); nv[2] = fr_add(EB[2 * b], f1.z);
+            nv[3] = fr_add(LS[2 * b], f2.x); nv[4] = fr_add(LSP[2 * b], f2.y); nv[5] = fr_add(LQ[2 * b], f2.z);
         }
         // fold CQ: columns then rows, staged through registers (n * np <= 512 = 2 per thread)
         fr_t cv[2];
         int cc = 0;
         for (int e = tid; e < n * np; e += blockDim.x) {
             int i = e / np, c = e % np;
-            cv[cc++] = fr_add(CQ[i][2 * c], fr_mul_cold(rt, fr_sub(CQ[i][2 * c + 1], CQ[i][2 * c])));
+            cv[cc++] = fr_add(CQ[i][2 * c], fr_mul_ni(rt, fr_sub(CQ[i][2 * c + 1], CQ[i][2 * c])));
         }
         __syncthreads();
         cc = 0;
@@ -520,7 +528,7 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         fr_t rv = fr_zero();
         if (tid < np * np) {
             int b = tid / np, c = tid % np;
-            rv = fr_add(CQ[2 * b][c], fr_mul_cold(rt, fr_sub(CQ[2 * b + 1][c], CQ[2 * b][c])));
+            rv = fr_add(CQ[2 * b][c], fr_mul_ni(rt, fr_sub(CQ[2 * b + 1][c], CQ[2 * b][c])));
         }
         __syncthreads();
         if (tid < np * np) CQ[tid / np][tid % np] = rv;
