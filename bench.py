@@ -198,13 +198,17 @@ def frmul_model(fams, persist_log: int = 16, hb: int = 5) -> dict:
         logD = D.bit_length() - 1
         H = logD - min(hb, logD)
         t0 = next((t for t in range(1, H) if (D >> (t + 1)) <= (1 << persist_log)), H)
-        # factored i-round, per pair (two sides): first round 2 x (6 E'a + 3 T_b) = 18; folding rounds
-        # 2 x (3 fold + 6 E'a + 3 T_c + 3 T_b) = 30, round 1 from the words (t0 >= 2) without the 3 fold
-        # products (byte tables scaled by 1 - r_0, r_0) = 24; plus 8 HI' products per thread and launch
-        # (not counted)
+        # factored i-round, per pair (two sides), X = 1 derived from the per-term sums (ZKDL_IR_DERIVE, the
+        # default): first round 2 x (T_a 1 + T_c 2 + T_b 4) = 14; folding rounds 2 x (3 fold + 1 + 4 + 4) = 24;
+        # round 1 from the words (t0 >= 2, fold by byte tables) 2 x 9 = 18.  Explicit X = 1 (the persistent
+        # rounds, ZKDL_IR_DERIVE=0): 18, 30, 24.  HI' products per thread and launch not counted.
+        derive = os.environ.get("ZKDL_IR_DERIVE", "1") != "0"
         for t in range(H):
             pairs = D >> (t + 1)
-            per = 18 if t == 0 else (24 if t == 1 and t0 >= 2 else 30)
+            if t < t0 and derive:
+                per = 14 if t == 0 else (18 if t == 1 and t0 >= 2 else 24)
+            else:
+                per = 18 if t == 0 else (24 if t == 1 and t0 >= 2 else 30)
             out["k_relu_iround_f" if t < t0 else "k_relu_ipersist"] += per * pairs
     for f in fams:
         if hasattr(f, "A"):
@@ -363,8 +367,10 @@ def run_ours(args, rank, world, local):
         cwctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(2)]
         # stage 2's claim merges (latency-bound sumchecks) side by side on budgeted streams
         mctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.merge_streams)]
-        for c in mctxs:
-            c.set_sm_budget(max(4, 148 // max(1, args.merge_streams)))
+        for c in mctxs:   # the merges' persistent grids together leave room for the zkReLU's persistent
+            # rounds of the previous window (k_relu_ipersist needs ~65 SMs co-resident; a cooperative launch
+            # that cannot get them waits, and the window's critical path with it)
+            c.set_sm_budget(max(4, (args.merge_budget or 148) // max(1, args.merge_streams)))
         streams_all = [c.stream for c in ctxs + cwctxs + mctxs]
         with torch.cuda.stream(stream):
             for i in range(2):
@@ -953,6 +959,8 @@ def main():
                     help="streams (contexts) the matmul families are spread over, side by side")
     ap.add_argument("--merge-aux", type=int, default=0, choices=[0, 1],
                     help="1: every zkReLU family ends with the aux-claim merge (P:L470, DESIGN.md D21)")
+    ap.add_argument("--merge-budget", type=int, default=0,
+                    help="chained window: total SM budget of the claim merges' persistent grids (0: 148)")
     ap.add_argument("--relu-priority", type=int, default=-1, help="CUDA stream priority of the zkReLU stream (lower = higher)")
     ap.add_argument("--mm-budget", type=int, default=37,
                     help="SM budget of each matmul stream's persistent sumcheck grid (0: 148 / mm-streams)")

@@ -221,7 +221,12 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         _fence(c, [wctx])
     for T in kids1:
         W.absorb_state("fcn/join", T)
-    # ---- stage 2: one claim per tensor family
+    # ---- stage 2: one claim per tensor family.  The merges wait for the zkReLU stream's earlier work (the
+    # previous window's stage 3): their persistent grids and the zkReLU's persistent rounds (k_relu_ipersist,
+    # ~65 SMs co-resident) then never compete for co-residency — measured, the overlapping version stalled
+    # for tens to hundreds of milliseconds in some runs.  Stage 1 still overlaps the previous stage 3.
+    if rctx.stream not in [c.stream for c in lanes2]:
+        _fence(rctx, lanes2)
     L2 = _Lanes(lanes2)
     home2 = [L2.pick(len(t.pad) * t.rows * t.cols) for t, *_ in lay2]
     kids2 = []

@@ -68,6 +68,12 @@ void zk_ctx_destroy(zk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     zk_ctx_detach_nccl(ctx);
+    if (ctx->aux) {
+        cudaStreamSynchronize(ctx->aux);
+        cudaStreamDestroy(ctx->aux);
+        cudaEventDestroy(ctx->aux_ev[0]);
+        cudaEventDestroy(ctx->aux_ev[1]);
+    }
     delete ctx;
 }
 

@@ -21,6 +21,17 @@ struct zk_ctx {
     int nccl_rank = 0, nccl_world = 1;
     uint64_t launches = 0;
     std::string err;
+    // a second stream for work off the critical path (created on first use; aux_ev: fork / join events)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t aux_ev[2] = {nullptr, nullptr};
+    cudaStream_t aux_stream() {
+        if (!aux) {
+            cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&aux_ev[0], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&aux_ev[1], cudaEventDisableTiming);
+        }
+        return aux;
+    }
     // per-launch CUDA-event profiling (zk_ctx_profile): events bracket each launch on the ctx stream
     bool prof = false;
     std::string prof_filter;   // only this kernel, every template instantiation (empty: all kernels)

@@ -396,6 +396,7 @@ struct JRoundArgs {
     fr_t* rj_out;          // logB challenges (Montgomery)
     fr_t* byte_tab;        // ceil(B/8) x 256 entries
     fr_t* kappa;           // [0] kZ [1] kA [2] kGA [3] kGZ [4] kb [5] r' [6] claim after the j-phase
+    fr_t* sigma;           // (nullable) the five per-term sums entering the i-phase (Z, A, GA, GZ, b)
 };
 
 __device__ __forceinline__ int tri_index(int j1, int j2, int B) {   // j1 <= j2, row-major upper triangle
@@ -556,6 +557,43 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
         ej[j] = e;
     }
     __syncthreads();
+    if (a.sigma) {
+        // per-term sums entering the i-phase (the derived-X=1 i-rounds): with e_j = beta(r_j, j),
+        //   sigma_x = kappa_x sum_j e_j M_x[j]                       (x = Z, A, GA, GZ: the linear cells)
+        //   sigma_b = kappa_b (S_0 - L_0) + kappa_b' (S_1 - L_1),     S_s = sum_{j1,j2} e_j1 e_j2 C_s[j1][j2],
+        //                                                            L_s = sum_j e_j C_s[j][j]
+        // (sum_i e_b(i) a(i)(a(i) - 1) through the Gram cells; their total is the claim kappa[6])
+        fr_t (*linp)[32] = CQ;   // (the j-rounds are done with CQ: rows 0-3 hold the linear products)
+        if (tid < 4 * B) {
+            const int x = tid / B, j = tid % B;
+            linp[x][j] = fr_mul_ni(ej[j], fr_load(&a.cells[x * B + j]));
+        }
+        fr_t gacc[2] = {fr_zero(), fr_zero()};
+        const int T = B * (B + 1) / 2;
+        for (int e = tid; e < T; e += blockDim.x) {
+            int j1 = 0, rem = e;
+            while (rem >= B - j1) {
+                rem -= B - j1;
+                j1++;
+            }
+            const int j2 = j1 + rem;
+            fr_t w = fr_mul_ni(ej[j1], ej[j2]);
+            w = j1 == j2 ? fr_sub(w, ej[j1]) : fr_add(w, w);
+            const fr2p_t c = fr_mul2_ni(w, fr_load(&C0[e]), w, fr_load(&C1[e]));
+            gacc[0] = fr_add(gacc[0], c.x);
+            gacc[1] = fr_add(gacc[1], c.y);
+        }
+        block_reduce_fr<2>(gacc, vals);   // (vals: 64 elements, free after the j-rounds)
+        if (tid < 4) {
+            fr_t acc = fr_zero();
+            for (int j = 0; j < B; j++) acc = fr_add(acc, linp[tid][j]);
+            const fr_t s = S[0], sp = SP[0];
+            const fr_t k = tid == 0 ? fr_mul_ni(r2, s) : tid == 1 ? fr_mul_ni(r, sp) :
+                           tid == 2 ? fr_mul_ni(fr_mul_ni(rp, r2), s) : fr_mul_ni(fr_mul_ni(rp, r), sp);
+            fr_store(&a.sigma[tid], fr_mul_ni(k, acc));
+        }
+        if (tid == 0) fr_store(&a.sigma[4], fr_add(fr_mul_ni(EB[0], gacc[0]), fr_mul_ni(fr_mul_ni(rp, EB[0]), gacc[1])));
+    }
     const int nb = (B + 7) / 8;
     for (int e = tid; e < nb * 256; e += blockDim.x) {
         int bb = e >> 8, v = e & 255;
@@ -608,6 +646,9 @@ struct IRoundArgs {
     const int32_t* words[2];
     const fr_t* byte_tab;
     uint32_t qr_mask, sig_bit, nbytes;
+    // MODE bit 2 (derived X = 1): the per-term running sums (read and updated by the finalizer) and u_x[t]^-1
+    fr_t* sigma;
+    const fr_t* uinv;
 };
 
 // Finalizer of an i-round (last block, after the grid reduction), in two parts so that the persistent
@@ -861,7 +902,7 @@ __device__ __forceinline__ fr_t byte_sum(const fr_t* tb, uint32_t w, const IPtrs
 
 // Accumulate this thread's pairs j = j0, j0 + js, ... < P_blk of HI block h into T[0..7] =
 // (T_a(0), T_a(1), T_c(0), T_c(1), T_c(inf), T_b(0), T_b(1), T_b(inf)) of its side.
-template <bool FOLD, int SRC = 0>
+template <bool FOLD, int SRC = 0, bool DER = false>
 __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint32_t h, uint32_t pb, uint64_t j0,
                                              uint64_t js, const int side, fr_t (&T)[8]) {
     const fr_t one = fr_one();
@@ -943,6 +984,26 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             fr_store(&q.nxC[j], eC);
             if (q.nxB) fr_store(&q.nxB[j], eB);
         }
+        if constexpr (DER) {
+            // derived X = 1 (the finalizer gets T_x(1) from the running per-term sum): T_a(0), T_c(0),
+            // T_c(inf) = sum e_C (a1 - a0)(oms1 - oms0), T_b(0), T_b(inf) = sum e_b (a1 - a0)^2 into T[0..4]
+            const fr_t dA = fr_sub(a1, a0);
+            const fr_t tA = fr_mul_ni(eA, a0);
+            const fr_t yC0 = fr_mul_ni(eC, a0), yD = fr_mul_ni(eC, dA);
+            const fr_t zB0 = fr_mul_ni(eB, a0), zD = fr_mul_ni(eB, dA);
+            T[0] = fr_add(T[0], tA);
+            if (FOLD) {
+                T[1] = fr_add(T[1], fr_mul_ni(yC0, om0));
+                T[2] = fr_add(T[2], fr_mul_ni(yD, fr_sub(om1, om0)));
+            } else {   // oms in {0, 1}
+                const fr_t zero = fr_zero();
+                T[1] = fr_add(T[1], o0 ? yC0 : zero);
+                T[2] = fr_add(T[2], o1 == o0 ? zero : (o1 ? yD : fr_neg(yD)));
+            }
+            T[3] = fr_add(T[3], fr_mul_ni(zB0, fr_sub(a0, one)));
+            T[4] = fr_add(T[4], fr_mul_ni(zD, dA));
+            continue;
+        }
         const fr3_t p = ir_mul3(eA, a0, eA, a1, eC, a0);
         const fr3_t pq = ir_mul3(eC, a1, eB, a0, eB, a1);
         T[0] = fr_add(T[0], p.x);
@@ -990,6 +1051,33 @@ __device__ __forceinline__ void iround_scale_scatter(fr_t (&T)[8], fr_t* const* 
     acc[11] = T[6];
     acc[12] = T[7];
     acc[13] = acc[14] = acc[15] = zero;
+}
+
+// The derived-X=1 layout: T[0..4] = (T_a(0), T_c(0), T_c(inf), T_b(0), T_b(inf)) of a side, times HI'; slots
+// 0 = Z, 1-2 = A, 3 = GA, 4-5 = GZ (the side's), 6-7 = b (both sides)
+constexpr int IR_NV_DER = 8;
+__device__ __forceinline__ void iround_scale_scatter_der(fr_t (&T)[8], fr_t* const* hi, uint32_t h, int side, bool any,
+                                                         fr_t (&acc)[16]) {
+    if (any) {
+        const fr_t hA = fr_load_l2(&(side ? hi[2] : hi[0])[h]);
+        const fr_t hC = fr_load_l2(&(side ? hi[3] : hi[1])[h]);
+        const fr_t hB = fr_load_l2(&(side ? hi[5] : hi[4])[h]);
+        T[0] = fr_mul_ni(T[0], hA);
+        T[1] = fr_mul_ni(T[1], hC);
+        T[2] = fr_mul_ni(T[2], hC);
+        T[3] = fr_mul_ni(T[3], hB);
+        T[4] = fr_mul_ni(T[4], hB);
+    }
+    const fr_t zero = fr_zero();
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        acc[k] = side ? zero : T[k];
+        acc[3 + k] = side ? T[k] : zero;
+    }
+    acc[6] = T[3];
+    acc[7] = T[4];
+#pragma unroll
+    for (int k = 8; k < 16; k++) acc[k] = zero;
 }
 
 // Transposed block reduction of 16 values per thread: each butterfly step of the warp halves the
@@ -1060,7 +1148,78 @@ __device__ __noinline__ void iround_g(const fr_t* tot, const fr_t* const* u, uin
     __syncthreads();
 }
 
-// MODE: bit 0 = FOLD, bit 1 = SRC (rounds 0 / 1 from the int32 words through byte tables in shared memory)
+// Derived X = 1 (MODE bit 2): per term x the round's totals V0 = T_x(0) (and V_inf for the quadratic terms)
+// come from the pairs; T_x(1) follows from the term's running sum sigma_x = beta(u, 0) T_x(0) + beta(u, 1) T_x(1):
+//     T_x(1) = (sigma_x - (1 - u) V0) u^-1                      (u = u_x[t], its inverse precomputed)
+// and g(X) = sum_x beta(u_x[t], X) T_x(X) as in iround_g.  After r_t: sigma_x <- beta(u_x[t], r_t) T_x(r_t).
+// (The proof is the same bytes: the three-value form of every term is the one the explicit path sums.)
+__device__ __noinline__ void iround_g_der(const fr_t* tot, const fr_t* const* u, uint32_t t, const fr_t* sigma,
+                                          const fr_t* uinv, fr_t* V /* smem [15] */, fr_t* prod, fr_t* g) {
+    const int lane = threadIdx.x;
+    if (lane < 5) {
+        const int x = lane, base = x == 0 ? 0 : x == 1 ? 1 : x == 2 ? 3 : x == 3 ? 4 : 6;
+        const bool quad = x != 0 && x != 2;
+        const fr_t V0 = tot[base], Vi = quad ? tot[base + 1] : fr_zero();
+        const fr_t uu = fr_load(&u[x][t]);
+        const fr_t V1 = fr_mul_cold(fr_sub(fr_load_l2(&sigma[x]), fr_mul_cold(fr_sub(fr_one(), uu), V0)), fr_load(&uinv[x]));
+        V[3 * x] = V0;
+        V[3 * x + 1] = V1;
+        V[3 * x + 2] = Vi;
+    }
+    __syncthreads();
+    const fr_t one = fr_one(), zero = fr_zero();
+    if (lane < 15) {
+        const int x = lane / 3, k = lane % 3;
+        const uint32_t X = k == 0 ? 0u : k + 1u;
+        const fr_t V0 = V[3 * x], V1 = V[3 * x + 1], Vi = V[3 * x + 2];
+        const fr_t lin = fr_sub(fr_sub(V1, V0), Vi);
+        fr_t T = V0;
+        for (uint32_t i = 0; i < X; i++) T = fr_add(T, lin);
+        for (uint32_t i = 0; i < X * X; i++) T = fr_add(T, Vi);
+        const fr_t uu = fr_load(&u[x][t]);
+        const fr_t slope = fr_sub(fr_add(uu, uu), one);
+        fr_t be = fr_sub(one, uu);
+        for (uint32_t i = 0; i < X; i++) be = fr_add(be, slope);
+        prod[lane] = fr_mul_cold(be, T);
+    }
+    __syncthreads();
+    if (lane < 3) {
+        fr_t sum = zero;
+        for (int x = 0; x < 5; x++) sum = fr_add(sum, prod[3 * x + lane]);
+        g[lane] = sum;
+    }
+    __syncthreads();
+}
+// sigma_x <- beta(u_x[t], r_t) T_x(r_t) (lanes 0-4, after r_t is published)
+__device__ __noinline__ void iround_sigma_der(const fr_t* V, const fr_t* const* u, uint32_t t, const fr_t* r_t, fr_t* sigma) {
+    const int x = threadIdx.x;
+    if (x < 5) {
+        const fr_t r = fr_load_l2(r_t), uu = fr_load(&u[x][t]);
+        const fr_t V0 = V[3 * x], V1 = V[3 * x + 1], Vi = V[3 * x + 2];
+        const fr_t lin = fr_sub(fr_sub(V1, V0), Vi);
+        const fr_t Tr = fr_add(fr_add(V0, fr_mul_cold(r, lin)), fr_mul_cold(fr_mul_cold(r, r), Vi));
+        const fr_t ur = fr_mul_cold(uu, r);
+        const fr_t be = fr_add(fr_sub(fr_sub(fr_one(), uu), r), fr_add(ur, ur));
+        fr_store(&sigma[x], fr_mul_cold(be, Tr));
+    }
+}
+
+// u^-1 for the derived-X=1 rounds: out[t][x] = u_x[t]^-1, t < t1 (Fermat; traps on u = 0, probability ~2^-250
+// per value, rather than emit a wrong proof)
+struct UPts {
+    const fr_t* u[5];
+};
+__global__ void k_relu_uinv(UPts P, uint32_t t1, fr_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 5 * t1) return;
+    const uint32_t t = i / 5, x = i % 5;
+    const fr_t u = fr_load(&P.u[x][t]);
+    if (fr_is_zero(u)) __trap();
+    fr_store(&out[i], fr_inv(u));
+}
+
+// MODE: bit 0 = FOLD, bit 1 = SRC (rounds 0 / 1 from the int32 words through byte tables in shared memory),
+// bit 2 = DER (the X = 1 totals derived from the per-term sums)
 template <int MODE>
 // the factored i-round's CTA shape (threads, CTAs per SM): registers per thread = 64K / (threads x CTAs)
 #ifndef ZKDL_IR_LB_T
@@ -1071,7 +1230,9 @@ template <int MODE>
 #endif
 __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IRoundArgs a) {
     constexpr bool FOLD = MODE & 1;
-    constexpr int SRC = MODE >> 1;
+    constexpr int SRC = (MODE >> 1) & 1;
+    constexpr bool DER = MODE & 4;
+    constexpr int NV = DER ? IR_NV_DER : IR_NV;
     const int side = threadIdx.x & 1;
     const uint32_t pb = a.lo_cnt - 1;   // log2 of the pairs per HI block
     const uint32_t h = blockIdx.x / a.cpb, cib = blockIdx.x % a.cpb;
@@ -1113,16 +1274,19 @@ __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IR
 #pragma unroll
     for (int k = 0; k < 8; k++) T[k] = fr_zero();
     const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
-    iround_pairs<FOLD, SRC>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+    iround_pairs<FOLD, SRC, DER>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
     fr_t v[16];
-    iround_scale_scatter(T, a.hi, h, side, j0 < (1ull << pb), v);
+    if constexpr (DER)
+        iround_scale_scatter_der(T, a.hi, h, side, j0 < (1ull << pb), v);
+    else
+        iround_scale_scatter(T, a.hi, h, side, j0 < (1ull << pb), v);
     __shared__ fr_t sm[8 * 16];
     __shared__ fr_t tot[16];
     __shared__ fr_t prod[15];
     __shared__ fr_t g[3];
     __shared__ bool is_last;
     block_transpose_sum16(v, sm);
-    if (threadIdx.x < IR_NV) fr_store(&a.partials[blockIdx.x * IR_NV + threadIdx.x], v[0]);
+    if (threadIdx.x < NV) fr_store(&a.partials[blockIdx.x * NV + threadIdx.x], v[0]);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -1137,14 +1301,25 @@ __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IR
         for (int k = 0; k < 16; k++) w[k] = fr_zero();
         for (unsigned int bb = threadIdx.x; bb < gridDim.x; bb += blockDim.x)
 #pragma unroll
-            for (int k = 0; k < IR_NV; k++) w[k] = fr_add(w[k], fr_load_l2(&a.partials[bb * IR_NV + k]));
+            for (int k = 0; k < NV; k++) w[k] = fr_add(w[k], fr_load_l2(&a.partials[bb * NV + k]));
         block_transpose_sum16(w, sm);
-        if (threadIdx.x < IR_NV) tot[threadIdx.x] = w[0];
+        if (threadIdx.x < NV) tot[threadIdx.x] = w[0];
     }
     if (threadIdx.x == 0) *a.ticket = 0;
     __syncthreads();
-    iround_g(tot, a.u, a.t, prod, g);
-    iround_finish(ifinish_of(a), g);
+    if constexpr (DER) {
+        __shared__ fr_t V[15];
+        __shared__ fr_t msg[4];
+        iround_g_der(tot, a.u, a.t, a.sigma, a.uinv, V, prod, g);
+        const IFinish f = ifinish_of(a);
+        iround_transcript(f, g, msg);
+        iround_rescale(f);
+        iround_claim(f, msg);
+        iround_sigma_der(V, a.u, a.t, a.r_out, a.sigma);
+    } else {
+        iround_g(tot, a.u, a.t, prod, g);
+        iround_finish(ifinish_of(a), g);
+    }
 }
 
 // The small i-rounds t0 .. t1-1 in ONE cooperative launch (1 + 2^hb * cpb CTAs, at most one per SM):
@@ -1496,6 +1671,24 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     ja.rj_out = r_all;
     ja.byte_tab = byte_tab;
     ja.kappa = kappa;
+    // derived X = 1 in the factored i-rounds (ZKDL_IR_DERIVE=0: every total from the pairs)
+    static const bool derive_off = getenv("ZKDL_IR_DERIVE") && atoi(getenv("ZKDL_IR_DERIVE")) == 0;
+    const bool unfactored_ = getenv("ZKDL_IROUND_V") && atoi(getenv("ZKDL_IROUND_V")) == 0;
+    const bool derive = !derive_off && !unfactored_;
+    fr_t* sigma = derive ? s.alloc<fr_t>(5) : nullptr;
+    ja.sigma = sigma;
+    fr_t* uinv = nullptr;
+    if (derive) {   // u_x[t]^-1 for every i-round (Fermat, ~0.2 ms) on the aux stream, behind the bit sums
+        uinv = s.alloc<fr_t>(5ull * logD);
+        UPts P;
+        for (int x = 0; x < 5; x++) P.u[x] = u_i[x];
+        cudaStream_t aux = ctx->aux_stream();
+        ZK_CUDA(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+        ZK_CUDA(cudaStreamWaitEvent(aux, ctx->aux_ev[0], 0));
+        k_relu_uinv<<<(5 * logD + 63) / 64, 64, 0, aux>>>(P, logD, uinv);
+        after_launch(ctx, "k_relu_uinv");
+        ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], aux));
+    }
     ZK_LAUNCH(ctx, k_relu_jrounds, 1, 256, 0, ja);
 
     const uint32_t hb = logD < 5 ? logD : 5;
@@ -1557,7 +1750,10 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     if (words) {
         ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
         ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
     }
+    if (derive) ZK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // u^-1 before the first i-round
     for (uint32_t t = 0; t < t0; t++) {
         IRoundArgs a;
         memset(&a, 0, sizeof a);
@@ -1585,6 +1781,8 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         a.msg_out = proof + 140 + 128ull * (logB + t);
         a.r_out = r_all + logB + t;
         a.point_out = out.d_point + 32ull * (logB + t);
+        a.sigma = sigma;
+        a.uinv = derive ? uinv + 5ull * t : nullptr;
         if (unfactored) {
             const unsigned int grid = grid_for(ctx, 2 * a.n_pairs, 256, 2);   // two threads per pair
             if (fold)
@@ -1609,14 +1807,24 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
                 a.qr_mask = qr_mask;
                 a.sig_bit = QR - 1;
                 a.nbytes = nbytes;
-                if (fold)
+                if (fold && derive)
+                    ZK_LAUNCH(ctx, k_relu_iround_f<7>, grid, ithreads, tb_smem, a);
+                else if (fold)
                     ZK_LAUNCH(ctx, k_relu_iround_f<3>, grid, ithreads, tb_smem, a);
+                else if (derive)
+                    ZK_LAUNCH(ctx, k_relu_iround_f<6>, grid, ithreads, tb_smem / 2, a);
                 else
                     ZK_LAUNCH(ctx, k_relu_iround_f<2>, grid, ithreads, tb_smem / 2, a);
             } else if (fold) {
-                ZK_LAUNCH(ctx, k_relu_iround_f<1>, grid, ithreads, 0, a);
+                if (derive)
+                    ZK_LAUNCH(ctx, k_relu_iround_f<5>, grid, ithreads, 0, a);
+                else
+                    ZK_LAUNCH(ctx, k_relu_iround_f<1>, grid, ithreads, 0, a);
             } else {
-                ZK_LAUNCH(ctx, k_relu_iround_f<0>, grid, ithreads, 0, a);
+                if (derive)
+                    ZK_LAUNCH(ctx, k_relu_iround_f<4>, grid, ithreads, 0, a);
+                else
+                    ZK_LAUNCH(ctx, k_relu_iround_f<0>, grid, ithreads, 0, a);
             }
         }
         lo_level ^= 1;
