@@ -1,7 +1,7 @@
 #!/bin/bash
 # closing run: full GPU suite, smoke, bench lines, C5 sweep, launch list and ncu captures
 set -u
-OUT=gpurun_out/r3z; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-r3z}; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()"
 timeout 2400 python -m pytest tests -m gpu -q --durations=10 > $OUT/gpu_tests.txt 2>&1; echo "tests exit=$?"; tail -3 $OUT/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke exit=$?"; tail -1 $OUT/smoke.txt
