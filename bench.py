@@ -398,7 +398,8 @@ def run_ours(args, rank, world, local):
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
             pend = [chain.enqueue_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                                 wctx=cwctxs[i % 2], merge_ctxs=mctxs) for i in range(args.steps)]
+                                                 wctx=cwctxs[i % 2], merge_ctxs=mctxs, serial=bool(args.chain_serial))
+                    for i in range(args.steps)]
             for st in streams_all:   # the region ends when every stream of every window has
                 ev = torch.cuda.Event()
                 ev.record(st)
@@ -412,7 +413,7 @@ def run_ours(args, rank, world, local):
         cms = max_over_ranks(c0.elapsed_time(c1), world) / args.steps
         cby = by_kernel(ctab)
         chained = {"ms_per_step": round(cms, 4), "s_per_update": cms / 1000.0 / shape.steps,
-                   "merge_streams": args.merge_streams,
+                   "merge_streams": args.merge_streams, "serial_windows": bool(args.chain_serial),
                    "kernels_ms_one_window_serialised": {k: round(t, 4) for k, (n, t) in
                                                         sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
                    "kernel_launches_one_window": {k: n for k, (n, t) in sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
@@ -959,6 +960,9 @@ def main():
                     help="streams (contexts) the matmul families are spread over, side by side")
     ap.add_argument("--merge-aux", type=int, default=0, choices=[0, 1],
                     help="1: every zkReLU family ends with the aux-claim merge (P:L470, DESIGN.md D21)")
+    ap.add_argument("--chain-serial", type=int, default=1, choices=[0, 1],
+                    help="chained window: 1 = each window starts after the previous window's zkReLU stage (no "
+                         "cross-window overlap: overlapping windows stalled on co-residency in some runs)")
     ap.add_argument("--merge-budget", type=int, default=0,
                     help="chained window: total SM budget of the claim merges' persistent grids (0: 148)")
     ap.add_argument("--relu-priority", type=int, default=-1, help="CUDA stream priority of the zkReLU stream (lower = higher)")

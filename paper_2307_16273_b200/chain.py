@@ -116,14 +116,15 @@ def _fence(src, dsts):
 
 def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
                            relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
-                           wctx: api.Context | None = None, merge_ctxs: list | None = None):
+                           wctx: api.Context | None = None, merge_ctxs: list | None = None, serial: bool = False):
     """Enqueue one chained window without synchronising; returns a handle for collect_window_chained.
     Streams: the window transcript W on wctx (default ctx); stages 1-2 over ctx + mm_ctxs; stage 3 on
     relu_ctx.  Nothing at the end of a window makes the stage 1-2 streams wait for its stage 3 (the
     child transcripts are freed in collect_window_chained), so with a different wctx per window the
     next window's matmul families and merges run while this window's zkReLU proves.  merge_ctxs
     (optional): the streams stage 2 spreads its claim merges over (latency-bound sumchecks: many
-    budgeted streams side by side), default ctx + mm_ctxs."""
+    budgeted streams side by side), default ctx + mm_ctxs.  serial: the window starts after the zkReLU stream's
+    earlier work (no overlap with the previous window's stage 3)."""
     dev = next(f.A for f in families if f.kind == "matmul").device
     mms = [f for f in families if f.kind == "matmul"]
     losses = [f for f in families if f.kind == "loss"]
@@ -195,6 +196,8 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         keep.append(g)
         return g
 
+    if serial:
+        _fence(rctx, lanes1 + [wctx])
     W = api.Transcript(wctx, seed)
     W.absorb("fcn/chdr", header)
     # ---- stage 1: the matmul families
