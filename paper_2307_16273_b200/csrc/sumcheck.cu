@@ -48,6 +48,10 @@ struct ScRoundArgs {
     uint8_t* point_out;      // r_t canonical
     fr_t* part_out;          // sharded mode: write the (scaled) K+1 totals here instead of the transcript step
     const fr_t* scale;       // sharded mode: the rank's eq factor over its high bits (nullptr = 1)
+    // running claim (single-device provers): c_t in, c_{t+1} = f_t(r_t) out after the challenge; the derived-X=1
+    // rounds (k_sc_round2f MODE bit 2) take f_t(1) from it: (c_t - (1 - w_t) f_t(0)) w_t^-1, or c_t - f_t(0)
+    fr_t* run_claim;
+    const fr_t* winv;        // w_t^-1 for every t < n_eq (derived rounds under the eq factor)
 };
 
 // Finalizer of a product-sumcheck round (last block, warp 0): the claim of round 0 (when computed),
@@ -86,6 +90,11 @@ __device__ __noinline__ void sc_finish(const ScRoundArgs& a, const fr_t* tot, co
     if (lane == 0) {
         fr_store(a.r_out, rt);
         fr_canon_to_bytes(fs.rc, a.point_out);
+        if (a.run_claim) {   // c_{t+1} = f_t(r_t) (Lagrange through the message's K + 1 points)
+            fr_t e[4];
+            for (int x = 0; x <= K; x++) e[x] = tot[x];
+            fr_store(a.run_claim, interp_small(e, K, rt));
+        }
     }
     fs_end(fs, a.st);
 }
@@ -356,7 +365,8 @@ __device__ __forceinline__ fr2p_t sc_mul2(const fr_t& a0, const fr_t& b0, const 
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     const ScRoundArgs& a = A.r;
-    constexpr bool FOLD = MODE == 1 || MODE == 3;   // MODE 3: round 1 folding straight from the int32 tables
+    constexpr bool FOLD = (MODE & 3) == 1 || (MODE & 3) == 3;   // MODE 3: round 1 folding straight from the int32 tables
+    constexpr bool DER = MODE & 4;   // f(1) derived in the finalizer from the running claim: P(0), P(inf) only
     const bool has_e = a.eq_mode != 0;
     const uint32_t lo_cnt = has_e ? a.lo_cnt : 0;
     // pairs per group (log2): the LO range; without eq weights the whole round is one group
@@ -371,7 +381,7 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     fr_t r;
     if (FOLD) r = fr_load(a.r_prev);
     FoldI32 fi;
-    if (MODE == 3) {   // residues (1 - r) R^2, r R^2, -2^31 R^2 (fr_mul(x R, R^2) = x R^2)
+    if ((MODE & 3) == 3) {   // residues (1 - r) R^2, r R^2, -2^31 R^2 (fr_mul(x R, R^2) = x R^2)
         fi.r2 = fr_mul(r, ZK_R2);
         fi.omr2 = fr_mul(fr_sub(fr_one(), r), ZK_R2);
         fi.cneg = fr_mul(fr_neg(fr_from_u32(0x80000000u)), ZK_R2);
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
             bool q_done = false;
             if (FOLD) {
                 fr_t x0, x1, x2, x3, z0, z1, z2, z3;
-                if constexpr (MODE == 3) {   // fold straight from the int32 tables (fold4_i32_ni)
+                if constexpr ((MODE & 3) == 3) {   // fold straight from the int32 tables (fold4_i32_ni)
                     const int4 ia = __ldcs(reinterpret_cast<const int4*>(A.i32[0]) + b);
                     const int4 ib = __ldcs(reinterpret_cast<const int4*>(A.i32[1]) + b);
                     const fr2_t fa = fold2_i32_ni(fi, ia), fb = fold2_i32_ni(fi, ib);
@@ -419,7 +429,7 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                 a1 = fr_add(x2, f.y);
                 b0 = fr_add(z0, f.z);
                 if (has_e && !(A.flat && a.eq_hi)) {
-                    q = sc_mul3(r, fr_sub(z3, z2), e, a0, e, a1);
+                    q = sc_mul3(r, fr_sub(z3, z2), e, a0, e, DER ? fr_sub(a1, a0) : a1);
                     b1 = fr_add(z2, q.x);
                     q_done = true;
                 } else {
@@ -429,7 +439,7 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                     if (has_e) e = g2.y;
                 }
                 }
-                if constexpr (MODE == 3) {
+                if constexpr ((MODE & 3) == 3) {
                     if (has_e && A.flat && a.eq_hi) e = fr_mul_ni(e, fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]));
                 }
                 fr_store(a.dst[0] + 2 * b, a0);
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                 fr_store(a.dst[1] + 2 * b, b0);
                 fr_store(a.dst[1] + 2 * b + 1, b1);
             } else {
-                if (MODE == 2) {
+                if ((MODE & 3) == 2) {
                     const int2 ia = __ldcs(reinterpret_cast<const int2*>(A.i32[0]) + b);
                     const int2 ib = __ldcs(reinterpret_cast<const int2*>(A.i32[1]) + b);
                     const fr4_t em = fr_embed4_ni(ia.x, ia.y, ib.x, ib.y);
@@ -456,6 +466,23 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
                     b1 = fr_load_cg(a.src[1] + 2 * b + 1);
                 }
                 if (has_e && A.flat && a.eq_hi) e = fr_mul_ni(e, fr_load(&a.eq_hi[(b >> lo_cnt) & hi_mask]));
+            }
+            if constexpr (DER) {   // y0 = E' a0, yd = E' (a1 - a0); P(0) = y0 b0, P(inf) = yd (b1 - b0)
+                fr_t y0 = a0, yd = fr_sub(a1, a0);
+                if (has_e) {
+                    if (q_done) {
+                        y0 = q.y;
+                        yd = q.z;
+                    } else {
+                        const fr2p_t q2 = sc_mul2(e, a0, e, yd);
+                        y0 = q2.x;
+                        yd = q2.y;
+                    }
+                }
+                const fr2p_t p = sc_mul2(y0, b0, yd, fr_sub(b1, b0));
+                s0 = fr_add(s0, p.x);
+                si = fr_add(si, p.y);
+                continue;
             }
             fr_t y0 = a0, y1 = a1;
             if (has_e) {
@@ -489,8 +516,18 @@ __global__ void __launch_bounds__(256, 2) k_sc_round2f(Sc2Args A) {
     if (grid_reduce_fr_block<3>(acc, a.partials, a.ticket, tt)) {
         if (threadIdx.x == 0) {   // evaluations at X = 0, 1, 2 of the quadratic with P(0), P(1), P(inf)
             msg[0] = tt[0];
-            msg[1] = tt[1];
-            msg[2] = fr_sub(fr_dbl(fr_add(tt[1], tt[2])), tt[0]);
+            if (DER) {   // (1 - w_t) f(0) + w_t f(1) = c_t under the eq factor, f(0) + f(1) = c_t after it
+                const fr_t c = fr_load_l2(a.run_claim);
+                if (a.t < a.n_eq) {
+                    const fr_t w = fr_load(&a.w[a.t]);
+                    msg[1] = fr_mul_cold(fr_sub(c, fr_mul_cold(fr_sub(fr_one(), w), tt[0])), fr_load(&a.winv[a.t]));
+                } else {
+                    msg[1] = fr_sub(c, tt[0]);
+                }
+            } else {
+                msg[1] = tt[1];
+            }
+            msg[2] = fr_sub(fr_dbl(fr_add(msg[1], tt[2])), tt[0]);
         }
         __syncthreads();
         sc_finish(a, msg, 2);
@@ -732,6 +769,12 @@ void ScEngine::round(fr_t* part_out) {
     a.point_out = d_point + 32ull * t;
     a.part_out = part_out;
     a.scale = d_scale;
+    const bool der = derive && fold && !part_out && K == 2 && factored && !zero;
+    if (derive && !part_out) {
+        a.run_claim = run_claim;
+        a.winv = winv;
+    }
+    if (der && tl == 1 && winv) ZK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // w^-1 ready
     if (zero) {
         const unsigned int grid = grid_for(ctx, n_pairs, 256, 4);
         if (fold)
@@ -773,9 +816,15 @@ void ScEngine::round(fr_t* part_out) {
         } else if (from_i32) {
             ZK_LAUNCH(ctx, k_sc_round2f<2>, grid, 256, 0, A);
         } else if (fold && tl == 1 && int0_used) {
-            ZK_LAUNCH(ctx, k_sc_round2f<3>, grid, 256, 0, A);
+            if (der)
+                ZK_LAUNCH(ctx, k_sc_round2f<7>, grid, 256, 0, A);
+            else
+                ZK_LAUNCH(ctx, k_sc_round2f<3>, grid, 256, 0, A);
         } else if (fold) {
-            ZK_LAUNCH(ctx, k_sc_round2f<1>, grid, 256, 0, A);
+            if (der)
+                ZK_LAUNCH(ctx, k_sc_round2f<5>, grid, 256, 0, A);
+            else
+                ZK_LAUNCH(ctx, k_sc_round2f<1>, grid, 256, 0, A);
         } else {
             ZK_LAUNCH(ctx, k_sc_round2f<0>, grid, 256, 0, A);
         }
@@ -1184,6 +1233,15 @@ static void sumcheck_prove_small(zk_ctx* ctx, zk_transcript* tr, const ScStateme
     }
 }
 
+// out[i] = in[i]^-1 (Fermat; traps on zero: probability ~2^-250 per transcript challenge)
+__global__ void k_fr_inv_batch(const fr_t* in, uint32_t n, fr_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const fr_t x = fr_load(&in[i]);
+    if (fr_is_zero(x)) __trap();
+    fr_store(&out[i], fr_inv(x));
+}
+
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
     const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
     ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
@@ -1211,6 +1269,21 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
     e.header();
     e.setup(S.tables, m, 0, n_eq);
     e.set_i32(S.i32);
+    // derived X = 1 in the folding rounds of the factored K = 2 kernel (ZKDL_SC_DERIVE=0: explicit f(1))
+    static const bool der_off = getenv("ZKDL_SC_DERIVE") && atoi(getenv("ZKDL_SC_DERIVE")) == 0;
+    if (!der_off && K == 2 && e.factored && m >= 2) {
+        e.derive = true;
+        e.run_claim = s.alloc<fr_t>(1);
+        if (n_eq) {
+            e.winv = s.alloc<fr_t>(n_eq);
+            cudaStream_t aux = ctx->aux_stream();
+            ZK_CUDA(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+            ZK_CUDA(cudaStreamWaitEvent(aux, ctx->aux_ev[0], 0));
+            k_fr_inv_batch<<<(n_eq + 63) / 64, 64, 0, aux>>>(S.d_w, n_eq, e.winv);
+            after_launch(ctx, "k_fr_inv_batch");
+            ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], aux));
+        }
+    }
     e.run_to_end();
 }
 

@@ -47,6 +47,11 @@ struct ScEngine {
     bool zero = false;      // N2 zero form (D22): K = 3 tables (Y, A, B), terms Y - A B, 3 evaluations
     bool int0_used = false; // round 0 ran on the int32 tables in integers (cur[] not embedded; round 1 folds
                             // from the int32 tables)
+    // derived X = 1 (single-device provers from round 0, K = 2 factored): the running claim every
+    // finalizer updates and w_t^-1 (computed on the aux stream; the rounds from 1 on wait for it)
+    bool derive = false;
+    fr_t* run_claim = nullptr;
+    fr_t* winv = nullptr;
     uint32_t nev() const { return zero ? 3 : K + 1; }   // evaluations per round message
 
     // int32 tables: round 0 of the factored kernel embeds them into the (scratch) cur tables; otherwise

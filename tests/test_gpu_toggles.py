@@ -2,6 +2,8 @@
 alternative path a switch selects is run in a subprocess and compared with the oracle (bit-exact).
 
     ZKDL_SC_INT0=0       C5 round 0 through the embedding kernel instead of the integer round 0
+    ZKDL_SC_DERIVE=0     product-sumcheck folding rounds with f(1) summed over the pairs (not derived from the
+                         running claim)
     ZKDL_RELU_WORDS=0    zkReLU i-rounds 0/1 from materialised tables instead of the words
     ZKDL_IR_DERIVE=0     zkReLU i-rounds with every X = 1 total summed over the pairs (not derived from the
                          per-term sums)
@@ -71,7 +73,8 @@ def run(snippet: str, env: dict, args=()) -> dict:
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{}, {"ZKDL_SC_INT0": "0"}])
+@pytest.mark.parametrize("env", [{}, {"ZKDL_SC_INT0": "0"}, {"ZKDL_SC_DERIVE": "0"},
+                                 {"ZKDL_SC_DERIVE": "0", "ZKDL_SC_INT0": "0"}])
 def test_c5_paths(oracle_lib, env):
     from oracle import drivers
     o = drivers.c5_prove(19)
