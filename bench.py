@@ -582,7 +582,10 @@ def c5_frmul_model(m: int, tail_log: int = 16, hb: int = 5) -> dict:
     group ("int_mac_per_pair"); round 1 (k_sc_round2f folding from int32): 4 folds, each two 32 x 256-bit
     multiply-accumulates and one reduction (3/4 of a product) + E' a (2) + 3 = 8; folding rounds: fold 4 + 2 + 3 = 9 (plus one HI product
     per pair where the groups are too small, "flat"); the last rounds (<= 2^tail_log entries after the
-    fold) in k_sc_all: fold 4 + eq 1 + 3 x 2 = 11 per pair (7 in the last, eq-free round)."""
+    fold) in k_sc_all: fold 4 + eq 1 + 3 x 2 = 11 per pair (7 in the last, eq-free round).  With f(1) derived
+    from the running claim (ZKDL_SC_DERIVE, the default) the folding rounds of k_sc_round2f skip one product:
+    round 1 7, folding rounds 8."""
+    derive = os.environ.get("ZKDL_SC_DERIVE", "1") != "0"
     out = {"k_sc_round2f": 0, "k_sc_all": 0, "k_sc_round0_int": 0}
     int0 = False
     for t in range(m):
@@ -598,7 +601,7 @@ def c5_frmul_model(m: int, tail_log: int = 16, hb: int = 5) -> dict:
             out["int_mac_per_pair"] = 3
             int0 = True
             continue
-        per = 7 if t == 0 else (8 if t == 1 and int0 else 9)
+        per = 7 if t == 0 else (8 if t == 1 and int0 else 9) - (1 if derive and t >= 1 else 0)
         out["k_sc_round2f"] += pairs * (per + (1 if flat else 0))
     out["total"] = out["k_sc_round2f"] + out["k_sc_all"]
     return out
