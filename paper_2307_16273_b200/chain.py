@@ -185,8 +185,9 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         L = api.claim_merge_layout(0, 2, logD + logB)
         layR.append((f, logD, logB, rl, L, off, api._a16(rl) + L["total"]))
         off += _slot(api._a16(rl) + L["total"])
-    out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(wctx.stream):   # on the window transcript's stream, which every stage forks from
+        out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
     keep = []   # device temporaries in use by enqueued work
 
     def gather(c, ranges):

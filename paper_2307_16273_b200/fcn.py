@@ -112,8 +112,6 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
         info, n = _layout(f, merge_aux)
         lay.append((f, info, off, n))
         off += _slot(n)
-    out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
-    flag = torch.zeros(1, dtype=torch.int32, device=dev)
     two = relu_ctx is not None and relu_ctx.stream != ctx.stream
     lanes = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
     home = {}
@@ -128,6 +126,11 @@ def enqueue_window(ctx: api.Context, seed: bytes, header: bytes, families: list,
     wc = wctx if own_w else ctx
     # streams that fork from and join back into the window transcript's stream
     side = ([relu_ctx] if two else []) + (lanes if own_w else lanes[1:])
+    # the output buffer and the range flag on the window transcript's stream: every proof stream forks from
+    # it after the zero fill, whatever the caller's current stream is
+    with torch.cuda.stream(wc.stream):
+        out = torch.empty(off + 256, dtype=torch.uint8, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
     W = api.Transcript(wc, seed)
     W.absorb("fcn/hdr", header)
     kids = []
