@@ -371,24 +371,41 @@ def run_ours(args, rank, world, local):
             # rounds of the previous window (k_relu_ipersist needs ~65 SMs co-resident; a cooperative launch
             # that cannot get them waits, and the window's critical path with it)
             c.set_sm_budget(max(4, (args.merge_budget or 148) // max(1, args.merge_streams)))
-        streams_all = [c.stream for c in ctxs + cwctxs + mctxs]
+        # the top layer's rescale (+ its aux merge) beside the zkReLU on a stream of its own
+        rsctx = api.Context(local, torch.cuda.Stream(device=local)) if args.rescale_stream else None
+        if rsctx is not None:   # its persistent grids (k_sc_all: one SM per CTA) beside k_relu_ipersist (129
+            # CTAs, two per SM): 2 x (148 - 32) >= 129, so neither can be left partly resident (no
+            # spin-wait deadlock between the two)
+            rsctx.set_sm_budget(32)
+        # the claim merges stage 3 does not wait for (D25 order), beside it: 4 streams x 12 SMs (+ the rescale's
+        # 32 <= 148 - 65, the co-residency rule of chain.enqueue_window_chained)
+        # stage 1 (the matmul families, latency-bound persistent sumchecks) alone on the GPU in serial windows: its
+        # own --chain-mm-streams contexts, 148 SMs shared out
+        nmm1 = max(1, args.chain_mm_streams)
+        c1ctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(nmm1)]
+        for c in c1ctxs:
+            c.set_sm_budget(max(4, 148 // nmm1))
+        lctxs = [api.Context(local, torch.cuda.Stream(device=local)) for _ in range(args.late_streams)]
+        for c in lctxs:
+            c.set_sm_budget(max(2, 48 // max(1, args.late_streams)))
+        streams_all = [c.stream for c in ctxs + cwctxs + mctxs + ([rsctx] if rsctx else []) + lctxs + c1ctxs]
         with torch.cuda.stream(stream):
             for i in range(2):
-                chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                           wctx=cwctxs[i % 2], merge_ctxs=mctxs)
+                chain.prove_window_chained(c1ctxs[0], cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=c1ctxs[1:],
+                                           wctx=cwctxs[i % 2], merge_ctxs=mctxs, rescale_ctx=rsctx, late_ctxs=lctxs or None)
             torch.cuda.synchronize()
             # the kernel table of one window (every launch bracketed, outside the timed region)
             prof_on(None)
             for c in cwctxs:
                 c.profile(True)
                 c.profile_read()
-            for c in mctxs:
+            for c in mctxs + ([rsctx] if rsctx else []) + lctxs + c1ctxs:
                 c.profile(True)
                 c.profile_read()
-            chain.prove_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs, wctx=cwctxs[0],
-                                       merge_ctxs=mctxs)
+            chain.prove_window_chained(c1ctxs[0], cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=c1ctxs[1:], wctx=cwctxs[0],
+                                       merge_ctxs=mctxs, rescale_ctx=rsctx, late_ctxs=lctxs or None)
             ctab = prof_off()
-            for c in cwctxs + mctxs:
+            for c in cwctxs + mctxs + ([rsctx] if rsctx else []) + lctxs + c1ctxs:
                 for k, v in c.profile_read().items():
                     n0, t0 = ctab.get(k, (0, 0.0))
                     ctab[k] = (n0 + v[0], t0 + v[1])
@@ -397,8 +414,10 @@ def run_ours(args, rank, world, local):
             barrier(world)
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record(stream)
-            pend = [chain.enqueue_window_chained(ctx, cseed, header, cfams, cts, relu_ctx=relu_ctx, mm_ctxs=mm_ctxs,
-                                                 wctx=cwctxs[i % 2], merge_ctxs=mctxs, serial=bool(args.chain_serial))
+            pend = [chain.enqueue_window_chained(c1ctxs[0], cseed, header, cfams, cts, relu_ctx=relu_ctx,
+                                                 mm_ctxs=c1ctxs[1:],
+                                                 wctx=cwctxs[i % 2], merge_ctxs=mctxs, serial=bool(args.chain_serial),
+                                                 rescale_ctx=rsctx, late_ctxs=lctxs or None)
                     for i in range(args.steps)]
             for st in streams_all:   # the region ends when every stream of every window has
                 ev = torch.cuda.Event()
@@ -414,6 +433,8 @@ def run_ours(args, rank, world, local):
         cby = by_kernel(ctab)
         chained = {"ms_per_step": round(cms, 4), "s_per_update": cms / 1000.0 / shape.steps,
                    "merge_streams": args.merge_streams, "serial_windows": bool(args.chain_serial),
+                   "rescale_stream": bool(args.rescale_stream), "late_merge_streams": args.late_streams,
+                   "stage1_streams": nmm1,
                    "kernels_ms_one_window_serialised": {k: round(t, 4) for k, (n, t) in
                                                         sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
                    "kernel_launches_one_window": {k: n for k, (n, t) in sorted(cby.items(), key=lambda kv: -kv[1][1])[:14]},
@@ -950,6 +971,12 @@ def main():
     ap.add_argument("--c5-log", type=int, default=26, help="C5: log2 m of the 2^m hypercube (22..30)")
     ap.add_argument("--no-c5", action="store_true", help="C4 line without the embedded C5 measurement")
     ap.add_argument("--no-chained", action="store_true", help="C4 line without the chained-window (N3) measurement")
+    ap.add_argument("--chain-mm-streams", type=int, default=8,
+                    help="chained window: streams (and SM budgets 148 / n) of stage 1's matmul families")
+    ap.add_argument("--late-streams", type=int, default=4,
+                    help="chained window: streams of the claim merges that prove beside stage 3 (0: after it)")
+    ap.add_argument("--rescale-stream", type=int, default=1,
+                    help="chained window: 1 = the top layer's rescale on its own stream, beside the zkReLU")
     ap.add_argument("--merge-streams", type=int, default=8, help="chained window: streams for the claim merges")
     ap.add_argument("--pipeline", type=int, default=0, choices=[0, 1],
                     help="1: consecutive windows on alternating zkReLU / transcript streams (measured 171 ms per "

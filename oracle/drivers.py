@@ -168,10 +168,12 @@ def fcn_prove_chained(shape, families, tensors, seed_name: str, top=None):
     """The claim-chained window (Protocol 1 lines 7-8; D25).  Window transcript W:
     "fcn/chdr" (header) | stage 1: per matmul family "fcn/fam" <name> and a fork; each family proved on
     its fork (D3a) | "fcn/join" per family | stage 2: per tensor family whose claims need merging (more
-    than one claim, or one claim on a view that is not the whole stack) "fcn/tfam" <name> and a fork; the
-    claim merge (D25) on it | joins | stage 3: per ReLU family "fcn/fam" <name> and a fork; the chained
-    zkReLU (points = the merged claims of its Z, A, G_A, G_Z stacks) and the aux merge (D21) on it
-    | joins.  Returns dict(matmul, merges, relu (per family name), opened: tensor family -> (point, value)
+    than one claim, or one claim on a view that is not the whole stack) AND that stage 3 is bound to (a ReLU
+    family's Z, A, G_A, G_Z, the rescale's Z, Z') "fcn/tfam" <name> and a fork; the claim merge (D25) on it
+    | joins | stage 3: per ReLU family "fcn/fam" <name> and a fork; the chained zkReLU (points = the merged
+    claims of its Z, A, G_A, G_Z stacks) and the aux merge (D21) on it; the rescale likewise; then
+    "fcn/tfam" <name> and a fork per remaining merge (the other tensor families, independent of stage 3) |
+    joins of stage 3, then of those merges.  Returns dict(matmul, merges, relu (per family name), opened: tensor family -> (point, value)
     for every committed stack and "aux:<ReLU family>" (one claim per tensor family, Protocol 1 line 10),
     window_state)."""
     W = O.Transcript(fs_seed(seed_name))
@@ -214,23 +216,39 @@ def fcn_prove_chained(shape, families, tensors, seed_name: str, top=None):
             opened[t.name] = (cl[0]["v"] + cl[0]["u"], cl[0]["c"])
         else:
             to_merge.append(t)
+    # stage 2 splits (D25, round-2 order): the merges of the stacks stage 3 is bound to (the ReLU families'
+    # Z, A, G_A, G_Z and the rescale's Z, Z') come first and are joined; the other merges are forked after
+    # stage 3's families, so they prove beside it
+    bound = {f.tensors[k] for f in relus for k in ("Z", "A", "GA", "GZ")} | \
+        {f.tensors[k] for f in rescales for k in ("Z", "Zp")}
+    merge_a = [t for t in to_merge if t.name in bound]
+    merge_b = [t for t in to_merge if t.name not in bound]
+    merges = {}
+
+    def prove_merges(ts, ks):
+        for t, T in zip(ts, ks):
+            r = O.claim_merge_prove(T, _tensor_values(t, families), claims[t.name])
+            r["state"] = T.state()
+            r["claims_in"] = claims[t.name]
+            merges[t.name] = r
+            opened[t.name] = (r["point"], r["claim"])
+
     mk = []
-    for t in to_merge:
+    for t in merge_a:
         W.absorb("fcn/tfam", t.name.encode())
         mk.append(fork())
-    merges = {}
-    for t, T in zip(to_merge, mk):
-        r = O.claim_merge_prove(T, _tensor_values(t, families), claims[t.name])
-        r["state"] = T.state()
-        r["claims_in"] = claims[t.name]
-        merges[t.name] = r
-        opened[t.name] = (r["point"], r["claim"])
+    prove_merges(merge_a, mk)
     for T in mk:
         W.absorb("fcn/join", T.state())
     rk = []
     for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
         rk.append(fork())
+    mkb = []
+    for t in merge_b:
+        W.absorb("fcn/tfam", t.name.encode())
+        mkb.append(fork())
+    prove_merges(merge_b, mkb)
     rres = {}
     for f, T in zip(relus + rescales, rk):
         if isinstance(f, RescaleFamily):   # D26, then the claim merge (D25) of its two aux claims
@@ -259,6 +277,6 @@ def fcn_prove_chained(shape, families, tensors, seed_name: str, top=None):
         logB = O.relu_logB(f.Q, f.R)
         rj, rs = r["merge"]["r"][:logB], r["merge"]["r"][logB:]
         opened["aux:" + f.name] = (rj + r["point"][logB:] + rs, r["merge"]["finals"][0])
-    for T in rk:
+    for T in rk + mkb:
         W.absorb("fcn/join", T.state())
     return dict(matmul=mres, merges=merges, relu=rres, opened=opened, window_state=W.state())

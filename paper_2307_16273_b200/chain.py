@@ -116,7 +116,9 @@ def _fence(src, dsts):
 
 def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
                            relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
-                           wctx: api.Context | None = None, merge_ctxs: list | None = None, serial: bool = False):
+                           wctx: api.Context | None = None, merge_ctxs: list | None = None, serial: bool = False,
+                           marks: list | None = None, rescale_ctx: api.Context | None = None,
+                           late_ctxs: list | None = None, late_after_relu: bool = False):
     """Enqueue one chained window without synchronising; returns a handle for collect_window_chained.
     Streams: the window transcript W on wctx (default ctx); stages 1-2 over ctx + mm_ctxs; stage 3 on
     relu_ctx.  Nothing at the end of a window makes the stage 1-2 streams wait for its stage 3 (the
@@ -124,7 +126,23 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     next window's matmul families and merges run while this window's zkReLU proves.  merge_ctxs
     (optional): the streams stage 2 spreads its claim merges over (latency-bound sumchecks: many
     budgeted streams side by side), default ctx + mm_ctxs.  serial: the window starts after the zkReLU stream's
-    earlier work (no overlap with the previous window's stage 3)."""
+    earlier work (no overlap with the previous window's stage 3).  rescale_ctx (optional): the stream of the
+    top layer's rescale and its aux merge, which then run beside the zkReLU instead of after it (their
+    transcript is a fork of its own, so only the scheduling changes, not a byte of the window).  late_ctxs
+    (optional): the streams of the claim merges stage 3 does not wait for (D25 order: forked after stage 3's
+    families), which then prove beside the zkReLU; default the zkReLU's stream (after it).  late_after_relu:
+    the late merges and the rescale start when the zkReLU sumcheck has been proved (beside its aux merge),
+    not at the start of stage 3 (the zkReLU's single-wave kernels lose most to throughput work beside them).  Co-residency:
+    k_relu_ipersist (129 CTAs, two per SM) must always find its SMs next to the persistent sumcheck grids
+    (k_sc_all, one SM per CTA) of the streams that run beside it, so the SM budgets of rescale_ctx and
+    late_ctxs should add up to <= 148 - 65.  marks (diagnostics): a list that receives
+    (label, stream, timing event) at the window's start, after every family / merge and at each stage join."""
+
+    def mark(label, c):
+        if marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(c.stream)
+            marks.append((label, c.stream, ev))
     dev = next(f.A for f in families if f.kind == "matmul").device
     mms = [f for f in families if f.kind == "matmul"]
     losses = [f for f in families if f.kind == "loss"]
@@ -133,6 +151,10 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     tmap = {t.name: t for t in tensors}
     lanes1 = [ctx] + [c for c in (mm_ctxs or []) if c.stream != ctx.stream]
     rctx = relu_ctx if relu_ctx is not None else ctx
+    sctx = rescale_ctx if rescale_ctx is not None else rctx
+    ctx3 = [rctx] + ([sctx] if sctx.stream != rctx.stream else [])
+    lanes2b = list(late_ctxs) if late_ctxs else [rctx]
+    ctx3 += [c for c in lanes2b if c.stream not in [x.stream for x in ctx3]]
     wctx = wctx if wctx is not None else ctx
     lanes2 = list(merge_ctxs) if merge_ctxs else lanes1
     # ---- layout of the window's output buffer
@@ -163,6 +185,11 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
             claims[tname].append(dict(map=mp, v=[(o, d)], u=[(o + 32 * d, m - d)], c=[(o + 32 * m + 32 * k, 1)],
                                       src=(f.name, role)))
     merges = [t for t in tensors if claims[t.name] and not is_whole(t.pad, [c["map"] for c in claims[t.name]])]
+    # D25 order: the merges of the stacks stage 3 is bound to first (joined before stage 3), the others after
+    # stage 3's forks
+    bound = {f.tensors[k] for f in relus for k in RELU_ROLES} | {f.tensors[k] for f in rescales for k in ("Z", "Zp")}
+    merges = [t for t in merges if t.name in bound] + [t for t in merges if t.name not in bound]
+    n2a = sum(1 for t in merges if t.name in bound)
     lay2 = []
     for t in merges:
         n = _log2(len(t.pad))
@@ -198,8 +225,10 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         return g
 
     if serial:
-        _fence(rctx, lanes1 + [wctx])
+        for c in ctx3:
+            _fence(c, lanes1 + [wctx])
     W = api.Transcript(wctx, seed)
+    mark("start", wctx)
     W.absorb("fcn/chdr", header)
     # ---- stage 1: the matmul families
     L1 = _Lanes(lanes1)
@@ -217,28 +246,34 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
         c, T = home1[i], kids1[i]
         api.matmul_prove(c, T, f.A, f.B, f.trans_a, f.trans_b, out=out[o:o + n])
         T.state_dev(out[o + n:o + n + 32])
+        mark("mm " + f.name, c)
     for i, (f, m, o, n) in enumerate(layL):
         c, T = home1[len(mms) + i], kids1[len(mms) + i]
         api.loss_grad_prove_dev(c, T, f.GZ, f.Zp, f.Y, out=out[o:o + n])
         T.state_dev(out[o + n:o + n + 32])
+        mark("loss " + f.name, c)
     for c in lanes1:
         _fence(c, [wctx])
     for T in kids1:
         W.absorb_state("fcn/join", T)
+    mark("stage 1 joined", wctx)
     # ---- stage 2: one claim per tensor family.  The merges wait for the zkReLU stream's earlier work (the
     # previous window's stage 3): their persistent grids and the zkReLU's persistent rounds (k_relu_ipersist,
     # ~65 SMs co-resident) then never compete for co-residency — measured, the overlapping version stalled
     # for tens to hundreds of milliseconds in some runs.  Stage 1 still overlaps the previous stage 3.
-    if rctx.stream not in [c.stream for c in lanes2]:
-        _fence(rctx, lanes2)
+    for c3 in ctx3:
+        if c3.stream not in [c.stream for c in lanes2]:
+            _fence(c3, lanes2)
+    lay2a, lay2b = lay2[:n2a], lay2[n2a:]
     L2 = _Lanes(lanes2)
-    home2 = [L2.pick(len(t.pad) * t.rows * t.cols) for t, *_ in lay2]
+    home2 = [L2.pick(len(t.pad) * t.rows * t.cols) for t, *_ in lay2a]
     kids2 = []
-    for (t, *_), c in zip(lay2, home2):
+    for (t, *_), c in zip(lay2a, home2):
         W.absorb("fcn/tfam", t.name.encode())
         kids2.append(W.fork("fcn/fork", c))
     _fence(wctx, lanes2)
-    for (t, n, cl, o, L), c, T in zip(lay2, home2, kids2):
+
+    def prove_merge(t, n, cl, o, L, c, T):
         d_pts = gather(c, [r for x in cl for r in x["v"] + x["u"]])
         d_cl = gather(c, [r for x in cl for r in x["c"]])
         maps = [x["map"] for x in cl]
@@ -254,10 +289,15 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
             api.claim_merge_dev(c, T, src[1], n, lr, lc, maps, d_pts, d_cl, source=src[0], X2=src[2], R=f.R,
                                 out=out[o:o + L["total"]])
         T.state_dev(out[o + L["total"]:o + L["total"] + 32])
+        mark("merge " + t.name, c)
+
+    for (t, n, cl, o, L), c, T in zip(lay2a, home2, kids2):
+        prove_merge(t, n, cl, o, L, c, T)
     for c in lanes2:
         _fence(c, [wctx])
     for T in kids2:
         W.absorb_state("fcn/join", T)
+    mark("stage 2 joined", wctx)
     # ---- stage 3: the chained zkReLU families and their aux merges; the top layer's rescale
     pos2 = {t.name: (o, L) for t, n, cl, o, L in lay2}
 
@@ -271,34 +311,56 @@ def enqueue_window_chained(ctx: api.Context, seed: bytes, header: bytes, familie
     kids3 = []
     for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
-        kids3.append(W.fork("fcn/fork", rctx))
-    _fence(wctx, [rctx])
+        kids3.append(W.fork("fcn/fork", rctx if f.kind == "relu" else sctx))
+    L2b = _Lanes(lanes2b)
+    home2b = [L2b.pick(len(t.pad) * t.rows * t.cols) for t, *_ in lay2b]
+    kids2b = []
+    for (t, *_), c in zip(lay2b, home2b):
+        W.absorb("fcn/tfam", t.name.encode())
+        kids2b.append(W.fork("fcn/fork", c))
+    _fence(wctx, ctx3)
+    mark("stage 3 start", rctx)
+    if late_ctxs and not late_after_relu:   # beside stage 3
+        for (t, n, cl, o, L), c, T in zip(lay2b, home2b, kids2b):
+            prove_merge(t, n, cl, o, L, c, T)
     for (f, logD, rn, o, n), T in zip(lay3, kids3):   # the zkReLU first: the window's critical path
         rngs = [r for role in RELU_ROLES for r in point_ranges(f.tensors[role])]
         d_pts = gather(rctx, rngs)
         api.relu_prove_chained_dev(rctx, T, f.Z, f.GA, f.Q, f.R, d_pts, flag, out=out[o:o + rn])
         mo = o + api._a16(rn)
+        mark("relu proved " + f.name, rctx)
+        if late_after_relu and f is relus[-1]:   # the late merges and the rescale beside the aux merge
+            _fence(rctx, ([sctx] if sctx.stream != rctx.stream else []) + (lanes2b if late_ctxs else []))
+            for (t, n_, cl, o_, L), c, T_ in zip(lay2b, home2b, kids2b):
+                prove_merge(t, n_, cl, o_, L, c, T_)
         api.relu_merge_dev(rctx, T, f.Z, f.GA, f.Q, f.R, out[o:o + rn], out=out[mo:o + n])
         T.state_dev(out[o + n:o + n + 32])
+        mark("relu+merge " + f.name, rctx)
     for (f, logD, logB, rl, L, o, n), T in zip(layR, kids3[len(relus):]):
-        d_pts = gather(rctx, point_ranges(f.tensors["Z"]) + point_ranges(f.tensors["Zp"]))
-        api.rescale_prove_dev(rctx, T, f.Z, f.Q, f.R, d_pts, flag, out=out[o:o + rl])
+        d_pts = gather(sctx, point_ranges(f.tensors["Z"]) + point_ranges(f.tensors["Zp"]))
+        api.rescale_prove_dev(sctx, T, f.Z, f.Q, f.R, d_pts, flag, out=out[o:o + rl])
         # the two aux claims -> one (claim merge, D25, on the bits of Z: one slice [D][B])
         po = o + api._a16(12 + 64 + 2 * (12 + 32 + 96 * (logD + logB) + 64))
         pla = o + 76 + (12 + 32 + 96 * (logD + logB) + 64) - 32          # A's second final: aux~(r_A)
         plb = o + 76 + 2 * (12 + 32 + 96 * (logD + logB) + 64) - 64      # B's first final: aux~(r_B)
-        d_apts = gather(rctx, [(po, logD + logB), (po + 32 * (logD + logB), logD + logB)])
-        d_acl = gather(rctx, [(pla, 1), (plb, 1)])
+        d_apts = gather(sctx, [(po, logD + logB), (po + 32 * (logD + logB), logD + logB)])
+        d_acl = gather(sctx, [(pla, 1), (plb, 1)])
         mo = o + api._a16(rl)
-        api.claim_merge_dev(rctx, T, f.Z, 0, logD, logB, [[0], [0]], d_apts, d_acl, source="bits", R=f.Q + f.R,
+        api.claim_merge_dev(sctx, T, f.Z, 0, logD, logB, [[0], [0]], d_apts, d_acl, source="bits", R=f.Q + f.R,
                             out=out[mo:mo + L["total"]])
         T.state_dev(out[o + n:o + n + 32])
-    _fence(rctx, [wctx])
-    for T in kids3:
+        mark("rescale+merge " + f.name, sctx)
+    if not late_ctxs:   # after stage 3 on the zkReLU's stream
+        for (t, n, cl, o, L), c, T in zip(lay2b, home2b, kids2b):
+            prove_merge(t, n, cl, o, L, c, T)
+    for c in ctx3:
+        _fence(c, [wctx])
+    for T in kids3 + kids2b:
         W.absorb_state("fcn/join", T)
     W.state_dev(out[off:off + 32])
+    mark("end", wctx)
     return dict(out=out, flag=flag, lay1=lay1, layL=layL, lay2=lay2, lay3=lay3, layR=layR, end=off, keep=keep,
-                claims=claims, transcripts=kids1 + kids2 + kids3 + [W])
+                claims=claims, transcripts=kids1 + kids2 + kids3 + kids2b + [W])
 
 
 def collect_window_chained(h: dict) -> dict:
@@ -338,6 +400,9 @@ def collect_window_chained(h: dict) -> dict:
 
 def prove_window_chained(ctx: api.Context, seed: bytes, header: bytes, families: list, tensors: list,
                          relu_ctx: api.Context | None = None, mm_ctxs: list | None = None,
-                         wctx: api.Context | None = None, merge_ctxs: list | None = None) -> dict:
+                         wctx: api.Context | None = None, merge_ctxs: list | None = None,
+                         rescale_ctx: api.Context | None = None, late_ctxs: list | None = None,
+                         late_after_relu: bool = False) -> dict:
     return collect_window_chained(enqueue_window_chained(ctx, seed, header, families, tensors, relu_ctx, mm_ctxs, wctx,
-                                                         merge_ctxs))
+                                                         merge_ctxs, rescale_ctx=rescale_ctx, late_ctxs=late_ctxs,
+                                                         late_after_relu=late_after_relu))

@@ -302,23 +302,37 @@ def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: l
             merged.append(t)
     if set(res["merges"]) != {t.name for t in merged}:
         raise Rejected("claim merges do not match the window plan", -4)
+    # D25 order: the merges stage 3 is bound to, joined before stage 3; the other merges forked after stage
+    # 3's families (they prove beside it) and joined after them
+    bound = {f.tensors[k] for f in relus for k in RELU_ROLES} | {f.tensors[k] for f in rescales for k in ("Z", "Zp")}
+    merged_a = [t for t in merged if t.name in bound]
+    merged_b = [t for t in merged if t.name not in bound]
+
+    def check_merges(ts, ks):
+        for t, T in zip(ts, ks):
+            n = len(pad_of(t)).bit_length() - 1
+            d = (t.rows * t.cols).bit_length() - 1
+            mr = res["merges"][t.name]
+            opened[t.name] = verify_claim_merge(T, n, d, claims[t.name], mr["proof"])
+            if T.state() != mr["state"]:
+                raise Rejected(f"claim merge {t.name} transcript state", -3)
+
     kids2 = []
-    for t in merged:
+    for t in merged_a:
         W.absorb("fcn/tfam", t.name.encode())
         kids2.append(W.fork("fcn/fork"))
-    for t, T in zip(merged, kids2):
-        n = len(pad_of(t)).bit_length() - 1
-        d = (t.rows * t.cols).bit_length() - 1
-        mr = res["merges"][t.name]
-        opened[t.name] = verify_claim_merge(T, n, d, claims[t.name], mr["proof"])
-        if T.state() != mr["state"]:
-            raise Rejected(f"claim merge {t.name} transcript state", -3)
+    check_merges(merged_a, kids2)
     for T in kids2:
         W.absorb("fcn/join", T.state())
     kids3 = []
     for f in relus + rescales:
         W.absorb("fcn/fam", f.name.encode())
         kids3.append(W.fork("fcn/fork"))
+    kids2b = []
+    for t in merged_b:
+        W.absorb("fcn/tfam", t.name.encode())
+        kids2b.append(W.fork("fcn/fork"))
+    check_merges(merged_b, kids2b)
     for f, T in zip(rescales, kids3[len(relus):]):
         r = res["rescale"][f.name]
         names = [f.tensors["Z"], f.tensors["Zp"]]
@@ -352,7 +366,7 @@ def verify_window_chained(seed: bytes, header: bytes, families: list, tensors: l
             del opened[nm]
         logB = max(0, (f.Q + f.R - 1).bit_length())
         opened["aux:" + f.name] = (mg["point"][:logB] + v["point"][logB:] + mg["point"][logB:], mg["claim"])
-    for T in kids3:
+    for T in kids3 + kids2b:
         W.absorb("fcn/join", T.state())
     if W.state() != res["window_state"]:
         raise Rejected("window transcript state", -3)

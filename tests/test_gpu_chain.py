@@ -63,8 +63,14 @@ def _run(ctx, O, shape, seed_name, streams, x_bits=11, w_bits=12, y_bits=10, ful
     dfams, dts = chain.upload_plan(fams, tensors, top=top)
     relu_ctx = api.Context(0, torch.cuda.Stream()) if streams else None
     mm = [api.Context(0, torch.cuda.Stream()) for _ in range(streams)]
+    # with streams: the bench's stage-3 layout (the rescale and the late claim merges beside the zkReLU, on
+    # budgeted streams)
+    rs = api.Context(0, torch.cuda.Stream()) if streams else None
+    late = [api.Context(0, torch.cuda.Stream()) for _ in range(2 * streams)]
+    for c in ([rs] if rs else []) + late:
+        c.set_sm_budget(12)
     g = chain.prove_window_chained(ctx, fs_seed(seed_name), fcn.fcn_header(shape), dfams, dts, relu_ctx=relu_ctx,
-                                   mm_ctxs=mm)
+                                   mm_ctxs=mm, rescale_ctx=rs, late_ctxs=late or None)
     opened = verify.verify_window_chained(fs_seed(seed_name), fcn.fcn_header(shape), fams + top, tensors, g)
     return fams, top, tensors, g, opened
 
@@ -144,27 +150,41 @@ def test_chained_window_full_size(ctx, O, cfg):
         claims[ref.tensor].append(dict(map=list(ref.map), u=list(u), v=list(v), c=c))
     merged = [t for t in tensors if claims[t.name] and not drivers._is_whole(t, claims[t.name])]
     assert sorted(t.name for t in merged) == sorted(g["merges"])
-    mk = []
-    for t in merged:
-        W.absorb("fcn/tfam", t.name.encode())
-        mk.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    # D25 order: the merges stage 3 is bound to, joined; stage 3's forks; the other merges' forks
+    st3 = [f for f in fams if not hasattr(f, "A")] + [resc]
+    bound = {f.tensors[k] for f in st3 if f is not resc for k in ("Z", "A", "GA", "GZ")} | \
+        {resc.tensors["Z"], resc.tensors["Zp"]}
+    merged_a = [t for t in merged if t.name in bound]
+    merged_b = [t for t in merged if t.name not in bound]
     one = {}
     for t in tensors:
         if claims[t.name] and t not in merged:
             one[t.name] = (claims[t.name][0]["v"] + claims[t.name][0]["u"], claims[t.name][0]["c"])
-    for t, T in zip(merged, mk):
-        r = Ol.claim_merge_prove(T, drivers._tensor_values(t, fams + top), claims[t.name])
-        a = g["merges"][t.name]
-        assert a["A"]["msgs"] == r["A"]["msgs"] and a["B"]["msgs"] == r["B"]["msgs"], t.name
-        assert a["point"] == r["point"] and a["claim"] == r["claim"] and a["state"] == T.state(), t.name
-        one[t.name] = (r["point"], r["claim"])
+
+    def check_merges(ts, ks):
+        for t, T in zip(ts, ks):
+            r = Ol.claim_merge_prove(T, drivers._tensor_values(t, fams + top), claims[t.name])
+            a = g["merges"][t.name]
+            assert a["A"]["msgs"] == r["A"]["msgs"] and a["B"]["msgs"] == r["B"]["msgs"], t.name
+            assert a["point"] == r["point"] and a["claim"] == r["claim"] and a["state"] == T.state(), t.name
+            one[t.name] = (r["point"], r["claim"])
+
+    mk = []
+    for t in merged_a:
+        W.absorb("fcn/tfam", t.name.encode())
+        mk.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    check_merges(merged_a, mk)
     for T in mk:
         W.absorb("fcn/join", T.state())
-    st3 = [f for f in fams if not hasattr(f, "A")] + [resc]
     forks3 = []
     for f in st3:                      # D25 stage 3: every fork first, then the proofs, then the joins
         W.absorb("fcn/fam", f.name.encode())
         forks3.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    mkb = []
+    for t in merged_b:
+        W.absorb("fcn/tfam", t.name.encode())
+        mkb.append(Ol.Transcript(W.challenges("fcn/fork", 1)[0].to_bytes(32, "little")))
+    check_merges(merged_b, mkb)
     for f, T in zip(st3, forks3):
         if f is resc:
             r = Ol.rescale_prove(T, f.Z, f.Q, f.R, [one[f.tensors["Z"]][0], one[f.tensors["Zp"]][0]])
@@ -189,7 +209,7 @@ def test_chained_window_full_size(ctx, O, cfg):
         assert Ol.sumcheck_verify(T, len(gr["merge"]["r"]), 0, 2, [], gr["merge"]["claim"], gr["merge"]["msgs"],
                                   gr["merge"]["finals"]) == 0
         assert gr["state"] == T.state()
-    for T in forks3:
+    for T in forks3 + mkb:
         W.absorb("fcn/join", T.state())
     assert g["window_state"] == W.state()
     for t in tensors:
