@@ -62,6 +62,12 @@ zk_status zk_ctx_synchronize(zk_ctx* ctx);
  * with budgets that add up to the SM count prove independent statements side by side instead of
  * each latency-bound statement spreading thinly over the whole GPU.  Never changes any output. */
 zk_status zk_ctx_set_sm_budget(zk_ctx* ctx, uint32_t sms);
+/* Allow (1, the default) or forbid (0) the context's persistent spin-waiting kernels (the one-launch
+ * small-statement sumcheck and its continuation): with 0 every sumcheck round is its own launch, so work on
+ * this context never holds SMs while waiting for CTAs that other streams keep from being scheduled (the
+ * co-residency a cooperative grid assumes).  For work proved beside another stream's persistent kernels.
+ * Never changes any output. */
+zk_status zk_ctx_set_persistent(zk_ctx* ctx, int allow);
 /* Per-launch profiling: while enabled, every kernel launch of the context is bracketed by two
  * CUDA events on the context stream.  zk_ctx_profile_read synchronises, writes one line per kernel
  * "name<TAB>launches<TAB>total_ms\n" (NUL-terminated, cap bytes max) and clears the records. */

@@ -65,6 +65,7 @@ def lib():
         "zk_ctx_profile_read": ([vp, c.c_char_p, u64], i32),
         "zk_ctx_profile_filter": ([vp, c.c_char_p], i32),
         "zk_ctx_set_sm_budget": ([vp, u32], i32),
+        "zk_ctx_set_persistent": ([vp, i32], i32),
         "zk_reindex_prove": ([vp, vp, vp, u32, u32, u32, vp, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_relu_merge": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, vp, c.POINTER(u64), vp, vp], i32),
         "zk_relu_merge_dev": ([vp, vp, vp, vp, u32, u32, u32, vp, vp, c.POINTER(u64)], i32),

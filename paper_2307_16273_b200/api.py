@@ -60,6 +60,10 @@ class Context:
     def synchronize(self):
         self.check(lib().zk_ctx_synchronize(self.h))
 
+    def set_persistent(self, allow: bool):
+        """zk_ctx_set_persistent: allow / forbid this context's persistent (spin-waiting) sumcheck kernels."""
+        self.check(lib().zk_ctx_set_persistent(self.h, 1 if allow else 0))
+
     def set_sm_budget(self, sms: int):
         """zk_ctx_set_sm_budget: cap the grid of this context's persistent kernels (0 = every SM)."""
         self.check(lib().zk_ctx_set_sm_budget(self.h, int(sms)))

@@ -92,6 +92,12 @@ zk_status zk_ctx_set_sm_budget(zk_ctx* ctx, uint32_t sms) {
     ZK_API_END(ctx)
 }
 
+zk_status zk_ctx_set_persistent(zk_ctx* ctx, int allow) {
+    ZK_API_BEGIN(ctx)
+    ctx->no_persist = !allow;
+    ZK_API_END(ctx)
+}
+
 zk_status zk_ctx_profile(zk_ctx* ctx, int enable) {
     ZK_API_BEGIN(ctx)
     ctx->prof = enable != 0;

@@ -17,6 +17,7 @@ struct zk_ctx {
     cudaStream_t stream = nullptr;
     int num_sms = 148;
     int sm_budget = 0;         // cap on the grid of persistent kernels (0 = every SM), zk_ctx_set_sm_budget
+    bool no_persist = false;   // zk_ctx_set_persistent(ctx, 0): per-round launches only
     void* nccl_comm = nullptr; // ncclComm_t owned by the context (zk_ctx_attach_nccl), sharded mode
     int nccl_rank = 0, nccl_world = 1;
     uint64_t launches = 0;

@@ -397,6 +397,8 @@ struct JRoundArgs {
     fr_t* byte_tab;        // ceil(B/8) x 256 entries
     fr_t* kappa;           // [0] kZ [1] kA [2] kGA [3] kGZ [4] kb [5] r' [6] claim after the j-phase
     fr_t* sigma;           // (nullable) the five per-term sums entering the i-phase (Z, A, GA, GZ, b)
+    const fr_t* r0cells;   // (nullable, with sigma) lin6 of relu_bitsums_gram: [s][par][q][j]
+    fr_t* r0ext;           // the first i-round's linear totals from r0cells (6: Z, A(0), A(inf), GA, GZ(0), GZ(inf))
 };
 
 __device__ __forceinline__ int tri_index(int j1, int j2, int B) {   // j1 <= j2, row-major upper triangle
@@ -593,6 +595,36 @@ __global__ void __launch_bounds__(256) k_relu_jrounds(JRoundArgs a) {
             fr_store(&a.sigma[tid], fr_mul_ni(k, acc));
         }
         if (tid == 0) fr_store(&a.sigma[4], fr_add(fr_mul_ni(EB[0], gacc[0]), fr_mul_ni(fr_mul_ni(rp, EB[0]), gacc[1])));
+        if (a.r0cells) {
+            // the first i-round's linear terms from the parity-split cells (gram.cu), with a(i) = sum_j e_j bit_j:
+            //   T_a(0)   = kappa_a sum_j e_j Lin[s][0][0][j]                               (slots 0, 3)
+            //   T_c(0)   = kappa_c sum_j e_j Lin[s][0][1][j]                               (slots 1, 4)
+            //   T_c(inf) = kappa_c sum_j e_j (Lin[s][1][1] - Lin[s][1][2] - Lin[s][0][2] + Lin[s][0][1])[j]
+            // (sum_b E'_c (a(2b+1) - a(2b)) (o(2b+1) - o(2b)) expanded), kappa as the i-round's HI' tables carry
+            fr_t (*r0p)[32] = CQ + 4;   // rows 4-9 of the free CQ
+            __syncthreads();
+            if (tid < 6 * B) {
+                const int sl = tid / B, j = tid % B, sw = sl / 3, k = sl % 3;
+                const fr_t* L = a.r0cells + 6 * B * sw;
+#define R0L(par, q) fr_load(&L[((par) * 3 + (q)) * B + j])
+                fr_t v;
+                if (k == 0) v = R0L(0, 0);
+                else if (k == 1) v = R0L(0, 1);
+                else v = fr_add(fr_sub(fr_sub(R0L(1, 1), R0L(1, 2)), R0L(0, 2)), R0L(0, 1));
+#undef R0L
+                r0p[sl][j] = fr_mul_ni(ej[j], v);
+            }
+            __syncthreads();
+            if (tid < 6) {
+                const int sw = tid / 3, k = tid % 3;
+                fr_t acc = fr_zero();
+                for (int j = 0; j < B; j++) acc = fr_add(acc, r0p[tid][j]);
+                const fr_t s = S[0], sp = SP[0];
+                const fr_t kap = sw == 0 ? (k == 0 ? fr_mul_ni(r2, s) : fr_mul_ni(r, sp))
+                                         : (k == 0 ? fr_mul_ni(fr_mul_ni(rp, r2), s) : fr_mul_ni(fr_mul_ni(rp, r), sp));
+                fr_store(&a.r0ext[tid], fr_mul_ni(kap, acc));
+            }
+        }
     }
     const int nb = (B + 7) / 8;
     for (int e = tid; e < nb * 256; e += blockDim.x) {
@@ -649,6 +681,9 @@ struct IRoundArgs {
     // MODE bit 2 (derived X = 1): the per-term running sums (read and updated by the finalizer) and u_x[t]^-1
     fr_t* sigma;
     const fr_t* uinv;
+    // MODE bit 3 (round 0 with the linear terms from the bit-sum cells): k_relu_jrounds' six totals, added by the
+    // finalizer to slots 0-5
+    const fr_t* r0ext;
 };
 
 // Finalizer of an i-round (last block, after the grid reduction), in two parts so that the persistent
@@ -902,7 +937,7 @@ __device__ __forceinline__ fr_t byte_sum(const fr_t* tb, uint32_t w, const IPtrs
 
 // Accumulate this thread's pairs j = j0, j0 + js, ... < P_blk of HI block h into T[0..7] =
 // (T_a(0), T_a(1), T_c(0), T_c(1), T_c(inf), T_b(0), T_b(1), T_b(inf)) of its side.
-template <bool FOLD, int SRC = 0, bool DER = false>
+template <bool FOLD, int SRC = 0, bool DER = false, bool CELLS = false>
 __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint32_t h, uint32_t pb, uint64_t j0,
                                              uint64_t js, const int side, fr_t (&T)[8]) {
     const fr_t one = fr_one();
@@ -976,9 +1011,25 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             o0 = !fr_is_zero(fr_load_cg(q.srcO + 2 * b));
             o1 = !fr_is_zero(fr_load_cg(q.srcO + 2 * b + 1));
         }
+        const fr_t eB = fr_add(fr_load_l2(&q.loB[2 * j]), fr_load_l2(&q.loB[2 * j + 1]));
+        if constexpr (CELLS) {   // the linear terms come from the bit-sum cells: only the binary check here
+            if (h == 0) {   // the next LO level: side 0 writes Z, A, b; side 1 writes GA, GZ
+                fr_store(&q.nxA[j], fr_add(fr_load_l2(&q.loA[2 * j]), fr_load_l2(&q.loA[2 * j + 1])));
+                fr_store(&q.nxC[j], fr_add(fr_load_l2(&q.loC[2 * j]), fr_load_l2(&q.loC[2 * j + 1])));
+                if (q.nxB) fr_store(&q.nxB[j], eB);
+            }
+            const fr_t dA = fr_sub(a1, a0);
+            const fr_t zB0 = fr_mul_ni(eB, a0), zD = fr_mul_ni(eB, dA);
+            T[3] = fr_add(T[3], fr_mul_ni(zB0, fr_sub(a0, one)));
+            T[4] = fr_add(T[4], fr_mul_ni(zD, dA));
+            (void)o0;
+            (void)o1;
+            (void)om0;
+            (void)om1;
+            continue;
+        }
         const fr_t eA = fr_add(fr_load_l2(&q.loA[2 * j]), fr_load_l2(&q.loA[2 * j + 1]));
         const fr_t eC = fr_add(fr_load_l2(&q.loC[2 * j]), fr_load_l2(&q.loC[2 * j + 1]));
-        const fr_t eB = fr_add(fr_load_l2(&q.loB[2 * j]), fr_load_l2(&q.loB[2 * j + 1]));
         if (h == 0) {   // the next LO level: side 0 writes Z, A, b; side 1 writes GA, GZ
             fr_store(&q.nxA[j], eA);
             fr_store(&q.nxC[j], eC);
@@ -1219,7 +1270,9 @@ __global__ void k_relu_uinv(UPts P, uint32_t t1, fr_t* out) {
 }
 
 // MODE: bit 0 = FOLD, bit 1 = SRC (rounds 0 / 1 from the int32 words through byte tables in shared memory),
-// bit 2 = DER (the X = 1 totals derived from the per-term sums)
+// bit 2 = DER (the X = 1 totals derived from the per-term sums), bit 3 = CELLS (round 0 only, with DER: the
+// linear terms T_a(0), T_c(0), T_c(inf) from the bit-sum cells, k_relu_jrounds' r0ext; the pairs sum the binary
+// check only)
 template <int MODE>
 // the factored i-round's CTA shape (threads, CTAs per SM): registers per thread = 64K / (threads x CTAs)
 #ifndef ZKDL_IR_LB_T
@@ -1232,6 +1285,8 @@ __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IR
     constexpr bool FOLD = MODE & 1;
     constexpr int SRC = (MODE >> 1) & 1;
     constexpr bool DER = MODE & 4;
+    constexpr bool CELLS = MODE & 8;
+    static_assert(!CELLS || (DER && !FOLD), "CELLS: the first (derived) round only");
     constexpr int NV = DER ? IR_NV_DER : IR_NV;
     const int side = threadIdx.x & 1;
     const uint32_t pb = a.lo_cnt - 1;   // log2 of the pairs per HI block
@@ -1274,7 +1329,7 @@ __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IR
 #pragma unroll
     for (int k = 0; k < 8; k++) T[k] = fr_zero();
     const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
-    iround_pairs<FOLD, SRC, DER>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+    iround_pairs<FOLD, SRC, DER, CELLS>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
     fr_t v[16];
     if constexpr (DER)
         iround_scale_scatter_der(T, a.hi, h, side, j0 < (1ull << pb), v);
@@ -1304,6 +1359,9 @@ __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IR
             for (int k = 0; k < NV; k++) w[k] = fr_add(w[k], fr_load_l2(&a.partials[bb * NV + k]));
         block_transpose_sum16(w, sm);
         if (threadIdx.x < NV) tot[threadIdx.x] = w[0];
+        if constexpr (CELLS) {
+            if (threadIdx.x < 6) tot[threadIdx.x] = fr_add(tot[threadIdx.x], fr_load_l2(&a.r0ext[threadIdx.x]));
+        }
     }
     if (threadIdx.x == 0) *a.ticket = 0;
     __syncthreads();
@@ -1591,8 +1649,10 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     const uint32_t ncell = 4 * B + B * (B + 1);
     fr_t* cell_tot = s.alloc<fr_t>(ncell);
     static const bool no_gram = getenv("ZKDL_NO_GRAM") != nullptr;   // A/B switch for the CUDA-core path
-    if (relu_gram_supported(logD, B) && !no_gram) {
-        relu_bitsums_gram(ctx, Z, GA, logD, qr_mask, QR - 1, B, u_i, cell_tot, s);
+    const bool gram = relu_gram_supported(logD, B) && !no_gram;
+    fr_t* lin6 = gram ? s.alloc<fr_t>(12ull * B) : nullptr;
+    if (gram) {
+        relu_bitsums_gram(ctx, Z, GA, logD, qr_mask, QR - 1, B, u_i, cell_tot, lin6, s);
     } else {
     const uint32_t lo_bits = logD < 12 ? logD : 12, hi_bits = logD - lo_bits;
     BitsumArgs ba;
@@ -1658,6 +1718,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     fr_t* kappa = s.alloc<fr_t>(8);
     fr_t* r_all = s.alloc<fr_t>(m);
     JRoundArgs ja;
+    memset(&ja, 0, sizeof ja);
     ja.cells = cell_tot;
     ja.B = B;
     ja.logB = logB;
@@ -1677,6 +1738,10 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     const bool derive = !derive_off && !unfactored_;
     fr_t* sigma = derive ? s.alloc<fr_t>(5) : nullptr;
     ja.sigma = sigma;
+    // the first i-round's linear terms from the bit-sum cells (gram.cu lin6; ZKDL_IR_CELLS=0: from the pairs);
+    // needs the word-sourced derived round 0 (decided below: t0 >= 2, the factored kernel)
+    static const bool cells_off = getenv("ZKDL_IR_CELLS") && atoi(getenv("ZKDL_IR_CELLS")) == 0;
+    fr_t* r0ext = nullptr;
     fr_t* uinv = nullptr;
     if (derive) {   // u_x[t]^-1 for every i-round (Fermat, ~0.2 ms) on the aux stream, behind the bit sums
         uinv = s.alloc<fr_t>(5ull * logD);
@@ -1688,6 +1753,24 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         k_relu_uinv<<<(5 * logD + 63) / 64, 64, 0, aux>>>(P, logD, uinv);
         after_launch(ctx, "k_relu_uinv");
         ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], aux));
+    }
+    {   // t0 >= 2 and the factored kernel (the word-sourced rounds 0 / 1), as decided below
+        const uint32_t hb_ = logD < 5 ? logD : 5, H_ = logD - hb_;
+        const int plog_ = getenv("ZKDL_IPERSIST_LOG") ? atoi(getenv("ZKDL_IPERSIST_LOG")) : 16;
+        const bool unf_ = getenv("ZKDL_IROUND_V") && atoi(getenv("ZKDL_IROUND_V")) == 0;
+        const bool words_off_ = getenv("ZKDL_RELU_WORDS") && atoi(getenv("ZKDL_RELU_WORDS")) == 0;
+        uint32_t t0_ = H_;
+        if (!unf_ && ((ctx->num_sms - 1) >> hb_) >= 1 && plog_ >= 0)
+            for (uint32_t t = 1; t < H_; t++)
+                if ((D >> (t + 1)) <= (1ull << plog_)) {
+                    t0_ = t;
+                    break;
+                }
+        if (gram && derive && !cells_off && !unf_ && t0_ >= 2 && !words_off_) {
+            r0ext = s.alloc<fr_t>(6);
+            ja.r0cells = lin6;
+            ja.r0ext = r0ext;
+        }
     }
     ZK_LAUNCH(ctx, k_relu_jrounds, 1, 256, 0, ja);
 
@@ -1752,7 +1835,9 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
         ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
         ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
+        ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
     }
+    ZK_REQUIRE(!r0ext || words, ZK_ERR_INTERNAL, "cell-sourced round 0 without the word-sourced rounds");
     if (derive) ZK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // u^-1 before the first i-round
     for (uint32_t t = 0; t < t0; t++) {
         IRoundArgs a;
@@ -1783,6 +1868,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         a.point_out = out.d_point + 32ull * (logB + t);
         a.sigma = sigma;
         a.uinv = derive ? uinv + 5ull * t : nullptr;
+        a.r0ext = r0ext;
         if (unfactored) {
             const unsigned int grid = grid_for(ctx, 2 * a.n_pairs, 256, 2);   // two threads per pair
             if (fold)
@@ -1811,6 +1897,8 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
                     ZK_LAUNCH(ctx, k_relu_iround_f<7>, grid, ithreads, tb_smem, a);
                 else if (fold)
                     ZK_LAUNCH(ctx, k_relu_iround_f<3>, grid, ithreads, tb_smem, a);
+                else if (derive && r0ext)
+                    ZK_LAUNCH(ctx, k_relu_iround_f<14>, grid, ithreads, tb_smem / 2, a);
                 else if (derive)
                     ZK_LAUNCH(ctx, k_relu_iround_f<6>, grid, ithreads, tb_smem / 2, a);
                 else

@@ -1245,7 +1245,7 @@ __global__ void k_fr_inv_batch(const fr_t* in, uint32_t n, fr_t* out) {
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
     const uint32_t m = S.m, n_eq = S.n_eq, K = S.K;
     ZK_REQUIRE(m >= 1 && m <= 40 && n_eq <= m && K >= 1 && K <= 3, ZK_ERR_ARG, "sumcheck: bad m / n_eq / K");
-    if (m <= SC_ALL_MAX_LOG && !getenv("ZKDL_NO_PERSISTENT")) {
+    if (m <= SC_ALL_MAX_LOG && !getenv("ZKDL_NO_PERSISTENT") && !ctx->no_persist) {
         for (uint32_t k = 0; k < K; k++)
             if (S.i32[k]) embed_i32_dev(ctx, S.i32[k], 1ull << m, const_cast<fr_t*>(S.tables[k]));
         sumcheck_prove_small(ctx, tr, S, s);
@@ -1290,7 +1290,7 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
 constexpr uint32_t SC_TAIL_LOG = 16;
 
 void ScEngine::run_to_end() {
-    const bool persistent_ok = !getenv("ZKDL_NO_PERSISTENT") && !zero;
+    const bool persistent_ok = !getenv("ZKDL_NO_PERSISTENT") && !ctx->no_persist && !zero;
     while (t < t0 + L) {
         const uint32_t tl = t - t0;
         if (tl >= 1 && persistent_ok && L - tl <= SC_TAIL_LOG) {

@@ -69,6 +69,7 @@ def _run(ctx, O, shape, seed_name, streams, x_bits=11, w_bits=12, y_bits=10, ful
     late = [api.Context(0, torch.cuda.Stream()) for _ in range(2 * streams)]
     for c in ([rs] if rs else []) + late:
         c.set_sm_budget(12)
+        c.set_persistent(False)
     g = chain.prove_window_chained(ctx, fs_seed(seed_name), fcn.fcn_header(shape), dfams, dts, relu_ctx=relu_ctx,
                                    mm_ctxs=mm, rescale_ctx=rs, late_ctxs=late or None)
     opened = verify.verify_window_chained(fs_seed(seed_name), fcn.fcn_header(shape), fams + top, tensors, g)

@@ -7,6 +7,8 @@ alternative path a switch selects is run in a subprocess and compared with the o
     ZKDL_RELU_WORDS=0    zkReLU i-rounds 0/1 from materialised tables instead of the words
     ZKDL_IR_DERIVE=0     zkReLU i-rounds with every X = 1 total summed over the pairs (not derived from the
                          per-term sums)
+    ZKDL_IR_CELLS=0      the first zkReLU i-round's linear terms summed over the pairs (not from the parity-split
+                         bit-sum cells of the Gram kernel)
     ZKDL_MLE4_FUSED=0    the four zkReLU claims through four row-dot launches
     ZKDL_COLSUM_TC=0     column sums on the CUDA cores instead of the tensor cores (TMA + MN-major int8 MMAs)
     ZKDL_COLSUM_ROWS=0   wide CUDA-core column sums through the column-strip kernel
@@ -85,7 +87,7 @@ def test_c5_paths(oracle_lib, env):
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"ZKDL_RELU_WORDS": "0"}, {"ZKDL_MLE4_FUSED": "0"},
                                  {"ZKDL_RELU_WORDS": "0", "ZKDL_MLE4_FUSED": "0"}, {"ZKDL_IR_DERIVE": "0"},
-                                 {"ZKDL_IR_DERIVE": "0", "ZKDL_RELU_WORDS": "0"}])
+                                 {"ZKDL_IR_DERIVE": "0", "ZKDL_RELU_WORDS": "0"}, {"ZKDL_IR_CELLS": "0"}])
 def test_relu_paths(oracle_lib, env):
     from oracle import drivers
     o = drivers.c2_prove()
