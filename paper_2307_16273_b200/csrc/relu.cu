@@ -905,6 +905,12 @@ struct IPtrs {   // one side's view of a round (L2 loads: the persistent kernel 
 #define ZKDL_IR_PREFETCH 0
 #endif
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// ZKDL_IR_PF=1 (A/B build): the per-round kernel's fold rounds read through L1 and prefetch the next pair's
+// inputs into L1 (the persistent kernel keeps its L2 reads: its tables are written inside the launch)
+#ifndef ZKDL_IR_PF
+#define ZKDL_IR_PF 0
+#endif
 
 // the i-round's three-product groups (ZKDL_IR_MULW): 3 = one three-product body (three interleaved
 // chains, ~21 KB of code), 1 = three calls of the single-product body (~7 KB: inside the L0 I-cache)
@@ -937,7 +943,7 @@ __device__ __forceinline__ fr_t byte_sum(const fr_t* tb, uint32_t w, const IPtrs
 
 // Accumulate this thread's pairs j = j0, j0 + js, ... < P_blk of HI block h into T[0..7] =
 // (T_a(0), T_a(1), T_c(0), T_c(1), T_c(inf), T_b(0), T_b(1), T_b(inf)) of its side.
-template <bool FOLD, int SRC = 0, bool DER = false, bool CELLS = false>
+template <bool FOLD, int SRC = 0, bool DER = false, bool CELLS = false, bool PF = false>
 __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint32_t h, uint32_t pb, uint64_t j0,
                                              uint64_t js, const int side, fr_t (&T)[8]) {
     const fr_t one = fr_one();
@@ -991,10 +997,23 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             o1 = !(((uint32_t)z2.y >> q.sig_bit) & 1);
         } else if (FOLD) {
             const fr_t* s = q.srcA + 4 * b;
-            const fr_t y0 = fr_load_l2(s), y1 = fr_load_l2(s + 1), y2 = fr_load_l2(s + 2), y3 = fr_load_l2(s + 3);
             // oms fold shared by the pair's two lanes: side s folds entry s and stores it
             const fr_t* so = q.srcO + 4 * b + 2 * side;
-            const fr_t z0 = fr_load_l2(so), z1 = fr_load_l2(so + 1);
+            fr_t y0, y1, y2, y3, z0, z1;
+            if constexpr (PF) {
+                if (j + js < P_blk) {   // the next pair's inputs into L1
+                    prefetch_l1(s + 4 * js);
+                    prefetch_l1(so + 4 * js);
+                    prefetch_l1(&q.loA[2 * (j + js)]);
+                    prefetch_l1(&q.loC[2 * (j + js)]);
+                    prefetch_l1(&q.loB[2 * (j + js)]);
+                }
+                y0 = fr_load(s); y1 = fr_load(s + 1); y2 = fr_load(s + 2); y3 = fr_load(s + 3);
+                z0 = fr_load(so); z1 = fr_load(so + 1);
+            } else {
+                y0 = fr_load_l2(s); y1 = fr_load_l2(s + 1); y2 = fr_load_l2(s + 2); y3 = fr_load_l2(s + 3);
+                z0 = fr_load_l2(so); z1 = fr_load_l2(so + 1);
+            }
             const fr3_t f = ir_mul3(r, fr_sub(y1, y0), r, fr_sub(y3, y2), r, fr_sub(z1, z0));
             a0 = fr_add(y0, f.x);
             a1 = fr_add(y2, f.y);
@@ -1011,7 +1030,8 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             o0 = !fr_is_zero(fr_load_cg(q.srcO + 2 * b));
             o1 = !fr_is_zero(fr_load_cg(q.srcO + 2 * b + 1));
         }
-        const fr_t eB = fr_add(fr_load_l2(&q.loB[2 * j]), fr_load_l2(&q.loB[2 * j + 1]));
+        const fr_t eB = PF ? fr_add(fr_load(&q.loB[2 * j]), fr_load(&q.loB[2 * j + 1]))
+                           : fr_add(fr_load_l2(&q.loB[2 * j]), fr_load_l2(&q.loB[2 * j + 1]));
         if constexpr (CELLS) {   // the linear terms come from the bit-sum cells: only the binary check here
             if (h == 0) {   // the next LO level: side 0 writes Z, A, b; side 1 writes GA, GZ
                 fr_store(&q.nxA[j], fr_add(fr_load_l2(&q.loA[2 * j]), fr_load_l2(&q.loA[2 * j + 1])));
@@ -1028,8 +1048,10 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             (void)om1;
             continue;
         }
-        const fr_t eA = fr_add(fr_load_l2(&q.loA[2 * j]), fr_load_l2(&q.loA[2 * j + 1]));
-        const fr_t eC = fr_add(fr_load_l2(&q.loC[2 * j]), fr_load_l2(&q.loC[2 * j + 1]));
+        const fr_t eA = PF ? fr_add(fr_load(&q.loA[2 * j]), fr_load(&q.loA[2 * j + 1]))
+                           : fr_add(fr_load_l2(&q.loA[2 * j]), fr_load_l2(&q.loA[2 * j + 1]));
+        const fr_t eC = PF ? fr_add(fr_load(&q.loC[2 * j]), fr_load(&q.loC[2 * j + 1]))
+                           : fr_add(fr_load_l2(&q.loC[2 * j]), fr_load_l2(&q.loC[2 * j + 1]));
         if (h == 0) {   // the next LO level: side 0 writes Z, A, b; side 1 writes GA, GZ
             fr_store(&q.nxA[j], eA);
             fr_store(&q.nxC[j], eC);
@@ -1329,7 +1351,8 @@ __global__ void __launch_bounds__(ZKDL_IR_LB_T, ZKDL_IR_LB_B) k_relu_iround_f(IR
 #pragma unroll
     for (int k = 0; k < 8; k++) T[k] = fr_zero();
     const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
-    iround_pairs<FOLD, SRC, DER, CELLS>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+    iround_pairs<FOLD, SRC, DER, CELLS, ZKDL_IR_PF != 0 && FOLD && SRC == 0>(q, r, h, pb, j0,
+                                                                            (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
     fr_t v[16];
     if constexpr (DER)
         iround_scale_scatter_der(T, a.hi, h, side, j0 < (1ull << pb), v);
