@@ -917,20 +917,25 @@ __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefe
 #ifndef ZKDL_IR_MULW
 #define ZKDL_IR_MULW 1
 #endif
+// the persistent kernel's product groups (its rounds are latency-bound: 3 = one three-chain body per group)
+#ifndef ZKDL_IP_MULW
+#define ZKDL_IP_MULW 3
+#endif
+template <int MW = ZKDL_IR_MULW>
 __device__ __forceinline__ fr3_t ir_mul3(const fr_t& a0, const fr_t& b0, const fr_t& a1, const fr_t& b1, const fr_t& a2,
                                          const fr_t& b2) {
-#if ZKDL_IR_MULW == 3
-    return fr_mul3_ni(a0, b0, a1, b1, a2, b2);
-#elif ZKDL_IR_MULW == 2
-    const fr2p_t p = fr_mul2_ni(a0, b0, a1, b1);
-    return fr3_t{p.x, p.y, fr_mul_ni(a2, b2)};
-#else
-    fr3_t r;
-    r.x = fr_mul_ni(a0, b0);
-    r.y = fr_mul_ni(a1, b1);
-    r.z = fr_mul_ni(a2, b2);
-    return r;
-#endif
+    if constexpr (MW == 3) {
+        return fr_mul3_ni(a0, b0, a1, b1, a2, b2);
+    } else if constexpr (MW == 2) {
+        const fr2p_t p = fr_mul2_ni(a0, b0, a1, b1);
+        return fr3_t{p.x, p.y, fr_mul_ni(a2, b2)};
+    } else {
+        fr3_t r;
+        r.x = fr_mul_ni(a0, b0);
+        r.y = fr_mul_ni(a1, b1);
+        r.z = fr_mul_ni(a2, b2);
+        return r;
+    }
 }
 
 // a(i) = sum_j beta(r_j, j) bit_j(w_i) as byte-table lookups (the table rows of k_relu_materialize)
@@ -943,7 +948,7 @@ __device__ __forceinline__ fr_t byte_sum(const fr_t* tb, uint32_t w, const IPtrs
 
 // Accumulate this thread's pairs j = j0, j0 + js, ... < P_blk of HI block h into T[0..7] =
 // (T_a(0), T_a(1), T_c(0), T_c(1), T_c(inf), T_b(0), T_b(1), T_b(inf)) of its side.
-template <bool FOLD, int SRC = 0, bool DER = false, bool CELLS = false, bool PF = false>
+template <bool FOLD, int SRC = 0, bool DER = false, bool CELLS = false, bool PF = false, int MW = ZKDL_IR_MULW>
 __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint32_t h, uint32_t pb, uint64_t j0,
                                              uint64_t js, const int side, fr_t (&T)[8]) {
     const fr_t one = fr_one();
@@ -1014,7 +1019,7 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
                 y0 = fr_load_l2(s); y1 = fr_load_l2(s + 1); y2 = fr_load_l2(s + 2); y3 = fr_load_l2(s + 3);
                 z0 = fr_load_l2(so); z1 = fr_load_l2(so + 1);
             }
-            const fr3_t f = ir_mul3(r, fr_sub(y1, y0), r, fr_sub(y3, y2), r, fr_sub(z1, z0));
+            const fr3_t f = ir_mul3<MW>(r, fr_sub(y1, y0), r, fr_sub(y3, y2), r, fr_sub(z1, z0));
             a0 = fr_add(y0, f.x);
             a1 = fr_add(y2, f.y);
             const fr_t mine = fr_add(z0, f.z);
@@ -1077,13 +1082,13 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             T[4] = fr_add(T[4], fr_mul_ni(zD, dA));
             continue;
         }
-        const fr3_t p = ir_mul3(eA, a0, eA, a1, eC, a0);
-        const fr3_t pq = ir_mul3(eC, a1, eB, a0, eB, a1);
+        const fr3_t p = ir_mul3<MW>(eA, a0, eA, a1, eC, a0);
+        const fr3_t pq = ir_mul3<MW>(eC, a1, eB, a0, eB, a1);
         T[0] = fr_add(T[0], p.x);
         T[1] = fr_add(T[1], p.y);
         const fr_t yC0 = p.z, yC1 = pq.x, zB0 = pq.y, zB1 = pq.z;
         if (FOLD) {
-            const fr3_t c = ir_mul3(yC0, om0, yC1, om1, fr_sub(yC1, yC0), fr_sub(om1, om0));
+            const fr3_t c = ir_mul3<MW>(yC0, om0, yC1, om1, fr_sub(yC1, yC0), fr_sub(om1, om0));
             T[2] = fr_add(T[2], c.x);
             T[3] = fr_add(T[3], c.y);
             T[4] = fr_add(T[4], c.z);
@@ -1094,7 +1099,7 @@ __device__ __forceinline__ void iround_pairs(const IPtrs& q, const fr_t& r, uint
             T[3] = fr_add(T[3], o1 ? yC1 : zero);
             T[4] = fr_add(T[4], o1 == o0 ? zero : (o1 ? yd : fr_neg(yd)));
         }
-        const fr3_t d = ir_mul3(zB0, fr_sub(a0, one), zB1, fr_sub(a1, one), fr_sub(zB1, zB0), fr_sub(a1, a0));
+        const fr3_t d = ir_mul3<MW>(zB0, fr_sub(a0, one), zB1, fr_sub(a1, one), fr_sub(zB1, zB0), fr_sub(a1, a0));
         T[5] = fr_add(T[5], d.x);
         T[6] = fr_add(T[6], d.y);
         T[7] = fr_add(T[7], d.z);
@@ -1482,7 +1487,10 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
 #pragma unroll
             for (int k = 0; k < 8; k++) T[k] = fr_zero();
             const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
-            iround_pairs<true>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1), side, T);
+            // the latency-bound rounds: three interleaved product chains per call (one call's latency for the
+            // three independent products of a step, instead of three calls in sequence)
+            iround_pairs<true, 0, false, false, false, ZKDL_IP_MULW>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1),
+                                                                    side, T);
             if (wtr) wtr[1] = globaltimer_ns();
             if (t > a.t0) wait_counter(a.hiflag, t);   // HI' rescaled by round t-1
             if (wtr) wtr[2] = globaltimer_ns();
@@ -1585,14 +1593,20 @@ __global__ void __launch_bounds__(256) k_relu_itail(ITailArgs a) {
         const int n = n0 >> t, np = n >> 1;
         if (tid < 4 * np) {
             const int b = tid >> 2, X = tid & 3;
-            const fr_t x = fr_from_u32((uint32_t)X);
+            // v(X) = T(2b) + X (T(2b+1) - T(2b)) for X in 0..3: additions only
             fr_t v[8];
-            for (int k = 0; k < 8; k++) v[k] = fr_add(T[k][2 * b], fr_mul_cold(x, fr_sub(T[k][2 * b + 1], T[k][2 * b])));
-            // tables: 0 a0, 1 a1, 2 oms, 3 EZ, 4 EA, 5 EGA, 6 EGZ, 7 Eb
-            fr_t t0 = fr_mul_cold(v[0], fr_add(v[3], fr_mul_cold(v[4], v[2])));
-            fr_t t1 = fr_mul_cold(v[1], fr_add(v[5], fr_mul_cold(v[6], v[2])));
-            fr_t q = fr_add(fr_mul_cold(v[0], fr_sub(v[0], fr_one())), fr_mul_cold(rp, fr_mul_cold(v[1], fr_sub(v[1], fr_one()))));
-            vals[b][X] = fr_add(fr_add(t0, t1), fr_mul_cold(v[7], q));
+            for (int k = 0; k < 8; k++) {
+                const fr_t y0 = T[k][2 * b], y1 = T[k][2 * b + 1], d = fr_sub(y1, y0);
+                v[k] = X == 0 ? y0 : X == 1 ? y1 : X == 2 ? fr_add(y1, d) : fr_add(fr_add(y1, d), d);
+            }
+            // tables: 0 a0, 1 a1, 2 oms, 3 EZ, 4 EA, 5 EGA, 6 EGZ, 7 Eb; independent products grouped in threes
+            // (latency: this single-CTA kernel is on the critical path)
+            const fr_t one = fr_one();
+            const fr3_t l1 = fr_mul3_ni(v[4], v[2], v[6], v[2], v[0], fr_sub(v[0], one));
+            const fr_t l1b = fr_mul_ni(v[1], fr_sub(v[1], one));
+            const fr3_t l2 = fr_mul3_ni(v[0], fr_add(v[3], l1.x), v[1], fr_add(v[5], l1.y), rp, l1b);
+            const fr_t q = fr_add(l1.z, l2.z);
+            vals[b][X] = fr_add(fr_add(l2.x, l2.y), fr_mul_ni(v[7], q));
         }
         __syncthreads();
         if (tid < 32) {
