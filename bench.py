@@ -480,6 +480,12 @@ def run_ours(args, rank, world, local):
             nz = np.flatnonzero(a.reshape(a.shape[0], -1).any(axis=1)) if a.ndim > 1 else np.array([0])
             n_real = int(nz[-1]) + 1 if nz.size else 1
             body = a[:n_real] if a.ndim > 1 else a
+            # a weight stack (slot = (step, layer)): the first step's slots + int8 differences to the same layer
+            # one step earlier (SGD moves a weight by a few quantisation steps), rebuilt by zk_undelta_i8
+            ds = dfcn.delta_stack(a, n_real) if (args.e2e_delta and small and a.ndim > 1) else None
+            if ds is not None:
+                pinned[id(a)] = ds
+                return ds
             t = torch.from_numpy(np.ascontiguousarray(body.astype(np.int16) if small else body)).pin_memory()
             pinned[id(a)] = dfcn.HostStack(t, a.shape) if (a.ndim > 1 and n_real < a.shape[0]) else t
         return pinned[id(a)]
@@ -580,7 +586,8 @@ def run_ours(args, rank, world, local):
                    "l2": "inputs larger than L2 (0.97 GB of distinct stacks, 1.59 GB of family operands read per window, vs 126 MB)", "parallelism": f"replica x{world}", "streams": args.streams, "mm_streams": args.mm_streams, "pipelined_windows": pipe, "mm_budget": args.mm_budget or max(8, 148 // args.mm_streams), "relu_aux_merge": bool(args.merge_aux)},
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "fcn.prove_windows_from_host: pinned host stacks -> HBM per family on a copy stream "
+                "path": "fcn.prove_windows_from_host: pinned host stacks (16-bit stacks as int16, weight stacks as "
+                        "their first step + int8 step differences, rebuilt on the device) -> HBM per family on a copy stream "
                         "(shared stacks once per window), each window's uploads behind the previous window's and "
                         "overlapped with the proofs; proofs back to the host", "windows": e2e_steps,
                 "uploads_alone_ms_per_window": None if uploads_ms is None else round(uploads_ms, 3)},
@@ -1000,6 +1007,8 @@ def main():
                     help="1: consecutive windows on alternating zkReLU / transcript streams (measured 171 ms per "
                          "window against 11.2: two windows' persistent spin-waiting kernels interleave on the SMs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-delta", type=int, default=1, choices=[0, 1],
+                    help="1: e2e ships weight stacks as their first step + int8 step-to-step differences (zk_undelta_i8)")
     ap.add_argument("--e2e-i16", type=int, default=1, choices=[0, 1],
                     help="1: e2e uploads stacks whose entries fit 16 bits as int16 (widened on the device)")
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2],

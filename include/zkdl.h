@@ -112,6 +112,15 @@ zk_status zk_embed_i32(zk_ctx* ctx, const int32_t* d_in, uint64_t n, void* d_out
  *   The end-to-end transport of stacks whose entries fit 16 bits (the matmul operands of the FCN trace):
  *   half the host-to-device bytes, the int32 tensor the provers read is rebuilt on the device. */
 zk_status zk_widen_i16(zk_ctx* ctx, const int16_t* d_in, uint64_t n, int32_t* d_out);
+/* zk_undelta_i8: rebuild an int32 stack of n_slots slices of slot_elems entries from its first L slices (int16,
+ *   d_base, [L][slot_elems]) and the int8 differences of every later slice to the slice L before it (d_delta,
+ *   [n_slots - L][slot_elems]):  out[s] = base[s] (s < L),  out[s] = out[s - L] + delta[s - L] (s >= L).
+ *   The end-to-end transport of the weight stacks (a weight changes by a few quantisation steps per SGD update,
+ *   so the slice of the same layer one training step earlier, L slices back, differs by int8 values): ~1 byte
+ *   per entry over PCIe instead of 2; the provers read the same int32 tensor.  slot_elems a multiple of 4;
+ *   d_out 16-, d_base 8-, d_delta 4-byte aligned; asynchronous on the context stream. */
+zk_status zk_undelta_i8(zk_ctx* ctx, const int16_t* d_base, const int8_t* d_delta, uint64_t slot_elems, uint32_t L,
+                        uint32_t n_slots, int32_t* d_out);
 zk_status zk_eq_table(zk_ctx* ctx, const zk_fr* point, uint32_t k, const zk_fr* scale, void* d_out);
 zk_status zk_mle_eval_i32(zk_ctx* ctx, const int32_t* d_tab, uint32_t m, const zk_fr* point, zk_fr* out);
 zk_status zk_mle_eval_fr(zk_ctx* ctx, const void* d_tab, uint32_t m, const zk_fr* point, zk_fr* out);

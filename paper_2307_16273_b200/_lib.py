@@ -79,6 +79,7 @@ def lib():
         "zk_transcript_free": ([vp], None),
         "zk_embed_i32": ([vp, vp, u64, vp], i32),
         "zk_widen_i16": ([vp, vp, u64, vp], i32),
+        "zk_undelta_i8": ([vp, vp, vp, u64, u32, u32, vp], i32),
         "zk_eq_table": ([vp, vp, u32, vp, vp], i32),
         "zk_mle_eval_i32": ([vp, vp, u32, vp, vp], i32),
         "zk_mle_eval_fr": ([vp, vp, u32, vp, vp], i32),

@@ -614,6 +614,20 @@ def parse_rescale_out(raw: bytes, logD: int, Q: int, R: int) -> dict:
     return dict(claims=claims, A=A, B=B, proof=raw[:plen])
 
 
+def undelta_i8(ctx: Context, base16: torch.Tensor, delta8: torch.Tensor | None, L: int, n_slots: int,
+               out: torch.Tensor) -> torch.Tensor:
+    """zk_undelta_i8: base16 [L][...] int16 and delta8 [n_slots - L][...] int8 device tensors -> out[:n_slots] int32
+    (out[s] = base[s], s < L; out[s] = out[s - L] + delta[s - L]), on the context stream."""
+    assert base16.dtype == torch.int16 and base16.is_cuda and base16.is_contiguous() and base16.shape[0] == L
+    slot = base16[0].numel()
+    if delta8 is not None:
+        assert delta8.dtype == torch.int8 and delta8.is_contiguous() and delta8.shape[0] == n_slots - L
+    assert out.dtype == torch.int32 and out.is_contiguous() and out[0].numel() == slot
+    ctx.check(lib().zk_undelta_i8(ctx.h, base16.data_ptr(), delta8.data_ptr() if delta8 is not None else None, slot, L,
+                                  n_slots, out.data_ptr()))
+    return out
+
+
 def widen_i16(ctx: Context, t16: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """zk_widen_i16: an int16 device tensor -> int32 (same shape), on the context stream."""
     assert t16.dtype == torch.int16 and t16.is_cuda and t16.is_contiguous()

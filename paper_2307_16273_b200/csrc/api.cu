@@ -256,6 +256,42 @@ __global__ void k_widen_i16(const int16_t* in, uint64_t n, int32_t* out) {
         out[i] = in[i];
 }
 
+// out[s][e] = base[s][e] (s < L), out[s][e] = out[s - L][e] + delta[s - L][e] (L <= s < n_slots): one thread per
+// (l < L, 4 consecutive entries), walking its slots l, l + L, ... (4 B of deltas in, 16 B out per slot step)
+__global__ void k_undelta_i8(const int16_t* base, const int8_t* delta, uint64_t slot, uint32_t L, uint32_t n_slots,
+                             int32_t* out) {
+    const uint64_t q = slot / 4, total = q * L;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t l = (uint32_t)(i / q);
+        const uint64_t e = 4 * (i % q);
+        const short2 b0 = *reinterpret_cast<const short2*>(base + (uint64_t)l * slot + e);
+        const short2 b1 = *reinterpret_cast<const short2*>(base + (uint64_t)l * slot + e + 2);
+        int4 v = make_int4(b0.x, b0.y, b1.x, b1.y);
+        __stcs(reinterpret_cast<int4*>(out + (uint64_t)l * slot + e), v);
+        for (uint32_t s = l + L; s < n_slots; s += L) {
+            const char4 d = __ldcs(reinterpret_cast<const char4*>(delta + (uint64_t)(s - L) * slot + e));
+            v.x += d.x;
+            v.y += d.y;
+            v.z += d.z;
+            v.w += d.w;
+            __stcs(reinterpret_cast<int4*>(out + (uint64_t)s * slot + e), v);
+        }
+    }
+}
+
+zk_status zk_undelta_i8(zk_ctx* ctx, const int16_t* d_base, const int8_t* d_delta, uint64_t slot_elems, uint32_t L,
+                        uint32_t n_slots, int32_t* d_out) {
+    ZK_API_BEGIN(ctx)
+    ZK_REQUIRE(d_base && d_out && L >= 1 && n_slots >= L && (d_delta || n_slots == L), ZK_ERR_ARG, "bad argument");
+    ZK_REQUIRE(slot_elems % 4 == 0 && ((uintptr_t)d_out & 15) == 0 && ((uintptr_t)d_base & 7) == 0 &&
+                   ((uintptr_t)d_delta & 3) == 0,
+               ZK_ERR_ARG, "slot_elems must be a multiple of 4, buffers aligned (out 16, base 8, delta 4 bytes)");
+    if (slot_elems)
+        ZK_LAUNCH(ctx, k_undelta_i8, grid_for(ctx, slot_elems / 4 * L, 256, 8), 256, 0, d_base, d_delta, slot_elems, L,
+                  n_slots, d_out);
+    ZK_API_END(ctx)
+}
+
 zk_status zk_widen_i16(zk_ctx* ctx, const int16_t* d_in, uint64_t n, int32_t* d_out) {
     ZK_API_BEGIN(ctx)
     ZK_REQUIRE((d_in && d_out) || !n, ZK_ERR_ARG, "null argument");

@@ -235,6 +235,48 @@ class HostStack:
         return self.data.element_size()
 
 
+class DeltaStack:
+    """A host stack shipped as its first L slots (int16) and the int8 differences of every later real slot to
+    the slot L before it (a weight stack: the slot of the same layer one training step earlier); rebuilt on
+    the device by zk_undelta_i8 into the int32 stack of `shape` (trailing padding slots zero-filled once).
+    delta_stack() builds one when every difference fits int8 and the first slots fit int16."""
+
+    def __init__(self, base: torch.Tensor, delta, L: int, n_real: int, shape):
+        self.base, self.delta, self.L, self.n_real, self.shape = base, delta, int(L), int(n_real), tuple(shape)
+        self.dtype = torch.int8
+
+    def data_ptr(self) -> int:
+        return self.base.data_ptr()
+
+    def numel(self) -> int:   # the transport bytes (element_size 1)
+        return self.base.numel() * 2 + (self.delta.numel() if self.delta is not None else 0)
+
+    def element_size(self) -> int:
+        return 1
+
+
+def delta_stack(a, n_real: int, max_stride: int = 16, pin: bool = True):
+    """numpy int32 stack a[N][...] (slots >= n_real zero padding) -> DeltaStack with the smallest stride L <=
+    max_stride for which a[s] - a[s - L] fits int8 for every real slot s >= L (and a[:L] fits int16), else None.
+    Transport encoding only: the device rebuilds a[:n_real] exactly."""
+    import numpy as np
+    body = a[:n_real]
+    if a.ndim < 2 or n_real < 2 or body[0].size % 4:
+        return None
+    for L in range(1, min(max_stride, n_real - 1) + 1):
+        base = body[:L]
+        if int(base.max()) >= (1 << 15) or int(base.min()) < -(1 << 15):
+            return None
+        d = body[L:].astype(np.int64) - body[:-L]
+        if int(d.max()) <= 127 and int(d.min()) >= -128:
+            tb = torch.from_numpy(np.ascontiguousarray(base.astype(np.int16)))
+            td = torch.from_numpy(np.ascontiguousarray(d.astype(np.int8)))
+            if pin:
+                tb, td = tb.pin_memory(), td.pin_memory()
+            return DeltaStack(tb, td, L, n_real, a.shape)
+    return None
+
+
 _RING: dict = {}   # persistent transport buffers: (device, host buffer, window slot) -> (staging, int32 output)
 
 
@@ -258,6 +300,21 @@ class _Uploader:
         self.ws = torch.cuda.Stream(device=dev)
         self.wctx = api.Context(dev.index if dev.index is not None else torch.cuda.current_device(), self.ws)
 
+    def _delta_buffers(self, t, slot):
+        key = (self.dev.index, t.base.data_ptr(), t.numel(), "delta", t.shape, slot)
+        bufs = _RING.get(key) if slot is not None else None
+        if bufs is None:
+            with torch.cuda.stream(self.cs):
+                sb = torch.empty(tuple(t.base.shape), dtype=torch.int16, device=self.dev)
+                sd = torch.empty(tuple(t.delta.shape), dtype=torch.int8, device=self.dev) if t.delta is not None else None
+                out = torch.empty(t.shape, dtype=torch.int32, device=self.dev)
+                if t.n_real < t.shape[0]:
+                    out[t.n_real:].zero_()
+            bufs = (sb, sd, out)
+            if slot is not None:
+                _RING[key] = bufs
+        return bufs
+
     def _buffers(self, t, slot):
         hs = isinstance(t, HostStack)
         data = t.data if hs else t
@@ -277,6 +334,16 @@ class _Uploader:
         return data, bufs
 
     def upload(self, t, slot=None) -> torch.Tensor:
+        if isinstance(t, DeltaStack):   # int16 first slots + int8 differences, rebuilt by zk_undelta_i8
+            sb, sd, out = self._delta_buffers(t, slot)
+            with torch.cuda.stream(self.cs):
+                sb.copy_(t.base, non_blocking=True)
+                if sd is not None:
+                    sd.copy_(t.delta, non_blocking=True)
+            self.ws.wait_stream(self.cs)
+            with torch.cuda.stream(self.ws):
+                api.undelta_i8(self.wctx, sb, sd, t.L, t.n_real, out)
+            return out
         data, (stage, out) = self._buffers(t, slot)
         n = data.shape[0]
         if stage is None:   # int32 stack, no padding: the copy is the upload

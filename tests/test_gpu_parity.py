@@ -802,3 +802,45 @@ def test_e2e_int16_transport_same_proofs(ctx):
     from paper_2307_16273_b200 import api
     y = api.widen_i16(ctx, x.cuda())
     assert torch.equal(y.cpu(), x.to(torch.int32))
+
+
+def test_e2e_delta_transport_same_proofs(ctx):
+    """Weight stacks shipped as their first slots (int16) + int8 slot differences (fcn.delta_stack, rebuilt by
+    zk_undelta_i8 on the device) give the bytes of the device-resident window; zk_undelta_i8 rebuilds a random
+    stack exactly (padding slots stay zero)."""
+    import numpy as np
+    from paper_2307_16273_b200 import api
+    from paper_2307_16273_b200 import fcn as dfcn
+    from synth import fcn
+    shape = fcn.tiny_shape(steps=2, layers=5, width=64, batch=16, din=128, dout=16)
+    fams = fcn.assemble_families(shape, fcn.generate_trace(shape))
+    seed, hdr = fs_seed("e2e-delta"), fcn.fcn_header(shape)
+    g = dfcn.prove_window(ctx, seed, hdr, dfcn.upload_families(fams))
+    deltas = []
+
+    def host(a):
+        if a.ndim > 1:
+            nz = np.flatnonzero(a.reshape(a.shape[0], -1).any(axis=1))
+            ds = dfcn.delta_stack(a, int(nz[-1]) + 1 if nz.size else 1)
+            if ds is not None:
+                deltas.append(ds)
+                return ds
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hf = [dfcn.DeviceFamily(f.name, "matmul", A=host(f.A), B=host(f.B), trans_a=f.transA, trans_b=f.transB)
+          if hasattr(f, "A") else dfcn.DeviceFamily(f.name, "relu", Z=host(f.Z), GA=host(f.GA), Q=f.Q, R=f.R) for f in fams]
+    assert any(d.L > 1 for d in deltas)   # the hidden-layer weight stack: stride = layers per step
+    h = dfcn.prove_windows_from_host(ctx, [(seed, hdr, hf)] * 2)
+    for w in h:
+        assert [r["proof"] for r in w] == [r["proof"] for r in g]
+    rng = np.random.default_rng(5)
+    a = np.zeros((16, 6, 8), np.int32)
+    a[:3] = rng.integers(-30000, 30000, (3, 6, 8))
+    for s in range(3, 13):
+        a[s] = a[s - 3] + rng.integers(-128, 128, (6, 8))
+    ds = dfcn.delta_stack(a, 13)
+    assert ds is not None and ds.L == 3
+    out = torch.full((16, 6, 8), -1, dtype=torch.int32, device="cuda")
+    out[13:].zero_()
+    api.undelta_i8(ctx, ds.base.cuda(), ds.delta.cuda(), 3, 13, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), a)
