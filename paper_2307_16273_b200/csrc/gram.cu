@@ -44,9 +44,6 @@ namespace zk {
 #ifndef GR_GATE_WARP
 #define GR_GATE_WARP 7   // builds the sign gates of the linear tile (a warp without linear-tile rows)
 #endif
-#ifndef GR_EXP
-#define GR_EXP 0   // timing experiments only (wrong cells): 1 natural entry order, 2 two linear warps
-#endif
 #if GR_SYM
 constexpr int GR_STAGES = 3;
 constexpr uint32_t GR_ACC_HI = 128;   // tiles t >= 4 (N = 16)
@@ -241,7 +238,7 @@ __global__ void __launch_bounds__(320, 1) k_relu_gram(GramArgs a) {
         // ---------------- operand producers + epilogue
         const int q = warp & 3, grp = warp >> 2;
         constexpr int LGRP = GR_SELFGATE ? 1 : 0;   // the warp group that builds the linear-tile rows
-        const bool lin = grp == LGRP && q < (GR_EXP == 2 ? 2 : 3);   // this warp also builds the linear-cell tile rows (q: 0 = E'_x1,
+        const bool lin = grp == LGRP && q < 3;   // this warp also builds the linear-cell tile rows (q: 0 = E'_x1,
                                               // 1 = E'_x2 o(own entry), 2 = E'_x2 o(pair partner))
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t it = 0, seg = 0, ci = 0;
@@ -255,7 +252,7 @@ __global__ void __launch_bounds__(320, 1) k_relu_gram(GramArgs a) {
             for (int kk = 0; kk < GR_CH_KS; kk++, it++) {
                 const uint32_t st = it % GR_STAGES, par = it & 1;
                 // K step kk: entries 64 (kk / 2) + 2 m + (kk & 1), m = lane (the pair 32 (kk / 2) + m of the chunk)
-                const uint32_t ei = GR_EXP == 1 ? 32 * kk + lane : 64 * (kk >> 1) + 2 * lane + (kk & 1);
+                const uint32_t ei = 64 * (kk >> 1) + 2 * lane + (kk & 1);
                 const uint32_t wv = Wsm[ei] & a.qr_mask;
                 uint32_t zv = 0, zo = 0;   // sign words of the entries and of their pair partners: the gate warp
                 if (!GR_SELFGATE && warp == GR_GATE_WARP) {
