@@ -477,7 +477,10 @@ void relu_bitsums_gram(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint32_
     ga.qr_mask = qr_mask;
     ga.sig_bit = sig_bit;
     ga.B = B;
-    uint32_t G = (uint32_t)ctx->num_sms / 2;
+    // CTAs per word: G = num_sms / 2 x ZKDL_GRAM_WAVES (one CTA per SM; more waves = finer work, less exposed to
+    // SMs held by other streams' kernels)
+    static const int waves = getenv("ZKDL_GRAM_WAVES") ? atoi(getenv("ZKDL_GRAM_WAVES")) : 1;
+    uint32_t G = (uint32_t)ctx->num_sms / 2 * (uint32_t)(waves < 1 ? 1 : waves);
     if ((uint64_t)G > ga.nch) G = (uint32_t)ga.nch;
     ga.G = G;
     const uint32_t T = B * (B + 1) / 2, ncs = 6 * B + T;

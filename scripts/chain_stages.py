@@ -31,11 +31,13 @@ wctx = api.Context(0, torch.cuda.Stream())
 rsctx = api.Context(0, torch.cuda.Stream()) if os.environ.get("CHAIN_RESCALE_STREAM", "1") != "0" else None
 if rsctx is not None:
     rsctx.set_sm_budget(32)
+    rsctx.set_persistent(os.environ.get("CHAIN_BESIDE_PERSIST", "0") == "1")
 nl = int(os.environ.get("CHAIN_LATE_STREAMS", "4"))
 after = os.environ.get("CHAIN_LATE_AFTER", "0") == "1"
 lctxs = [api.Context(0, torch.cuda.Stream()) for _ in range(nl)]
 for c in lctxs:
     c.set_sm_budget(max(2, 48 // max(1, nl)))
+    c.set_persistent(os.environ.get("CHAIN_BESIDE_PERSIST", "0") == "1")
 header = fcn.fcn_header(shape)
 seed = fs_seed("C4-chained-rank0")
 with torch.cuda.stream(stream):
