@@ -1432,6 +1432,9 @@ struct IPersistArgs {
     unsigned int* flag;     // rounds whose r_t is published
     unsigned int* hiflag;   // rounds whose HI' rescale is published
     unsigned long long* trace;   // diagnostics (ZKDL_IPERSIST_TRACE): 4 timestamps per round, or null
+    // DER (derived X = 1, as k_relu_iround_f MODE bit 2): the per-term running sums and u_x[t]^-1 (5 per round)
+    fr_t* sigma;
+    const fr_t* uinv;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -1454,7 +1457,9 @@ __device__ __forceinline__ void wait_counter(const unsigned int* p, unsigned int
     __syncthreads();
 }
 
+template <bool DER>
 __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
+    constexpr int NV = DER ? IR_NV_DER : IR_NV;
     __shared__ fr_t sm[8 * 16];
     __shared__ fr_t tot[16];
     __shared__ fr_t prod[15];
@@ -1489,15 +1494,18 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
             const uint64_t j0 = (uint64_t)cib * (blockDim.x >> 1) + (threadIdx.x >> 1);
             // the latency-bound rounds: three interleaved product chains per call (one call's latency for the
             // three independent products of a step, instead of three calls in sequence)
-            iround_pairs<true, 0, false, false, false, ZKDL_IP_MULW>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1),
-                                                                    side, T);
+            iround_pairs<true, 0, DER, false, false, ZKDL_IP_MULW>(q, r, h, pb, j0, (uint64_t)a.cpb * (blockDim.x >> 1),
+                                                                  side, T);
             if (wtr) wtr[1] = globaltimer_ns();
             if (t > a.t0) wait_counter(a.hiflag, t);   // HI' rescaled by round t-1
             if (wtr) wtr[2] = globaltimer_ns();
             fr_t v[16];
-            iround_scale_scatter(T, a.hi[hv], h, side, j0 < (1ull << pb), v);
+            if constexpr (DER)
+                iround_scale_scatter_der(T, a.hi[hv], h, side, j0 < (1ull << pb), v);
+            else
+                iround_scale_scatter(T, a.hi[hv], h, side, j0 < (1ull << pb), v);
             block_transpose_sum16(v, sm);
-            if (threadIdx.x < IR_NV) fr_store(&a.partials[w * IR_NV + threadIdx.x], v[0]);
+            if (threadIdx.x < NV) fr_store(&a.partials[w * NV + threadIdx.x], v[0]);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
@@ -1513,13 +1521,17 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
                 for (int k = 0; k < 16; k++) v[k] = fr_zero();
                 for (unsigned int bb = threadIdx.x; bb < nworkers; bb += blockDim.x)
 #pragma unroll
-                    for (int k = 0; k < IR_NV; k++) v[k] = fr_add(v[k], fr_load_l2(&a.partials[bb * IR_NV + k]));
+                    for (int k = 0; k < NV; k++) v[k] = fr_add(v[k], fr_load_l2(&a.partials[bb * NV + k]));
                 block_transpose_sum16(v, sm);
-                if (threadIdx.x < IR_NV) tot[threadIdx.x] = v[0];
+                if (threadIdx.x < NV) tot[threadIdx.x] = v[0];
             }
             __syncthreads();
             if (a.trace && threadIdx.x == 0) a.trace[(t - a.t0) * 4 + 1] = globaltimer_ns();
-            iround_g(tot, a.u, t, prod, g);
+            __shared__ fr_t Vd[15];
+            if constexpr (DER)
+                iround_g_der(tot, a.u, t, a.sigma, a.uinv + 5ull * t, Vd, prod, g);
+            else
+                iround_g(tot, a.u, t, prod, g);
             IFinish f;
             f.st = a.st;
             f.claim = a.claim;
@@ -1547,6 +1559,7 @@ __global__ void __launch_bounds__(256, 2) k_relu_ipersist(IPersistArgs a) {
                 if (a.trace) a.trace[(t - a.t0) * 4 + 3] = globaltimer_ns();
             }
             iround_claim(f, msg);   // needed only by the next round's message
+            if constexpr (DER) iround_sigma_der(Vd, a.u, t, a.r_i + t, a.sigma);
         }
     }
 }
@@ -1985,6 +1998,8 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         pa.st = tr->d_st;
         const unsigned int grid = 1 + (pcpb << hb);
         pa.partials = s.alloc<fr_t>((size_t)grid * IR_NV);
+        pa.sigma = sigma;
+        pa.uinv = uinv;
         unsigned int* ctr = s.alloc_zero<unsigned int>(3);
         pa.arrive = ctr;
         pa.flag = ctr + 1;
@@ -1999,7 +2014,10 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
             ev_b = ctx->take_event();
             cudaEventRecord(ev_a, ctx->stream);
         }
-        ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_relu_ipersist, dim3(grid), dim3(256), args, 0, ctx->stream));
+        if (derive)
+            ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_relu_ipersist<true>, dim3(grid), dim3(256), args, 0, ctx->stream));
+        else
+            ZK_CUDA(cudaLaunchCooperativeKernel((const void*)k_relu_ipersist<false>, dim3(grid), dim3(256), args, 0, ctx->stream));
         after_launch(ctx, "k_relu_ipersist");
         if (prof) {
             cudaEventRecord(ev_b, ctx->stream);
