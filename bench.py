@@ -208,7 +208,7 @@ def frmul_model(fams, persist_log: int = 16, hb: int = 5) -> dict:
         cells = derive and os.environ.get("ZKDL_IR_CELLS", "1") != "0" and logD >= 12 and t0 >= 2
         for t in range(H):
             pairs = D >> (t + 1)
-            if t < t0 and derive:
+            if derive:   # the per-round and (round 2, later) the persistent rounds
                 per = (8 if cells else 14) if t == 0 else (18 if t == 1 and t0 >= 2 else 24)
             else:
                 per = 18 if t == 0 else (24 if t == 1 and t0 >= 2 else 30)
