@@ -280,7 +280,18 @@ void mle_i32_relu(zk_ctx* ctx, int kind, const int32_t* d_z, const int32_t* d_g,
 __global__ void __launch_bounds__(256) k_mle4_rows(const int32_t* Z, const int32_t* GA, uint32_t R, uint64_t rows,
                                                    const fr_t* H0, const fr_t* H1, const fr_t* H2, const fr_t* H3,
                                                    fr_t* partials) {
+    // the CTA's rows of the four row tables staged in shared memory (the loop then waits only on the words),
+    // and the words of the next four rows loaded while the current ones are accumulated (memory latency was
+    // the bound: ncu long_sb 68%, 0.47 TB/s)
+    extern __shared__ fr_t sH[];
     const uint64_t r0 = blockIdx.x * rows / gridDim.x, r1 = (blockIdx.x + 1) * rows / gridDim.x;
+    const uint32_t nr = (uint32_t)(r1 - r0);
+    for (uint32_t e = threadIdx.x; e < 4 * nr; e += blockDim.x) {
+        const uint32_t k = e / nr, i = e % nr;
+        const fr_t* H = k == 0 ? H0 : k == 1 ? H1 : k == 2 ? H2 : H3;
+        sH[k * nr + i] = fr_load(&H[r0 + i]);
+    }
+    __syncthreads();
     const uint32_t c = threadIdx.x;
     uint32_t acc[4][10];
 #pragma unroll
@@ -289,31 +300,48 @@ __global__ void __launch_bounds__(256) k_mle4_rows(const int32_t* Z, const int32
         for (int l = 0; l < 10; l++) acc[k][l] = 0;
     const int64_t half = 1ll << (R - 1);
     uint64_t r = r0;
-    for (; r + 3 < r1; r += 4) {   // 8 loads in flight per thread
+    int32_t zn[4], gn[4];
+    if (r + 3 < r1) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            zn[i] = __ldcs(Z + (r + i) * 256 + c);
+            gn[i] = __ldcs(GA + (r + i) * 256 + c);
+        }
+    }
+    for (; r + 3 < r1; r += 4) {
         int32_t z[4], g[4];
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            z[i] = __ldcs(Z + (r + i) * 256 + c);
-            g[i] = __ldcs(GA + (r + i) * 256 + c);
+            z[i] = zn[i];
+            g[i] = gn[i];
         }
+        if (r + 7 < r1) {   // the next four rows in flight
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                zn[i] = __ldcs(Z + (r + 4 + i) * 256 + c);
+                gn[i] = __ldcs(GA + (r + 4 + i) * 256 + c);
+            }
+        }
+        const uint32_t o = (uint32_t)(r - r0);
 #pragma unroll
         for (int i = 0; i < 4; i++) {
             const int32_t a = z[i] >= 0 ? (int32_t)(((int64_t)z[i] + half) >> R) : 0;      // A = 1{Z >= 0} round(Z / 2^R)
             const int32_t gz = z[i] >= 0 ? (int32_t)(((int64_t)g[i] + half) >> R) : 0;     // G_Z = 1{Z >= 0} round(G_A / 2^R)
-            ZK_MAC_WIDE(acc[0], fr_load(&H0[r + i]), (uint32_t)z[i] + 0x80000000u);
-            ZK_MAC_WIDE(acc[1], fr_load(&H1[r + i]), (uint32_t)a + 0x80000000u);
-            ZK_MAC_WIDE(acc[2], fr_load(&H2[r + i]), (uint32_t)g[i] + 0x80000000u);
-            ZK_MAC_WIDE(acc[3], fr_load(&H3[r + i]), (uint32_t)gz + 0x80000000u);
+            ZK_MAC_WIDE(acc[0], sH[o + i], (uint32_t)z[i] + 0x80000000u);
+            ZK_MAC_WIDE(acc[1], sH[nr + o + i], (uint32_t)a + 0x80000000u);
+            ZK_MAC_WIDE(acc[2], sH[2 * nr + o + i], (uint32_t)g[i] + 0x80000000u);
+            ZK_MAC_WIDE(acc[3], sH[3 * nr + o + i], (uint32_t)gz + 0x80000000u);
         }
     }
     for (; r < r1; r++) {
         const int32_t z = __ldcs(Z + r * 256 + c), g = __ldcs(GA + r * 256 + c);
         const int32_t a = z >= 0 ? (int32_t)(((int64_t)z + half) >> R) : 0;
         const int32_t gz = z >= 0 ? (int32_t)(((int64_t)g + half) >> R) : 0;
-        ZK_MAC_WIDE(acc[0], fr_load(&H0[r]), (uint32_t)z + 0x80000000u);
-        ZK_MAC_WIDE(acc[1], fr_load(&H1[r]), (uint32_t)a + 0x80000000u);
-        ZK_MAC_WIDE(acc[2], fr_load(&H2[r]), (uint32_t)g + 0x80000000u);
-        ZK_MAC_WIDE(acc[3], fr_load(&H3[r]), (uint32_t)gz + 0x80000000u);
+        const uint32_t o = (uint32_t)(r - r0);
+        ZK_MAC_WIDE(acc[0], sH[o], (uint32_t)z + 0x80000000u);
+        ZK_MAC_WIDE(acc[1], sH[nr + o], (uint32_t)a + 0x80000000u);
+        ZK_MAC_WIDE(acc[2], sH[2 * nr + o], (uint32_t)g + 0x80000000u);
+        ZK_MAC_WIDE(acc[3], sH[3 * nr + o], (uint32_t)gz + 0x80000000u);
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) fr_store(&partials[((uint64_t)blockIdx.x * 4 + k) * 256 + c], fr_redc_wide(acc[k]));
@@ -350,7 +378,8 @@ __global__ void k_mle4_final(const fr_t* mid, fr_t* out) {
 void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t R, uint32_t m, const fr_t* d_U,
                    fr_t* d_out, Scratch& s) {
     static const bool fused_off = getenv("ZKDL_MLE4_FUSED") && atoi(getenv("ZKDL_MLE4_FUSED")) == 0;
-    if (!fused_off && m >= 16 && R >= 1) {
+    // (the fused kernel stages a CTA's rows of the four row tables in shared memory: <= 2^26 entries)
+    if (!fused_off && m >= 16 && m <= 26 && R >= 1) {
         const uint32_t lo = 8, hi = m - 8;
         fr_t* E[4];
         fr_t* H[4];
@@ -366,7 +395,10 @@ void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t
         uint32_t nb = (uint32_t)ctx->num_sms * 2;
         if ((uint64_t)nb > rows / 4) nb = (uint32_t)(rows / 4);
         fr_t* P = s.alloc<fr_t>((uint64_t)nb * 4 * 256);
-        ZK_LAUNCH(ctx, k_mle4_rows, nb, 256, 0, d_z, d_g, R, rows, (const fr_t*)H[0], (const fr_t*)H[1],
+        const size_t hsm = 4 * sizeof(fr_t) * (size_t)((rows + nb - 1) / nb + 1);
+        if (hsm > 48 * 1024)
+            ZK_CUDA(cudaFuncSetAttribute(k_mle4_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+        ZK_LAUNCH(ctx, k_mle4_rows, nb, 256, hsm, d_z, d_g, R, rows, (const fr_t*)H[0], (const fr_t*)H[1],
                   (const fr_t*)H[2], (const fr_t*)H[3], P);
         fr_t* mid = s.alloc<fr_t>(32);
         ZK_LAUNCH(ctx, k_mle4_finish, 32, 256, 0, (const fr_t*)P, nb, (const fr_t*)E[0], (const fr_t*)E[1],
