@@ -386,9 +386,12 @@ __global__ void __launch_bounds__(320, 1) k_relu_gram(GramArgs a) {
 
 // Sums over the G CTAs of a word.  lin6[s][par][q][j] (12 B values, the linear cells per parity) and the Gram
 // cells of both words into cell_tot[4B ..) (relu.cu cell_decode order).
+// One warp per output: the lanes add strided partials, then a shuffle tree (the 74-long serial chain per thread
+// was latency-bound: 41 us).
 __global__ void k_relu_gram_reduce(const fr_t* partials, uint32_t G, uint32_t B, fr_t* cell_tot, fr_t* lin6) {
     const uint32_t T = B * (B + 1) / 2, ncs = 6 * B + T, nout = 12 * B + 2 * T;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nout; c += gridDim.x * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nout; c += nw) {
         uint32_t s, local;
         fr_t* dst;
         if (c < 12 * B) {
@@ -400,9 +403,10 @@ __global__ void k_relu_gram_reduce(const fr_t* partials, uint32_t G, uint32_t B,
             local = 6 * B + (c - 12 * B) % T;
             dst = &cell_tot[4 * B + (c - 12 * B)];
         }
-        fr_t acc = fr_zero();
-        for (uint32_t gg = 0; gg < G; gg++) acc = fr_add(acc, fr_load(&partials[((size_t)s * G + gg) * ncs + local]));
-        fr_store(dst, acc);
+        fr_t acc[1] = {fr_zero()};
+        for (uint32_t gg = lane; gg < G; gg += 32) acc[0] = fr_add(acc[0], fr_load(&partials[((size_t)s * G + gg) * ncs + local]));
+        warp_reduce_fr<1>(acc);
+        if (lane == 0) fr_store(dst, acc[0]);
     }
 }
 
@@ -489,8 +493,7 @@ void relu_bitsums_gram(zk_ctx* ctx, const int32_t* Z, const int32_t* GA, uint32_
     const size_t smem = sizeof(GramSmem) + 1024 > 120 * 1024 ? sizeof(GramSmem) + 1024 : 120 * 1024;
     ZK_CUDA(cudaFuncSetAttribute(k_relu_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ZK_LAUNCH(ctx, k_relu_gram, 2 * G, 320, smem, ga);
-    ZK_LAUNCH(ctx, k_relu_gram_reduce, (12 * B + 2 * T + 127) / 128, 128, 0, (const fr_t*)ga.partials, G, B, cell_tot,
-              lin6);
+    ZK_LAUNCH(ctx, k_relu_gram_reduce, (12 * B + 2 * T + 7) / 8, 256, 0, (const fr_t*)ga.partials, G, B, cell_tot, lin6);
     GramU0 U;
     for (int x = 0; x < 4; x++) U.u[x] = u_i[x];
     ZK_LAUNCH(ctx, k_relu_gram_lin, (4 * B + 127) / 128, 128, 0, (const fr_t*)lin6, B, U, cell_tot);

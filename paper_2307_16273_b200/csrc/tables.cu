@@ -346,15 +346,19 @@ __global__ void __launch_bounds__(256) k_mle4_rows(const int32_t* Z, const int32
 #pragma unroll
     for (int k = 0; k < 4; k++) fr_store(&partials[((uint64_t)blockIdx.x * 4 + k) * 256 + c], fr_redc_wide(acc[k]));
 }
-// block (k, q): claim k, columns 32 q .. 32 q + 31; warp w adds the partials of CTAs b = w, w + 8, ...; the
-// column sums are weighted by E_k[c] and summed into mid[k * 8 + q]
+// block (k, q, part): claim k, columns 32 q .. 32 q + 31, CTAs b = part (mod MLE4_PARTS); warp w adds the partials of
+// CTAs b = part + MLE4_PARTS (w + 8 i); the column sums are weighted by E_k[c] and summed into
+// mid[(k * 8 + q) * MLE4_PARTS + part]
+constexpr uint32_t MLE4_PARTS = 4;
 __global__ void __launch_bounds__(256) k_mle4_finish(const fr_t* partials, uint32_t nb, const fr_t* E0, const fr_t* E1,
                                                      const fr_t* E2, const fr_t* E3, fr_t* mid) {
     __shared__ fr_t sm[8][32];
-    const uint32_t k = blockIdx.x >> 3, q = blockIdx.x & 7, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint32_t part = blockIdx.x % MLE4_PARTS, kq = blockIdx.x / MLE4_PARTS;
+    const uint32_t k = kq >> 3, q = kq & 7, w = threadIdx.x >> 5, l = threadIdx.x & 31;
     const uint32_t c = q * 32 + l;
     fr_t s = fr_zero();
-    for (uint32_t b = w; b < nb; b += 8) s = fr_add(s, fr_load(&partials[((uint64_t)b * 4 + k) * 256 + c]));
+    for (uint32_t b = part + MLE4_PARTS * w; b < nb; b += 8 * MLE4_PARTS)
+        s = fr_add(s, fr_load(&partials[((uint64_t)b * 4 + k) * 256 + c]));
     sm[w][l] = s;
     __syncthreads();
     if (w == 0) {
@@ -363,15 +367,15 @@ __global__ void __launch_bounds__(256) k_mle4_finish(const fr_t* partials, uint3
         const fr_t* E = k == 0 ? E0 : k == 1 ? E1 : k == 2 ? E2 : E3;
         fr_t v[1] = {fr_mul(s, fr_load(&E[c]))};
         warp_reduce_fr<1>(v);
-        if (l == 0) fr_store(&mid[k * 8 + q], v[0]);
+        if (l == 0) fr_store(&mid[kq * MLE4_PARTS + part], v[0]);
     }
 }
-// out[k] = sum_q mid[k * 8 + q] - 2^31 (the bias of the lazy sums)
+// out[k] = sum of mid[k * 8 * MLE4_PARTS ..] - 2^31 (the bias of the lazy sums)
 __global__ void k_mle4_final(const fr_t* mid, fr_t* out) {
     const uint32_t k = threadIdx.x;
     if (k >= 4) return;
     fr_t s = fr_zero();
-    for (int q = 0; q < 8; q++) s = fr_add(s, fr_load(&mid[k * 8 + q]));
+    for (uint32_t q = 0; q < 8 * MLE4_PARTS; q++) s = fr_add(s, fr_load(&mid[k * 8 * MLE4_PARTS + q]));
     fr_store(&out[k], fr_sub(s, ZK_TWO31_MONT));
 }
 
@@ -400,8 +404,8 @@ void mle_i32_relu4(zk_ctx* ctx, const int32_t* d_z, const int32_t* d_g, uint32_t
             ZK_CUDA(cudaFuncSetAttribute(k_mle4_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
         ZK_LAUNCH(ctx, k_mle4_rows, nb, 256, hsm, d_z, d_g, R, rows, (const fr_t*)H[0], (const fr_t*)H[1],
                   (const fr_t*)H[2], (const fr_t*)H[3], P);
-        fr_t* mid = s.alloc<fr_t>(32);
-        ZK_LAUNCH(ctx, k_mle4_finish, 32, 256, 0, (const fr_t*)P, nb, (const fr_t*)E[0], (const fr_t*)E[1],
+        fr_t* mid = s.alloc<fr_t>(32 * MLE4_PARTS);
+        ZK_LAUNCH(ctx, k_mle4_finish, 32 * MLE4_PARTS, 256, 0, (const fr_t*)P, nb, (const fr_t*)E[0], (const fr_t*)E[1],
                   (const fr_t*)E[2], (const fr_t*)E[3], mid);
         ZK_LAUNCH(ctx, k_mle4_final, 1, 32, 0, (const fr_t*)mid, d_out);
         return;
