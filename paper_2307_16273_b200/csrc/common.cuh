@@ -320,6 +320,10 @@ __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mo
 // d_copy (nullable, len <= 256 only): the kernel also writes msg to this device buffer
 void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t len, uint8_t* d_copy = nullptr);
 void tr_challenges_dev(zk_transcript* tr, const char* tag, uint32_t n, fr_t* d_out_mont, uint8_t* d_out_canon);
+// k <= 4 challenge vectors (tags[t], ns[t] each, Montgomery outputs) drawn in order in one launch: the same
+// transcript as k tr_challenges_dev calls
+void tr_challenges_multi_dev(zk_transcript* tr, uint32_t k, const char* const* tags, const uint32_t* ns,
+                             fr_t* const* d_out_mont, uint8_t* const* d_out_canon = nullptr);
 
 // eq tables (tables.cu): out[x] = scale * prod_{s<k} eq(u[s], bit s of x) for x < 2^k
 void eq_table_dev(zk_ctx* ctx, const fr_t* d_u, uint32_t k, const fr_t* d_scale, fr_t* d_out, Scratch& s);

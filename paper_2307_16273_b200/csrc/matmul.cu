@@ -37,9 +37,14 @@ void matmul_reduce_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* A, const i
     fr_t* w = d_pts;
     fr_t* u1 = d_pts + lN;
     fr_t* u3 = d_pts + lN + l1;
-    tr_challenges_dev(tr, "mm/w", lN, w, d_pts_canon);
-    tr_challenges_dev(tr, "mm/u1", l1, u1, d_pts_canon + 32ull * lN);
-    tr_challenges_dev(tr, "mm/u3", l3, u3, d_pts_canon + 32ull * (lN + l1));
+    {   // one launch for the three vectors (the same chain as three draws)
+        const char* tags[3] = {"mm/w", "mm/u1", "mm/u3"};
+        const uint32_t ns[3] = {lN, l1, l3};
+        fr_t* outs[3] = {w, u1, u3};
+        uint8_t* canon[3] = {d_pts_canon, d_pts_canon ? d_pts_canon + 32ull * lN : nullptr,
+                             d_pts_canon ? d_pts_canon + 32ull * (lN + l1) : nullptr};
+        tr_challenges_multi_dev(tr, 3, tags, ns, outs, canon);
+    }
     fr_t* E1 = s.alloc<fr_t>(D1);
     fr_t* E3 = s.alloc<fr_t>(D3);
     eq_table_r2_dev(ctx, u1, l1, E1, s);

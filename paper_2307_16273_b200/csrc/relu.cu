@@ -1677,10 +1677,10 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     if (d_pts) {   // chained (D25): the window's merged claims give the points; nothing is drawn
         ZK_LAUNCH(ctx, k_canon_to_mont, 1, 128, 0, d_pts, 4 * logD, U);
     } else {
-        tr_challenges_dev(tr, "relu/uZ", logD, U, nullptr);
-        tr_challenges_dev(tr, "relu/uA", logD, U + logD, nullptr);
-        tr_challenges_dev(tr, "relu/uGA", logD, U + 2 * logD, nullptr);
-        tr_challenges_dev(tr, "relu/uGZ", logD, U + 3 * logD, nullptr);
+        const char* tags[4] = {"relu/uZ", "relu/uA", "relu/uGA", "relu/uGZ"};
+        const uint32_t ns[4] = {logD, logD, logD, logD};
+        fr_t* outs[4] = {U, U + logD, U + 2 * logD, U + 3 * logD};
+        tr_challenges_multi_dev(tr, 4, tags, ns, outs);
     }
     // claims Z~(u_Z), A~(u_A), G_A~(u_GA), G_Z~(u_GZ) with A, G_Z formed on the fly (Lemma 1)
     fr_t* claims = s.alloc<fr_t>(4);
@@ -1689,9 +1689,12 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     // r, r', u_bin
     fr_t* rr = s.alloc<fr_t>(2);
     fr_t* ubin = s.alloc<fr_t>(m);
-    tr_challenges_dev(tr, "relu/r", 1, rr, nullptr);
-    tr_challenges_dev(tr, "relu/rp", 1, rr + 1, nullptr);
-    tr_challenges_dev(tr, "relu/ubin", m, ubin, nullptr);
+    {
+        const char* tags[3] = {"relu/r", "relu/rp", "relu/ubin"};
+        const uint32_t ns[3] = {1, 1, m};
+        fr_t* outs[3] = {rr, rr + 1, ubin};
+        tr_challenges_multi_dev(tr, 3, tags, ns, outs);
+    }
     const fr_t* u_i[5] = {U, U + logD, U + 2 * logD, U + 3 * logD, ubin + logB};
 
     // ---- bit sums

@@ -103,6 +103,79 @@ __global__ void k_tr_absorb_frs(uint8_t* st, Tag32 tag, const fr_t* v, uint32_t 
 // H(st_{i+1} || 1)) mod p).  Thread 0 advances the state chain word-wise (the block's tail after the state
 // is the same for every step: built once), then thread j < 2n computes squeeze half j & 1 of challenge
 // j / 2, and thread i < n converts.  blockDim.x >= max(32, 2n); n <= 256 per launch.
+// Up to TRM_MAX challenge vectors (tags) in one launch, drawn in order (the same chain as one launch per tag).
+constexpr int TRM_MAX = 4;
+struct TrMulti {
+    Tag32 tag[TRM_MAX];
+    uint32_t n[TRM_MAX];
+    fr_t* out_mont[TRM_MAX];
+    uint8_t* out_canon[TRM_MAX];
+    uint32_t ntag;
+};
+__global__ void k_tr_challenges_multi(uint8_t* st, TrMulti a) {
+    __shared__ uint32_t states[256][8];
+    __shared__ fr_t half[256][2];
+    __shared__ uint32_t m[16];   // the chain's message block (shared memory: the compression reads it in place)
+    uint32_t total = 0;
+    for (uint32_t t = 0; t < a.ntag; t++) total += a.n[t];
+    if (threadIdx.x == 0) {
+        uint32_t cur[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            cur[k] = (uint32_t)st[4 * k] | ((uint32_t)st[4 * k + 1] << 8) | ((uint32_t)st[4 * k + 2] << 16) |
+                     ((uint32_t)st[4 * k + 3] << 24);
+        uint32_t idx = 0;
+        for (uint32_t t = 0; t < a.ntag; t++) {
+            const uint32_t tl = zk_strlen(a.tag[t].s);
+#pragma unroll
+            for (int k = 8; k < 16; k++) m[k] = 0;
+            // bytes 32.. of the block: 0x02, |tag|, tag (|tag| <= 30)
+            uint8_t* tb = reinterpret_cast<uint8_t*>(m + 8);
+            tb[0] = 0x02;
+            tb[1] = (uint8_t)tl;
+            for (uint32_t k = 0; k < tl; k++) tb[2 + k] = (uint8_t)a.tag[t].s[k];
+            for (uint32_t i = 0; i < a.n[t]; i++, idx++) {
+#pragma unroll
+                for (int k = 0; k < 8; k++) m[k] = cur[k];
+                hash_init(cur);
+                hash_compress(cur, m, 34 + tl, true);
+#pragma unroll
+                for (int k = 0; k < 8; k++) states[idx][k] = cur[k];
+            }
+        }
+        st_words_to_bytes(cur, st);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < 2 * total; j += blockDim.x) {   // one squeeze compression: H(st_i || k)
+        const uint32_t i = j >> 1, k = j & 1;
+        uint32_t q[16], d[8];
+#pragma unroll
+        for (int w = 0; w < 8; w++) q[w] = states[i][w];
+        q[8] = k;
+#pragma unroll
+        for (int w = 9; w < 16; w++) q[w] = 0;
+        hash_init(d);
+        hash_compress(d, q, 33, true);
+        fr_t x;
+#pragma unroll
+        for (int w = 0; w < 8; w++) x.v[w] = d[w];   // little-endian digest words = limbs
+        half[i][k] = x;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+        uint32_t t = 0, o = i;
+        while (o >= a.n[t]) o -= a.n[t++];
+        const fr_t lo = half[i][0], hi = half[i][1];
+        if (a.out_mont[t]) fr_store(&a.out_mont[t][o], fr_add(fr_mul(ZK_R2, lo), fr_mul(ZK_R3, hi)));
+        if (a.out_canon[t])
+            fr_canon_to_bytes(fr_add(fr_reduce_once(fr_reduce_once(lo)), fr_mul(ZK_R2, hi)), a.out_canon[t] + 32 * o);
+    }
+}
+
+// n challenges with one tag (D3: st_{i+1} = H(st_i || 0x02 || u8(|tag|) || tag), x_i = LE512(H(st_{i+1} || 0) ||
+// H(st_{i+1} || 1)) mod p).  Thread 0 advances the state chain word-wise (the block's tail after the state
+// is the same for every step: built once), then thread j < 2n computes squeeze half j & 1 of challenge
+// j / 2, and thread i < n converts.  blockDim.x >= max(32, 2n); n <= 256 per launch.
 __global__ void k_tr_challenges(uint8_t* st, Tag32 tag, uint32_t n, fr_t* out_mont, uint8_t* out_canon) {
     __shared__ uint32_t states[256][8];
     __shared__ fr_t half[256][2];
@@ -167,6 +240,28 @@ void tr_absorb_host(zk_transcript* tr, const char* tag, const void* msg, size_t 
         ZK_LAUNCH(ctx, k_tr_absorb_dev, 1, 32, 0, tr->d_st, make_tag(tag), d, (uint64_t)len);
         ZK_CUDA(cudaStreamSynchronize(ctx->stream));   // msg is a pageable host buffer
     }
+}
+
+void tr_challenges_multi_dev(zk_transcript* tr, uint32_t k, const char* const* tags, const uint32_t* ns,
+                             fr_t* const* d_out_mont, uint8_t* const* d_out_canon) {
+    ZK_REQUIRE(k >= 1 && k <= (uint32_t)TRM_MAX, ZK_ERR_ARG, "1..4 challenge vectors per launch");
+    TrMulti a;
+    memset(&a, 0, sizeof a);
+    uint32_t total = 0;
+    for (uint32_t t = 0; t < k; t++) {
+        ZK_REQUIRE(strlen(tags[t]) <= 30, ZK_ERR_ARG, "challenge tag longer than 30 bytes (one-block chain step)");
+        a.tag[t] = make_tag(tags[t]);
+        a.n[t] = ns[t];
+        a.out_mont[t] = d_out_mont[t];
+        a.out_canon[t] = d_out_canon ? d_out_canon[t] : nullptr;
+        total += ns[t];
+    }
+    a.ntag = k;
+    if (total > 256) {   // one launch per vector
+        for (uint32_t t = 0; t < k; t++) tr_challenges_dev(tr, tags[t], ns[t], d_out_mont[t], a.out_canon[t]);
+        return;
+    }
+    ZK_LAUNCH(tr->ctx, k_tr_challenges_multi, 1, 256, 0, tr->d_st, a);
 }
 
 void tr_challenges_dev(zk_transcript* tr, const char* tag, uint32_t n, fr_t* d_out_mont, uint8_t* d_out_canon) {
