@@ -407,7 +407,8 @@ zk_status zk_verify_rescale(uint8_t st[32], const uint8_t* proof, uint64_t proof
 
 /* ----------------------------------------------------------------- diagnostics
  * zk_diag_fr_op: element-wise d_out[i] = op(d_a[i], d_b[i]) on Montgomery tables, op 0 add, 1 sub,
- *   2 mul, 3 inverse, 4 negate, 5 square (d_b may be NULL for 3-5).  Used by the parity tests.
+ *   2 mul, 3 inverse (Fermat), 4 negate, 5 square, 6 inverse (binary extended Euclid) (d_b may be NULL for 3-6).
+ *   Used by the parity tests.
  * zk_diag_mul_bench: blocks x 256 threads each run 4 independent chains of `iters` Montgomery
  *   products on register-resident values (d_seed: 1024 elements; d_out: blocks*256 elements);
  *   bench.py times it to measure this implementation's sustained Fr-mul rate. */

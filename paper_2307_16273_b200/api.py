@@ -389,7 +389,7 @@ def parse_relu_out(raw: bytes, logD: int, Q: int, R: int) -> dict:
 
 # ---------------------------------------------------------------- diagnostics
 def diag_fr_op(ctx: Context, op: str, a: torch.Tensor, b: torch.Tensor | None = None) -> torch.Tensor:
-    code = {"add": 0, "sub": 1, "mul": 2, "inv": 3, "neg": 4, "sqr": 5}[op]
+    code = {"add": 0, "sub": 1, "mul": 2, "inv": 3, "neg": 4, "sqr": 5, "inv_bgcd": 6}[op]
     out = torch.empty_like(a)
     ctx.check(lib().zk_diag_fr_op(ctx.h, code, _dev_ptr(a), None if b is None else _dev_ptr(b), a.shape[0],
                                   out.data_ptr()))

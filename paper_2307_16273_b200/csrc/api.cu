@@ -583,7 +583,7 @@ zk_status zk_transcript_state_dev(zk_transcript* tr, void* d_out) {
 // ------------------------------------------------------------------ diagnostics (tests and the Fr-mul peak probe)
 zk_status zk_diag_fr_op(zk_ctx* ctx, int op, const void* d_a, const void* d_b, uint64_t n, void* d_out) {
     ZK_API_BEGIN(ctx)
-    ZK_REQUIRE(d_a && d_out && op >= 0 && op <= 5, ZK_ERR_ARG, "bad argument");
+    ZK_REQUIRE(d_a && d_out && op >= 0 && op <= 6, ZK_ERR_ARG, "bad argument");
     selftest_op_dev(ctx, op, static_cast<const fr_t*>(d_a), static_cast<const fr_t*>(d_b), n, static_cast<fr_t*>(d_out));
     ZK_API_END(ctx)
 }

@@ -1287,13 +1287,14 @@ __device__ __noinline__ void iround_sigma_der(const fr_t* V, const fr_t* const* 
 struct UPts {
     const fr_t* u[5];
 };
+// one value per warp (lane 0): the binary GCD's data-dependent loops would serialise a warp's lanes
 __global__ void k_relu_uinv(UPts P, uint32_t t1, fr_t* out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 5 * t1) return;
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= 5 * t1 || (threadIdx.x & 31)) return;
     const uint32_t t = i / 5, x = i % 5;
     const fr_t u = fr_load(&P.u[x][t]);
     if (fr_is_zero(u)) __trap();
-    fr_store(&out[i], fr_inv(u));
+    fr_store(&out[i], fr_inv_bgcd(u));
 }
 
 // MODE: bit 0 = FOLD, bit 1 = SRC (rounds 0 / 1 from the int32 words through byte tables in shared memory),
@@ -1803,7 +1804,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         cudaStream_t aux = ctx->aux_stream();
         ZK_CUDA(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
         ZK_CUDA(cudaStreamWaitEvent(aux, ctx->aux_ev[0], 0));
-        k_relu_uinv<<<(5 * logD + 63) / 64, 64, 0, aux>>>(P, logD, uinv);
+        k_relu_uinv<<<(5 * logD + 3) / 4, 128, 0, aux>>>(P, logD, uinv);
         after_launch(ctx, "k_relu_uinv");
         ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], aux));
     }

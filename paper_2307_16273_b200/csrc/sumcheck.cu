@@ -1233,13 +1233,14 @@ static void sumcheck_prove_small(zk_ctx* ctx, zk_transcript* tr, const ScStateme
     }
 }
 
-// out[i] = in[i]^-1 (Fermat; traps on zero: probability ~2^-250 per transcript challenge)
+// out[i] = in[i]^-1 (binary extended Euclid, one value per warp; traps on zero: probability ~2^-250 per transcript
+// challenge)
 __global__ void k_fr_inv_batch(const fr_t* in, uint32_t n, fr_t* out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (i >= n || (threadIdx.x & 31)) return;
     const fr_t x = fr_load(&in[i]);
     if (fr_is_zero(x)) __trap();
-    fr_store(&out[i], fr_inv(x));
+    fr_store(&out[i], fr_inv_bgcd(x));
 }
 
 void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Scratch& s) {
@@ -1279,7 +1280,7 @@ void sumcheck_prove_dev(zk_ctx* ctx, zk_transcript* tr, const ScStatement& S, Sc
             cudaStream_t aux = ctx->aux_stream();
             ZK_CUDA(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
             ZK_CUDA(cudaStreamWaitEvent(aux, ctx->aux_ev[0], 0));
-            k_fr_inv_batch<<<(n_eq + 63) / 64, 64, 0, aux>>>(S.d_w, n_eq, e.winv);
+            k_fr_inv_batch<<<(n_eq + 3) / 4, 128, 0, aux>>>(S.d_w, n_eq, e.winv);
             after_launch(ctx, "k_fr_inv_batch");
             ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], aux));
         }

@@ -466,6 +466,7 @@ __global__ void k_selftest_op(int op, const fr_t* a, const fr_t* b, uint64_t n, 
             case 3: r = fr_inv(x); break;
             case 4: r = fr_neg(x); break;
             case 5: r = fr_sqr(x); break;
+            case 6: r = fr_inv_bgcd(x); break;
             default: r = fr_zero();
         }
         fr_store(&out[i], r);

@@ -58,6 +58,8 @@ def test_fr_ops_vs_python_ints(ctx):
     small = api.fr_table_from_ints(ctx, a[1:200])
     got = api.fr_table_to_ints(ctx, api.diag_fr_op(ctx, "inv", small))
     assert got == [pow(x, P - 2, P) for x in a[1:200]]
+    got = api.fr_table_to_ints(ctx, api.diag_fr_op(ctx, "inv_bgcd", small))   # the u^-1 kernels' inversion
+    assert got == [pow(x, P - 2, P) for x in a[1:200]]
 
 
 def test_noncanonical_rejected(ctx):
