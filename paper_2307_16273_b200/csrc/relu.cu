@@ -1806,8 +1806,41 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         ZK_CUDA(cudaStreamWaitEvent(aux, ctx->aux_ev[0], 0));
         k_relu_uinv<<<(5 * logD + 3) / 4, 128, 0, aux>>>(P, logD, uinv);
         after_launch(ctx, "k_relu_uinv");
-        ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], aux));
     }
+    // the i-phase LO tables (eq over the first H i-variables; no kappa) on the aux stream too, beside the j-rounds
+    const uint32_t hb = logD < 5 ? logD : 5;
+    const uint32_t H = logD - hb;
+    fr_t* LOs[5][2];
+    {
+        EqJob lj[5];
+        uint32_t nl = 0;
+        for (int x = 0; x < 5; x++) {
+            LOs[x][0] = LOs[x][1] = nullptr;
+            if (H) {
+                LOs[x][0] = s.alloc<fr_t>(1ull << H);
+                LOs[x][1] = s.alloc<fr_t>(1ull << (H - 1));
+                lj[nl++] = EqJob{u_i[x], H, nullptr, 0, LOs[x][0]};
+            }
+        }
+        if (nl) {
+            cudaStream_t aux = ctx->aux_stream();
+            if (!derive) {   // (the u^-1 kernel forked the aux stream otherwise)
+                ZK_CUDA(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+                ZK_CUDA(cudaStreamWaitEvent(aux, ctx->aux_ev[0], 0));
+            }
+            cudaStream_t main_stream = ctx->stream;
+            ctx->stream = aux;   // eq_tables_batch launches on the context stream
+            try {
+                eq_tables_batch(ctx, nl, lj, s);
+            } catch (...) {
+                ctx->stream = main_stream;
+                throw;
+            }
+            ctx->stream = main_stream;
+        }
+    }
+    const bool aux_used = derive || H > 0;
+    if (aux_used) ZK_CUDA(cudaEventRecord(ctx->aux_ev[1], ctx->aux_stream()));
     {   // t0 >= 2 and the factored kernel (the word-sourced rounds 0 / 1), as decided below
         const uint32_t hb_ = logD < 5 ? logD : 5, H_ = logD - hb_;
         const int plog_ = getenv("ZKDL_IPERSIST_LOG") ? atoi(getenv("ZKDL_IPERSIST_LOG")) : 16;
@@ -1828,27 +1861,18 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
     }
     ZK_LAUNCH(ctx, k_relu_jrounds, 1, 256, 0, ja);
 
-    const uint32_t hb = logD < 5 ? logD : 5;
-    const uint32_t H = logD - hb;
     fr_t* HIs[6];
-    fr_t* LOs[5][2];
     EqJob jobs[11];
     uint32_t nj = 0;
-    for (int x = 0; x < 5; x++) {
+    for (int x = 0; x < 5; x++) {   // (the LO tables were built on the aux stream beside the j-rounds)
         HIs[x] = s.alloc<fr_t>(1ull << hb);
         jobs[nj++] = EqJob{u_i[x] + H, hb, kappa + (x < 4 ? x : 4), 0, HIs[x]};
         if (x == 4) {   // E_b' = r' E_b for the a1 side of the AIVP
             HIs[5] = s.alloc<fr_t>(1ull << hb);
             jobs[nj++] = EqJob{u_i[4] + H, hb, kappa + 7, 0, HIs[5]};
         }
-        LOs[x][0] = LOs[x][1] = nullptr;
-        if (H) {
-            LOs[x][0] = s.alloc<fr_t>(1ull << H);
-            LOs[x][1] = s.alloc<fr_t>(1ull << (H - 1));
-            jobs[nj++] = EqJob{u_i[x], H, nullptr, 0, LOs[x][0]};
-        }
     }
-    eq_tables_batch(ctx, nj, jobs, s);   // 11 tables in two launches
+    eq_tables_batch(ctx, nj, jobs, s);   // the HI tables (they need kappa from the j-rounds)
     fr_t* buf[2][3];
     for (int k = 0; k < 3; k++) {
         buf[1][k] = s.alloc<fr_t>(D >> 1);
@@ -1892,7 +1916,7 @@ void relu_prove_dev(zk_ctx* ctx, zk_transcript* tr, const int32_t* Z, const int3
         ZK_CUDA(cudaFuncSetAttribute(k_relu_iround_f<14>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_smem));
     }
     ZK_REQUIRE(!r0ext || words, ZK_ERR_INTERNAL, "cell-sourced round 0 without the word-sourced rounds");
-    if (derive) ZK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // u^-1 before the first i-round
+    if (aux_used) ZK_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));   // u^-1, LO tables before round 0
     for (uint32_t t = 0; t < t0; t++) {
         IRoundArgs a;
         memset(&a, 0, sizeof a);
