@@ -15,6 +15,7 @@
 // Both phases run on the product-sumcheck engine (rows a4-a6).  Everything is stream-ordered on the
 // context stream: no host synchronisation, no pageable copies (maps travel as kernel parameters).
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "sumcheck.cuh"
@@ -72,6 +73,13 @@ static void cm_slice_mles(zk_ctx* ctx, Load load, uint64_t N, uint32_t lr, uint3
                           fr_t* out, Scratch& s) {
     const uint64_t rows = 1ull << lr, cols = 1ull << lc;
     fr_t* T = s.alloc<fr_t>(N * rows);
+    if constexpr (std::is_same_v<Load, LoadPlain>) {
+        if (rowdot_tc_ok(N * rows, (uint32_t)cols)) {   // a stored stack: the row dots on the tensor cores (TMA)
+            rowdot_tc(ctx, load.p, N * rows, (uint32_t)cols, Ec, T, N * rows, n_log(N) + lr, 1, s);
+            ZK_LAUNCH(ctx, k_rowdot_fr, grid_for(ctx, N * 32, 256, 8), 256, 0, (const fr_t*)T, N, (uint32_t)rows, Er, out);
+            return;
+        }
+    }
     ZK_LAUNCH(ctx, k_rowdot_i32<Load>, grid_for(ctx, N * rows * 32, 256, 8), 256, 0, load, N * rows, (uint32_t)cols,
               Ec, T, N * rows, (uint32_t)(n_log(N) + lr), (uint64_t)1);
     // the row dots are in natural order (inner = nrows: identity map)
