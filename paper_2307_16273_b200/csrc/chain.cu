@@ -53,7 +53,12 @@ __global__ void k_cm_scatter(CmMaps M, const fr_t* E, const fr_t* rho, fr_t* P) 
 // Xr[y] = sum_i beta(r_i, i) X(i, y): the column sums of the [N][D] stack (E2 = beta(r_i) scaled by R)
 template <class Load>
 static void cm_colsum(zk_ctx* ctx, Load load, uint64_t N, uint64_t D, const fr_t* E2, fr_t* out, Scratch& s) {
-    (void)s;
+    if constexpr (std::is_same_v<Load, LoadPlain>) {
+        if (D <= 0xffffffffull && colsum_tc_ok(1, (uint32_t)N, (uint32_t)D)) {   // a stored stack: tensor cores (TMA)
+            colsum_tc(ctx, load.p, 1, (uint32_t)N, (uint32_t)D, E2, out, s);
+            return;
+        }
+    }
     const uint64_t blocks = (D + 127) / 128;
     const unsigned int grid = (unsigned int)(blocks < (uint64_t)ctx->num_sms * 7 ? blocks : (uint64_t)ctx->num_sms * 7);
     ZK_LAUNCH(ctx, k_colsum_i32<Load>, grid, 128, 0, load, (uint64_t)1, (uint32_t)N, (uint32_t)D, E2, out, 1u,
